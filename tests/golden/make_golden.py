@@ -1,0 +1,333 @@
+"""Generate golden fixtures by running the REFERENCE implementation (qnmt).
+
+Run in the build container only (``/root/reference`` does not exist on the
+GPU box):
+
+    NUMBA_CACHE_DIR=/tmp/numba_cache python tests/golden/make_golden.py
+
+Two modes of the reference are recorded:
+
+* Tier A -- the unmodified reference.
+* Tier B -- the reference with exactly five elementwise functions of
+  ``qnmt.layers`` replaced by "evaluate in float64, round once to float32"
+  versions: ``sigmoid`` (layers.py:35), ``tanh_f32`` (:42), ``softmax`` (:47),
+  ``_log_softmax_cols`` (:60) and the ``gemm_f32`` name used for the
+  attention context (:237).  Quantization, integer GEMMs, scales, gate
+  arithmetic and search remain the reference's own code.  Tier B is the
+  end-to-end bit-exact contract of the B200 kernels.
+
+Outputs (committed, small): ``qmath_kat.npz``, ``small_model.npz``,
+``translate_small.json``, ``baseline_dims.npz``.
+"""
+
+from __future__ import annotations
+
+import contextlib
+import hashlib
+import json
+import os
+import sys
+
+import numpy as np
+
+REF_SRC = "/root/reference/pkg/src"
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REF_SRC)
+sys.path.insert(0, os.path.join(HERE, "..", ".."))
+
+import qnmt  # noqa: E402  (the reference)
+from qnmt import layers as ref_layers  # noqa: E402
+from qnmt import model as ref_model  # noqa: E402
+from qnmt import qmath as ref_qmath  # noqa: E402
+from qnmt.decoder import DecodeConfig, translate  # noqa: E402
+
+F32, F64 = np.float32, np.float64
+
+
+def sha(a: np.ndarray) -> str:
+    a = np.ascontiguousarray(a)
+    return hashlib.sha256(a.tobytes()).hexdigest()
+
+
+# ---------------------------------------------------------------------------
+# Tier-B patch
+# ---------------------------------------------------------------------------
+
+def _sigmoid_b(v):
+    ref_layers._require_finite(v, "sigmoid")
+    v64 = v.astype(F64)
+    with np.errstate(over="ignore"):
+        pos = 1.0 / (1.0 + np.exp(-v64))
+        e = np.exp(v64)
+        neg = e / (1.0 + e)
+    return np.where(v64 >= 0, pos, neg).astype(F32)
+
+
+def _tanh_b(v):
+    ref_layers._require_finite(v, "tanh")
+    return np.tanh(v.astype(F64)).astype(F32)
+
+
+def _softmax_b(v, axis=0):
+    ref_layers._require_finite(v, "softmax")
+    v64 = v.astype(F64)
+    e = np.exp(v64 - np.max(v64, axis=axis, keepdims=True))
+    return (e / np.sum(e, axis=axis, keepdims=True)).astype(F32)
+
+
+def _log_softmax_cols_b(v):
+    v64 = v.astype(F64)
+    t = v64 - np.max(v64, axis=0, keepdims=True)
+    lse = np.log(np.sum(np.exp(t), axis=0, keepdims=True))
+    if not np.isfinite(lse).all():
+        raise ref_layers.NumericError("log_softmax received non-finite logits")
+    return (t - lse).astype(F32)
+
+
+def _gemm_f32_b(a, b):
+    return (np.asarray(a, F64) @ np.asarray(b, F64)).astype(F32)
+
+
+@contextlib.contextmanager
+def tier_b():
+    saved = {k: getattr(ref_layers, k) for k in
+             ("sigmoid", "tanh_f32", "softmax", "_log_softmax_cols", "gemm_f32")}
+    ref_layers.sigmoid = _sigmoid_b
+    ref_layers.tanh_f32 = _tanh_b
+    ref_layers.softmax = _softmax_b
+    ref_layers._log_softmax_cols = _log_softmax_cols_b
+    ref_layers.gemm_f32 = _gemm_f32_b
+    try:
+        yield
+    finally:
+        for k, v in saved.items():
+            setattr(ref_layers, k, v)
+
+
+# ---------------------------------------------------------------------------
+# models: same recipe as oracle.synthetic_tensors / package synthetic model
+# ---------------------------------------------------------------------------
+
+def make_params(dims: ref_model.Dims, seed: int, bias_std=0.0, s0_mode="transform",
+                attention_query="current", weight_std=0.05, eos_bias=0.0):
+    from oracle.qnmt_oracle import Dims as ODims, synthetic_tensors
+    od = ODims(**dims.as_dict())
+    tensors = synthetic_tensors(od, seed, weight_std, bias_std, eos_bias)
+    vs = ref_model._synthetic_vocab(dims.src_vocab)
+    vt = ref_model._synthetic_vocab(dims.tgt_vocab)
+    return ref_model._build_params(dims, tensors, vs, vt, s0_mode, attention_query), tensors
+
+
+# ---------------------------------------------------------------------------
+# 1. qmath known answers
+# ---------------------------------------------------------------------------
+
+def gen_qmath():
+    out = {}
+    cases = {
+        "zeros": np.zeros((3, 3), F32),
+        "ten": np.array([[10.0]], F32),
+        "ties": np.array([[2.0, 1.0, -1.0]], F32),
+        "halfulp": np.array([[127.0, 0.49999997]], F32),
+        "u8x8": np.random.default_rng(7).uniform(-1, 1, (8, 8)).astype(F32),
+        "n5x7": np.random.default_rng(3).normal(0, 10, (5, 7)).astype(F32),
+        "u6x5": np.random.default_rng(11).uniform(-50, 50, (6, 5)).astype(F32),
+        "n64x200": np.random.default_rng(12).normal(0, 1, (64, 200)).astype(F32),
+        "tiny": (np.random.default_rng(13).normal(0, 1, (4, 9)) * 1e-30).astype(F32),
+        "huge": (np.random.default_rng(14).normal(0, 1, (4, 9)) * 1e30).astype(F32),
+        "halfgrid": (np.arange(-300, 301, dtype=F32) / F32(2.0)).reshape(1, -1),
+    }
+    for name, m in cases.items():
+        q = ref_qmath.quantize(m)
+        out[f"q_{name}_in"] = m
+        out[f"q_{name}_codes"] = q.data
+        out[f"q_{name}_scale"] = np.array(q.scale, F64)
+        qa = ref_qmath.quantize_activations(m)
+        assert np.array_equal(qa.data, q.data) and qa.scale == q.scale
+    # random int8 GEMMs (test_qmath.py:41-44 operand style), incl. ragged shapes
+    rng = np.random.default_rng(2024)
+    shapes = [(1, 1, 1), (4, 8, 1), (6, 10, 5), (13, 33, 8), (64, 64, 3), (3, 5, 2),
+              (7, 70, 2), (33, 129, 7), (100, 96, 16), (5, 1000, 8), (1000, 1000, 1)]
+    for i, (m, k, p) in enumerate(shapes):
+        a = ref_qmath.QuantizedMatrix(rng.integers(-127, 128, (m, k)).astype(np.int8),
+                                      float(F32(rng.uniform(0.5, 200.0))))
+        b = ref_qmath.QuantizedMatrix(rng.integers(-127, 128, (k, p)).astype(np.int8),
+                                      float(F32(rng.uniform(0.5, 200.0))))
+        y = ref_qmath.qgemm_panel(a, b)
+        assert np.array_equal(y, ref_qmath.qgemm(a, b))
+        out[f"g{i}_a"], out[f"g{i}_b"] = a.data, b.data
+        out[f"g{i}_sa"], out[f"g{i}_sb"] = np.array(a.scale, F64), np.array(b.scale, F64)
+        out[f"g{i}_y"] = y
+    out["g_count"] = np.array(len(shapes))
+    # cfg1: W ~ N(0,0.05) [3072x1024], X ~ N(0,1) [1024xB], B in {1, 64}
+    w = np.random.default_rng(1804).normal(0, 0.05, (3072, 1024)).astype(F32)
+    wq = ref_qmath.quantize(w)
+    out["cfg1_w_scale"] = np.array(wq.scale, F64)
+    out["cfg1_w_codes_sha"] = np.array(sha(wq.data))
+    for bsz in (1, 64):
+        x = np.random.default_rng(5038 + bsz).normal(0, 1, (1024, bsz)).astype(F32)
+        xq = ref_qmath.quantize_activations(x)
+        y = ref_qmath.qgemm_panel(wq, xq)
+        acc = wq.data.astype(np.int64) @ xq.data.astype(np.int64)
+        out[f"cfg1_b{bsz}_x_scale"] = np.array(xq.scale, F64)
+        out[f"cfg1_b{bsz}_x_codes_sha"] = np.array(sha(xq.data))
+        out[f"cfg1_b{bsz}_acc_sha"] = np.array(sha(acc.astype(np.int32)))
+        out[f"cfg1_b{bsz}_y_sha"] = np.array(sha(y))
+        out[f"cfg1_b{bsz}_y_head"] = y[:64].copy()
+    np.savez_compressed(os.path.join(HERE, "qmath_kat.npz"), **out)
+    print("qmath_kat.npz:", len(out), "arrays")
+
+
+# ---------------------------------------------------------------------------
+# 2. small model: op-level (both tiers) + translations (Tier B and A)
+# ---------------------------------------------------------------------------
+
+SMALL_DIMS = dict(src_vocab=40, tgt_vocab=37, embed=8, hidden=12, attn=10, readout=6)
+MED_DIMS = dict(src_vocab=300, tgt_vocab=251, embed=32, hidden=48, attn=40, readout=24)
+# (tag, dims, seed, weight_std, bias_std, eos_bias, s0_mode, attention_query)
+MODELS = [
+    ("small", SMALL_DIMS, 11, 0.05, 0.05, 0.0, "transform", "current"),
+    ("med", MED_DIMS, 12, 0.05, 0.05, 0.0, "transform", "current"),
+    ("eos", SMALL_DIMS, 13, 0.6, 0.1, 0.75, "transform", "current"),   # terminates early
+    ("eosmed", MED_DIMS, 14, 0.3, 0.1, 0.6, "transform", "current"),
+    ("flags", SMALL_DIMS, 15, 0.6, 0.1, 0.5, "zero", "previous"),      # model-header flags
+]
+
+
+def op_level(prefix, params, out, rng, p=3, length=7):
+    qm = ref_model.quantize_model(params)
+    net = ref_layers.build_network(qm)
+    d = params.dims
+    ids = rng.integers(3, d.src_vocab, length)
+    enc = net.encode(ids)
+    out[f"{prefix}_src"] = ids
+    out[f"{prefix}_states"] = enc.states
+    out[f"{prefix}_att_proj"] = enc.att_proj
+    out[f"{prefix}_s0"] = enc.s0
+    # teacher-forced decoder step at width p from a random state
+    s = rng.normal(0, 0.5, (d.hidden, p)).astype(F32)
+    sp = rng.normal(0, 0.5, (d.hidden, p)).astype(F32)
+    y = rng.integers(0, d.tgt_vocab, p)
+    st = ref_layers.DecoderState(s=s, s_prime=sp)
+    lp, st2, alpha = net.decoder_step(y, st, enc)
+    out[f"{prefix}_step_s"], out[f"{prefix}_step_sp"], out[f"{prefix}_step_y"] = s, sp, y
+    out[f"{prefix}_step_lp"] = lp
+    out[f"{prefix}_step_snew"] = st2.s
+    out[f"{prefix}_step_sint"] = st2.s_prime
+    out[f"{prefix}_step_alpha"] = alpha
+    # single ops
+    x = rng.normal(0, 1, (d.embed, p)).astype(F32)
+    h = rng.normal(0, 0.5, (d.hidden, p)).astype(F32)
+    out[f"{prefix}_gru_x"], out[f"{prefix}_gru_h"] = x, h
+    out[f"{prefix}_gru_out"] = ref_layers.gru_step(net.dec_r, x, h)
+    ctx, al = ref_layers.attend(net.attention, h, enc)
+    out[f"{prefix}_att_ctx"], out[f"{prefix}_att_alpha"] = ctx, al
+    out[f"{prefix}_lin_out"] = net.dec_r.update_in.apply(x)
+
+
+def gen_small():
+    out = {}
+    tr = {"cases": []}
+    for tag, dims_kw, seed, ws, bs, eb, s0m, aq in MODELS:
+        dims = ref_model.Dims(**dims_kw)
+        params, _ = make_params(dims, seed, bias_std=bs, weight_std=ws, eos_bias=eb,
+                                s0_mode=s0m, attention_query=aq)
+        for tier in ("A", "B"):
+            rng = np.random.default_rng(100 + seed)
+            ctx = tier_b() if tier == "B" else contextlib.nullcontext()
+            with ctx:
+                op_level(f"{tag}{tier}", params, out, rng)
+        qm = ref_model.quantize_model(params)
+        rng = np.random.default_rng(200 + seed)
+        for n in range(24):
+            length = int(rng.integers(1, 12))
+            ids = rng.integers(3, dims.src_vocab, length).tolist()
+            if n % 7 == 3:
+                ids[0] = 1  # UNK id in the source
+            beam = [1, 2, 3, 5, 8][n % 5]
+            ratio = [1.5, 3.0, 0.5, 2.0][n % 4]
+            toks = [params.src_tokens[i] for i in ids]
+            cfg = DecodeConfig(beam=beam, max_ratio=ratio, precision="int8")
+            case = {"model": tag, "src": ids, "beam": beam, "max_ratio": ratio}
+            for tier in ("A", "B"):
+                ctx = tier_b() if tier == "B" else contextlib.nullcontext()
+                with ctx:
+                    words, logp = translate(qm, toks, cfg)
+                tgt_index = {t: i for i, t in enumerate(params.tgt_tokens)}
+                case[f"out_{tier}"] = [tgt_index[w] for w in words]
+                case[f"logp_{tier}"] = logp
+            tr["cases"].append(case)
+    tr["models"] = {m[0]: dict(dims=m[1], seed=m[2], weight_std=m[3], bias_std=m[4],
+                               eos_bias=m[5], s0_mode=m[6], attention_query=m[7])
+                    for m in MODELS}
+    np.savez_compressed(os.path.join(HERE, "small_model.npz"), **out)
+    with open(os.path.join(HERE, "translate_small.json"), "w") as fh:
+        json.dump(tr, fh, indent=1)
+    print("small_model.npz:", len(out), "arrays; translate_small.json:", len(tr["cases"]), "cases")
+
+
+# ---------------------------------------------------------------------------
+# 3. BASELINE dims (cfg2/cfg3 and one beam-5 sentence)
+# ---------------------------------------------------------------------------
+
+BASE_DIMS = dict(src_vocab=32000, tgt_vocab=32000, embed=512, hidden=1024, attn=2048, readout=512)
+
+
+def gen_baseline():
+    out = {}
+    dims = ref_model.Dims(**BASE_DIMS)
+    params, _ = make_params(dims, 1804)
+    qm = ref_model.quantize_model(params)
+    out["w_scales"] = np.array([qm.stats[k].scale for k in sorted(qm.stats)], F64)
+    out["w_scale_names"] = np.array(sorted(qm.stats))
+    net = ref_layers.build_network(qm)
+    rng = np.random.default_rng(5038)
+    src50 = rng.integers(3, 32000, 50)
+    out["src50"] = src50
+    with tier_b():
+        enc = net.encode(src50)
+        out["B_states_sha"] = np.array(sha(enc.states))
+        out["B_att_proj_sha"] = np.array(sha(enc.att_proj))
+        out["B_states_col0"] = enc.states[:, 0].copy()
+        out["B_states_col49"] = enc.states[:, 49].copy()
+        out["B_s0"] = enc.s0
+        toks = [params.src_tokens[i] for i in src50]
+        words, logp = translate(qm, toks, DecodeConfig(beam=1, max_ratio=0.98, precision="int8"))
+        idx = {t: i for i, t in enumerate(params.tgt_tokens)}
+        out["B_greedy50"] = np.array([idx[w] for w in words])
+        out["B_greedy50_logp"] = np.array(logp, F64)
+        # first decoder step log-probs (teacher forced from s0)
+        st = net.initial_state(enc, 1)
+        lp, st2, alpha = net.decoder_step(np.array([2]), st, enc)
+        out["B_step1_lp_sha"] = np.array(sha(lp))
+        out["B_step1_lp_top"] = np.sort(lp[:, 0])[-16:]
+        out["B_step1_alpha"] = alpha
+        out["B_step1_snew"] = st2.s
+        src10 = src50[:10]
+        toks10 = [params.src_tokens[i] for i in src10]
+        words, logp = translate(qm, toks10, DecodeConfig(beam=5, max_ratio=1.5, precision="int8"))
+        out["B_beam5_src"] = src10
+        out["B_beam5"] = np.array([idx[w] for w in words])
+        out["B_beam5_logp"] = np.array(logp, F64)
+    # Tier A (unpatched) op-level at full dims: one decoder step at P=5
+    enc_a = net.encode(src50[:20])
+    out["A_enc20_states_col0"] = enc_a.states[:, 0].copy()
+    s = np.repeat(enc_a.s0, 5, axis=1)
+    y = np.array([2, 5, 77, 1000, 31999])
+    lp, st2, alpha = net.decoder_step(y, ref_layers.DecoderState(s=s, s_prime=s.copy()), enc_a)
+    out["A_step_y"] = y
+    out["A_step_lp_top"] = np.sort(lp, axis=0)[-8:]
+    out["A_step_argmax"] = np.argmax(lp, axis=0)
+    out["A_step_snew"] = st2.s
+    np.savez_compressed(os.path.join(HERE, "baseline_dims.npz"), **out)
+    print("baseline_dims.npz:", len(out), "arrays")
+
+
+if __name__ == "__main__":
+    which = sys.argv[1:] or ["qmath", "small", "baseline"]
+    if "qmath" in which:
+        gen_qmath()
+    if "small" in which:
+        gen_small()
+    if "baseline" in which:
+        gen_baseline()
