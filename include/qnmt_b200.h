@@ -1,0 +1,263 @@
+/*
+ * qnmt_b200.h -- C ABI of the B200-native int8 NMT decode path.
+ *
+ * The reference (arXiv 1804.05038's engine, Python package ``qnmt`` under
+ * /root/reference/pkg/src/qnmt) has no FFI: its drop-in surface is the Python
+ * API.  Each entry point below replaces the arithmetic behind one reference
+ * function; the Python package ``paper_1804_05038_b200`` binds them with
+ * ctypes and mirrors the reference names, argument meaning and exceptions.
+ *
+ * Conventions
+ *  - All tensor pointers are DEVICE pointers unless a parameter says "host".
+ *    Callers own every buffer (the library never frees caller memory); the
+ *    engine handle owns only its scratch.
+ *  - Activations are stored column-major w.r.t. the reference's ``[features, P]``
+ *    convention (layers.py:9-11): one contiguous row of ``features`` values per
+ *    column, i.e. a ``[N][K]`` array with row stride ``ld``.  Weights are the
+ *    reference's ``[out][in]`` row-major int8 codes (qmath.py:63).
+ *  - ``stream`` is a ``cudaStream_t`` (NULL = legacy default stream).
+ *  - Return value: QNMT_OK or an error code; codes map 1:1 onto the reference
+ *    exceptions (errors.py:4-47).  ``qnmt_last_error()`` gives a message.
+ *  - Device-side numeric checks (non-finite activations, out-of-range ids)
+ *    set bits in a caller-provided sticky ``err_flag`` (int32, device); the
+ *    caller maps them with QNMT_FLAG_* after synchronising.
+ */
+#ifndef QNMT_B200_H
+#define QNMT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#pragma GCC visibility push(default)
+#endif
+
+#define QNMT_ABI_VERSION 1
+
+enum {
+    QNMT_OK = 0,
+    QNMT_ERR_SHAPE = 1,          /* errors.py:12  ShapeError        */
+    QNMT_ERR_INVALID_INPUT = 2,  /* errors.py:8   InvalidInputError */
+    QNMT_ERR_NUMERIC = 3,        /* errors.py:45  NumericError      */
+    QNMT_ERR_VOCAB = 4,          /* errors.py:29  VocabError        */
+    QNMT_ERR_CONFIG = 5,         /* errors.py:37  ConfigError       */
+    QNMT_ERR_EMPTY = 6,          /* errors.py:33  EmptyInputError   */
+    QNMT_ERR_CUDA = 7            /* device / launch failure          */
+};
+
+/* sticky device error-flag bits */
+#define QNMT_FLAG_NUMERIC 1   /* non-finite activation (qmath.py:180, layers.py:30/65) */
+#define QNMT_FLAG_INVALID 2   /* non-finite weight (qmath.py:152)                        */
+#define QNMT_FLAG_VOCAB 4     /* token id outside the vocabulary (layers.py:318, :366)    */
+
+/* qmath.py:41 -- int32 accumulation is safe up to this K */
+#define QNMT_INT32_SAFE_K 131000
+
+int qnmt_abi_version(void);
+const char* qnmt_last_error(void);
+int qnmt_device_sync(void);
+
+/* ---------------------------------------------------------------------------
+ * K1 quantize  (replaces qmath.quantize :145-154, quantize_activations
+ * :172-182, _max_abs_scan :157-169, _encode :136-142, _encode_i8 :119-133)
+ *
+ * x: [ncols][K] f32, row stride ldx.  Column c belongs to segment
+ * col_seg[c] (col_seg == NULL: every column is segment 0).  One scale per
+ * segment: s = fl32(127 / max|x_seg|) (1.0 when the max is 0); codes are
+ * sign(v)*floor(fl32(|v|+0.5)), v = fl32(x*s), clamped to +-127.
+ * q: [ncols][ldq] int8; scales: [nseg] f32; seg_maxbits: [nseg] u32 scratch.
+ * mode 0 = weights (non-finite -> QNMT_FLAG_INVALID),
+ * mode 1 = activations (non-finite -> QNMT_FLAG_NUMERIC).
+ * ------------------------------------------------------------------------- */
+int qnmt_quantize(const float* x, int64_t ncols, int64_t K, int64_t ldx,
+                  const int32_t* col_seg, int32_t nseg,
+                  int8_t* q, int64_t ldq, float* scales, uint32_t* seg_maxbits,
+                  int32_t mode, int32_t* err_flag, void* stream);
+
+/* dequantize (qmath.py:185-187): y = f32(code) / scale, scale a host float */
+int qnmt_dequantize(const int8_t* q, int64_t n, float scale, float* y, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * K2/K3 int8 GEMM with fused dequant epilogue  (replaces qgemm :384-397,
+ * qgemm_panel :400-427, _scale_output :379-381, and LinearOp.apply's bias
+ * add layers.py:144-145)
+ *
+ *   acc[n][m] = sum_k W[m][k] * X[n][k]              (exact; int64 if K > SAFE_K)
+ *   y = fl32( f64(acc) / (f64(w_scales[m / w_rows_per_scale]) * f64(x_scales[seg(n)])) )
+ *   if bias:            y = fl32(y + bias[m])
+ *   if ACCUMULATE:      y = fl32(Y[n][m] + y)
+ *   Y[n][m] = y           (Y: [N][ldy] f32; may be NULL if acc_out given)
+ *   acc_out (nullable): [N][M] int64 raw accumulators
+ * seg(n) = col_seg[n] (col_seg NULL -> 0).  Scales are device f32 arrays.
+ * ------------------------------------------------------------------------- */
+#define QNMT_GEMM_ACCUMULATE 1
+int qnmt_gemm_i8(const int8_t* W, int64_t M, int64_t K, int64_t ldw,
+                 const float* w_scales, int64_t w_rows_per_scale,
+                 const int8_t* X, int64_t N, int64_t ldx,
+                 const float* x_scales, const int32_t* col_seg,
+                 const float* bias, float* Y, int64_t ldy,
+                 int64_t* acc_out, int32_t flags, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * GRU gate arithmetic (layers.py:170-181), f32 ops in the reference's
+ * association order, sigmoid/tanh evaluated in fp64 and rounded once.
+ *   gx : [*][3H] x-side pre-activations (Wz x+bz | Wr x+br | Wc x+bc), row of
+ *        column n is gx_row[n] (NULL -> n), stride ldgx
+ *   gh : [N][2H] state-side products (Uz h | Ur h), stride ldgh
+ *   z  = sigmoid(gx_z + gh_z), r = sigmoid(gx_r + gh_r), rh = r * h
+ * qnmt_gru_combine:  cand = tanh(gx_c + ghc); h_out = (1 - z) * h + z * cand
+ *   h_out row n also copied to out2 row out2_row[n] (if out2 != NULL).
+ * ------------------------------------------------------------------------- */
+int qnmt_gru_gates(const float* gx, int64_t ldgx, const int32_t* gx_row,
+                   const float* gh, int64_t ldgh, const float* h, int64_t ldh,
+                   int64_t N, int64_t H, float* z, float* rh, int32_t* err_flag, void* stream);
+int qnmt_gru_combine(const float* gx, int64_t ldgx, const int32_t* gx_row,
+                     const float* ghc, int64_t ldghc, const float* z, const float* h, int64_t ldh,
+                     int64_t N, int64_t H, float* h_out, int64_t ldo,
+                     float* out2, int64_t ld2, const int32_t* out2_row,
+                     int32_t* err_flag, void* stream);
+
+/* y = tanh(x) elementwise (fp64-evaluated, rounded once), [N][D] rows */
+int qnmt_tanh(const float* x, int64_t N, int64_t D, int64_t ldx, float* y, int64_t ldy,
+              int32_t* err_flag, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * Attention (layers.py:214-241) for N query columns.
+ *   column n belongs to sentence col_sent[n] with length sent_len[s]; its
+ *   att_proj / states rows start at row sent_row[s] of
+ *   att_proj [*][A] and states [*][2H] (position-major).
+ *   u = state_proj(query) : [N][A] (stride ldu), v: [A] int8 codes, v_scale
+ *   device f32[1].
+ *   scores[n][i] = v . q(tanh(att_proj_i + u_n)) with ONE scale per column
+ *   over its whole [A, l] block (layers.py:224-226);
+ *   alpha = softmax_i(scores) (fp64, rounded); ctx = sum_i alpha_i states_i
+ *   (fp64, rounded).
+ *   ctx: [N][2H] (ldc); alpha (nullable): [N][lda]; scratch: >= N*(max_len+1)*4 bytes
+ * ------------------------------------------------------------------------- */
+int qnmt_attention(const float* u, int64_t ldu, int64_t N, const int32_t* col_sent,
+                   const float* att_proj, const float* states, const int64_t* sent_row,
+                   const int32_t* sent_len, int32_t max_len, int64_t A, int64_t H2,
+                   const int8_t* v_codes, const float* v_scale,
+                   float* ctx, int64_t ldc, float* alpha, int64_t lda,
+                   void* scratch, int32_t* err_flag, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * Output softmax (layers.py:60-67) and beam candidates (decoder.py:74-85,
+ * :125).  logits: [N][V] f32 (ld).
+ *   lp = fl32( (f64 v - f64 max) - log(sum exp(f64 v - f64 max)) )
+ * qnmt_log_softmax writes lp [N][ldlp].
+ * qnmt_topk_candidates: per column n, the k best (score desc, token asc) with
+ *   score = live_scores[n] + f64(lp); cand_score [N][k] f64, cand_tok [N][k].
+ * ------------------------------------------------------------------------- */
+int qnmt_log_softmax(const float* logits, int64_t N, int64_t V, int64_t ld,
+                     float* lp, int64_t ldlp, int32_t* err_flag, void* stream);
+int qnmt_topk_candidates(const float* logits, int64_t N, int64_t V, int64_t ld,
+                         const double* live_scores, int32_t k,
+                         double* cand_score, int32_t* cand_tok, int32_t* err_flag, void* stream);
+
+/* Embedding gather (layers.py:324, :367): out[n] = table[ids[n]] ([rows][E]);
+ * ids outside [0, rows) raise QNMT_FLAG_VOCAB and yield zeros. */
+int qnmt_embed_gather(const float* table, int64_t rows, int64_t E, const int32_t* ids,
+                      int64_t n, float* out, int64_t ldo, int32_t* err_flag, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * Model + batched translation engine (decoder.py:88-160 translate,
+ * layers.py:313-384 encode / decoder_step, bench.py:126-132 corpus loop).
+ *
+ * qnmt_model_create takes device pointers in the order of QNMT_T_* below
+ * (the per-cell weights are the reference's per-gate tensors stacked:
+ * WX = [wz; wr; wc] with 3 scales, UZR = [uz; ur] with 2 scales, UC = uc).
+ * ------------------------------------------------------------------------- */
+enum {
+    QNMT_T_SRC_EMBED = 0, QNMT_T_TGT_EMBED = 1,
+    /* cell c in {0 enc_fwd, 1 enc_bwd, 2 dec_r, 3 dec_q}: base = 2 + 7*c */
+    QNMT_T_CELL_WX = 0, QNMT_T_CELL_WX_SCALES = 1, QNMT_T_CELL_BX = 2,
+    QNMT_T_CELL_UZR = 3, QNMT_T_CELL_UZR_SCALES = 4, QNMT_T_CELL_UC = 5,
+    QNMT_T_CELL_UC_SCALE = 6,
+    QNMT_T_ATT_WENC = 30, QNMT_T_ATT_WENC_SCALE = 31, QNMT_T_ATT_BENC = 32,
+    QNMT_T_ATT_USTATE = 33, QNMT_T_ATT_USTATE_SCALE = 34,
+    QNMT_T_ATT_V = 35, QNMT_T_ATT_V_SCALE = 36,
+    QNMT_T_OUT_WSTATE = 37, QNMT_T_OUT_WSTATE_SCALE = 38, QNMT_T_OUT_BREADOUT = 39,
+    QNMT_T_OUT_WEMBED = 40, QNMT_T_OUT_WEMBED_SCALE = 41,
+    QNMT_T_OUT_WCTX = 42, QNMT_T_OUT_WCTX_SCALE = 43,
+    QNMT_T_OUT_WVOCAB = 44, QNMT_T_OUT_WVOCAB_SCALE = 45, QNMT_T_OUT_BVOCAB = 46,
+    QNMT_T_S0_W = 47, QNMT_T_S0_W_SCALE = 48, QNMT_T_S0_B = 49,
+    QNMT_T_COUNT = 50
+};
+
+/* dims: {src_vocab, tgt_vocab, embed, hidden, attn, readout, s0_mode(0 transform,
+ *        1 zero), attention_query(0 current, 1 previous)} */
+typedef struct qnmt_model qnmt_model;
+typedef struct qnmt_engine qnmt_engine;
+
+int qnmt_model_create(const int32_t* dims, const void* const* tensors, int32_t ntensors,
+                      qnmt_model** out);
+int qnmt_model_destroy(qnmt_model* m);
+
+/* Engine: scratch for up to max_sentences sentences of length <= max_src_len
+ * at beam width <= max_beam. */
+int qnmt_engine_create(const qnmt_model* m, int32_t max_sentences, int32_t max_src_len,
+                       int32_t max_beam, qnmt_engine** out);
+int qnmt_engine_destroy(qnmt_engine* e);
+
+/* Translate n_sent sentences (each exactly as decoder.translate with one
+ * model and the given beam / max_ratio).
+ *   src_ids (host): concatenated source ids; src_len (host): lengths.
+ *   out_tokens (host): [n_sent][out_stride] target ids without the final EOS
+ *   out_len (host), out_logp (host): length and total log-prob per sentence.
+ *   out_stride must be >= ceil(max_ratio * max_len) + 1.
+ * Returns QNMT_ERR_EMPTY / _VOCAB / _NUMERIC / _CONFIG like translate. */
+int qnmt_translate_batch(qnmt_engine* e, const int32_t* src_ids, const int32_t* src_len,
+                         int32_t n_sent, int32_t beam, double max_ratio,
+                         int32_t* out_tokens, int32_t out_stride, int32_t* out_len,
+                         double* out_logp, void* stream);
+
+/* Encoder only (layers.py:313-348) for a batch, device in/out:
+ *   src_ids (device) concatenated, sent_row (host) row offsets, src_len (host).
+ *   states [sum_l][2H] (backward half first, layers.py:342), att_proj [sum_l][A],
+ *   s0 [n_sent][H]. */
+int qnmt_encode_batch(qnmt_engine* e, const int32_t* src_ids_dev, const int32_t* src_len,
+                      int32_t n_sent, float* states, float* att_proj, float* s0,
+                      void* stream);
+
+/* One decoder step (layers.py:356-384) for N hypothesis columns of n_sent
+ * sentences, all buffers on device:
+ *   col_sent [N] sentence of each column (activation scales are per sentence,
+ *   i.e. per reference decoder_step call); y [N] previous tokens; s, sp [N][H]
+ *   state and previous intermediate state; states/att_proj from
+ *   qnmt_encode_batch with sent_row [n_sent] (int64) / sent_len [n_sent];
+ *   outputs s_int, s_new [N][H], logits [N][V] (log_softmax is separate),
+ *   alpha [N][lda] (nullable). */
+int qnmt_decoder_step(qnmt_engine* e, int64_t N, const int32_t* col_sent, int32_t n_sent,
+                      const int32_t* y, const float* s, const float* sp, const float* states,
+                      const float* att_proj, const int64_t* sent_row, const int32_t* sent_len,
+                      int32_t max_len, float* s_int, float* s_new, float* logits, float* alpha,
+                      int64_t lda, void* stream);
+
+/* Device-resident variant for benchmarking / pipelines: src_ids already on the
+ * device, results kept in the engine until qnmt_fetch_results (D2H + the
+ * final host-side min-by-(-logp, tokens) selection of decoder.py:157). */
+int qnmt_decode_batch_device(qnmt_engine* e, const int32_t* src_ids_dev, const int32_t* src_len,
+                             int32_t n_sent, int32_t beam, double max_ratio, void* stream);
+int qnmt_fetch_results(qnmt_engine* e, int32_t* out_tokens, int32_t out_stride, int32_t* out_len,
+                       double* out_logp, void* stream);
+/* bytes copied device->host by the last fetch */
+int64_t qnmt_last_d2h_bytes(const qnmt_engine* e);
+/* kernels launched by this library since load (process-wide counter) */
+int64_t qnmt_kernel_launches(void);
+
+/* device bytes held by the engine (scratch + history) */
+size_t qnmt_engine_bytes(const qnmt_engine* e);
+
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* QNMT_B200_H */

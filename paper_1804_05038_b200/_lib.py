@@ -1,0 +1,102 @@
+"""ctypes binding of ``_lib/libqnmt_b200.so`` (the C ABI of include/qnmt_b200.h).
+
+There is deliberately no fallback: if the shared library is missing, or no
+CUDA device is present when a kernel is requested, the call raises.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+
+from . import errors
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libqnmt_b200.so")
+
+P = C.c_void_p
+I64 = C.c_int64
+I32 = C.c_int32
+F32 = C.c_float
+F64 = C.c_double
+
+# name -> (restype, argtypes); mirrors include/qnmt_b200.h
+SIGNATURES = {
+    "qnmt_abi_version": (I32, []),
+    "qnmt_last_error": (C.c_char_p, []),
+    "qnmt_device_sync": (I32, []),
+    "qnmt_quantize": (I32, [P, I64, I64, I64, P, I32, P, I64, P, P, I32, P, P]),
+    "qnmt_dequantize": (I32, [P, I64, F32, P, P]),
+    "qnmt_gemm_i8": (I32, [P, I64, I64, I64, P, I64, P, I64, I64, P, P, P, P, I64, P, I32, P]),
+    "qnmt_gru_gates": (I32, [P, I64, P, P, I64, P, I64, I64, I64, P, P, P, P]),
+    "qnmt_gru_combine": (I32, [P, I64, P, P, I64, P, P, I64, I64, I64, P, I64, P, I64, P, P, P]),
+    "qnmt_tanh": (I32, [P, I64, I64, I64, P, I64, P, P]),
+    "qnmt_attention": (I32, [P, I64, I64, P, P, P, P, P, I32, I64, I64, P, P, P, I64, P, I64, P, P, P]),
+    "qnmt_log_softmax": (I32, [P, I64, I64, I64, P, I64, P, P]),
+    "qnmt_topk_candidates": (I32, [P, I64, I64, I64, P, I32, P, P, P, P]),
+    "qnmt_embed_gather": (I32, [P, I64, I64, P, I64, P, I64, P, P]),
+    "qnmt_model_create": (I32, [P, P, I32, P]),
+    "qnmt_model_destroy": (I32, [P]),
+    "qnmt_engine_create": (I32, [P, I32, I32, I32, P]),
+    "qnmt_engine_destroy": (I32, [P]),
+    "qnmt_engine_bytes": (C.c_size_t, [P]),
+    "qnmt_translate_batch": (I32, [P, P, P, I32, I32, F64, P, I32, P, P, P]),
+    "qnmt_encode_batch": (I32, [P, P, P, I32, P, P, P, P]),
+    "qnmt_decoder_step": (I32, [P, I64, P, I32, P, P, P, P, P, P, P, I32, P, P, P, P, I64, P]),
+    "qnmt_decode_batch_device": (I32, [P, P, P, I32, I32, F64, P]),
+    "qnmt_fetch_results": (I32, [P, P, I32, P, P, P]),
+    "qnmt_last_d2h_bytes": (I64, [P]),
+    "qnmt_kernel_launches": (I64, []),
+}
+
+QNMT_OK, ERR_SHAPE, ERR_INVALID, ERR_NUMERIC, ERR_VOCAB, ERR_CONFIG, ERR_EMPTY, ERR_CUDA = range(8)
+FLAG_NUMERIC, FLAG_INVALID, FLAG_VOCAB = 1, 2, 4
+GEMM_ACCUMULATE = 1
+INT32_SAFE_K = 131_000
+
+_EXC = {
+    ERR_SHAPE: errors.ShapeError,
+    ERR_INVALID: errors.InvalidInputError,
+    ERR_NUMERIC: errors.NumericError,
+    ERR_VOCAB: errors.VocabError,
+    ERR_CONFIG: errors.ConfigError,
+    ERR_EMPTY: errors.EmptyInputError,
+    ERR_CUDA: errors.DeviceError,
+}
+
+_lib = None
+_lock = threading.Lock()
+
+
+def load() -> C.CDLL:
+    """Load the shared library (no GPU needed just to load it)."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise errors.DeviceError(
+                    f"{LIB_PATH} is missing: build it with `python -m paper_1804_05038_b200._build` "
+                    "(there is no CPU fallback)")
+            lib = C.CDLL(LIB_PATH)
+            for name, (res, args) in SIGNATURES.items():
+                fn = getattr(lib, name)
+                fn.restype = res
+                fn.argtypes = args
+            _lib = lib
+    return _lib
+
+
+def check(rc: int, what: str):
+    if rc != QNMT_OK:
+        msg = load().qnmt_last_error().decode(errors="replace")
+        raise _EXC.get(rc, errors.DeviceError)(f"{what}: {msg}")
+
+
+def call(name: str, *args):
+    rc = getattr(load(), name)(*args)
+    check(rc, name)
+    return rc
+
+
+def exported_symbols() -> list:
+    return list(SIGNATURES)

@@ -1,0 +1,114 @@
+// common.cuh -- shared helpers for the qnmt B200 kernels (sm_100a).
+//
+// Numerics rules:
+//  * f32 elementwise ops that the reference performs as separate numpy f32
+//    ufuncs are written with __fadd_rn / __fmul_rn / __fsub_rn so ptxas can
+//    never contract them into FMAs.
+//  * sigmoid / tanh / exp / log are evaluated in fp64 and rounded once to f32
+//    (the "Tier B" contract of oracle/qnmt_oracle.py).
+//  * dequantization is fl32(f64(acc) / (f64(sa) * f64(sb))) (qmath.py:379-381).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+
+#include "../../include/qnmt_b200.h"
+
+namespace qnmt {
+
+void set_error(const char* fmt, ...);
+int cuda_status(cudaError_t e, const char* where);
+void count_launch();
+
+#define QNMT_CHECK_LAUNCH(where)                                              \
+    do {                                                                      \
+        ::qnmt::count_launch();                                               \
+        cudaError_t _e = cudaGetLastError();                                  \
+        if (_e != cudaSuccess) return ::qnmt::cuda_status(_e, where);         \
+    } while (0)
+
+#define QNMT_CUDA(call)                                                       \
+    do {                                                                      \
+        cudaError_t _e = (call);                                              \
+        if (_e != cudaSuccess) return ::qnmt::cuda_status(_e, #call);         \
+    } while (0)
+
+static inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+static inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// ---------------------------------------------------------------------------
+// device math
+// ---------------------------------------------------------------------------
+
+// Tier-B transcendental helpers: evaluate in fp64, round once to f32.
+__device__ __forceinline__ float tanh_b(float x) {
+    return __double2float_rn(tanh((double)x));
+}
+
+__device__ __forceinline__ float sigmoid_b(float x) {
+    double v = (double)x;
+    double r;
+    if (v >= 0.0) {
+        r = 1.0 / (1.0 + exp(-v));
+    } else {
+        double e = exp(v);
+        r = e / (1.0 + e);
+    }
+    return __double2float_rn(r);
+}
+
+__device__ __forceinline__ bool is_finite_f(float x) {
+    return (__float_as_uint(x) & 0x7f800000u) != 0x7f800000u;
+}
+
+// Code assignment of qmath.py:119-133 for one value with scale s.
+__device__ __forceinline__ int quant_code(float x, float s) {
+    float v = __fmul_rn(x, s);
+    float q = floorf(__fadd_rn(fabsf(v), 0.5f));
+    if (v < 0.0f) q = -q;
+    q = fminf(fmaxf(q, -127.0f), 127.0f);
+    return (int)q;
+}
+
+// Scale rule of qmath.py:136-142 from the max magnitude (as u32 bits of |x|).
+__device__ __forceinline__ float scale_from_maxbits(uint32_t bits) {
+    float m = __uint_as_float(bits);
+    return (bits == 0u) ? 1.0f : __fdiv_rn(127.0f, m);
+}
+
+// Dequantization of qmath.py:379-381.
+__device__ __forceinline__ float dequant(long long acc, float sa, float sb) {
+    double den = __dmul_rn((double)sa, (double)sb);
+    return __double2float_rn(__ddiv_rn((double)acc, den));
+}
+
+__device__ __forceinline__ void set_flag(int32_t* flag, int bit) {
+    if (flag) atomicOr(flag, bit);
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_max(T v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// 16-byte streaming load that bypasses L1 allocation (weights are read once).
+__device__ __forceinline__ int4 ld_stream16(const void* p) {
+    int4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p));
+    return r;
+}
+
+}  // namespace qnmt

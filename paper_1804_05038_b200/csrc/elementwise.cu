@@ -1,0 +1,153 @@
+// elementwise.cu -- GRU gate arithmetic, tanh, embedding gather.
+//
+// GRU (layers.py:170-181):
+//   z  = sigmoid((Wz x + bz) + Uz h)            -- f32 add, fp64 sigmoid, round
+//   r  = sigmoid((Wr x + br) + Ur h)
+//   rh = r * h                                  -- f32 mul (feeds the 2nd phase)
+//   h~ = tanh((Wc x + bc) + Uc (r*h))
+//   h' = (1 - z) * h + z * h~                   -- four separate f32 ops
+// Every f32 op is an explicit __f*_rn intrinsic, so no FMA contraction can
+// change the association the reference's numpy expression fixes.
+#include "common.cuh"
+
+namespace qnmt {
+
+__global__ void k_gru_gates(const float* __restrict__ gx, int64_t ldgx, const int32_t* __restrict__ gx_row,
+                            const float* __restrict__ gh, int64_t ldgh, const float* __restrict__ h,
+                            int64_t ldh, int64_t N, int64_t H, float* __restrict__ z,
+                            float* __restrict__ rh, int32_t* err_flag) {
+    int64_t n = blockIdx.y;
+    int64_t rowx = gx_row ? gx_row[n] : n;
+    const float* gxr = gx + rowx * ldgx;
+    const float* ghr = gh + n * ldgh;
+    bool bad = false;
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < H; j += (int64_t)gridDim.x * blockDim.x) {
+        float pz = __fadd_rn(gxr[j], ghr[j]);
+        float pr = __fadd_rn(gxr[H + j], ghr[H + j]);
+        bad |= !is_finite_f(pz) || !is_finite_f(pr);
+        float zz = sigmoid_b(pz);
+        float rr = sigmoid_b(pr);
+        z[n * H + j] = zz;
+        rh[n * H + j] = __fmul_rn(rr, h[n * ldh + j]);
+    }
+    if (bad) set_flag(err_flag, QNMT_FLAG_NUMERIC);
+}
+
+__global__ void k_gru_combine(const float* __restrict__ gx, int64_t ldgx, const int32_t* __restrict__ gx_row,
+                              const float* __restrict__ ghc, int64_t ldghc, const float* __restrict__ z,
+                              const float* __restrict__ h, int64_t ldh, int64_t N, int64_t H,
+                              float* __restrict__ h_out, int64_t ldo, float* __restrict__ out2,
+                              int64_t ld2, const int32_t* __restrict__ out2_row, int32_t* err_flag) {
+    int64_t n = blockIdx.y;
+    int64_t rowx = gx_row ? gx_row[n] : n;
+    const float* gxr = gx + rowx * ldgx + 2 * H;
+    bool bad = false;
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < H; j += (int64_t)gridDim.x * blockDim.x) {
+        float pc = __fadd_rn(gxr[j], ghc[n * ldghc + j]);
+        bad |= !is_finite_f(pc);
+        float c = tanh_b(pc);
+        float zz = z[n * H + j];
+        float hh = h[n * ldh + j];
+        float v = __fadd_rn(__fmul_rn(__fsub_rn(1.0f, zz), hh), __fmul_rn(zz, c));
+        h_out[n * ldo + j] = v;
+        if (out2) out2[(int64_t)out2_row[n] * ld2 + j] = v;
+    }
+    if (bad) set_flag(err_flag, QNMT_FLAG_NUMERIC);
+}
+
+__global__ void k_tanh(const float* __restrict__ x, int64_t N, int64_t D, int64_t ldx,
+                       float* __restrict__ y, int64_t ldy, int32_t* err_flag) {
+    int64_t n = blockIdx.y;
+    bool bad = false;
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < D; j += (int64_t)gridDim.x * blockDim.x) {
+        float v = x[n * ldx + j];
+        bad |= !is_finite_f(v);
+        y[n * ldy + j] = tanh_b(v);
+    }
+    if (bad) set_flag(err_flag, QNMT_FLAG_NUMERIC);
+}
+
+__global__ void k_embed_gather(const float* __restrict__ table, int64_t rows, int64_t E,
+                               const int32_t* __restrict__ ids, float* __restrict__ out,
+                               int64_t ldo, int32_t* err_flag) {
+    int64_t n = blockIdx.x;
+    int32_t id = ids[n];
+    bool ok = id >= 0 && id < rows;
+    if (!ok && threadIdx.x == 0) set_flag(err_flag, QNMT_FLAG_VOCAB);
+    for (int64_t j = threadIdx.x; j < E; j += blockDim.x)
+        out[n * ldo + j] = ok ? table[(int64_t)id * E + j] : 0.0f;
+}
+
+static inline dim3 rows_grid(int64_t N, int64_t D, int threads) {
+    int64_t bx = cdiv(D, threads);
+    if (bx > 64) bx = 64;
+    return dim3((unsigned)bx, (unsigned)N);
+}
+
+int gru_gates_launch(const float* gx, int64_t ldgx, const int32_t* gx_row, const float* gh,
+                     int64_t ldgh, const float* h, int64_t ldh, int64_t N, int64_t H, float* z,
+                     float* rh, int32_t* err_flag, cudaStream_t st) {
+    if (N <= 0) return QNMT_OK;
+    k_gru_gates<<<rows_grid(N, H, 256), 256, 0, st>>>(gx, ldgx, gx_row, gh, ldgh, h, ldh, N, H, z, rh, err_flag);
+    QNMT_CHECK_LAUNCH("k_gru_gates");
+    return QNMT_OK;
+}
+
+int gru_combine_launch(const float* gx, int64_t ldgx, const int32_t* gx_row, const float* ghc,
+                       int64_t ldghc, const float* z, const float* h, int64_t ldh, int64_t N,
+                       int64_t H, float* h_out, int64_t ldo, float* out2, int64_t ld2,
+                       const int32_t* out2_row, int32_t* err_flag, cudaStream_t st) {
+    if (N <= 0) return QNMT_OK;
+    k_gru_combine<<<rows_grid(N, H, 256), 256, 0, st>>>(gx, ldgx, gx_row, ghc, ldghc, z, h, ldh, N, H,
+                                                        h_out, ldo, out2, ld2, out2_row, err_flag);
+    QNMT_CHECK_LAUNCH("k_gru_combine");
+    return QNMT_OK;
+}
+
+int tanh_launch(const float* x, int64_t N, int64_t D, int64_t ldx, float* y, int64_t ldy,
+                int32_t* err_flag, cudaStream_t st) {
+    if (N <= 0) return QNMT_OK;
+    k_tanh<<<rows_grid(N, D, 256), 256, 0, st>>>(x, N, D, ldx, y, ldy, err_flag);
+    QNMT_CHECK_LAUNCH("k_tanh");
+    return QNMT_OK;
+}
+
+int embed_gather_launch(const float* table, int64_t rows, int64_t E, const int32_t* ids, int64_t n,
+                        float* out, int64_t ldo, int32_t* err_flag, cudaStream_t st) {
+    if (n <= 0) return QNMT_OK;
+    k_embed_gather<<<(unsigned)n, 128, 0, st>>>(table, rows, E, ids, out, ldo, err_flag);
+    QNMT_CHECK_LAUNCH("k_embed_gather");
+    return QNMT_OK;
+}
+
+}  // namespace qnmt
+
+extern "C" {
+
+int qnmt_gru_gates(const float* gx, int64_t ldgx, const int32_t* gx_row, const float* gh,
+                   int64_t ldgh, const float* h, int64_t ldh, int64_t N, int64_t H, float* z,
+                   float* rh, int32_t* err_flag, void* stream) {
+    return qnmt::gru_gates_launch(gx, ldgx, gx_row, gh, ldgh, h, ldh, N, H, z, rh, err_flag,
+                                  qnmt::as_stream(stream));
+}
+
+int qnmt_gru_combine(const float* gx, int64_t ldgx, const int32_t* gx_row, const float* ghc,
+                     int64_t ldghc, const float* z, const float* h, int64_t ldh, int64_t N,
+                     int64_t H, float* h_out, int64_t ldo, float* out2, int64_t ld2,
+                     const int32_t* out2_row, int32_t* err_flag, void* stream) {
+    return qnmt::gru_combine_launch(gx, ldgx, gx_row, ghc, ldghc, z, h, ldh, N, H, h_out, ldo, out2,
+                                    ld2, out2_row, err_flag, qnmt::as_stream(stream));
+}
+
+int qnmt_tanh(const float* x, int64_t N, int64_t D, int64_t ldx, float* y, int64_t ldy,
+              int32_t* err_flag, void* stream) {
+    return qnmt::tanh_launch(x, N, D, ldx, y, ldy, err_flag, qnmt::as_stream(stream));
+}
+
+int qnmt_embed_gather(const float* table, int64_t rows, int64_t E, const int32_t* ids, int64_t n,
+                      float* out, int64_t ldo, int32_t* err_flag, void* stream) {
+    return qnmt::embed_gather_launch(table, rows, E, ids, n, out, ldo, err_flag,
+                                     qnmt::as_stream(stream));
+}
+
+}  // extern "C"

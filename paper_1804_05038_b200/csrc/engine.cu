@@ -1,0 +1,743 @@
+// engine.cu -- model handle and the batched translation engine.
+//
+// Batched form of decoder.translate (decoder.py:88-160) over many sentences
+// at once, bit-identical to running translate sentence by sentence:
+//  * every activation quantization keeps the reference's granularity
+//    (one scale per LinearOp.apply call) via per-segment
+//    scales: segment = sentence (decoder), = (sentence, direction) (encoder
+//    state side), = position (encoder input side), = sentence (att_proj, s0);
+//  * the search runs on device (search.cu) one thread per sentence;
+//  * the host only reads back the live-column count once per step and the
+//    finished lists / history once per batch.
+#include <math.h>
+#include <string.h>
+
+#include <algorithm>
+#include <numeric>
+#include <vector>
+
+#include "common.cuh"
+#include "gemm.cuh"
+#include "search.cuh"
+
+namespace qnmt {
+
+int gru_gates_launch(const float* gx, int64_t ldgx, const int32_t* gx_row, const float* gh,
+                     int64_t ldgh, const float* h, int64_t ldh, int64_t N, int64_t H, float* z,
+                     float* rh, int32_t* err_flag, cudaStream_t st);
+int gru_combine_launch(const float* gx, int64_t ldgx, const int32_t* gx_row, const float* ghc,
+                       int64_t ldghc, const float* z, const float* h, int64_t ldh, int64_t N,
+                       int64_t H, float* h_out, int64_t ldo, float* out2, int64_t ld2,
+                       const int32_t* out2_row, int32_t* err_flag, cudaStream_t st);
+int tanh_launch(const float* x, int64_t N, int64_t D, int64_t ldx, float* y, int64_t ldy,
+                int32_t* err_flag, cudaStream_t st);
+int embed_gather_launch(const float* table, int64_t rows, int64_t E, const int32_t* ids, int64_t n,
+                        float* out, int64_t ldo, int32_t* err_flag, cudaStream_t st);
+int attention_launch(const float* u, int64_t ldu, int64_t N, const int32_t* col_sent,
+                     const float* att_proj, const float* states, const int64_t* sent_row,
+                     const int32_t* sent_len, int32_t max_len, int64_t A, int64_t H2,
+                     const int8_t* v_codes, const float* v_scale, float* ctx, int64_t ldc,
+                     float* alpha, int64_t lda, void* scratch, int32_t* err_flag, cudaStream_t st);
+int topk_launch(const float* logits, int64_t N, int64_t V, int64_t ld, const double* live, int32_t k,
+                double* cand_score, int32_t* cand_tok, int32_t* err_flag, cudaStream_t st);
+
+struct Cell {
+    const int8_t* wx;
+    const float* wx_s;
+    const float* bx;
+    const int8_t* uzr;
+    const float* uzr_s;
+    const int8_t* uc;
+    const float* uc_s;
+    int in;
+};
+
+}  // namespace qnmt
+
+struct qnmt_model {
+    int Vs, Vt, E, H, A, R, s0_mode, aq;
+    const float* src_embed;
+    const float* tgt_embed;
+    qnmt::Cell cell[4];
+    const int8_t* w_enc; const float* w_enc_s; const float* b_enc;
+    const int8_t* u_att; const float* u_att_s;
+    const int8_t* v; const float* v_s;
+    const int8_t* w_state; const float* w_state_s; const float* b_r;
+    const int8_t* w_embed; const float* w_embed_s;
+    const int8_t* w_ctx; const float* w_ctx_s;
+    const int8_t* w_vocab; const float* w_vocab_s; const float* b_vocab;
+    const int8_t* s0_w; const float* s0_s; const float* s0_b;
+};
+
+namespace qnmt {
+
+// simple bump allocator over one cudaMalloc block
+struct Arena {
+    char* base = nullptr;
+    size_t cap = 0, used = 0;
+    template <typename T>
+    T* take(size_t n) {
+        size_t bytes = (n * sizeof(T) + 255) & ~(size_t)255;
+        T* p = reinterpret_cast<T*>(base + used);
+        used += bytes;
+        return p;
+    }
+};
+
+}  // namespace qnmt
+
+struct qnmt_engine {
+    const qnmt_model* m;
+    int S, L, B;       // max sentences, max source length, max beam
+    int64_t NMAX;      // S * B
+    int64_t PMAX;      // S * L
+    char* block = nullptr;
+    size_t block_bytes = 0;
+    // shared
+    int32_t* err;            // device sticky flag
+    uint32_t* seg_bits;      // [max(PMAX, 2S, S)]
+    int32_t* iota;           // [max(PMAX, 2S)] identity
+    int32_t* even;           // [S] 0,2,4..
+    int32_t* odd;            // [S] 1,3,5..
+    // encoder
+    int32_t* src_ids;        // [PMAX]
+    float* emb_src;          // [PMAX][E]
+    int8_t* q_emb_src;       // [PMAX][E]
+    float* sc_pos;           // [PMAX]
+    float* gx_enc;           // [PMAX][2][3H]
+    float* h2;               // [S][2][H]
+    int8_t* q_h2;            // [S][2][H]
+    float* sc_h2;            // [2S]
+    float* gh2;              // [S][2][2H]
+    float* z2;               // [2S][H]
+    float* rh2;              // [2S][H]
+    int8_t* q_rh2;           // [2S][H]
+    float* sc_rh2;           // [2S]
+    float* ghc2;             // [S][2][H]
+    int32_t* enc_rows;       // [L][2S] gx rows per step
+    int32_t* enc_out_rows;   // [L][2S] states half-rows per step
+    int8_t* q_states;        // [PMAX][2H]
+    float* sc_sent;          // [S]
+    int32_t* pos_sent;       // [PMAX] sentence of each position
+    float* s0tmp;            // [S][H]
+    int32_t* s0_dst;         // [S] original index of sorted slot
+    float* enc_states;       // [PMAX][2H]  (engine-owned encoder output for translate)
+    float* enc_att;          // [PMAX][A]
+    float* enc_s0;           // [S][H]
+    int64_t* sent_row;       // [S]
+    int32_t* sent_len;       // [S]
+    // decoder (NMAX columns)
+    float* emb;              // [N][E]
+    int8_t* q_emb;           // [N][E]
+    float* sc_emb;           // [S]
+    int8_t* q_s;             // [N][H]
+    float* sc_s;
+    float* gx;               // [N][3H]
+    float* gh;               // [N][2H]
+    float* z;                // [N][H]
+    float* rh;               // [N][H]
+    int8_t* q_rh;
+    float* sc_rh;
+    float* ghc;              // [N][H]
+    int8_t* q_q;             // query codes [N][H]
+    float* sc_q;
+    float* u;                // [N][A]
+    float* ctx;              // [N][2H]
+    int8_t* q_ctx;
+    float* sc_ctx;
+    int8_t* q_si;            // s_int codes (when query != s_int)
+    float* sc_si;
+    int8_t* q_sn;
+    float* sc_sn;
+    float* ro;               // [N][R]
+    int8_t* q_ro;
+    float* sc_ro;
+    float* logits;           // [N][V]
+    void* att_scratch;
+    // translate loop state
+    float* st_s[2];          // [N][H] s
+    float* st_sp[2];         // [N][H] s_prime
+    float* s_int;            // [N][H]
+    float* s_new;            // [N][H]
+    int32_t* y[2];
+    int32_t* col_sent[2];
+    double* live[2];
+    int32_t* parent_col;
+    double* cand_score;      // [N][B]
+    int32_t* cand_tok;
+    int32_t* n_live;
+    int32_t* P; int32_t* col_off; int32_t* done; int32_t* max_steps; int32_t* steps_run;
+    int32_t* fin_cnt; double* fin_best;
+    // history/finished (grown on demand)
+    char* hblock = nullptr;
+    size_t hblock_bytes = 0;
+    int hist_steps = 0;
+    double* fin_score; int32_t* fin_step; int32_t* fin_slot; int32_t* fin_eos;
+    int32_t* hist_tok; int32_t* hist_par;
+    int32_t* h_pinned = nullptr;   // host pinned scalar
+    int last_n = 0, last_tmax = 0;
+    int64_t d2h_bytes = 0;
+};
+
+namespace qnmt {
+
+static int check_flag(qnmt_engine* e, cudaStream_t st) {
+    int32_t f = 0;
+    QNMT_CUDA(cudaMemcpyAsync(&f, e->err, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    QNMT_CUDA(cudaStreamSynchronize(st));
+    if (f & QNMT_FLAG_VOCAB) { set_error("token id outside the vocabulary"); return QNMT_ERR_VOCAB; }
+    if (f & QNMT_FLAG_NUMERIC) { set_error("activations contain non-finite values"); return QNMT_ERR_NUMERIC; }
+    if (f & QNMT_FLAG_INVALID) { set_error("non-finite weight"); return QNMT_ERR_INVALID_INPUT; }
+    return QNMT_OK;
+}
+
+#define TRY(x) do { int _r = (x); if (_r != QNMT_OK) return _r; } while (0)
+
+static int gemm(const int8_t* W, int64_t M, int64_t K, const float* ws, int64_t rps, const int8_t* X,
+                int64_t N, int64_t ldx, const float* xs, const int32_t* seg, const float* bias, float* Y,
+                int64_t ldy, int32_t flags, cudaStream_t st) {
+    GemmArgs g{W, M, K, K, ws, rps, X, N, ldx, xs, seg, bias, Y, ldy, nullptr, flags};
+    return gemm_i8_launch(g, st);
+}
+
+// ---------------------------------------------------------------------------
+// encoder (layers.py:313-348) for n sentences in arbitrary order.
+//   ids: device, concatenated; len/row: host.  Outputs at caller pointers.
+// ---------------------------------------------------------------------------
+static int encode_core(qnmt_engine* e, const int32_t* ids_dev, const int32_t* len, const int64_t* row,
+                       int n, float* states, float* att_proj, float* s0, cudaStream_t st) {
+    const qnmt_model* m = e->m;
+    const int64_t E = m->E, H = m->H, A = m->A;
+    int64_t P = 0;
+    int Lmax = 0;
+    for (int i = 0; i < n; ++i) {
+        if (len[i] < 1) { set_error("cannot encode an empty sentence"); return QNMT_ERR_EMPTY; }
+        if (len[i] > e->L) { set_error("sentence length %d exceeds engine max %d", len[i], e->L); return QNMT_ERR_CONFIG; }
+        P = std::max<int64_t>(P, row[i] + len[i]);
+        Lmax = std::max(Lmax, len[i]);
+    }
+    if (n > e->S || P > e->PMAX) { set_error("batch exceeds engine capacity"); return QNMT_ERR_CONFIG; }
+    // sorted slots: longest first (stable) -> active sentences are a prefix
+    std::vector<int> perm(n);
+    std::iota(perm.begin(), perm.end(), 0);
+    std::stable_sort(perm.begin(), perm.end(), [&](int a, int b) { return len[a] > len[b]; });
+    std::vector<int32_t> rows((size_t)Lmax * 2 * n), orows((size_t)Lmax * 2 * n), pos_sent(P, 0);
+    for (int t = 0; t < Lmax; ++t) {
+        for (int k = 0; k < n; ++k) {
+            int s = perm[k];
+            if (len[s] <= t) continue;
+            int64_t pf = row[s] + t, pb = row[s] + len[s] - 1 - t;
+            rows[(size_t)t * 2 * n + 2 * k] = (int32_t)(2 * pf + 0);
+            rows[(size_t)t * 2 * n + 2 * k + 1] = (int32_t)(2 * pb + 1);
+            orows[(size_t)t * 2 * n + 2 * k] = (int32_t)(2 * pf + 1);      // fwd half = upper
+            orows[(size_t)t * 2 * n + 2 * k + 1] = (int32_t)(2 * pb + 0);  // bwd half = lower
+        }
+    }
+    for (int s = 0; s < n; ++s)
+        for (int i = 0; i < len[s]; ++i) pos_sent[row[s] + i] = s;
+    std::vector<int32_t> s0dst(n);   // slot of each sentence (inverse permutation)
+    for (int k = 0; k < n; ++k) s0dst[perm[k]] = k;
+    QNMT_CUDA(cudaMemcpyAsync(e->enc_rows, rows.data(), rows.size() * 4, cudaMemcpyHostToDevice, st));
+    QNMT_CUDA(cudaMemcpyAsync(e->enc_out_rows, orows.data(), orows.size() * 4, cudaMemcpyHostToDevice, st));
+    QNMT_CUDA(cudaMemcpyAsync(e->pos_sent, pos_sent.data(), (size_t)P * 4, cudaMemcpyHostToDevice, st));
+    QNMT_CUDA(cudaMemcpyAsync(e->s0_dst, s0dst.data(), (size_t)n * 4, cudaMemcpyHostToDevice, st));
+
+    // input side for every position at once (per-position scales; one GEMM per direction)
+    TRY(embed_gather_launch(m->src_embed, m->Vs, E, ids_dev, P, e->emb_src, E, e->err, st));
+    TRY(quantize_launch(e->emb_src, P, E, E, e->iota, (int32_t)P, e->q_emb_src, E, e->sc_pos,
+                        e->seg_bits, 1, e->err, st));
+    for (int d = 0; d < 2; ++d) {
+        const Cell& c = m->cell[d];
+        TRY(gemm(c.wx, 3 * H, E, c.wx_s, H, e->q_emb_src, P, E, e->sc_pos, e->iota, c.bx,
+                 e->gx_enc + d * 3 * H, 6 * H, 0, st));
+    }
+    QNMT_CUDA(cudaMemsetAsync(e->h2, 0, sizeof(float) * (size_t)n * 2 * H, st));
+    for (int t = 0; t < Lmax; ++t) {
+        int na = 0;
+        while (na < n && len[perm[na]] > t) ++na;
+        int64_t N2 = 2 * (int64_t)na;
+        const int32_t* gxr = e->enc_rows + (size_t)t * 2 * n;
+        const int32_t* outr = e->enc_out_rows + (size_t)t * 2 * n;
+        TRY(quantize_launch(e->h2, N2, H, H, e->iota, (int32_t)N2, e->q_h2, H, e->sc_h2, e->seg_bits, 1,
+                            e->err, st));
+        for (int d = 0; d < 2; ++d) {
+            const Cell& c = m->cell[d];
+            TRY(gemm(c.uzr, 2 * H, H, c.uzr_s, H, e->q_h2 + d * H, na, 2 * H, e->sc_h2,
+                     d ? e->odd : e->even, nullptr, e->gh2 + d * 2 * H, 4 * H, 0, st));
+        }
+        TRY(gru_gates_launch(e->gx_enc, 3 * H, gxr, e->gh2, 2 * H, e->h2, H, N2, H, e->z2, e->rh2, e->err, st));
+        TRY(quantize_launch(e->rh2, N2, H, H, e->iota, (int32_t)N2, e->q_rh2, H, e->sc_rh2, e->seg_bits,
+                            1, e->err, st));
+        for (int d = 0; d < 2; ++d) {
+            const Cell& c = m->cell[d];
+            TRY(gemm(c.uc, H, H, c.uc_s, H, e->q_rh2 + d * H, na, 2 * H, e->sc_rh2, d ? e->odd : e->even,
+                     nullptr, e->ghc2 + d * H, 2 * H, 0, st));
+        }
+        TRY(gru_combine_launch(e->gx_enc, 3 * H, gxr, e->ghc2, H, e->z2, e->h2, H, N2, H, e->h2, H,
+                               states, H, outr, e->err, st));
+    }
+    // att_proj = enc_proj(states) with one scale per sentence over [2H, l] (layers.py:343)
+    TRY(quantize_launch(states, P, 2 * H, 2 * H, e->pos_sent, n, e->q_states, 2 * H, e->sc_sent,
+                        e->seg_bits, 1, e->err, st));
+    TRY(gemm(m->w_enc, A, 2 * H, m->w_enc_s, A, e->q_states, P, 2 * H, e->sc_sent, e->pos_sent, m->b_enc,
+             att_proj, A, 0, st));
+    // s0 = tanh(W_s0 . q(bwd[:, 0]) + b) (layers.py:347); bwd final states are odd rows of h2
+    if (m->s0_mode == 1) {
+        QNMT_CUDA(cudaMemsetAsync(s0, 0, sizeof(float) * (size_t)n * H, st));
+    } else {
+        TRY(quantize_launch(e->h2, 2 * (int64_t)n, H, H, e->iota, 2 * n, e->q_h2, H, e->sc_h2,
+                            e->seg_bits, 1, e->err, st));
+        TRY(gemm(m->s0_w, H, H, m->s0_s, H, e->q_h2 + H, n, 2 * H, e->sc_h2, e->odd, m->s0_b,
+                 e->s0tmp, H, 0, st));
+        // tanh, then rows back to the caller's sentence order: s0[s] = s0tmp[slot_of[s]]
+        TRY(tanh_launch(e->s0tmp, n, H, H, e->s0tmp, H, e->err, st));
+        TRY(gather_rows_launch(e->s0tmp, nullptr, e->s0_dst, n, H, s0, nullptr, st));
+    }
+    return QNMT_OK;
+}
+
+// ---------------------------------------------------------------------------
+// one decoder step (layers.py:356-384) for N columns; logits [N][V] out.
+// ---------------------------------------------------------------------------
+struct StepIO {
+    int64_t N;
+    int nseg;
+    const int32_t* col_sent;
+    const int32_t* y;
+    const float* s;
+    const float* sp;
+    const float* states;
+    const float* att_proj;
+    const int64_t* sent_row;
+    const int32_t* sent_len;
+    int max_len;
+    float* s_int;
+    float* s_new;
+    float* logits;
+    float* alpha;
+    int64_t lda;
+};
+
+static int gru_cell(qnmt_engine* e, const Cell& c, int64_t N, int nseg, const int32_t* seg,
+                    const int8_t* qx, const float* sx, const int8_t* qh, const float* sh,
+                    const float* h, float* h_out, cudaStream_t st) {
+    const int64_t H = e->m->H;
+    TRY(gemm(c.wx, 3 * H, c.in, c.wx_s, H, qx, N, c.in, sx, seg, c.bx, e->gx, 3 * H, 0, st));
+    TRY(gemm(c.uzr, 2 * H, H, c.uzr_s, H, qh, N, H, sh, seg, nullptr, e->gh, 2 * H, 0, st));
+    TRY(gru_gates_launch(e->gx, 3 * H, nullptr, e->gh, 2 * H, h, H, N, H, e->z, e->rh, e->err, st));
+    TRY(quantize_launch(e->rh, N, H, H, seg, nseg, e->q_rh, H, e->sc_rh, e->seg_bits, 1, e->err, st));
+    TRY(gemm(c.uc, H, H, c.uc_s, H, e->q_rh, N, H, e->sc_rh, seg, nullptr, e->ghc, H, 0, st));
+    TRY(gru_combine_launch(e->gx, 3 * H, nullptr, e->ghc, H, e->z, h, H, N, H, h_out, H, nullptr, 0,
+                           nullptr, e->err, st));
+    return QNMT_OK;
+}
+
+static int step_core(qnmt_engine* e, const StepIO& io, cudaStream_t st) {
+    const qnmt_model* m = e->m;
+    const int64_t N = io.N, E = m->E, H = m->H, A = m->A, R = m->R, V = m->Vt;
+    const int32_t* seg = io.col_sent;
+    const int ns = io.nseg;
+    if (N <= 0) return QNMT_OK;
+    TRY(embed_gather_launch(m->tgt_embed, V, E, io.y, N, e->emb, E, e->err, st));
+    TRY(quantize_launch(e->emb, N, E, E, seg, ns, e->q_emb, E, e->sc_emb, e->seg_bits, 1, e->err, st));
+    TRY(quantize_launch(io.s, N, H, H, seg, ns, e->q_s, H, e->sc_s, e->seg_bits, 1, e->err, st));
+    // s' = GRU_r(emb, s)                                        (layers.py:372)
+    TRY(gru_cell(e, m->cell[2], N, ns, seg, e->q_emb, e->sc_emb, e->q_s, e->sc_s, io.s, io.s_int, st));
+    // attention query (layers.py:373)
+    const float* query = (m->aq == 1) ? io.sp : io.s_int;
+    TRY(quantize_launch(query, N, H, H, seg, ns, e->q_q, H, e->sc_q, e->seg_bits, 1, e->err, st));
+    TRY(gemm(m->u_att, A, H, m->u_att_s, A, e->q_q, N, H, e->sc_q, seg, nullptr, e->u, A, 0, st));
+    TRY(attention_launch(e->u, A, N, seg, io.att_proj, io.states, io.sent_row, io.sent_len, io.max_len,
+                         A, 2 * H, m->v, m->v_s, e->ctx, 2 * H, io.alpha, io.lda, e->att_scratch,
+                         e->err, st));
+    TRY(quantize_launch(e->ctx, N, 2 * H, 2 * H, seg, ns, e->q_ctx, 2 * H, e->sc_ctx, e->seg_bits, 1,
+                        e->err, st));
+    // s = GRU_q(ctx, s')                                        (layers.py:375)
+    const int8_t* q_si = e->q_q;
+    const float* sc_si = e->sc_q;
+    if (m->aq == 1) {
+        TRY(quantize_launch(io.s_int, N, H, H, seg, ns, e->q_si, H, e->sc_si, e->seg_bits, 1, e->err, st));
+        q_si = e->q_si;
+        sc_si = e->sc_si;
+    }
+    TRY(gru_cell(e, m->cell[3], N, ns, seg, e->q_ctx, e->sc_ctx, q_si, sc_si, io.s_int, io.s_new, st));
+    // readout = tanh(((W_s s + b_r) + W_e emb) + W_c ctx)       (layers.py:255-265)
+    TRY(quantize_launch(io.s_new, N, H, H, seg, ns, e->q_sn, H, e->sc_sn, e->seg_bits, 1, e->err, st));
+    TRY(gemm(m->w_state, R, H, m->w_state_s, R, e->q_sn, N, H, e->sc_sn, seg, m->b_r, e->ro, R, 0, st));
+    TRY(gemm(m->w_embed, R, E, m->w_embed_s, R, e->q_emb, N, E, e->sc_emb, seg, nullptr, e->ro, R,
+             QNMT_GEMM_ACCUMULATE, st));
+    TRY(gemm(m->w_ctx, R, 2 * H, m->w_ctx_s, R, e->q_ctx, N, 2 * H, e->sc_ctx, seg, nullptr, e->ro, R,
+             QNMT_GEMM_ACCUMULATE, st));
+    TRY(tanh_launch(e->ro, N, R, R, e->ro, R, e->err, st));
+    TRY(quantize_launch(e->ro, N, R, R, seg, ns, e->q_ro, R, e->sc_ro, e->seg_bits, 1, e->err, st));
+    TRY(gemm(m->w_vocab, V, R, m->w_vocab_s, V, e->q_ro, N, R, e->sc_ro, seg, m->b_vocab, io.logits, V,
+             0, st));
+    return QNMT_OK;
+}
+
+static int grow_history(qnmt_engine* e, int steps) {
+    if (steps <= e->hist_steps) return QNMT_OK;
+    if (e->hblock) cudaFree(e->hblock);
+    size_t S = e->S, B = e->B, T = steps;
+    size_t fin_cap = (T + 1) * B;
+    size_t bytes = S * fin_cap * (8 + 4 + 4 + 4) + 2 * S * T * B * 4 + 4096;
+    QNMT_CUDA(cudaMalloc(&e->hblock, bytes));
+    e->hblock_bytes = bytes;
+    Arena a{e->hblock, bytes, 0};
+    e->fin_score = a.take<double>(S * fin_cap);
+    e->fin_step = a.take<int32_t>(S * fin_cap);
+    e->fin_slot = a.take<int32_t>(S * fin_cap);
+    e->fin_eos = a.take<int32_t>(S * fin_cap);
+    e->hist_tok = a.take<int32_t>(S * T * B);
+    e->hist_par = a.take<int32_t>(S * T * B);
+    e->hist_steps = steps;
+    return QNMT_OK;
+}
+
+}  // namespace qnmt
+
+using namespace qnmt;
+
+extern "C" {
+
+int qnmt_model_create(const int32_t* dims, const void* const* t, int32_t nt, qnmt_model** out) {
+    if (nt != QNMT_T_COUNT) { set_error("expected %d tensors, got %d", QNMT_T_COUNT, nt); return QNMT_ERR_CONFIG; }
+    qnmt_model* m = new qnmt_model();
+    m->Vs = dims[0]; m->Vt = dims[1]; m->E = dims[2]; m->H = dims[3]; m->A = dims[4]; m->R = dims[5];
+    m->s0_mode = dims[6]; m->aq = dims[7];
+    m->src_embed = (const float*)t[QNMT_T_SRC_EMBED];
+    m->tgt_embed = (const float*)t[QNMT_T_TGT_EMBED];
+    for (int c = 0; c < 4; ++c) {
+        int b = 2 + 7 * c;
+        Cell& k = m->cell[c];
+        k.wx = (const int8_t*)t[b + QNMT_T_CELL_WX];
+        k.wx_s = (const float*)t[b + QNMT_T_CELL_WX_SCALES];
+        k.bx = (const float*)t[b + QNMT_T_CELL_BX];
+        k.uzr = (const int8_t*)t[b + QNMT_T_CELL_UZR];
+        k.uzr_s = (const float*)t[b + QNMT_T_CELL_UZR_SCALES];
+        k.uc = (const int8_t*)t[b + QNMT_T_CELL_UC];
+        k.uc_s = (const float*)t[b + QNMT_T_CELL_UC_SCALE];
+        k.in = (c == 3) ? 2 * m->H : m->E;
+    }
+    m->w_enc = (const int8_t*)t[QNMT_T_ATT_WENC]; m->w_enc_s = (const float*)t[QNMT_T_ATT_WENC_SCALE];
+    m->b_enc = (const float*)t[QNMT_T_ATT_BENC];
+    m->u_att = (const int8_t*)t[QNMT_T_ATT_USTATE]; m->u_att_s = (const float*)t[QNMT_T_ATT_USTATE_SCALE];
+    m->v = (const int8_t*)t[QNMT_T_ATT_V]; m->v_s = (const float*)t[QNMT_T_ATT_V_SCALE];
+    m->w_state = (const int8_t*)t[QNMT_T_OUT_WSTATE]; m->w_state_s = (const float*)t[QNMT_T_OUT_WSTATE_SCALE];
+    m->b_r = (const float*)t[QNMT_T_OUT_BREADOUT];
+    m->w_embed = (const int8_t*)t[QNMT_T_OUT_WEMBED]; m->w_embed_s = (const float*)t[QNMT_T_OUT_WEMBED_SCALE];
+    m->w_ctx = (const int8_t*)t[QNMT_T_OUT_WCTX]; m->w_ctx_s = (const float*)t[QNMT_T_OUT_WCTX_SCALE];
+    m->w_vocab = (const int8_t*)t[QNMT_T_OUT_WVOCAB]; m->w_vocab_s = (const float*)t[QNMT_T_OUT_WVOCAB_SCALE];
+    m->b_vocab = (const float*)t[QNMT_T_OUT_BVOCAB];
+    m->s0_w = (const int8_t*)t[QNMT_T_S0_W]; m->s0_s = (const float*)t[QNMT_T_S0_W_SCALE];
+    m->s0_b = (const float*)t[QNMT_T_S0_B];
+    *out = m;
+    return QNMT_OK;
+}
+
+int qnmt_model_destroy(qnmt_model* m) {
+    delete m;
+    return QNMT_OK;
+}
+
+int qnmt_engine_create(const qnmt_model* m, int32_t max_sentences, int32_t max_src_len,
+                       int32_t max_beam, qnmt_engine** out) {
+    if (max_sentences < 1 || max_sentences > 1024 || max_src_len < 1 || max_beam < 1 || max_beam > 16) {
+        set_error("engine limits: 1<=sentences<=1024, len>=1, 1<=beam<=16");
+        return QNMT_ERR_CONFIG;
+    }
+    qnmt_engine* e = new qnmt_engine();
+    e->m = m;
+    e->S = max_sentences; e->L = max_src_len; e->B = max_beam;
+    const size_t S = e->S, L = e->L, B = e->B;
+    const size_t E = m->E, H = m->H, A = m->A, R = m->R, V = m->Vt;
+    const size_t N = S * B, P = S * L;
+    e->NMAX = N; e->PMAX = P;
+    const size_t idx = std::max(P, std::max(2 * S, N));
+    size_t bytes = 0;
+    // size pass then carve pass
+    for (int pass = 0; pass < 2; ++pass) {
+        Arena a{e->block, pass ? e->block_bytes : 0, 0};
+        e->err = a.take<int32_t>(4);
+        e->seg_bits = a.take<uint32_t>(idx);
+        e->iota = a.take<int32_t>(idx);
+        e->even = a.take<int32_t>(S);
+        e->odd = a.take<int32_t>(S);
+        e->src_ids = a.take<int32_t>(P);
+        e->emb_src = a.take<float>(P * E);
+        e->q_emb_src = a.take<int8_t>(P * E);
+        e->sc_pos = a.take<float>(P);
+        e->gx_enc = a.take<float>(P * 6 * H);
+        e->h2 = a.take<float>(2 * S * H);
+        e->q_h2 = a.take<int8_t>(2 * S * H);
+        e->sc_h2 = a.take<float>(2 * S);
+        e->gh2 = a.take<float>(4 * S * H);
+        e->z2 = a.take<float>(2 * S * H);
+        e->rh2 = a.take<float>(2 * S * H);
+        e->q_rh2 = a.take<int8_t>(2 * S * H);
+        e->sc_rh2 = a.take<float>(2 * S);
+        e->ghc2 = a.take<float>(2 * S * H);
+        e->enc_rows = a.take<int32_t>(L * 2 * S);
+        e->enc_out_rows = a.take<int32_t>(L * 2 * S);
+        e->q_states = a.take<int8_t>(P * 2 * H);
+        e->sc_sent = a.take<float>(S);
+        e->pos_sent = a.take<int32_t>(P);
+        e->s0tmp = a.take<float>(S * H);
+        e->s0_dst = a.take<int32_t>(S);
+        e->enc_states = a.take<float>(P * 2 * H);
+        e->enc_att = a.take<float>(P * A);
+        e->enc_s0 = a.take<float>(S * H);
+        e->sent_row = a.take<int64_t>(S);
+        e->sent_len = a.take<int32_t>(S);
+        e->emb = a.take<float>(N * E);
+        e->q_emb = a.take<int8_t>(N * E);
+        e->sc_emb = a.take<float>(S);
+        e->q_s = a.take<int8_t>(N * H);
+        e->sc_s = a.take<float>(S);
+        e->gx = a.take<float>(N * 3 * H);
+        e->gh = a.take<float>(N * 2 * H);
+        e->z = a.take<float>(N * H);
+        e->rh = a.take<float>(N * H);
+        e->q_rh = a.take<int8_t>(N * H);
+        e->sc_rh = a.take<float>(S);
+        e->ghc = a.take<float>(N * H);
+        e->q_q = a.take<int8_t>(N * H);
+        e->sc_q = a.take<float>(S);
+        e->u = a.take<float>(N * A);
+        e->ctx = a.take<float>(N * 2 * H);
+        e->q_ctx = a.take<int8_t>(N * 2 * H);
+        e->sc_ctx = a.take<float>(S);
+        e->q_si = a.take<int8_t>(N * H);
+        e->sc_si = a.take<float>(S);
+        e->q_sn = a.take<int8_t>(N * H);
+        e->sc_sn = a.take<float>(S);
+        e->ro = a.take<float>(N * R);
+        e->q_ro = a.take<int8_t>(N * R);
+        e->sc_ro = a.take<float>(S);
+        e->logits = a.take<float>(N * V);
+        e->att_scratch = a.take<char>(N * (L + 2) * 4 + 64);
+        for (int i = 0; i < 2; ++i) {
+            e->st_s[i] = a.take<float>(N * H);
+            e->st_sp[i] = a.take<float>(N * H);
+            e->y[i] = a.take<int32_t>(N);
+            e->col_sent[i] = a.take<int32_t>(N);
+            e->live[i] = a.take<double>(N);
+        }
+        e->s_int = a.take<float>(N * H);
+        e->s_new = a.take<float>(N * H);
+        e->parent_col = a.take<int32_t>(N);
+        e->cand_score = a.take<double>(N * B);
+        e->cand_tok = a.take<int32_t>(N * B);
+        e->n_live = a.take<int32_t>(4);
+        e->P = a.take<int32_t>(S);
+        e->col_off = a.take<int32_t>(S);
+        e->done = a.take<int32_t>(S);
+        e->max_steps = a.take<int32_t>(S);
+        e->steps_run = a.take<int32_t>(S);
+        e->fin_cnt = a.take<int32_t>(S);
+        e->fin_best = a.take<double>(S);
+        if (pass == 0) {
+            bytes = a.used;
+            e->block_bytes = bytes;
+            cudaError_t ce = cudaMalloc(&e->block, bytes);
+            if (ce != cudaSuccess) { delete e; return cuda_status(ce, "engine cudaMalloc"); }
+        }
+    }
+    std::vector<int32_t> io(idx), ev(S), od(S);
+    for (size_t i = 0; i < idx; ++i) io[i] = (int32_t)i;
+    for (size_t i = 0; i < S; ++i) { ev[i] = (int32_t)(2 * i); od[i] = (int32_t)(2 * i + 1); }
+    cudaMemcpy(e->iota, io.data(), idx * 4, cudaMemcpyHostToDevice);
+    cudaMemcpy(e->even, ev.data(), S * 4, cudaMemcpyHostToDevice);
+    cudaMemcpy(e->odd, od.data(), S * 4, cudaMemcpyHostToDevice);
+    cudaMemset(e->err, 0, 16);
+    cudaError_t ce = cudaMallocHost(&e->h_pinned, 64);
+    if (ce != cudaSuccess) { cudaFree(e->block); delete e; return cuda_status(ce, "cudaMallocHost"); }
+    *out = e;
+    return QNMT_OK;
+}
+
+int qnmt_engine_destroy(qnmt_engine* e) {
+    if (!e) return QNMT_OK;
+    cudaDeviceSynchronize();
+    if (e->block) cudaFree(e->block);
+    if (e->hblock) cudaFree(e->hblock);
+    if (e->h_pinned) cudaFreeHost(e->h_pinned);
+    delete e;
+    return QNMT_OK;
+}
+
+size_t qnmt_engine_bytes(const qnmt_engine* e) { return e ? e->block_bytes + e->hblock_bytes : 0; }
+
+int qnmt_encode_batch(qnmt_engine* e, const int32_t* src_ids_dev, const int32_t* src_len, int32_t n,
+                      float* states, float* att_proj, float* s0, void* stream) {
+    cudaStream_t st = as_stream(stream);
+    if (n < 1) { set_error("no sentences"); return QNMT_ERR_EMPTY; }
+    std::vector<int64_t> row(n);
+    int64_t acc = 0;
+    for (int i = 0; i < n; ++i) { row[i] = acc; acc += src_len[i]; }
+    QNMT_CUDA(cudaMemsetAsync(e->err, 0, 4, st));
+    TRY(encode_core(e, src_ids_dev, src_len, row.data(), n, states, att_proj, s0, st));
+    return check_flag(e, st);
+}
+
+int qnmt_decoder_step(qnmt_engine* e, int64_t N, const int32_t* col_sent, int32_t n_sent,
+                      const int32_t* y, const float* s, const float* sp, const float* states,
+                      const float* att_proj, const int64_t* sent_row, const int32_t* sent_len,
+                      int32_t max_len, float* s_int, float* s_new, float* logits, float* alpha,
+                      int64_t lda, void* stream) {
+    cudaStream_t st = as_stream(stream);
+    if (N > e->NMAX || n_sent > e->S || max_len > e->L) { set_error("step exceeds engine capacity"); return QNMT_ERR_CONFIG; }
+    QNMT_CUDA(cudaMemsetAsync(e->err, 0, 4, st));
+    StepIO io{N, n_sent, col_sent, y, s, sp, states, att_proj, sent_row, sent_len, max_len,
+              s_int, s_new, logits, alpha, lda};
+    TRY(step_core(e, io, st));
+    return check_flag(e, st);
+}
+
+// device-resident decode of one batch; results stay in the engine until finalize.
+static int decode_core(qnmt_engine* e, const int32_t* src_ids, bool ids_on_device, const int32_t* src_len,
+                       int32_t n, int32_t beam, double max_ratio, cudaStream_t st) {
+    const qnmt_model* m = e->m;
+    const int64_t H = m->H, V = m->Vt;
+    if (n < 1) { set_error("no sentences"); return QNMT_ERR_EMPTY; }
+    if (beam < 1 || beam > e->B || !(max_ratio > 0)) { set_error("bad beam/max_ratio"); return QNMT_ERR_CONFIG; }
+    if (n > e->S) { set_error("batch of %d exceeds engine capacity %d", n, e->S); return QNMT_ERR_CONFIG; }
+    std::vector<int64_t> row(n);
+    std::vector<int32_t> msteps(n);
+    int64_t P = 0;
+    int Lmax = 0, Tmax = 0;
+    for (int i = 0; i < n; ++i) {
+        if (src_len[i] < 1) { set_error("cannot translate an empty sentence"); return QNMT_ERR_EMPTY; }
+        row[i] = P;
+        P += src_len[i];
+        Lmax = std::max(Lmax, src_len[i]);
+        msteps[i] = (int32_t)ceil(max_ratio * (double)src_len[i]) + 1;   // decoder.py:103
+        Tmax = std::max(Tmax, msteps[i]);
+    }
+    if (!ids_on_device)
+        for (int64_t i = 0; i < P; ++i)
+            if (src_ids[i] < 0 || src_ids[i] >= m->Vs) { set_error("source id outside [0, %d)", m->Vs); return QNMT_ERR_VOCAB; }
+    TRY(grow_history(e, Tmax));
+    e->last_n = n;
+    e->last_tmax = Tmax;
+    QNMT_CUDA(cudaMemsetAsync(e->err, 0, 4, st));
+    QNMT_CUDA(cudaMemcpyAsync(e->src_ids, src_ids, (size_t)P * 4,
+                              ids_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
+    TRY(encode_core(e, e->src_ids, src_len, row.data(), n, e->enc_states, e->enc_att, e->enc_s0, st));
+    // decoder init: one column per sentence, s = s' = s0, y = EOS (BOS), live score 0 (decoder.py:105-110)
+    std::vector<int32_t> iota_n(n), y0(n, 2), ones(n, 1);
+    std::iota(iota_n.begin(), iota_n.end(), 0);
+    std::vector<double> dz(n, 0.0);
+    QNMT_CUDA(cudaMemcpyAsync(e->sent_row, row.data(), (size_t)n * 8, cudaMemcpyHostToDevice, st));
+    QNMT_CUDA(cudaMemcpyAsync(e->sent_len, src_len, (size_t)n * 4, cudaMemcpyHostToDevice, st));
+    QNMT_CUDA(cudaMemcpyAsync(e->max_steps, msteps.data(), (size_t)n * 4, cudaMemcpyHostToDevice, st));
+    QNMT_CUDA(cudaMemcpyAsync(e->P, ones.data(), (size_t)n * 4, cudaMemcpyHostToDevice, st));
+    QNMT_CUDA(cudaMemcpyAsync(e->col_off, iota_n.data(), (size_t)n * 4, cudaMemcpyHostToDevice, st));
+    QNMT_CUDA(cudaMemcpyAsync(e->col_sent[0], iota_n.data(), (size_t)n * 4, cudaMemcpyHostToDevice, st));
+    QNMT_CUDA(cudaMemcpyAsync(e->y[0], y0.data(), (size_t)n * 4, cudaMemcpyHostToDevice, st));
+    QNMT_CUDA(cudaMemcpyAsync(e->live[0], dz.data(), (size_t)n * 8, cudaMemcpyHostToDevice, st));
+    QNMT_CUDA(cudaMemsetAsync(e->done, 0, (size_t)n * 4, st));
+    QNMT_CUDA(cudaMemsetAsync(e->fin_cnt, 0, (size_t)n * 4, st));
+    QNMT_CUDA(cudaMemsetAsync(e->steps_run, 0, (size_t)n * 4, st));
+    QNMT_CUDA(cudaMemcpyAsync(e->st_s[0], e->enc_s0, (size_t)n * H * 4, cudaMemcpyDeviceToDevice, st));
+    QNMT_CUDA(cudaMemcpyAsync(e->st_sp[0], e->enc_s0, (size_t)n * H * 4, cudaMemcpyDeviceToDevice, st));
+    const int k_list = (int)std::min<int64_t>(beam, V);
+    int64_t N = n;
+    int cur = 0;
+    for (int t = 0; t < Tmax && N > 0; ++t) {
+        StepIO io{N, n, e->col_sent[cur], e->y[cur], e->st_s[cur], e->st_sp[cur], e->enc_states,
+                  e->enc_att, e->sent_row, e->sent_len, Lmax, e->s_int, e->s_new, e->logits, nullptr, 0};
+        TRY(step_core(e, io, st));
+        TRY(topk_launch(e->logits, N, V, V, e->live[cur], k_list, e->cand_score, e->cand_tok, e->err, st));
+        SearchState ss{e->P, e->col_off, e->done, e->max_steps, e->steps_run, e->fin_cnt, e->fin_best,
+                       e->fin_score, e->fin_step, e->fin_slot, e->fin_eos, e->hist_tok, e->hist_par,
+                       (e->hist_steps + 1) * e->B, e->hist_steps, e->B,
+                       e->cand_score, e->cand_tok,
+                       e->col_sent[cur ^ 1], e->parent_col, e->y[cur ^ 1], e->live[cur ^ 1], e->n_live};
+        TRY(search_step_launch(ss, t, n, beam, k_list, st));
+        QNMT_CUDA(cudaMemcpyAsync(e->h_pinned, e->n_live, 4, cudaMemcpyDeviceToHost, st));
+        QNMT_CUDA(cudaStreamSynchronize(st));
+        int64_t N2 = e->h_pinned[0];
+        TRY(gather_rows_launch(e->s_new, e->s_int, e->parent_col, N2, H, e->st_s[cur ^ 1], e->st_sp[cur ^ 1], st));
+        N = N2;
+        cur ^= 1;
+    }
+    return check_flag(e, st);
+}
+
+// D2H of the finished lists + history, then min by (-logp, tokens) (decoder.py:157-160)
+static int finalize(qnmt_engine* e, int32_t* out_tokens, int32_t out_stride, int32_t* out_len,
+                    double* out_logp, cudaStream_t st) {
+    const int n = e->last_n;
+    if (out_stride < e->last_tmax) { set_error("out_stride %d < max steps %d", out_stride, e->last_tmax); return QNMT_ERR_CONFIG; }
+    const int B = e->B, T = e->hist_steps, FC = (T + 1) * B;
+    std::vector<int32_t> fin_cnt(n), hist_tok((size_t)n * T * B), hist_par((size_t)n * T * B);
+    std::vector<double> fin_score((size_t)n * FC);
+    std::vector<int32_t> fin_step((size_t)n * FC), fin_slot((size_t)n * FC), fin_eos((size_t)n * FC);
+    QNMT_CUDA(cudaMemcpyAsync(fin_cnt.data(), e->fin_cnt, (size_t)n * 4, cudaMemcpyDeviceToHost, st));
+    QNMT_CUDA(cudaMemcpyAsync(fin_score.data(), e->fin_score, fin_score.size() * 8, cudaMemcpyDeviceToHost, st));
+    QNMT_CUDA(cudaMemcpyAsync(fin_step.data(), e->fin_step, fin_step.size() * 4, cudaMemcpyDeviceToHost, st));
+    QNMT_CUDA(cudaMemcpyAsync(fin_slot.data(), e->fin_slot, fin_slot.size() * 4, cudaMemcpyDeviceToHost, st));
+    QNMT_CUDA(cudaMemcpyAsync(fin_eos.data(), e->fin_eos, fin_eos.size() * 4, cudaMemcpyDeviceToHost, st));
+    QNMT_CUDA(cudaMemcpyAsync(hist_tok.data(), e->hist_tok, hist_tok.size() * 4, cudaMemcpyDeviceToHost, st));
+    QNMT_CUDA(cudaMemcpyAsync(hist_par.data(), e->hist_par, hist_par.size() * 4, cudaMemcpyDeviceToHost, st));
+    QNMT_CUDA(cudaStreamSynchronize(st));
+    e->d2h_bytes = (int64_t)(fin_cnt.size() + hist_tok.size() + hist_par.size() + fin_step.size() +
+                             fin_slot.size() + fin_eos.size()) * 4 + (int64_t)fin_score.size() * 8;
+    for (int s = 0; s < n; ++s) {
+        auto backtrack = [&](int t, int j, std::vector<int32_t>& out) {
+            out.clear();
+            for (int tt = t; tt >= 0; --tt) {
+                size_t h = ((size_t)s * T + tt) * B + j;
+                out.push_back(hist_tok[h]);
+                j = hist_par[h];
+            }
+            std::reverse(out.begin(), out.end());
+        };
+        std::vector<int32_t> best, cand;
+        double best_s = 0;
+        bool have = false;
+        for (int f = 0; f < fin_cnt[s]; ++f) {
+            size_t fb = (size_t)s * FC + f;
+            if (fin_eos[fb]) {
+                backtrack(fin_step[fb] - 1, fin_slot[fb], cand);
+                cand.push_back(2);
+            } else {
+                backtrack(fin_step[fb], fin_slot[fb], cand);
+            }
+            double sc = fin_score[fb];
+            if (!have || sc > best_s || (sc == best_s && cand < best)) {
+                best = cand;
+                best_s = sc;
+                have = true;
+            }
+        }
+        if (!best.empty() && best.back() == 2) best.pop_back();
+        out_len[s] = (int32_t)best.size();
+        out_logp[s] = best_s;
+        for (size_t i = 0; i < best.size(); ++i) out_tokens[(size_t)s * out_stride + i] = best[i];
+    }
+    return QNMT_OK;
+}
+
+int qnmt_translate_batch(qnmt_engine* e, const int32_t* src_ids, const int32_t* src_len, int32_t n,
+                         int32_t beam, double max_ratio, int32_t* out_tokens, int32_t out_stride,
+                         int32_t* out_len, double* out_logp, void* stream) {
+    cudaStream_t st = as_stream(stream);
+    TRY(decode_core(e, src_ids, false, src_len, n, beam, max_ratio, st));
+    return finalize(e, out_tokens, out_stride, out_len, out_logp, st);
+}
+
+int qnmt_decode_batch_device(qnmt_engine* e, const int32_t* src_ids_dev, const int32_t* src_len,
+                             int32_t n, int32_t beam, double max_ratio, void* stream) {
+    return decode_core(e, src_ids_dev, true, src_len, n, beam, max_ratio, as_stream(stream));
+}
+
+int qnmt_fetch_results(qnmt_engine* e, int32_t* out_tokens, int32_t out_stride, int32_t* out_len,
+                       double* out_logp, void* stream) {
+    return finalize(e, out_tokens, out_stride, out_len, out_logp, as_stream(stream));
+}
+
+int64_t qnmt_last_d2h_bytes(const qnmt_engine* e) { return e ? e->d2h_bytes : 0; }
+
+}  // extern "C"

@@ -1,0 +1,29 @@
+// gemm.cuh -- internal GEMM entry shared by the ABI wrapper and the engine.
+#pragma once
+#include "common.cuh"
+
+namespace qnmt {
+
+struct GemmArgs {
+    const int8_t* W;
+    int64_t M, K, ldw;
+    const float* w_scales;
+    int64_t w_rows_per_scale;
+    const int8_t* X;
+    int64_t N, ldx;
+    const float* x_scales;
+    const int32_t* col_seg;
+    const float* bias;
+    float* Y;
+    int64_t ldy;
+    int64_t* acc_out;
+    int32_t flags;
+};
+
+int gemm_i8_launch(const GemmArgs& g, cudaStream_t st);
+
+int quantize_launch(const float* x, int64_t ncols, int64_t K, int64_t ldx, const int32_t* col_seg,
+                    int32_t nseg, int8_t* q, int64_t ldq, float* scales, uint32_t* seg_maxbits,
+                    int32_t mode, int32_t* err_flag, cudaStream_t st);
+
+}  // namespace qnmt

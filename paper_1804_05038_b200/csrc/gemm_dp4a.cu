@@ -1,0 +1,264 @@
+// gemm_dp4a.cu -- int8 x int8 -> int32 products on CUDA cores with the fused
+// dequant / bias / accumulate epilogue.
+//
+// Replaces qmath.py:400-427 (qgemm_panel), :302-328 (_panel_vnni), :243-299
+// (_vnni_dot64), :331-360 (_panel_maddw), :205-228 (naive kernels), and the
+// epilogue of :379-381 + layers.py:144-145.
+//
+//   k_gemv<ROWS, NC>  : N <= 8 columns (beam-sized panels, batch-1 latency path).
+//                       Each warp streams ROWS weight rows with 16-byte
+//                       L1-bypassing loads (every weight byte read once), the
+//                       NC activation columns come through the read-only path
+//                       (L1 hits shared by all warps), dp4a, warp butterfly sum.
+//   k_gemm_tile       : N > 8, 64x64x64 smem-tiled dp4a (interim bulk path;
+//                       the tcgen05 kernel in gemm_tcgen05.cu supersedes it
+//                       where it applies).
+//   k_gemm_generic    : any alignment, int64 accumulation for K > INT32_SAFE_K.
+#include "common.cuh"
+#include "gemm.cuh"
+
+namespace qnmt {
+
+struct EpiArgs {
+    const float* w_scales;
+    int64_t w_rows_per_scale;
+    const float* x_scales;
+    const int32_t* col_seg;
+    const float* bias;
+    float* Y;
+    int64_t ldy;
+    int64_t* acc_out;
+    int64_t M;
+    int32_t flags;
+};
+
+__device__ __forceinline__ void epilogue(const EpiArgs& e, int64_t m, int64_t n, long long acc) {
+    if (e.acc_out) e.acc_out[n * e.M + m] = acc;
+    if (!e.Y) return;
+    float sw = e.w_scales[m / e.w_rows_per_scale];
+    float sx = e.x_scales[e.col_seg ? e.col_seg[n] : 0];
+    float y = dequant(acc, sw, sx);
+    if (e.bias) y = __fadd_rn(y, e.bias[m]);
+    float* dst = e.Y + n * e.ldy + m;
+    if (e.flags & QNMT_GEMM_ACCUMULATE) y = __fadd_rn(*dst, y);
+    *dst = y;
+}
+
+__device__ __forceinline__ int dp4a16(int acc, const int4& a, const int4& b) {
+    acc = __dp4a(a.x, b.x, acc);
+    acc = __dp4a(a.y, b.y, acc);
+    acc = __dp4a(a.z, b.z, acc);
+    acc = __dp4a(a.w, b.w, acc);
+    return acc;
+}
+
+// ---------------------------------------------------------------------------
+// GEMV-class kernel: N <= 8
+// ---------------------------------------------------------------------------
+template <int ROWS, int NC>
+__global__ void __launch_bounds__(256)
+k_gemv(const int8_t* __restrict__ W, int64_t M, int64_t K, int64_t ldw,
+       const int8_t* __restrict__ X, int64_t ldx, EpiArgs e) {
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    const int64_t row0 = ((int64_t)blockIdx.x * 8 + warp) * ROWS;
+    if (row0 >= M) return;
+    const int64_t nch = K >> 4;   // 16-byte chunks per row
+    int acc[ROWS][NC];
+#pragma unroll
+    for (int r = 0; r < ROWS; ++r)
+#pragma unroll
+        for (int j = 0; j < NC; ++j) acc[r][j] = 0;
+
+    constexpr int U = 2;   // chunk-iterations whose loads are issued together
+    for (int64_t c0 = lane; c0 < nch; c0 += 32 * U) {
+        int4 w[U][ROWS];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            int64_t c = c0 + 32 * u;
+#pragma unroll
+            for (int r = 0; r < ROWS; ++r) {
+                if (c < nch && row0 + r < M)
+                    w[u][r] = ld_stream16(W + (row0 + r) * ldw + (c << 4));
+                else
+                    w[u][r] = make_int4(0, 0, 0, 0);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            int64_t c = c0 + 32 * u;
+            if (c < nch) {
+#pragma unroll
+                for (int j = 0; j < NC; ++j) {
+                    int4 xv = __ldg(reinterpret_cast<const int4*>(X + j * ldx + (c << 4)));
+#pragma unroll
+                    for (int r = 0; r < ROWS; ++r) acc[r][j] = dp4a16(acc[r][j], w[u][r], xv);
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int r = 0; r < ROWS; ++r)
+#pragma unroll
+        for (int j = 0; j < NC; ++j) acc[r][j] = warp_sum(acc[r][j]);
+#pragma unroll
+    for (int t = 0; t < ROWS * NC; ++t) {
+        if ((t & 31) == lane) {
+            int r = t / NC, j = t % NC;
+            if (row0 + r < M) epilogue(e, row0 + r, j, (long long)acc[r][j]);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Tiled dp4a GEMM: 64(M) x 64(N) x 64(K) tiles, 256 threads, 4x4 per thread
+// ---------------------------------------------------------------------------
+constexpr int TBM = 64, TBN = 64, TBK = 64;
+constexpr int TSTR = 17;   // smem row stride in 32-bit words (conflict-free reads)
+
+__global__ void __launch_bounds__(256)
+k_gemm_tile(const int8_t* __restrict__ W, int64_t M, int64_t K, int64_t ldw,
+            const int8_t* __restrict__ X, int64_t N, int64_t ldx, EpiArgs e) {
+    __shared__ int sA[TBM * TSTR];
+    __shared__ int sB[TBN * TSTR];
+    const int tid = threadIdx.x;
+    const int tx = tid & 15;   // M direction
+    const int ty = tid >> 4;   // N direction
+    const int64_t m0 = (int64_t)blockIdx.x * TBM;
+    const int64_t n0 = (int64_t)blockIdx.y * TBN;
+    int acc[4][4] = {};
+    // loader mapping: 256 threads x 16 bytes = 64 rows x 64 bytes
+    const int lrow = tid >> 2, lcol = (tid & 3) * 4;   // lcol in words
+    for (int64_t k0 = 0; k0 < K; k0 += TBK) {
+        int4 a = make_int4(0, 0, 0, 0), b = make_int4(0, 0, 0, 0);
+        if (m0 + lrow < M) a = ld_stream16(W + (m0 + lrow) * ldw + k0 + lcol * 4);
+        if (n0 + lrow < N) b = __ldg(reinterpret_cast<const int4*>(X + (n0 + lrow) * ldx + k0 + lcol * 4));
+        __syncthreads();
+        int* pa = sA + lrow * TSTR + lcol;
+        pa[0] = a.x; pa[1] = a.y; pa[2] = a.z; pa[3] = a.w;
+        int* pb = sB + lrow * TSTR + lcol;
+        pb[0] = b.x; pb[1] = b.y; pb[2] = b.z; pb[3] = b.w;
+        __syncthreads();
+#pragma unroll
+        for (int w = 0; w < TBK / 4; ++w) {
+            int av[4], bv[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) av[i] = sA[(tx + 16 * i) * TSTR + w];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) bv[j] = sB[(ty + 16 * j) * TSTR + w];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) acc[i][j] = __dp4a(av[i], bv[j], acc[i][j]);
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        int64_t n = n0 + ty + 16 * j;
+        if (n >= N) continue;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            int64_t m = m0 + tx + 16 * i;
+            if (m < M) epilogue(e, m, n, (long long)acc[i][j]);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Generic: one block per output element, int64 partial sums.
+// ---------------------------------------------------------------------------
+__global__ void k_gemm_generic(const int8_t* __restrict__ W, int64_t M, int64_t K, int64_t ldw,
+                               const int8_t* __restrict__ X, int64_t N, int64_t ldx, EpiArgs e) {
+    int64_t idx = blockIdx.x;
+    int64_t m = idx % M, n = idx / M;
+    const int8_t* a = W + m * ldw;
+    const int8_t* b = X + n * ldx;
+    long long s = 0;
+    for (int64_t k = threadIdx.x; k < K; k += blockDim.x) s += (int)a[k] * (int)b[k];
+    s = warp_sum(s);
+    __shared__ long long part[32];
+    if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        long long t = 0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += part[w];
+        epilogue(e, m, n, t);
+    }
+}
+
+template <int ROWS, int NC>
+static void launch_gemv(const int8_t* W, int64_t M, int64_t K, int64_t ldw, const int8_t* X,
+                        int64_t ldx, const EpiArgs& e, cudaStream_t st) {
+    unsigned grid = (unsigned)cdiv(M, 8 * ROWS);
+    k_gemv<ROWS, NC><<<grid, 256, 0, st>>>(W, M, K, ldw, X, ldx, e);
+}
+
+template <int ROWS>
+static void dispatch_gemv(int64_t N, const int8_t* W, int64_t M, int64_t K, int64_t ldw,
+                          const int8_t* X, int64_t ldx, const EpiArgs& e, cudaStream_t st) {
+    switch (N) {
+        case 1: launch_gemv<ROWS, 1>(W, M, K, ldw, X, ldx, e, st); break;
+        case 2: launch_gemv<ROWS, 2>(W, M, K, ldw, X, ldx, e, st); break;
+        case 3: launch_gemv<ROWS, 3>(W, M, K, ldw, X, ldx, e, st); break;
+        case 4: launch_gemv<ROWS, 4>(W, M, K, ldw, X, ldx, e, st); break;
+        case 5: launch_gemv<ROWS, 5>(W, M, K, ldw, X, ldx, e, st); break;
+        case 6: launch_gemv<ROWS, 6>(W, M, K, ldw, X, ldx, e, st); break;
+        case 7: launch_gemv<ROWS, 7>(W, M, K, ldw, X, ldx, e, st); break;
+        default: launch_gemv<ROWS, 8>(W, M, K, ldw, X, ldx, e, st); break;
+    }
+}
+
+int gemm_i8_launch(const GemmArgs& g, cudaStream_t st) {
+    if (g.M <= 0 || g.N <= 0) return QNMT_OK;
+    EpiArgs e{g.w_scales, g.w_rows_per_scale, g.x_scales, g.col_seg, g.bias, g.Y, g.ldy,
+              g.acc_out, g.M, g.flags};
+    bool aligned = (g.K % 16 == 0) && (g.ldw % 16 == 0) && (g.ldx % 16 == 0) &&
+                   ((uintptr_t)g.W % 16 == 0) && ((uintptr_t)g.X % 16 == 0);
+    if (g.K > QNMT_INT32_SAFE_K || !aligned || g.K == 0) {
+        k_gemm_generic<<<(unsigned)(g.M * g.N), 128, 0, st>>>(g.W, g.M, g.K, g.ldw, g.X, g.N, g.ldx, e);
+        QNMT_CHECK_LAUNCH("k_gemm_generic");
+        return QNMT_OK;
+    }
+    if (g.N <= 8) {
+        if (g.K <= 512)
+            dispatch_gemv<4>(g.N, g.W, g.M, g.K, g.ldw, g.X, g.ldx, e, st);
+        else
+            dispatch_gemv<2>(g.N, g.W, g.M, g.K, g.ldw, g.X, g.ldx, e, st);
+        QNMT_CHECK_LAUNCH("k_gemv");
+        return QNMT_OK;
+    }
+    if (g.K % TBK == 0) {
+        dim3 grid((unsigned)cdiv(g.M, TBM), (unsigned)cdiv(g.N, TBN));
+        k_gemm_tile<<<grid, 256, 0, st>>>(g.W, g.M, g.K, g.ldw, g.X, g.N, g.ldx, e);
+        QNMT_CHECK_LAUNCH("k_gemm_tile");
+        return QNMT_OK;
+    }
+    // K multiple of 16 but not of 64: process N in panels of 8 with the GEMV kernel
+    for (int64_t n0 = 0; n0 < g.N; n0 += 8) {
+        EpiArgs e2 = e;
+        int64_t nn = g.N - n0 < 8 ? g.N - n0 : 8;
+        if (e2.Y) e2.Y += n0 * g.ldy;
+        if (e2.acc_out) e2.acc_out += n0 * g.M;
+        if (e2.col_seg) e2.col_seg += n0;
+        dispatch_gemv<2>(nn, g.W, g.M, g.K, g.ldw, g.X + n0 * g.ldx, g.ldx, e2, st);
+        QNMT_CHECK_LAUNCH("k_gemv(panel)");
+    }
+    return QNMT_OK;
+}
+
+}  // namespace qnmt
+
+extern "C" int qnmt_gemm_i8(const int8_t* W, int64_t M, int64_t K, int64_t ldw,
+                            const float* w_scales, int64_t w_rows_per_scale, const int8_t* X,
+                            int64_t N, int64_t ldx, const float* x_scales, const int32_t* col_seg,
+                            const float* bias, float* Y, int64_t ldy, int64_t* acc_out,
+                            int32_t flags, void* stream) {
+    if (M < 0 || N < 0 || K < 0 || ldw < K || ldx < K || (Y && ldy < M) || w_rows_per_scale < 1) {
+        qnmt::set_error("qnmt_gemm_i8: bad shape M=%lld N=%lld K=%lld", (long long)M,
+                        (long long)N, (long long)K);
+        return QNMT_ERR_SHAPE;
+    }
+    qnmt::GemmArgs g{W, M, K, ldw, w_scales, w_rows_per_scale, X, N, ldx, x_scales, col_seg,
+                     bias, Y, ldy, acc_out, flags};
+    return qnmt::gemm_i8_launch(g, qnmt::as_stream(stream));
+}

@@ -1,0 +1,167 @@
+// search.cu -- device-resident beam bookkeeping for a batch of sentences.
+//
+// One thread per sentence executes one iteration of decoder.py:112-155:
+//   chosen  = top-`beam` of the parent-major candidates under
+//             (score desc, token asc, parent asc)            (_select_candidates :74-85)
+//   EOS candidates -> finished list; others -> next live set  (:127-141)
+//   no live candidate -> stop                                 (:143-144)
+//   best finished >= best live -> stop (survivors dropped)    (:150-151)
+//   last allowed step -> survivors frozen into finished       (:152-155, for-else)
+// Per-column inputs come from output.cu's per-parent candidate lists (each
+// sorted by (score desc, token asc)); a P-way merge over them is exact.
+// History (token, parent slot) per step lets the host rebuild token lists for
+// the final min-by-(-logp, tokens) selection (:157).
+#include <float.h>
+
+#include "common.cuh"
+#include "search.cuh"
+
+namespace qnmt {
+
+constexpr int SEARCH_T = 1024;
+constexpr int EOS = 2;   // model.py:33
+
+__device__ __forceinline__ bool cand_better(double sa, int ta, int pa, double sb, int tb, int pb) {
+    if (sa != sb) return sa > sb;
+    if (ta != tb) return ta < tb;
+    return pa < pb;
+}
+
+__global__ void __launch_bounds__(SEARCH_T)
+k_search_step(SearchState ss, int step, int n_sent, int beam, int k_list) {
+    __shared__ int s_cnt[SEARCH_T];
+    const int tid = threadIdx.x;
+    int new_p = 0;
+    // per-thread selection results
+    int sel_tok[16], sel_par[16];
+    double sel_sc[16];
+    int nsel = 0;
+    const int s = tid;
+    if (s < n_sent && !ss.done[s]) {
+        const int P = ss.P[s];
+        const int off = ss.col_off[s];
+        int ptr[16];
+        for (int p = 0; p < P; ++p) ptr[p] = 0;
+        for (int r = 0; r < beam; ++r) {
+            int bp = -1;
+            double bs = 0.0;
+            int bt = 0;
+            for (int p = 0; p < P; ++p) {
+                if (ptr[p] >= k_list) continue;
+                int64_t idx = (int64_t)(off + p) * k_list + ptr[p];
+                double cs = ss.cand_score[idx];
+                int ct = ss.cand_tok[idx];
+                if (bp < 0 || cand_better(cs, ct, p, bs, bt, bp)) {
+                    bp = p;
+                    bs = cs;
+                    bt = ct;
+                }
+            }
+            if (bp < 0) break;
+            ptr[bp]++;
+            sel_tok[nsel] = bt;
+            sel_par[nsel] = bp;
+            sel_sc[nsel] = bs;
+            nsel++;
+        }
+        // split into finished / live
+        double best_live = -DBL_MAX;
+        int64_t hbase = ((int64_t)s * ss.max_steps_cap + step) * ss.beam_cap;
+        for (int i = 0; i < nsel; ++i) {
+            if (sel_tok[i] == EOS) {
+                int f = ss.fin_cnt[s]++;
+                int64_t fb = (int64_t)s * ss.fin_cap + f;
+                ss.fin_score[fb] = sel_sc[i];
+                ss.fin_step[fb] = step;
+                ss.fin_slot[fb] = sel_par[i];
+                ss.fin_eos[fb] = 1;
+                if (f == 0 || sel_sc[i] > ss.fin_best[s]) ss.fin_best[s] = sel_sc[i];
+            } else {
+                ss.hist_tok[hbase + new_p] = sel_tok[i];
+                ss.hist_par[hbase + new_p] = sel_par[i];
+                if (sel_sc[i] > best_live) best_live = sel_sc[i];
+                sel_tok[new_p] = sel_tok[i];
+                sel_par[new_p] = sel_par[i];
+                sel_sc[new_p] = sel_sc[i];
+                new_p++;
+            }
+        }
+        bool stop = false;
+        if (new_p == 0) {
+            stop = true;                                   // :143-144
+        } else if (ss.fin_cnt[s] > 0 && ss.fin_best[s] >= best_live) {
+            stop = true;                                   // :150-151
+        } else if (step == ss.max_steps[s] - 1) {
+            for (int j = 0; j < new_p; ++j) {              // :152-155
+                int f = ss.fin_cnt[s]++;
+                int64_t fb = (int64_t)s * ss.fin_cap + f;
+                ss.fin_score[fb] = sel_sc[j];
+                ss.fin_step[fb] = step;
+                ss.fin_slot[fb] = j;
+                ss.fin_eos[fb] = 0;
+            }
+            stop = true;
+        }
+        ss.steps_run[s] = step + 1;
+        if (stop) {
+            ss.done[s] = 1;
+            new_p = 0;
+        }
+    }
+    // exclusive prefix sum of new_p over sentences
+    s_cnt[tid] = new_p;
+    __syncthreads();
+    for (int o = 1; o < SEARCH_T; o <<= 1) {
+        int v = tid >= o ? s_cnt[tid - o] : 0;
+        __syncthreads();
+        s_cnt[tid] += v;
+        __syncthreads();
+    }
+    int new_off = s_cnt[tid] - new_p;
+    if (tid == SEARCH_T - 1) *ss.n_live = s_cnt[tid];
+    if (s < n_sent) {
+        const int old_off = ss.col_off[s];
+        for (int j = 0; j < new_p; ++j) {
+            int n = new_off + j;
+            ss.col_sent_next[n] = s;
+            ss.parent_col[n] = old_off + sel_par[j];
+            ss.y_next[n] = sel_tok[j];
+            ss.live_next[n] = sel_sc[j];
+        }
+        ss.P[s] = new_p;
+        ss.col_off[s] = new_off;
+    }
+}
+
+// next-step state columns: dst[n] = src[parent_col[n]] for the state tensors
+__global__ void k_gather_rows(const float* __restrict__ a, const float* __restrict__ b,
+                              const int32_t* __restrict__ parent, int64_t H,
+                              float* __restrict__ a_out, float* __restrict__ b_out) {
+    int64_t n = blockIdx.x;
+    int64_t p = parent[n];
+    for (int64_t j = threadIdx.x; j < H; j += blockDim.x) {
+        a_out[n * H + j] = a[p * H + j];
+        if (b) b_out[n * H + j] = b[p * H + j];
+    }
+}
+
+int search_step_launch(const SearchState& ss, int step, int n_sent, int beam, int k_list,
+                       cudaStream_t st) {
+    if (n_sent > SEARCH_T || beam > 16) {
+        set_error("search: n_sent=%d beam=%d exceed limits (%d, 16)", n_sent, beam, SEARCH_T);
+        return QNMT_ERR_CONFIG;
+    }
+    k_search_step<<<1, SEARCH_T, 0, st>>>(ss, step, n_sent, beam, k_list);
+    QNMT_CHECK_LAUNCH("k_search_step");
+    return QNMT_OK;
+}
+
+int gather_rows_launch(const float* a, const float* b, const int32_t* parent, int64_t N, int64_t H,
+                       float* a_out, float* b_out, cudaStream_t st) {
+    if (N <= 0) return QNMT_OK;
+    k_gather_rows<<<(unsigned)N, 256, 0, st>>>(a, b, parent, H, a_out, b_out);
+    QNMT_CHECK_LAUNCH("k_gather_rows");
+    return QNMT_OK;
+}
+
+}  // namespace qnmt

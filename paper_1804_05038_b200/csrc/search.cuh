@@ -1,0 +1,39 @@
+// search.cuh -- device state of the batched beam search (search.cu).
+#pragma once
+#include "common.cuh"
+
+namespace qnmt {
+
+struct SearchState {
+    // per sentence
+    int32_t* P;            // live columns this step
+    int32_t* col_off;      // offset of the sentence's columns
+    int32_t* done;
+    int32_t* max_steps;    // ceil(max_ratio * l) + 1   (decoder.py:103)
+    int32_t* steps_run;
+    int32_t* fin_cnt;
+    double* fin_best;
+    double* fin_score;     // [S][fin_cap]
+    int32_t* fin_step;
+    int32_t* fin_slot;     // parent slot (EOS) or own slot (frozen survivor)
+    int32_t* fin_eos;
+    int32_t* hist_tok;     // [S][max_steps_cap][beam_cap]
+    int32_t* hist_par;
+    int32_t fin_cap, max_steps_cap, beam_cap;
+    // per column (current step)
+    const double* cand_score;   // [N][k_list]
+    const int32_t* cand_tok;
+    // per column (next step)
+    int32_t* col_sent_next;
+    int32_t* parent_col;
+    int32_t* y_next;
+    double* live_next;
+    int32_t* n_live;       // device scalar: columns of the next step
+};
+
+int search_step_launch(const SearchState& ss, int step, int n_sent, int beam, int k_list,
+                       cudaStream_t st);
+int gather_rows_launch(const float* a, const float* b, const int32_t* parent, int64_t N, int64_t H,
+                       float* a_out, float* b_out, cudaStream_t st);
+
+}  // namespace qnmt

@@ -1,0 +1,256 @@
+"""Parameter containers, synthetic models and on-device weight quantization.
+
+Mirrors the reference ``model.py``: :class:`Dims` (:42-52), the canonical
+tensor directory :func:`tensor_specs` (:151-177), :class:`ModelParams`
+(fp32), :class:`QuantizedModel` (int8 codes + one f32 scale per tensor,
+embeddings and biases fp32, :394-437) and the seeded generators.
+
+B200 layout: :func:`quantize_model` uploads the fp32 tensors once, quantizes
+every weight matrix with the device K1 kernel (bit-identical to the
+reference's ``quantize``), and additionally packs the per-gate GRU tensors
+into the stacked form the fused kernels consume (``WX = [wz; wr; wc]`` with
+three row-block scales, ``UZR = [uz; ur]`` with two, ``UC``).  The packed
+device tensors are referenced by the C engine handle (``qnmt_model_create``).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _dev, _lib
+from .errors import ParameterError
+from .qmath import QuantizedMatrix, quantization_stats, quantize
+
+PAD_ID, UNK_ID, EOS_ID = 0, 1, 2
+PAD_TOKEN, UNK_TOKEN, EOS_TOKEN = "<pad>", "<unk>", "</s>"
+DEFAULT_WEIGHT_SCALE = 0.08
+GRU_FIELDS = ("wz", "uz", "bz", "wr", "ur", "br", "wc", "uc", "bc")
+CELLS = ("enc_fwd", "enc_bwd", "dec_r", "dec_q")
+
+
+@dataclass
+class Dims:
+    src_vocab: int
+    tgt_vocab: int
+    embed: int
+    hidden: int
+    attn: int
+    readout: int
+
+    def as_dict(self) -> dict:
+        return dict(self.__dict__)
+
+
+def tensor_specs(dims: Dims) -> list:
+    """Canonical (name, shape) directory; defines serialization order (model.py:151-177)."""
+    specs = [("src_embed", (dims.src_vocab, dims.embed)), ("tgt_embed", (dims.tgt_vocab, dims.embed))]
+    h = dims.hidden
+    for cell, in_dim in (("enc_fwd", dims.embed), ("enc_bwd", dims.embed),
+                         ("dec_r", dims.embed), ("dec_q", 2 * h)):
+        shapes = {"wz": (h, in_dim), "uz": (h, h), "bz": (h,), "wr": (h, in_dim), "ur": (h, h),
+                  "br": (h,), "wc": (h, in_dim), "uc": (h, h), "bc": (h,)}
+        specs.extend((f"{cell}.{f}", shapes[f]) for f in GRU_FIELDS)
+    specs.extend([
+        ("attn.w_enc", (dims.attn, 2 * h)), ("attn.b_enc", (dims.attn,)),
+        ("attn.u_state", (dims.attn, h)), ("attn.v", (1, dims.attn)),
+        ("out.w_state", (dims.readout, h)), ("out.w_embed", (dims.readout, dims.embed)),
+        ("out.w_ctx", (dims.readout, 2 * h)), ("out.b_readout", (dims.readout,)),
+        ("out.w_vocab", (dims.tgt_vocab, dims.readout)), ("out.b_vocab", (dims.tgt_vocab,)),
+        ("s0.w", (h, h)), ("s0.b", (h,)),
+    ])
+    return specs
+
+
+def synthetic_vocab(size: int) -> list:
+    """model.py:230-231: reserved pad/unk/eos then w0001 ..."""
+    return [PAD_TOKEN, UNK_TOKEN, EOS_TOKEN] + [f"w{i:04d}" for i in range(1, size - 2)]
+
+
+@dataclass(eq=False)
+class ModelParams:
+    """All trained tensors in float32 (numpy, host), keyed by tensor_specs names."""
+
+    dims: Dims
+    tensors: dict
+    src_tokens: list
+    tgt_tokens: list
+    s0_mode: str = "transform"
+    attention_query: str = "current"
+    precision = "fp32"
+
+    def __post_init__(self):
+        self._src_index = None
+
+    def src_ids(self, tokens) -> np.ndarray:
+        """Map source tokens to ids; unknown tokens become UNK (model.py:110-115)."""
+        if self._src_index is None:
+            self._src_index = {t: i for i, t in enumerate(self.src_tokens)}
+        idx = self._src_index
+        return np.array([idx.get(t, UNK_ID) for t in tokens], dtype=np.int64)
+
+    def tgt_token(self, token_id: int) -> str:
+        return self.tgt_tokens[token_id]
+
+
+def _check_dims(dims: Dims):
+    for name, value in dims.as_dict().items():
+        if value < 1:
+            raise ParameterError(f"{name} must be >= 1, got {value}")
+    if dims.src_vocab < 3 or dims.tgt_vocab < 3:
+        raise ParameterError("vocabularies must cover the reserved pad/unk/eos ids")
+
+
+def synthetic_model(dims: Dims, seed: int, weight_std: float = 0.05, bias_std: float = 0.0,
+                    eos_bias: float = 0.0, s0_mode: str = "transform",
+                    attention_query: str = "current") -> ModelParams:
+    """BASELINE.json recipe: numpy default_rng(seed); every
+    2-D tensor ~ N(0, weight_std) cast to f32 in tensor_specs order; biases 0
+    (or N(0, bias_std) drawn after all weights); ``eos_bias`` added to
+    b_vocab[EOS] for test models that terminate early."""
+    _check_dims(dims)
+    rng = np.random.default_rng(seed)
+    t = {}
+    specs = tensor_specs(dims)
+    for name, shape in specs:
+        if len(shape) == 2:
+            t[name] = rng.normal(0.0, weight_std, shape).astype(np.float32)
+    for name, shape in specs:
+        if len(shape) == 1:
+            t[name] = (rng.normal(0.0, bias_std, shape).astype(np.float32) if bias_std > 0
+                       else np.zeros(shape, dtype=np.float32))
+    if eos_bias:
+        t["out.b_vocab"][EOS_ID] += np.float32(eos_bias)
+    return ModelParams(dims, t, synthetic_vocab(dims.src_vocab), synthetic_vocab(dims.tgt_vocab),
+                       s0_mode, attention_query)
+
+
+def generate_model(src_vocab: int, tgt_vocab: int, embed: int, hidden: int, seed: int,
+                   attn: int | None = None, readout: int | None = None,
+                   weight_scale: float = DEFAULT_WEIGHT_SCALE, s0_mode: str = "transform",
+                   attention_query: str = "current") -> ModelParams:
+    """model.py:234-269: PCG64(seed), uniform [-weight_scale, weight_scale) f32 in spec order."""
+    dims = Dims(src_vocab, tgt_vocab, embed, hidden, attn=attn or hidden, readout=readout or embed)
+    _check_dims(dims)
+    if not (0 < weight_scale < 16):
+        raise ParameterError(f"weight_scale out of range: {weight_scale}")
+    total = sum(int(np.prod(s)) for _, s in tensor_specs(dims))
+    if total > 2 ** 31:
+        raise ParameterError(f"model of {total} parameters exceeds the supported size")
+    rng = np.random.Generator(np.random.PCG64(seed))
+    ws = np.float32(weight_scale)
+    t = {}
+    for name, shape in tensor_specs(dims):
+        u = rng.random(shape, dtype=np.float32)
+        t[name] = (u * np.float32(2.0) - np.float32(1.0)) * ws
+    return ModelParams(dims, t, synthetic_vocab(src_vocab), synthetic_vocab(tgt_vocab), s0_mode,
+                       attention_query)
+
+
+@dataclass(eq=False)
+class QuantizedModel:
+    """Device-resident int8 model: ``q[name]`` QuantizedMatrix (device codes),
+    ``f[name]`` f32 device tensors (embeddings, biases), packed GRU stacks,
+    and the C model handle for the engine."""
+
+    dims: Dims
+    q: dict
+    f: dict
+    src_tokens: list
+    tgt_tokens: list
+    s0_mode: str = "transform"
+    attention_query: str = "current"
+    stats: dict = field(default_factory=dict)
+    precision = "int8"
+
+    def __post_init__(self):
+        self._src_index = None
+        self._handle = None
+        self._keep = []
+
+    src_ids = ModelParams.src_ids
+    tgt_token = ModelParams.tgt_token
+
+    # -- packed tensors for the engine --------------------------------------
+    def packed_cell(self, cell: str):
+        """(WX [3H,in] int8, WX scales [3], BX [3H], UZR [2H,H], UZR scales [2], UC, UC scale [1])."""
+        key = f"_packed_{cell}"
+        if not hasattr(self, key):
+            q, f = self.q, self.f
+            wx = torch.cat([q[f"{cell}.w{g}"].device_data() for g in "zrc"]).contiguous()
+            wxs = torch.cat([q[f"{cell}.w{g}"].device_scale() for g in "zrc"]).contiguous()
+            bx = torch.cat([f[f"{cell}.b{g}"] for g in "zrc"]).contiguous()
+            uzr = torch.cat([q[f"{cell}.u{g}"].device_data() for g in "zr"]).contiguous()
+            uzrs = torch.cat([q[f"{cell}.u{g}"].device_scale() for g in "zr"]).contiguous()
+            uc = q[f"{cell}.uc"].device_data()
+            ucs = q[f"{cell}.uc"].device_scale()
+            setattr(self, key, (wx, wxs, bx, uzr, uzrs, uc, ucs))
+        return getattr(self, key)
+
+    def handle(self):
+        """C ``qnmt_model*`` (created once; tensors kept alive by this object)."""
+        if self._handle is None:
+            ptrs = [0] * 50
+            keep = []
+
+            def put(i, t):
+                keep.append(t)
+                ptrs[i] = t.data_ptr()
+
+            put(0, self.f["src_embed"])
+            put(1, self.f["tgt_embed"])
+            for c, cell in enumerate(CELLS):
+                for j, t in enumerate(self.packed_cell(cell)):
+                    put(2 + 7 * c + j, t)
+            q, f = self.q, self.f
+            put(30, q["attn.w_enc"].device_data()); put(31, q["attn.w_enc"].device_scale())
+            put(32, f["attn.b_enc"])
+            put(33, q["attn.u_state"].device_data()); put(34, q["attn.u_state"].device_scale())
+            put(35, q["attn.v"].device_data()); put(36, q["attn.v"].device_scale())
+            put(37, q["out.w_state"].device_data()); put(38, q["out.w_state"].device_scale())
+            put(39, f["out.b_readout"])
+            put(40, q["out.w_embed"].device_data()); put(41, q["out.w_embed"].device_scale())
+            put(42, q["out.w_ctx"].device_data()); put(43, q["out.w_ctx"].device_scale())
+            put(44, q["out.w_vocab"].device_data()); put(45, q["out.w_vocab"].device_scale())
+            put(46, f["out.b_vocab"])
+            put(47, q["s0.w"].device_data()); put(48, q["s0.w"].device_scale())
+            put(49, f["s0.b"])
+            d = self.dims
+            dims = (C.c_int32 * 8)(d.src_vocab, d.tgt_vocab, d.embed, d.hidden, d.attn, d.readout,
+                                   1 if self.s0_mode == "zero" else 0,
+                                   1 if self.attention_query == "previous" else 0)
+            arr = (C.c_void_p * 50)(*ptrs)
+            h = C.c_void_p()
+            _lib.call("qnmt_model_create", C.cast(dims, C.c_void_p), C.cast(arr, C.c_void_p), 50,
+                      C.byref(h))
+            self._keep = keep
+            self._handle = h
+        return self._handle
+
+    def __del__(self):
+        try:
+            if self._handle is not None:
+                _lib.load().qnmt_model_destroy(self._handle)
+        except Exception:
+            pass
+
+
+def quantize_model(params: ModelParams, with_stats: bool = False) -> QuantizedModel:
+    """Quantize every weight matrix once on the device (model.py:394-437);
+    biases and embeddings stay f32 (uploaded)."""
+    q, f, stats = {}, {}, {}
+    for name, shape in tensor_specs(params.dims):
+        arr = params.tensors[name]
+        if len(shape) == 2 and name not in ("src_embed", "tgt_embed"):
+            dev = _dev.to_device(np.ascontiguousarray(arr, dtype=np.float32)).contiguous()
+            qm = quantize(dev)
+            q[name] = qm
+            if with_stats:
+                stats[name] = quantization_stats(name, dev, qm)
+        else:
+            f[name] = _dev.to_device(np.ascontiguousarray(arr, dtype=np.float32)).contiguous()
+    return QuantizedModel(params.dims, q, f, params.src_tokens, params.tgt_tokens, params.s0_mode,
+                          params.attention_query, stats)

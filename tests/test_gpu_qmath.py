@@ -1,0 +1,178 @@
+"""GPU parity of K1 (quantize) and K2/K3 (int8 GEMM + dequant) against the
+reference goldens and the oracle: bit-exact for codes, scales, int32/int64
+accumulators and dequantized f32 outputs."""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import qnmt_oracle as O
+from qnmt_test_helpers import F32, golden, sha
+
+pytestmark = pytest.mark.gpu
+
+pb = pytest.importorskip("paper_1804_05038_b200")
+from paper_1804_05038_b200 import _lib  # noqa: E402
+from paper_1804_05038_b200.errors import InvalidInputError, NumericError, ShapeError  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def kat():
+    return golden("qmath_kat.npz")
+
+
+def rand_q(rng, rows, cols):
+    codes = rng.integers(-127, 128, (rows, cols)).astype(np.int8)
+    return pb.QuantizedMatrix(codes, float(np.float32(rng.uniform(0.5, 200.0))))
+
+
+def test_quantize_known_answers(kat):
+    names = sorted({k[2:-3] for k in kat.files if k.startswith("q_") and k.endswith("_in")})
+    for n in names:
+        q = pb.quantize(kat[f"q_{n}_in"])
+        assert np.array_equal(q.data, kat[f"q_{n}_codes"]), n
+        assert q.scale == float(kat[f"q_{n}_scale"]), n
+        qa = pb.quantize_activations(kat[f"q_{n}_in"])
+        assert np.array_equal(qa.data, kat[f"q_{n}_codes"]), n
+    assert pb.quantize(np.array([[2, 1, -1]], F32)).data.tolist() == [[127, 64, -64]]
+    assert pb.quantize(np.array([[127, 0.49999997]], F32)).data.tolist() == [[127, 1]]
+    q = pb.quantize(np.array([[10.0]], F32))
+    assert q.data[0, 0] == 127 and q.scale == pytest.approx(12.7, abs=1e-5)
+    z = pb.quantize(np.zeros((3, 3), F32))
+    assert z.scale == 1.0 and not z.data.any()
+
+
+def test_quantize_errors():
+    with pytest.raises(InvalidInputError):
+        pb.quantize(np.array([[1.0, np.nan]], F32))
+    with pytest.raises(InvalidInputError):
+        pb.quantize(np.array([[np.inf]], F32))
+    with pytest.raises(NumericError):
+        pb.quantize_activations(np.array([[1.0], [np.nan]], F32))
+    with pytest.raises(ShapeError):
+        pb.quantize(np.zeros((0, 3), F32))
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_quantize_random_vs_oracle(seed):
+    rng = np.random.default_rng(seed)
+    shape = (int(rng.integers(1, 70)), int(rng.integers(1, 300)))
+    scale = [1e-3, 1.0, 50.0, 1e6][seed % 4]
+    m = (rng.normal(0, 1, shape) * scale).astype(F32)
+    if seed % 5 == 0:
+        m[rng.integers(0, shape[0]), rng.integers(0, shape[1])] = 0.5 / F32(127) * m.max()
+    q = pb.quantize(m)
+    oc, os_ = O.quantize(m)
+    assert np.array_equal(q.data, oc) and q.scale == os_
+    # symmetry and idempotence (test_qmath.py:84-103)
+    qn = pb.quantize(-m)
+    assert np.array_equal(qn.data, -q.data) and qn.scale == q.scale
+    q2 = pb.quantize(pb.dequantize(q))
+    assert np.array_equal(q2.data, q.data)
+
+
+def test_dequantize():
+    q = pb.QuantizedMatrix(np.array([[127]], dtype=np.int8), 12.7)
+    assert pb.dequantize(q)[0, 0] == pytest.approx(10.0, abs=1e-5)
+    rng = np.random.default_rng(0)
+    q = rand_q(rng, 7, 9)
+    assert np.array_equal(pb.dequantize(q), O.dequantize(q.data, q.scale))
+
+
+def test_qgemm_known_answers(kat):
+    for i in range(int(kat["g_count"])):
+        a = pb.QuantizedMatrix(kat[f"g{i}_a"], float(kat[f"g{i}_sa"]))
+        b = pb.QuantizedMatrix(kat[f"g{i}_b"], float(kat[f"g{i}_sb"]))
+        y = pb.qgemm_panel(a, b)
+        assert np.array_equal(y, kat[f"g{i}_y"]), i
+        assert np.array_equal(pb.qgemm(a, b), kat[f"g{i}_y"]), i
+
+
+@pytest.mark.parametrize("seed", range(60))
+def test_qgemm_random_bit_exact(seed):
+    """test_qmath.py:153-163 property, extended to the tiled shapes (N up to 300)."""
+    rng = np.random.default_rng(1000 + seed)
+    if seed < 30:
+        m, k, p = int(rng.integers(1, 65)), int(rng.integers(1, 65)), int(rng.integers(1, 9))
+    else:
+        m = int(rng.integers(1, 400))
+        k = int(16 * rng.integers(1, 80)) if seed % 2 else int(64 * rng.integers(1, 20))
+        p = int(rng.integers(1, 300))
+    a, b = rand_q(rng, m, k), rand_q(rng, k, p)
+    expect = O.qgemm(a.data, a.scale, b.data, b.scale)
+    assert np.array_equal(pb.qgemm(a, b), expect)
+    acc = pb.qmath.qgemm_acc(a, b).cpu().numpy()
+    assert np.array_equal(acc, O.int_product(a.data, b.data))
+
+
+def test_int64_widening_beyond_safe_k():
+    rng = np.random.default_rng(5)
+    k = pb.INT32_SAFE_K + 64
+    a = pb.QuantizedMatrix(rng.integers(-127, 128, (2, k)).astype(np.int8), 1.0)
+    b = pb.QuantizedMatrix(rng.integers(-127, 128, (k, 2)).astype(np.int8), 1.0)
+    expect = O.qgemm(a.data, 1.0, b.data, 1.0)
+    assert np.array_equal(pb.qgemm(a, b), expect)
+    big = pb.QuantizedMatrix(np.full((1, k), 127, np.int8), 1.0)
+    bb = pb.QuantizedMatrix(np.full((k, 1), 127, np.int8), 1.0)
+    assert pb.qmath.qgemm_acc(big, bb).item() == 127 * 127 * k   # > 2^31
+
+
+def test_shape_errors():
+    rng = np.random.default_rng(0)
+    with pytest.raises(ShapeError):
+        pb.qgemm(rand_q(rng, 3, 4), rand_q(rng, 5, 2))
+    with pytest.raises(InvalidInputError):
+        pb.qgemm(np.zeros((2, 2), np.int8), rand_q(rng, 2, 2))
+
+
+@pytest.mark.parametrize("bsz", [1, 64])
+def test_cfg1_bit_exact(kat, bsz):
+    """BASELINE cfg1: W [3072x1024] N(0,0.05), X [1024xB] N(0,1)."""
+    w = np.random.default_rng(1804).normal(0, 0.05, (3072, 1024)).astype(F32)
+    wq = pb.quantize(w)
+    assert wq.scale == float(kat["cfg1_w_scale"]) and sha(wq.data) == str(kat["cfg1_w_codes_sha"])
+    x = np.random.default_rng(5038 + bsz).normal(0, 1, (1024, bsz)).astype(F32)
+    xq = pb.quantize_activations(x)
+    assert xq.scale == float(kat[f"cfg1_b{bsz}_x_scale"])
+    assert sha(xq.data) == str(kat[f"cfg1_b{bsz}_x_codes_sha"])
+    acc = pb.qmath.qgemm_acc(wq, xq).cpu().numpy()
+    assert sha(acc.astype(np.int32)) == str(kat[f"cfg1_b{bsz}_acc_sha"])
+    y = pb.qgemm_panel(wq, xq)
+    assert sha(y) == str(kat[f"cfg1_b{bsz}_y_sha"])
+    # the same through torch tensors (device-resident API)
+    yt = pb.qgemm(pb.quantize(torch.from_numpy(w).cuda()), pb.quantize_activations(torch.from_numpy(x).cuda()))
+    assert isinstance(yt, torch.Tensor) and np.array_equal(yt.cpu().numpy(), y)
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_segmented_quantize_vs_oracle(seed):
+    """Per-segment scales (batched decode): each segment equals an independent
+    quantize_activations of that segment's columns."""
+    rng = np.random.default_rng(77 + seed)
+    K = int(rng.choice([12, 512, 1024, 2048]))
+    nseg = int(rng.integers(1, 9))
+    widths = rng.integers(1, 6, nseg)
+    cols = []
+    seg = []
+    for s, w in enumerate(widths):
+        cols.append((rng.normal(0, 1, (w, K)) * 10.0 ** rng.uniform(-3, 3)).astype(F32))
+        seg += [s] * int(w)
+    x = np.concatenate(cols)
+    from paper_1804_05038_b200.layers import _quant_k
+    xd = torch.from_numpy(x).cuda()
+    segd = torch.tensor(seg, dtype=torch.int32, device="cuda")
+    q, sc = _quant_k(xd, segd, nseg)
+    q, sc = q.cpu().numpy(), sc.cpu().numpy()
+    r = 0
+    for s, w in enumerate(widths):
+        oc, os_ = O.quantize_activations(cols[s].T)
+        assert sc[s] == np.float32(os_)
+        assert np.array_equal(q[r:r + w].T, oc)
+        r += w
+
+
+def test_library_loaded_from_tree():
+    import os
+    assert os.path.exists(_lib.LIB_PATH)
+    maps = open("/proc/self/maps").read()
+    assert "libqnmt_b200.so" in maps
