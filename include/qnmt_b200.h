@@ -102,6 +102,11 @@ int qnmt_gemm_i8(const int8_t* W, int64_t M, int64_t K, int64_t ldw,
                  const float* bias, float* Y, int64_t ldy,
                  int64_t* acc_out, int32_t flags, void* stream);
 
+/* GEMM implementation selector (testing / A-B measurement): 0 = auto
+ * (tcgen05 for N > 8, dp4a GEMV otherwise), 1 = CUDA-core dp4a only,
+ * 2 = tcgen05 whenever the shape is eligible.  Returns the previous value. */
+int qnmt_set_gemm_impl(int impl);
+
 /* ---------------------------------------------------------------------------
  * GRU gate arithmetic (layers.py:170-181), f32 ops in the reference's
  * association order, sigmoid/tanh evaluated in fp64 and rounded once.

@@ -47,6 +47,7 @@ SIGNATURES = {
     "qnmt_fetch_results": (I32, [P, P, I32, P, P, P]),
     "qnmt_last_d2h_bytes": (I64, [P]),
     "qnmt_kernel_launches": (I64, []),
+    "qnmt_set_gemm_impl": (I32, [I32]),
 }
 
 QNMT_OK, ERR_SHAPE, ERR_INVALID, ERR_NUMERIC, ERR_VOCAB, ERR_CONFIG, ERR_EMPTY, ERR_CUDA = range(8)

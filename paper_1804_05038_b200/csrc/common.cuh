@@ -84,6 +84,22 @@ __device__ __forceinline__ float dequant(long long acc, float sa, float sb) {
     return __double2float_rn(__ddiv_rn((double)acc, den));
 }
 
+// Same value as dequant(), but via a reciprocal multiply: q = acc * (1/sa)(1/sb)
+// carries at most a few f64 ulps of error, so fl32(q) equals the correctly
+// rounded fl32(acc / (sa*sb)) unless q lies within a few f64 ulps of an f32
+// rounding midpoint (low 29 mantissa bits ~ 0x10000000) or outside the normal
+// f32 range -- only then is the exact __ddiv_rn evaluated (~1e-7 of elements).
+__device__ __forceinline__ float dequant_rcp(long long acc, double rcp, float sa, float sb) {
+    double q = (double)acc * rcp;
+    unsigned long long b = (unsigned long long)__double_as_longlong(q);
+    int low = (int)(b & 0x1fffffffull);
+    int ex = (int)((b >> 52) & 0x7ff);
+    bool safe = (low - 0x10000000 > 64 || 0x10000000 - low > 64) && ex > 1023 - 125 && ex < 1023 + 127;
+    if (acc == 0) return 0.0f;
+    if (safe) return __double2float_rn(q);
+    return dequant(acc, sa, sb);
+}
+
 __device__ __forceinline__ void set_flag(int32_t* flag, int bit) {
     if (flag) atomicOr(flag, bit);
 }

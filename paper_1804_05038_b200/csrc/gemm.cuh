@@ -21,6 +21,9 @@ struct GemmArgs {
 };
 
 int gemm_i8_launch(const GemmArgs& g, cudaStream_t st);
+bool tc_eligible(const GemmArgs& g);
+int gemm_tc_launch(const GemmArgs& g, cudaStream_t st);
+extern int g_gemm_impl;   // 0 auto, 1 CUDA-core dp4a only, 2 tcgen05 whenever eligible
 
 int quantize_launch(const float* x, int64_t ncols, int64_t K, int64_t ldx, const int32_t* col_seg,
                     int32_t nseg, int8_t* q, int64_t ldq, float* scales, uint32_t* seg_maxbits,

@@ -37,7 +37,7 @@ __device__ __forceinline__ void epilogue(const EpiArgs& e, int64_t m, int64_t n,
     if (!e.Y) return;
     float sw = e.w_scales[m / e.w_rows_per_scale];
     float sx = e.x_scales[e.col_seg ? e.col_seg[n] : 0];
-    float y = dequant(acc, sw, sx);
+    float y = dequant_rcp(acc, (1.0 / (double)sw) * (1.0 / (double)sx), sw, sx);
     if (e.bias) y = __fadd_rn(y, e.bias[m]);
     float* dst = e.Y + n * e.ldy + m;
     if (e.flags & QNMT_GEMM_ACCUMULATE) y = __fadd_rn(*dst, y);
@@ -208,8 +208,11 @@ static void dispatch_gemv(int64_t N, const int8_t* W, int64_t M, int64_t K, int6
     }
 }
 
+int g_gemm_impl = 0;
+
 int gemm_i8_launch(const GemmArgs& g, cudaStream_t st) {
     if (g.M <= 0 || g.N <= 0) return QNMT_OK;
+    if (g_gemm_impl != 1 && tc_eligible(g) && (g.N > 8 || g_gemm_impl == 2)) return gemm_tc_launch(g, st);
     EpiArgs e{g.w_scales, g.w_rows_per_scale, g.x_scales, g.col_seg, g.bias, g.Y, g.ldy,
               g.acc_out, g.M, g.flags};
     bool aligned = (g.K % 16 == 0) && (g.ldw % 16 == 0) && (g.ldx % 16 == 0) &&
@@ -247,6 +250,12 @@ int gemm_i8_launch(const GemmArgs& g, cudaStream_t st) {
 }
 
 }  // namespace qnmt
+
+extern "C" int qnmt_set_gemm_impl(int impl) {
+    int old = qnmt::g_gemm_impl;
+    qnmt::g_gemm_impl = impl;
+    return old;
+}
 
 extern "C" int qnmt_gemm_i8(const int8_t* W, int64_t M, int64_t K, int64_t ldw,
                             const float* w_scales, int64_t w_rows_per_scale, const int8_t* X,

@@ -1,0 +1,319 @@
+// gemm_tcgen05.cu -- K3: int8 GEMM on the 5th-generation tensor cores.
+//
+//   D[m][n] = sum_k W[m][k] * X[n][k]    (both operands K-major int8)
+//
+// Replaces qmath.py:400-427 (qgemm_panel) for wide panels (batched decode:
+// N = live hypotheses of many sentences; encoder input side: N = positions).
+//
+// Persistent, warp-specialised CTA (one per SM):
+//   warp 0      TMA producer: W tile [128 x 128B] and X tile [BN x 128B] per
+//               k-block into a STAGES-deep ring (SWIZZLE_128B), mbarrier
+//               complete_tx signalling.
+//   warp 1      TMEM allocator + single-thread MMA issuer:
+//               tcgen05.mma.cta_group::1.kind::i8, M=128, N=BN, K=32 x4 per
+//               k-block, int32 accumulators in TMEM (2 buffers -> the epilogue
+//               of tile i overlaps the MMAs of tile i+1); tcgen05.commit frees
+//               ring slots and publishes finished accumulators.
+//   warps 2..9  epilogue: tcgen05.ld 32x32b.x16 -> exact dequant
+//               fl32(acc / (sw*sx)) (reciprocal fast path, __ddiv_rn near f32
+//               midpoints) -> +bias -> (+Y) -> coalesced f32 stores of Y[n][m].
+// Tiles are visited n-fastest so consecutive CTAs share the W block in L2.
+#include <mutex>
+#include <unordered_map>
+
+#include "gemm.cuh"
+#include "tc_common.cuh"
+
+namespace qnmt {
+
+constexpr int TC_BM = 128;
+constexpr int TC_BK = 128;   // bytes of K per stage (= int8 elements)
+constexpr int TC_EPI_WARPS = 8;
+constexpr int TC_THREADS = 64 + 32 * TC_EPI_WARPS;
+
+template <int BN>
+struct TcCfg {
+    static constexpr int A_BYTES = TC_BM * TC_BK;
+    static constexpr int B_BYTES = BN * TC_BK;
+    static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+    static constexpr int STAGES = (BN == 256) ? 4 : (BN == 128 ? 6 : 8);
+    static constexpr int TMEM_COLS = 2 * BN;   // 128 / 256 / 512 (power of two)
+    static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+};
+
+struct TcEpi {
+    const float* w_scales;
+    int64_t w_rows_per_scale;
+    const float* x_scales;
+    const int32_t* col_seg;
+    const float* bias;
+    float* Y;
+    int64_t ldy;
+    int64_t* acc_out;
+    int32_t flags;
+};
+
+template <int BN>
+__global__ void __launch_bounds__(TC_THREADS, 1)
+k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N, int K,
+          TcEpi e) {
+    using C = TcCfg<BN>;
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char* smem = (unsigned char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
+    uint64_t* empty = full + C::STAGES;
+    uint64_t* tfull = empty + C::STAGES;    // [2]
+    uint64_t* tempty = tfull + 2;           // [2]
+    uint32_t* tmem_base_smem = reinterpret_cast<uint32_t*>(tempty + 2);
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const int m_blocks = (M + TC_BM - 1) / TC_BM;
+    const int n_blocks = (N + BN - 1) / BN;
+    const int tiles = m_blocks * n_blocks;
+    const int k_blocks = (K + TC_BK - 1) / TC_BK;
+
+    if (warp == 0 && lane == 0) {
+        tc::prefetch_tmap(&tmA);
+        tc::prefetch_tmap(&tmB);
+        for (int s = 0; s < C::STAGES; ++s) {
+            tc::mbar_init(&full[s], 1);
+            tc::mbar_init(&empty[s], 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            tc::mbar_init(&tfull[b], 1);
+            tc::mbar_init(&tempty[b], TC_EPI_WARPS);
+        }
+        tc::fence_mbar_init();
+    }
+    if (warp == 1) tc::tmem_alloc<C::TMEM_COLS>(tmem_base_smem);
+    tc::tc_fence_before();
+    __syncthreads();
+    tc::tc_fence_after();
+    const uint32_t tmem_base = *tmem_base_smem;
+
+    if (warp == 0) {
+        // ---------------- TMA producer ----------------
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+                const int mb = tile / n_blocks, nb = tile % n_blocks;
+                for (int kb = 0; kb < k_blocks; ++kb) {
+                    tc::mbar_wait(&empty[stage], phase ^ 1);
+                    unsigned char* sa = smem + stage * C::STAGE_BYTES;
+                    unsigned char* sb = sa + C::A_BYTES;
+                    tc::mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
+                    tc::tma_load_2d(sa, &tmA, &full[stage], kb * TC_BK, mb * TC_BM);
+                    tc::tma_load_2d(sb, &tmB, &full[stage], kb * TC_BK, nb * BN);
+                    if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ---------------- MMA issuer ----------------
+        constexpr uint32_t IDESC = tc::idesc_i8(TC_BM, BN);
+        int stage = 0;
+        uint32_t phase = 0;
+        int it = 0;
+        for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++it) {
+            const int buf = it & 1;
+            const uint32_t use = (uint32_t)(it >> 1) & 1u;
+            tc::mbar_wait(&tempty[buf], use ^ 1);
+            tc::tc_fence_after();
+            const uint32_t d = tmem_base + (uint32_t)(buf * BN);
+            for (int kb = 0; kb < k_blocks; ++kb) {
+                tc::mbar_wait(&full[stage], phase);
+                tc::tc_fence_after();
+                if (lane == 0) {
+                    const uint32_t a0 = tc::smem_u32(smem + stage * C::STAGE_BYTES);
+                    const uint32_t b0 = a0 + C::A_BYTES;
+#pragma unroll
+                    for (int k = 0; k < TC_BK / 32; ++k) {
+                        tc::mma_i8(d, tc::sw128_kmajor_desc(a0 + 32 * k), tc::sw128_kmajor_desc(b0 + 32 * k), IDESC,
+                                   (kb | k) != 0);
+                    }
+                    tc::mma_commit(&empty[stage]);
+                    if (kb == k_blocks - 1) tc::mma_commit(&tfull[buf]);
+                }
+                __syncwarp();
+                if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+            }
+        }
+    } else {
+        // ---------------- epilogue ----------------
+        const int ew = warp - 2;                 // 0..7
+        const int lg = warp & 3;                 // TMEM lane group this warp may access
+        const int half = ew >> 2;                // column half of the tile
+        constexpr int COLS = BN / 2;
+        int it = 0;
+        for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++it) {
+            const int mb = tile / n_blocks, nb = tile % n_blocks;
+            const int buf = it & 1;
+            const uint32_t use = (uint32_t)(it >> 1) & 1u;
+            tc::mbar_wait(&tfull[buf], use);
+            tc::tc_fence_after();
+            const int m = mb * TC_BM + lg * 32 + lane;
+            const bool mok = m < M;
+            float sw = 1.0f, bias = 0.0f;
+            double isw = 1.0;
+            if (mok) {
+                sw = e.w_scales[m / e.w_rows_per_scale];
+                isw = 1.0 / (double)sw;
+                if (e.bias) bias = e.bias[m];
+            }
+#pragma unroll 1
+            for (int c0 = half * COLS; c0 < (half + 1) * COLS; c0 += 16) {
+                uint32_t r[16];
+                tc::tmem_ld16(tmem_base + ((uint32_t)(lg * 32) << 16) + (uint32_t)(buf * BN + c0), r);
+                tc::tmem_ld_wait();
+                const int nbase = nb * BN + c0;
+                // per-column activation scale and its reciprocal, one column per lane (lanes 0..15)
+                float sxl = 1.0f;
+                double isxl = 1.0;
+                {
+                    int n = nbase + (lane & 15);
+                    if (n < N) {
+                        sxl = e.x_scales[e.col_seg ? e.col_seg[n] : 0];
+                        isxl = 1.0 / (double)sxl;
+                    }
+                }
+#pragma unroll
+                for (int j = 0; j < 16; ++j) {
+                    const int n = nbase + j;
+                    const float sx = __shfl_sync(0xffffffffu, sxl, j);
+                    const double isx = __shfl_sync(0xffffffffu, isxl, j);
+                    if (mok && n < N) {
+                        const int acc = (int)r[j];
+                        if (e.acc_out) e.acc_out[(int64_t)n * M + m] = acc;
+                        if (e.Y) {
+                            float y = dequant_rcp(acc, isw * isx, sw, sx);
+                            if (e.bias) y = __fadd_rn(y, bias);
+                            float* dst = e.Y + (int64_t)n * e.ldy + m;
+                            if (e.flags & QNMT_GEMM_ACCUMULATE) y = __fadd_rn(*dst, y);
+                            *dst = y;
+                        }
+                    }
+                }
+            }
+            tc::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(&tempty[buf]);
+        }
+    }
+    __syncthreads();
+    if (warp == 1) {
+        tc::tc_fence_after();
+        tc::tmem_dealloc<C::TMEM_COLS>(tmem_base);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// host side: tensor maps (cached per (pointer, shape)) and launch
+// ---------------------------------------------------------------------------
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+    static EncodeTiledFn fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeTiledFn>(p);
+    });
+    return fn;
+}
+
+struct MapKey {
+    const void* p;
+    int64_t rows, cols, ld;
+    int box_rows;
+    bool operator==(const MapKey& o) const {
+        return p == o.p && rows == o.rows && cols == o.cols && ld == o.ld && box_rows == o.box_rows;
+    }
+};
+struct MapKeyHash {
+    size_t operator()(const MapKey& k) const {
+        return std::hash<const void*>()(k.p) ^ (size_t)(k.rows * 1315423911u) ^ (size_t)(k.cols << 20) ^
+               (size_t)(k.ld * 2654435761u) ^ (size_t)k.box_rows;
+    }
+};
+
+static int get_map(const int8_t* p, int64_t rows, int64_t cols, int64_t ld, int box_rows, CUtensorMap* out) {
+    static std::mutex mu;
+    static std::unordered_map<MapKey, CUtensorMap, MapKeyHash> cache;
+    MapKey key{p, rows, cols, ld, box_rows};
+    std::lock_guard<std::mutex> g(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) {
+        *out = it->second;
+        return QNMT_OK;
+    }
+    EncodeTiledFn fn = encode_fn();
+    if (!fn) { set_error("cuTensorMapEncodeTiled unavailable"); return QNMT_ERR_CUDA; }
+    CUtensorMap m;
+    cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)ld};
+    cuuint32_t box[2] = {(cuuint32_t)TC_BK, (cuuint32_t)box_rows};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = fn(&m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, (void*)p, dims, strides, box, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) { set_error("cuTensorMapEncodeTiled failed (%d)", (int)r); return QNMT_ERR_CUDA; }
+    if (cache.size() > 4096) cache.clear();
+    cache[key] = m;
+    *out = m;
+    return QNMT_OK;
+}
+
+static int sm_count() {
+    static int n = 0;
+    if (!n) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        if (n <= 0) n = 148;
+    }
+    return n;
+}
+
+template <int BN>
+static int launch_tc(const GemmArgs& g, cudaStream_t st) {
+    using C = TcCfg<BN>;
+    static bool attr_set = false;
+    if (!attr_set) {
+        QNMT_CUDA(cudaFuncSetAttribute(k_gemm_tc<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+        attr_set = true;
+    }
+    CUtensorMap ta, tb;
+    int rc = get_map(g.W, g.M, g.K, g.ldw, TC_BM, &ta);
+    if (rc) return rc;
+    rc = get_map(g.X, g.N, g.K, g.ldx, BN, &tb);
+    if (rc) return rc;
+    TcEpi e{g.w_scales, g.w_rows_per_scale, g.x_scales, g.col_seg, g.bias, g.Y, g.ldy, g.acc_out, g.flags};
+    int tiles = (int)(cdiv(g.M, TC_BM) * cdiv(g.N, BN));
+    int grid = tiles < sm_count() ? tiles : sm_count();
+    k_gemm_tc<BN><<<grid, TC_THREADS, C::SMEM, st>>>(ta, tb, (int)g.M, (int)g.N, (int)g.K, e);
+    QNMT_CHECK_LAUNCH("k_gemm_tc");
+    return QNMT_OK;
+}
+
+bool tc_eligible(const GemmArgs& g) {
+    return g.K % 16 == 0 && g.ldw % 16 == 0 && g.ldx % 16 == 0 && ((uintptr_t)g.W % 16 == 0) &&
+           ((uintptr_t)g.X % 16 == 0) && g.K <= QNMT_INT32_SAFE_K && g.K > 0 && g.M < (1 << 30) &&
+           g.N < (1 << 30);
+}
+
+int gemm_tc_launch(const GemmArgs& g, cudaStream_t st) {
+    const int64_t mb = cdiv(g.M, TC_BM);
+    const int sms = sm_count();
+    if (g.N > 128 && mb * cdiv(g.N, 256) >= sms) return launch_tc<256>(g, st);
+    if (g.N > 64 && mb * cdiv(g.N, 128) >= sms / 2) return launch_tc<128>(g, st);
+    return launch_tc<64>(g, st);
+}
+
+}  // namespace qnmt

@@ -176,3 +176,60 @@ def test_library_loaded_from_tree():
     assert os.path.exists(_lib.LIB_PATH)
     maps = open("/proc/self/maps").read()
     assert "libqnmt_b200.so" in maps
+
+
+SHAPES_TC = [(128, 128, 16), (128, 128, 64), (130, 256, 9), (3072, 1024, 1280), (50000 // 7, 512, 333),
+             (2048, 1024, 256), (1024, 2048, 1000), (77, 80, 300), (512, 96, 17), (1000, 1024, 64),
+             (256, 2048, 2), (384, 512, 1)]
+
+
+@pytest.mark.parametrize("shape", SHAPES_TC)
+def test_tcgen05_gemm_bit_exact(shape):
+    """K3 (tcgen05.mma kind::i8) == CUDA-core path == oracle, incl. M/N/K tails."""
+    M, K, N = shape
+    rng = np.random.default_rng(M * 7 + K + N)
+    W = pb.QuantizedMatrix(rng.integers(-127, 128, (M, K)).astype(np.int8), float(np.float32(rng.uniform(1, 300))))
+    X = pb.QuantizedMatrix(rng.integers(-127, 128, (K, N)).astype(np.int8), float(np.float32(rng.uniform(1, 300))))
+    expect = O.qgemm(W.data, W.scale, X.data, X.scale)
+    lib = _lib.load()
+    old = lib.qnmt_set_gemm_impl(2)
+    try:
+        y_tc = pb.qgemm(W, X)
+        acc_tc = pb.qmath.qgemm_acc(W, X).cpu().numpy()
+        lib.qnmt_set_gemm_impl(1)
+        y_dp = pb.qgemm(W, X)
+    finally:
+        lib.qnmt_set_gemm_impl(old)
+    assert np.array_equal(acc_tc, O.int_product(W.data, X.data))
+    assert np.array_equal(y_tc, expect)
+    assert np.array_equal(y_dp, expect)
+
+
+def test_tcgen05_segmented_bias_accumulate():
+    """Segmented activation scales + bias + ACCUMULATE epilogue on the tensor-core path."""
+    import torch
+    rng = np.random.default_rng(9)
+    M, K, N, S = 640, 1024, 700, 37
+    Wc = rng.integers(-127, 128, (M, K)).astype(np.int8)
+    Xc = rng.integers(-127, 128, (N, K)).astype(np.int8)
+    seg = np.sort(rng.integers(0, S, N)).astype(np.int32)
+    ws = np.float32(rng.uniform(10, 200, 2))          # two row blocks of 320
+    xs = np.float32(rng.uniform(10, 200, S))
+    bias = rng.normal(0, 1, M).astype(np.float32)
+    y0 = rng.normal(0, 1, (N, M)).astype(np.float32)
+    d = lambda a: torch.from_numpy(a).cuda()
+    Y = d(y0.copy())
+    lib = _lib.load()
+    old = lib.qnmt_set_gemm_impl(2)
+    try:
+        pb.qmath.gemm_kmajor(d(Wc), d(ws), 320, d(Xc), d(xs), col_seg=d(seg), bias=d(bias), Y=Y, accumulate=True)
+    finally:
+        lib.qnmt_set_gemm_impl(old)
+    acc = O.int_product(Wc, Xc.T)                       # [M, N]
+    ref = np.empty((N, M), np.float32)
+    for n in range(N):
+        for blk in range(2):
+            rows = slice(320 * blk, 320 * (blk + 1))
+            yv = O.scale_output(acc[rows, n], ws[blk], xs[seg[n]])
+            ref[n, rows] = y0[n, rows] + (yv + bias[rows])
+    assert np.array_equal(Y.cpu().numpy(), ref)
