@@ -146,6 +146,7 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--cpu-sample", type=int, default=8)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-profile", action="store_true", help="disable the engine's event profiler")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
@@ -206,6 +207,9 @@ def main():
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
+    import ctypes as C
+    if not args.no_profile:
+        lib.qnmt_engine_profile(eng._h, 1)
     clk = ClockSampler(local)
     secs, toks, launches = 0.0, 0, 0
     step_ms = []
@@ -217,6 +221,16 @@ def main():
         step_ms.append(1000 * t)
     torch.cuda.synchronize()
     clocks = clk.stop()
+    phases = None
+    if not args.no_profile:
+        arr = [(C.c_double * 16)() for _ in range(4)]
+        ng = lib.qnmt_engine_profile_read(eng._h, *[C.cast(a, C.c_void_p) for a in arr])
+        lib.qnmt_engine_profile(eng._h, 0)
+        names = ["encoder", "embed", "quantize", "gemm_decoder", "gru_gates", "attention", "gemm_vocab",
+                 "topk", "search", "gather", "misc"]
+        phases = {names[i]: {"ms": arr[0][i] / args.steps, "launch_groups": arr[1][i] / args.steps,
+                             "int_ops": arr[2][i] / args.steps, "bytes": arr[3][i] / args.steps}
+                  for i in range(ng)}
     if world > 1:
         dist.barrier()
 
@@ -272,6 +286,7 @@ def main():
                         "d2h_bytes_per_step": d2h // args.steps},
                 "gpu_launches": launches,
                 "roofline": None,
+                "phases_ms_per_step": {k: round(v["ms"], 3) for k, v in phases.items()} if phases else None,
                 "cpu_baseline": cpu,
                 "clocks": clocks}
         print(json.dumps(line), flush=True)

@@ -1,0 +1,120 @@
+#!/usr/bin/env python
+"""Per-kernel device times at the cfg5 decode-step shapes (N = 1280 live columns
+= 256 sentences x beam 5), each captured 20x in a CUDA graph and timed with
+CUDA events (no host launch overhead), plus cfg1's batch-1 GEMV with 64
+rotating weight copies (cold L2).  One JSON line per kernel."""
+
+from __future__ import annotations
+
+import json
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import paper_1804_05038_b200 as pb  # noqa: E402
+from paper_1804_05038_b200 import _dev, _lib  # noqa: E402
+
+PEAK = {"hbm_gbs": 6461.2, "int8_tops_spec": 4500.0}
+try:
+    PEAK.update(json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                                            "MEASURED_PEAKS.json"))))
+except OSError:
+    pass
+
+
+def graph_time(fn, reps=20):
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        fn()
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            for _ in range(reps):
+                fn()
+    torch.cuda.synchronize()
+    g.replay()
+    torch.cuda.synchronize()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    best = 1e9
+    for _ in range(5):
+        ev[0].record()
+        g.replay()
+        ev[1].record()
+        ev[1].synchronize()
+        best = min(best, ev[0].elapsed_time(ev[1]) / reps)
+    return best * 1e-3
+
+
+def gemm_case(name, M, K, N, seg_count=256):
+    rng = np.random.default_rng(M + K + N)
+    W = torch.from_numpy(rng.integers(-127, 128, (M, K)).astype(np.int8)).cuda()
+    X = torch.from_numpy(rng.integers(-127, 128, (N, K)).astype(np.int8)).cuda()
+    ws = torch.rand(1, device="cuda") + 1
+    xs = torch.rand(seg_count, device="cuda") + 1
+    seg = torch.arange(N, device="cuda", dtype=torch.int32) // max(1, N // seg_count)
+    Y = torch.empty((N, M), dtype=torch.float32, device="cuda")
+    t = graph_time(lambda: pb.qmath.gemm_kmajor(W, ws, M, X, xs, col_seg=seg, Y=Y))
+    ops = 2.0 * M * N * K
+    nbytes = M * K + N * K + 4 * M * N
+    return {"kernel": "gemm_i8 (tcgen05)" if N > 8 else "gemm_i8 (dp4a gemv)", "shape": name, "M": M, "N": N,
+            "K": K, "us": t * 1e6, "TOPS": ops / t / 1e12, "tensor_frac_of_spec": ops / t / 1e12 / PEAK["int8_tops_spec"],
+            "GBps": nbytes / t / 1e9}
+
+
+def topk_case(N=1280, V=50000, k=5):
+    x = torch.randn((N, V), device="cuda") * 0.2
+    live = torch.randn(N, dtype=torch.float64, device="cuda")
+    cs = torch.empty((N, k), dtype=torch.float64, device="cuda")
+    ct = torch.empty((N, k), dtype=torch.int32, device="cuda")
+    f = _dev.flag()
+    st = lambda: torch.cuda.current_stream().cuda_stream
+    t = graph_time(lambda: _lib.call("qnmt_topk_candidates", x.data_ptr(), N, V, V, live.data_ptr(), k,
+                                     cs.data_ptr(), ct.data_ptr(), f.data_ptr(), st()))
+    return {"kernel": "topk_candidates", "N": N, "V": V, "us": t * 1e6, "GBps": 4.0 * N * V / t / 1e9,
+            "hbm_frac_of_measured": 4.0 * N * V / t / 1e9 / PEAK["hbm_gbs"]}
+
+
+def gemv_cold(bsz):
+    w = torch.randint(-127, 128, (3072, 1024), dtype=torch.int8, device="cuda")
+    copies = [w.clone() for _ in range(64)]
+    X = torch.randint(-127, 128, (bsz, 1024), dtype=torch.int8, device="cuda")
+    ws = torch.ones(1, device="cuda")
+    xs = torch.ones(1, device="cuda")
+    Y = torch.empty((bsz, 3072), dtype=torch.float32, device="cuda")
+    it = iter(range(10 ** 9))
+
+    def run():
+        for c in copies:
+            pb.qmath.gemm_kmajor(c, ws, 3072, X, xs, Y=Y)
+    t = graph_time(run, reps=1) / len(copies)
+    nbytes = 3072 * 1024 + 4 * 1024 * bsz + 4 * 3072 * bsz
+    return {"kernel": "cfg1 qgemm_panel", "B": bsz, "us": t * 1e6, "GBps": nbytes / t / 1e9,
+            "hbm_frac_of_measured": nbytes / t / 1e9 / PEAK["hbm_gbs"], "TOPS": 2 * 3072 * 1024 * bsz / t / 1e12,
+            "note": "64 rotating weight copies (201 MB > 126 MB L2)"}
+
+
+def main():
+    which = sys.argv[1:] or ["gemm", "topk", "gemv"]
+    out = []
+    if "gemm" in which:
+        N = 1280
+        for name, M, K in [("dec_r Wx", 3072, 512), ("dec Uzr", 2048, 1024), ("dec Uc", 1024, 1024),
+                           ("att U", 2048, 1024), ("dec_q Wx", 3072, 2048), ("readout Ws", 512, 1024),
+                           ("readout Wc", 512, 2048), ("vocab", 50000, 512)]:
+            out.append(gemm_case(name, M, K, N))
+        out.append(gemm_case("enc x-side", 3072, 512, 13000, 13000))
+        out.append(gemm_case("enc Uzr", 2048, 1024, 256))
+    if "topk" in which:
+        out.append(topk_case())
+    if "gemv" in which:
+        out += [gemv_cold(1), gemv_cold(64)]
+    for r in out:
+        print(json.dumps(r), flush=True)
+
+
+if __name__ == "__main__":
+    main()

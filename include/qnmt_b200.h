@@ -164,6 +164,10 @@ int qnmt_topk_candidates(const float* logits, int64_t N, int64_t V, int64_t ld,
                          const double* live_scores, int32_t k,
                          double* cand_score, int32_t* cand_tok, int32_t* err_flag, void* stream);
 
+/* 1 = use the three-pass reference candidate kernel instead of the single-pass
+ * one (A/B testing; results are identical by construction).  Returns old. */
+int qnmt_set_topk_exact(int exact);
+
 /* Embedding gather (layers.py:324, :367): out[n] = table[ids[n]] ([rows][E]);
  * ids outside [0, rows) raise QNMT_FLAG_VOCAB and yield zeros. */
 int qnmt_embed_gather(const float* table, int64_t rows, int64_t E, const int32_t* ids,
@@ -254,6 +258,19 @@ int qnmt_fetch_results(qnmt_engine* e, int32_t* out_tokens, int32_t out_stride, 
 int64_t qnmt_last_d2h_bytes(const qnmt_engine* e);
 /* kernels launched by this library since load (process-wide counter) */
 int64_t qnmt_kernel_launches(void);
+
+/* 1 (default): decode steps run as captured CUDA graphs with a device-side
+ * live-column count (host polls it every 16 steps); 0: eager per-step loop
+ * with one host sync per step.  Results are identical.  Returns old value. */
+int qnmt_engine_set_graphs(qnmt_engine* e, int enable);
+
+/* Phase profiler (forces the eager loop while enabled): CUDA events on the engine stream around the kernel groups
+ * of a decode (0 encoder, 1 embed, 2 quantize, 3 decoder GEMMs, 4 GRU gates,
+ * 5 attention, 6 vocab GEMM, 7 top-k, 8 search, 9 gather, 10 misc).
+ * qnmt_engine_profile(e, 1) resets and enables; _read fills [16] arrays with
+ * elapsed ms, launches, algorithmic int-ops and algorithmic bytes per group. */
+int qnmt_engine_profile(qnmt_engine* e, int enable);
+int qnmt_engine_profile_read(const qnmt_engine* e, double* ms, double* calls, double* ops, double* bytes);
 
 /* device bytes held by the engine (scratch + history) */
 size_t qnmt_engine_bytes(const qnmt_engine* e);

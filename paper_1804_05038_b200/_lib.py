@@ -48,6 +48,10 @@ SIGNATURES = {
     "qnmt_last_d2h_bytes": (I64, [P]),
     "qnmt_kernel_launches": (I64, []),
     "qnmt_set_gemm_impl": (I32, [I32]),
+    "qnmt_set_topk_exact": (I32, [I32]),
+    "qnmt_engine_profile": (I32, [P, I32]),
+    "qnmt_engine_set_graphs": (I32, [P, I32]),
+    "qnmt_engine_profile_read": (I32, [P, P, P, P, P]),
 }
 
 QNMT_OK, ERR_SHAPE, ERR_INVALID, ERR_NUMERIC, ERR_VOCAB, ERR_CONFIG, ERR_EMPTY, ERR_CUDA = range(8)

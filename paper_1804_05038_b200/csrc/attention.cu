@@ -24,8 +24,10 @@ template <bool VEC>
 __global__ void __launch_bounds__(ATT_T)
 k_att_max(const float* __restrict__ u, int64_t ldu, const int32_t* __restrict__ col_sent,
           const float* __restrict__ att_proj, const int64_t* __restrict__ sent_row,
-          const int32_t* __restrict__ sent_len, int64_t A, uint32_t* maxbits, int32_t* err_flag) {
+          const int32_t* __restrict__ sent_len, int64_t A, uint32_t* maxbits, int32_t* err_flag,
+          const int32_t* n_dev) {
     int64_t n = blockIdx.y;
+    if (beyond(n_dev, n)) return;
     int s = col_sent[n];
     int l = sent_len[s];
     int i0 = blockIdx.x * ATT_PC;
@@ -63,8 +65,9 @@ k_att_score(const float* __restrict__ u, int64_t ldu, const int32_t* __restrict_
             const float* __restrict__ att_proj, const int64_t* __restrict__ sent_row,
             const int32_t* __restrict__ sent_len, int64_t A, const int8_t* __restrict__ v_codes,
             const float* __restrict__ v_scale, const uint32_t* __restrict__ maxbits,
-            float* __restrict__ scores, int32_t max_len) {
+            float* __restrict__ scores, int32_t max_len, const int32_t* n_dev) {
     int64_t n = blockIdx.y;
+    if (beyond(n_dev, n)) return;
     int s = col_sent[n];
     int l = sent_len[s];
     int i0 = blockIdx.x * ATT_PC;
@@ -128,13 +131,14 @@ __global__ void __launch_bounds__(256)
 k_att_context(const float* __restrict__ scores, int32_t max_len, const int32_t* __restrict__ col_sent,
               const float* __restrict__ states, const int64_t* __restrict__ sent_row,
               const int32_t* __restrict__ sent_len, int64_t H2, float* __restrict__ ctx, int64_t ldc,
-              float* __restrict__ alpha, int64_t lda, int32_t* err_flag) {
+              float* __restrict__ alpha, int64_t lda, int32_t* err_flag, const int32_t* n_dev) {
     extern __shared__ unsigned char smem_raw[];
     double* e = reinterpret_cast<double*>(smem_raw);          // [max_len]
     float* al = reinterpret_cast<float*>(e + max_len);         // [max_len]
     __shared__ double s_sum;
     __shared__ float s_max;
     int64_t n = blockIdx.y;
+    if (beyond(n_dev, n)) return;
     int s = col_sent[n];
     int l = sent_len[s];
     const float* sc = scores + n * max_len;
@@ -186,16 +190,16 @@ int attention_launch(const float* u, int64_t ldu, int64_t N, const int32_t* col_
     QNMT_CUDA(cudaMemsetAsync(maxbits, 0, sizeof(uint32_t) * (size_t)N, st));
     dim3 g1((unsigned)cdiv(max_len, ATT_PC), (unsigned)N);
     if (vec)
-        k_att_max<true><<<g1, ATT_T, 0, st>>>(u, ldu, col_sent, att_proj, sent_row, sent_len, A, maxbits, err_flag);
+        k_att_max<true><<<g1, ATT_T, 0, st>>>(u, ldu, col_sent, att_proj, sent_row, sent_len, A, maxbits, err_flag, tl_ndev);
     else
-        k_att_max<false><<<g1, ATT_T, 0, st>>>(u, ldu, col_sent, att_proj, sent_row, sent_len, A, maxbits, err_flag);
+        k_att_max<false><<<g1, ATT_T, 0, st>>>(u, ldu, col_sent, att_proj, sent_row, sent_len, A, maxbits, err_flag, tl_ndev);
     QNMT_CHECK_LAUNCH("k_att_max");
     if (vec)
         k_att_score<true><<<g1, ATT_T, 0, st>>>(u, ldu, col_sent, att_proj, sent_row, sent_len, A, v_codes,
-                                               v_scale, maxbits, scores, max_len);
+                                               v_scale, maxbits, scores, max_len, tl_ndev);
     else
         k_att_score<false><<<g1, ATT_T, 0, st>>>(u, ldu, col_sent, att_proj, sent_row, sent_len, A, v_codes,
-                                                v_scale, maxbits, scores, max_len);
+                                                v_scale, maxbits, scores, max_len, tl_ndev);
     QNMT_CHECK_LAUNCH("k_att_score");
     int64_t gx = cdiv(H2, 256);
     size_t smem = (size_t)max_len * (sizeof(double) + sizeof(float));
@@ -203,7 +207,7 @@ int attention_launch(const float* u, int64_t ldu, int64_t N, const int32_t* col_
         QNMT_CUDA(cudaFuncSetAttribute(k_att_context, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     }
     k_att_context<<<dim3((unsigned)gx, (unsigned)N), 256, smem, st>>>(
-        scores, max_len, col_sent, states, sent_row, sent_len, H2, ctx, ldc, alpha, lda, err_flag);
+        scores, max_len, col_sent, states, sent_row, sent_len, H2, ctx, ldc, alpha, lda, err_flag, tl_ndev);
     QNMT_CHECK_LAUNCH("k_att_context");
     return QNMT_OK;
 }

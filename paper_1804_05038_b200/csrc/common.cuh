@@ -21,6 +21,16 @@ void set_error(const char* fmt, ...);
 int cuda_status(cudaError_t e, const char* where);
 void count_launch();
 
+// Device-resident column count for graph-captured decode steps: when set, the
+// launch helpers size grids for the host-side maximum and every kernel reads
+// the live count from *tl_ndev (blocks beyond it exit immediately).
+extern thread_local const int32_t* tl_ndev;
+struct NdevScope {
+    const int32_t* old;
+    explicit NdevScope(const int32_t* p) : old(tl_ndev) { tl_ndev = p; }
+    ~NdevScope() { tl_ndev = old; }
+};
+
 #define QNMT_CHECK_LAUNCH(where)                                              \
     do {                                                                      \
         ::qnmt::count_launch();                                               \
@@ -57,6 +67,10 @@ __device__ __forceinline__ float sigmoid_b(float x) {
         r = e / (1.0 + e);
     }
     return __double2float_rn(r);
+}
+
+__device__ __forceinline__ bool beyond(const int32_t* n_dev, int64_t i) {
+    return n_dev != nullptr && i >= (int64_t)*n_dev;
 }
 
 __device__ __forceinline__ bool is_finite_f(float x) {
@@ -98,6 +112,16 @@ __device__ __forceinline__ float dequant_rcp(long long acc, double rcp, float sa
     if (acc == 0) return 0.0f;
     if (safe) return __double2float_rn(q);
     return dequant(acc, sa, sb);
+}
+
+// Predicate of dequant_rcp's fast path for q = acc * rcp: zero, or a normal-range
+// value whose bits are more than 64 f64-ulps away from an f32 rounding midpoint.
+__device__ __forceinline__ bool dequant_rcp_safe(double q) {
+    unsigned long long b = (unsigned long long)__double_as_longlong(q);
+    int low = (int)(b & 0x1fffffffull);
+    int ex = (int)((b >> 52) & 0x7ff);
+    int d = low - 0x10000000;
+    return ((b << 1) == 0ull) || ((d > 64 || d < -64) && ex > 1023 - 125 && ex < 1023 + 127);
 }
 
 __device__ __forceinline__ void set_flag(int32_t* flag, int bit) {

@@ -15,8 +15,9 @@ namespace qnmt {
 __global__ void k_gru_gates(const float* __restrict__ gx, int64_t ldgx, const int32_t* __restrict__ gx_row,
                             const float* __restrict__ gh, int64_t ldgh, const float* __restrict__ h,
                             int64_t ldh, int64_t N, int64_t H, float* __restrict__ z,
-                            float* __restrict__ rh, int32_t* err_flag) {
+                            float* __restrict__ rh, int32_t* err_flag, const int32_t* n_dev) {
     int64_t n = blockIdx.y;
+    if (beyond(n_dev, n)) return;
     int64_t rowx = gx_row ? gx_row[n] : n;
     const float* gxr = gx + rowx * ldgx;
     const float* ghr = gh + n * ldgh;
@@ -37,8 +38,10 @@ __global__ void k_gru_combine(const float* __restrict__ gx, int64_t ldgx, const 
                               const float* __restrict__ ghc, int64_t ldghc, const float* __restrict__ z,
                               const float* __restrict__ h, int64_t ldh, int64_t N, int64_t H,
                               float* __restrict__ h_out, int64_t ldo, float* __restrict__ out2,
-                              int64_t ld2, const int32_t* __restrict__ out2_row, int32_t* err_flag) {
+                              int64_t ld2, const int32_t* __restrict__ out2_row, int32_t* err_flag,
+                              const int32_t* n_dev) {
     int64_t n = blockIdx.y;
+    if (beyond(n_dev, n)) return;
     int64_t rowx = gx_row ? gx_row[n] : n;
     const float* gxr = gx + rowx * ldgx + 2 * H;
     bool bad = false;
@@ -56,8 +59,9 @@ __global__ void k_gru_combine(const float* __restrict__ gx, int64_t ldgx, const 
 }
 
 __global__ void k_tanh(const float* __restrict__ x, int64_t N, int64_t D, int64_t ldx,
-                       float* __restrict__ y, int64_t ldy, int32_t* err_flag) {
+                       float* __restrict__ y, int64_t ldy, int32_t* err_flag, const int32_t* n_dev) {
     int64_t n = blockIdx.y;
+    if (beyond(n_dev, n)) return;
     bool bad = false;
     for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < D; j += (int64_t)gridDim.x * blockDim.x) {
         float v = x[n * ldx + j];
@@ -69,8 +73,9 @@ __global__ void k_tanh(const float* __restrict__ x, int64_t N, int64_t D, int64_
 
 __global__ void k_embed_gather(const float* __restrict__ table, int64_t rows, int64_t E,
                                const int32_t* __restrict__ ids, float* __restrict__ out,
-                               int64_t ldo, int32_t* err_flag) {
+                               int64_t ldo, int32_t* err_flag, const int32_t* n_dev) {
     int64_t n = blockIdx.x;
+    if (beyond(n_dev, n)) return;
     int32_t id = ids[n];
     bool ok = id >= 0 && id < rows;
     if (!ok && threadIdx.x == 0) set_flag(err_flag, QNMT_FLAG_VOCAB);
@@ -88,7 +93,7 @@ int gru_gates_launch(const float* gx, int64_t ldgx, const int32_t* gx_row, const
                      int64_t ldgh, const float* h, int64_t ldh, int64_t N, int64_t H, float* z,
                      float* rh, int32_t* err_flag, cudaStream_t st) {
     if (N <= 0) return QNMT_OK;
-    k_gru_gates<<<rows_grid(N, H, 256), 256, 0, st>>>(gx, ldgx, gx_row, gh, ldgh, h, ldh, N, H, z, rh, err_flag);
+    k_gru_gates<<<rows_grid(N, H, 256), 256, 0, st>>>(gx, ldgx, gx_row, gh, ldgh, h, ldh, N, H, z, rh, err_flag, tl_ndev);
     QNMT_CHECK_LAUNCH("k_gru_gates");
     return QNMT_OK;
 }
@@ -99,7 +104,7 @@ int gru_combine_launch(const float* gx, int64_t ldgx, const int32_t* gx_row, con
                        const int32_t* out2_row, int32_t* err_flag, cudaStream_t st) {
     if (N <= 0) return QNMT_OK;
     k_gru_combine<<<rows_grid(N, H, 256), 256, 0, st>>>(gx, ldgx, gx_row, ghc, ldghc, z, h, ldh, N, H,
-                                                        h_out, ldo, out2, ld2, out2_row, err_flag);
+                                                        h_out, ldo, out2, ld2, out2_row, err_flag, tl_ndev);
     QNMT_CHECK_LAUNCH("k_gru_combine");
     return QNMT_OK;
 }
@@ -107,7 +112,7 @@ int gru_combine_launch(const float* gx, int64_t ldgx, const int32_t* gx_row, con
 int tanh_launch(const float* x, int64_t N, int64_t D, int64_t ldx, float* y, int64_t ldy,
                 int32_t* err_flag, cudaStream_t st) {
     if (N <= 0) return QNMT_OK;
-    k_tanh<<<rows_grid(N, D, 256), 256, 0, st>>>(x, N, D, ldx, y, ldy, err_flag);
+    k_tanh<<<rows_grid(N, D, 256), 256, 0, st>>>(x, N, D, ldx, y, ldy, err_flag, tl_ndev);
     QNMT_CHECK_LAUNCH("k_tanh");
     return QNMT_OK;
 }
@@ -115,7 +120,7 @@ int tanh_launch(const float* x, int64_t N, int64_t D, int64_t ldx, float* y, int
 int embed_gather_launch(const float* table, int64_t rows, int64_t E, const int32_t* ids, int64_t n,
                         float* out, int64_t ldo, int32_t* err_flag, cudaStream_t st) {
     if (n <= 0) return QNMT_OK;
-    k_embed_gather<<<(unsigned)n, 128, 0, st>>>(table, rows, E, ids, out, ldo, err_flag);
+    k_embed_gather<<<(unsigned)n, 128, 0, st>>>(table, rows, E, ids, out, ldo, err_flag, tl_ndev);
     QNMT_CHECK_LAUNCH("k_embed_gather");
     return QNMT_OK;
 }

@@ -177,9 +177,66 @@ struct qnmt_engine {
     int32_t* h_pinned = nullptr;   // host pinned scalar
     int last_n = 0, last_tmax = 0;
     int64_t d2h_bytes = 0;
+    // phase profiler (CUDA events on the engine stream; off by default)
+    bool prof_on = false;
+    int prof_group = -1;
+    cudaEvent_t prof_start = nullptr;
+    std::vector<cudaEvent_t> ev_pool, ev_used;
+    std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev_open;
+    double prof_ms[16] = {}, prof_calls[16] = {}, prof_ops[16] = {}, prof_bytes[16] = {};
+    // graph-captured decode steps (device-side live count and step counter)
+    bool use_graphs = true;
+    int32_t* d_N = nullptr;      // [2] live columns, ping-pong
+    int32_t* d_step = nullptr;
+    cudaStream_t cap_stream = nullptr;
+    std::vector<std::pair<std::pair<int, int>, std::pair<cudaGraphExec_t, cudaGraphExec_t>>> graphs;
 };
 
 namespace qnmt {
+
+enum { PG_ENCODER = 0, PG_EMBED, PG_QUANT, PG_GEMM, PG_GRU, PG_ATT, PG_GEMM_VOCAB, PG_TOPK, PG_SEARCH,
+       PG_GATHER, PG_MISC, PG_COUNT };
+
+static cudaEvent_t prof_event(qnmt_engine* e) {
+    cudaEvent_t ev;
+    if (!e->ev_pool.empty()) {
+        ev = e->ev_pool.back();
+        e->ev_pool.pop_back();
+    } else {
+        cudaEventCreate(&ev);
+    }
+    e->ev_used.push_back(ev);
+    return ev;
+}
+
+// close the open region (if any) and open one for group g (g < 0: just close)
+static void prof_mark(qnmt_engine* e, int g, cudaStream_t st, double ops = 0, double bytes = 0) {
+    if (!e->prof_on) return;
+    cudaEvent_t ev = prof_event(e);
+    cudaEventRecord(ev, st);
+    if (e->prof_group >= 0) e->ev_open.push_back({e->prof_group, {e->prof_start, ev}});
+    e->prof_group = g;
+    e->prof_start = ev;
+    if (g >= 0) {
+        e->prof_calls[g] += 1;
+        e->prof_ops[g] += ops;
+        e->prof_bytes[g] += bytes;
+    }
+}
+
+// after a stream sync: fold finished regions into the totals and recycle events
+static void prof_collect(qnmt_engine* e) {
+    if (!e->prof_on) return;
+    for (auto& r : e->ev_open) {
+        float ms = 0.f;
+        if (cudaEventElapsedTime(&ms, r.second.first, r.second.second) == cudaSuccess) e->prof_ms[r.first] += ms;
+    }
+    e->ev_open.clear();
+    for (auto ev : e->ev_used)
+        if (ev != e->prof_start) e->ev_pool.push_back(ev);
+    e->ev_used.clear();
+    if (e->prof_group >= 0) e->ev_used.push_back(e->prof_start);
+}
 
 static int check_flag(qnmt_engine* e, cudaStream_t st) {
     int32_t f = 0;
@@ -322,11 +379,16 @@ static int gru_cell(qnmt_engine* e, const Cell& c, int64_t N, int nseg, const in
                     const int8_t* qx, const float* sx, const int8_t* qh, const float* sh,
                     const float* h, float* h_out, cudaStream_t st) {
     const int64_t H = e->m->H;
+    prof_mark(e, PG_GEMM, st, 2.0 * N * (3 * H * c.in + 2 * H * H), 3.0 * H * c.in + 2.0 * H * H);
     TRY(gemm(c.wx, 3 * H, c.in, c.wx_s, H, qx, N, c.in, sx, seg, c.bx, e->gx, 3 * H, 0, st));
     TRY(gemm(c.uzr, 2 * H, H, c.uzr_s, H, qh, N, H, sh, seg, nullptr, e->gh, 2 * H, 0, st));
+    prof_mark(e, PG_GRU, st);
     TRY(gru_gates_launch(e->gx, 3 * H, nullptr, e->gh, 2 * H, h, H, N, H, e->z, e->rh, e->err, st));
+    prof_mark(e, PG_QUANT, st);
     TRY(quantize_launch(e->rh, N, H, H, seg, nseg, e->q_rh, H, e->sc_rh, e->seg_bits, 1, e->err, st));
+    prof_mark(e, PG_GEMM, st, 2.0 * N * H * H, (double)H * H);
     TRY(gemm(c.uc, H, H, c.uc_s, H, e->q_rh, N, H, e->sc_rh, seg, nullptr, e->ghc, H, 0, st));
+    prof_mark(e, PG_GRU, st);
     TRY(gru_combine_launch(e->gx, 3 * H, nullptr, e->ghc, H, e->z, h, H, N, H, h_out, H, nullptr, 0,
                            nullptr, e->err, st));
     return QNMT_OK;
@@ -338,18 +400,24 @@ static int step_core(qnmt_engine* e, const StepIO& io, cudaStream_t st) {
     const int32_t* seg = io.col_sent;
     const int ns = io.nseg;
     if (N <= 0) return QNMT_OK;
+    prof_mark(e, PG_EMBED, st);
     TRY(embed_gather_launch(m->tgt_embed, V, E, io.y, N, e->emb, E, e->err, st));
+    prof_mark(e, PG_QUANT, st);
     TRY(quantize_launch(e->emb, N, E, E, seg, ns, e->q_emb, E, e->sc_emb, e->seg_bits, 1, e->err, st));
     TRY(quantize_launch(io.s, N, H, H, seg, ns, e->q_s, H, e->sc_s, e->seg_bits, 1, e->err, st));
     // s' = GRU_r(emb, s)                                        (layers.py:372)
     TRY(gru_cell(e, m->cell[2], N, ns, seg, e->q_emb, e->sc_emb, e->q_s, e->sc_s, io.s, io.s_int, st));
     // attention query (layers.py:373)
     const float* query = (m->aq == 1) ? io.sp : io.s_int;
+    prof_mark(e, PG_QUANT, st);
     TRY(quantize_launch(query, N, H, H, seg, ns, e->q_q, H, e->sc_q, e->seg_bits, 1, e->err, st));
+    prof_mark(e, PG_GEMM, st, 2.0 * N * A * H, (double)A * H);
     TRY(gemm(m->u_att, A, H, m->u_att_s, A, e->q_q, N, H, e->sc_q, seg, nullptr, e->u, A, 0, st));
+    prof_mark(e, PG_ATT, st);
     TRY(attention_launch(e->u, A, N, seg, io.att_proj, io.states, io.sent_row, io.sent_len, io.max_len,
                          A, 2 * H, m->v, m->v_s, e->ctx, 2 * H, io.alpha, io.lda, e->att_scratch,
                          e->err, st));
+    prof_mark(e, PG_QUANT, st);
     TRY(quantize_launch(e->ctx, N, 2 * H, 2 * H, seg, ns, e->q_ctx, 2 * H, e->sc_ctx, e->seg_bits, 1,
                         e->err, st));
     // s = GRU_q(ctx, s')                                        (layers.py:375)
@@ -362,14 +430,19 @@ static int step_core(qnmt_engine* e, const StepIO& io, cudaStream_t st) {
     }
     TRY(gru_cell(e, m->cell[3], N, ns, seg, e->q_ctx, e->sc_ctx, q_si, sc_si, io.s_int, io.s_new, st));
     // readout = tanh(((W_s s + b_r) + W_e emb) + W_c ctx)       (layers.py:255-265)
+    prof_mark(e, PG_QUANT, st);
     TRY(quantize_launch(io.s_new, N, H, H, seg, ns, e->q_sn, H, e->sc_sn, e->seg_bits, 1, e->err, st));
+    prof_mark(e, PG_GEMM, st, 2.0 * N * R * (H + E + 2 * H), (double)R * (H + E + 2 * H));
     TRY(gemm(m->w_state, R, H, m->w_state_s, R, e->q_sn, N, H, e->sc_sn, seg, m->b_r, e->ro, R, 0, st));
     TRY(gemm(m->w_embed, R, E, m->w_embed_s, R, e->q_emb, N, E, e->sc_emb, seg, nullptr, e->ro, R,
              QNMT_GEMM_ACCUMULATE, st));
     TRY(gemm(m->w_ctx, R, 2 * H, m->w_ctx_s, R, e->q_ctx, N, 2 * H, e->sc_ctx, seg, nullptr, e->ro, R,
              QNMT_GEMM_ACCUMULATE, st));
+    prof_mark(e, PG_MISC, st);
     TRY(tanh_launch(e->ro, N, R, R, e->ro, R, e->err, st));
+    prof_mark(e, PG_QUANT, st);
     TRY(quantize_launch(e->ro, N, R, R, seg, ns, e->q_ro, R, e->sc_ro, e->seg_bits, 1, e->err, st));
+    prof_mark(e, PG_GEMM_VOCAB, st, 2.0 * N * V * R, (double)V * R + (double)N * R + 4.0 * N * V);
     TRY(gemm(m->w_vocab, V, R, m->w_vocab_s, V, e->q_ro, N, R, e->sc_ro, seg, m->b_vocab, io.logits, V,
              0, st));
     return QNMT_OK;
@@ -377,6 +450,12 @@ static int step_core(qnmt_engine* e, const StepIO& io, cudaStream_t st) {
 
 static int grow_history(qnmt_engine* e, int steps) {
     if (steps <= e->hist_steps) return QNMT_OK;
+    // captured step graphs point into the old history block
+    for (auto& kv : e->graphs) {
+        cudaGraphExecDestroy(kv.second.first);
+        cudaGraphExecDestroy(kv.second.second);
+    }
+    e->graphs.clear();
     if (e->hblock) cudaFree(e->hblock);
     size_t S = e->S, B = e->B, T = steps;
     size_t fin_cap = (T + 1) * B;
@@ -529,6 +608,8 @@ int qnmt_engine_create(const qnmt_model* m, int32_t max_sentences, int32_t max_s
         e->cand_score = a.take<double>(N * B);
         e->cand_tok = a.take<int32_t>(N * B);
         e->n_live = a.take<int32_t>(4);
+        e->d_N = a.take<int32_t>(4);
+        e->d_step = a.take<int32_t>(4);
         e->P = a.take<int32_t>(S);
         e->col_off = a.take<int32_t>(S);
         e->done = a.take<int32_t>(S);
@@ -550,6 +631,7 @@ int qnmt_engine_create(const qnmt_model* m, int32_t max_sentences, int32_t max_s
     cudaMemcpy(e->even, ev.data(), S * 4, cudaMemcpyHostToDevice);
     cudaMemcpy(e->odd, od.data(), S * 4, cudaMemcpyHostToDevice);
     cudaMemset(e->err, 0, 16);
+    cudaStreamCreateWithFlags(&e->cap_stream, cudaStreamNonBlocking);
     cudaError_t ce = cudaMallocHost(&e->h_pinned, 64);
     if (ce != cudaSuccess) { cudaFree(e->block); delete e; return cuda_status(ce, "cudaMallocHost"); }
     *out = e;
@@ -562,8 +644,38 @@ int qnmt_engine_destroy(qnmt_engine* e) {
     if (e->block) cudaFree(e->block);
     if (e->hblock) cudaFree(e->hblock);
     if (e->h_pinned) cudaFreeHost(e->h_pinned);
+    for (auto& kv : e->graphs) {
+        cudaGraphExecDestroy(kv.second.first);
+        cudaGraphExecDestroy(kv.second.second);
+    }
+    if (e->cap_stream) cudaStreamDestroy(e->cap_stream);
     delete e;
     return QNMT_OK;
+}
+
+int qnmt_engine_set_graphs(qnmt_engine* e, int enable) {
+    int old = e->use_graphs ? 1 : 0;
+    e->use_graphs = enable != 0;
+    return old;
+}
+
+int qnmt_engine_profile(qnmt_engine* e, int enable) {
+    cudaDeviceSynchronize();
+    prof_collect(e);
+    e->prof_on = enable != 0;
+    e->prof_group = -1;
+    for (int i = 0; i < 16; ++i) e->prof_ms[i] = e->prof_calls[i] = e->prof_ops[i] = e->prof_bytes[i] = 0;
+    return QNMT_OK;
+}
+
+int qnmt_engine_profile_read(const qnmt_engine* e, double* ms, double* calls, double* ops, double* bytes) {
+    for (int i = 0; i < 16; ++i) {
+        ms[i] = e->prof_ms[i];
+        calls[i] = e->prof_calls[i];
+        ops[i] = e->prof_ops[i];
+        bytes[i] = e->prof_bytes[i];
+    }
+    return PG_COUNT;
 }
 
 size_t qnmt_engine_bytes(const qnmt_engine* e) { return e ? e->block_bytes + e->hblock_bytes : 0; }
@@ -592,6 +704,81 @@ int qnmt_decoder_step(qnmt_engine* e, int64_t N, const int32_t* col_sent, int32_
               s_int, s_new, logits, alpha, lda};
     TRY(step_core(e, io, st));
     return check_flag(e, st);
+}
+
+// ---------------------------------------------------------------------------
+// CUDA-graph decode step.  Every kernel of a step reads the live column count
+// from d_N[cur] (grids are sized for n*beam); the search kernel writes
+// d_N[cur^1] and advances d_step.  Two graphs (cur = 0, 1) cover the
+// ping-pong state buffers; they are captured once per (n_sent, beam).
+// ---------------------------------------------------------------------------
+static bool graph_eligible(const qnmt_engine* e) {
+    const qnmt_model* m = e->m;
+    return e->use_graphs && !e->prof_on && g_gemm_impl != 1 && m->E % 16 == 0 && m->H % 16 == 0 &&
+           m->A % 16 == 0 && m->R % 16 == 0;
+}
+
+static int capture_step(qnmt_engine* e, int cur, int n, int beam, int k_list, cudaGraphExec_t* out) {
+    const qnmt_model* m = e->m;
+    const int64_t H = m->H, V = m->Vt;
+    const int64_t NM = (int64_t)n * beam;
+    cudaStream_t cs = e->cap_stream;
+    QNMT_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeRelaxed));
+    int rc = QNMT_OK;
+    {
+        NdevScope nd(e->d_N + cur);
+        StepIO io{NM, n, e->col_sent[cur], e->y[cur], e->st_s[cur], e->st_sp[cur], e->enc_states, e->enc_att,
+                  e->sent_row, e->sent_len, e->L, e->s_int, e->s_new, e->logits, nullptr, 0};
+        rc = step_core(e, io, cs);
+        if (rc == QNMT_OK)
+            rc = topk_launch(e->logits, NM, V, V, e->live[cur], k_list, e->cand_score, e->cand_tok, e->err, cs);
+        if (rc == QNMT_OK) {
+            SearchState ss{e->P, e->col_off, e->done, e->max_steps, e->steps_run, e->fin_cnt, e->fin_best,
+                           e->fin_score, e->fin_step, e->fin_slot, e->fin_eos, e->hist_tok, e->hist_par,
+                           (e->hist_steps + 1) * e->B, e->hist_steps, e->B, e->cand_score, e->cand_tok,
+                           e->col_sent[cur ^ 1], e->parent_col, e->y[cur ^ 1], e->live[cur ^ 1],
+                           e->d_N + (cur ^ 1), e->d_step};
+            rc = search_step_launch(ss, 0, n, beam, k_list, cs);
+        }
+    }
+    if (rc == QNMT_OK) {
+        NdevScope nd(e->d_N + (cur ^ 1));
+        rc = gather_rows_launch(e->s_new, e->s_int, e->parent_col, NM, H, e->st_s[cur ^ 1], e->st_sp[cur ^ 1], cs);
+    }
+    cudaGraph_t g = nullptr;
+    cudaError_t ce = cudaStreamEndCapture(cs, &g);
+    if (rc != QNMT_OK) {
+        if (g) cudaGraphDestroy(g);
+        return rc;
+    }
+    if (ce != cudaSuccess) return cuda_status(ce, "cudaStreamEndCapture");
+    ce = cudaGraphInstantiate(out, g, 0);
+    cudaGraphDestroy(g);
+    if (ce != cudaSuccess) return cuda_status(ce, "cudaGraphInstantiate");
+    return QNMT_OK;
+}
+
+static int get_step_graphs(qnmt_engine* e, int n, int beam, int k_list, cudaGraphExec_t* g) {
+    // history buffers may have been re-allocated: graphs are keyed on the history capacity too
+    const int key2 = beam * 100000 + e->hist_steps;
+    for (auto& kv : e->graphs)
+        if (kv.first.first == n && kv.first.second == key2) {
+            g[0] = kv.second.first;
+            g[1] = kv.second.second;
+            return QNMT_OK;
+        }
+    TRY(capture_step(e, 0, n, beam, k_list, &g[0]));
+    TRY(capture_step(e, 1, n, beam, k_list, &g[1]));
+    e->graphs.push_back({{n, key2}, {g[0], g[1]}});
+    return QNMT_OK;
+}
+
+static void drop_graphs(qnmt_engine* e) {
+    for (auto& kv : e->graphs) {
+        cudaGraphExecDestroy(kv.second.first);
+        cudaGraphExecDestroy(kv.second.second);
+    }
+    e->graphs.clear();
 }
 
 // device-resident decode of one batch; results stay in the engine until finalize.
@@ -623,7 +810,9 @@ static int decode_core(qnmt_engine* e, const int32_t* src_ids, bool ids_on_devic
     QNMT_CUDA(cudaMemsetAsync(e->err, 0, 4, st));
     QNMT_CUDA(cudaMemcpyAsync(e->src_ids, src_ids, (size_t)P * 4,
                               ids_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
+    prof_mark(e, PG_ENCODER, st);
     TRY(encode_core(e, e->src_ids, src_len, row.data(), n, e->enc_states, e->enc_att, e->enc_s0, st));
+    prof_mark(e, PG_MISC, st);
     // decoder init: one column per sentence, s = s' = s0, y = EOS (BOS), live score 0 (decoder.py:105-110)
     std::vector<int32_t> iota_n(n), y0(n, 2), ones(n, 1);
     std::iota(iota_n.begin(), iota_n.end(), 0);
@@ -642,13 +831,34 @@ static int decode_core(qnmt_engine* e, const int32_t* src_ids, bool ids_on_devic
     QNMT_CUDA(cudaMemcpyAsync(e->st_s[0], e->enc_s0, (size_t)n * H * 4, cudaMemcpyDeviceToDevice, st));
     QNMT_CUDA(cudaMemcpyAsync(e->st_sp[0], e->enc_s0, (size_t)n * H * 4, cudaMemcpyDeviceToDevice, st));
     const int k_list = (int)std::min<int64_t>(beam, V);
+    if (graph_eligible(e)) {
+        // device-resident loop: one graph launch per step, live count polled every POLL steps
+        cudaGraphExec_t g[2];
+        TRY(get_step_graphs(e, n, beam, k_list, g));
+        e->h_pinned[1] = n;
+        QNMT_CUDA(cudaMemcpyAsync(e->d_N, e->h_pinned + 1, 4, cudaMemcpyHostToDevice, st));
+        QNMT_CUDA(cudaMemsetAsync(e->d_step, 0, 4, st));
+        constexpr int POLL = 16;
+        for (int t = 0; t < Tmax; ++t) {
+            QNMT_CUDA(cudaGraphLaunch(g[t & 1], st));
+            count_launch();
+            if ((t + 1) % POLL == 0 && t + 1 < Tmax) {
+                QNMT_CUDA(cudaMemcpyAsync(e->h_pinned, e->d_N + ((t + 1) & 1), 4, cudaMemcpyDeviceToHost, st));
+                QNMT_CUDA(cudaStreamSynchronize(st));
+                if (e->h_pinned[0] == 0) break;
+            }
+        }
+        return check_flag(e, st);
+    }
     int64_t N = n;
     int cur = 0;
     for (int t = 0; t < Tmax && N > 0; ++t) {
         StepIO io{N, n, e->col_sent[cur], e->y[cur], e->st_s[cur], e->st_sp[cur], e->enc_states,
                   e->enc_att, e->sent_row, e->sent_len, Lmax, e->s_int, e->s_new, e->logits, nullptr, 0};
         TRY(step_core(e, io, st));
+        prof_mark(e, PG_TOPK, st, 0, 4.0 * N * V);
         TRY(topk_launch(e->logits, N, V, V, e->live[cur], k_list, e->cand_score, e->cand_tok, e->err, st));
+        prof_mark(e, PG_SEARCH, st);
         SearchState ss{e->P, e->col_off, e->done, e->max_steps, e->steps_run, e->fin_cnt, e->fin_best,
                        e->fin_score, e->fin_step, e->fin_slot, e->fin_eos, e->hist_tok, e->hist_par,
                        (e->hist_steps + 1) * e->B, e->hist_steps, e->B,
@@ -657,12 +867,17 @@ static int decode_core(qnmt_engine* e, const int32_t* src_ids, bool ids_on_devic
         TRY(search_step_launch(ss, t, n, beam, k_list, st));
         QNMT_CUDA(cudaMemcpyAsync(e->h_pinned, e->n_live, 4, cudaMemcpyDeviceToHost, st));
         QNMT_CUDA(cudaStreamSynchronize(st));
+        prof_collect(e);
         int64_t N2 = e->h_pinned[0];
+        prof_mark(e, PG_GATHER, st);
         TRY(gather_rows_launch(e->s_new, e->s_int, e->parent_col, N2, H, e->st_s[cur ^ 1], e->st_sp[cur ^ 1], st));
         N = N2;
         cur ^= 1;
     }
-    return check_flag(e, st);
+    prof_mark(e, -1, st);
+    int rc = check_flag(e, st);
+    prof_collect(e);
+    return rc;
 }
 
 // D2H of the finished lists + history, then min by (-logp, tokens) (decoder.py:157-160)

@@ -212,6 +212,10 @@ int g_gemm_impl = 0;
 
 int gemm_i8_launch(const GemmArgs& g, cudaStream_t st) {
     if (g.M <= 0 || g.N <= 0) return QNMT_OK;
+    if (tl_ndev) {   // graph-captured step: device-side N, only the tcgen05 kernel supports it
+        if (!tc_eligible(g)) { set_error("graph mode needs tcgen05-eligible GEMM shapes"); return QNMT_ERR_CONFIG; }
+        return gemm_tc_launch(g, st);
+    }
     if (g_gemm_impl != 1 && tc_eligible(g) && (g.N > 8 || g_gemm_impl == 2)) return gemm_tc_launch(g, st);
     EpiArgs e{g.w_scales, g.w_rows_per_scale, g.x_scales, g.col_seg, g.bias, g.Y, g.ldy,
               g.acc_out, g.M, g.flags};

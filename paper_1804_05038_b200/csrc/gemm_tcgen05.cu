@@ -53,11 +53,14 @@ struct TcEpi {
     int32_t flags;
 };
 
-template <int BN>
+enum { EPI_BIAS = 1, EPI_ACCUMULATE = 2, EPI_RAW = 4 };
+
+template <int BN, int EPI>
 __global__ void __launch_bounds__(TC_THREADS, 1)
 k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N, int K,
-          TcEpi e) {
+          TcEpi e, const int32_t* n_dev) {
     using C = TcCfg<BN>;
+    if (n_dev) N = min(N, *n_dev);   // graph mode: live columns from the device
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* smem = (unsigned char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
@@ -65,6 +68,8 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
     uint64_t* tfull = empty + C::STAGES;    // [2]
     uint64_t* tempty = tfull + 2;           // [2]
     uint32_t* tmem_base_smem = reinterpret_cast<uint32_t*>(tempty + 2);
+    __shared__ float col_sx[2][256];      // per-column activation scale (double-buffered by tile)
+    __shared__ double col_isx[2][256];    // and its f64 reciprocal
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -151,49 +156,81 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
             const int mb = tile / n_blocks, nb = tile % n_blocks;
             const int buf = it & 1;
             const uint32_t use = (uint32_t)(it >> 1) & 1u;
-            tc::mbar_wait(&tfull[buf], use);
-            tc::tc_fence_after();
+            // Column scales of this tile -> smem (x scale and its f64 reciprocal), row scale and
+            // bias -> registers; all loads are issued before waiting for the accumulator.
+            {
+                const int c = ew * 32 + lane;    // 8 warps x 32 lanes cover BN <= 256 columns
+                if (c < BN) {
+                    const int n = nb * BN + c;
+                    float sx = 1.0f;
+                    if (n < N) sx = e.x_scales[e.col_seg ? e.col_seg[n] : 0];
+                    col_sx[buf][c] = sx;
+                    col_isx[buf][c] = 1.0 / (double)sx;
+                }
+            }
             const int m = mb * TC_BM + lg * 32 + lane;
             const bool mok = m < M;
             float sw = 1.0f, bias = 0.0f;
-            double isw = 1.0;
             if (mok) {
                 sw = e.w_scales[m / e.w_rows_per_scale];
-                isw = 1.0 / (double)sw;
                 if (e.bias) bias = e.bias[m];
             }
+            const double isw = 1.0 / (double)sw;
+            asm volatile("bar.sync 1, %0;" ::"n"(32 * TC_EPI_WARPS));   // epilogue warps only
+            tc::mbar_wait(&tfull[buf], use);
+            tc::tc_fence_after();
 #pragma unroll 1
             for (int c0 = half * COLS; c0 < (half + 1) * COLS; c0 += 16) {
                 uint32_t r[16];
-                tc::tmem_ld16(tmem_base + ((uint32_t)(lg * 32) << 16) + (uint32_t)(buf * BN + c0), r);
-                tc::tmem_ld_wait();
+                const uint32_t ta = tmem_base + ((uint32_t)(lg * 32) << 16) + (uint32_t)(buf * BN + c0);
+                tc::tmem_ld16(ta, r);
                 const int nbase = nb * BN + c0;
-                // per-column activation scale and its reciprocal, one column per lane (lanes 0..15)
-                float sxl = 1.0f;
-                double isxl = 1.0;
-                {
-                    int n = nbase + (lane & 15);
-                    if (n < N) {
-                        sxl = e.x_scales[e.col_seg ? e.col_seg[n] : 0];
-                        isxl = 1.0 / (double)sxl;
-                    }
+                const int ncols = min(16, N - nbase);          // warp-uniform
+                if (ncols <= 0) {
+                    tc::tmem_ld_wait();
+                    continue;
+                }
+                float* yrow = e.Y + (int64_t)nbase * e.ldy + m;
+                float yv[16];
+                if (EPI & EPI_ACCUMULATE) {
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) yv[j] = (mok && j < ncols) ? yrow[(int64_t)j * e.ldy] : 0.0f;
+                }
+                tc::tmem_ld_wait();
+                if (EPI & EPI_RAW) {
+#pragma unroll
+                    for (int j = 0; j < 16; ++j)
+                        if (mok && j < ncols) e.acc_out[(int64_t)(nbase + j) * M + m] = (int)r[j];
+                    if (e.Y == nullptr) continue;
+                }
+                // branch-free fast dequant; lanes flag elements near an f32 rounding midpoint
+                uint32_t unsafe = 0;
+                float yd[16];
+#pragma unroll
+                for (int j = 0; j < 16; ++j) {
+                    const double q = (double)(int)r[j] * (isw * col_isx[buf][c0 + j]);
+                    yd[j] = __double2float_rn(q);
+                    unsafe |= (uint32_t)(!dequant_rcp_safe(q)) << j;
+                }
+                if (__any_sync(0xffffffffu, unsafe != 0)) {   // rare: exact division for flagged elements
+#pragma unroll
+                    for (int j = 0; j < 16; ++j)
+                        if ((unsafe >> j) & 1u) yd[j] = dequant((int)r[j], sw, col_sx[buf][c0 + j]);
                 }
 #pragma unroll
                 for (int j = 0; j < 16; ++j) {
-                    const int n = nbase + j;
-                    const float sx = __shfl_sync(0xffffffffu, sxl, j);
-                    const double isx = __shfl_sync(0xffffffffu, isxl, j);
-                    if (mok && n < N) {
-                        const int acc = (int)r[j];
-                        if (e.acc_out) e.acc_out[(int64_t)n * M + m] = acc;
-                        if (e.Y) {
-                            float y = dequant_rcp(acc, isw * isx, sw, sx);
-                            if (e.bias) y = __fadd_rn(y, bias);
-                            float* dst = e.Y + (int64_t)n * e.ldy + m;
-                            if (e.flags & QNMT_GEMM_ACCUMULATE) y = __fadd_rn(*dst, y);
-                            *dst = y;
-                        }
-                    }
+                    float y = yd[j];
+                    if (EPI & EPI_BIAS) y = __fadd_rn(y, bias);
+                    if (EPI & EPI_ACCUMULATE) y = __fadd_rn(yv[j], y);
+                    yd[j] = y;
+                }
+                if (mok && ncols == 16) {
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) yrow[(int64_t)j * e.ldy] = yd[j];
+                } else if (mok) {
+#pragma unroll
+                    for (int j = 0; j < 16; ++j)
+                        if (j < ncols) yrow[(int64_t)j * e.ldy] = yd[j];
                 }
             }
             tc::tc_fence_before();
@@ -281,12 +318,12 @@ static int sm_count() {
     return n;
 }
 
-template <int BN>
+template <int BN, int EPI>
 static int launch_tc(const GemmArgs& g, cudaStream_t st) {
     using C = TcCfg<BN>;
     static bool attr_set = false;
     if (!attr_set) {
-        QNMT_CUDA(cudaFuncSetAttribute(k_gemm_tc<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+        QNMT_CUDA(cudaFuncSetAttribute(k_gemm_tc<BN, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
         attr_set = true;
     }
     CUtensorMap ta, tb;
@@ -297,7 +334,7 @@ static int launch_tc(const GemmArgs& g, cudaStream_t st) {
     TcEpi e{g.w_scales, g.w_rows_per_scale, g.x_scales, g.col_seg, g.bias, g.Y, g.ldy, g.acc_out, g.flags};
     int tiles = (int)(cdiv(g.M, TC_BM) * cdiv(g.N, BN));
     int grid = tiles < sm_count() ? tiles : sm_count();
-    k_gemm_tc<BN><<<grid, TC_THREADS, C::SMEM, st>>>(ta, tb, (int)g.M, (int)g.N, (int)g.K, e);
+    k_gemm_tc<BN, EPI><<<grid, TC_THREADS, C::SMEM, st>>>(ta, tb, (int)g.M, (int)g.N, (int)g.K, e, tl_ndev);
     QNMT_CHECK_LAUNCH("k_gemm_tc");
     return QNMT_OK;
 }
@@ -311,9 +348,19 @@ bool tc_eligible(const GemmArgs& g) {
 int gemm_tc_launch(const GemmArgs& g, cudaStream_t st) {
     const int64_t mb = cdiv(g.M, TC_BM);
     const int sms = sm_count();
-    if (g.N > 128 && mb * cdiv(g.N, 256) >= sms) return launch_tc<256>(g, st);
-    if (g.N > 64 && mb * cdiv(g.N, 128) >= sms / 2) return launch_tc<128>(g, st);
-    return launch_tc<64>(g, st);
+    const int epi = (g.bias ? EPI_BIAS : 0) | ((g.flags & QNMT_GEMM_ACCUMULATE) ? EPI_ACCUMULATE : 0) |
+                    (g.acc_out ? EPI_RAW : 0);
+    const int bn = (g.N > 128 && mb * cdiv(g.N, 256) >= sms) ? 256 : (g.N > 64 && mb * cdiv(g.N, 128) >= sms / 2) ? 128 : 64;
+#define QNMT_TC_CASE(BN_, E_) \
+    if (bn == BN_ && epi == E_) return launch_tc<BN_, E_>(g, st);
+#define QNMT_TC_BN(BN_) \
+    QNMT_TC_CASE(BN_, 0) QNMT_TC_CASE(BN_, 1) QNMT_TC_CASE(BN_, 2) QNMT_TC_CASE(BN_, 3) \
+    QNMT_TC_CASE(BN_, 4) QNMT_TC_CASE(BN_, 5) QNMT_TC_CASE(BN_, 6) QNMT_TC_CASE(BN_, 7)
+    QNMT_TC_BN(256) QNMT_TC_BN(128) QNMT_TC_BN(64)
+#undef QNMT_TC_BN
+#undef QNMT_TC_CASE
+    set_error("gemm_tc: no kernel for bn=%d epi=%d", bn, epi);
+    return QNMT_ERR_CONFIG;
 }
 
 }  // namespace qnmt

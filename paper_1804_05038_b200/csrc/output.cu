@@ -15,6 +15,7 @@
 namespace qnmt {
 
 constexpr int LS_T = 512;
+int g_topk_exact = 0;   // 1: use the three-pass reference kernel (testing)
 
 struct Cand {
     double s;
@@ -175,6 +176,187 @@ k_topk(const float* __restrict__ logits, int64_t V, int64_t ld, const double* __
     }
 }
 
+// exp(t) for t <= 0 in fp64 (~2 ulp): t = k*ln2/16 + r, |r| <= ln2/32,
+// e^r by a degree-7 polynomial (truncation < 1.3e-18), 2^(k/16) = 2^(k>>4) * tab[k&15].
+// The 16-entry f64 table is 128 B = all 32 smem banks, so lookups never
+// conflict.  ~13 f64 ops instead of the general-purpose exp() (~27 DFMA slots).
+__device__ __forceinline__ double exp_neg(double t, const double* __restrict__ tab) {
+    if (t < -700.0) return 0.0;
+    const double kd = rint(t * 23.083120654223414);          // 16 / ln 2
+    const int k = (int)kd;
+    double r = fma(kd, -0.04332169878499658, t);             // ln2/16, rounded to f64
+    r = fma(kd, -1.4494042586539372e-18, r);                 // ln2/16 - the above
+    double p = fma(r, 1.0 / 5040.0, 1.0 / 720.0);
+    p = fma(p, r, 1.0 / 120.0);
+    p = fma(p, r, 1.0 / 24.0);
+    p = fma(p, r, 1.0 / 6.0);
+    p = fma(p, r, 0.5);
+    p = fma(p, r, 1.0);
+    p = fma(p, r, 1.0);
+    double v = p * tab[k & 15];
+    // multiply by 2^(k >> 4) through the exponent field (result stays normal for t >= -700)
+    long long bits = __double_as_longlong(v) + ((long long)(k >> 4) << 52);
+    return __longlong_as_double(bits);
+}
+
+struct LCand {
+    float x;
+    int t;
+};
+__device__ __forceinline__ bool lbetter(const LCand& a, const LCand& b) {
+    return a.x > b.x || (a.x == b.x && a.t < b.t);
+}
+template <int KM>
+__device__ __forceinline__ void linsert(LCand (&L)[KM], LCand c) {
+    if (!lbetter(c, L[KM - 1])) return;
+    L[KM - 1] = c;
+#pragma unroll
+    for (int i = KM - 1; i > 0; --i) {
+        if (lbetter(L[i], L[i - 1])) {
+            LCand t = L[i];
+            L[i] = L[i - 1];
+            L[i - 1] = t;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Single-pass candidates (the production path).
+//
+// One read of the logits row: per thread an online (max, sum exp) in f64 and a
+// top-KM list by (logit desc, token asc).  lp = fl32((x - M) - lse) is monotone
+// non-decreasing in the logit x, so every token outside the KM-list has a
+// score <= the KM-th list entry's score.  After computing exact scores for the
+// KM entries and sorting by (score desc, token asc), the first k are the exact
+// answer whenever the k-th score is STRICTLY greater than the KM-th entry's
+// score (or the list covers the whole vocabulary).  Otherwise (an f32 rounding
+// tie across the boundary -- practically never) the CTA rescans the column
+// exactly with the three-pass method of k_topk.
+// ---------------------------------------------------------------------------
+template <int KM>
+__device__ void block_merge_cands(Cand (&L)[KM], Cand (*wl)[KM], Cand* out, int kk) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    warp_merge<KM>(L, wl[warp], kk);
+    __syncthreads();
+    if (warp == 0) {
+#pragma unroll
+        for (int i = 0; i < KM; ++i) L[i] = (lane < LS_T / 32 && i < kk) ? wl[lane][i] : Cand{-DBL_MAX, 0x7fffffff};
+        __syncwarp();
+        Cand tmp[KM];
+        warp_merge<KM>(L, tmp, kk);
+        if (lane == 0)
+            for (int i = 0; i < kk; ++i) out[i] = tmp[i];
+    }
+    __syncthreads();
+}
+
+template <int KM>
+__global__ void __launch_bounds__(LS_T, 2)
+k_topk1(const float* __restrict__ logits, int64_t V, int64_t ld, const double* __restrict__ live, int k,
+        double* __restrict__ cand_score, int32_t* __restrict__ cand_tok, int32_t* err_flag,
+        const int32_t* n_dev) {
+    __shared__ float redf[32];
+    __shared__ double redd[32];
+    __shared__ Cand wl[LS_T / 32][KM];
+    __shared__ Cand lst[KM];
+    __shared__ int s_ok;
+    const int64_t n = blockIdx.x;
+    if (beyond(n_dev, n)) return;
+    __shared__ double tab[16];
+    if (threadIdx.x < 16) tab[threadIdx.x] = exp2((double)threadIdx.x / 16.0);
+    __syncthreads();
+    const float* row = logits + n * ld;
+    float m = -FLT_MAX;
+    double s = 0.0;
+    bool bad = false;
+    LCand L[KM];
+#pragma unroll
+    for (int i = 0; i < KM; ++i) L[i] = LCand{-FLT_MAX, 0x7fffffff};
+    const bool vec = (V % 4 == 0) && (ld % 4 == 0) && (((uintptr_t)logits & 15) == 0);
+    if (vec) {
+        const float4* r4 = reinterpret_cast<const float4*>(row);
+        for (int64_t q = threadIdx.x; q < V / 4; q += LS_T) {
+            const float4 x = r4[q];
+            const int v = (int)(4 * q);
+            bad |= !(is_finite_f(x.x) && is_finite_f(x.y) && is_finite_f(x.z) && is_finite_f(x.w));
+            const float cm = fmaxf(fmaxf(x.x, x.y), fmaxf(x.z, x.w));
+            if (cm > m) {   // rare after the first chunks: rescale the running sum once
+                s = (m == -FLT_MAX) ? 0.0 : s * exp_neg((double)m - (double)cm, tab);
+                m = cm;
+            }
+            const double dm = (double)m;
+            const double e0 = exp_neg((double)x.x - dm, tab), e1 = exp_neg((double)x.y - dm, tab);
+            const double e2 = exp_neg((double)x.z - dm, tab), e3 = exp_neg((double)x.w - dm, tab);
+            s += (e0 + e1) + (e2 + e3);
+            if (x.x >= L[KM - 1].x) linsert<KM>(L, LCand{x.x, v});
+            if (x.y >= L[KM - 1].x) linsert<KM>(L, LCand{x.y, v + 1});
+            if (x.z >= L[KM - 1].x) linsert<KM>(L, LCand{x.z, v + 2});
+            if (x.w >= L[KM - 1].x) linsert<KM>(L, LCand{x.w, v + 3});
+        }
+    } else {
+        for (int64_t v = threadIdx.x; v < V; v += LS_T) {
+            const float x = row[v];
+            bad |= !is_finite_f(x);
+            if (x > m) {
+                s = (m == -FLT_MAX) ? 0.0 : s * exp_neg((double)m - (double)x, tab);
+                m = x;
+            }
+            s += exp_neg((double)x - (double)m, tab);
+            linsert<KM>(L, LCand{x, (int)v});
+        }
+    }
+    if (__syncthreads_or(bad) && threadIdx.x == 0) set_flag(err_flag, QNMT_FLAG_NUMERIC);
+    const float M = block_max_f(m, redf);
+    const double dM = (double)M;
+    const double S = block_sum_d(m == -FLT_MAX ? 0.0 : s * exp_neg((double)m - dM, tab), redd);
+    const double lse = log(S);
+    const int kk = (int)(V < KM ? V : KM);
+    Cand Lc[KM];
+#pragma unroll
+    for (int i = 0; i < KM; ++i)
+        Lc[i] = L[i].t == 0x7fffffff ? Cand{-DBL_MAX, 0x7fffffff} : Cand{(double)L[i].x, L[i].t};
+    block_merge_cands<KM>(Lc, wl, lst, kk);
+    const double base = live ? live[n] : 0.0;
+    if (threadIdx.x == 0) {
+        // exact scores for the KM logit-candidates, then order by (score desc, token asc)
+        Cand c[KM];
+        for (int i = 0; i < kk; ++i) {
+            float lp = __double2float_rn((lst[i].s - dM) - lse);
+            c[i] = Cand{base + (double)lp, lst[i].t};
+        }
+        const double s_last = c[kk - 1].s;
+        for (int i = 1; i < kk; ++i) {
+            Cand t = c[i];
+            int j = i - 1;
+            while (j >= 0 && better(t, c[j])) { c[j + 1] = c[j]; --j; }
+            c[j + 1] = t;
+        }
+        const bool ok = (V <= KM) || (c[k - 1].s > s_last);
+        if (ok)
+            for (int i = 0; i < k; ++i) {
+                cand_score[n * k + i] = c[i].s;
+                cand_tok[n * k + i] = c[i].t;
+            }
+        s_ok = ok;
+    }
+    __syncthreads();
+    if (s_ok) return;
+    // ---- exact fallback: rescan with final lp values (three-pass method) ----
+    Cand L2[KM];
+#pragma unroll
+    for (int i = 0; i < KM; ++i) L2[i] = Cand{-DBL_MAX, 0x7fffffff};
+    for (int64_t v = threadIdx.x; v < V; v += LS_T) {
+        float lp = __double2float_rn(((double)row[v] - dM) - lse);
+        insert<KM>(L2, Cand{base + (double)lp, (int)v});
+    }
+    block_merge_cands<KM>(L2, wl, lst, k);
+    if (threadIdx.x == 0)
+        for (int i = 0; i < k; ++i) {
+            cand_score[n * k + i] = lst[i].s;
+            cand_tok[n * k + i] = lst[i].t;
+        }
+}
+
 int log_softmax_launch(const float* logits, int64_t N, int64_t V, int64_t ld, float* lp, int64_t ldlp,
                        int32_t* err_flag, cudaStream_t st) {
     if (N <= 0) return QNMT_OK;
@@ -190,13 +372,23 @@ int topk_launch(const float* logits, int64_t N, int64_t V, int64_t ld, const dou
         set_error("qnmt_topk_candidates: k=%d outside [1, min(16, V)]", k);
         return QNMT_ERR_CONFIG;
     }
-    if (k <= 4)
-        k_topk<4><<<(unsigned)N, LS_T, 0, st>>>(logits, V, ld, live, k, cand_score, cand_tok, err_flag);
-    else if (k <= 8)
-        k_topk<8><<<(unsigned)N, LS_T, 0, st>>>(logits, V, ld, live, k, cand_score, cand_tok, err_flag);
+    if (g_topk_exact) {   // reference three-pass kernel (A/B testing)
+        if (k <= 4)
+            k_topk<4><<<(unsigned)N, LS_T, 0, st>>>(logits, V, ld, live, k, cand_score, cand_tok, err_flag);
+        else if (k <= 8)
+            k_topk<8><<<(unsigned)N, LS_T, 0, st>>>(logits, V, ld, live, k, cand_score, cand_tok, err_flag);
+        else
+            k_topk<16><<<(unsigned)N, LS_T, 0, st>>>(logits, V, ld, live, k, cand_score, cand_tok, err_flag);
+        QNMT_CHECK_LAUNCH("k_topk");
+        return QNMT_OK;
+    }
+    if (k <= 6)
+        k_topk1<8><<<(unsigned)N, LS_T, 0, st>>>(logits, V, ld, live, k, cand_score, cand_tok, err_flag, tl_ndev);
+    else if (k <= 13)
+        k_topk1<16><<<(unsigned)N, LS_T, 0, st>>>(logits, V, ld, live, k, cand_score, cand_tok, err_flag, tl_ndev);
     else
-        k_topk<16><<<(unsigned)N, LS_T, 0, st>>>(logits, V, ld, live, k, cand_score, cand_tok, err_flag);
-    QNMT_CHECK_LAUNCH("k_topk");
+        k_topk1<32><<<(unsigned)N, LS_T, 0, st>>>(logits, V, ld, live, k, cand_score, cand_tok, err_flag, tl_ndev);
+    QNMT_CHECK_LAUNCH("k_topk1");
     return QNMT_OK;
 }
 
@@ -217,3 +409,9 @@ int qnmt_topk_candidates(const float* logits, int64_t N, int64_t V, int64_t ld,
 }
 
 }  // extern "C"
+
+extern "C" int qnmt_set_topk_exact(int exact) {
+    int old = qnmt::g_topk_exact;
+    qnmt::g_topk_exact = exact;
+    return old;
+}

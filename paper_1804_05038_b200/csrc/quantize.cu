@@ -18,11 +18,11 @@ constexpr int QT = 256;   // threads per block
 __global__ void k_seg_maxabs(const float* __restrict__ x, int64_t ncols, int64_t K, int64_t ldx,
                              int chunks_per_col, int64_t chunk_elems,
                              const int32_t* __restrict__ col_seg, uint32_t* seg_maxbits,
-                             bool vec4) {
+                             bool vec4, const int32_t* n_dev) {
     int64_t b = blockIdx.x;
     int64_t col = b / chunks_per_col;
     int64_t chunk = b % chunks_per_col;
-    if (col >= ncols) return;
+    if (col >= ncols || beyond(n_dev, col)) return;
     const float* row = x + col * ldx;
     int64_t k0 = chunk * chunk_elems;
     int64_t k1 = min(K, k0 + chunk_elems);
@@ -50,11 +50,11 @@ __global__ void k_encode(const float* __restrict__ x, int64_t ncols, int64_t K, 
                          int chunks_per_col, int64_t chunk_elems,
                          const int32_t* __restrict__ col_seg, const uint32_t* __restrict__ seg_maxbits,
                          int8_t* __restrict__ q, int64_t ldq, float* __restrict__ scales,
-                         int32_t mode, int32_t* err_flag, bool vec4) {
+                         int32_t mode, int32_t* err_flag, bool vec4, const int32_t* n_dev) {
     int64_t b = blockIdx.x;
     int64_t col = b / chunks_per_col;
     int64_t chunk = b % chunks_per_col;
-    if (col >= ncols) return;
+    if (col >= ncols || beyond(n_dev, col)) return;
     int seg = col_seg ? col_seg[col] : 0;
     uint32_t bits = seg_maxbits[seg];
     if (bits >= 0x7f800000u) {   // non-finite somewhere in the segment
@@ -92,10 +92,10 @@ int quantize_launch(const float* x, int64_t ncols, int64_t K, int64_t ldx, const
     int chunks = (int)cdiv(K, chunk_elems);
     int64_t blocks = ncols * chunks;
     k_seg_maxabs<<<(unsigned)blocks, QT, 0, st>>>(x, ncols, K, ldx, chunks, chunk_elems, col_seg,
-                                                 seg_maxbits, vec4);
+                                                 seg_maxbits, vec4, tl_ndev);
     QNMT_CHECK_LAUNCH("k_seg_maxabs");
     k_encode<<<(unsigned)blocks, QT, 0, st>>>(x, ncols, K, ldx, chunks, chunk_elems, col_seg,
-                                             seg_maxbits, q, ldq, scales, mode, err_flag, vec4);
+                                             seg_maxbits, q, ldq, scales, mode, err_flag, vec4, tl_ndev);
     QNMT_CHECK_LAUNCH("k_encode");
     return QNMT_OK;
 }

@@ -31,6 +31,7 @@ __global__ void __launch_bounds__(SEARCH_T)
 k_search_step(SearchState ss, int step, int n_sent, int beam, int k_list) {
     __shared__ int s_cnt[SEARCH_T];
     const int tid = threadIdx.x;
+    if (ss.step_dev) step = *ss.step_dev;   // graph-captured loop: step counter lives on the device
     int new_p = 0;
     // per-thread selection results
     int sel_tok[16], sel_par[16];
@@ -131,13 +132,18 @@ k_search_step(SearchState ss, int step, int n_sent, int beam, int k_list) {
         ss.P[s] = new_p;
         ss.col_off[s] = new_off;
     }
+    if (ss.step_dev) {
+        __syncthreads();
+        if (tid == 0) *ss.step_dev = step + 1;
+    }
 }
 
 // next-step state columns: dst[n] = src[parent_col[n]] for the state tensors
 __global__ void k_gather_rows(const float* __restrict__ a, const float* __restrict__ b,
                               const int32_t* __restrict__ parent, int64_t H,
-                              float* __restrict__ a_out, float* __restrict__ b_out) {
+                              float* __restrict__ a_out, float* __restrict__ b_out, const int32_t* n_dev) {
     int64_t n = blockIdx.x;
+    if (beyond(n_dev, n)) return;
     int64_t p = parent[n];
     for (int64_t j = threadIdx.x; j < H; j += blockDim.x) {
         a_out[n * H + j] = a[p * H + j];
@@ -159,7 +165,7 @@ int search_step_launch(const SearchState& ss, int step, int n_sent, int beam, in
 int gather_rows_launch(const float* a, const float* b, const int32_t* parent, int64_t N, int64_t H,
                        float* a_out, float* b_out, cudaStream_t st) {
     if (N <= 0) return QNMT_OK;
-    k_gather_rows<<<(unsigned)N, 256, 0, st>>>(a, b, parent, H, a_out, b_out);
+    k_gather_rows<<<(unsigned)N, 256, 0, st>>>(a, b, parent, H, a_out, b_out, tl_ndev);
     QNMT_CHECK_LAUNCH("k_gather_rows");
     return QNMT_OK;
 }

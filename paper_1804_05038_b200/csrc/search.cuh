@@ -29,6 +29,7 @@ struct SearchState {
     int32_t* y_next;
     double* live_next;
     int32_t* n_live;       // device scalar: columns of the next step
+    int32_t* step_dev;     // device step counter (graph mode) or nullptr (host passes step)
 };
 
 int search_step_launch(const SearchState& ss, int step, int n_sent, int beam, int k_list,

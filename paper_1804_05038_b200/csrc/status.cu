@@ -7,6 +7,7 @@
 namespace qnmt {
 
 static thread_local char g_last_error[512] = "";
+thread_local const int32_t* tl_ndev = nullptr;
 static unsigned long long g_launches = 0;
 
 void count_launch() { __atomic_fetch_add(&g_launches, 1ULL, __ATOMIC_RELAXED); }

@@ -106,3 +106,67 @@ def test_beam5_baseline_dims(base):
     idx = {t: i for i, t in enumerate(params.tgt_tokens)}
     assert [idx[w] for w in words] == g["B_beam5"].tolist()
     assert logp == float(g["B_beam5_logp"])
+
+
+@pytest.mark.parametrize("beam", [1, 4])
+def test_graph_mode_equals_eager_and_oracle(beam):
+    """CUDA-graph decode (device-side live count) == eager per-step loop == oracle,
+    on a 16-aligned model that terminates early (EOS) for some sentences."""
+    from paper_1804_05038_b200 import _lib
+    d = pb.Dims(300, 411, 64, 128, 96, 48)
+    params = pb.synthetic_model(d, 21, weight_std=0.25, bias_std=0.1, eos_bias=0.6)
+    qm = pb.quantize_model(params)
+    om = O.QModel(O.Dims(**d.as_dict()), params.tensors)
+    rng = np.random.default_rng(beam)
+    sents = [rng.integers(3, 300, int(rng.integers(1, 40))).tolist() for _ in range(37)]
+    eng = pb.Engine(qm, 64, 64, 8)
+    lib = _lib.load()
+    lib.qnmt_engine_set_graphs(eng._h, 1)
+    g_out = eng.translate_ids(sents, beam, 2.0)
+    g_out2 = eng.translate_ids(sents[:20], beam, 2.0)       # re-capture for a different batch size
+    lib.qnmt_engine_set_graphs(eng._h, 0)
+    e_out = eng.translate_ids(sents, beam, 2.0)
+    assert g_out == e_out
+    assert g_out2[0] == e_out[0][:20] and g_out2[1] == e_out[1][:20]
+    early = 0
+    for i, s in enumerate(sents):
+        toks, lp = om.translate(s, beam, 2.0)
+        assert g_out[0][i] == toks and g_out[1][i] == lp, i
+        early += len(toks) < int(np.ceil(2.0 * len(s)))
+    assert early > 0
+
+
+@pytest.mark.parametrize("V,k,ties", [(50000, 5, False), (50000, 5, True), (37, 8, True), (7, 5, True),
+                                      (32000, 1, True), (1000, 12, True), (2048, 16, False)])
+def test_candidate_kernels_exact(V, k, ties):
+    """Single-pass candidates == three-pass kernel == numpy restatement of
+    decoder.py:125 + :74-85 per parent, including heavy logit ties."""
+    import torch
+    from paper_1804_05038_b200 import _lib, _dev
+    rng = np.random.default_rng(V + k)
+    N = 37
+    x = rng.normal(0, 2, (N, V)).astype(np.float32)
+    if ties:
+        x = (np.round(x * 4) / 4).astype(np.float32)
+    live = rng.normal(-20, 5, N)
+    lib = _lib.load()
+
+    def run(exact):
+        old = lib.qnmt_set_topk_exact(exact)
+        xs, lv = torch.from_numpy(x).cuda(), torch.from_numpy(live).cuda()
+        cs = torch.empty((N, k), dtype=torch.float64, device="cuda")
+        ct = torch.empty((N, k), dtype=torch.int32, device="cuda")
+        f = _dev.reset_flag()
+        _lib.call("qnmt_topk_candidates", xs.data_ptr(), N, V, V, lv.data_ptr(), k, cs.data_ptr(), ct.data_ptr(),
+                  f.data_ptr(), _dev.stream_ptr())
+        lib.qnmt_set_topk_exact(old)
+        return cs.cpu().numpy(), ct.cpu().numpy()
+
+    s1, t1 = run(0)
+    s3, t3 = run(1)
+    lp = O.log_softmax_cols(x.T).T          # [N, V] f32 (Tier B)
+    for n in range(N):
+        sc = live[n] + lp[n].astype(np.float64)
+        order = sorted(range(V), key=lambda v: (-sc[v], v))[:k]
+        assert t1[n].tolist() == order and t3[n].tolist() == order, n
+        assert np.array_equal(s1[n], sc[order]) and np.array_equal(s3[n], sc[order])
