@@ -78,6 +78,38 @@ def topk_case(N=1280, V=50000, k=5):
             "hbm_frac_of_measured": 4.0 * N * V / t / 1e9 / PEAK["hbm_gbs"]}
 
 
+def attention_case(S=256, beam=5, A=2048, H2=2048, seed=0):
+    """One decoder step of attention for 256 sentences x 5 hypotheses, l ~ U[5, 100]."""
+    rng = np.random.default_rng(seed)
+    lens = rng.integers(5, 101, S).astype(np.int32)
+    rows = np.concatenate([[0], np.cumsum(lens)[:-1]]).astype(np.int64)
+    P = int(lens.sum())
+    N = S * beam
+    att = torch.randn((P, A), device="cuda") * 0.5
+    states = torch.randn((P, H2), device="cuda") * 0.5
+    u = torch.randn((N, A), device="cuda") * 0.5
+    v = torch.randint(-127, 128, (A,), dtype=torch.int8, device="cuda")
+    vs = torch.full((1,), 90.0, device="cuda")
+    off = torch.arange(0, N, beam, dtype=torch.int32, device="cuda")
+    cnt = torch.full((S,), beam, dtype=torch.int32, device="cuda")
+    rows_d = torch.from_numpy(rows).cuda()
+    lens_d = torch.from_numpy(lens).cuda()
+    ctx = torch.empty((N, H2), device="cuda")
+    scratch = torch.empty(N * 104 + 64, dtype=torch.int32, device="cuda")
+    mm = torch.empty((S, 2, A), device="cuda")
+    f = _dev.flag()
+    _lib.call("qnmt_attention_stats", att.data_ptr(), rows_d.data_ptr(), lens_d.data_ptr(), S, A, mm.data_ptr(),
+              torch.cuda.current_stream().cuda_stream)
+    t = graph_time(lambda: _lib.call("qnmt_attention", u.data_ptr(), A, N, off.data_ptr(), cnt.data_ptr(), S,
+                                     att.data_ptr(), mm.data_ptr(), states.data_ptr(), rows_d.data_ptr(), lens_d.data_ptr(), 100,
+                                     A, H2, v.data_ptr(), vs.data_ptr(), ctx.data_ptr(), H2, None, 0,
+                                     scratch.data_ptr(), f.data_ptr(), torch.cuda.current_stream().cuda_stream))
+    tanh_count = beam * A * int(lens.sum())
+    nbytes = 4.0 * (2 * P * A + P * H2 + N * A + N * H2)   # att_proj x2 passes, states, u, ctx
+    return {"kernel": "attention step", "N": N, "sum_l": P, "us": t * 1e6, "tanh_per_s": tanh_count / t,
+            "GBps": nbytes / t / 1e9}
+
+
 def gemv_cold(bsz):
     w = torch.randint(-127, 128, (3072, 1024), dtype=torch.int8, device="cuda")
     copies = [w.clone() for _ in range(64)]
@@ -110,6 +142,8 @@ def main():
         out.append(gemm_case("enc Uzr", 2048, 1024, 256))
     if "topk" in which:
         out.append(topk_case())
+    if "att" in which:
+        out.append(attention_case())
     if "gemv" in which:
         out += [gemv_cold(1), gemv_cold(64)]
     for r in out:

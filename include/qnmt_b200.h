@@ -132,19 +132,27 @@ int qnmt_tanh(const float* x, int64_t N, int64_t D, int64_t ldx, float* y, int64
 
 /* ---------------------------------------------------------------------------
  * Attention (layers.py:214-241) for N query columns.
- *   column n belongs to sentence col_sent[n] with length sent_len[s]; its
- *   att_proj / states rows start at row sent_row[s] of
- *   att_proj [*][A] and states [*][2H] (position-major).
+ *   sentence s (< n_sent) owns columns [sent_col_off[s], +sent_ncols[s]) (at
+ *   most 16), has length sent_len[s], and its att_proj / states rows start at
+ *   row sent_row[s] of att_proj [*][A] and states [*][2H] (position-major);
+ *   A <= 2048.
  *   u = state_proj(query) : [N][A] (stride ldu), v: [A] int8 codes, v_scale
  *   device f32[1].
  *   scores[n][i] = v . q(tanh(att_proj_i + u_n)) with ONE scale per column
  *   over its whole [A, l] block (layers.py:224-226);
  *   alpha = softmax_i(scores) (fp64, rounded); ctx = sum_i alpha_i states_i
  *   (fp64, rounded).
- *   ctx: [N][2H] (ldc); alpha (nullable): [N][lda]; scratch: >= N*(max_len+1)*4 bytes
+ *   att_minmax (nullable): [n_sent][2][A] per-sentence column max / min of
+ *   att_proj (qnmt_attention_stats); computed into scratch when NULL.
+ *   ctx: [N][2H] (ldc); alpha (nullable): [N][lda];
+ *   scratch: >= 4*(N*max_len + 64 + 2*n_sent*A) bytes
  * ------------------------------------------------------------------------- */
-int qnmt_attention(const float* u, int64_t ldu, int64_t N, const int32_t* col_sent,
-                   const float* att_proj, const float* states, const int64_t* sent_row,
+int qnmt_attention_stats(const float* att_proj, const int64_t* sent_row, const int32_t* sent_len,
+                         int32_t n_sent, int64_t A, float* att_minmax, void* stream);
+int qnmt_attention(const float* u, int64_t ldu, int64_t N, const int32_t* sent_col_off,
+                   const int32_t* sent_ncols, int32_t n_sent,
+                   const float* att_proj, const float* att_minmax, const float* states,
+                   const int64_t* sent_row,
                    const int32_t* sent_len, int32_t max_len, int64_t A, int64_t H2,
                    const int8_t* v_codes, const float* v_scale,
                    float* ctx, int64_t ldc, float* alpha, int64_t lda,

@@ -31,7 +31,8 @@ SIGNATURES = {
     "qnmt_gru_gates": (I32, [P, I64, P, P, I64, P, I64, I64, I64, P, P, P, P]),
     "qnmt_gru_combine": (I32, [P, I64, P, P, I64, P, P, I64, I64, I64, P, I64, P, I64, P, P, P]),
     "qnmt_tanh": (I32, [P, I64, I64, I64, P, I64, P, P]),
-    "qnmt_attention": (I32, [P, I64, I64, P, P, P, P, P, I32, I64, I64, P, P, P, I64, P, I64, P, P, P]),
+    "qnmt_attention": (I32, [P, I64, I64, P, P, I32, P, P, P, P, P, I32, I64, I64, P, P, P, I64, P, I64, P, P, P]),
+    "qnmt_attention_stats": (I32, [P, P, P, I32, I64, P, P]),
     "qnmt_log_softmax": (I32, [P, I64, I64, I64, P, I64, P, P]),
     "qnmt_topk_candidates": (I32, [P, I64, I64, I64, P, I32, P, P, P, P]),
     "qnmt_embed_gather": (I32, [P, I64, I64, P, I64, P, I64, P, P]),

@@ -33,11 +33,15 @@ int tanh_launch(const float* x, int64_t N, int64_t D, int64_t ldx, float* y, int
                 int32_t* err_flag, cudaStream_t st);
 int embed_gather_launch(const float* table, int64_t rows, int64_t E, const int32_t* ids, int64_t n,
                         float* out, int64_t ldo, int32_t* err_flag, cudaStream_t st);
-int attention_launch(const float* u, int64_t ldu, int64_t N, const int32_t* col_sent,
-                     const float* att_proj, const float* states, const int64_t* sent_row,
-                     const int32_t* sent_len, int32_t max_len, int64_t A, int64_t H2,
-                     const int8_t* v_codes, const float* v_scale, float* ctx, int64_t ldc,
-                     float* alpha, int64_t lda, void* scratch, int32_t* err_flag, cudaStream_t st);
+int attention_launch(const float* u, int64_t ldu, int64_t N, const int32_t* sent_col_off,
+                     const int32_t* sent_ncols, int32_t n_sent, const float* att_proj, const float* att_minmax,
+                     const float* states, const int64_t* sent_row, const int32_t* sent_len, int32_t max_len, int64_t A, int64_t H2,
+                     const int8_t* v_codes, const float* v_scale, float* ctx, int64_t ldc, float* alpha,
+                     int64_t lda, void* scratch, int32_t* err_flag, cudaStream_t st);
+int att_minmax_launch(const float* att_proj, const int64_t* sent_row, const int32_t* sent_len, int32_t n_sent,
+                      int64_t A, float* mm, cudaStream_t st);
+int col_ranges_launch(const int32_t* col_sent, int64_t N, int32_t n_sent, int32_t* off, int32_t* cnt,
+                      cudaStream_t st);
 int topk_launch(const float* logits, int64_t N, int64_t V, int64_t ld, const double* live, int32_t k,
                 double* cand_score, int32_t* cand_tok, int32_t* err_flag, cudaStream_t st);
 
@@ -154,6 +158,7 @@ struct qnmt_engine {
     float* sc_ro;
     float* logits;           // [N][V]
     void* att_scratch;
+    float* att_mm;           // [S][2][A] per-sentence column max / min of att_proj
     // translate loop state
     float* st_s[2];          // [N][H] s
     float* st_sp[2];         // [N][H] s_prime
@@ -187,6 +192,8 @@ struct qnmt_engine {
     // graph-captured decode steps (device-side live count and step counter)
     bool use_graphs = true;
     int32_t* d_N = nullptr;      // [2] live columns, ping-pong
+    int32_t* rng_off = nullptr;  // [S] column ranges for qnmt_decoder_step callers
+    int32_t* rng_cnt = nullptr;
     int32_t* d_step = nullptr;
     cudaStream_t cap_stream = nullptr;
     std::vector<std::pair<std::pair<int, int>, std::pair<cudaGraphExec_t, cudaGraphExec_t>>> graphs;
@@ -373,6 +380,9 @@ struct StepIO {
     float* logits;
     float* alpha;
     int64_t lda;
+    const int32_t* sent_col_off;   // [nseg] first column of each sentence (columns grouped by sentence)
+    const int32_t* sent_ncols;     // [nseg] live columns of each sentence
+    const float* att_minmax;       // [nseg][2][A] column extrema of att_proj (nullable)
 };
 
 static int gru_cell(qnmt_engine* e, const Cell& c, int64_t N, int nseg, const int32_t* seg,
@@ -414,9 +424,9 @@ static int step_core(qnmt_engine* e, const StepIO& io, cudaStream_t st) {
     prof_mark(e, PG_GEMM, st, 2.0 * N * A * H, (double)A * H);
     TRY(gemm(m->u_att, A, H, m->u_att_s, A, e->q_q, N, H, e->sc_q, seg, nullptr, e->u, A, 0, st));
     prof_mark(e, PG_ATT, st);
-    TRY(attention_launch(e->u, A, N, seg, io.att_proj, io.states, io.sent_row, io.sent_len, io.max_len,
-                         A, 2 * H, m->v, m->v_s, e->ctx, 2 * H, io.alpha, io.lda, e->att_scratch,
-                         e->err, st));
+    TRY(attention_launch(e->u, A, N, io.sent_col_off, io.sent_ncols, io.nseg, io.att_proj, io.att_minmax, io.states,
+                         io.sent_row, io.sent_len, io.max_len, A, 2 * H, m->v, m->v_s, e->ctx, 2 * H,
+                         io.alpha, io.lda, e->att_scratch, e->err, st));
     prof_mark(e, PG_QUANT, st);
     TRY(quantize_launch(e->ctx, N, 2 * H, 2 * H, seg, ns, e->q_ctx, 2 * H, e->sc_ctx, e->seg_bits, 1,
                         e->err, st));
@@ -594,7 +604,8 @@ int qnmt_engine_create(const qnmt_model* m, int32_t max_sentences, int32_t max_s
         e->q_ro = a.take<int8_t>(N * R);
         e->sc_ro = a.take<float>(S);
         e->logits = a.take<float>(N * V);
-        e->att_scratch = a.take<char>(N * (L + 2) * 4 + 64);
+        e->att_scratch = a.take<char>(N * (L + 2) * 4 + 2 * S * A * 4 + 1024);
+        e->att_mm = a.take<float>(2 * S * A);
         for (int i = 0; i < 2; ++i) {
             e->st_s[i] = a.take<float>(N * H);
             e->st_sp[i] = a.take<float>(N * H);
@@ -609,6 +620,8 @@ int qnmt_engine_create(const qnmt_model* m, int32_t max_sentences, int32_t max_s
         e->cand_tok = a.take<int32_t>(N * B);
         e->n_live = a.take<int32_t>(4);
         e->d_N = a.take<int32_t>(4);
+        e->rng_off = a.take<int32_t>(S);
+        e->rng_cnt = a.take<int32_t>(S);
         e->d_step = a.take<int32_t>(4);
         e->P = a.take<int32_t>(S);
         e->col_off = a.take<int32_t>(S);
@@ -700,8 +713,9 @@ int qnmt_decoder_step(qnmt_engine* e, int64_t N, const int32_t* col_sent, int32_
     cudaStream_t st = as_stream(stream);
     if (N > e->NMAX || n_sent > e->S || max_len > e->L) { set_error("step exceeds engine capacity"); return QNMT_ERR_CONFIG; }
     QNMT_CUDA(cudaMemsetAsync(e->err, 0, 4, st));
+    TRY(col_ranges_launch(col_sent, N, n_sent, e->rng_off, e->rng_cnt, st));
     StepIO io{N, n_sent, col_sent, y, s, sp, states, att_proj, sent_row, sent_len, max_len,
-              s_int, s_new, logits, alpha, lda};
+              s_int, s_new, logits, alpha, lda, e->rng_off, e->rng_cnt, nullptr};
     TRY(step_core(e, io, st));
     return check_flag(e, st);
 }
@@ -728,7 +742,8 @@ static int capture_step(qnmt_engine* e, int cur, int n, int beam, int k_list, cu
     {
         NdevScope nd(e->d_N + cur);
         StepIO io{NM, n, e->col_sent[cur], e->y[cur], e->st_s[cur], e->st_sp[cur], e->enc_states, e->enc_att,
-                  e->sent_row, e->sent_len, e->L, e->s_int, e->s_new, e->logits, nullptr, 0};
+                  e->sent_row, e->sent_len, e->L, e->s_int, e->s_new, e->logits, nullptr, 0,
+                  e->col_off, e->P, e->att_mm};
         rc = step_core(e, io, cs);
         if (rc == QNMT_OK)
             rc = topk_launch(e->logits, NM, V, V, e->live[cur], k_list, e->cand_score, e->cand_tok, e->err, cs);
@@ -820,6 +835,7 @@ static int decode_core(qnmt_engine* e, const int32_t* src_ids, bool ids_on_devic
     QNMT_CUDA(cudaMemcpyAsync(e->sent_row, row.data(), (size_t)n * 8, cudaMemcpyHostToDevice, st));
     QNMT_CUDA(cudaMemcpyAsync(e->sent_len, src_len, (size_t)n * 4, cudaMemcpyHostToDevice, st));
     QNMT_CUDA(cudaMemcpyAsync(e->max_steps, msteps.data(), (size_t)n * 4, cudaMemcpyHostToDevice, st));
+    TRY(att_minmax_launch(e->enc_att, e->sent_row, e->sent_len, n, m->A, e->att_mm, st));
     QNMT_CUDA(cudaMemcpyAsync(e->P, ones.data(), (size_t)n * 4, cudaMemcpyHostToDevice, st));
     QNMT_CUDA(cudaMemcpyAsync(e->col_off, iota_n.data(), (size_t)n * 4, cudaMemcpyHostToDevice, st));
     QNMT_CUDA(cudaMemcpyAsync(e->col_sent[0], iota_n.data(), (size_t)n * 4, cudaMemcpyHostToDevice, st));
@@ -854,7 +870,8 @@ static int decode_core(qnmt_engine* e, const int32_t* src_ids, bool ids_on_devic
     int cur = 0;
     for (int t = 0; t < Tmax && N > 0; ++t) {
         StepIO io{N, n, e->col_sent[cur], e->y[cur], e->st_s[cur], e->st_sp[cur], e->enc_states,
-                  e->enc_att, e->sent_row, e->sent_len, Lmax, e->s_int, e->s_new, e->logits, nullptr, 0};
+                  e->enc_att, e->sent_row, e->sent_len, Lmax, e->s_int, e->s_new, e->logits, nullptr, 0,
+                  e->col_off, e->P, e->att_mm};
         TRY(step_core(e, io, st));
         prof_mark(e, PG_TOPK, st, 0, 4.0 * N * V);
         TRY(topk_launch(e->logits, N, V, V, e->live[cur], k_list, e->cand_score, e->cand_tok, e->err, st));

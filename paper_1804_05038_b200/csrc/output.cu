@@ -269,29 +269,57 @@ k_topk1(const float* __restrict__ logits, int64_t V, int64_t ld, const double* _
     float m = -FLT_MAX;
     double s = 0.0;
     bool bad = false;
-    LCand L[KM];
-#pragma unroll
-    for (int i = 0; i < KM; ++i) L[i] = LCand{-FLT_MAX, 0x7fffffff};
+    // per-thread top-3 by (logit desc, token asc), branch-free: elements arrive in
+    // increasing token order, so strict '>' keeps the smaller token on ties
+    float a1 = -FLT_MAX, a2 = -FLT_MAX, a3 = -FLT_MAX;
+    int i1 = 0x7fffffff, i2 = 0x7fffffff, i3 = 0x7fffffff;
+    auto top3 = [&](float x, int v) {
+        const bool g1 = x > a1, g2 = x > a2, g3 = x > a3;
+        a3 = g2 ? a2 : (g3 ? x : a3);
+        i3 = g2 ? i2 : (g3 ? v : i3);
+        a2 = g1 ? a1 : (g2 ? x : a2);
+        i2 = g1 ? i1 : (g2 ? v : i2);
+        a1 = g1 ? x : a1;
+        i1 = g1 ? v : i1;
+    };
     const bool vec = (V % 4 == 0) && (ld % 4 == 0) && (((uintptr_t)logits & 15) == 0);
     if (vec) {
         const float4* r4 = reinterpret_cast<const float4*>(row);
-        for (int64_t q = threadIdx.x; q < V / 4; q += LS_T) {
-            const float4 x = r4[q];
-            const int v = (int)(4 * q);
-            bad |= !(is_finite_f(x.x) && is_finite_f(x.y) && is_finite_f(x.z) && is_finite_f(x.w));
-            const float cm = fmaxf(fmaxf(x.x, x.y), fmaxf(x.z, x.w));
+        const int64_t Q = V / 4;
+        constexpr int U = 4;   // float4 loads in flight per thread
+        for (int64_t q0 = threadIdx.x; q0 < Q; q0 += U * LS_T) {
+            float4 xs[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int64_t q = q0 + (int64_t)u * LS_T;
+                xs[u] = q < Q ? __ldg(r4 + q) : make_float4(-FLT_MAX, -FLT_MAX, -FLT_MAX, -FLT_MAX);
+            }
+            float cm = -FLT_MAX;
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const float4 x = xs[u];
+                bad |= !(is_finite_f(x.x) && is_finite_f(x.y) && is_finite_f(x.z) && is_finite_f(x.w));
+                cm = fmaxf(cm, fmaxf(fmaxf(x.x, x.y), fmaxf(x.z, x.w)));
+            }
             if (cm > m) {   // rare after the first chunks: rescale the running sum once
                 s = (m == -FLT_MAX) ? 0.0 : s * exp_neg((double)m - (double)cm, tab);
                 m = cm;
             }
             const double dm = (double)m;
-            const double e0 = exp_neg((double)x.x - dm, tab), e1 = exp_neg((double)x.y - dm, tab);
-            const double e2 = exp_neg((double)x.z - dm, tab), e3 = exp_neg((double)x.w - dm, tab);
-            s += (e0 + e1) + (e2 + e3);
-            if (x.x >= L[KM - 1].x) linsert<KM>(L, LCand{x.x, v});
-            if (x.y >= L[KM - 1].x) linsert<KM>(L, LCand{x.y, v + 1});
-            if (x.z >= L[KM - 1].x) linsert<KM>(L, LCand{x.z, v + 2});
-            if (x.w >= L[KM - 1].x) linsert<KM>(L, LCand{x.w, v + 3});
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int64_t q = q0 + (int64_t)u * LS_T;
+                if (q >= Q) break;
+                const float4 x = xs[u];
+                const int v = (int)(4 * q);
+                const double e0 = exp_neg((double)x.x - dm, tab), e1 = exp_neg((double)x.y - dm, tab);
+                const double e2 = exp_neg((double)x.z - dm, tab), e3 = exp_neg((double)x.w - dm, tab);
+                s += (e0 + e1) + (e2 + e3);
+                top3(x.x, v);
+                top3(x.y, v + 1);
+                top3(x.z, v + 2);
+                top3(x.w, v + 3);
+            }
         }
     } else {
         for (int64_t v = threadIdx.x; v < V; v += LS_T) {
@@ -302,7 +330,7 @@ k_topk1(const float* __restrict__ logits, int64_t V, int64_t ld, const double* _
                 m = x;
             }
             s += exp_neg((double)x - (double)m, tab);
-            linsert<KM>(L, LCand{x, (int)v});
+            top3(x, (int)v);
         }
     }
     if (__syncthreads_or(bad) && threadIdx.x == 0) set_flag(err_flag, QNMT_FLAG_NUMERIC);
@@ -311,11 +339,31 @@ k_topk1(const float* __restrict__ logits, int64_t V, int64_t ld, const double* _
     const double S = block_sum_d(m == -FLT_MAX ? 0.0 : s * exp_neg((double)m - dM, tab), redd);
     const double lse = log(S);
     const int kk = (int)(V < KM ? V : KM);
-    Cand Lc[KM];
+    {
+        Cand Lc[KM];
 #pragma unroll
-    for (int i = 0; i < KM; ++i)
-        Lc[i] = L[i].t == 0x7fffffff ? Cand{-DBL_MAX, 0x7fffffff} : Cand{(double)L[i].x, L[i].t};
-    block_merge_cands<KM>(Lc, wl, lst, kk);
+        for (int i = 0; i < KM; ++i) Lc[i] = Cand{-DBL_MAX, 0x7fffffff};
+        if (i1 != 0x7fffffff) Lc[0] = Cand{(double)a1, i1};
+        if (i2 != 0x7fffffff) Lc[1] = Cand{(double)a2, i2};
+        if (i3 != 0x7fffffff) Lc[2] = Cand{(double)a3, i3};
+        block_merge_cands<KM>(Lc, wl, lst, kk);
+    }
+    // The merged list is the exact top-KM unless some thread may hold a 4th element
+    // that belongs to it, i.e. its 3rd entry still reaches the KM-th value: then rescan.
+    {
+        const Cand thr = lst[kk - 1];
+        const bool maybe_more = (i3 != 0x7fffffff) && !better(thr, Cand{(double)a3, i3});
+        if (__syncthreads_or(maybe_more)) {
+            Cand L[KM];
+#pragma unroll
+            for (int i = 0; i < KM; ++i) L[i] = Cand{-DBL_MAX, 0x7fffffff};
+            for (int64_t v = threadIdx.x; v < V; v += LS_T) {
+                const float x = row[v];
+                if ((double)x >= thr.s) insert<KM>(L, Cand{(double)x, (int)v});
+            }
+            block_merge_cands<KM>(L, wl, lst, kk);
+        }
+    }
     const double base = live ? live[n] : 0.0;
     if (threadIdx.x == 0) {
         // exact scores for the KM logit-candidates, then order by (score desc, token asc)

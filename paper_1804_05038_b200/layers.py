@@ -270,12 +270,17 @@ def attend_k(att: AttentionNet, q_k: torch.Tensor, enc: EncoderStates):
     length = enc.length
     H2 = enc.states_k.shape[1]
     dev = u.device
-    sent_row, sent_len, col_sent = _one_sentence_meta(length, P, dev)
+    sent_row, sent_len, _ = _one_sentence_meta(length, P, dev)
+    col_off = torch.zeros(1, dtype=torch.int32, device=dev)
+    ncols = torch.full((1,), P, dtype=torch.int32, device=dev)
     ctx = torch.empty((P, H2), dtype=torch.float32, device=dev)
     alpha = torch.empty((P, length), dtype=torch.float32, device=dev)
-    scratch = torch.empty(P * (length + 2) + 64, dtype=torch.int32, device=dev)
+    scratch = torch.empty(P * (length + 2) + 2 * A + 1024, dtype=torch.int32, device=dev)
     v = att.scorer.weight
-    _lib.call("qnmt_attention", u.data_ptr(), A, P, col_sent.data_ptr(), enc.att_proj_k.data_ptr(),
+    if P > 16:
+        raise ShapeError("attend supports at most 16 query columns per call")
+    _lib.call("qnmt_attention", u.data_ptr(), A, P, col_off.data_ptr(), ncols.data_ptr(), 1,
+              enc.att_proj_k.data_ptr(), None,
               enc.states_k.data_ptr(), sent_row.data_ptr(), sent_len.data_ptr(), length, A, H2,
               v.device_data().data_ptr(), v.device_scale().data_ptr(), ctx.data_ptr(), H2,
               alpha.data_ptr(), length, scratch.data_ptr(), _dev.flag().data_ptr(), _dev.stream_ptr())
