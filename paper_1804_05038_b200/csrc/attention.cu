@@ -36,12 +36,30 @@ constexpr int AKA = 8;         // a-elements per thread kept in registers (A <= 
 // Fast code of t = tanh(x) at scale st.  Returns the code from tanhf (<= 2 ulp)
 // and sets `unsafe` when fl(|v| + 1/2) is within 2.5e-4 of an integer, where
 // the exact fp64 tanh could give a different floor (att_code_exact).
-__device__ __forceinline__ int att_code_fast(float x, float st, bool& unsafe) {
-    const float v = __fmul_rn(tanhf(x), st);
+__device__ __forceinline__ float ex2_approx(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ float rcp_approx(float x) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+// tanh with absolute error < ~1.2e-6 from two MUFU ops: 1 - 2 / (1 + e^{2|x|})
+__device__ __forceinline__ float tanh_fast(float x) {
+    const float e = ex2_approx(fabsf(x) * 2.8853900817779268f);   // 2 / ln 2
+    const float r = rcp_approx(e + 1.0f);
+    return copysignf(fmaf(-2.0f, r, 1.0f), x);
+}
+
+// win = max(4e-4, st * 2e-6) bounds |v_fast - v_exact| (+ rounding) with margin.
+__device__ __forceinline__ int att_code_fast(float x, float st, float win, bool& unsafe) {
+    const float v = __fmul_rn(tanh_fast(x), st);
     const float r = __fadd_rn(fabsf(v), 0.5f);
     const float q = floorf(r);
     const float f = r - q;
-    unsafe = (f < 2.5e-4f) | (f > 1.0f - 2.5e-4f);
+    unsafe = (f < win) | (f > 1.0f - win);
     const float qc = fminf(q, 127.0f);
     return (int)(v < 0.0f ? -qc : qc);
 }
@@ -153,6 +171,7 @@ k_att_score3(const float* __restrict__ u, int64_t ldu, const int32_t* __restrict
     }
     for (int j = 0; j < P; ++j) {
         const float st = s_st[j];
+        const float win = fmaxf(4e-4f, st * 2e-6f);
         const float* un = u + (int64_t)(c0 + j) * ldu;
         float uvv[AKA];
 #pragma unroll
@@ -168,7 +187,7 @@ k_att_score3(const float* __restrict__ u, int64_t ldu, const int32_t* __restrict
 #pragma unroll
             for (int k = 0; k < AKA; ++k) {
                 bool uk;
-                const int c = att_code_fast(__fadd_rn(apv[p][k], uvv[k]), st, uk);
+                const int c = att_code_fast(__fadd_rn(apv[p][k], uvv[k]), st, win, uk);
                 acc[p] += vv[k] * c;                        // vv = 0 for a >= A
                 unsafe |= (uint32_t)uk << (p * AKA + k);
             }
@@ -185,7 +204,7 @@ k_att_score3(const float* __restrict__ u, int64_t ldu, const int32_t* __restrict
                     for (int kk = 0; kk < AKA; ++kk)
                         if (pp * AKA + kk == b) xv = __fadd_rn(apv[pp][kk], uvv[kk]);
                 bool dummy;
-                const int fast = att_code_fast(xv, st, dummy);
+                const int fast = att_code_fast(xv, st, win, dummy);
                 const int exact = att_code_exact(xv, st);
                 int vk = 0;
 #pragma unroll

@@ -182,8 +182,10 @@ k_topk(const float* __restrict__ logits, int64_t V, int64_t ld, const double* __
 // conflict.  ~13 f64 ops instead of the general-purpose exp() (~27 DFMA slots).
 __device__ __forceinline__ double exp_neg(double t, const double* __restrict__ tab) {
     if (t < -700.0) return 0.0;
-    const double kd = rint(t * 23.083120654223414);          // 16 / ln 2
-    const int k = (int)kd;
+    // round(t * 16/ln2) without FRND/F2I: add 1.5*2^52 so the integer lands in the low word
+    const double kd_m = fma(t, 23.083120654223414, 6755399441055744.0);
+    const int k = __double2loint(kd_m);
+    const double kd = kd_m - 6755399441055744.0;
     double r = fma(kd, -0.04332169878499658, t);             // ln2/16, rounded to f64
     r = fma(kd, -1.4494042586539372e-18, r);                 // ln2/16 - the above
     double p = fma(r, 1.0 / 5040.0, 1.0 / 720.0);
