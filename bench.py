@@ -4,16 +4,25 @@
 Workload (BASELINE.json configs[4], the config the metric is quoted on at
 1/2/4/8 B200): V_src 32000, V_tgt 50000, E 512, H 1024, A 2048, R 512, beam 5,
 max_ratio 1.5, a seeded 8192-sentence corpus with lengths ~ U[5, 100]; one
-"step" = one batch of 256 sentences per GPU (weak scaling, no collective on
-the data path).  Random N(0, 0.05) weights, synthetic token ids.
+"step" = one batch of 256 sentences per GPU (weak scaling: every rank decodes
+its own batch, no collective on the data path).  Seeded N(0, 0.05) weights,
+uniform synthetic token ids (no datasets / checkpoints in this environment).
 
-  value  : target tokens/s (EOS excluded, bench.py:161 of the reference) of the
-           device-resident decode (qnmt_decode_batch_device: source ids already
-           in HBM), CUDA events on the launching stream, max over ranks.
-  e2e    : same metric through the public C-ABI call qnmt_translate_batch with
-           HOST buffers (H2D of ids, D2H of finished lists + host selection).
-  --impl reference : the reference algorithm on the host CPU (the oracle port;
-           the reference itself is Python and cannot travel to the GPU box).
+  value  : target tokens/s (EOS excluded, as the reference's bench.py:161 counts)
+           of the device-resident decode (qnmt_decode_batch_device: source ids
+           already in HBM), CUDA events on the launching stream, L2 flushed
+           before every step, max over ranks.
+  e2e    : the same metric through the public C-ABI call qnmt_translate_batch
+           with HOST buffers (H2D of ids, D2H of finished lists + history, host
+           selection of the best hypothesis), wall clock per step.
+  roofline: per-kernel device time measured live in the timed steps by
+           %globaltimer stamps captured into the step graphs (a CUDA graph step
+           cannot be bracketed by host events); algorithmic bytes / int-ops per
+           launch from the live column count of each step.
+  --impl reference : the reference algorithm on the host CPU.  The reference is
+           a Python package that cannot travel to the GPU box, so this arm runs
+           the numpy port oracle/qnmt_oracle.py (pinned bit-exact against the
+           reference) with all host cores.
 """
 
 from __future__ import annotations
@@ -25,7 +34,6 @@ import os
 import subprocess
 import sys
 import tempfile
-import threading
 import time
 
 import numpy as np
@@ -36,8 +44,19 @@ sys.path.insert(0, ROOT)
 DIMS = dict(src_vocab=32000, tgt_vocab=50000, embed=512, hidden=1024, attn=2048, readout=512)
 BEAM, MAX_RATIO, PER_GPU, CORPUS = 5, 1.5, 256, 8192
 MODEL_SEED, CORPUS_SEED = 1804, 5038
+METRIC = "tokens/sec (int8 beam-5 decode, target tokens excl. EOS)"
 WORKLOAD = ("cfg5 bulk translation shard: 256 sentences/GPU/step of a seeded 8192-sentence corpus, "
-            "l~U[5,100], beam 5, max_ratio 1.5, V_tgt 50000, H 1024, E 512, A 2048")
+            "l~U[5,100], beam 5, max_ratio 1.5, V_tgt 50000, H 1024, E 512, A 2048, R 512")
+# DRAM bytes per algorithmic byte measured by `ncu --set full` at N = 1280 (profiles/r01_ncu_summary.md)
+NCU_TRAFFIC_RATIO = {"topk": 256.9 / 256.0, "attention": None, "gemm_vocab": None}
+
+
+def peaks():
+    try:
+        p = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        return float(p["hbm_gbs"]), "measured"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "fallback"
 
 
 def corpus():
@@ -86,56 +105,82 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(rows)}
 
 
-def cpu_baseline(params, sents, sample: int, budget_s: float = 25.0):
-    """Reference algorithm (oracle port) on host cores over a bounded sample."""
+def cpu_translate(params, sents, threads=None):
+    """Reference algorithm (oracle port, numpy) on host cores, one sentence per thread
+    (the reference's own bench.py:129-132 scheme)."""
     import concurrent.futures as cf
 
     from oracle import qnmt_oracle as O
     om = O.QModel(O.Dims(**DIMS), params.tensors)
-    cores = os.cpu_count() or 1
-    sub = sents[:sample]
+    cores = threads or os.cpu_count() or 1
     t0 = time.perf_counter()
-    done, tokens, outs = 0, 0, []
     with cf.ThreadPoolExecutor(max_workers=cores) as pool:
-        futs = [pool.submit(om.translate, s.tolist(), BEAM, MAX_RATIO) for s in sub]
-        for f in futs:
-            toks, lp = f.result()
-            outs.append((toks, lp))
-            tokens += len(toks)
-            done += 1
-    wall = time.perf_counter() - t0
-    return {"value": tokens / wall, "unit": "tokens/s", "cores": cores, "kind": "port",
-            "sample": f"{done} sentences of the first timed batch (beam 5, V_tgt 50000), "
-                      f"oracle/qnmt_oracle.py numpy port, {cores} threads, {wall:.1f}s",
-            "sentences_per_s": done / wall}, outs
+        outs = list(pool.map(lambda s: om.translate(s.tolist(), BEAM, MAX_RATIO), sents))
+    return outs, time.perf_counter() - t0, cores
 
 
 def run_reference(args, rank, world):
     if rank != 0:
         return
-    import paper_1804_05038_b200 as pb   # only for the seeded synthetic model recipe (host code)
+    import paper_1804_05038_b200 as pb   # host-side synthetic model recipe only (numpy)
     params = pb.synthetic_model(pb.Dims(**DIMS), MODEL_SEED)
     sents = corpus()
     sample = args.cpu_sample
     for w in range(args.warmup):
-        cpu_baseline(params, batch_for(w, 0, 1, sents)[:2], 2)
-    vals, secs, toks = [], 0.0, 0
+        cpu_translate(params, batch_for(w, 0, 1, sents)[:1])
+    secs, toks, cores = 0.0, 0, 1
     for k in range(args.steps):
-        r, outs = cpu_baseline(params, batch_for(args.warmup + k, 0, 1, sents), sample)
-        vals.append(r)
-        n = sum(len(o[0]) for o in outs)
-        toks += n
-        secs += n / r["value"]
+        outs, dt, cores = cpu_translate(params, batch_for(args.warmup + k, 0, 1, sents)[:sample])
+        toks += sum(len(o[0]) for o in outs)
+        secs += dt
     value = toks / secs
-    line = {"metric": "tokens/sec (int8 beam-5 decode, target tokens excl. EOS)", "value": value,
-            "unit": "tokens/s", "impl": "reference", "n_gpus": args.gpus, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": 1000 * secs / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "int8", "data": "synthetic",
-            "config": {"workload": WORKLOAD, "sample_per_step": sample},
-            "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": vals[0]["cores"],
-                             "kind": "port", "sample": vals[0]["sample"]},
+    desc = (f"{sample} sentences per step (first {sample} of each 256-sentence batch), beam 5, V_tgt 50000, "
+            f"oracle/qnmt_oracle.py numpy port, {cores} threads")
+    line = {"metric": METRIC, "value": value, "unit": "tokens/s", "impl": "reference", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * secs / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int8",
+            "data": "synthetic", "config": {"workload": WORKLOAD, "sample_per_step": sample},
+            "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores, "kind": "port", "sample": desc},
             "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def kernel_rooflines(rows, hbm, peak_kind):
+    """rows: stamps of the timed steps -> per-kernel achieved vs roofline."""
+    V, R, A, H2 = DIMS["tgt_vocab"], DIMS["readout"], DIMS["attn"], 2 * DIMS["hidden"]
+    t = {"attention": 0.0, "topk": 0.0, "gemm_vocab": 0.0, "step": 0.0}
+    work = {"attention": 0.0, "topk": 0.0, "gemm_vocab": 0.0}
+    ops_vocab = 0.0
+    launches = 0
+    for r in rows:
+        n, sl = float(r[8]), float(r[9])
+        if n <= 0:
+            continue
+        launches += 1
+        t["attention"] += (r[2] - r[1]) * 1e-9
+        t["topk"] += (r[4] - r[3]) * 1e-9
+        t["gemm_vocab"] += (r[6] - r[5]) * 1e-9
+        t["step"] += (r[4] - r[0]) * 1e-9
+        # algorithmic bytes per launch
+        work["attention"] += 4.0 * (sl * A + sl * H2 + n * A + n * H2)   # att_proj, states, u, ctx
+        work["topk"] += 4.0 * n * V                                       # logits read once
+        work["gemm_vocab"] += V * R + n * R + 4.0 * n * V                 # W, X codes, logits write
+        ops_vocab += 2.0 * V * R * n
+    out = {}
+    for k in ("attention", "topk", "gemm_vocab"):
+        if t[k] <= 0:
+            continue
+        ach = work[k] / t[k] / 1e9
+        ratio = NCU_TRAFFIC_RATIO.get(k)
+        out[k] = {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
+                  "us_per_launch": 1e6 * t[k] / max(launches, 1),
+                  "traffic": (work[k] / max(launches, 1) * ratio) if ratio else None,
+                  "algorithmic_bytes_per_launch": work[k] / max(launches, 1), "peak_source": peak_kind,
+                  "share_of_step": t[k] / t["step"] if t["step"] > 0 else None}
+    if "gemm_vocab" in out:
+        out["gemm_vocab"]["int_ops_per_s"] = ops_vocab / t["gemm_vocab"]
+        out["gemm_vocab"]["tensor_frac_of_int8_spec_4500T"] = ops_vocab / t["gemm_vocab"] / 4.5e15
+    return out
 
 
 def main():
@@ -146,7 +191,8 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--cpu-sample", type=int, default=8)
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--no-profile", action="store_true", help="disable the engine's event profiler")
+    ap.add_argument("--no-stamps", action="store_true", help="no device-clock stamps (no roofline)")
+    ap.add_argument("--no-profile", action="store_true", help="(kept for compatibility)")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
@@ -155,11 +201,13 @@ def main():
         run_reference(args, rank, world)
         return
 
+    import ctypes as C
+
     import torch
     import torch.distributed as dist
 
     import paper_1804_05038_b200 as pb
-    from paper_1804_05038_b200 import _lib, _dev
+    from paper_1804_05038_b200 import _lib
 
     torch.cuda.set_device(local)
     if world > 1:
@@ -172,11 +220,9 @@ def main():
     lib = _lib.load()
     stream = torch.cuda.current_stream()
     flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device=dev)   # > 126 MB L2
-
-    def upload(batch):
-        lens = np.array([len(s) for s in batch], dtype=np.int32)
-        ids = torch.from_numpy(np.concatenate(batch)).to(dev)
-        return ids, lens
+    stamps_on = not args.no_stamps
+    lib.qnmt_engine_stamps(eng._h, 1 if stamps_on else 0)   # graphs are captured during warm-up
+    stamp_buf = np.zeros((256, 10), dtype=np.int64)
 
     def fetch(batch):
         stride = int(math.ceil(MAX_RATIO * max(len(s) for s in batch))) + 1
@@ -188,7 +234,8 @@ def main():
         return out, ol, lp
 
     def device_step(batch):
-        ids, lens = upload(batch)
+        lens = np.array([len(s) for s in batch], dtype=np.int32)
+        ids = torch.from_numpy(np.concatenate(batch)).to(dev)
         flush.fill_(1)
         torch.cuda.synchronize()
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -199,38 +246,32 @@ def main():
         ev1.record(stream)
         ev1.synchronize()
         launches = lib.qnmt_kernel_launches() - l0
+        rows = []
+        if stamps_on:
+            nr = lib.qnmt_engine_stamps_read(eng._h, stamp_buf.ctypes.data, stamp_buf.shape[0], stream.cuda_stream)
+            rows = [stamp_buf[i].copy() for i in range(nr)]
         out, ol, lp = fetch(batch)
-        return ev0.elapsed_time(ev1) / 1000.0, int(ol.sum()), launches
+        return ev0.elapsed_time(ev1) / 1000.0, int(ol.sum()), launches, rows, (out, ol, lp)
 
     for w in range(args.warmup):
         device_step(batch_for(w, rank, world, sents))
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    import ctypes as C
-    if not args.no_profile:
-        lib.qnmt_engine_profile(eng._h, 1)
     clk = ClockSampler(local)
-    secs, toks, launches = 0.0, 0, 0
-    step_ms = []
+    secs, toks, launches, step_ms, all_rows = 0.0, 0, 0, [], []
+    first_result = None
     for k in range(args.steps):
-        t, n, nl = device_step(batch_for(args.warmup + k, rank, world, sents))
+        t, n, nl, rows, res = device_step(batch_for(args.warmup + k, rank, world, sents))
         secs += t
         toks += n
         launches += nl
         step_ms.append(1000 * t)
+        all_rows += rows
+        if first_result is None:
+            first_result = res
     torch.cuda.synchronize()
     clocks = clk.stop()
-    phases = None
-    if not args.no_profile:
-        arr = [(C.c_double * 16)() for _ in range(4)]
-        ng = lib.qnmt_engine_profile_read(eng._h, *[C.cast(a, C.c_void_p) for a in arr])
-        lib.qnmt_engine_profile(eng._h, 0)
-        names = ["encoder", "embed", "quantize", "gemm_decoder", "gru_gates", "attention", "gemm_vocab",
-                 "topk", "search", "gather", "misc"]
-        phases = {names[i]: {"ms": arr[0][i] / args.steps, "launch_groups": arr[1][i] / args.steps,
-                             "int_ops": arr[2][i] / args.steps, "bytes": arr[3][i] / args.steps}
-                  for i in range(ng)}
     if world > 1:
         dist.barrier()
 
@@ -252,6 +293,7 @@ def main():
         e2e_secs += time.perf_counter() - t0
         e2e_toks += int(ol.sum())
         n = len(batch)
+        # ids + per-sentence metadata (row, len, max_steps, P, col_off, col_sent, y, live) + encoder row maps
         h2d += ids.nbytes + n * 40 + 2 * 2 * n * int(lens.max()) * 4 + ids.nbytes + n * 4
         d2h += int(lib.qnmt_last_d2h_bytes(eng._h))
 
@@ -266,27 +308,42 @@ def main():
     value = toks / secs
     e2e_value = e2e_toks / e2e_secs
 
+    hbm, peak_kind = peaks()
+    kern = kernel_rooflines(all_rows, hbm, peak_kind) if all_rows else {}
+    roof = None
+    if kern:
+        dom = max(kern, key=lambda k: kern[k]["us_per_launch"])
+        roof = dict(kern[dom])
+        roof["kernel"] = dom
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        first = batch_for(args.warmup, 0, 1, sents)
-        cpu, outs = cpu_baseline(params, first, args.cpu_sample)
-        cpu["gpu_match"] = None
+        first = batch_for(args.warmup, 0, 1, sents)[:args.cpu_sample]
+        outs, dt, cores = cpu_translate(params, first)
+        ctoks = sum(len(o[0]) for o in outs)
+        gout, gol, glp = first_result
+        match = sum(1 for i, o in enumerate(outs)
+                    if o[0] == gout[i, :gol[i]].tolist() and o[1] == glp[i])
+        cpu = {"value": ctoks / dt, "unit": "tokens/s", "cores": cores, "kind": "port",
+               "sample": f"first {len(first)} sentences of the first timed batch (beam 5, V_tgt 50000), "
+                         f"oracle/qnmt_oracle.py numpy port, {cores} threads, {dt:.1f} s",
+               "gpu_outputs_identical": f"{match}/{len(first)}"}
     if rank == 0:
-        line = {"metric": "tokens/sec (int8 beam-5 decode, target tokens excl. EOS)",
-                "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+        line = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": 1000 * secs / args.steps,
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int8",
                 "data": "synthetic (seeded N(0,0.05) weights, uniform token ids)",
                 "config": {"workload": WORKLOAD, "sentences_per_gpu_step": PER_GPU,
                            "parallelism": f"sentence-sharded x{world} (no collective)",
-                           "l2": "flushed (512 MB write) before every timed step"},
+                           "l2": "flushed (512 MB write) before every timed step",
+                           "decode_loop": "CUDA-graph steps, device-side live count"},
                 "sentences_per_s": world * PER_GPU * args.steps / secs,
                 "step_ms": step_ms,
                 "e2e": {"value": e2e_value, "unit": "tokens/s", "h2d_bytes_per_step": h2d // args.steps,
                         "d2h_bytes_per_step": d2h // args.steps},
                 "gpu_launches": launches,
-                "roofline": None,
-                "phases_ms_per_step": {k: round(v["ms"], 3) for k, v in phases.items()} if phases else None,
+                "roofline": roof,
+                "kernels": kern,
                 "cpu_baseline": cpu,
                 "clocks": clocks}
         print(json.dumps(line), flush=True)

@@ -272,6 +272,16 @@ int64_t qnmt_kernel_launches(void);
  * with one host sync per step.  Results are identical.  Returns old value. */
 int qnmt_engine_set_graphs(qnmt_engine* e, int enable);
 
+/* Device-clock stamps (%globaltimer) inside the captured decode steps, for
+ * live per-kernel timing in graph mode.  After a decode, _read copies one row
+ * of QNMT_STAMP_COLS int64 per executed step: [step start, attention start,
+ * attention end, top-k start, top-k end, vocab GEMM start, vocab GEMM end,
+ * (unused), live columns N, sum of source lengths of live sentences];
+ * returns the number of rows. */
+#define QNMT_STAMP_COLS 10
+int qnmt_engine_stamps(qnmt_engine* e, int enable);
+int qnmt_engine_stamps_read(qnmt_engine* e, int64_t* out, int32_t max_rows, void* stream);
+
 /* Phase profiler (forces the eager loop while enabled): CUDA events on the engine stream around the kernel groups
  * of a decode (0 encoder, 1 embed, 2 quantize, 3 decoder GEMMs, 4 GRU gates,
  * 5 attention, 6 vocab GEMM, 7 top-k, 8 search, 9 gather, 10 misc).

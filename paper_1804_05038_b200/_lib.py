@@ -52,6 +52,8 @@ SIGNATURES = {
     "qnmt_set_topk_exact": (I32, [I32]),
     "qnmt_engine_profile": (I32, [P, I32]),
     "qnmt_engine_set_graphs": (I32, [P, I32]),
+    "qnmt_engine_stamps": (I32, [P, I32]),
+    "qnmt_engine_stamps_read": (I32, [P, P, I32, P]),
     "qnmt_engine_profile_read": (I32, [P, P, P, P, P]),
 }
 

@@ -54,14 +54,18 @@ __device__ __forceinline__ float tanh_fast(float x) {
 }
 
 // win = max(4e-4, st * 2e-6) bounds |v_fast - v_exact| (+ rounding) with margin.
+// No XU-pipe ops besides the two MUFU: floor(|v| + 1/2) equals round-to-nearest-
+// even(|v|) except at exact ties |v| = k + 1/2, which lie inside the unsafe window
+// (handled exactly); the rounding uses the 1.5*2^23 magic add, whose low mantissa
+// bits are the integer code.
 __device__ __forceinline__ int att_code_fast(float x, float st, float win, bool& unsafe) {
     const float v = __fmul_rn(tanh_fast(x), st);
-    const float r = __fadd_rn(fabsf(v), 0.5f);
-    const float q = floorf(r);
-    const float f = r - q;
-    unsafe = (f < win) | (f > 1.0f - win);
-    const float qc = fminf(q, 127.0f);
-    return (int)(v < 0.0f ? -qc : qc);
+    const float av = fminf(fabsf(v), 127.0f);
+    const float m = __fadd_rn(av, 12582912.0f);            // 1.5 * 2^23
+    const float d = __fsub_rn(av, __fsub_rn(m, 12582912.0f));   // av - rint(av), exact
+    unsafe = fabsf(d) > 0.5f - win;
+    const int q = __float_as_int(m) - 0x4B400000;
+    return v < 0.0f ? -q : q;
 }
 __device__ __noinline__ int att_code_exact(float x, float st) { return quant_code(tanh_b(x), st); }
 

@@ -195,6 +195,9 @@ struct qnmt_engine {
     int32_t* rng_off = nullptr;  // [S] column ranges for qnmt_decoder_step callers
     int32_t* rng_cnt = nullptr;
     int32_t* d_step = nullptr;
+    int graph_kernels = 1;        // kernel nodes in one captured step graph
+    bool stamp_on = false;        // device-clock stamps in captured steps (qnmt_engine_stamps)
+    long long* stamps = nullptr;  // [hist_steps][ST_COLS]
     cudaStream_t cap_stream = nullptr;
     std::vector<std::pair<std::pair<int, int>, std::pair<cudaGraphExec_t, cudaGraphExec_t>>> graphs;
 };
@@ -385,6 +388,46 @@ struct StepIO {
     const float* att_minmax;       // [nseg][2][A] column extrema of att_proj (nullable)
 };
 
+// ---------------------------------------------------------------------------
+// Device-clock stamps inside captured decode steps (for live per-kernel timing
+// in graph mode, where host events cannot bracket single kernels).  Row t of
+// e->stamps holds %globaltimer at ST_* points of step t, the live column count
+// and the sum of source lengths of live sentences (algorithmic-work accounting).
+// ---------------------------------------------------------------------------
+enum { ST_STEP0 = 0, ST_ATT0, ST_ATT1, ST_TOPK0, ST_TOPK1, ST_VOC0, ST_VOC1, ST_STEP1, ST_N, ST_SUML, ST_COLS };
+
+__global__ void k_stamp(long long* stamps, const int32_t* step_dev, int slot, const int32_t* n_dev,
+                        const int32_t* P, const int32_t* len, int n_sent) {
+    const int t = *step_dev;
+    long long* row = stamps + (int64_t)t * ST_COLS;
+    if (slot == ST_ATT0) {   // also record the work descriptors of this step
+        __shared__ int red[32];
+        int sl = 0;
+        for (int s = threadIdx.x; s < n_sent; s += blockDim.x) sl += P[s] > 0 ? len[s] : 0;
+        sl = warp_sum(sl);
+        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = sl;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            long long tot = 0;
+            for (int w = 0; w < (int)(blockDim.x >> 5); ++w) tot += red[w];
+            row[ST_SUML] = tot;
+            row[ST_N] = *n_dev;
+        }
+    }
+    if (threadIdx.x == 0) {
+        long long g;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+        row[slot] = g;
+    }
+}
+
+static int stamp(qnmt_engine* e, int slot, const StepIO& io, cudaStream_t st) {
+    if (!e->stamp_on || !tl_ndev || !e->stamps) return QNMT_OK;   // graph-captured steps only
+    k_stamp<<<1, 256, 0, st>>>(e->stamps, e->d_step, slot, tl_ndev, io.sent_ncols, io.sent_len, io.nseg);
+    QNMT_CHECK_LAUNCH("k_stamp");
+    return QNMT_OK;
+}
+
 static int gru_cell(qnmt_engine* e, const Cell& c, int64_t N, int nseg, const int32_t* seg,
                     const int8_t* qx, const float* sx, const int8_t* qh, const float* sh,
                     const float* h, float* h_out, cudaStream_t st) {
@@ -424,9 +467,11 @@ static int step_core(qnmt_engine* e, const StepIO& io, cudaStream_t st) {
     prof_mark(e, PG_GEMM, st, 2.0 * N * A * H, (double)A * H);
     TRY(gemm(m->u_att, A, H, m->u_att_s, A, e->q_q, N, H, e->sc_q, seg, nullptr, e->u, A, 0, st));
     prof_mark(e, PG_ATT, st);
+    TRY(stamp(e, ST_ATT0, io, st));
     TRY(attention_launch(e->u, A, N, io.sent_col_off, io.sent_ncols, io.nseg, io.att_proj, io.att_minmax, io.states,
                          io.sent_row, io.sent_len, io.max_len, A, 2 * H, m->v, m->v_s, e->ctx, 2 * H,
                          io.alpha, io.lda, e->att_scratch, e->err, st));
+    TRY(stamp(e, ST_ATT1, io, st));
     prof_mark(e, PG_QUANT, st);
     TRY(quantize_launch(e->ctx, N, 2 * H, 2 * H, seg, ns, e->q_ctx, 2 * H, e->sc_ctx, e->seg_bits, 1,
                         e->err, st));
@@ -453,8 +498,10 @@ static int step_core(qnmt_engine* e, const StepIO& io, cudaStream_t st) {
     prof_mark(e, PG_QUANT, st);
     TRY(quantize_launch(e->ro, N, R, R, seg, ns, e->q_ro, R, e->sc_ro, e->seg_bits, 1, e->err, st));
     prof_mark(e, PG_GEMM_VOCAB, st, 2.0 * N * V * R, (double)V * R + (double)N * R + 4.0 * N * V);
+    TRY(stamp(e, ST_VOC0, io, st));
     TRY(gemm(m->w_vocab, V, R, m->w_vocab_s, V, e->q_ro, N, R, e->sc_ro, seg, m->b_vocab, io.logits, V,
              0, st));
+    TRY(stamp(e, ST_VOC1, io, st));
     return QNMT_OK;
 }
 
@@ -469,10 +516,11 @@ static int grow_history(qnmt_engine* e, int steps) {
     if (e->hblock) cudaFree(e->hblock);
     size_t S = e->S, B = e->B, T = steps;
     size_t fin_cap = (T + 1) * B;
-    size_t bytes = S * fin_cap * (8 + 4 + 4 + 4) + 2 * S * T * B * 4 + 4096;
+    size_t bytes = S * fin_cap * (8 + 4 + 4 + 4) + 2 * S * T * B * 4 + (T + 1) * ST_COLS * 8 + 4096;
     QNMT_CUDA(cudaMalloc(&e->hblock, bytes));
     e->hblock_bytes = bytes;
     Arena a{e->hblock, bytes, 0};
+    e->stamps = a.take<long long>((T + 1) * ST_COLS);
     e->fin_score = a.take<double>(S * fin_cap);
     e->fin_step = a.take<int32_t>(S * fin_cap);
     e->fin_slot = a.take<int32_t>(S * fin_cap);
@@ -666,6 +714,25 @@ int qnmt_engine_destroy(qnmt_engine* e) {
     return QNMT_OK;
 }
 
+int qnmt_engine_stamps(qnmt_engine* e, int enable) {
+    int old = e->stamp_on ? 1 : 0;
+    e->stamp_on = enable != 0;
+    return old;
+}
+
+int qnmt_engine_stamps_read(qnmt_engine* e, int64_t* out, int32_t max_rows, void* stream) {
+    cudaStream_t st = as_stream(stream);
+    int32_t steps = 0;
+    QNMT_CUDA(cudaMemcpyAsync(&steps, e->d_step, 4, cudaMemcpyDeviceToHost, st));
+    QNMT_CUDA(cudaStreamSynchronize(st));
+    int rows = std::min(std::min(steps, max_rows), e->hist_steps);
+    if (rows > 0) {
+        QNMT_CUDA(cudaMemcpyAsync(out, e->stamps, (size_t)rows * ST_COLS * 8, cudaMemcpyDeviceToHost, st));
+        QNMT_CUDA(cudaStreamSynchronize(st));
+    }
+    return rows;
+}
+
 int qnmt_engine_set_graphs(qnmt_engine* e, int enable) {
     int old = e->use_graphs ? 1 : 0;
     e->use_graphs = enable != 0;
@@ -744,9 +811,12 @@ static int capture_step(qnmt_engine* e, int cur, int n, int beam, int k_list, cu
         StepIO io{NM, n, e->col_sent[cur], e->y[cur], e->st_s[cur], e->st_sp[cur], e->enc_states, e->enc_att,
                   e->sent_row, e->sent_len, e->L, e->s_int, e->s_new, e->logits, nullptr, 0,
                   e->col_off, e->P, e->att_mm};
-        rc = step_core(e, io, cs);
+        rc = stamp(e, ST_STEP0, io, cs);
+        if (rc == QNMT_OK) rc = step_core(e, io, cs);
+        if (rc == QNMT_OK) rc = stamp(e, ST_TOPK0, io, cs);
         if (rc == QNMT_OK)
             rc = topk_launch(e->logits, NM, V, V, e->live[cur], k_list, e->cand_score, e->cand_tok, e->err, cs);
+        if (rc == QNMT_OK) rc = stamp(e, ST_TOPK1, io, cs);
         if (rc == QNMT_OK) {
             SearchState ss{e->P, e->col_off, e->done, e->max_steps, e->steps_run, e->fin_cnt, e->fin_best,
                            e->fin_score, e->fin_step, e->fin_slot, e->fin_eos, e->hist_tok, e->hist_par,
@@ -767,6 +837,18 @@ static int capture_step(qnmt_engine* e, int cur, int n, int beam, int k_list, cu
         return rc;
     }
     if (ce != cudaSuccess) return cuda_status(ce, "cudaStreamEndCapture");
+    {   // kernel nodes per step graph (for the launch counter: one graph launch runs all of them)
+        size_t nn = 0;
+        cudaGraphGetNodes(g, nullptr, &nn);
+        std::vector<cudaGraphNode_t> nodes(nn);
+        if (nn) cudaGraphGetNodes(g, nodes.data(), &nn);
+        int kn = 0;
+        for (auto nd : nodes) {
+            cudaGraphNodeType ty;
+            if (cudaGraphNodeGetType(nd, &ty) == cudaSuccess && ty == cudaGraphNodeTypeKernel) ++kn;
+        }
+        e->graph_kernels = kn;
+    }
     ce = cudaGraphInstantiate(out, g, 0);
     cudaGraphDestroy(g);
     if (ce != cudaSuccess) return cuda_status(ce, "cudaGraphInstantiate");
@@ -775,7 +857,7 @@ static int capture_step(qnmt_engine* e, int cur, int n, int beam, int k_list, cu
 
 static int get_step_graphs(qnmt_engine* e, int n, int beam, int k_list, cudaGraphExec_t* g) {
     // history buffers may have been re-allocated: graphs are keyed on the history capacity too
-    const int key2 = beam * 100000 + e->hist_steps;
+    const int key2 = (beam * 100000 + e->hist_steps) * 2 + (e->stamp_on ? 1 : 0);
     for (auto& kv : e->graphs)
         if (kv.first.first == n && kv.first.second == key2) {
             g[0] = kv.second.first;
@@ -857,7 +939,7 @@ static int decode_core(qnmt_engine* e, const int32_t* src_ids, bool ids_on_devic
         constexpr int POLL = 16;
         for (int t = 0; t < Tmax; ++t) {
             QNMT_CUDA(cudaGraphLaunch(g[t & 1], st));
-            count_launch();
+            for (int q = 0; q < e->graph_kernels; ++q) count_launch();
             if ((t + 1) % POLL == 0 && t + 1 < Tmax) {
                 QNMT_CUDA(cudaMemcpyAsync(e->h_pinned, e->d_N + ((t + 1) & 1), 4, cudaMemcpyDeviceToHost, st));
                 QNMT_CUDA(cudaStreamSynchronize(st));

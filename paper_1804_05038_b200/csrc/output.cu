@@ -181,7 +181,7 @@ k_topk(const float* __restrict__ logits, int64_t V, int64_t ld, const double* __
 // The 16-entry f64 table is 128 B = all 32 smem banks, so lookups never
 // conflict.  ~13 f64 ops instead of the general-purpose exp() (~27 DFMA slots).
 __device__ __forceinline__ double exp_neg(double t, const double* __restrict__ tab) {
-    if (t < -700.0) return 0.0;
+    t = fmax(t, -700.0);   // below: contributes < 1e-304 (branch-free range guard)
     // round(t * 16/ln2) without FRND/F2I: add 1.5*2^52 so the integer lands in the low word
     const double kd_m = fma(t, 23.083120654223414, 6755399441055744.0);
     const int k = __double2loint(kd_m);
@@ -317,10 +317,13 @@ k_topk1(const float* __restrict__ logits, int64_t V, int64_t ld, const double* _
                 const double e0 = exp_neg((double)x.x - dm, tab), e1 = exp_neg((double)x.y - dm, tab);
                 const double e2 = exp_neg((double)x.z - dm, tab), e3 = exp_neg((double)x.w - dm, tab);
                 s += (e0 + e1) + (e2 + e3);
-                top3(x.x, v);
-                top3(x.y, v + 1);
-                top3(x.z, v + 2);
-                top3(x.w, v + 3);
+                const float gm = fmaxf(fmaxf(x.x, x.y), fmaxf(x.z, x.w));
+                if (__any_sync(__activemask(), gm > a3)) {   // warp-uniform; rare after the first groups
+                    top3(x.x, v);
+                    top3(x.y, v + 1);
+                    top3(x.z, v + 2);
+                    top3(x.w, v + 3);
+                }
             }
         }
     } else {
