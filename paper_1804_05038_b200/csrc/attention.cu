@@ -22,7 +22,7 @@
 // and only those elements are recomputed with the fp64-exact tanh.
 #include <algorithm>
 
-#include "common.cuh"
+#include "kernels.cuh"
 
 #define TRY_LAUNCH(x) do { int _r = (x); if (_r != QNMT_OK) return _r; } while (0)
 
@@ -245,7 +245,7 @@ __device__ __forceinline__ void att_context_body(const float* __restrict__ score
                                                  const int64_t* __restrict__ sent_row, const int32_t* __restrict__ sent_len,
                                                  int64_t H2, float* __restrict__ ctx, int64_t ldc,
                                                  float* __restrict__ alpha, int64_t lda, int32_t* err_flag,
-                                                 unsigned char* smem_raw) {
+                                                 unsigned char* smem_raw, uint32_t* ctx_segmax) {
     double* ex = reinterpret_cast<double*>(smem_raw);                   // [AMAXP][max_len]
     float* al = reinterpret_cast<float*>(ex + AMAXP * max_len);         // [max_len][AMAXP]
     const int s = blockIdx.y;
@@ -297,21 +297,32 @@ __device__ __forceinline__ void att_context_body(const float* __restrict__ score
 #pragma unroll
         for (int j = 0; j < P; ++j) acc[j] += sv * (double)al[i * AMAXP + j];
     }
+    uint32_t mx = 0;
 #pragma unroll
-    for (int j = 0; j < P; ++j) ctx[(int64_t)(c0 + j) * ldc + c] = __double2float_rn(acc[j]);
+    for (int j = 0; j < P; ++j) {
+        const float v = __double2float_rn(acc[j]);
+        ctx[(int64_t)(c0 + j) * ldc + c] = v;
+        mx = max(mx, __float_as_uint(v) & 0x7fffffffu);
+    }
+    if (ctx_segmax) {   // per-sentence max |ctx| for the next quantization (segment = sentence)
+        const unsigned act = __activemask();   // threads with c >= H2 have returned
+        mx = __reduce_max_sync(act, mx);
+        if ((act & ((1u << lane) - 1u)) == 0 && mx) atomicMax(ctx_segmax + s, mx);
+    }
 }
 
 __global__ void __launch_bounds__(AT)
 k_att_context3(const float* __restrict__ scores, int32_t max_len, const int32_t* __restrict__ sent_col_off,
                const int32_t* __restrict__ sent_ncols, const float* __restrict__ states,
                const int64_t* __restrict__ sent_row, const int32_t* __restrict__ sent_len, int64_t H2,
-               float* __restrict__ ctx, int64_t ldc, float* __restrict__ alpha, int64_t lda, int32_t* err_flag) {
+               float* __restrict__ ctx, int64_t ldc, float* __restrict__ alpha, int64_t lda, int32_t* err_flag,
+               uint32_t* ctx_segmax) {
     extern __shared__ unsigned char smem_raw[];
     const int P = sent_ncols[blockIdx.y];
 #define QNMT_CTX_P(P_)                                                                                      \
     case P_:                                                                                               \
         att_context_body<P_>(scores, max_len, sent_col_off, states, sent_row, sent_len, H2, ctx, ldc, alpha, \
-                             lda, err_flag, smem_raw);                                                     \
+                             lda, err_flag, smem_raw, ctx_segmax);                                         \
         break;
     switch (P) {
         QNMT_CTX_P(1) QNMT_CTX_P(2) QNMT_CTX_P(3) QNMT_CTX_P(4) QNMT_CTX_P(5) QNMT_CTX_P(6) QNMT_CTX_P(7)
@@ -326,7 +337,8 @@ int attention_launch(const float* u, int64_t ldu, int64_t N, const int32_t* sent
                      const int32_t* sent_ncols, int32_t n_sent, const float* att_proj, const float* att_minmax,
                      const float* states, const int64_t* sent_row, const int32_t* sent_len, int32_t max_len,
                      int64_t A, int64_t H2, const int8_t* v_codes, const float* v_scale, float* ctx, int64_t ldc,
-                     float* alpha, int64_t lda, void* scratch, int32_t* err_flag, cudaStream_t st) {
+                     float* alpha, int64_t lda, void* scratch, int32_t* err_flag, cudaStream_t st,
+                     uint32_t* ctx_segmax) {
     if (N <= 0 || n_sent <= 0) return QNMT_OK;
     if (A > (int64_t)AT * AKA) {
         set_error("qnmt_attention: attention dim %lld > %d", (long long)A, AT * AKA);
@@ -347,7 +359,7 @@ int attention_launch(const float* u, int64_t ldu, int64_t N, const int32_t* sent
 if (smem > 48 * 1024)
         QNMT_CUDA(cudaFuncSetAttribute(k_att_context3, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     k_att_context3<<<g2, AT, smem, st>>>(scores, max_len, sent_col_off, sent_ncols, states, sent_row, sent_len, H2,
-                                          ctx, ldc, alpha, lda, err_flag);
+                                          ctx, ldc, alpha, lda, err_flag, ctx_segmax);
     QNMT_CHECK_LAUNCH("k_att_context3");
     return QNMT_OK;
 }

@@ -16,34 +16,12 @@
 #include <numeric>
 #include <vector>
 
-#include "common.cuh"
 #include "gemm.cuh"
+#include "kernels.cuh"
 #include "search.cuh"
 
 namespace qnmt {
 
-int gru_gates_launch(const float* gx, int64_t ldgx, const int32_t* gx_row, const float* gh,
-                     int64_t ldgh, const float* h, int64_t ldh, int64_t N, int64_t H, float* z,
-                     float* rh, int32_t* err_flag, cudaStream_t st);
-int gru_combine_launch(const float* gx, int64_t ldgx, const int32_t* gx_row, const float* ghc,
-                       int64_t ldghc, const float* z, const float* h, int64_t ldh, int64_t N,
-                       int64_t H, float* h_out, int64_t ldo, float* out2, int64_t ld2,
-                       const int32_t* out2_row, int32_t* err_flag, cudaStream_t st);
-int tanh_launch(const float* x, int64_t N, int64_t D, int64_t ldx, float* y, int64_t ldy,
-                int32_t* err_flag, cudaStream_t st);
-int embed_gather_launch(const float* table, int64_t rows, int64_t E, const int32_t* ids, int64_t n,
-                        float* out, int64_t ldo, int32_t* err_flag, cudaStream_t st);
-int attention_launch(const float* u, int64_t ldu, int64_t N, const int32_t* sent_col_off,
-                     const int32_t* sent_ncols, int32_t n_sent, const float* att_proj, const float* att_minmax,
-                     const float* states, const int64_t* sent_row, const int32_t* sent_len, int32_t max_len, int64_t A, int64_t H2,
-                     const int8_t* v_codes, const float* v_scale, float* ctx, int64_t ldc, float* alpha,
-                     int64_t lda, void* scratch, int32_t* err_flag, cudaStream_t st);
-int att_minmax_launch(const float* att_proj, const int64_t* sent_row, const int32_t* sent_len, int32_t n_sent,
-                      int64_t A, float* mm, cudaStream_t st);
-int col_ranges_launch(const int32_t* col_sent, int64_t N, int32_t n_sent, int32_t* off, int32_t* cnt,
-                      cudaStream_t st);
-int topk_launch(const float* logits, int64_t N, int64_t V, int64_t ld, const double* live, int32_t k,
-                double* cand_score, int32_t* cand_tok, int32_t* err_flag, cudaStream_t st);
 
 struct Cell {
     const int8_t* wx;
@@ -120,6 +98,7 @@ struct qnmt_engine {
     float* ghc2;             // [S][2][H]
     int32_t* enc_rows;       // [L][2S] gx rows per step
     int32_t* enc_out_rows;   // [L][2S] states half-rows per step
+    uint32_t* enc_qm;        // [L+1][2][2S] fused max-abs bits of h2 (slot 0) / rh2 (slot 1) per step
     int8_t* q_states;        // [PMAX][2H]
     float* sc_sent;          // [S]
     int32_t* pos_sent;       // [PMAX] sentence of each position
@@ -159,6 +138,7 @@ struct qnmt_engine {
     float* logits;           // [N][V]
     void* att_scratch;
     float* att_mm;           // [S][2][A] per-sentence column max / min of att_proj
+    uint32_t* qm[3];         // [QM_COUNT][S] fused quantization max-abs bits: ping-pong + external steps
     // translate loop state
     float* st_s[2];          // [N][H] s
     float* st_sp[2];         // [N][H] s_prime
@@ -203,6 +183,11 @@ struct qnmt_engine {
 };
 
 namespace qnmt {
+
+// Slots of the fused quantization statistics of one decoder step: every
+// quantized activation's per-segment max-abs (u32 bits) is produced by the
+// kernel that writes the activation, so each quantization is one encode pass.
+enum { QM_EMB = 0, QM_S, QM_SP, QM_RH0, QM_SI, QM_CTX, QM_RH1, QM_SN, QM_RO, QM_COUNT };
 
 enum { PG_ENCODER = 0, PG_EMBED, PG_QUANT, PG_GEMM, PG_GRU, PG_ATT, PG_GEMM_VOCAB, PG_TOPK, PG_SEARCH,
        PG_GATHER, PG_MISC, PG_COUNT };
@@ -319,29 +304,34 @@ static int encode_core(qnmt_engine* e, const int32_t* ids_dev, const int32_t* le
                  e->gx_enc + d * 3 * H, 6 * H, 0, st));
     }
     QNMT_CUDA(cudaMemsetAsync(e->h2, 0, sizeof(float) * (size_t)n * 2 * H, st));
+    // per-step max-abs bits (column c = its own segment): the gates kernel of step t
+    // produces rh2's, the combine kernel of step t the next step's h2's
+    QNMT_CUDA(cudaMemsetAsync(e->enc_qm, 0, sizeof(uint32_t) * (size_t)(Lmax + 1) * 4 * n, st));
     for (int t = 0; t < Lmax; ++t) {
         int na = 0;
         while (na < n && len[perm[na]] > t) ++na;
         int64_t N2 = 2 * (int64_t)na;
         const int32_t* gxr = e->enc_rows + (size_t)t * 2 * n;
         const int32_t* outr = e->enc_out_rows + (size_t)t * 2 * n;
-        TRY(quantize_launch(e->h2, N2, H, H, e->iota, (int32_t)N2, e->q_h2, H, e->sc_h2, e->seg_bits, 1,
-                            e->err, st));
+        uint32_t* qm_h = e->enc_qm + (size_t)t * 4 * n;
+        uint32_t* qm_rh = qm_h + 2 * n;
+        uint32_t* qm_hn = qm_h + 4 * n;
+        TRY(quantize_encode_launch(e->h2, N2, H, H, e->iota, e->q_h2, H, e->sc_h2, qm_h, 1, e->err, st));
         for (int d = 0; d < 2; ++d) {
             const Cell& c = m->cell[d];
             TRY(gemm(c.uzr, 2 * H, H, c.uzr_s, H, e->q_h2 + d * H, na, 2 * H, e->sc_h2,
                      d ? e->odd : e->even, nullptr, e->gh2 + d * 2 * H, 4 * H, 0, st));
         }
-        TRY(gru_gates_launch(e->gx_enc, 3 * H, gxr, e->gh2, 2 * H, e->h2, H, N2, H, e->z2, e->rh2, e->err, st));
-        TRY(quantize_launch(e->rh2, N2, H, H, e->iota, (int32_t)N2, e->q_rh2, H, e->sc_rh2, e->seg_bits,
-                            1, e->err, st));
+        TRY(gru_gates_launch(e->gx_enc, 3 * H, gxr, e->gh2, 2 * H, e->h2, H, N2, H, e->z2, e->rh2, e->err, st,
+                             qm_rh, nullptr));
+        TRY(quantize_encode_launch(e->rh2, N2, H, H, e->iota, e->q_rh2, H, e->sc_rh2, qm_rh, 1, e->err, st));
         for (int d = 0; d < 2; ++d) {
             const Cell& c = m->cell[d];
             TRY(gemm(c.uc, H, H, c.uc_s, H, e->q_rh2 + d * H, na, 2 * H, e->sc_rh2, d ? e->odd : e->even,
                      nullptr, e->ghc2 + d * H, 2 * H, 0, st));
         }
         TRY(gru_combine_launch(e->gx_enc, 3 * H, gxr, e->ghc2, H, e->z2, e->h2, H, N2, H, e->h2, H,
-                               states, H, outr, e->err, st));
+                               states, H, outr, e->err, st, qm_hn, nullptr));
     }
     // att_proj = enc_proj(states) with one scale per sentence over [2H, l] (layers.py:343)
     TRY(quantize_launch(states, P, 2 * H, 2 * H, e->pos_sent, n, e->q_states, 2 * H, e->sc_sent,
@@ -386,6 +376,8 @@ struct StepIO {
     const int32_t* sent_col_off;   // [nseg] first column of each sentence (columns grouped by sentence)
     const int32_t* sent_ncols;     // [nseg] live columns of each sentence
     const float* att_minmax;       // [nseg][2][A] column extrema of att_proj (nullable)
+    uint32_t* qm;                  // [QM_COUNT][S] this step's max-abs bits (zeroed but for QM_S/QM_SP)
+    bool qm_ready;                 // QM_S / QM_SP already hold the maxima of s / sp (gather_rows)
 };
 
 // ---------------------------------------------------------------------------
@@ -430,20 +422,20 @@ static int stamp(qnmt_engine* e, int slot, const StepIO& io, cudaStream_t st) {
 
 static int gru_cell(qnmt_engine* e, const Cell& c, int64_t N, int nseg, const int32_t* seg,
                     const int8_t* qx, const float* sx, const int8_t* qh, const float* sh,
-                    const float* h, float* h_out, cudaStream_t st) {
+                    const float* h, float* h_out, uint32_t* rh_max, uint32_t* out_max, cudaStream_t st) {
     const int64_t H = e->m->H;
     prof_mark(e, PG_GEMM, st, 2.0 * N * (3 * H * c.in + 2 * H * H), 3.0 * H * c.in + 2.0 * H * H);
     TRY(gemm(c.wx, 3 * H, c.in, c.wx_s, H, qx, N, c.in, sx, seg, c.bx, e->gx, 3 * H, 0, st));
     TRY(gemm(c.uzr, 2 * H, H, c.uzr_s, H, qh, N, H, sh, seg, nullptr, e->gh, 2 * H, 0, st));
     prof_mark(e, PG_GRU, st);
-    TRY(gru_gates_launch(e->gx, 3 * H, nullptr, e->gh, 2 * H, h, H, N, H, e->z, e->rh, e->err, st));
+    TRY(gru_gates_launch(e->gx, 3 * H, nullptr, e->gh, 2 * H, h, H, N, H, e->z, e->rh, e->err, st, rh_max, seg));
     prof_mark(e, PG_QUANT, st);
-    TRY(quantize_launch(e->rh, N, H, H, seg, nseg, e->q_rh, H, e->sc_rh, e->seg_bits, 1, e->err, st));
+    TRY(quantize_encode_launch(e->rh, N, H, H, seg, e->q_rh, H, e->sc_rh, rh_max, 1, e->err, st));
     prof_mark(e, PG_GEMM, st, 2.0 * N * H * H, (double)H * H);
     TRY(gemm(c.uc, H, H, c.uc_s, H, e->q_rh, N, H, e->sc_rh, seg, nullptr, e->ghc, H, 0, st));
     prof_mark(e, PG_GRU, st);
     TRY(gru_combine_launch(e->gx, 3 * H, nullptr, e->ghc, H, e->z, h, H, N, H, h_out, H, nullptr, 0,
-                           nullptr, e->err, st));
+                           nullptr, e->err, st, out_max, seg));
     return QNMT_OK;
 }
 
@@ -453,40 +445,50 @@ static int step_core(qnmt_engine* e, const StepIO& io, cudaStream_t st) {
     const int32_t* seg = io.col_sent;
     const int ns = io.nseg;
     if (N <= 0) return QNMT_OK;
+    auto qm = [&](int slot) { return io.qm + (size_t)slot * e->S; };
+    if (!io.qm_ready) {   // standalone step: the state maxima were not produced by a gather
+        prof_mark(e, PG_QUANT, st);
+        QNMT_CUDA(cudaMemsetAsync(io.qm, 0, sizeof(uint32_t) * QM_COUNT * e->S, st));
+        TRY(quantize_max_launch(io.s, N, H, H, seg, qm(QM_S), st));
+        if (m->aq == 1) TRY(quantize_max_launch(io.sp, N, H, H, seg, qm(QM_SP), st));
+    }
     prof_mark(e, PG_EMBED, st);
-    TRY(embed_gather_launch(m->tgt_embed, V, E, io.y, N, e->emb, E, e->err, st));
+    TRY(embed_gather_launch(m->tgt_embed, V, E, io.y, N, e->emb, E, e->err, st, qm(QM_EMB), seg));
     prof_mark(e, PG_QUANT, st);
-    TRY(quantize_launch(e->emb, N, E, E, seg, ns, e->q_emb, E, e->sc_emb, e->seg_bits, 1, e->err, st));
-    TRY(quantize_launch(io.s, N, H, H, seg, ns, e->q_s, H, e->sc_s, e->seg_bits, 1, e->err, st));
+    TRY(quantize_encode_launch(e->emb, N, E, E, seg, e->q_emb, E, e->sc_emb, qm(QM_EMB), 1, e->err, st));
+    TRY(quantize_encode_launch(io.s, N, H, H, seg, e->q_s, H, e->sc_s, qm(QM_S), 1, e->err, st));
     // s' = GRU_r(emb, s)                                        (layers.py:372)
-    TRY(gru_cell(e, m->cell[2], N, ns, seg, e->q_emb, e->sc_emb, e->q_s, e->sc_s, io.s, io.s_int, st));
+    TRY(gru_cell(e, m->cell[2], N, ns, seg, e->q_emb, e->sc_emb, e->q_s, e->sc_s, io.s, io.s_int, qm(QM_RH0),
+                 qm(QM_SI), st));
     // attention query (layers.py:373)
     const float* query = (m->aq == 1) ? io.sp : io.s_int;
     prof_mark(e, PG_QUANT, st);
-    TRY(quantize_launch(query, N, H, H, seg, ns, e->q_q, H, e->sc_q, e->seg_bits, 1, e->err, st));
+    TRY(quantize_encode_launch(query, N, H, H, seg, e->q_q, H, e->sc_q, qm(m->aq == 1 ? QM_SP : QM_SI), 1,
+                               e->err, st));
     prof_mark(e, PG_GEMM, st, 2.0 * N * A * H, (double)A * H);
     TRY(gemm(m->u_att, A, H, m->u_att_s, A, e->q_q, N, H, e->sc_q, seg, nullptr, e->u, A, 0, st));
     prof_mark(e, PG_ATT, st);
     TRY(stamp(e, ST_ATT0, io, st));
     TRY(attention_launch(e->u, A, N, io.sent_col_off, io.sent_ncols, io.nseg, io.att_proj, io.att_minmax, io.states,
                          io.sent_row, io.sent_len, io.max_len, A, 2 * H, m->v, m->v_s, e->ctx, 2 * H,
-                         io.alpha, io.lda, e->att_scratch, e->err, st));
+                         io.alpha, io.lda, e->att_scratch, e->err, st, qm(QM_CTX)));
     TRY(stamp(e, ST_ATT1, io, st));
     prof_mark(e, PG_QUANT, st);
-    TRY(quantize_launch(e->ctx, N, 2 * H, 2 * H, seg, ns, e->q_ctx, 2 * H, e->sc_ctx, e->seg_bits, 1,
-                        e->err, st));
+    TRY(quantize_encode_launch(e->ctx, N, 2 * H, 2 * H, seg, e->q_ctx, 2 * H, e->sc_ctx, qm(QM_CTX), 1, e->err,
+                               st));
     // s = GRU_q(ctx, s')                                        (layers.py:375)
     const int8_t* q_si = e->q_q;
     const float* sc_si = e->sc_q;
     if (m->aq == 1) {
-        TRY(quantize_launch(io.s_int, N, H, H, seg, ns, e->q_si, H, e->sc_si, e->seg_bits, 1, e->err, st));
+        TRY(quantize_encode_launch(io.s_int, N, H, H, seg, e->q_si, H, e->sc_si, qm(QM_SI), 1, e->err, st));
         q_si = e->q_si;
         sc_si = e->sc_si;
     }
-    TRY(gru_cell(e, m->cell[3], N, ns, seg, e->q_ctx, e->sc_ctx, q_si, sc_si, io.s_int, io.s_new, st));
+    TRY(gru_cell(e, m->cell[3], N, ns, seg, e->q_ctx, e->sc_ctx, q_si, sc_si, io.s_int, io.s_new, qm(QM_RH1),
+                 qm(QM_SN), st));
     // readout = tanh(((W_s s + b_r) + W_e emb) + W_c ctx)       (layers.py:255-265)
     prof_mark(e, PG_QUANT, st);
-    TRY(quantize_launch(io.s_new, N, H, H, seg, ns, e->q_sn, H, e->sc_sn, e->seg_bits, 1, e->err, st));
+    TRY(quantize_encode_launch(io.s_new, N, H, H, seg, e->q_sn, H, e->sc_sn, qm(QM_SN), 1, e->err, st));
     prof_mark(e, PG_GEMM, st, 2.0 * N * R * (H + E + 2 * H), (double)R * (H + E + 2 * H));
     TRY(gemm(m->w_state, R, H, m->w_state_s, R, e->q_sn, N, H, e->sc_sn, seg, m->b_r, e->ro, R, 0, st));
     TRY(gemm(m->w_embed, R, E, m->w_embed_s, R, e->q_emb, N, E, e->sc_emb, seg, nullptr, e->ro, R,
@@ -494,9 +496,9 @@ static int step_core(qnmt_engine* e, const StepIO& io, cudaStream_t st) {
     TRY(gemm(m->w_ctx, R, 2 * H, m->w_ctx_s, R, e->q_ctx, N, 2 * H, e->sc_ctx, seg, nullptr, e->ro, R,
              QNMT_GEMM_ACCUMULATE, st));
     prof_mark(e, PG_MISC, st);
-    TRY(tanh_launch(e->ro, N, R, R, e->ro, R, e->err, st));
+    TRY(tanh_launch(e->ro, N, R, R, e->ro, R, e->err, st, qm(QM_RO), seg));
     prof_mark(e, PG_QUANT, st);
-    TRY(quantize_launch(e->ro, N, R, R, seg, ns, e->q_ro, R, e->sc_ro, e->seg_bits, 1, e->err, st));
+    TRY(quantize_encode_launch(e->ro, N, R, R, seg, e->q_ro, R, e->sc_ro, qm(QM_RO), 1, e->err, st));
     prof_mark(e, PG_GEMM_VOCAB, st, 2.0 * N * V * R, (double)V * R + (double)N * R + 4.0 * N * V);
     TRY(stamp(e, ST_VOC0, io, st));
     TRY(gemm(m->w_vocab, V, R, m->w_vocab_s, V, e->q_ro, N, R, e->sc_ro, seg, m->b_vocab, io.logits, V,
@@ -616,6 +618,7 @@ int qnmt_engine_create(const qnmt_model* m, int32_t max_sentences, int32_t max_s
         e->ghc2 = a.take<float>(2 * S * H);
         e->enc_rows = a.take<int32_t>(L * 2 * S);
         e->enc_out_rows = a.take<int32_t>(L * 2 * S);
+        e->enc_qm = a.take<uint32_t>((L + 1) * 4 * S);
         e->q_states = a.take<int8_t>(P * 2 * H);
         e->sc_sent = a.take<float>(S);
         e->pos_sent = a.take<int32_t>(P);
@@ -654,6 +657,7 @@ int qnmt_engine_create(const qnmt_model* m, int32_t max_sentences, int32_t max_s
         e->logits = a.take<float>(N * V);
         e->att_scratch = a.take<char>(N * (L + 2) * 4 + 2 * S * A * 4 + 1024);
         e->att_mm = a.take<float>(2 * S * A);
+        for (int i = 0; i < 3; ++i) e->qm[i] = a.take<uint32_t>(qnmt::QM_COUNT * S);
         for (int i = 0; i < 2; ++i) {
             e->st_s[i] = a.take<float>(N * H);
             e->st_sp[i] = a.take<float>(N * H);
@@ -782,7 +786,7 @@ int qnmt_decoder_step(qnmt_engine* e, int64_t N, const int32_t* col_sent, int32_
     QNMT_CUDA(cudaMemsetAsync(e->err, 0, 4, st));
     TRY(col_ranges_launch(col_sent, N, n_sent, e->rng_off, e->rng_cnt, st));
     StepIO io{N, n_sent, col_sent, y, s, sp, states, att_proj, sent_row, sent_len, max_len,
-              s_int, s_new, logits, alpha, lda, e->rng_off, e->rng_cnt, nullptr};
+              s_int, s_new, logits, alpha, lda, e->rng_off, e->rng_cnt, nullptr, e->qm[2], false};
     TRY(step_core(e, io, st));
     return check_flag(e, st);
 }
@@ -810,7 +814,7 @@ static int capture_step(qnmt_engine* e, int cur, int n, int beam, int k_list, cu
         NdevScope nd(e->d_N + cur);
         StepIO io{NM, n, e->col_sent[cur], e->y[cur], e->st_s[cur], e->st_sp[cur], e->enc_states, e->enc_att,
                   e->sent_row, e->sent_len, e->L, e->s_int, e->s_new, e->logits, nullptr, 0,
-                  e->col_off, e->P, e->att_mm};
+                  e->col_off, e->P, e->att_mm, e->qm[cur], true};
         rc = stamp(e, ST_STEP0, io, cs);
         if (rc == QNMT_OK) rc = step_core(e, io, cs);
         if (rc == QNMT_OK) rc = stamp(e, ST_TOPK0, io, cs);
@@ -828,7 +832,11 @@ static int capture_step(qnmt_engine* e, int cur, int n, int beam, int k_list, cu
     }
     if (rc == QNMT_OK) {
         NdevScope nd(e->d_N + (cur ^ 1));
-        rc = gather_rows_launch(e->s_new, e->s_int, e->parent_col, NM, H, e->st_s[cur ^ 1], e->st_sp[cur ^ 1], cs);
+        uint32_t* qn = e->qm[cur ^ 1];
+        if (cudaMemsetAsync(qn, 0, sizeof(uint32_t) * QM_COUNT * e->S, cs) != cudaSuccess) rc = QNMT_ERR_CUDA;
+        if (rc == QNMT_OK)
+            rc = gather_rows_launch(e->s_new, e->s_int, e->parent_col, NM, H, e->st_s[cur ^ 1], e->st_sp[cur ^ 1],
+                                    cs, qn + (size_t)QM_S * e->S, qn + (size_t)QM_SP * e->S, e->col_sent[cur ^ 1]);
     }
     cudaGraph_t g = nullptr;
     cudaError_t ce = cudaStreamEndCapture(cs, &g);
@@ -928,6 +936,10 @@ static int decode_core(qnmt_engine* e, const int32_t* src_ids, bool ids_on_devic
     QNMT_CUDA(cudaMemsetAsync(e->steps_run, 0, (size_t)n * 4, st));
     QNMT_CUDA(cudaMemcpyAsync(e->st_s[0], e->enc_s0, (size_t)n * H * 4, cudaMemcpyDeviceToDevice, st));
     QNMT_CUDA(cudaMemcpyAsync(e->st_sp[0], e->enc_s0, (size_t)n * H * 4, cudaMemcpyDeviceToDevice, st));
+    // first step's state maxima (later steps get them from gather_rows); column n = sentence n
+    QNMT_CUDA(cudaMemsetAsync(e->qm[0], 0, sizeof(uint32_t) * QM_COUNT * e->S, st));
+    TRY(quantize_max_launch(e->enc_s0, n, H, H, e->iota, e->qm[0] + (size_t)QM_S * e->S, st));
+    TRY(quantize_max_launch(e->enc_s0, n, H, H, e->iota, e->qm[0] + (size_t)QM_SP * e->S, st));
     const int k_list = (int)std::min<int64_t>(beam, V);
     if (graph_eligible(e)) {
         // device-resident loop: one graph launch per step, live count polled every POLL steps
@@ -953,7 +965,7 @@ static int decode_core(qnmt_engine* e, const int32_t* src_ids, bool ids_on_devic
     for (int t = 0; t < Tmax && N > 0; ++t) {
         StepIO io{N, n, e->col_sent[cur], e->y[cur], e->st_s[cur], e->st_sp[cur], e->enc_states,
                   e->enc_att, e->sent_row, e->sent_len, Lmax, e->s_int, e->s_new, e->logits, nullptr, 0,
-                  e->col_off, e->P, e->att_mm};
+                  e->col_off, e->P, e->att_mm, e->qm[cur], true};
         TRY(step_core(e, io, st));
         prof_mark(e, PG_TOPK, st, 0, 4.0 * N * V);
         TRY(topk_launch(e->logits, N, V, V, e->live[cur], k_list, e->cand_score, e->cand_tok, e->err, st));
@@ -969,7 +981,10 @@ static int decode_core(qnmt_engine* e, const int32_t* src_ids, bool ids_on_devic
         prof_collect(e);
         int64_t N2 = e->h_pinned[0];
         prof_mark(e, PG_GATHER, st);
-        TRY(gather_rows_launch(e->s_new, e->s_int, e->parent_col, N2, H, e->st_s[cur ^ 1], e->st_sp[cur ^ 1], st));
+        uint32_t* qn = e->qm[cur ^ 1];
+        QNMT_CUDA(cudaMemsetAsync(qn, 0, sizeof(uint32_t) * QM_COUNT * e->S, st));
+        TRY(gather_rows_launch(e->s_new, e->s_int, e->parent_col, N2, H, e->st_s[cur ^ 1], e->st_sp[cur ^ 1], st,
+                               qn + (size_t)QM_S * e->S, qn + (size_t)QM_SP * e->S, e->col_sent[cur ^ 1]));
         N = N2;
         cur ^= 1;
     }

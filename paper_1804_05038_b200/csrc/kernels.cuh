@@ -1,0 +1,44 @@
+// kernels.cuh -- internal launch helpers shared by the C ABI wrappers and the engine.
+// Optional trailing `segmax`/`col_seg`: fused per-segment max-abs of the output
+// (u32 bits, atomicMax) for the next quantization (see elementwise.cu).
+#pragma once
+#include "common.cuh"
+
+namespace qnmt {
+
+int gru_gates_launch(const float* gx, int64_t ldgx, const int32_t* gx_row, const float* gh,
+                     int64_t ldgh, const float* h, int64_t ldh, int64_t N, int64_t H, float* z,
+                     float* rh, int32_t* err_flag, cudaStream_t st, uint32_t* segmax = nullptr,
+                     const int32_t* col_seg = nullptr);
+int gru_combine_launch(const float* gx, int64_t ldgx, const int32_t* gx_row, const float* ghc,
+                       int64_t ldghc, const float* z, const float* h, int64_t ldh, int64_t N,
+                       int64_t H, float* h_out, int64_t ldo, float* out2, int64_t ld2,
+                       const int32_t* out2_row, int32_t* err_flag, cudaStream_t st,
+                       uint32_t* segmax = nullptr, const int32_t* col_seg = nullptr);
+int tanh_launch(const float* x, int64_t N, int64_t D, int64_t ldx, float* y, int64_t ldy,
+                int32_t* err_flag, cudaStream_t st, uint32_t* segmax = nullptr,
+                const int32_t* col_seg = nullptr);
+int embed_gather_launch(const float* table, int64_t rows, int64_t E, const int32_t* ids, int64_t n,
+                        float* out, int64_t ldo, int32_t* err_flag, cudaStream_t st,
+                        uint32_t* segmax = nullptr, const int32_t* col_seg = nullptr);
+int attention_launch(const float* u, int64_t ldu, int64_t N, const int32_t* sent_col_off,
+                     const int32_t* sent_ncols, int32_t n_sent, const float* att_proj, const float* att_minmax,
+                     const float* states, const int64_t* sent_row, const int32_t* sent_len, int32_t max_len,
+                     int64_t A, int64_t H2, const int8_t* v_codes, const float* v_scale, float* ctx, int64_t ldc,
+                     float* alpha, int64_t lda, void* scratch, int32_t* err_flag, cudaStream_t st,
+                     uint32_t* ctx_segmax = nullptr);
+int att_minmax_launch(const float* att_proj, const int64_t* sent_row, const int32_t* sent_len, int32_t n_sent,
+                      int64_t A, float* mm, cudaStream_t st);
+int col_ranges_launch(const int32_t* col_sent, int64_t N, int32_t n_sent, int32_t* off, int32_t* cnt,
+                      cudaStream_t st);
+int topk_launch(const float* logits, int64_t N, int64_t V, int64_t ld, const double* live, int32_t k,
+                double* cand_score, int32_t* cand_tok, int32_t* err_flag, cudaStream_t st);
+// encode pass only: seg_maxbits already holds the per-segment max-abs bits
+int quantize_encode_launch(const float* x, int64_t ncols, int64_t K, int64_t ldx, const int32_t* col_seg,
+                           int8_t* q, int64_t ldq, float* scales, const uint32_t* seg_maxbits, int32_t mode,
+                           int32_t* err_flag, cudaStream_t st);
+// max-abs pass only, accumulating into (already zeroed) seg_maxbits
+int quantize_max_launch(const float* x, int64_t ncols, int64_t K, int64_t ldx, const int32_t* col_seg,
+                        uint32_t* seg_maxbits, cudaStream_t st);
+
+}  // namespace qnmt

@@ -9,7 +9,7 @@
 //   has bits >= 0x7f800000, so the same max doubles as the finiteness probe.
 // Pass 2 (k_encode): scale = fl32(127/max) per segment, 128-bit loads of x,
 //   32-bit packed stores of 4 codes.
-#include "common.cuh"
+#include "kernels.cuh"
 
 namespace qnmt {
 
@@ -97,6 +97,32 @@ int quantize_launch(const float* x, int64_t ncols, int64_t K, int64_t ldx, const
     k_encode<<<(unsigned)blocks, QT, 0, st>>>(x, ncols, K, ldx, chunks, chunk_elems, col_seg,
                                              seg_maxbits, q, ldq, scales, mode, err_flag, vec4, tl_ndev);
     QNMT_CHECK_LAUNCH("k_encode");
+    return QNMT_OK;
+}
+
+int quantize_encode_launch(const float* x, int64_t ncols, int64_t K, int64_t ldx, const int32_t* col_seg,
+                           int8_t* q, int64_t ldq, float* scales, const uint32_t* seg_maxbits, int32_t mode,
+                           int32_t* err_flag, cudaStream_t st) {
+    if (ncols <= 0 || K <= 0) return QNMT_OK;
+    bool vec4 = (K % 4 == 0) && (ldx % 4 == 0) && (ldq % 4 == 0) &&
+                ((uintptr_t)x % 16 == 0) && ((uintptr_t)q % 4 == 0);
+    int64_t chunk_elems = 4096;
+    int chunks = (int)cdiv(K, chunk_elems);
+    k_encode<<<(unsigned)(ncols * chunks), QT, 0, st>>>(x, ncols, K, ldx, chunks, chunk_elems, col_seg,
+                                                       seg_maxbits, q, ldq, scales, mode, err_flag, vec4, tl_ndev);
+    QNMT_CHECK_LAUNCH("k_encode");
+    return QNMT_OK;
+}
+
+int quantize_max_launch(const float* x, int64_t ncols, int64_t K, int64_t ldx, const int32_t* col_seg,
+                        uint32_t* seg_maxbits, cudaStream_t st) {
+    if (ncols <= 0 || K <= 0) return QNMT_OK;
+    bool vec4 = (K % 4 == 0) && (ldx % 4 == 0) && ((uintptr_t)x % 16 == 0);
+    int64_t chunk_elems = 4096;
+    int chunks = (int)cdiv(K, chunk_elems);
+    k_seg_maxabs<<<(unsigned)(ncols * chunks), QT, 0, st>>>(x, ncols, K, ldx, chunks, chunk_elems, col_seg,
+                                                           seg_maxbits, vec4, tl_ndev);
+    QNMT_CHECK_LAUNCH("k_seg_maxabs");
     return QNMT_OK;
 }
 

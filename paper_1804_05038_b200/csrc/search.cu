@@ -138,16 +138,34 @@ k_search_step(SearchState ss, int step, int n_sent, int beam, int k_list) {
     }
 }
 
-// next-step state columns: dst[n] = src[parent_col[n]] for the state tensors
+// next-step state columns: dst[n] = src[parent_col[n]] for the state tensors,
+// plus (optionally) the per-segment max-abs bits the next step's quantization needs
 __global__ void k_gather_rows(const float* __restrict__ a, const float* __restrict__ b,
                               const int32_t* __restrict__ parent, int64_t H,
-                              float* __restrict__ a_out, float* __restrict__ b_out, const int32_t* n_dev) {
+                              float* __restrict__ a_out, float* __restrict__ b_out, const int32_t* n_dev,
+                              uint32_t* a_max, uint32_t* b_max, const int32_t* __restrict__ col_seg) {
     int64_t n = blockIdx.x;
     if (beyond(n_dev, n)) return;
     int64_t p = parent[n];
+    uint32_t ma = 0, mb = 0;
     for (int64_t j = threadIdx.x; j < H; j += blockDim.x) {
-        a_out[n * H + j] = a[p * H + j];
-        if (b) b_out[n * H + j] = b[p * H + j];
+        const float va = a[p * H + j];
+        a_out[n * H + j] = va;
+        ma = max(ma, __float_as_uint(va) & 0x7fffffffu);
+        if (b) {
+            const float vb = b[p * H + j];
+            b_out[n * H + j] = vb;
+            mb = max(mb, __float_as_uint(vb) & 0x7fffffffu);
+        }
+    }
+    if (a_max) {
+        const int seg = col_seg[n];
+        ma = warp_max(ma);
+        mb = warp_max(mb);
+        if ((threadIdx.x & 31) == 0) {
+            if (ma) atomicMax(a_max + seg, ma);
+            if (b_max && mb) atomicMax(b_max + seg, mb);
+        }
     }
 }
 
@@ -163,9 +181,10 @@ int search_step_launch(const SearchState& ss, int step, int n_sent, int beam, in
 }
 
 int gather_rows_launch(const float* a, const float* b, const int32_t* parent, int64_t N, int64_t H,
-                       float* a_out, float* b_out, cudaStream_t st) {
+                       float* a_out, float* b_out, cudaStream_t st, uint32_t* a_max, uint32_t* b_max,
+                       const int32_t* col_seg) {
     if (N <= 0) return QNMT_OK;
-    k_gather_rows<<<(unsigned)N, 256, 0, st>>>(a, b, parent, H, a_out, b_out, tl_ndev);
+    k_gather_rows<<<(unsigned)N, 256, 0, st>>>(a, b, parent, H, a_out, b_out, tl_ndev, a_max, b_max, col_seg);
     QNMT_CHECK_LAUNCH("k_gather_rows");
     return QNMT_OK;
 }

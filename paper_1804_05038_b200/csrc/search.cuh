@@ -34,7 +34,9 @@ struct SearchState {
 
 int search_step_launch(const SearchState& ss, int step, int n_sent, int beam, int k_list,
                        cudaStream_t st);
+// optional a_max/b_max: per-segment max |a_out| / |b_out| (segment = col_seg[n]) for the next step
 int gather_rows_launch(const float* a, const float* b, const int32_t* parent, int64_t N, int64_t H,
-                       float* a_out, float* b_out, cudaStream_t st);
+                       float* a_out, float* b_out, cudaStream_t st, uint32_t* a_max = nullptr,
+                       uint32_t* b_max = nullptr, const int32_t* col_seg = nullptr);
 
 }  // namespace qnmt
