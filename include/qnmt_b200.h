@@ -145,7 +145,7 @@ int qnmt_tanh(const float* x, int64_t N, int64_t D, int64_t ldx, float* y, int64
  *   att_minmax (nullable): [n_sent][2][A] per-sentence column max / min of
  *   att_proj (qnmt_attention_stats); computed into scratch when NULL.
  *   ctx: [N][2H] (ldc); alpha (nullable): [N][lda];
- *   scratch: >= 4*(N*max_len + 64 + 2*n_sent*A) bytes
+ *   scratch: >= 4*(N*max_len + 2*N + 128 + 2*n_sent*A) bytes
  * ------------------------------------------------------------------------- */
 int qnmt_attention_stats(const float* att_proj, const int64_t* sent_row, const int32_t* sent_len,
                          int32_t n_sent, int64_t A, float* att_minmax, void* stream);

@@ -33,9 +33,10 @@ constexpr int APC = 4;         // encoder positions per CTA (max / score passes)
 constexpr int AMAXP = 16;      // max live hypotheses per sentence (beam <= 16)
 constexpr int AKA = 8;         // a-elements per thread kept in registers (A <= AT * AKA)
 
-// Fast code of t = tanh(x) at scale st.  Returns the code from tanhf (<= 2 ulp)
-// and sets `unsafe` when fl(|v| + 1/2) is within 2.5e-4 of an integer, where
-// the exact fp64 tanh could give a different floor (att_code_exact).
+// Fast tanh from two MUFU ops, signed form: t = 1 - 2 / (1 + 2^(2x log2 e)).
+// Exhaustive over every f32 x with 2^-24 <= |x| < 64 (benchmarks/tanh_err.cu,
+// profiles/r01_tanh_err.jsonl): |t_fast - tanh(x)| <= 2.37e-7; outside that
+// range t_fast is 0 / +-1 / within the same bound.
 __device__ __forceinline__ float ex2_approx(float x) {
     float y;
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -46,27 +47,17 @@ __device__ __forceinline__ float rcp_approx(float x) {
     asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
 }
-// tanh with absolute error < ~1.2e-6 from two MUFU ops: 1 - 2 / (1 + e^{2|x|})
-__device__ __forceinline__ float tanh_fast(float x) {
-    const float e = ex2_approx(fabsf(x) * 2.8853900817779268f);   // 2 / ln 2
-    const float r = rcp_approx(e + 1.0f);
-    return copysignf(fmaf(-2.0f, r, 1.0f), x);
-}
 
-// win = max(4e-4, st * 2e-6) bounds |v_fast - v_exact| (+ rounding) with margin.
-// No XU-pipe ops besides the two MUFU: floor(|v| + 1/2) equals round-to-nearest-
-// even(|v|) except at exact ties |v| = k + 1/2, which lie inside the unsafe window
-// (handled exactly); the rounding uses the 1.5*2^23 magic add, whose low mantissa
-// bits are the integer code.
-__device__ __forceinline__ int att_code_fast(float x, float st, float win, bool& unsafe) {
-    const float v = __fmul_rn(tanh_fast(x), st);
-    const float av = fminf(fabsf(v), 127.0f);
-    const float m = __fadd_rn(av, 12582912.0f);            // 1.5 * 2^23
-    const float d = __fsub_rn(av, __fsub_rn(m, 12582912.0f));   // av - rint(av), exact
-    unsafe = fabsf(d) > 0.5f - win;
-    const int q = __float_as_int(m) - 0x4B400000;
-    return v < 0.0f ? -q : q;
-}
+// Fast-path rounding window.  v_fast = fl(st - 2 st r) (one FFMA rounding,
+// <= 3.9e-6 at |v| <= 128) differs from the reference's v = fl(fl32(tanh x) * st)
+// by at most st * (2.37e-7 + 3e-8) + 7.7e-6; the window below has >= 1.5x
+// margin on both terms.  Where fl(v + 1.5*2^23) - 1.5*2^23 (round-to-nearest-even,
+// exact) is farther than the window from a half-integer, the reference's
+// floor(|v| + 1/2) (qmath.py:136-142) gives the same integer; otherwise the
+// element is recomputed with the fp64-exact tanh (att_code_exact).
+__device__ __forceinline__ float att_threshold(float st) { return 0.5f - (st * 4e-7f + 1.6e-5f); }
+constexpr float ATT_ST_FAST_MAX = 1.0e6f;   // above: window > 0.5, every element exact
+
 __device__ __noinline__ int att_code_exact(float x, float st) { return quant_code(tanh_b(x), st); }
 
 // load this thread's strided slice of APC att_proj rows (a = tid + AT*k)
@@ -111,15 +102,52 @@ int att_minmax_launch(const float* att_proj, const int64_t* sent_row, const int3
     return QNMT_OK;
 }
 
+// Per-hypothesis scale of the whole [A, l] tanh block (layers.py:226) from the
+// column extrema, and the fast-path threshold: st_thr[c] = {st, att_threshold(st)}.
+// Grid (n_sent, AMAXP): CTA (s, j) handles hypothesis j of sentence s.
 __global__ void __launch_bounds__(AT)
-k_att_score3(const float* __restrict__ u, int64_t ldu, const int32_t* __restrict__ sent_col_off,
+k_att_scale(const float* __restrict__ u, int64_t ldu, const int32_t* __restrict__ sent_col_off,
+            const int32_t* __restrict__ sent_ncols, const float* __restrict__ mm, int64_t A,
+            float2* __restrict__ st_thr, int32_t* err_flag) {
+    __shared__ uint32_t mred[AT / 32];
+    const int s = blockIdx.x, j = blockIdx.y;
+    if (j >= sent_ncols[s]) return;
+    const int c = sent_col_off[s] + j;
+    const float* un = u + (int64_t)c * ldu;
+    const float* mx = mm + ((int64_t)s * 2) * A;
+    const float* mn = mx + A;
+    uint32_t m = 0;
+    for (int64_t a = threadIdx.x; a < A; a += AT) {
+        const float uv = un[a];
+        m = max(m, __float_as_uint(__fadd_rn(mx[a], uv)) & 0x7fffffffu);
+        m = max(m, __float_as_uint(__fadd_rn(mn[a], uv)) & 0x7fffffffu);
+    }
+    m = warp_max(m);
+    if ((threadIdx.x & 31) == 0) mred[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 0; w < AT / 32; ++w) m = max(m, mred[w]);
+        if (m >= 0x7f800000u) {
+            set_flag(err_flag, QNMT_FLAG_NUMERIC);
+            m = 0;
+        }
+        const float tmax = tanh_b(__uint_as_float(m));   // max |fl32(tanh)| = fl32(tanh(max |x|))
+        const float st = (tmax == 0.0f) ? 1.0f : __fdiv_rn(127.0f, tmax);
+        st_thr[c] = make_float2(st, att_threshold(st));
+    }
+}
+
+// scores for APC positions x all P hypotheses of one sentence.  Per element:
+// FADD, FMUL, 2 MUFU, FADD, FFMA, 2 FADD + IADD (magic rounding), FADD, FMNMX,
+// IMAD.  A thread whose max distance to a half-integer falls inside the window
+// rescans its 32 elements and corrects the flagged ones exactly (rare).
+__global__ void __launch_bounds__(AT, 2)
+k_att_score4(const float* __restrict__ u, int64_t ldu, const int32_t* __restrict__ sent_col_off,
              const int32_t* __restrict__ sent_ncols, const float* __restrict__ att_proj,
-             const float* __restrict__ mm, const int64_t* __restrict__ sent_row,
+             const float2* __restrict__ st_thr, const int64_t* __restrict__ sent_row,
              const int32_t* __restrict__ sent_len, int64_t A, const int8_t* __restrict__ v_codes,
-             const float* __restrict__ v_scale, float* __restrict__ scores, int32_t max_len, int32_t* err_flag) {
+             const float* __restrict__ v_scale, float* __restrict__ scores, int32_t max_len) {
     __shared__ int red[AMAXP][APC][AT / 32];
-    __shared__ uint32_t mred[AMAXP][AT / 32];
-    __shared__ float s_st[AMAXP];
     const int s = blockIdx.y;
     const int P = sent_ncols[s];
     const int l = sent_len[s];
@@ -128,95 +156,65 @@ k_att_score3(const float* __restrict__ u, int64_t ldu, const int32_t* __restrict
     const int i1 = min(l, i0 + APC);
     const int c0 = sent_col_off[s];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    // per-hypothesis scale of the whole [A, l] block (layers.py:226) from the column extrema
-    {
-        float mxv[AKA], mnv[AKA];
-#pragma unroll
-        for (int k = 0; k < AKA; ++k) {
-            const int64_t a = threadIdx.x + (int64_t)AT * k;
-            mxv[k] = a < A ? mm[((int64_t)s * 2) * A + a] : 0.0f;
-            mnv[k] = a < A ? mm[((int64_t)s * 2 + 1) * A + a] : 0.0f;
-        }
-        for (int j = 0; j < P; ++j) {
-            const float* un = u + (int64_t)(c0 + j) * ldu;
-            uint32_t m = 0;
-#pragma unroll
-            for (int k = 0; k < AKA; ++k) {
-                const int64_t a = threadIdx.x + (int64_t)AT * k;
-                if (a < A) {
-                    const float uv = un[a];
-                    m = max(m, __float_as_uint(__fadd_rn(mxv[k], uv)) & 0x7fffffffu);
-                    m = max(m, __float_as_uint(__fadd_rn(mnv[k], uv)) & 0x7fffffffu);
-                }
-            }
-            m = warp_max(m);
-            if (lane == 0) mred[j][warp] = m;
-        }
-        __syncthreads();
-        if (threadIdx.x < P) {
-            uint32_t m = 0;
-            for (int w = 0; w < AT / 32; ++w) m = max(m, mred[threadIdx.x][w]);
-            if (m >= 0x7f800000u) {
-                set_flag(err_flag, QNMT_FLAG_NUMERIC);
-                m = 0;
-            }
-            const float tmax = tanh_b(__uint_as_float(m));
-            s_st[threadIdx.x] = (tmax == 0.0f) ? 1.0f : __fdiv_rn(127.0f, tmax);
-        }
-        __syncthreads();
-    }
     float apv[APC][AKA];
     load_ap(att_proj + sent_row[s] * A, A, i0, i1, apv);
     int vv[AKA];
+    float uvv[AKA], unx[AKA];
 #pragma unroll
     for (int k = 0; k < AKA; ++k) {
         const int64_t a = threadIdx.x + (int64_t)AT * k;
         vv[k] = a < A ? (int)v_codes[a] : 0;
+        uvv[k] = a < A ? u[(int64_t)c0 * ldu + a] : 0.0f;
     }
     for (int j = 0; j < P; ++j) {
-        const float st = s_st[j];
-        const float win = fmaxf(4e-4f, st * 2e-6f);
-        const float* un = u + (int64_t)(c0 + j) * ldu;
-        float uvv[AKA];
-#pragma unroll
-        for (int k = 0; k < AKA; ++k) {
-            const int64_t a = threadIdx.x + (int64_t)AT * k;
-            uvv[k] = a < A ? un[a] : 0.0f;
-        }
-        int acc[APC] = {};
-        uint32_t unsafe = 0;   // bit p*AKA + k
-#pragma unroll
-        for (int p = 0; p < APC; ++p) {
-            if (i0 + p >= i1) break;                       // block-uniform
+        if (j + 1 < P) {   // prefetch the next hypothesis' query row
+            const float* un = u + (int64_t)(c0 + j + 1) * ldu;
 #pragma unroll
             for (int k = 0; k < AKA; ++k) {
-                bool uk;
-                const int c = att_code_fast(__fadd_rn(apv[p][k], uvv[k]), st, win, uk);
-                acc[p] += vv[k] * c;                        // vv = 0 for a >= A
-                unsafe |= (uint32_t)uk << (p * AKA + k);
+                const int64_t a = threadIdx.x + (int64_t)AT * k;
+                unx[k] = a < A ? un[a] : 0.0f;
             }
         }
-        if (__any_sync(0xffffffffu, unsafe != 0)) {       // rare: exact fp64 codes for flagged elements
-            while (unsafe) {
-                const int b = __ffs(unsafe) - 1;
-                unsafe &= unsafe - 1;
-                const int p = b / AKA, k = b % AKA;
-                float xv = 0.0f;
+        const float2 sp = st_thr[c0 + j];
+        const float st = sp.x, thr = sp.y, m2st = -2.0f * st;
+        int acc[APC] = {};
+        if (st <= ATT_ST_FAST_MAX) {   // CTA-uniform
+            float dmax = 0.0f;
 #pragma unroll
-                for (int pp = 0; pp < APC; ++pp)
+            for (int p = 0; p < APC; ++p) {
+                if (i0 + p >= i1) break;   // CTA-uniform
 #pragma unroll
-                    for (int kk = 0; kk < AKA; ++kk)
-                        if (pp * AKA + kk == b) xv = __fadd_rn(apv[pp][kk], uvv[kk]);
-                bool dummy;
-                const int fast = att_code_fast(xv, st, win, dummy);
-                const int exact = att_code_exact(xv, st);
-                int vk = 0;
+                for (int k = 0; k < AKA; ++k) {
+                    const float x = __fadd_rn(apv[p][k], uvv[k]);
+                    const float r = rcp_approx(__fadd_rn(ex2_approx(__fmul_rn(x, 2.8853900817779268f)), 1.0f));
+                    const float v = fmaf(m2st, r, st);
+                    const float mg = __fadd_rn(v, 12582912.0f);   // 1.5 * 2^23
+                    dmax = fmaxf(dmax, fabsf(__fsub_rn(v, __fsub_rn(mg, 12582912.0f))));
+                    acc[p] += vv[k] * (__float_as_int(mg) - 0x4B400000);
+                }
+            }
+            if (dmax > thr) {   // rare: some element within the window of a rounding boundary
 #pragma unroll
-                for (int kk = 0; kk < AKA; ++kk)
-                    if (kk == k) vk = vv[kk];
+                for (int p = 0; p < APC; ++p) {
+                    if (i0 + p >= i1) break;
 #pragma unroll
-                for (int pp = 0; pp < APC; ++pp)
-                    if (pp == p) acc[pp] += vk * (exact - fast);
+                    for (int k = 0; k < AKA; ++k) {
+                        const float x = __fadd_rn(apv[p][k], uvv[k]);
+                        const float r = rcp_approx(__fadd_rn(ex2_approx(__fmul_rn(x, 2.8853900817779268f)), 1.0f));
+                        const float v = fmaf(m2st, r, st);
+                        const float mg = __fadd_rn(v, 12582912.0f);
+                        if (fabsf(__fsub_rn(v, __fsub_rn(mg, 12582912.0f))) > thr && vv[k] != 0)
+                            acc[p] += vv[k] * (att_code_exact(x, st) - (__float_as_int(mg) - 0x4B400000));
+                    }
+                }
+            }
+        } else {   // degenerate scale (max |tanh| < 1.3e-4): exact codes throughout
+#pragma unroll
+            for (int p = 0; p < APC; ++p) {
+                if (i0 + p >= i1) break;
+#pragma unroll
+                for (int k = 0; k < AKA; ++k)
+                    if (vv[k] != 0) acc[p] += vv[k] * att_code_exact(__fadd_rn(apv[p][k], uvv[k]), st);
             }
         }
 #pragma unroll
@@ -224,6 +222,8 @@ k_att_score3(const float* __restrict__ u, int64_t ldu, const int32_t* __restrict
             const int t = warp_sum(acc[p]);
             if (lane == 0) red[j][p][warp] = t;
         }
+#pragma unroll
+        for (int k = 0; k < AKA; ++k) uvv[k] = unx[k];
     }
     __syncthreads();
     for (int idx = threadIdx.x; idx < P * APC; idx += AT) {
@@ -231,7 +231,7 @@ k_att_score3(const float* __restrict__ u, int64_t ldu, const int32_t* __restrict
         if (i0 + p >= i1) continue;
         long long t = 0;
         for (int w = 0; w < AT / 32; ++w) t += red[j][p][w];
-        scores[(int64_t)(c0 + j) * max_len + i0 + p] = dequant(t, v_scale[0], s_st[j]);
+        scores[(int64_t)(c0 + j) * max_len + i0 + p] = dequant(t, v_scale[0], st_thr[c0 + j].x);
     }
 }
 
@@ -247,7 +247,7 @@ __device__ __forceinline__ void att_context_body(const float* __restrict__ score
                                                  float* __restrict__ alpha, int64_t lda, int32_t* err_flag,
                                                  unsigned char* smem_raw, uint32_t* ctx_segmax) {
     double* ex = reinterpret_cast<double*>(smem_raw);                   // [AMAXP][max_len]
-    float* al = reinterpret_cast<float*>(ex + AMAXP * max_len);         // [max_len][AMAXP]
+    double* al = ex + AMAXP * max_len;   // [max_len][AMAXP] f32 alpha widened once (no per-use F2F)
     const int s = blockIdx.y;
     const int l = sent_len[s];
     const int c0 = sent_col_off[s];
@@ -271,7 +271,7 @@ __device__ __forceinline__ void att_context_body(const float* __restrict__ score
         sum = __shfl_sync(0xffffffffu, sum, 0);
         for (int i = lane; i < l; i += 32) {
             const float a = __double2float_rn(ex[j * max_len + i] / sum);
-            al[i * AMAXP + j] = a;
+            al[i * AMAXP + j] = (double)a;
             if (alpha && blockIdx.x == 0) alpha[(int64_t)(c0 + j) * lda + i] = a;
         }
     }
@@ -290,12 +290,12 @@ __device__ __forceinline__ void att_context_body(const float* __restrict__ score
 #pragma unroll
         for (int q = 0; q < 4; ++q)
 #pragma unroll
-            for (int j = 0; j < P; ++j) acc[j] += (double)sv[q] * (double)al[(i + q) * AMAXP + j];
+            for (int j = 0; j < P; ++j) acc[j] += (double)sv[q] * al[(i + q) * AMAXP + j];
     }
     for (; i < l; ++i) {
         const double sv = (double)st[(int64_t)i * H2];
 #pragma unroll
-        for (int j = 0; j < P; ++j) acc[j] += sv * (double)al[i * AMAXP + j];
+        for (int j = 0; j < P; ++j) acc[j] += sv * al[i * AMAXP + j];
     }
     uint32_t mx = 0;
 #pragma unroll
@@ -344,17 +344,22 @@ int attention_launch(const float* u, int64_t ldu, int64_t N, const int32_t* sent
         set_error("qnmt_attention: attention dim %lld > %d", (long long)A, AT * AKA);
         return QNMT_ERR_SHAPE;
     }
+    // scratch: scores [N][max_len] | st_thr [N] float2 | (column extrema [n_sent][2][A])
     float* scores = reinterpret_cast<float*>(scratch);
+    float2* st_thr = reinterpret_cast<float2*>(scores + ((N * max_len + 63) / 64) * 64);
     if (!att_minmax) {   // extrema not supplied by the caller: compute them into scratch
-        float* mm = scores + ((N * max_len + 63) / 64) * 64;
+        float* mm = reinterpret_cast<float*>(st_thr) + ((2 * N + 63) / 64) * 64;
         TRY_LAUNCH(att_minmax_launch(att_proj, sent_row, sent_len, n_sent, A, mm, st));
         att_minmax = mm;
     }
+    k_att_scale<<<dim3((unsigned)n_sent, AMAXP), AT, 0, st>>>(u, ldu, sent_col_off, sent_ncols, att_minmax, A,
+                                                              st_thr, err_flag);
+    QNMT_CHECK_LAUNCH("k_att_scale");
     dim3 g1((unsigned)cdiv(max_len, APC), (unsigned)n_sent);
-    k_att_score3<<<g1, AT, 0, st>>>(u, ldu, sent_col_off, sent_ncols, att_proj, att_minmax, sent_row, sent_len, A,
-                                    v_codes, v_scale, scores, max_len, err_flag);
-    QNMT_CHECK_LAUNCH("k_att_score3");
-    const size_t smem = (size_t)AMAXP * max_len * (sizeof(float) + sizeof(double));
+    k_att_score4<<<g1, AT, 0, st>>>(u, ldu, sent_col_off, sent_ncols, att_proj, st_thr, sent_row, sent_len, A,
+                                    v_codes, v_scale, scores, max_len);
+    QNMT_CHECK_LAUNCH("k_att_score4");
+    const size_t smem = (size_t)AMAXP * max_len * 2 * sizeof(double);
     const dim3 g2((unsigned)cdiv(H2, AT), (unsigned)n_sent);
 if (smem > 48 * 1024)
         QNMT_CUDA(cudaFuncSetAttribute(k_att_context3, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

@@ -72,6 +72,25 @@ def test_ops_vs_oracle(specs, small, tag):
     assert np.array_equal(lp, g[f"{p}_step_lp"])
 
 
+@pytest.mark.parametrize("scale", [1e-7, 1e-4, 1e-2, 1.0, 40.0])
+@pytest.mark.parametrize("P", [1, 5, 16])
+def test_attention_magnitudes(specs, small, scale, P):
+    """Attention over query / att_proj magnitudes that drive the per-hypothesis
+    scale from ~1e9 (every code from the exact fp64 path) to saturation, and
+    1..16 hypotheses per sentence: bit-identical to the oracle."""
+    net, om, qm, _ = net_and_oracle(specs, "med")
+    g = small
+    enc = net.encode(g["medB_src"])
+    rng = np.random.default_rng(int(P * 1000 + np.log10(scale) * 10 + 500))
+    h = (rng.normal(0, 0.5, (om.dims.hidden, P)) * scale).astype(F32)
+    att_proj = (enc.att_proj * F32(scale)).astype(F32)
+    enc2 = pb.EncoderStates(enc.states, att_proj, enc.s0)
+    ctx, alpha = pb.attend(net.attention, h, enc2)
+    ctx_o, alpha_o = om.attend(h, enc.states, att_proj)
+    assert np.array_equal(alpha, alpha_o)
+    assert np.array_equal(ctx, ctx_o)
+
+
 @pytest.mark.parametrize("tag", MODELS)
 def test_output_net_per_op_path(specs, tag):
     """OutputNet.logits via the per-op path equals the oracle (layers.py:255-266)."""
