@@ -117,10 +117,14 @@ k_att_scale(const float* __restrict__ u, int64_t ldu, const int32_t* __restrict_
     const float* mx = mm + ((int64_t)s * 2) * A;
     const float* mn = mx + A;
     uint32_t m = 0;
-    for (int64_t a = threadIdx.x; a < A; a += AT) {
-        const float uv = un[a];
-        m = max(m, __float_as_uint(__fadd_rn(mx[a], uv)) & 0x7fffffffu);
-        m = max(m, __float_as_uint(__fadd_rn(mn[a], uv)) & 0x7fffffffu);
+#pragma unroll
+    for (int k = 0; k < AKA; ++k) {   // A <= AT * AKA: all loads in flight at once
+        const int64_t a = threadIdx.x + (int64_t)AT * k;
+        if (a < A) {
+            const float uv = un[a];
+            m = max(m, __float_as_uint(__fadd_rn(mx[a], uv)) & 0x7fffffffu);
+            m = max(m, __float_as_uint(__fadd_rn(mn[a], uv)) & 0x7fffffffu);
+        }
     }
     m = warp_max(m);
     if ((threadIdx.x & 31) == 0) mred[threadIdx.x >> 5] = m;
@@ -166,16 +170,18 @@ k_att_score4(const float* __restrict__ u, int64_t ldu, const int32_t* __restrict
         vv[k] = a < A ? (int)v_codes[a] : 0;
         uvv[k] = a < A ? u[(int64_t)c0 * ldu + a] : 0.0f;
     }
+    float2 sp = st_thr[c0];
     for (int j = 0; j < P; ++j) {
-        if (j + 1 < P) {   // prefetch the next hypothesis' query row
+        float2 spx = sp;
+        if (j + 1 < P) {   // prefetch the next hypothesis' query row and scale
             const float* un = u + (int64_t)(c0 + j + 1) * ldu;
 #pragma unroll
             for (int k = 0; k < AKA; ++k) {
                 const int64_t a = threadIdx.x + (int64_t)AT * k;
                 unx[k] = a < A ? un[a] : 0.0f;
             }
+            spx = st_thr[c0 + j + 1];
         }
-        const float2 sp = st_thr[c0 + j];
         const float st = sp.x, thr = sp.y, m2st = -2.0f * st;
         int acc[APC] = {};
         if (st <= ATT_ST_FAST_MAX) {   // CTA-uniform
@@ -219,11 +225,12 @@ k_att_score4(const float* __restrict__ u, int64_t ldu, const int32_t* __restrict
         }
 #pragma unroll
         for (int p = 0; p < APC; ++p) {
-            const int t = warp_sum(acc[p]);
+            const int t = __reduce_add_sync(0xffffffffu, acc[p]);
             if (lane == 0) red[j][p][warp] = t;
         }
 #pragma unroll
         for (int k = 0; k < AKA; ++k) uvv[k] = unx[k];
+        sp = spx;
     }
     __syncthreads();
     for (int idx = threadIdx.x; idx < P * APC; idx += AT) {
