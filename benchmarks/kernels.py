@@ -110,6 +110,39 @@ def attention_case(S=256, beam=5, A=2048, H2=2048, seed=0):
             "GBps": nbytes / t / 1e9}
 
 
+def vocab_case(N=1280, V=50000, K=512, k=5, fused=True):
+    """Vocab projection + candidates of one cfg5 decode step: fused (vocab_topk.cu)
+    vs tcgen05 GEMM (bias) + single-pass candidate kernel."""
+    rng = np.random.default_rng(7)
+    W = torch.from_numpy(rng.integers(-127, 128, (V, K)).astype(np.int8)).cuda()
+    X = torch.from_numpy(rng.integers(-127, 128, (N, K)).astype(np.int8)).cuda()
+    ws = torch.full((1,), 3000.0, device="cuda")
+    xs = torch.full((N // 5,), 2000.0, device="cuda") + torch.rand(N // 5, device="cuda")
+    seg = torch.arange(N, device="cuda", dtype=torch.int32) // 5
+    bias = torch.randn(V, device="cuda") * 0.1
+    live = torch.randn(N, dtype=torch.float64, device="cuda")
+    cs = torch.empty((N, k), dtype=torch.float64, device="cuda")
+    ct = torch.empty((N, k), dtype=torch.int32, device="cuda")
+    f = _dev.flag()
+    st = lambda: torch.cuda.current_stream().cuda_stream
+    if fused:
+        scratch = torch.empty(int(_lib.load().qnmt_vocab_candidates_scratch(N, V)), dtype=torch.uint8,
+                              device="cuda")
+        fn = lambda: _lib.call("qnmt_vocab_candidates", X.data_ptr(), N, K, xs.data_ptr(), seg.data_ptr(),
+                               W.data_ptr(), V, K, K, ws.data_ptr(), V, bias.data_ptr(), live.data_ptr(), k,
+                               scratch.data_ptr(), cs.data_ptr(), ct.data_ptr(), f.data_ptr(), st())
+    else:
+        Y = torch.empty((N, V), dtype=torch.float32, device="cuda")
+
+        def fn():
+            pb.qmath.gemm_kmajor(W, ws, V, X, xs, col_seg=seg, bias=bias, Y=Y)
+            _lib.call("qnmt_topk_candidates", Y.data_ptr(), N, V, V, live.data_ptr(), k, cs.data_ptr(),
+                      ct.data_ptr(), f.data_ptr(), st())
+    t = graph_time(fn, reps=5)
+    return {"kernel": "vocab+candidates " + ("fused" if fused else "gemm+topk"), "N": N, "V": V, "K": K,
+            "us": t * 1e6, "logits_per_s": N * V / t, "TOPS": 2.0 * N * V * K / t / 1e12}
+
+
 def gemv_cold(bsz):
     w = torch.randint(-127, 128, (3072, 1024), dtype=torch.int8, device="cuda")
     copies = [w.clone() for _ in range(64)]
@@ -142,6 +175,8 @@ def main():
         out.append(gemm_case("enc Uzr", 2048, 1024, 256))
     if "topk" in which:
         out.append(topk_case())
+    if "vocab" in which:
+        out += [vocab_case(fused=True), vocab_case(fused=False)]
     if "att" in which:
         out.append(attention_case())
     if "gemv" in which:

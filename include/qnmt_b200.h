@@ -176,6 +176,26 @@ int qnmt_topk_candidates(const float* logits, int64_t N, int64_t V, int64_t ld,
  * one (A/B testing; results are identical by construction).  Returns old. */
 int qnmt_set_topk_exact(int exact);
 
+/* 1 (default) = the engine's decode loop runs the vocabulary projection fused
+ * with the log-softmax statistics and the candidate selection (the [N][V]
+ * logits never reach HBM); 0 = vocab GEMM + qnmt_topk_candidates (A/B
+ * testing; results are identical by construction).  Returns old. */
+int qnmt_set_vocab_fused(int enable);
+
+/* Fused vocabulary projection + log-softmax statistics + beam candidates
+ * (vocab_topk.cu): the same candidates as qnmt_gemm_i8 (bias) followed by
+ * qnmt_topk_candidates, without materialising the [N][V] logits.
+ *   X: [N][ldx] readout codes, x_scales[row_seg[n]]; W: [V][ldw] vocabulary
+ *   codes, w_scales[v / w_rows_per_scale]; bias: [V] or NULL; live: [N] or NULL.
+ *   K % 16 == 0, ldx/ldw % 16 == 0, 16-byte aligned X/W, 1 <= k <= min(16, V).
+ *   scratch: qnmt_vocab_candidates_scratch(N, V) bytes of device memory. */
+int qnmt_vocab_candidates(const int8_t* X, int64_t N, int64_t ldx, const float* x_scales,
+                          const int32_t* row_seg, const int8_t* W, int64_t V, int64_t K, int64_t ldw,
+                          const float* w_scales, int64_t w_rows_per_scale, const float* bias,
+                          const double* live_scores, int32_t k, void* scratch, double* cand_score,
+                          int32_t* cand_tok, int32_t* err_flag, void* stream);
+int64_t qnmt_vocab_candidates_scratch(int64_t N, int64_t V);
+
 /* Embedding gather (layers.py:324, :367): out[n] = table[ids[n]] ([rows][E]);
  * ids outside [0, rows) raise QNMT_FLAG_VOCAB and yield zeros. */
 int qnmt_embed_gather(const float* table, int64_t rows, int64_t E, const int32_t* ids,

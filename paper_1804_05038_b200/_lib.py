@@ -35,6 +35,8 @@ SIGNATURES = {
     "qnmt_attention_stats": (I32, [P, P, P, I32, I64, P, P]),
     "qnmt_log_softmax": (I32, [P, I64, I64, I64, P, I64, P, P]),
     "qnmt_topk_candidates": (I32, [P, I64, I64, I64, P, I32, P, P, P, P]),
+    "qnmt_vocab_candidates": (I32, [P, I64, I64, P, P, P, I64, I64, I64, P, I64, P, P, I32, P, P, P, P, P]),
+    "qnmt_vocab_candidates_scratch": (I64, [I64, I64]),
     "qnmt_embed_gather": (I32, [P, I64, I64, P, I64, P, I64, P, P]),
     "qnmt_model_create": (I32, [P, P, I32, P]),
     "qnmt_model_destroy": (I32, [P]),
@@ -50,6 +52,7 @@ SIGNATURES = {
     "qnmt_kernel_launches": (I64, []),
     "qnmt_set_gemm_impl": (I32, [I32]),
     "qnmt_set_topk_exact": (I32, [I32]),
+    "qnmt_set_vocab_fused": (I32, [I32]),
     "qnmt_engine_profile": (I32, [P, I32]),
     "qnmt_engine_set_graphs": (I32, [P, I32]),
     "qnmt_engine_stamps": (I32, [P, I32]),

@@ -136,6 +136,7 @@ struct qnmt_engine {
     int8_t* q_ro;
     float* sc_ro;
     float* logits;           // [N][V]
+    void* vocab_part;        // fused vocab projection partials (vocab_topk_part_bytes(N, V))
     void* att_scratch;
     float* att_mm;           // [S][2][A] per-sentence column max / min of att_proj
     uint32_t* qm[3];         // [QM_COUNT][S] fused quantization max-abs bits: ping-pong + external steps
@@ -378,6 +379,7 @@ struct StepIO {
     const float* att_minmax;       // [nseg][2][A] column extrema of att_proj (nullable)
     uint32_t* qm;                  // [QM_COUNT][S] this step's max-abs bits (zeroed but for QM_S/QM_SP)
     bool qm_ready;                 // QM_S / QM_SP already hold the maxima of s / sp (gather_rows)
+    bool fuse_vocab;               // skip the vocab GEMM: the caller runs cands_launch (vocab_topk.cu)
 };
 
 // ---------------------------------------------------------------------------
@@ -388,7 +390,7 @@ struct StepIO {
 // ---------------------------------------------------------------------------
 enum { ST_STEP0 = 0, ST_ATT0, ST_ATT1, ST_TOPK0, ST_TOPK1, ST_VOC0, ST_VOC1, ST_STEP1, ST_N, ST_SUML, ST_COLS };
 
-__global__ void k_stamp(long long* stamps, const int32_t* step_dev, int slot, const int32_t* n_dev,
+__global__ void k_stamp(long long* stamps, const int32_t* step_dev, int slot, int slot2, const int32_t* n_dev,
                         const int32_t* P, const int32_t* len, int n_sent) {
     const int t = *step_dev;
     long long* row = stamps + (int64_t)t * ST_COLS;
@@ -410,12 +412,13 @@ __global__ void k_stamp(long long* stamps, const int32_t* step_dev, int slot, co
         long long g;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
         row[slot] = g;
+        if (slot2 >= 0) row[slot2] = g;
     }
 }
 
-static int stamp(qnmt_engine* e, int slot, const StepIO& io, cudaStream_t st) {
+static int stamp(qnmt_engine* e, int slot, const StepIO& io, cudaStream_t st, int slot2 = -1) {
     if (!e->stamp_on || !tl_ndev || !e->stamps) return QNMT_OK;   // graph-captured steps only
-    k_stamp<<<1, 256, 0, st>>>(e->stamps, e->d_step, slot, tl_ndev, io.sent_ncols, io.sent_len, io.nseg);
+    k_stamp<<<1, 256, 0, st>>>(e->stamps, e->d_step, slot, slot2, tl_ndev, io.sent_ncols, io.sent_len, io.nseg);
     QNMT_CHECK_LAUNCH("k_stamp");
     return QNMT_OK;
 }
@@ -499,12 +502,40 @@ static int step_core(qnmt_engine* e, const StepIO& io, cudaStream_t st) {
     TRY(tanh_launch(e->ro, N, R, R, e->ro, R, e->err, st, qm(QM_RO), seg));
     prof_mark(e, PG_QUANT, st);
     TRY(quantize_encode_launch(e->ro, N, R, R, seg, e->q_ro, R, e->sc_ro, qm(QM_RO), 1, e->err, st));
+    if (io.fuse_vocab) return QNMT_OK;
     prof_mark(e, PG_GEMM_VOCAB, st, 2.0 * N * V * R, (double)V * R + (double)N * R + 4.0 * N * V);
     TRY(stamp(e, ST_VOC0, io, st));
     TRY(gemm(m->w_vocab, V, R, m->w_vocab_s, V, e->q_ro, N, R, e->sc_ro, seg, m->b_vocab, io.logits, V,
              0, st));
     TRY(stamp(e, ST_VOC1, io, st));
     return QNMT_OK;
+}
+
+static bool vocab_fusable(const qnmt_engine* e, int k) {
+    const qnmt_model* m = e->m;
+    return g_vocab_fused && g_gemm_impl != 1 && vocab_topk_eligible(m->R, m->R, m->R, e->q_ro, m->w_vocab, k);
+}
+
+// beam candidates of the step: fused vocab projection + statistics + merge, or
+// the plain vocab GEMM (inside step_core) followed by the candidate kernel
+static int cands_launch(qnmt_engine* e, const StepIO& io, const double* live, int k, cudaStream_t st) {
+    const qnmt_model* m = e->m;
+    const int64_t N = io.N, V = m->Vt, R = m->R;
+    if (io.fuse_vocab) {
+        VocabTopk p{e->q_ro, N, R, e->sc_ro, io.col_sent, m->w_vocab, V, R, R, m->w_vocab_s, V, m->b_vocab,
+                    live, k, e->vocab_part, e->cand_score, e->cand_tok, e->err};
+        prof_mark(e, PG_GEMM_VOCAB, st, 2.0 * N * V * R, (double)V * R + (double)N * R);
+        TRY(stamp(e, ST_VOC0, io, st));
+        TRY(vocab_stats_launch(p, st));
+        TRY(stamp(e, ST_VOC1, io, st, ST_TOPK0));
+        prof_mark(e, PG_TOPK, st);
+        TRY(vocab_merge_launch(p, st));
+        return stamp(e, ST_TOPK1, io, st);
+    }
+    TRY(stamp(e, ST_TOPK0, io, st));
+    prof_mark(e, PG_TOPK, st, 0, 4.0 * N * V);
+    TRY(topk_launch(io.logits, N, V, V, live, k, e->cand_score, e->cand_tok, e->err, st));
+    return stamp(e, ST_TOPK1, io, st);
 }
 
 static int grow_history(qnmt_engine* e, int steps) {
@@ -655,6 +686,7 @@ int qnmt_engine_create(const qnmt_model* m, int32_t max_sentences, int32_t max_s
         e->q_ro = a.take<int8_t>(N * R);
         e->sc_ro = a.take<float>(S);
         e->logits = a.take<float>(N * V);
+        e->vocab_part = a.take<char>(vocab_topk_part_bytes((int64_t)N, (int64_t)V));
         e->att_scratch = a.take<char>(N * (L + 2) * 4 + 2 * S * A * 4 + 1024);
         e->att_mm = a.take<float>(2 * S * A);
         for (int i = 0; i < 3; ++i) e->qm[i] = a.take<uint32_t>(qnmt::QM_COUNT * S);
@@ -786,7 +818,7 @@ int qnmt_decoder_step(qnmt_engine* e, int64_t N, const int32_t* col_sent, int32_
     QNMT_CUDA(cudaMemsetAsync(e->err, 0, 4, st));
     TRY(col_ranges_launch(col_sent, N, n_sent, e->rng_off, e->rng_cnt, st));
     StepIO io{N, n_sent, col_sent, y, s, sp, states, att_proj, sent_row, sent_len, max_len,
-              s_int, s_new, logits, alpha, lda, e->rng_off, e->rng_cnt, nullptr, e->qm[2], false};
+              s_int, s_new, logits, alpha, lda, e->rng_off, e->rng_cnt, nullptr, e->qm[2], false, false};
     TRY(step_core(e, io, st));
     return check_flag(e, st);
 }
@@ -814,13 +846,10 @@ static int capture_step(qnmt_engine* e, int cur, int n, int beam, int k_list, cu
         NdevScope nd(e->d_N + cur);
         StepIO io{NM, n, e->col_sent[cur], e->y[cur], e->st_s[cur], e->st_sp[cur], e->enc_states, e->enc_att,
                   e->sent_row, e->sent_len, e->L, e->s_int, e->s_new, e->logits, nullptr, 0,
-                  e->col_off, e->P, e->att_mm, e->qm[cur], true};
+                  e->col_off, e->P, e->att_mm, e->qm[cur], true, vocab_fusable(e, k_list)};
         rc = stamp(e, ST_STEP0, io, cs);
         if (rc == QNMT_OK) rc = step_core(e, io, cs);
-        if (rc == QNMT_OK) rc = stamp(e, ST_TOPK0, io, cs);
-        if (rc == QNMT_OK)
-            rc = topk_launch(e->logits, NM, V, V, e->live[cur], k_list, e->cand_score, e->cand_tok, e->err, cs);
-        if (rc == QNMT_OK) rc = stamp(e, ST_TOPK1, io, cs);
+        if (rc == QNMT_OK) rc = cands_launch(e, io, e->live[cur], k_list, cs);
         if (rc == QNMT_OK) {
             SearchState ss{e->P, e->col_off, e->done, e->max_steps, e->steps_run, e->fin_cnt, e->fin_best,
                            e->fin_score, e->fin_step, e->fin_slot, e->fin_eos, e->hist_tok, e->hist_par,
@@ -865,7 +894,7 @@ static int capture_step(qnmt_engine* e, int cur, int n, int beam, int k_list, cu
 
 static int get_step_graphs(qnmt_engine* e, int n, int beam, int k_list, cudaGraphExec_t* g) {
     // history buffers may have been re-allocated: graphs are keyed on the history capacity too
-    const int key2 = (beam * 100000 + e->hist_steps) * 2 + (e->stamp_on ? 1 : 0);
+    const int key2 = ((beam * 100000 + e->hist_steps) * 2 + (e->stamp_on ? 1 : 0)) * 2 + (vocab_fusable(e, k_list) ? 1 : 0);
     for (auto& kv : e->graphs)
         if (kv.first.first == n && kv.first.second == key2) {
             g[0] = kv.second.first;
@@ -965,10 +994,9 @@ static int decode_core(qnmt_engine* e, const int32_t* src_ids, bool ids_on_devic
     for (int t = 0; t < Tmax && N > 0; ++t) {
         StepIO io{N, n, e->col_sent[cur], e->y[cur], e->st_s[cur], e->st_sp[cur], e->enc_states,
                   e->enc_att, e->sent_row, e->sent_len, Lmax, e->s_int, e->s_new, e->logits, nullptr, 0,
-                  e->col_off, e->P, e->att_mm, e->qm[cur], true};
+                  e->col_off, e->P, e->att_mm, e->qm[cur], true, vocab_fusable(e, k_list)};
         TRY(step_core(e, io, st));
-        prof_mark(e, PG_TOPK, st, 0, 4.0 * N * V);
-        TRY(topk_launch(e->logits, N, V, V, e->live[cur], k_list, e->cand_score, e->cand_tok, e->err, st));
+        TRY(cands_launch(e, io, e->live[cur], k_list, st));
         prof_mark(e, PG_SEARCH, st);
         SearchState ss{e->P, e->col_off, e->done, e->max_steps, e->steps_run, e->fin_cnt, e->fin_best,
                        e->fin_score, e->fin_step, e->fin_slot, e->fin_eos, e->hist_tok, e->hist_par,

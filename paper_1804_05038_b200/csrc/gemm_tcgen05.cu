@@ -22,24 +22,15 @@
 #include <unordered_map>
 
 #include "gemm.cuh"
-#include "tc_common.cuh"
+#include "tc_mainloop.cuh"
 
 namespace qnmt {
 
-constexpr int TC_BM = 128;
-constexpr int TC_BK = 128;   // bytes of K per stage (= int8 elements)
 constexpr int TC_EPI_WARPS = 8;
 constexpr int TC_THREADS = 64 + 32 * TC_EPI_WARPS;
 
 template <int BN>
-struct TcCfg {
-    static constexpr int A_BYTES = TC_BM * TC_BK;
-    static constexpr int B_BYTES = BN * TC_BK;
-    static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-    static constexpr int STAGES = (BN == 256) ? 4 : (BN == 128 ? 6 : 8);
-    static constexpr int TMEM_COLS = 2 * BN;   // 128 / 256 / 512 (power of two)
-    static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
-};
+using TcCfg = TcRing<BN, (BN == 256) ? 4 : (BN == 128 ? 6 : 8)>;
 
 struct TcEpi {
     const float* w_scales;
@@ -63,11 +54,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
     if (n_dev) N = min(N, *n_dev);   // graph mode: live columns from the device
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* smem = (unsigned char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
-    uint64_t* empty = full + C::STAGES;
-    uint64_t* tfull = empty + C::STAGES;    // [2]
-    uint64_t* tempty = tfull + 2;           // [2]
-    uint32_t* tmem_base_smem = reinterpret_cast<uint32_t*>(tempty + 2);
+    const TcBars<C> bars(smem);
     __shared__ float col_sx[2][256];      // per-column activation scale (double-buffered by tile)
     __shared__ double col_isx[2][256];    // and its f64 reciprocal
 
@@ -77,74 +64,12 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
     const int n_blocks = (N + BN - 1) / BN;
     const int tiles = m_blocks * n_blocks;
     const int k_blocks = (K + TC_BK - 1) / TC_BK;
-
-    if (warp == 0 && lane == 0) {
-        tc::prefetch_tmap(&tmA);
-        tc::prefetch_tmap(&tmB);
-        for (int s = 0; s < C::STAGES; ++s) {
-            tc::mbar_init(&full[s], 1);
-            tc::mbar_init(&empty[s], 1);
-        }
-        for (int b = 0; b < 2; ++b) {
-            tc::mbar_init(&tfull[b], 1);
-            tc::mbar_init(&tempty[b], TC_EPI_WARPS);
-        }
-        tc::fence_mbar_init();
-    }
-    if (warp == 1) tc::tmem_alloc<C::TMEM_COLS>(tmem_base_smem);
-    tc::tc_fence_before();
-    __syncthreads();
-    tc::tc_fence_after();
-    const uint32_t tmem_base = *tmem_base_smem;
+    const uint32_t tmem_base = tc_setup<C>(&tmA, &tmB, bars, TC_EPI_WARPS);
 
     if (warp == 0) {
-        // ---------------- TMA producer ----------------
-        if (lane == 0) {
-            int stage = 0;
-            uint32_t phase = 0;
-            for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
-                const int mb = tile / n_blocks, nb = tile % n_blocks;
-                for (int kb = 0; kb < k_blocks; ++kb) {
-                    tc::mbar_wait(&empty[stage], phase ^ 1);
-                    unsigned char* sa = smem + stage * C::STAGE_BYTES;
-                    unsigned char* sb = sa + C::A_BYTES;
-                    tc::mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
-                    tc::tma_load_2d(sa, &tmA, &full[stage], kb * TC_BK, mb * TC_BM);
-                    tc::tma_load_2d(sb, &tmB, &full[stage], kb * TC_BK, nb * BN);
-                    if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
-                }
-            }
-        }
+        tc_produce<C, BN>(&tmA, &tmB, smem, bars, tiles, n_blocks, k_blocks);
     } else if (warp == 1) {
-        // ---------------- MMA issuer ----------------
-        constexpr uint32_t IDESC = tc::idesc_i8(TC_BM, BN);
-        int stage = 0;
-        uint32_t phase = 0;
-        int it = 0;
-        for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++it) {
-            const int buf = it & 1;
-            const uint32_t use = (uint32_t)(it >> 1) & 1u;
-            tc::mbar_wait(&tempty[buf], use ^ 1);
-            tc::tc_fence_after();
-            const uint32_t d = tmem_base + (uint32_t)(buf * BN);
-            for (int kb = 0; kb < k_blocks; ++kb) {
-                tc::mbar_wait(&full[stage], phase);
-                tc::tc_fence_after();
-                if (lane == 0) {
-                    const uint32_t a0 = tc::smem_u32(smem + stage * C::STAGE_BYTES);
-                    const uint32_t b0 = a0 + C::A_BYTES;
-#pragma unroll
-                    for (int k = 0; k < TC_BK / 32; ++k) {
-                        tc::mma_i8(d, tc::sw128_kmajor_desc(a0 + 32 * k), tc::sw128_kmajor_desc(b0 + 32 * k), IDESC,
-                                   (kb | k) != 0);
-                    }
-                    tc::mma_commit(&empty[stage]);
-                    if (kb == k_blocks - 1) tc::mma_commit(&tfull[buf]);
-                }
-                __syncwarp();
-                if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
-            }
-        }
+        tc_issue<C, BN>(smem, bars, tmem_base, tiles, k_blocks);
     } else {
         // ---------------- epilogue ----------------
         const int ew = warp - 2;                 // 0..7
@@ -177,7 +102,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
             }
             const double isw = 1.0 / (double)sw;
             asm volatile("bar.sync 1, %0;" ::"n"(32 * TC_EPI_WARPS));   // epilogue warps only
-            tc::mbar_wait(&tfull[buf], use);
+            tc::mbar_wait(&bars.tfull[buf], use);
             tc::tc_fence_after();
 #pragma unroll 1
             for (int c0 = half * COLS; c0 < (half + 1) * COLS; c0 += 16) {
@@ -235,7 +160,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
             }
             tc::tc_fence_before();
             __syncwarp();
-            if (lane == 0) tc::mbar_arrive(&tempty[buf]);
+            if (lane == 0) tc::mbar_arrive(&bars.tempty[buf]);
         }
     }
     __syncthreads();
@@ -280,7 +205,7 @@ struct MapKeyHash {
     }
 };
 
-static int get_map(const int8_t* p, int64_t rows, int64_t cols, int64_t ld, int box_rows, CUtensorMap* out) {
+int tc_get_map(const int8_t* p, int64_t rows, int64_t cols, int64_t ld, int box_rows, CUtensorMap* out) {
     static std::mutex mu;
     static std::unordered_map<MapKey, CUtensorMap, MapKeyHash> cache;
     MapKey key{p, rows, cols, ld, box_rows};
@@ -307,7 +232,7 @@ static int get_map(const int8_t* p, int64_t rows, int64_t cols, int64_t ld, int 
     return QNMT_OK;
 }
 
-static int sm_count() {
+int tc_sm_count() {
     static int n = 0;
     if (!n) {
         int dev = 0;
@@ -327,13 +252,13 @@ static int launch_tc(const GemmArgs& g, cudaStream_t st) {
         attr_set = true;
     }
     CUtensorMap ta, tb;
-    int rc = get_map(g.W, g.M, g.K, g.ldw, TC_BM, &ta);
+    int rc = tc_get_map(g.W, g.M, g.K, g.ldw, TC_BM, &ta);
     if (rc) return rc;
-    rc = get_map(g.X, g.N, g.K, g.ldx, BN, &tb);
+    rc = tc_get_map(g.X, g.N, g.K, g.ldx, BN, &tb);
     if (rc) return rc;
     TcEpi e{g.w_scales, g.w_rows_per_scale, g.x_scales, g.col_seg, g.bias, g.Y, g.ldy, g.acc_out, g.flags};
     int tiles = (int)(cdiv(g.M, TC_BM) * cdiv(g.N, BN));
-    int grid = tiles < sm_count() ? tiles : sm_count();
+    int grid = tiles < tc_sm_count() ? tiles : tc_sm_count();
     k_gemm_tc<BN, EPI><<<grid, TC_THREADS, C::SMEM, st>>>(ta, tb, (int)g.M, (int)g.N, (int)g.K, e, tl_ndev);
     QNMT_CHECK_LAUNCH("k_gemm_tc");
     return QNMT_OK;
@@ -347,7 +272,7 @@ bool tc_eligible(const GemmArgs& g) {
 
 int gemm_tc_launch(const GemmArgs& g, cudaStream_t st) {
     const int64_t mb = cdiv(g.M, TC_BM);
-    const int sms = sm_count();
+    const int sms = tc_sm_count();
     const int epi = (g.bias ? EPI_BIAS : 0) | ((g.flags & QNMT_GEMM_ACCUMULATE) ? EPI_ACCUMULATE : 0) |
                     (g.acc_out ? EPI_RAW : 0);
     const int bn = (g.N > 128 && mb * cdiv(g.N, 256) >= sms) ? 256 : (g.N > 64 && mb * cdiv(g.N, 128) >= sms / 2) ? 128 : 64;

@@ -41,4 +41,28 @@ int quantize_encode_launch(const float* x, int64_t ncols, int64_t K, int64_t ldx
 int quantize_max_launch(const float* x, int64_t ncols, int64_t K, int64_t ldx, const int32_t* col_seg,
                         uint32_t* seg_maxbits, cudaStream_t st);
 
+// fused vocab projection + log-softmax statistics + beam candidates (vocab_topk.cu)
+struct VocabTopk {
+    const int8_t* X;          // [N][ldx] readout codes (K-major)
+    int64_t N, ldx;
+    const float* x_scales;
+    const int32_t* row_seg;
+    const int8_t* W;          // [V][ldw] vocabulary codes
+    int64_t V, K, ldw;
+    const float* w_scales;
+    int64_t w_rows_per_scale;
+    const float* bias;
+    const double* live;       // [N] running hypothesis scores
+    int32_t k;
+    void* part;               // vocab_topk_part_bytes(N, V)
+    double* cand_score;       // [N][k]
+    int32_t* cand_tok;
+    int32_t* err_flag;
+};
+extern int g_vocab_fused;
+bool vocab_topk_eligible(int64_t K, int64_t ldx, int64_t ldw, const void* X, const void* W, int k);
+size_t vocab_topk_part_bytes(int64_t rows, int64_t V);
+int vocab_stats_launch(const VocabTopk& p, cudaStream_t st);
+int vocab_merge_launch(const VocabTopk& p, cudaStream_t st);
+
 }  // namespace qnmt

@@ -10,52 +10,11 @@
 //   top-`beam` list (selection is finished by search.cu).
 #include <float.h>
 
-#include "common.cuh"
+#include "cand.cuh"
 
 namespace qnmt {
 
-constexpr int LS_T = 512;
 int g_topk_exact = 0;   // 1: use the three-pass reference kernel (testing)
-
-struct Cand {
-    double s;
-    int t;
-};
-
-__device__ __forceinline__ bool better(const Cand& a, const Cand& b) {
-    return a.s > b.s || (a.s == b.s && a.t < b.t);
-}
-
-// block-wide reductions (LS_T threads)
-__device__ float block_max_f(float v, float* red) {
-    v = warp_max(v);
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
-    __syncthreads();
-    if (threadIdx.x < 32) {
-        float t = threadIdx.x < LS_T / 32 ? red[threadIdx.x] : -FLT_MAX;
-        t = warp_max(t);
-        if (threadIdx.x == 0) red[0] = t;
-    }
-    __syncthreads();
-    float r = red[0];
-    __syncthreads();
-    return r;
-}
-
-__device__ double block_sum_d(double v, double* red) {
-    v = warp_sum(v);
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
-    __syncthreads();
-    if (threadIdx.x < 32) {
-        double t = threadIdx.x < LS_T / 32 ? red[threadIdx.x] : 0.0;
-        t = warp_sum(t);
-        if (threadIdx.x == 0) red[0] = t;
-    }
-    __syncthreads();
-    double r = red[0];
-    __syncthreads();
-    return r;
-}
 
 // max and lse of one column; non-finite logits poison both (flag raised).
 __device__ void column_stats(const float* __restrict__ row, int64_t V, float* redf, double* redd,
@@ -92,47 +51,6 @@ k_log_softmax(const float* __restrict__ logits, int64_t V, int64_t ld, float* __
     double dm = (double)mx;
     for (int64_t v = threadIdx.x; v < V; v += LS_T)
         lp[n * ldlp + v] = __double2float_rn(((double)row[v] - dm) - lse);
-}
-
-template <int KM>
-__device__ __forceinline__ void insert(Cand (&L)[KM], Cand c) {
-    if (!better(c, L[KM - 1])) return;
-    L[KM - 1] = c;
-#pragma unroll
-    for (int i = KM - 1; i > 0; --i) {
-        if (better(L[i], L[i - 1])) {
-            Cand t = L[i];
-            L[i] = L[i - 1];
-            L[i - 1] = t;
-        }
-    }
-}
-
-// warp-cooperative k-way merge of 32 sorted per-lane lists; result in lane 0..k-1 order
-template <int KM>
-__device__ void warp_merge(Cand (&L)[KM], Cand* out, int k) {
-    const int lane = threadIdx.x & 31;
-    for (int r = 0; r < k; ++r) {
-        Cand b = L[0];
-        int bl = lane;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            double os = __shfl_xor_sync(0xffffffffu, b.s, o);
-            int ot = __shfl_xor_sync(0xffffffffu, b.t, o);
-            int ol = __shfl_xor_sync(0xffffffffu, bl, o);
-            Cand oc{os, ot};
-            if (better(oc, b) || (!better(b, oc) && ol < bl)) {
-                b = oc;
-                bl = ol;
-            }
-        }
-        if (lane == 0) out[r] = b;
-        if (lane == bl) {
-#pragma unroll
-            for (int i = 0; i < KM - 1; ++i) L[i] = L[i + 1];
-            L[KM - 1] = Cand{-DBL_MAX, 0x7fffffff};
-        }
-    }
 }
 
 template <int KM>
@@ -176,31 +94,6 @@ k_topk(const float* __restrict__ logits, int64_t V, int64_t ld, const double* __
     }
 }
 
-// exp(t) for t <= 0 in fp64 (~2 ulp): t = k*ln2/16 + r, |r| <= ln2/32,
-// e^r by a degree-7 polynomial (truncation < 1.3e-18), 2^(k/16) = 2^(k>>4) * tab[k&15].
-// The 16-entry f64 table is 128 B = all 32 smem banks, so lookups never
-// conflict.  ~13 f64 ops instead of the general-purpose exp() (~27 DFMA slots).
-__device__ __forceinline__ double exp_neg(double t, const double* __restrict__ tab) {
-    t = fmax(t, -700.0);   // below: contributes < 1e-304 (branch-free range guard)
-    // round(t * 16/ln2) without FRND/F2I: add 1.5*2^52 so the integer lands in the low word
-    const double kd_m = fma(t, 23.083120654223414, 6755399441055744.0);
-    const int k = __double2loint(kd_m);
-    const double kd = kd_m - 6755399441055744.0;
-    double r = fma(kd, -0.04332169878499658, t);             // ln2/16, rounded to f64
-    r = fma(kd, -1.4494042586539372e-18, r);                 // ln2/16 - the above
-    double p = fma(r, 1.0 / 5040.0, 1.0 / 720.0);
-    p = fma(p, r, 1.0 / 120.0);
-    p = fma(p, r, 1.0 / 24.0);
-    p = fma(p, r, 1.0 / 6.0);
-    p = fma(p, r, 0.5);
-    p = fma(p, r, 1.0);
-    p = fma(p, r, 1.0);
-    double v = p * tab[k & 15];
-    // multiply by 2^(k >> 4) through the exponent field (result stays normal for t >= -700)
-    long long bits = __double_as_longlong(v) + ((long long)(k >> 4) << 52);
-    return __longlong_as_double(bits);
-}
-
 struct LCand {
     float x;
     int t;
@@ -235,23 +128,6 @@ __device__ __forceinline__ void linsert(LCand (&L)[KM], LCand c) {
 // tie across the boundary -- practically never) the CTA rescans the column
 // exactly with the three-pass method of k_topk.
 // ---------------------------------------------------------------------------
-template <int KM>
-__device__ void block_merge_cands(Cand (&L)[KM], Cand (*wl)[KM], Cand* out, int kk) {
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    warp_merge<KM>(L, wl[warp], kk);
-    __syncthreads();
-    if (warp == 0) {
-#pragma unroll
-        for (int i = 0; i < KM; ++i) L[i] = (lane < LS_T / 32 && i < kk) ? wl[lane][i] : Cand{-DBL_MAX, 0x7fffffff};
-        __syncwarp();
-        Cand tmp[KM];
-        warp_merge<KM>(L, tmp, kk);
-        if (lane == 0)
-            for (int i = 0; i < kk; ++i) out[i] = tmp[i];
-    }
-    __syncthreads();
-}
-
 template <int KM>
 __global__ void __launch_bounds__(LS_T, 2)
 k_topk1(const float* __restrict__ logits, int64_t V, int64_t ld, const double* __restrict__ live, int k,

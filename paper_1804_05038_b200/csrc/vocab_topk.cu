@@ -1,0 +1,478 @@
+// vocab_topk.cu -- vocabulary projection fused with the log-softmax statistics
+// and the beam candidates: the [N][V] logits never touch HBM.
+//
+// Same numbers as gemm (layers.py:266, W_vocab . q(readout) + b) followed by
+// topk_launch (output.cu: layers.py:60-67 + decoder.py:125/:74-85):
+//   x[n][v]  = fl32(fl32(acc / (s_w * s_x)) + b[v])             exact dequant
+//   lp[n][v] = fl32((f64 x - f64 max_n) - log(sum_v exp(f64 x - f64 max_n)))
+//   cand     = top-k of (live[n] + f64 lp, token asc)
+//
+// K5a k_vocab_stats: the tcgen05 main loop (tc_mainloop.cuh) with the roles
+//   swapped -- A = activations (TMEM lane = hypothesis row), B = W_vocab (TMEM
+//   column = token) -- so every epilogue thread owns one hypothesis row and a
+//   128-token half-tile.  Per (row, tile, half) it keeps an online (max, sum
+//   exp) in fp64, the token of the max (smallest on ties) and the runner-up
+//   value, and writes one 24-byte partial.  Traffic: 24 B per 128 logits
+//   instead of 512 B written + 512 B re-read.
+// K5b k_vocab_merge: one warp per row combines the partials into (max, lse) and
+//   the top-KM of the half-tile maxima.  That is the exact top-KM unless some
+//   half-tile's runner-up reaches the KM-th value (~C(KM,2)/#half-tiles of the
+//   rows); those half-tiles are recomputed exactly (dp4a over K) and merged in
+//   full.  Exact scores, ordering and the f32 tie check then follow k_topk1
+//   (output.cu); a tie across the KM boundary recomputes the whole row (never
+//   seen outside constructed tie tests).
+#include "cand.cuh"
+#include "kernels.cuh"
+#include "tc_mainloop.cuh"
+
+namespace qnmt {
+
+constexpr int VT_BN = 256;
+constexpr int VT_EPI_WARPS = 8;
+constexpr int VT_THREADS = 64 + 32 * VT_EPI_WARPS;
+using VtRing = TcRing<VT_BN, 4>;
+constexpr int VT_HALF = VT_BN / 2;   // tokens per partial
+constexpr int VT_RESCAN_MAX = 64;    // flagged half-tiles handled per row before a full row rescan
+
+struct VtPart {
+    double s;       // sum exp(x - m) over the half-tile
+    float m;        // max logit (-FLT_MAX: empty)
+    float a2;       // second-largest logit (may equal m; -FLT_MAX: fewer than 2 tokens)
+    int32_t i1;     // smallest token with logit m (INT_MAX: empty)
+    int32_t pad;
+};
+
+struct VtArgs {
+    const float* x_scales;    // activation scale per segment
+    const int32_t* row_seg;   // segment of each hypothesis row
+    const float* w_scales;    // weight scale per w_rows_per_scale vocabulary rows
+    int64_t w_rows_per_scale;
+    const float* bias;        // [V]
+    VtPart* part;             // [rows][2 * n_blocks]
+    int32_t* err_flag;
+};
+
+__global__ void __launch_bounds__(VT_THREADS, 1)
+k_vocab_stats(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW, int M, int V,
+              int K, VtArgs e, const int32_t* n_dev) {
+    using C = VtRing;
+    if (n_dev) M = min(M, *n_dev);
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char* smem = (unsigned char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    const TcBars<C> bars(smem);
+    __shared__ double col_isw[2][VT_BN];   // 1 / s_w per token (double-buffered by tile)
+    __shared__ float col_sw[2][VT_BN];
+    __shared__ float col_b[2][VT_BN];
+    __shared__ double tab[16];
+    __shared__ double tab64[64];
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const int m_blocks = (M + TC_BM - 1) / TC_BM;
+    const int n_blocks = (V + VT_BN - 1) / VT_BN;
+    const int tiles = m_blocks * n_blocks;
+    const int k_blocks = (K + TC_BK - 1) / TC_BK;
+    if (threadIdx.x < 16) tab[threadIdx.x] = exp2((double)threadIdx.x / 16.0);
+    if (threadIdx.x < 64) tab64[threadIdx.x] = exp2((double)threadIdx.x / 64.0);
+    const uint32_t tmem_base = tc_setup<C>(&tmX, &tmW, bars, VT_EPI_WARPS);   // includes __syncthreads
+
+    if (warp == 0) {
+        tc_produce<C, VT_BN>(&tmX, &tmW, smem, bars, tiles, n_blocks, k_blocks);
+    } else if (warp == 1) {
+        tc_issue<C, VT_BN>(smem, bars, tmem_base, tiles, k_blocks);
+    } else {
+        const int ew = warp - 2;
+        const int lg = warp & 3;     // TMEM lane group
+        const int half = ew >> 2;    // token half of the tile
+        const int np = 2 * n_blocks;
+        const bool one_scale = e.w_rows_per_scale >= V;   // kernel-uniform
+        const double isw0 = 1.0 / (double)e.w_scales[0];
+        bool bad = false;
+        int it = 0;
+        for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++it) {
+            const int mb = tile / n_blocks, nb = tile % n_blocks;
+            const int buf = it & 1;
+            const uint32_t use = (uint32_t)(it >> 1) & 1u;
+            {   // per-token weight scale and bias of this tile -> smem
+                const int c = ew * 32 + lane;
+                const int v = nb * VT_BN + c;
+                float sw = 1.0f, b = 0.0f;
+                if (v < V) {
+                    sw = e.w_scales[v / e.w_rows_per_scale];
+                    b = e.bias ? e.bias[v] : 0.0f;
+                }
+                col_sw[buf][c] = sw;
+                col_isw[buf][c] = 1.0 / (double)sw;
+                col_b[buf][c] = b;
+                bad |= !is_finite_f(b);
+            }
+            const int row = mb * TC_BM + lg * 32 + lane;
+            const bool rok = row < M;
+            const float sx = rok ? e.x_scales[e.row_seg ? e.row_seg[row] : 0] : 1.0f;
+            const double isx = 1.0 / (double)sx;
+            const double rs0 = isx * isw0;   // acc -> logit multiplier when W has one scale
+            asm volatile("bar.sync 1, %0;" ::"n"(32 * VT_EPI_WARPS));
+            tc::mbar_wait(&bars.tfull[buf], use);
+            tc::tc_fence_after();
+            // fast-path preconditions, per thread and tile: one weight scale, and every
+            // nonzero |q| = |acc| * rs in [2^-124, 2^127) (f32 normal range for |acc| < 2^31)
+            const bool fast_row = one_scale && rs0 >= 0x1p-124 && rs0 * 2147483648.0 < 0x1p127;
+            // top-1 (value, smallest token) and runner-up value, as 4 interleaved chains
+            // (token j of a chunk goes to chain j & 3) to keep the dependency chains short
+            float cm4[4] = {-FLT_MAX, -FLT_MAX, -FLT_MAX, -FLT_MAX}, ca4[4] = {-FLT_MAX, -FLT_MAX, -FLT_MAX, -FLT_MAX};
+            int ci4[4] = {0x7fffffff, 0x7fffffff, 0x7fffffff, 0x7fffffff};
+            float m = -FLT_MAX;   // running max of the half-tile (the exp reference)
+            double s = 0.0;
+#pragma unroll 1
+            for (int c0 = half * VT_HALF; c0 < (half + 1) * VT_HALF; c0 += 16) {
+                uint32_t r[16];
+                tc::tmem_ld16(tmem_base + ((uint32_t)(lg * 32) << 16) + (uint32_t)(buf * VT_BN + c0), r);
+                const int vbase = nb * VT_BN + c0;
+                const int ncols = min(16, V - vbase);   // warp-uniform
+                tc::tmem_ld_wait();
+                if (ncols <= 0) continue;
+                float x[16];
+                if (__all_sync(0xffffffffu, fast_row) && ncols == 16) {
+                    // exact dequant fl32(acc * rs): safe unless q's bits below f32 precision lie
+                    // within 64 f64-ulps of the rounding midpoint (0x10000000)
+                    uint32_t dmin = 0xffffffffu;
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) {
+                        const double q = (double)(int)r[j] * rs0;
+                        x[j] = __double2float_rn(q);
+                        const int d = (int)((uint32_t)__double2loint(q) & 0x1fffffffu) - 0x10000000;
+                        dmin = min(dmin, (uint32_t)abs(d));
+                    }
+                    if (__any_sync(0xffffffffu, dmin <= 64u)) {   // rare: exact division where needed
+#pragma unroll
+                        for (int j = 0; j < 16; ++j) {
+                            const double q = (double)(int)r[j] * rs0;
+                            const int d = (int)((uint32_t)__double2loint(q) & 0x1fffffffu) - 0x10000000;
+                            if (abs(d) <= 64) x[j] = dequant((int)r[j], col_sw[buf][c0 + j], sx);
+                        }
+                    }
+                    const float4* b4 = reinterpret_cast<const float4*>(&col_b[buf][c0]);
+#pragma unroll
+                    for (int q4 = 0; q4 < 4; ++q4) {
+                        const float4 bb = b4[q4];
+                        x[4 * q4 + 0] = __fadd_rn(x[4 * q4 + 0], bb.x);
+                        x[4 * q4 + 1] = __fadd_rn(x[4 * q4 + 1], bb.y);
+                        x[4 * q4 + 2] = __fadd_rn(x[4 * q4 + 2], bb.z);
+                        x[4 * q4 + 3] = __fadd_rn(x[4 * q4 + 3], bb.w);
+                    }
+                } else {   // vocabulary tail, per-row weight scales or extreme scales
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) {
+                        if (j < ncols) {
+                            const double q = (double)(int)r[j] * (isx * col_isw[buf][c0 + j]);
+                            x[j] = dequant_rcp_safe(q) ? __double2float_rn(q)
+                                                       : dequant((int)r[j], col_sw[buf][c0 + j], sx);
+                            x[j] = __fadd_rn(x[j], col_b[buf][c0 + j]);
+                        } else {
+                            x[j] = -FLT_MAX;   // excluded below (exp skipped, never above a real logit)
+                        }
+                    }
+                }
+                float cm, cn;
+                {   // chunk max / min as shallow trees (invalid tail tokens are -FLT_MAX: skipped for min)
+                    float t[8], u[8];
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) {
+                        t[j] = fmaxf(x[2 * j], x[2 * j + 1]);
+                        u[j] = fminf(2 * j < ncols ? x[2 * j] : FLT_MAX, 2 * j + 1 < ncols ? x[2 * j + 1] : FLT_MAX);
+                    }
+                    cm = fmaxf(fmaxf(fmaxf(t[0], t[1]), fmaxf(t[2], t[3])), fmaxf(fmaxf(t[4], t[5]), fmaxf(t[6], t[7])));
+                    cn = fminf(fminf(fminf(u[0], u[1]), fminf(u[2], u[3])), fminf(fminf(u[4], u[5]), fminf(u[6], u[7])));
+                }
+                bad |= !(is_finite_f(cm) && is_finite_f(cn));   // +-inf (NaN only from non-finite bias)
+                if (cm > m) {   // rescale the running sum (first chunk, then rare)
+                    s = (m == -FLT_MAX) ? 0.0 : s * exp_neg((double)m - (double)cm, tab);
+                    m = cm;
+                }
+                const double dm = (double)m;
+                double e4[4] = {0.0, 0.0, 0.0, 0.0};
+                if (ncols == 16 && !__any_sync(0xffffffffu, (double)cn - dm < -700.0)) {
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) e4[j & 3] += exp_neg64((double)x[j] - dm, tab64);
+                } else {   // vocabulary tail or a logit range beyond 700 (range-guarded exp)
+#pragma unroll
+                    for (int j = 0; j < 16; ++j)
+                        if (j < ncols) e4[j & 3] += exp_neg((double)x[j] - dm, tab);
+                }
+                s += (e4[0] + e4[1]) + (e4[2] + e4[3]);
+#pragma unroll
+                for (int j = 0; j < 16; ++j) {   // strict '>': the first (smallest) token wins ties
+                    const int k = j & 3;
+                    const bool g = x[j] > cm4[k];
+                    ca4[k] = fmaxf(ca4[k], fminf(cm4[k], x[j]));
+                    cm4[k] = fmaxf(cm4[k], x[j]);
+                    ci4[k] = g ? vbase + j : ci4[k];
+                }
+            }
+            // merge the 4 chains: larger value, then smaller token; runner-up = max(min of maxima, runner-ups)
+            float a2 = -FLT_MAX;
+            int i1 = ci4[0];
+            float mm = cm4[0];
+            a2 = ca4[0];
+#pragma unroll
+            for (int k = 1; k < 4; ++k) {
+                a2 = fmaxf(fmaxf(a2, ca4[k]), fminf(mm, cm4[k]));
+                const bool g = cm4[k] > mm || (cm4[k] == mm && ci4[k] < i1);
+                i1 = g ? ci4[k] : i1;
+                mm = fmaxf(mm, cm4[k]);
+            }
+            tc::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(&bars.tempty[buf]);
+            if (rok) {
+                VtPart p;
+                p.s = s;
+                p.m = m;
+                p.a2 = a2;
+                p.i1 = i1;
+                p.pad = 0;
+                e.part[(int64_t)row * np + nb * 2 + half] = p;
+            }
+        }
+        if (bad) set_flag(e.err_flag, QNMT_FLAG_NUMERIC);
+    }
+    __syncthreads();
+    if (warp == 1) {
+        tc::tc_fence_after();
+        tc::tmem_dealloc<C::TMEM_COLS>(tmem_base);
+    }
+}
+
+// exact logit of (row, token): dp4a over K (K % 16 == 0, 16-byte aligned rows)
+__device__ __forceinline__ float vt_logit(const int8_t* __restrict__ xr, const int8_t* __restrict__ wr, int K,
+                                          float sw, float sx, float b) {
+    int acc = 0;
+    for (int k = 0; k < K; k += 16) {
+        const int4 xa = *reinterpret_cast<const int4*>(xr + k);
+        const int4 wa = *reinterpret_cast<const int4*>(wr + k);
+        acc = __dp4a(xa.x, wa.x, acc);
+        acc = __dp4a(xa.y, wa.y, acc);
+        acc = __dp4a(xa.z, wa.z, acc);
+        acc = __dp4a(xa.w, wa.w, acc);
+    }
+    return __fadd_rn(dequant(acc, sw, sx), b);
+}
+
+struct VtMergeArgs {
+    const int8_t* X;
+    int64_t ldx;
+    const int8_t* W;
+    int64_t ldw;
+    int K, V, n_blocks;
+    const float* x_scales;
+    const int32_t* row_seg;
+    const float* w_scales;
+    int64_t w_rows_per_scale;
+    const float* bias;
+    const VtPart* part;
+    const double* live;
+    int k;
+    double* cand_score;
+    int32_t* cand_tok;
+};
+
+constexpr int VM_WARPS = 4;   // rows per merge CTA (one warp per row)
+
+template <int KM>
+__global__ void __launch_bounds__(32 * VM_WARPS)
+k_vocab_merge(VtMergeArgs a, int64_t N, const int32_t* n_dev) {
+    __shared__ double tab[16];
+    __shared__ Cand lst[VM_WARPS][KM];
+    __shared__ int flagged[VM_WARPS][VT_RESCAN_MAX];
+    const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x < 16) tab[threadIdx.x] = exp2((double)threadIdx.x / 16.0);
+    __syncthreads();
+    const int64_t n = (int64_t)blockIdx.x * VM_WARPS + wib;
+    if (n >= N || beyond(n_dev, n)) return;   // warp-uniform
+    const int np = 2 * a.n_blocks;
+    const VtPart* pr = a.part + n * np;
+    // one pass: online (max, sum exp) and the top-KM of the half-tile maxima
+    const int kk = a.V < KM ? a.V : KM;
+    Cand* out = lst[wib];
+    Cand L[KM];
+#pragma unroll
+    for (int i = 0; i < KM; ++i) L[i] = Cand{-DBL_MAX, 0x7fffffff};
+    float ml = -FLT_MAX;
+    double sl = 0.0;
+#pragma unroll 4
+    for (int b = lane; b < np; b += 32) {
+        const VtPart p = pr[b];
+        if (p.i1 == 0x7fffffff) continue;
+        if (p.m > ml) {
+            sl = (ml == -FLT_MAX) ? 0.0 : sl * exp_neg((double)ml - (double)p.m, tab);
+            ml = p.m;
+        }
+        sl += p.s * exp_neg((double)p.m - (double)ml, tab);
+        insert<KM>(L, Cand{(double)p.m, p.i1});
+    }
+    const float M = warp_max(ml);
+    const double dM = (double)M;
+    const double lse = log(warp_sum(ml == -FLT_MAX ? 0.0 : sl * exp_neg((double)ml - dM, tab)));
+    warp_merge<KM>(L, out, kk);
+    __syncwarp();
+    // half-tiles whose runner-up reaches the KM-th value may hold more of the top-KM
+    const Cand thr = out[kk - 1];
+    int nf = 0;
+    for (int b0 = 0; b0 < np; b0 += 32) {
+        const int b = b0 + lane;
+        const bool f = b < np && pr[b].a2 != -FLT_MAX && (double)pr[b].a2 >= thr.s;
+        const unsigned mask = __ballot_sync(0xffffffffu, f);
+        const int slot = nf + __popc(mask & ((1u << lane) - 1u));
+        if (f && slot < VT_RESCAN_MAX) flagged[wib][slot] = b;
+        nf += __popc(mask);
+    }
+    __syncwarp();
+    const int8_t* xr = a.X + n * a.ldx;
+    const float sx = a.x_scales[a.row_seg ? a.row_seg[n] : 0];
+    if (nf > 0 && nf <= VT_RESCAN_MAX) {
+        // rebuild: unflagged partials' entries + every token of the flagged half-tiles
+#pragma unroll
+        for (int i = 0; i < KM; ++i) L[i] = Cand{-DBL_MAX, 0x7fffffff};
+        for (int b = lane; b < np; b += 32) {
+            bool fl = false;
+            for (int f = 0; f < nf; ++f) fl |= flagged[wib][f] == b;
+            if (!fl && pr[b].i1 != 0x7fffffff) insert<KM>(L, Cand{(double)pr[b].m, pr[b].i1});
+        }
+        for (int idx = lane; idx < nf * VT_HALF; idx += 32) {
+            const int b = flagged[wib][idx / VT_HALF];
+            const int v = (b >> 1) * VT_BN + (b & 1) * VT_HALF + idx % VT_HALF;
+            if (v >= a.V) continue;
+            const float x = vt_logit(xr, a.W + (int64_t)v * a.ldw, a.K, a.w_scales[v / a.w_rows_per_scale], sx,
+                                     a.bias ? a.bias[v] : 0.0f);
+            insert<KM>(L, Cand{(double)x, v});
+        }
+        __syncwarp();
+        warp_merge<KM>(L, out, kk);
+        __syncwarp();
+    }
+    const double base = a.live ? a.live[n] : 0.0;
+    int ok = 0;
+    if (lane == 0 && nf <= VT_RESCAN_MAX) {
+        // exact scores of the KM logit-candidates, ordered by (score desc, token asc)
+        Cand c[KM];
+        for (int i = 0; i < kk; ++i) c[i] = Cand{base + (double)__double2float_rn((out[i].s - dM) - lse), out[i].t};
+        const double s_last = c[kk - 1].s;
+        for (int i = 1; i < kk; ++i) {
+            Cand t = c[i];
+            int j = i - 1;
+            while (j >= 0 && better(t, c[j])) { c[j + 1] = c[j]; --j; }
+            c[j + 1] = t;
+        }
+        ok = (a.V <= KM) || (c[a.k - 1].s > s_last);
+        if (ok)
+            for (int i = 0; i < a.k; ++i) {
+                a.cand_score[n * a.k + i] = c[i].s;
+                a.cand_tok[n * a.k + i] = c[i].t;
+            }
+    }
+    if (__shfl_sync(0xffffffffu, ok, 0)) return;
+    // f32 tie across the KM boundary (or too many flagged half-tiles): exact scores for the whole row
+#pragma unroll
+    for (int i = 0; i < KM; ++i) L[i] = Cand{-DBL_MAX, 0x7fffffff};
+    for (int v = lane; v < a.V; v += 32) {
+        const float x = vt_logit(xr, a.W + (int64_t)v * a.ldw, a.K, a.w_scales[v / a.w_rows_per_scale], sx,
+                                 a.bias ? a.bias[v] : 0.0f);
+        insert<KM>(L, Cand{base + (double)__double2float_rn(((double)x - dM) - lse), v});
+    }
+    __syncwarp();
+    warp_merge<KM>(L, out, a.k);
+    __syncwarp();
+    if (lane == 0)
+        for (int i = 0; i < a.k; ++i) {
+            a.cand_score[n * a.k + i] = out[i].s;
+            a.cand_tok[n * a.k + i] = out[i].t;
+        }
+}
+
+bool vocab_topk_eligible(int64_t K, int64_t ldx, int64_t ldw, const void* X, const void* W, int k) {
+    return K % 16 == 0 && K > 0 && K <= QNMT_INT32_SAFE_K && ldx % 16 == 0 && ldw % 16 == 0 &&
+           ((uintptr_t)X % 16 == 0) && ((uintptr_t)W % 16 == 0) && k >= 1 && k <= 16;
+}
+
+size_t vocab_topk_part_bytes(int64_t rows, int64_t V) {
+    return (size_t)rows * 2 * (size_t)cdiv(V, VT_BN) * sizeof(VtPart);
+}
+
+int g_vocab_fused = 1;
+
+int vocab_stats_launch(const VocabTopk& p, cudaStream_t st) {
+    const int8_t* X = p.X;
+    const int64_t N = p.N, ldx = p.ldx, V = p.V, K = p.K, ldw = p.ldw;
+    const int8_t* W = p.W;
+    const int k = p.k;
+    if (N <= 0) return QNMT_OK;
+    if (!vocab_topk_eligible(K, ldx, ldw, X, W, k) || k > V) {
+        set_error("vocab_topk: ineligible shape K=%lld k=%d V=%lld", (long long)K, k, (long long)V);
+        return QNMT_ERR_CONFIG;
+    }
+    static bool attr_set = false;
+    if (!attr_set) {
+        QNMT_CUDA(cudaFuncSetAttribute(k_vocab_stats, cudaFuncAttributeMaxDynamicSharedMemorySize, VtRing::SMEM));
+        attr_set = true;
+    }
+    CUtensorMap tx, tw;
+    int rc = tc_get_map(X, N, K, ldx, TC_BM, &tx);
+    if (rc) return rc;
+    rc = tc_get_map(W, V, K, ldw, VT_BN, &tw);
+    if (rc) return rc;
+    VtArgs e{p.x_scales, p.row_seg, p.w_scales, p.w_rows_per_scale, p.bias, reinterpret_cast<VtPart*>(p.part),
+             p.err_flag};
+    const int n_blocks = (int)cdiv(V, VT_BN);
+    const int tiles = (int)(cdiv(N, TC_BM) * n_blocks);
+    const int grid = tiles < tc_sm_count() ? tiles : tc_sm_count();
+    k_vocab_stats<<<grid, VT_THREADS, VtRing::SMEM, st>>>(tx, tw, (int)N, (int)V, (int)K, e, tl_ndev);
+    QNMT_CHECK_LAUNCH("k_vocab_stats");
+    return QNMT_OK;
+}
+
+int vocab_merge_launch(const VocabTopk& p, cudaStream_t st) {
+    const int64_t N = p.N;
+    const int k = p.k;
+    if (N <= 0) return QNMT_OK;
+    VtMergeArgs ma{p.X, p.ldx, p.W, p.ldw, (int)p.K, (int)p.V, (int)cdiv(p.V, VT_BN), p.x_scales, p.row_seg,
+                   p.w_scales, p.w_rows_per_scale, p.bias, reinterpret_cast<const VtPart*>(p.part), p.live, k,
+                   p.cand_score, p.cand_tok};
+    const unsigned g = (unsigned)cdiv(N, VM_WARPS);
+    if (k <= 6)
+        k_vocab_merge<8><<<g, 32 * VM_WARPS, 0, st>>>(ma, N, tl_ndev);
+    else if (k <= 13)
+        k_vocab_merge<16><<<g, 32 * VM_WARPS, 0, st>>>(ma, N, tl_ndev);
+    else
+        k_vocab_merge<32><<<g, 32 * VM_WARPS, 0, st>>>(ma, N, tl_ndev);
+    QNMT_CHECK_LAUNCH("k_vocab_merge");
+    return QNMT_OK;
+}
+
+}  // namespace qnmt
+
+extern "C" int qnmt_set_vocab_fused(int enable) {
+    const int old = qnmt::g_vocab_fused;
+    qnmt::g_vocab_fused = enable;
+    return old;
+}
+
+extern "C" int qnmt_vocab_candidates(const int8_t* X, int64_t N, int64_t ldx, const float* x_scales,
+                                     const int32_t* row_seg, const int8_t* W, int64_t V, int64_t K, int64_t ldw,
+                                     const float* w_scales, int64_t w_rows_per_scale, const float* bias,
+                                     const double* live_scores, int32_t k, void* scratch, double* cand_score,
+                                     int32_t* cand_tok, int32_t* err_flag, void* stream) {
+    if (N < 0 || V < 1 || w_rows_per_scale < 1) {
+        qnmt::set_error("qnmt_vocab_candidates: bad shape N=%lld V=%lld", (long long)N, (long long)V);
+        return QNMT_ERR_SHAPE;
+    }
+    const qnmt::VocabTopk p{X, N, ldx, x_scales, row_seg, W, V, K, ldw, w_scales, w_rows_per_scale, bias,
+                            live_scores, k, scratch, cand_score, cand_tok, err_flag};
+    const cudaStream_t st = qnmt::as_stream(stream);
+    int rc = qnmt::vocab_stats_launch(p, st);
+    if (rc != QNMT_OK) return rc;
+    return qnmt::vocab_merge_launch(p, st);
+}
+
+extern "C" int64_t qnmt_vocab_candidates_scratch(int64_t N, int64_t V) {
+    return (int64_t)qnmt::vocab_topk_part_bytes(N, V);
+}

@@ -170,3 +170,91 @@ def test_candidate_kernels_exact(V, k, ties):
         order = sorted(range(V), key=lambda v: (-sc[v], v))[:k]
         assert t1[n].tolist() == order and t3[n].tolist() == order, n
         assert np.array_equal(s1[n], sc[order]) and np.array_equal(s3[n], sc[order])
+
+
+def _fused_pair(eng, sents, beam, ratio):
+    from paper_1804_05038_b200 import _lib
+    lib = _lib.load()
+    old = lib.qnmt_set_vocab_fused(1)
+    try:
+        fused = eng.translate_ids(sents, beam, ratio)
+        lib.qnmt_set_vocab_fused(0)
+        plain = eng.translate_ids(sents, beam, ratio)
+    finally:
+        lib.qnmt_set_vocab_fused(old)
+    return fused, plain
+
+
+@pytest.mark.parametrize("beam", [1, 5, 12])
+def test_vocab_fused_equals_unfused_and_oracle(beam):
+    """Fused vocab projection + softmax statistics + candidates (vocab_topk.cu)
+    == vocab GEMM + candidate kernel == oracle, V not a multiple of the tile."""
+    d = pb.Dims(200, 1333, 64, 64, 64, 48)
+    params = pb.synthetic_model(d, 5, weight_std=0.3, bias_std=0.2, eos_bias=0.5)
+    qm = pb.quantize_model(params)
+    om = O.QModel(O.Dims(**d.as_dict()), params.tensors)
+    rng = np.random.default_rng(beam + 100)
+    sents = [rng.integers(3, 200, int(rng.integers(1, 20))).tolist() for _ in range(19)]
+    eng = pb.Engine(qm, 32, 32, 16)
+    fused, plain = _fused_pair(eng, sents, beam, 1.5)
+    assert fused == plain
+    for i, s in enumerate(sents[:8]):
+        toks, lp = om.translate(s, beam, 1.5)
+        assert fused[0][i] == toks and fused[1][i] == lp, i
+
+
+@pytest.mark.parametrize("dup", [3, 40])
+def test_vocab_fused_ties(dup):
+    """Tie-heavy vocabularies: W_vocab rows repeat every `dup` tokens, so whole
+    groups of tokens share one logit.  Exercises the fused merge's exact rescan
+    of half-tiles (many equal logits in one 128-token half) and its full-row
+    fallback (ties across the candidate boundary)."""
+    d = pb.Dims(120, 700, 32, 32, 32, 32)
+    params = pb.synthetic_model(d, 9, weight_std=0.4, bias_std=0.0, eos_bias=0.3)
+    w = params.tensors["out.w_vocab"]
+    params.tensors["out.w_vocab"] = np.ascontiguousarray(w[np.arange(d.tgt_vocab) % dup]).astype(F32)
+    qm = pb.quantize_model(params)
+    om = O.QModel(O.Dims(**d.as_dict()), params.tensors)
+    rng = np.random.default_rng(dup)
+    sents = [rng.integers(3, 120, int(rng.integers(1, 9))).tolist() for _ in range(6)]
+    eng = pb.Engine(qm, 8, 16, 8)
+    fused, plain = _fused_pair(eng, sents, 5, 1.5)
+    assert fused == plain
+    for i, s in enumerate(sents):
+        toks, lp = om.translate(s, 5, 1.5)
+        assert fused[0][i] == toks and fused[1][i] == lp, i
+
+
+@pytest.mark.parametrize("V,k,dup", [(50000, 5, 0), (50000, 5, 97), (3001, 8, 7), (700, 16, 0), (300, 12, 2),
+                                     (20, 5, 0)])
+def test_vocab_candidates_abi(V, k, dup):
+    """qnmt_vocab_candidates (fused) == qnmt_gemm_i8 + qnmt_topk_candidates on
+    the same codes, including vocabularies with repeated rows (exact ties)."""
+    import torch
+    from paper_1804_05038_b200 import _lib, _dev
+    rng = np.random.default_rng(V + 31 * k + dup)
+    N, K = 37, 64
+    w = rng.integers(-127, 128, (V, K)).astype(np.int8)
+    if dup:
+        w = w[np.arange(V) % dup]
+    W = torch.from_numpy(np.ascontiguousarray(w)).cuda()
+    X = torch.from_numpy(rng.integers(-127, 128, (N, K)).astype(np.int8)).cuda()
+    ws = torch.full((1,), 900.0, device="cuda")
+    seg = torch.from_numpy((np.arange(N) // 5).astype(np.int32)).cuda()
+    xs = torch.from_numpy(rng.uniform(300, 900, N // 5 + 1).astype(np.float32)).cuda()
+    bias = torch.from_numpy((np.round(rng.normal(0, 0.5, V) * 8) / 8).astype(np.float32)).cuda()
+    live = torch.from_numpy(rng.normal(-10, 3, N)).cuda()
+    Y = pb.qmath.gemm_kmajor(W, ws, V, X, xs, col_seg=seg, bias=bias)
+    cs0 = torch.empty((N, k), dtype=torch.float64, device="cuda")
+    ct0 = torch.empty((N, k), dtype=torch.int32, device="cuda")
+    f = _dev.reset_flag()
+    _lib.call("qnmt_topk_candidates", Y.data_ptr(), N, V, V, live.data_ptr(), k, cs0.data_ptr(), ct0.data_ptr(),
+              f.data_ptr(), _dev.stream_ptr())
+    cs1 = torch.empty_like(cs0)
+    ct1 = torch.empty_like(ct0)
+    scratch = torch.empty(int(_lib.load().qnmt_vocab_candidates_scratch(N, V)), dtype=torch.uint8, device="cuda")
+    _lib.call("qnmt_vocab_candidates", X.data_ptr(), N, K, xs.data_ptr(), seg.data_ptr(), W.data_ptr(), V, K, K,
+              ws.data_ptr(), V, bias.data_ptr(), live.data_ptr(), k, scratch.data_ptr(), cs1.data_ptr(),
+              ct1.data_ptr(), f.data_ptr(), _dev.stream_ptr())
+    _dev.raise_flag(f)
+    assert torch.equal(ct0, ct1) and torch.equal(cs0, cs1)
