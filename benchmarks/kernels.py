@@ -139,8 +139,14 @@ def vocab_case(N=1280, V=50000, K=512, k=5, fused=True):
             _lib.call("qnmt_topk_candidates", Y.data_ptr(), N, V, V, live.data_ptr(), k, cs.data_ptr(),
                       ct.data_ptr(), f.data_ptr(), st())
     t = graph_time(fn, reps=5)
-    return {"kernel": "vocab+candidates " + ("fused" if fused else "gemm+topk"), "N": N, "V": V, "K": K,
-            "us": t * 1e6, "logits_per_s": N * V / t, "TOPS": 2.0 * N * V * K / t / 1e12}
+    out = {"kernel": "vocab+candidates " + ("fused" if fused else "gemm+topk"), "N": N, "V": V, "K": K,
+           "us": t * 1e6, "logits_per_s": N * V / t, "TOPS": 2.0 * N * V * K / t / 1e12}
+    if fused:   # merge path per row (pad of the row's first 24-byte partial)
+        np_ = scratch.numel() // (24 * N)
+        pad = scratch.view(torch.int32).view(N, np_ * 6)[:, 5].cpu().numpy()
+        vals, cnts = np.unique(pad, return_counts=True)
+        out["merge_paths"] = {int(v): int(c) for v, c in zip(vals, cnts)}
+    return out
 
 
 def gemv_cold(bsz):

@@ -23,7 +23,7 @@ struct TcRing {
     static constexpr int B_BYTES = BN * TC_BK;
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
     static constexpr int STAGES = STAGES_;
-    static constexpr int TMEM_COLS = 2 * BN;   // power of two for BN in {64, 128, 256}
+    static constexpr int TMEM_COLS = 2 * BN <= 64 ? 64 : 2 * BN <= 128 ? 128 : 2 * BN <= 256 ? 256 : 512;   // pow2
     static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
 };
 

@@ -27,11 +27,12 @@
 
 namespace qnmt {
 
-constexpr int VT_BN = 256;
-constexpr int VT_EPI_WARPS = 8;
+constexpr int VT_BN = 192;          // tokens per tile (UMMA N); 2 accumulators in a 512-column TMEM slot
+constexpr int VT_EPI_WARPS = 12;   // 3 per TMEM lane group (64 tokens each): latency hiding for the fp64 epilogue
 constexpr int VT_THREADS = 64 + 32 * VT_EPI_WARPS;
 using VtRing = TcRing<VT_BN, 4>;
-constexpr int VT_HALF = VT_BN / 2;   // tokens per partial
+constexpr int VT_SPLIT = VT_EPI_WARPS / 4;   // token groups per tile (one per warp of a lane group)
+constexpr int VT_HALF = VT_BN / VT_SPLIT;    // tokens per partial
 constexpr int VT_RESCAN_MAX = 64;    // flagged half-tiles handled per row before a full row rescan
 
 struct VtPart {
@@ -39,7 +40,7 @@ struct VtPart {
     float m;        // max logit (-FLT_MAX: empty)
     float a2;       // second-largest logit (may equal m; -FLT_MAX: fewer than 2 tokens)
     int32_t i1;     // smallest token with logit m (INT_MAX: empty)
-    int32_t pad;
+    int32_t pad;    // row's first partial, after the merge: path taken (diagnostics, see k_vocab_merge)
 };
 
 struct VtArgs {
@@ -83,8 +84,8 @@ k_vocab_stats(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ C
     } else {
         const int ew = warp - 2;
         const int lg = warp & 3;     // TMEM lane group
-        const int half = ew >> 2;    // token half of the tile
-        const int np = 2 * n_blocks;
+        const int half = ew >> 2;    // token group of the tile
+        const int np = VT_SPLIT * n_blocks;
         const bool one_scale = e.w_rows_per_scale >= V;   // kernel-uniform
         const double isw0 = 1.0 / (double)e.w_scales[0];
         bool bad = false;
@@ -93,7 +94,7 @@ k_vocab_stats(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ C
             const int mb = tile / n_blocks, nb = tile % n_blocks;
             const int buf = it & 1;
             const uint32_t use = (uint32_t)(it >> 1) & 1u;
-            {   // per-token weight scale and bias of this tile -> smem
+            if (ew * 32 < VT_BN) {   // per-token weight scale and bias of this tile -> smem
                 const int c = ew * 32 + lane;
                 const int v = nb * VT_BN + c;
                 float sw = 1.0f, b = 0.0f;
@@ -231,7 +232,7 @@ k_vocab_stats(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ C
                 p.a2 = a2;
                 p.i1 = i1;
                 p.pad = 0;
-                e.part[(int64_t)row * np + nb * 2 + half] = p;
+                e.part[(int64_t)row * np + nb * VT_SPLIT + half] = p;
             }
         }
         if (bad) set_flag(e.err_flag, QNMT_FLAG_NUMERIC);
@@ -241,21 +242,6 @@ k_vocab_stats(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ C
         tc::tc_fence_after();
         tc::tmem_dealloc<C::TMEM_COLS>(tmem_base);
     }
-}
-
-// exact logit of (row, token): dp4a over K (K % 16 == 0, 16-byte aligned rows)
-__device__ __forceinline__ float vt_logit(const int8_t* __restrict__ xr, const int8_t* __restrict__ wr, int K,
-                                          float sw, float sx, float b) {
-    int acc = 0;
-    for (int k = 0; k < K; k += 16) {
-        const int4 xa = *reinterpret_cast<const int4*>(xr + k);
-        const int4 wa = *reinterpret_cast<const int4*>(wr + k);
-        acc = __dp4a(xa.x, wa.x, acc);
-        acc = __dp4a(xa.y, wa.y, acc);
-        acc = __dp4a(xa.z, wa.z, acc);
-        acc = __dp4a(xa.w, wa.w, acc);
-    }
-    return __fadd_rn(dequant(acc, sw, sx), b);
 }
 
 struct VtMergeArgs {
@@ -269,12 +255,47 @@ struct VtMergeArgs {
     const float* w_scales;
     int64_t w_rows_per_scale;
     const float* bias;
-    const VtPart* part;
+    VtPart* part;
     const double* live;
     int k;
     double* cand_score;
     int32_t* cand_tok;
 };
+
+// Warp-cooperative exact logits of tokens v0 .. v0+31 for one row: lane j returns
+// the logit of token v0 + j (-FLT_MAX past the vocabulary).  Every token's K
+// codes are read as one coalesced 512-byte row slice (16 B per lane), dot
+// products by dp4a, reduced with one REDUX each; 8 tokens' loads in flight.
+__device__ __forceinline__ float vt_logits32(const VtMergeArgs& a, const int8_t* __restrict__ xr, int v0, float sx) {
+    const int lane = threadIdx.x & 31;
+    int mytot = 0;
+#pragma unroll 1
+    for (int t0 = 0; t0 < 32; t0 += 16) {
+        int part[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) part[u] = 0;
+        for (int k = lane * 16; k < a.K; k += 512) {
+            const int4 xa = *reinterpret_cast<const int4*>(xr + k);
+#pragma unroll
+            for (int u = 0; u < 16; ++u) {
+                const int v = min(v0 + t0 + u, a.V - 1);   // clamped tokens are discarded below
+                const int4 wa = *reinterpret_cast<const int4*>(a.W + (int64_t)v * a.ldw + k);
+                part[u] = __dp4a(xa.x, wa.x, part[u]);
+                part[u] = __dp4a(xa.y, wa.y, part[u]);
+                part[u] = __dp4a(xa.z, wa.z, part[u]);
+                part[u] = __dp4a(xa.w, wa.w, part[u]);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+            const int tot = __reduce_add_sync(0xffffffffu, part[u]);
+            if (lane == t0 + u) mytot = tot;
+        }
+    }
+    const int v = v0 + lane;   // one exact dequant per lane, in parallel
+    if (v >= a.V) return -FLT_MAX;
+    return __fadd_rn(dequant(mytot, a.w_scales[v / a.w_rows_per_scale], sx), a.bias ? a.bias[v] : 0.0f);
+}
 
 constexpr int VM_WARPS = 4;   // rows per merge CTA (one warp per row)
 
@@ -289,35 +310,89 @@ k_vocab_merge(VtMergeArgs a, int64_t N, const int32_t* n_dev) {
     __syncthreads();
     const int64_t n = (int64_t)blockIdx.x * VM_WARPS + wib;
     if (n >= N || beyond(n_dev, n)) return;   // warp-uniform
-    const int np = 2 * a.n_blocks;
-    const VtPart* pr = a.part + n * np;
-    // one pass: online (max, sum exp) and the top-KM of the half-tile maxima
+    const int np = VT_SPLIT * a.n_blocks;
+    VtPart* pr = a.part + n * np;
+    // pass 1: online (max, sum exp), each lane's best (max, token) and largest runner-up
     const int kk = a.V < KM ? a.V : KM;
     Cand* out = lst[wib];
-    Cand L[KM];
-#pragma unroll
-    for (int i = 0; i < KM; ++i) L[i] = Cand{-DBL_MAX, 0x7fffffff};
-    float ml = -FLT_MAX;
+    float ml = -FLT_MAX, a2l = -FLT_MAX;
+    int tl = 0x7fffffff;   // token of the lane's best max (smallest on ties)
     double sl = 0.0;
-#pragma unroll 4
-    for (int b = lane; b < np; b += 32) {
-        const VtPart p = pr[b];
-        if (p.i1 == 0x7fffffff) continue;
-        if (p.m > ml) {
-            sl = (ml == -FLT_MAX) ? 0.0 : sl * exp_neg((double)ml - (double)p.m, tab);
-            ml = p.m;
+    constexpr int PB = 8;   // partials per lane in flight
+    for (int b0 = lane; b0 < np; b0 += 32 * PB) {
+        VtPart p[PB];
+#pragma unroll
+        for (int i = 0; i < PB; ++i) {
+            const int b = b0 + 32 * i;
+            if (b < np) {
+                p[i] = pr[b];
+            } else {
+                p[i].m = -FLT_MAX;
+                p[i].a2 = -FLT_MAX;
+                p[i].i1 = 0x7fffffff;
+            }
         }
-        sl += p.s * exp_neg((double)p.m - (double)ml, tab);
-        insert<KM>(L, Cand{(double)p.m, p.i1});
+        float cmx = ml;
+#pragma unroll
+        for (int i = 0; i < PB; ++i) {
+            cmx = fmaxf(cmx, p[i].m);
+            a2l = fmaxf(a2l, p[i].a2);
+        }
+        if (cmx > ml) {
+            sl = (ml == -FLT_MAX) ? 0.0 : sl * exp_neg((double)ml - (double)cmx, tab);
+            ml = cmx;
+            tl = 0x7fffffff;
+        }
+#pragma unroll
+        for (int i = 0; i < PB; ++i) {
+            if (p[i].i1 != 0x7fffffff) {
+                sl += p[i].s * exp_neg((double)p[i].m - (double)ml, tab);
+                if (p[i].m == ml && p[i].i1 < tl) tl = p[i].i1;
+            }
+        }
     }
     const float M = warp_max(ml);
     const double dM = (double)M;
     const double lse = log(warp_sum(ml == -FLT_MAX ? 0.0 : sl * exp_neg((double)ml - dM, tab)));
+    // tau = kk-th best of the 32 lane maxima: at least kk half-tile maxima are >= tau, so every
+    // member of the top-kk is too; only those candidates enter the per-lane lists
+    Cand tau{-DBL_MAX, 0x7fffffff};
+    {
+        Cand mine{ml == -FLT_MAX ? -DBL_MAX : (double)ml, ml == -FLT_MAX ? 0x7fffffff : tl};
+        for (int r = 0; r < kk; ++r) {
+            Cand bst = mine;
+            int bl = lane;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const double os = __shfl_xor_sync(0xffffffffu, bst.s, o);
+                const int ot = __shfl_xor_sync(0xffffffffu, bst.t, o);
+                const int ol = __shfl_xor_sync(0xffffffffu, bl, o);
+                const Cand oc{os, ot};
+                if (better(oc, bst) || (!better(bst, oc) && ol < bl)) {
+                    bst = oc;
+                    bl = ol;
+                }
+            }
+            tau = bst;
+            if (lane == bl) mine = Cand{-DBL_MAX, 0x7fffffff};
+        }
+    }
+    Cand L[KM];
+#pragma unroll
+    for (int i = 0; i < KM; ++i) L[i] = Cand{-DBL_MAX, 0x7fffffff};
+    for (int b = lane; b < np; b += 32) {   // pass 2 (L1-resident): the few candidates >= tau
+        const float pm = pr[b].m;
+        if ((double)pm >= tau.s && pm != -FLT_MAX) {
+            const Cand c{(double)pm, pr[b].i1};
+            if (!better(tau, c)) insert<KM>(L, c);
+        }
+    }
     warp_merge<KM>(L, out, kk);
     __syncwarp();
     // half-tiles whose runner-up reaches the KM-th value may hold more of the top-KM
     const Cand thr = out[kk - 1];
     int nf = 0;
+    if (__any_sync(0xffffffffu, a2l != -FLT_MAX && (double)a2l >= thr.s))   // rare: find the half-tiles
     for (int b0 = 0; b0 < np; b0 += 32) {
         const int b = b0 + lane;
         const bool f = b < np && pr[b].a2 != -FLT_MAX && (double)pr[b].a2 >= thr.s;
@@ -333,18 +408,23 @@ k_vocab_merge(VtMergeArgs a, int64_t N, const int32_t* n_dev) {
         // rebuild: unflagged partials' entries + every token of the flagged half-tiles
 #pragma unroll
         for (int i = 0; i < KM; ++i) L[i] = Cand{-DBL_MAX, 0x7fffffff};
+        // (only candidates not worse than tau can be in the top-kk)
         for (int b = lane; b < np; b += 32) {
+            const float pm = pr[b].m;
+            if ((double)pm < tau.s || pm == -FLT_MAX) continue;
             bool fl = false;
             for (int f = 0; f < nf; ++f) fl |= flagged[wib][f] == b;
-            if (!fl && pr[b].i1 != 0x7fffffff) insert<KM>(L, Cand{(double)pr[b].m, pr[b].i1});
+            const Cand c{(double)pm, pr[b].i1};
+            if (!fl && !better(tau, c)) insert<KM>(L, c);
         }
-        for (int idx = lane; idx < nf * VT_HALF; idx += 32) {
-            const int b = flagged[wib][idx / VT_HALF];
-            const int v = (b >> 1) * VT_BN + (b & 1) * VT_HALF + idx % VT_HALF;
-            if (v >= a.V) continue;
-            const float x = vt_logit(xr, a.W + (int64_t)v * a.ldw, a.K, a.w_scales[v / a.w_rows_per_scale], sx,
-                                     a.bias ? a.bias[v] : 0.0f);
-            insert<KM>(L, Cand{(double)x, v});
+        for (int f = 0; f < nf; ++f) {
+            const int b = flagged[wib][f];
+            const int vb = (b / VT_SPLIT) * VT_BN + (b % VT_SPLIT) * VT_HALF;
+            for (int g = 0; g < VT_HALF; g += 32) {
+                const float x = vt_logits32(a, xr, vb + g, sx);
+                const Cand c{(double)x, vb + g + lane};
+                if (vb + g + lane < a.V && !better(tau, c)) insert<KM>(L, c);
+            }
         }
         __syncwarp();
         warp_merge<KM>(L, out, kk);
@@ -352,32 +432,76 @@ k_vocab_merge(VtMergeArgs a, int64_t N, const int32_t* n_dev) {
     }
     const double base = a.live ? a.live[n] : 0.0;
     int ok = 0;
-    if (lane == 0 && nf <= VT_RESCAN_MAX) {
-        // exact scores of the KM logit-candidates, ordered by (score desc, token asc)
-        Cand c[KM];
-        for (int i = 0; i < kk; ++i) c[i] = Cand{base + (double)__double2float_rn((out[i].s - dM) - lse), out[i].t};
-        const double s_last = c[kk - 1].s;
-        for (int i = 1; i < kk; ++i) {
-            Cand t = c[i];
-            int j = i - 1;
-            while (j >= 0 && better(t, c[j])) { c[j + 1] = c[j]; --j; }
-            c[j + 1] = t;
+    if (nf <= VT_RESCAN_MAX) {
+        // exact scores of the KM logit-candidates (lane i: candidate i), then each lane's rank
+        // in (score desc, token asc) order; exact unless the k-th score ties the KM-th
+        Cand c{-DBL_MAX, 0x7fffffff};
+        if (lane < kk) c = Cand{base + (double)__double2float_rn((out[lane].s - dM) - lse), out[lane].t};
+        const double s_last = __shfl_sync(0xffffffffu, c.s, kk - 1);
+        int rank = 0;
+#pragma unroll
+        for (int j = 0; j < KM; ++j) {
+            const double os = __shfl_sync(0xffffffffu, c.s, j);
+            const int ot = __shfl_sync(0xffffffffu, c.t, j);
+            rank += (j < kk && j != lane && better(Cand{os, ot}, c)) ? 1 : 0;
         }
-        ok = (a.V <= KM) || (c[a.k - 1].s > s_last);
-        if (ok)
-            for (int i = 0; i < a.k; ++i) {
-                a.cand_score[n * a.k + i] = c[i].s;
-                a.cand_tok[n * a.k + i] = c[i].t;
-            }
+        const unsigned at_k = __ballot_sync(0xffffffffu, lane < kk && rank == a.k - 1);
+        const double sk = __shfl_sync(0xffffffffu, c.s, at_k ? __ffs(at_k) - 1 : 0);
+        ok = (a.V <= KM) || (sk > s_last);
+        if (ok && lane < kk && rank < a.k) {
+            a.cand_score[n * a.k + rank] = c.s;
+            a.cand_tok[n * a.k + rank] = c.t;
+        }
     }
-    if (__shfl_sync(0xffffffffu, ok, 0)) return;
-    // f32 tie across the KM boundary (or too many flagged half-tiles): exact scores for the whole row
+    // diagnostics: pad of the row's first partial = flagged half-tiles (phase 1) + 1000 * path
+    // (0 merged, 1 boundary-tie rescan, 2 whole row)
+    if (ok) {
+        if (lane == 0) pr[0].pad = nf;
+        return;
+    }
 #pragma unroll
     for (int i = 0; i < KM; ++i) L[i] = Cand{-DBL_MAX, 0x7fffffff};
-    for (int v = lane; v < a.V; v += 32) {
-        const float x = vt_logit(xr, a.W + (int64_t)v * a.ldw, a.K, a.w_scales[v / a.w_rows_per_scale], sx,
-                                 a.bias ? a.bias[v] : 0.0f);
-        insert<KM>(L, Cand{base + (double)__double2float_rn(((double)x - dM) - lse), v});
+    // f32 tie across the KM boundary: tokens outside the list whose log-prob rounds to the KM-th
+    // candidate's have logits within a few f32 ulps of lp below x_KM.  Every other token scores
+    // strictly lower, so the exact answer is the top-k of the exact scores of all tokens in the
+    // half-tiles that may hold a logit >= x_KM - 4 ulp(lp_KM) (max or runner-up reaching it).
+    int nf2 = VT_RESCAN_MAX + 1;
+    if (nf <= VT_RESCAN_MAX) {
+        const float lpk = __double2float_rn((out[kk - 1].s - dM) - lse);
+        const int ex = (int)((__float_as_uint(lpk) >> 23) & 0xffu);
+        const double tau2 = out[kk - 1].s - ldexp(1.0, max(ex, 1) - 150 + 2);
+        nf2 = 0;
+        for (int b0 = 0; b0 < np; b0 += 32) {
+            const int b = b0 + lane;
+            const bool f = b < np && ((pr[b].i1 != 0x7fffffff && (double)pr[b].m >= tau2) ||
+                                      (pr[b].a2 != -FLT_MAX && (double)pr[b].a2 >= tau2));
+            const unsigned mask = __ballot_sync(0xffffffffu, f);
+            const int slot = nf2 + __popc(mask & ((1u << lane) - 1u));
+            if (f && slot < VT_RESCAN_MAX) flagged[wib][slot] = b;
+            nf2 += __popc(mask);
+        }
+        __syncwarp();
+        if (nf2 <= VT_RESCAN_MAX) {
+            for (int f = 0; f < nf2; ++f) {
+                const int b = flagged[wib][f];
+                const int vb = (b / VT_SPLIT) * VT_BN + (b % VT_SPLIT) * VT_HALF;
+                for (int g = 0; g < VT_HALF; g += 32) {
+                    const float x = vt_logits32(a, xr, vb + g, sx);
+                    if (vb + g + lane < a.V)
+                        insert<KM>(L, Cand{base + (double)__double2float_rn(((double)x - dM) - lse), vb + g + lane});
+                }
+            }
+        }
+    }
+    if (lane == 0) pr[0].pad = nf + (nf2 > VT_RESCAN_MAX ? 2000 : 1000) + 10000 * min(nf2, 99);
+    if (nf2 > VT_RESCAN_MAX) {   // pathological ties (e.g. repeated vocabulary rows): the whole row
+#pragma unroll
+        for (int i = 0; i < KM; ++i) L[i] = Cand{-DBL_MAX, 0x7fffffff};
+        for (int v0 = 0; v0 < a.V; v0 += 32) {
+            const float x = vt_logits32(a, xr, v0, sx);
+            if (v0 + lane < a.V)
+                insert<KM>(L, Cand{base + (double)__double2float_rn(((double)x - dM) - lse), v0 + lane});
+        }
     }
     __syncwarp();
     warp_merge<KM>(L, out, a.k);
@@ -395,7 +519,7 @@ bool vocab_topk_eligible(int64_t K, int64_t ldx, int64_t ldw, const void* X, con
 }
 
 size_t vocab_topk_part_bytes(int64_t rows, int64_t V) {
-    return (size_t)rows * 2 * (size_t)cdiv(V, VT_BN) * sizeof(VtPart);
+    return (size_t)rows * VT_SPLIT * (size_t)cdiv(V, VT_BN) * sizeof(VtPart);
 }
 
 int g_vocab_fused = 1;
@@ -435,7 +559,7 @@ int vocab_merge_launch(const VocabTopk& p, cudaStream_t st) {
     const int k = p.k;
     if (N <= 0) return QNMT_OK;
     VtMergeArgs ma{p.X, p.ldx, p.W, p.ldw, (int)p.K, (int)p.V, (int)cdiv(p.V, VT_BN), p.x_scales, p.row_seg,
-                   p.w_scales, p.w_rows_per_scale, p.bias, reinterpret_cast<const VtPart*>(p.part), p.live, k,
+                   p.w_scales, p.w_rows_per_scale, p.bias, reinterpret_cast<VtPart*>(p.part), p.live, k,
                    p.cand_score, p.cand_tok};
     const unsigned g = (unsigned)cdiv(N, VM_WARPS);
     if (k <= 6)
