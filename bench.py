@@ -48,7 +48,7 @@ METRIC = "tokens/sec (int8 beam-5 decode, target tokens excl. EOS)"
 WORKLOAD = ("cfg5 bulk translation shard: 256 sentences/GPU/step of a seeded 8192-sentence corpus, "
             "l~U[5,100], beam 5, max_ratio 1.5, V_tgt 50000, H 1024, E 512, A 2048, R 512")
 # DRAM bytes per algorithmic byte measured by `ncu --set full` at N = 1280 (profiles/r01_ncu_summary.md)
-NCU_TRAFFIC_RATIO = {"topk": 256.9 / 256.0, "attention": None, "gemm_vocab": None}
+NCU_TRAFFIC_RATIO = {"attention": 264.4 / 249.8, "vocab_stats": 34.47 / 50.30, "vocab_merge": 24.14 / 24.13}
 
 
 def peaks():
@@ -145,29 +145,46 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
-def kernel_rooflines(rows, hbm, peak_kind):
-    """rows: stamps of the timed steps -> per-kernel achieved vs roofline."""
+VT_TILE, VT_GROUPS, VT_PART_BYTES = 192, 3, 24   # vocab_topk.cu: tokens per tile, partials per tile, bytes
+
+
+def kernel_rooflines(rows, hbm, peak_kind, sm_mhz=None):
+    """rows: stamps of the timed steps -> per-kernel achieved vs roofline.
+
+    Every kernel gets the contract's HBM roofline (algorithmic bytes / device
+    time, against the measured copy bandwidth) and, where the kernel is bound by
+    an arithmetic pipe instead, a "compute" roofline for that pipe:
+      attention    MUFU: 2 ops (ex2, rcp) per tanh element, 16 ops/clk/SM
+      vocab_stats  fp64: 14 ops per logit (dequant, exp, sum), 64 ops/clk/SM
+    """
     V, R, A, H2 = DIMS["tgt_vocab"], DIMS["readout"], DIMS["attn"], 2 * DIMS["hidden"]
-    t = {"attention": 0.0, "topk": 0.0, "gemm_vocab": 0.0, "step": 0.0}
-    work = {"attention": 0.0, "topk": 0.0, "gemm_vocab": 0.0}
+    f = (sm_mhz or 1965.0) * 1e6
+    n_parts = VT_GROUPS * ((V + VT_TILE - 1) // VT_TILE)
+    t = {"attention": 0.0, "vocab_merge": 0.0, "vocab_stats": 0.0, "step": 0.0}
+    work = {"attention": 0.0, "vocab_merge": 0.0, "vocab_stats": 0.0}
+    comp = {"attention": 0.0, "vocab_stats": 0.0}
     ops_vocab = 0.0
     launches = 0
     for r in rows:
-        n, sl = float(r[8]), float(r[9])
+        n, sl, spl = float(r[8]), float(r[9]), float(r[10])
         if n <= 0:
             continue
         launches += 1
         t["attention"] += (r[2] - r[1]) * 1e-9
-        t["topk"] += (r[4] - r[3]) * 1e-9
-        t["gemm_vocab"] += (r[6] - r[5]) * 1e-9
+        t["vocab_merge"] += (r[4] - r[3]) * 1e-9
+        t["vocab_stats"] += (r[6] - r[5]) * 1e-9
         t["step"] += (r[4] - r[0]) * 1e-9
         # algorithmic bytes per launch
         work["attention"] += 4.0 * (sl * A + sl * H2 + n * A + n * H2)   # att_proj, states, u, ctx
-        work["topk"] += 4.0 * n * V                                       # logits read once
-        work["gemm_vocab"] += V * R + n * R + 4.0 * n * V                 # W, X codes, logits write
+        work["vocab_stats"] += V * R + n * R + n * n_parts * VT_PART_BYTES   # W, X codes, partials
+        work["vocab_merge"] += n * n_parts * VT_PART_BYTES + n * BEAM * 12  # partials, candidates
+        comp["attention"] += spl * A              # tanh elements
+        comp["vocab_stats"] += n * V              # logits
         ops_vocab += 2.0 * V * R * n
+    peaks_c = {"attention": ("tanh elements/s (2 MUFU ops each)", 16 * 148 * f / 2),
+               "vocab_stats": ("logits/s (14 fp64 ops each)", 64 * 148 * f / 14)}
     out = {}
-    for k in ("attention", "topk", "gemm_vocab"):
+    for k in ("attention", "vocab_stats", "vocab_merge"):
         if t[k] <= 0:
             continue
         ach = work[k] / t[k] / 1e9
@@ -177,9 +194,12 @@ def kernel_rooflines(rows, hbm, peak_kind):
                   "traffic": (work[k] / max(launches, 1) * ratio) if ratio else None,
                   "algorithmic_bytes_per_launch": work[k] / max(launches, 1), "peak_source": peak_kind,
                   "share_of_step": t[k] / t["step"] if t["step"] > 0 else None}
-    if "gemm_vocab" in out:
-        out["gemm_vocab"]["int_ops_per_s"] = ops_vocab / t["gemm_vocab"]
-        out["gemm_vocab"]["tensor_frac_of_int8_spec_4500T"] = ops_vocab / t["gemm_vocab"] / 4.5e15
+        if k in peaks_c:
+            unit, pk = peaks_c[k]
+            ca = comp[k] / t[k]
+            out[k]["compute"] = {"unit": unit, "achieved": ca, "peak": pk, "frac": ca / pk}
+    if "vocab_stats" in out:
+        out["vocab_stats"]["int8_tensor_ops_per_s"] = ops_vocab / t["vocab_stats"]
     return out
 
 
@@ -222,7 +242,7 @@ def main():
     flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device=dev)   # > 126 MB L2
     stamps_on = not args.no_stamps
     lib.qnmt_engine_stamps(eng._h, 1 if stamps_on else 0)   # graphs are captured during warm-up
-    stamp_buf = np.zeros((256, 10), dtype=np.int64)
+    stamp_buf = np.zeros((256, 11), dtype=np.int64)   # QNMT_STAMP_COLS
 
     def fetch(batch):
         stride = int(math.ceil(MAX_RATIO * max(len(s) for s in batch))) + 1
@@ -309,7 +329,7 @@ def main():
     e2e_value = e2e_toks / e2e_secs
 
     hbm, peak_kind = peaks()
-    kern = kernel_rooflines(all_rows, hbm, peak_kind) if all_rows else {}
+    kern = kernel_rooflines(all_rows, hbm, peak_kind, clocks.get("sm_mhz") if clocks else None) if all_rows else {}
     roof = None
     if kern:
         dom = max(kern, key=lambda k: kern[k]["us_per_launch"])

@@ -295,10 +295,13 @@ int qnmt_engine_set_graphs(qnmt_engine* e, int enable);
 /* Device-clock stamps (%globaltimer) inside the captured decode steps, for
  * live per-kernel timing in graph mode.  After a decode, _read copies one row
  * of QNMT_STAMP_COLS int64 per executed step: [step start, attention start,
- * attention end, top-k start, top-k end, vocab GEMM start, vocab GEMM end,
- * (unused), live columns N, sum of source lengths of live sentences];
- * returns the number of rows. */
-#define QNMT_STAMP_COLS 10
+ * attention end, candidate merge start, candidate merge end, vocab projection
+ * start, vocab projection end, (unused), live columns N, sum of source lengths
+ * of live sentences, sum over sentences of live hypotheses x source length];
+ * returns the number of rows.  With the fused vocabulary path the projection
+ * interval is k_vocab_stats and the merge interval k_vocab_merge; otherwise
+ * the vocab GEMM and qnmt_topk_candidates. */
+#define QNMT_STAMP_COLS 11
 int qnmt_engine_stamps(qnmt_engine* e, int enable);
 int qnmt_engine_stamps_read(qnmt_engine* e, int64_t* out, int32_t max_rows, void* stream);
 

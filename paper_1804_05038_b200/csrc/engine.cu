@@ -388,23 +388,36 @@ struct StepIO {
 // e->stamps holds %globaltimer at ST_* points of step t, the live column count
 // and the sum of source lengths of live sentences (algorithmic-work accounting).
 // ---------------------------------------------------------------------------
-enum { ST_STEP0 = 0, ST_ATT0, ST_ATT1, ST_TOPK0, ST_TOPK1, ST_VOC0, ST_VOC1, ST_STEP1, ST_N, ST_SUML, ST_COLS };
+enum { ST_STEP0 = 0, ST_ATT0, ST_ATT1, ST_TOPK0, ST_TOPK1, ST_VOC0, ST_VOC1, ST_STEP1, ST_N, ST_SUML, ST_SUMPL,
+       ST_COLS };
+static_assert(ST_COLS == QNMT_STAMP_COLS, "stamp row layout");
 
 __global__ void k_stamp(long long* stamps, const int32_t* step_dev, int slot, int slot2, const int32_t* n_dev,
                         const int32_t* P, const int32_t* len, int n_sent) {
     const int t = *step_dev;
     long long* row = stamps + (int64_t)t * ST_COLS;
     if (slot == ST_ATT0) {   // also record the work descriptors of this step
-        __shared__ int red[32];
-        int sl = 0;
-        for (int s = threadIdx.x; s < n_sent; s += blockDim.x) sl += P[s] > 0 ? len[s] : 0;
+        __shared__ int red[2][32];
+        int sl = 0, spl = 0;
+        for (int s = threadIdx.x; s < n_sent; s += blockDim.x) {
+            sl += P[s] > 0 ? len[s] : 0;
+            spl += P[s] * len[s];
+        }
         sl = warp_sum(sl);
-        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = sl;
+        spl = warp_sum(spl);
+        if ((threadIdx.x & 31) == 0) {
+            red[0][threadIdx.x >> 5] = sl;
+            red[1][threadIdx.x >> 5] = spl;
+        }
         __syncthreads();
         if (threadIdx.x == 0) {
-            long long tot = 0;
-            for (int w = 0; w < (int)(blockDim.x >> 5); ++w) tot += red[w];
+            long long tot = 0, totp = 0;
+            for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+                tot += red[0][w];
+                totp += red[1][w];
+            }
             row[ST_SUML] = tot;
+            row[ST_SUMPL] = totp;
             row[ST_N] = *n_dev;
         }
     }
