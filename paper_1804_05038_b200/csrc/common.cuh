@@ -14,6 +14,7 @@
 #include <stdio.h>
 
 #include "../../include/qnmt_b200.h"
+#include "act.cuh"
 
 namespace qnmt {
 
@@ -52,23 +53,7 @@ static inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 // device math
 // ---------------------------------------------------------------------------
 
-// Tier-B transcendental helpers: evaluate in fp64, round once to f32.
-__device__ __forceinline__ float tanh_b(float x) {
-    return __double2float_rn(tanh((double)x));
-}
-
-__device__ __forceinline__ float sigmoid_b(float x) {
-    double v = (double)x;
-    double r;
-    if (v >= 0.0) {
-        r = 1.0 / (1.0 + exp(-v));
-    } else {
-        double e = exp(v);
-        r = e / (1.0 + e);
-    }
-    return __double2float_rn(r);
-}
-
+// Tier-B transcendental helpers (evaluate in fp64, round once to f32): act.cuh
 __device__ __forceinline__ bool beyond(const int32_t* n_dev, int64_t i) {
     return n_dev != nullptr && i >= (int64_t)*n_dev;
 }

@@ -139,7 +139,8 @@ struct qnmt_engine {
     void* vocab_part;        // fused vocab projection partials (vocab_topk_part_bytes(N, V))
     void* att_scratch;
     float* att_mm;           // [S][2][A] per-sentence column max / min of att_proj
-    uint32_t* qm[3];         // [QM_COUNT][S] fused quantization max-abs bits: ping-pong + external steps
+    uint32_t* ctx_max;       // [S] max |ctx| bits per sentence (attention context -> its quantization)
+    bool fq_ok = false;      // per-sentence fused op + quantize kernels fit in shared memory (fused_q.cu)
     // translate loop state
     float* st_s[2];          // [N][H] s
     float* st_sp[2];         // [N][H] s_prime
@@ -184,11 +185,6 @@ struct qnmt_engine {
 };
 
 namespace qnmt {
-
-// Slots of the fused quantization statistics of one decoder step: every
-// quantized activation's per-segment max-abs (u32 bits) is produced by the
-// kernel that writes the activation, so each quantization is one encode pass.
-enum { QM_EMB = 0, QM_S, QM_SP, QM_RH0, QM_SI, QM_CTX, QM_RH1, QM_SN, QM_RO, QM_COUNT };
 
 enum { PG_ENCODER = 0, PG_EMBED, PG_QUANT, PG_GEMM, PG_GRU, PG_ATT, PG_GEMM_VOCAB, PG_TOPK, PG_SEARCH,
        PG_GATHER, PG_MISC, PG_COUNT };
@@ -240,7 +236,7 @@ static int check_flag(qnmt_engine* e, cudaStream_t st) {
     QNMT_CUDA(cudaStreamSynchronize(st));
     if (f & QNMT_FLAG_VOCAB) { set_error("token id outside the vocabulary"); return QNMT_ERR_VOCAB; }
     if (f & QNMT_FLAG_NUMERIC) { set_error("activations contain non-finite values"); return QNMT_ERR_NUMERIC; }
-    if (f & QNMT_FLAG_INVALID) { set_error("non-finite weight"); return QNMT_ERR_INVALID_INPUT; }
+    if (f & QNMT_FLAG_INVALID) { set_error("invalid input (non-finite weight, or more than 16 hypotheses of one sentence in a step)"); return QNMT_ERR_INVALID_INPUT; }
     return QNMT_OK;
 }
 
@@ -377,8 +373,8 @@ struct StepIO {
     const int32_t* sent_col_off;   // [nseg] first column of each sentence (columns grouped by sentence)
     const int32_t* sent_ncols;     // [nseg] live columns of each sentence
     const float* att_minmax;       // [nseg][2][A] column extrema of att_proj (nullable)
-    uint32_t* qm;                  // [QM_COUNT][S] this step's max-abs bits (zeroed but for QM_S/QM_SP)
-    bool qm_ready;                 // QM_S / QM_SP already hold the maxima of s / sp (gather_rows)
+    int max_cols;                  // bound on columns per sentence (fused quantize smem)
+    bool codes_ready;              // q_s (and q_q for the previous-state query) hold this step's state codes
     bool fuse_vocab;               // skip the vocab GEMM: the caller runs cands_launch (vocab_topk.cu)
 };
 
@@ -436,22 +432,37 @@ static int stamp(qnmt_engine* e, int slot, const StepIO& io, cudaStream_t st, in
     return QNMT_OK;
 }
 
-static int gru_cell(qnmt_engine* e, const Cell& c, int64_t N, int nseg, const int32_t* seg,
-                    const int8_t* qx, const float* sx, const int8_t* qh, const float* sh,
-                    const float* h, float* h_out, uint32_t* rh_max, uint32_t* out_max, cudaStream_t st) {
-    const int64_t H = e->m->H;
+// one GRU cell (layers.py:170-181) over the step's columns; h_out's codes -> q_out / sc_out.
+// fq: gates and combine are the per-sentence fused op+quantize kernels (fused_q.cu);
+// otherwise elementwise kernels followed by the two-pass quantization.
+static int gru_cell(qnmt_engine* e, const Cell& c, const StepIO& io, const int8_t* qx, const float* sx,
+                    const int8_t* qh, const float* sh, const float* h, float* h_out, int8_t* q_out, float* sc_out,
+                    cudaStream_t st) {
+    const int64_t H = e->m->H, N = io.N;
+    const int32_t* seg = io.col_sent;
+    const int ns = io.nseg;
     prof_mark(e, PG_GEMM, st, 2.0 * N * (3 * H * c.in + 2 * H * H), 3.0 * H * c.in + 2.0 * H * H);
     TRY(gemm(c.wx, 3 * H, c.in, c.wx_s, H, qx, N, c.in, sx, seg, c.bx, e->gx, 3 * H, 0, st));
     TRY(gemm(c.uzr, 2 * H, H, c.uzr_s, H, qh, N, H, sh, seg, nullptr, e->gh, 2 * H, 0, st));
     prof_mark(e, PG_GRU, st);
-    TRY(gru_gates_launch(e->gx, 3 * H, nullptr, e->gh, 2 * H, h, H, N, H, e->z, e->rh, e->err, st, rh_max, seg));
-    prof_mark(e, PG_QUANT, st);
-    TRY(quantize_encode_launch(e->rh, N, H, H, seg, e->q_rh, H, e->sc_rh, rh_max, 1, e->err, st));
+    if (e->fq_ok) {
+        TRY(gates_q_launch(e->gx, 3 * H, e->gh, 2 * H, h, H, H, io.sent_col_off, io.sent_ncols, ns, io.max_cols,
+                           e->z, e->q_rh, e->sc_rh, e->err, st));
+    } else {
+        TRY(gru_gates_launch(e->gx, 3 * H, nullptr, e->gh, 2 * H, h, H, N, H, e->z, e->rh, e->err, st));
+        TRY(quantize_launch(e->rh, N, H, H, seg, ns, e->q_rh, H, e->sc_rh, e->seg_bits, 1, e->err, st));
+    }
     prof_mark(e, PG_GEMM, st, 2.0 * N * H * H, (double)H * H);
     TRY(gemm(c.uc, H, H, c.uc_s, H, e->q_rh, N, H, e->sc_rh, seg, nullptr, e->ghc, H, 0, st));
     prof_mark(e, PG_GRU, st);
-    TRY(gru_combine_launch(e->gx, 3 * H, nullptr, e->ghc, H, e->z, h, H, N, H, h_out, H, nullptr, 0,
-                           nullptr, e->err, st, out_max, seg));
+    if (e->fq_ok) {
+        TRY(combine_q_launch(e->gx + 2 * H, 3 * H, e->ghc, H, e->z, h, H, H, io.sent_col_off, io.sent_ncols, ns,
+                             io.max_cols, h_out, H, q_out, sc_out, e->err, st));
+    } else {
+        TRY(gru_combine_launch(e->gx, 3 * H, nullptr, e->ghc, H, e->z, h, H, N, H, h_out, H, nullptr, 0,
+                               nullptr, e->err, st));
+        TRY(quantize_launch(h_out, N, H, H, seg, ns, q_out, H, sc_out, e->seg_bits, 1, e->err, st));
+    }
     return QNMT_OK;
 }
 
@@ -461,50 +472,45 @@ static int step_core(qnmt_engine* e, const StepIO& io, cudaStream_t st) {
     const int32_t* seg = io.col_sent;
     const int ns = io.nseg;
     if (N <= 0) return QNMT_OK;
-    auto qm = [&](int slot) { return io.qm + (size_t)slot * e->S; };
-    if (!io.qm_ready) {   // standalone step: the state maxima were not produced by a gather
+    const bool fq = e->fq_ok;
+    // codes of the state (and, for the previous-state query, of s') when not produced by gather_q
+    if (!io.codes_ready) {
         prof_mark(e, PG_QUANT, st);
-        QNMT_CUDA(cudaMemsetAsync(io.qm, 0, sizeof(uint32_t) * QM_COUNT * e->S, st));
-        TRY(quantize_max_launch(io.s, N, H, H, seg, qm(QM_S), st));
-        if (m->aq == 1) TRY(quantize_max_launch(io.sp, N, H, H, seg, qm(QM_SP), st));
+        TRY(quantize_launch(io.s, N, H, H, seg, ns, e->q_s, H, e->sc_s, e->seg_bits, 1, e->err, st));
+        if (m->aq == 1) TRY(quantize_launch(io.sp, N, H, H, seg, ns, e->q_q, H, e->sc_q, e->seg_bits, 1, e->err, st));
     }
     prof_mark(e, PG_EMBED, st);
-    TRY(embed_gather_launch(m->tgt_embed, V, E, io.y, N, e->emb, E, e->err, st, qm(QM_EMB), seg));
-    prof_mark(e, PG_QUANT, st);
-    TRY(quantize_encode_launch(e->emb, N, E, E, seg, e->q_emb, E, e->sc_emb, qm(QM_EMB), 1, e->err, st));
-    TRY(quantize_encode_launch(io.s, N, H, H, seg, e->q_s, H, e->sc_s, qm(QM_S), 1, e->err, st));
-    // s' = GRU_r(emb, s)                                        (layers.py:372)
-    TRY(gru_cell(e, m->cell[2], N, ns, seg, e->q_emb, e->sc_emb, e->q_s, e->sc_s, io.s, io.s_int, qm(QM_RH0),
-                 qm(QM_SI), st));
-    // attention query (layers.py:373)
-    const float* query = (m->aq == 1) ? io.sp : io.s_int;
-    prof_mark(e, PG_QUANT, st);
-    TRY(quantize_encode_launch(query, N, H, H, seg, e->q_q, H, e->sc_q, qm(m->aq == 1 ? QM_SP : QM_SI), 1,
-                               e->err, st));
+    if (fq) {
+        TRY(embed_q_launch(m->tgt_embed, V, E, io.y, io.sent_col_off, io.sent_ncols, ns, io.max_cols, e->q_emb,
+                           e->sc_emb, e->err, st));
+    } else {
+        TRY(embed_gather_launch(m->tgt_embed, V, E, io.y, N, e->emb, E, e->err, st));
+        TRY(quantize_launch(e->emb, N, E, E, seg, ns, e->q_emb, E, e->sc_emb, e->seg_bits, 1, e->err, st));
+    }
+    // s' = GRU_r(emb, s) (layers.py:372); the query (layers.py:373) is s' or the previous s'
+    int8_t* q_si = m->aq == 1 ? e->q_si : e->q_q;
+    float* sc_si = m->aq == 1 ? e->sc_si : e->sc_q;
+    TRY(gru_cell(e, m->cell[2], io, e->q_emb, e->sc_emb, e->q_s, e->sc_s, io.s, io.s_int, q_si, sc_si, st));
     prof_mark(e, PG_GEMM, st, 2.0 * N * A * H, (double)A * H);
     TRY(gemm(m->u_att, A, H, m->u_att_s, A, e->q_q, N, H, e->sc_q, seg, nullptr, e->u, A, 0, st));
     prof_mark(e, PG_ATT, st);
     TRY(stamp(e, ST_ATT0, io, st));
+    if (fq) QNMT_CUDA(cudaMemsetAsync(e->ctx_max, 0, sizeof(uint32_t) * (size_t)ns, st));
     TRY(attention_launch(e->u, A, N, io.sent_col_off, io.sent_ncols, io.nseg, io.att_proj, io.att_minmax, io.states,
                          io.sent_row, io.sent_len, io.max_len, A, 2 * H, m->v, m->v_s, e->ctx, 2 * H,
-                         io.alpha, io.lda, e->att_scratch, e->err, st, qm(QM_CTX)));
+                         io.alpha, io.lda, e->att_scratch, e->err, st, fq ? e->ctx_max : nullptr));
     TRY(stamp(e, ST_ATT1, io, st));
     prof_mark(e, PG_QUANT, st);
-    TRY(quantize_encode_launch(e->ctx, N, 2 * H, 2 * H, seg, e->q_ctx, 2 * H, e->sc_ctx, qm(QM_CTX), 1, e->err,
-                               st));
-    // s = GRU_q(ctx, s')                                        (layers.py:375)
-    const int8_t* q_si = e->q_q;
-    const float* sc_si = e->sc_q;
-    if (m->aq == 1) {
-        TRY(quantize_encode_launch(io.s_int, N, H, H, seg, e->q_si, H, e->sc_si, qm(QM_SI), 1, e->err, st));
-        q_si = e->q_si;
-        sc_si = e->sc_si;
+    if (fq) {
+        TRY(quantize_encode_launch(e->ctx, N, 2 * H, 2 * H, seg, e->q_ctx, 2 * H, e->sc_ctx, e->ctx_max, 1, e->err,
+                                   st));
+    } else {
+        TRY(quantize_launch(e->ctx, N, 2 * H, 2 * H, seg, ns, e->q_ctx, 2 * H, e->sc_ctx, e->seg_bits, 1, e->err,
+                            st));
     }
-    TRY(gru_cell(e, m->cell[3], N, ns, seg, e->q_ctx, e->sc_ctx, q_si, sc_si, io.s_int, io.s_new, qm(QM_RH1),
-                 qm(QM_SN), st));
+    // s = GRU_q(ctx, s')                                        (layers.py:375)
+    TRY(gru_cell(e, m->cell[3], io, e->q_ctx, e->sc_ctx, q_si, sc_si, io.s_int, io.s_new, e->q_sn, e->sc_sn, st));
     // readout = tanh(((W_s s + b_r) + W_e emb) + W_c ctx)       (layers.py:255-265)
-    prof_mark(e, PG_QUANT, st);
-    TRY(quantize_encode_launch(io.s_new, N, H, H, seg, e->q_sn, H, e->sc_sn, qm(QM_SN), 1, e->err, st));
     prof_mark(e, PG_GEMM, st, 2.0 * N * R * (H + E + 2 * H), (double)R * (H + E + 2 * H));
     TRY(gemm(m->w_state, R, H, m->w_state_s, R, e->q_sn, N, H, e->sc_sn, seg, m->b_r, e->ro, R, 0, st));
     TRY(gemm(m->w_embed, R, E, m->w_embed_s, R, e->q_emb, N, E, e->sc_emb, seg, nullptr, e->ro, R,
@@ -512,9 +518,13 @@ static int step_core(qnmt_engine* e, const StepIO& io, cudaStream_t st) {
     TRY(gemm(m->w_ctx, R, 2 * H, m->w_ctx_s, R, e->q_ctx, N, 2 * H, e->sc_ctx, seg, nullptr, e->ro, R,
              QNMT_GEMM_ACCUMULATE, st));
     prof_mark(e, PG_MISC, st);
-    TRY(tanh_launch(e->ro, N, R, R, e->ro, R, e->err, st, qm(QM_RO), seg));
-    prof_mark(e, PG_QUANT, st);
-    TRY(quantize_encode_launch(e->ro, N, R, R, seg, e->q_ro, R, e->sc_ro, qm(QM_RO), 1, e->err, st));
+    if (fq) {
+        TRY(tanh_q_launch(e->ro, R, R, io.sent_col_off, io.sent_ncols, ns, io.max_cols, e->q_ro, e->sc_ro, e->err,
+                          st));
+    } else {
+        TRY(tanh_launch(e->ro, N, R, R, e->ro, R, e->err, st));
+        TRY(quantize_launch(e->ro, N, R, R, seg, ns, e->q_ro, R, e->sc_ro, e->seg_bits, 1, e->err, st));
+    }
     if (io.fuse_vocab) return QNMT_OK;
     prof_mark(e, PG_GEMM_VOCAB, st, 2.0 * N * V * R, (double)V * R + (double)N * R + 4.0 * N * V);
     TRY(stamp(e, ST_VOC0, io, st));
@@ -522,6 +532,17 @@ static int step_core(qnmt_engine* e, const StepIO& io, cudaStream_t st) {
              0, st));
     TRY(stamp(e, ST_VOC1, io, st));
     return QNMT_OK;
+}
+
+// next-step state columns by parent (decoder.py:131-140) and, with fq, their codes
+static int gather_next(qnmt_engine* e, int cur, int64_t N2, int n, int beam, cudaStream_t st) {
+    const qnmt_model* m = e->m;
+    const int64_t H = m->H;
+    if (e->fq_ok)
+        return gather_q_launch(e->s_new, m->aq == 1 ? e->s_int : nullptr, e->parent_col, H, e->col_off, e->P, n,
+                               beam, e->st_s[cur ^ 1], e->st_sp[cur ^ 1], e->q_s, e->sc_s,
+                               m->aq == 1 ? e->q_q : nullptr, m->aq == 1 ? e->sc_q : nullptr, e->err, st);
+    return gather_rows_launch(e->s_new, e->s_int, e->parent_col, N2, H, e->st_s[cur ^ 1], e->st_sp[cur ^ 1], st);
 }
 
 static bool vocab_fusable(const qnmt_engine* e, int k) {
@@ -702,7 +723,7 @@ int qnmt_engine_create(const qnmt_model* m, int32_t max_sentences, int32_t max_s
         e->vocab_part = a.take<char>(vocab_topk_part_bytes((int64_t)N, (int64_t)V));
         e->att_scratch = a.take<char>(N * (L + 2) * 4 + 2 * S * A * 4 + 1024);
         e->att_mm = a.take<float>(2 * S * A);
-        for (int i = 0; i < 3; ++i) e->qm[i] = a.take<uint32_t>(qnmt::QM_COUNT * S);
+        e->ctx_max = a.take<uint32_t>(S);
         for (int i = 0; i < 2; ++i) {
             e->st_s[i] = a.take<float>(N * H);
             e->st_sp[i] = a.take<float>(N * H);
@@ -741,6 +762,11 @@ int qnmt_engine_create(const qnmt_model* m, int32_t max_sentences, int32_t max_s
     cudaMemcpy(e->even, ev.data(), S * 4, cudaMemcpyHostToDevice);
     cudaMemcpy(e->odd, od.data(), S * 4, cudaMemcpyHostToDevice);
     cudaMemset(e->err, 0, 16);
+    {   // per-sentence fused op + quantize: [16 columns][max(E, H, R)] values, gather [2][B][H]
+        const size_t d = std::max(E, std::max(H, R));
+        e->fq_ok = 16 * d * 4 <= FQ_SMEM_MAX && 2 * B * H * 4 <= FQ_SMEM_MAX && E % 4 == 0 && H % 4 == 0 &&
+                   R % 4 == 0 && ((uintptr_t)m->tgt_embed % 16) == 0;   // float4 groups (fused_q.cu)
+    }
     cudaStreamCreateWithFlags(&e->cap_stream, cudaStreamNonBlocking);
     cudaError_t ce = cudaMallocHost(&e->h_pinned, 64);
     if (ce != cudaSuccess) { cudaFree(e->block); delete e; return cuda_status(ce, "cudaMallocHost"); }
@@ -831,7 +857,7 @@ int qnmt_decoder_step(qnmt_engine* e, int64_t N, const int32_t* col_sent, int32_
     QNMT_CUDA(cudaMemsetAsync(e->err, 0, 4, st));
     TRY(col_ranges_launch(col_sent, N, n_sent, e->rng_off, e->rng_cnt, st));
     StepIO io{N, n_sent, col_sent, y, s, sp, states, att_proj, sent_row, sent_len, max_len,
-              s_int, s_new, logits, alpha, lda, e->rng_off, e->rng_cnt, nullptr, e->qm[2], false, false};
+              s_int, s_new, logits, alpha, lda, e->rng_off, e->rng_cnt, nullptr, 16, false, false};
     TRY(step_core(e, io, st));
     return check_flag(e, st);
 }
@@ -859,7 +885,7 @@ static int capture_step(qnmt_engine* e, int cur, int n, int beam, int k_list, cu
         NdevScope nd(e->d_N + cur);
         StepIO io{NM, n, e->col_sent[cur], e->y[cur], e->st_s[cur], e->st_sp[cur], e->enc_states, e->enc_att,
                   e->sent_row, e->sent_len, e->L, e->s_int, e->s_new, e->logits, nullptr, 0,
-                  e->col_off, e->P, e->att_mm, e->qm[cur], true, vocab_fusable(e, k_list)};
+                  e->col_off, e->P, e->att_mm, beam, e->fq_ok, vocab_fusable(e, k_list)};
         rc = stamp(e, ST_STEP0, io, cs);
         if (rc == QNMT_OK) rc = step_core(e, io, cs);
         if (rc == QNMT_OK) rc = cands_launch(e, io, e->live[cur], k_list, cs);
@@ -874,11 +900,7 @@ static int capture_step(qnmt_engine* e, int cur, int n, int beam, int k_list, cu
     }
     if (rc == QNMT_OK) {
         NdevScope nd(e->d_N + (cur ^ 1));
-        uint32_t* qn = e->qm[cur ^ 1];
-        if (cudaMemsetAsync(qn, 0, sizeof(uint32_t) * QM_COUNT * e->S, cs) != cudaSuccess) rc = QNMT_ERR_CUDA;
-        if (rc == QNMT_OK)
-            rc = gather_rows_launch(e->s_new, e->s_int, e->parent_col, NM, H, e->st_s[cur ^ 1], e->st_sp[cur ^ 1],
-                                    cs, qn + (size_t)QM_S * e->S, qn + (size_t)QM_SP * e->S, e->col_sent[cur ^ 1]);
+        rc = gather_next(e, cur, NM, n, beam, cs);
     }
     cudaGraph_t g = nullptr;
     cudaError_t ce = cudaStreamEndCapture(cs, &g);
@@ -978,10 +1000,11 @@ static int decode_core(qnmt_engine* e, const int32_t* src_ids, bool ids_on_devic
     QNMT_CUDA(cudaMemsetAsync(e->steps_run, 0, (size_t)n * 4, st));
     QNMT_CUDA(cudaMemcpyAsync(e->st_s[0], e->enc_s0, (size_t)n * H * 4, cudaMemcpyDeviceToDevice, st));
     QNMT_CUDA(cudaMemcpyAsync(e->st_sp[0], e->enc_s0, (size_t)n * H * 4, cudaMemcpyDeviceToDevice, st));
-    // first step's state maxima (later steps get them from gather_rows); column n = sentence n
-    QNMT_CUDA(cudaMemsetAsync(e->qm[0], 0, sizeof(uint32_t) * QM_COUNT * e->S, st));
-    TRY(quantize_max_launch(e->enc_s0, n, H, H, e->iota, e->qm[0] + (size_t)QM_S * e->S, st));
-    TRY(quantize_max_launch(e->enc_s0, n, H, H, e->iota, e->qm[0] + (size_t)QM_SP * e->S, st));
+    if (e->fq_ok) {   // first step's state codes (later steps get them from gather_q); column n = sentence n
+        TRY(quantize_launch(e->enc_s0, n, H, H, e->iota, n, e->q_s, H, e->sc_s, e->seg_bits, 1, e->err, st));
+        if (m->aq == 1)
+            TRY(quantize_launch(e->enc_s0, n, H, H, e->iota, n, e->q_q, H, e->sc_q, e->seg_bits, 1, e->err, st));
+    }
     const int k_list = (int)std::min<int64_t>(beam, V);
     if (graph_eligible(e)) {
         // device-resident loop: one graph launch per step, live count polled every POLL steps
@@ -1007,7 +1030,7 @@ static int decode_core(qnmt_engine* e, const int32_t* src_ids, bool ids_on_devic
     for (int t = 0; t < Tmax && N > 0; ++t) {
         StepIO io{N, n, e->col_sent[cur], e->y[cur], e->st_s[cur], e->st_sp[cur], e->enc_states,
                   e->enc_att, e->sent_row, e->sent_len, Lmax, e->s_int, e->s_new, e->logits, nullptr, 0,
-                  e->col_off, e->P, e->att_mm, e->qm[cur], true, vocab_fusable(e, k_list)};
+                  e->col_off, e->P, e->att_mm, beam, e->fq_ok, vocab_fusable(e, k_list)};
         TRY(step_core(e, io, st));
         TRY(cands_launch(e, io, e->live[cur], k_list, st));
         prof_mark(e, PG_SEARCH, st);
@@ -1022,10 +1045,7 @@ static int decode_core(qnmt_engine* e, const int32_t* src_ids, bool ids_on_devic
         prof_collect(e);
         int64_t N2 = e->h_pinned[0];
         prof_mark(e, PG_GATHER, st);
-        uint32_t* qn = e->qm[cur ^ 1];
-        QNMT_CUDA(cudaMemsetAsync(qn, 0, sizeof(uint32_t) * QM_COUNT * e->S, st));
-        TRY(gather_rows_launch(e->s_new, e->s_int, e->parent_col, N2, H, e->st_s[cur ^ 1], e->st_sp[cur ^ 1], st,
-                               qn + (size_t)QM_S * e->S, qn + (size_t)QM_SP * e->S, e->col_sent[cur ^ 1]));
+        TRY(gather_next(e, cur, N2, n, beam, st));
         N = N2;
         cur ^= 1;
     }

@@ -1,0 +1,297 @@
+// fused_q.cu -- decoder elementwise ops fused with the quantization of their
+// output, one CTA per quantization segment.
+//
+// In the batched decoder a quantization segment is one sentence: the columns
+// [off[s], off[s] + cnt[s]) of all its live hypotheses (LinearOp.apply on the
+// sentence's [features, P] block, layers.py:118-146).  A CTA that owns the whole
+// segment can compute the op, reduce max|v| (qmath.py:157-169), derive the scale
+// (qmath.py:136-142) and write the int8 codes (qmath.py:119-133) in one launch,
+// instead of op + max-abs pass + encode pass.  Values wait in shared memory
+// ([cnt][D] f32) between the reduction and the encode.
+//
+//   k_gates_q    z, q(r*h)        GRU first phase      (layers.py:170-176)
+//   k_combine_q  h', q(h')        GRU second phase     (layers.py:177-181)
+//   k_embed_q    q(E[y])          target embedding     (layers.py:367)
+//   k_tanh_q     q(tanh(x))       readout activation   (layers.py:265)
+//   k_gather_q   s, s', q(s), q(s') next-step states by parent column (decoder.py:131-140)
+#include "kernels.cuh"
+
+namespace qnmt {
+
+constexpr int FQ_T = 1024;   // threads per segment CTA (the fp64 sigmoid/tanh work needs the occupancy)
+
+// block max of |v| bits -> scale of the segment (non-finite: flag, scale 1 as k_encode)
+__device__ __forceinline__ float seg_scale(uint32_t m, uint32_t* red, int32_t* err_flag, float* sc_out) {
+    m = warp_max(m);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+    __syncthreads();
+    uint32_t mm = 0;
+#pragma unroll
+    for (int w = 0; w < FQ_T / 32; ++w) mm = max(mm, red[w]);
+    if (mm >= 0x7f800000u) {
+        if (threadIdx.x == 0) set_flag(err_flag, QNMT_FLAG_NUMERIC);
+        mm = 0;
+    }
+    const float sc = scale_from_maxbits(mm);
+    if (threadIdx.x == 0 && sc_out) *sc_out = sc;
+    return sc;
+}
+
+__device__ __forceinline__ uint32_t absbits(float v) { return __float_as_uint(v) & 0x7fffffffu; }
+
+// Elements are processed in groups of 4 consecutive features of one column
+// (D % 4 == 0 and 16-byte aligned rows, checked by the engine): group g of the
+// flattened [P][D] segment is column (4g) / D, features 4g % D .. +3.
+__device__ __forceinline__ void seg_encode(const float* vals, int P, int64_t D, int c0, float sc, int8_t* q,
+                                           int64_t ldq) {
+    const int64_t G = (int64_t)P * D / 4;
+#pragma unroll 4
+    for (int64_t g = threadIdx.x; g < G; g += FQ_T) {
+        const int64_t c = (4 * g) / D, j = 4 * g - c * D;
+        const float4 v = *reinterpret_cast<const float4*>(vals + 4 * g);
+        const uint32_t packed = (uint32_t)(quant_code(v.x, sc) & 0xff) | ((uint32_t)(quant_code(v.y, sc) & 0xff) << 8) |
+                                ((uint32_t)(quant_code(v.z, sc) & 0xff) << 16) |
+                                ((uint32_t)(quant_code(v.w, sc) & 0xff) << 24);
+        *reinterpret_cast<uint32_t*>(q + (int64_t)(c0 + c) * ldq + j) = packed;
+    }
+}
+
+__device__ __forceinline__ float4 ld4(const float* p) { return *reinterpret_cast<const float4*>(p); }
+__device__ __forceinline__ void st4(float* p, float4 v) { *reinterpret_cast<float4*>(p) = v; }
+__device__ __forceinline__ uint32_t max4(uint32_t m, float4 v) {
+    return max(max(m, max(absbits(v.x), absbits(v.y))), max(absbits(v.z), absbits(v.w)));
+}
+__device__ __forceinline__ bool fin4(float4 v) {
+    return is_finite_f(v.x) && is_finite_f(v.y) && is_finite_f(v.z) && is_finite_f(v.w);
+}
+
+#define FQ_SEG_PROLOGUE                                                  \
+    extern __shared__ float vals[];                                      \
+    __shared__ uint32_t red[FQ_T / 32];                                  \
+    const int s = blockIdx.x;                                            \
+    const int P = cnt[s];                                                \
+    if (P == 0) return;                                                  \
+    if (P > max_cols) { /* more columns than smem was sized for */       \
+        if (threadIdx.x == 0) set_flag(err_flag, QNMT_FLAG_INVALID);     \
+        return;                                                          \
+    }                                                                    \
+    const int c0 = off[s];
+
+__global__ void __launch_bounds__(FQ_T)
+k_gates_q(const float* __restrict__ gx, int64_t ldgx, const float* __restrict__ gh, int64_t ldgh,
+          const float* __restrict__ h, int64_t ldh, int64_t H, const int32_t* __restrict__ off,
+          const int32_t* __restrict__ cnt, float* __restrict__ z, int8_t* __restrict__ q_rh, float* sc_rh,
+          int32_t* err_flag, int max_cols) {
+    FQ_SEG_PROLOGUE
+    uint32_t m = 0;
+    bool bad = false;
+    const int64_t G = (int64_t)P * H / 4;
+#pragma unroll 2
+    for (int64_t g = threadIdx.x; g < G; g += FQ_T) {
+        const int64_t c = (4 * g) / H, j = 4 * g - c * H, n = c0 + c;
+        const float4 xz = ld4(gx + n * ldgx + j), xr = ld4(gx + n * ldgx + H + j);
+        const float4 hz = ld4(gh + n * ldgh + j), hr = ld4(gh + n * ldgh + H + j);
+        const float4 hh = ld4(h + n * ldh + j);
+        const float4 pz = make_float4(__fadd_rn(xz.x, hz.x), __fadd_rn(xz.y, hz.y), __fadd_rn(xz.z, hz.z),
+                                      __fadd_rn(xz.w, hz.w));
+        const float4 pr = make_float4(__fadd_rn(xr.x, hr.x), __fadd_rn(xr.y, hr.y), __fadd_rn(xr.z, hr.z),
+                                      __fadd_rn(xr.w, hr.w));
+        bad |= !fin4(pz) || !fin4(pr);
+        st4(z + n * H + j, make_float4(sigmoid_b(pz.x), sigmoid_b(pz.y), sigmoid_b(pz.z), sigmoid_b(pz.w)));
+        const float4 v = make_float4(__fmul_rn(sigmoid_b(pr.x), hh.x), __fmul_rn(sigmoid_b(pr.y), hh.y),
+                                     __fmul_rn(sigmoid_b(pr.z), hh.z), __fmul_rn(sigmoid_b(pr.w), hh.w));
+        st4(vals + 4 * g, v);
+        m = max4(m, v);
+    }
+    if (bad) set_flag(err_flag, QNMT_FLAG_NUMERIC);
+    const float sc = seg_scale(m, red, err_flag, sc_rh + s);
+    seg_encode(vals, P, H, c0, sc, q_rh, H);
+}
+
+__global__ void __launch_bounds__(FQ_T)
+k_combine_q(const float* __restrict__ gxc, int64_t ldgx, const float* __restrict__ ghc, int64_t ldghc,
+            const float* __restrict__ z, const float* __restrict__ h, int64_t ldh, int64_t H,
+            const int32_t* __restrict__ off, const int32_t* __restrict__ cnt, float* __restrict__ h_out,
+            int64_t ldo, int8_t* __restrict__ q_out, float* sc_out, int32_t* err_flag, int max_cols) {
+    FQ_SEG_PROLOGUE
+    uint32_t m = 0;
+    bool bad = false;
+    const int64_t G = (int64_t)P * H / 4;
+#pragma unroll 2
+    for (int64_t g = threadIdx.x; g < G; g += FQ_T) {
+        const int64_t c = (4 * g) / H, j = 4 * g - c * H, n = c0 + c;
+        const float4 xc = ld4(gxc + n * ldgx + j), hc = ld4(ghc + n * ldghc + j);
+        const float4 zz = ld4(z + n * H + j), hh = ld4(h + n * ldh + j);
+        const float4 pc = make_float4(__fadd_rn(xc.x, hc.x), __fadd_rn(xc.y, hc.y), __fadd_rn(xc.z, hc.z),
+                                      __fadd_rn(xc.w, hc.w));
+        bad |= !fin4(pc);
+        float4 v;
+        v.x = __fadd_rn(__fmul_rn(__fsub_rn(1.0f, zz.x), hh.x), __fmul_rn(zz.x, tanh_b(pc.x)));
+        v.y = __fadd_rn(__fmul_rn(__fsub_rn(1.0f, zz.y), hh.y), __fmul_rn(zz.y, tanh_b(pc.y)));
+        v.z = __fadd_rn(__fmul_rn(__fsub_rn(1.0f, zz.z), hh.z), __fmul_rn(zz.z, tanh_b(pc.z)));
+        v.w = __fadd_rn(__fmul_rn(__fsub_rn(1.0f, zz.w), hh.w), __fmul_rn(zz.w, tanh_b(pc.w)));
+        st4(h_out + n * ldo + j, v);
+        st4(vals + 4 * g, v);
+        m = max4(m, v);
+    }
+    if (bad) set_flag(err_flag, QNMT_FLAG_NUMERIC);
+    const float sc = seg_scale(m, red, err_flag, sc_out + s);
+    seg_encode(vals, P, H, c0, sc, q_out, H);
+}
+
+__global__ void __launch_bounds__(FQ_T)
+k_embed_q(const float* __restrict__ table, int64_t rows, int64_t E, const int32_t* __restrict__ ids,
+          const int32_t* __restrict__ off, const int32_t* __restrict__ cnt, int8_t* __restrict__ q_out,
+          float* sc_out, int32_t* err_flag, int max_cols) {
+    FQ_SEG_PROLOGUE
+    uint32_t m = 0;
+    const int64_t G = (int64_t)P * E / 4;
+#pragma unroll 2
+    for (int64_t g = threadIdx.x; g < G; g += FQ_T) {
+        const int64_t c = (4 * g) / E, j = 4 * g - c * E;
+        const int32_t id = ids[c0 + c];
+        const bool ok = id >= 0 && id < rows;
+        if (!ok && j == 0) set_flag(err_flag, QNMT_FLAG_VOCAB);
+        const float4 v = ok ? ld4(table + (int64_t)id * E + j) : make_float4(0.f, 0.f, 0.f, 0.f);
+        st4(vals + 4 * g, v);
+        m = max4(m, v);
+    }
+    const float sc = seg_scale(m, red, err_flag, sc_out + s);
+    seg_encode(vals, P, E, c0, sc, q_out, E);
+}
+
+__global__ void __launch_bounds__(FQ_T)
+k_tanh_q(const float* __restrict__ x, int64_t ldx, int64_t D, const int32_t* __restrict__ off,
+         const int32_t* __restrict__ cnt, int8_t* __restrict__ q_out, float* sc_out, int32_t* err_flag,
+         int max_cols) {
+    FQ_SEG_PROLOGUE
+    uint32_t m = 0;
+    bool bad = false;
+    const int64_t G = (int64_t)P * D / 4;
+#pragma unroll 2
+    for (int64_t g = threadIdx.x; g < G; g += FQ_T) {
+        const int64_t c = (4 * g) / D, j = 4 * g - c * D;
+        const float4 xv = ld4(x + (int64_t)(c0 + c) * ldx + j);
+        bad |= !fin4(xv);
+        const float4 v = make_float4(tanh_b(xv.x), tanh_b(xv.y), tanh_b(xv.z), tanh_b(xv.w));
+        st4(vals + 4 * g, v);
+        m = max4(m, v);
+    }
+    if (bad) set_flag(err_flag, QNMT_FLAG_NUMERIC);
+    const float sc = seg_scale(m, red, err_flag, sc_out + s);
+    seg_encode(vals, P, D, c0, sc, q_out, D);
+}
+
+// a_out[n] = a[parent[n]] (+ codes qa); optionally the same for b (second state)
+__global__ void __launch_bounds__(FQ_T)
+k_gather_q(const float* __restrict__ a, const float* __restrict__ b, const int32_t* __restrict__ parent,
+           int64_t H, const int32_t* __restrict__ off, const int32_t* __restrict__ cnt, float* __restrict__ a_out,
+           float* __restrict__ b_out, int8_t* __restrict__ qa, float* sca, int8_t* __restrict__ qb, float* scb,
+           int32_t* err_flag, int max_cols) {
+    FQ_SEG_PROLOGUE
+    float* va = vals;                    // [P][H]
+    float* vb = vals + (int64_t)P * H;   // [P][H]
+    uint32_t ma = 0, mb = 0;
+    const int64_t G = (int64_t)P * H / 4;
+#pragma unroll 2
+    for (int64_t g = threadIdx.x; g < G; g += FQ_T) {
+        const int64_t c = (4 * g) / H, j = 4 * g - c * H, n = c0 + c;
+        const int64_t p = parent[n];
+        const float4 xa = ld4(a + p * H + j);
+        st4(a_out + n * H + j, xa);
+        st4(va + 4 * g, xa);
+        ma = max4(ma, xa);
+        if (b) {
+            const float4 xb = ld4(b + p * H + j);
+            st4(b_out + n * H + j, xb);
+            st4(vb + 4 * g, xb);
+            mb = max4(mb, xb);
+        }
+    }
+    const float sa = seg_scale(ma, red, err_flag, sca + s);
+    seg_encode(va, P, H, c0, sa, qa, H);
+    if (qb) {
+        __syncthreads();   // red reused
+        const float sb = seg_scale(mb, red, err_flag, scb + s);
+        seg_encode(vb, P, H, c0, sb, qb, H);
+    }
+}
+
+static int set_smem(const void* fn, size_t bytes, size_t& done) {
+    if (bytes > FQ_SMEM_MAX) {
+        set_error("fused quantize: %zu bytes of segment values exceed shared memory", bytes);
+        return QNMT_ERR_CONFIG;
+    }
+    if (bytes > 48 * 1024 && bytes > done) {
+        QNMT_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+        done = bytes;
+    }
+    return QNMT_OK;
+}
+
+#define FQ_TRY(x) do { int _r = (x); if (_r != QNMT_OK) return _r; } while (0)
+
+int gates_q_launch(const float* gx, int64_t ldgx, const float* gh, int64_t ldgh, const float* h, int64_t ldh,
+                   int64_t H, const int32_t* off, const int32_t* cnt, int n_seg, int max_cols, float* z,
+                   int8_t* q_rh, float* sc_rh, int32_t* err_flag, cudaStream_t st) {
+    if (n_seg <= 0) return QNMT_OK;
+    const size_t smem = (size_t)max_cols * H * sizeof(float);
+    static size_t done = 0;
+    FQ_TRY(set_smem((const void*)k_gates_q, smem, done));
+    k_gates_q<<<(unsigned)n_seg, FQ_T, smem, st>>>(gx, ldgx, gh, ldgh, h, ldh, H, off, cnt, z, q_rh, sc_rh,
+                                                    err_flag, max_cols);
+    QNMT_CHECK_LAUNCH("k_gates_q");
+    return QNMT_OK;
+}
+
+int combine_q_launch(const float* gxc, int64_t ldgx, const float* ghc, int64_t ldghc, const float* z,
+                     const float* h, int64_t ldh, int64_t H, const int32_t* off, const int32_t* cnt, int n_seg,
+                     int max_cols, float* h_out, int64_t ldo, int8_t* q_out, float* sc_out, int32_t* err_flag,
+                     cudaStream_t st) {
+    if (n_seg <= 0) return QNMT_OK;
+    const size_t smem = (size_t)max_cols * H * sizeof(float);
+    static size_t done = 0;
+    FQ_TRY(set_smem((const void*)k_combine_q, smem, done));
+    k_combine_q<<<(unsigned)n_seg, FQ_T, smem, st>>>(gxc, ldgx, ghc, ldghc, z, h, ldh, H, off, cnt, h_out, ldo,
+                                                      q_out, sc_out, err_flag, max_cols);
+    QNMT_CHECK_LAUNCH("k_combine_q");
+    return QNMT_OK;
+}
+
+int embed_q_launch(const float* table, int64_t rows, int64_t E, const int32_t* ids, const int32_t* off,
+                   const int32_t* cnt, int n_seg, int max_cols, int8_t* q_out, float* sc_out, int32_t* err_flag,
+                   cudaStream_t st) {
+    if (n_seg <= 0) return QNMT_OK;
+    const size_t smem = (size_t)max_cols * E * sizeof(float);
+    static size_t done = 0;
+    FQ_TRY(set_smem((const void*)k_embed_q, smem, done));
+    k_embed_q<<<(unsigned)n_seg, FQ_T, smem, st>>>(table, rows, E, ids, off, cnt, q_out, sc_out, err_flag, max_cols);
+    QNMT_CHECK_LAUNCH("k_embed_q");
+    return QNMT_OK;
+}
+
+int tanh_q_launch(const float* x, int64_t ldx, int64_t D, const int32_t* off, const int32_t* cnt, int n_seg,
+                  int max_cols, int8_t* q_out, float* sc_out, int32_t* err_flag, cudaStream_t st) {
+    if (n_seg <= 0) return QNMT_OK;
+    const size_t smem = (size_t)max_cols * D * sizeof(float);
+    static size_t done = 0;
+    FQ_TRY(set_smem((const void*)k_tanh_q, smem, done));
+    k_tanh_q<<<(unsigned)n_seg, FQ_T, smem, st>>>(x, ldx, D, off, cnt, q_out, sc_out, err_flag, max_cols);
+    QNMT_CHECK_LAUNCH("k_tanh_q");
+    return QNMT_OK;
+}
+
+int gather_q_launch(const float* a, const float* b, const int32_t* parent, int64_t H, const int32_t* off,
+                    const int32_t* cnt, int n_seg, int max_cols, float* a_out, float* b_out, int8_t* qa,
+                    float* sca, int8_t* qb, float* scb, int32_t* err_flag, cudaStream_t st) {
+    if (n_seg <= 0) return QNMT_OK;
+    const size_t smem = (size_t)2 * max_cols * H * sizeof(float);
+    static size_t done = 0;
+    FQ_TRY(set_smem((const void*)k_gather_q, smem, done));
+    k_gather_q<<<(unsigned)n_seg, FQ_T, smem, st>>>(a, b, parent, H, off, cnt, a_out, b_out, qa, sca, qb, scb,
+                                                     err_flag, max_cols);
+    QNMT_CHECK_LAUNCH("k_gather_q");
+    return QNMT_OK;
+}
+
+}  // namespace qnmt

@@ -65,4 +65,23 @@ size_t vocab_topk_part_bytes(int64_t rows, int64_t V);
 int vocab_stats_launch(const VocabTopk& p, cudaStream_t st);
 int vocab_merge_launch(const VocabTopk& p, cudaStream_t st);
 
+// decoder elementwise ops fused with the quantization of their output, one CTA per
+// sentence segment [off[s], off[s] + cnt[s]) (fused_q.cu); max_cols bounds cnt[s]
+constexpr size_t FQ_SMEM_MAX = 227 * 1024;
+int gates_q_launch(const float* gx, int64_t ldgx, const float* gh, int64_t ldgh, const float* h, int64_t ldh,
+                   int64_t H, const int32_t* off, const int32_t* cnt, int n_seg, int max_cols, float* z,
+                   int8_t* q_rh, float* sc_rh, int32_t* err_flag, cudaStream_t st);
+int combine_q_launch(const float* gxc, int64_t ldgx, const float* ghc, int64_t ldghc, const float* z,
+                     const float* h, int64_t ldh, int64_t H, const int32_t* off, const int32_t* cnt, int n_seg,
+                     int max_cols, float* h_out, int64_t ldo, int8_t* q_out, float* sc_out, int32_t* err_flag,
+                     cudaStream_t st);
+int embed_q_launch(const float* table, int64_t rows, int64_t E, const int32_t* ids, const int32_t* off,
+                   const int32_t* cnt, int n_seg, int max_cols, int8_t* q_out, float* sc_out, int32_t* err_flag,
+                   cudaStream_t st);
+int tanh_q_launch(const float* x, int64_t ldx, int64_t D, const int32_t* off, const int32_t* cnt, int n_seg,
+                  int max_cols, int8_t* q_out, float* sc_out, int32_t* err_flag, cudaStream_t st);
+int gather_q_launch(const float* a, const float* b, const int32_t* parent, int64_t H, const int32_t* off,
+                    const int32_t* cnt, int n_seg, int max_cols, float* a_out, float* b_out, int8_t* qa,
+                    float* sca, int8_t* qb, float* scb, int32_t* err_flag, cudaStream_t st);
+
 }  // namespace qnmt
