@@ -49,13 +49,15 @@ __device__ __forceinline__ float rcp_approx(float x) {
 }
 
 // Fast-path rounding window.  v_fast = fl(st - 2 st r) (one FFMA rounding,
-// <= 3.9e-6 at |v| <= 128) differs from the reference's v = fl(fl32(tanh x) * st)
-// by at most st * (2.37e-7 + 3e-8) + 7.7e-6; the window below has >= 1.5x
-// margin on both terms.  Where fl(v + 1.5*2^23) - 1.5*2^23 (round-to-nearest-even,
-// exact) is farther than the window from a half-integer, the reference's
-// floor(|v| + 1/2) (qmath.py:136-142) gives the same integer; otherwise the
-// element is recomputed with the fp64-exact tanh (att_code_exact).
-__device__ __forceinline__ float att_threshold(float st) { return 0.5f - (st * 4e-7f + 1.6e-5f); }
+// <= 3.8e-6 at |v| <= 128) differs from the reference's v = fl(fl32(tanh x) * st)
+// by at most st * (2.37e-7 + 3e-8) + 7.6e-6 (2.37e-7: exhaustive max of
+// |t_fast - tanh| over every f32 x, profiles/r01_tanh_err.jsonl); the window
+// below is that bound plus ~9% / ~18% margin.  Where fl(v + 1.5*2^23) - 1.5*2^23
+// (round-to-nearest-even, exact) is farther than the window from a
+// half-integer, the reference's floor(|v| + 1/2) (qmath.py:136-142) gives the
+// same integer; otherwise the element is recomputed with the fp64 tanh
+// (att_code_exact).
+__device__ __forceinline__ float att_threshold(float st) { return 0.5f - (st * 2.9e-7f + 9e-6f); }
 constexpr float ATT_ST_FAST_MAX = 1.0e6f;   // above: window > 0.5, every element exact
 
 __device__ __noinline__ int att_code_exact(float x, float st) { return quant_code(tanh_b(x), st); }
@@ -242,6 +244,161 @@ k_att_score4(const float* __restrict__ u, int64_t ldu, const int32_t* __restrict
     }
 }
 
+// Same scores with each thread's slice of the att_proj tile parked in shared
+// memory (APC5 positions x its a-quads; a thread only ever reads its own slots,
+// so no barrier), registers holding just the query slice, codes and
+// accumulators: 3 CTAs / SM instead of 2 to hide the MUFU / FMA latency.  Thread
+// t owns a-quads 4t + 4*AT*k; quads past A are zero (no bounds checks in the
+// hot loop).  Warps add their per-position sums into shared memory and the last
+// warp to finish writes the scores (no end-of-CTA barrier wait).
+constexpr int APC5 = 8;        // positions per CTA
+constexpr int AQ5 = 2;         // a-quads per thread (A <= 4 * AT * AQ5 = 2048)
+
+__global__ void __launch_bounds__(AT, 3)
+k_att_score5(const float* __restrict__ u, int64_t ldu, const int32_t* __restrict__ sent_col_off,
+             const int32_t* __restrict__ sent_ncols, const float* __restrict__ att_proj,
+             const float2* __restrict__ st_thr, const int64_t* __restrict__ sent_row,
+             const int32_t* __restrict__ sent_len, int64_t A, const int8_t* __restrict__ v_codes,
+             const float* __restrict__ v_scale, float* __restrict__ scores, int32_t max_len) {
+    extern __shared__ float4 sap[];   // [APC5][AQ5][AT]
+    __shared__ int sums[AMAXP][APC5];
+    __shared__ int s_done;
+    const int s = blockIdx.y;
+    const int P = sent_ncols[s];
+    const int l = sent_len[s];
+    const int i0 = blockIdx.x * APC5;
+    if (P == 0 || i0 >= l) return;
+    const int i1 = min(l, i0 + APC5);
+    const int np = i1 - i0;
+    const int c0 = sent_col_off[s];
+    const int lane = threadIdx.x & 31;
+    const int64_t A4 = A / 4;
+    if (threadIdx.x < AMAXP * APC5) (&sums[0][0])[threadIdx.x] = 0;
+    if (threadIdx.x == 0) s_done = 0;
+    {   // this thread's slots of the tile (positions past i1 and quads past A are zero)
+        const float4* src = reinterpret_cast<const float4*>(att_proj + (sent_row[s] + i0) * A);
+#pragma unroll
+        for (int p = 0; p < APC5; ++p)
+#pragma unroll
+            for (int k = 0; k < AQ5; ++k) {
+                const int64_t q = threadIdx.x + (int64_t)AT * k;
+                sap[(p * AQ5 + k) * AT + threadIdx.x] =
+                    (p < np && q < A4) ? src[p * A4 + q] : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+    }
+    int vv[AQ5][4];
+    float4 uq[AQ5], ux[AQ5];
+#pragma unroll
+    for (int k = 0; k < AQ5; ++k) {
+        const int64_t q = threadIdx.x + (int64_t)AT * k;
+        const bool ok = q < A4;
+        const char4 c = ok ? reinterpret_cast<const char4*>(v_codes)[q] : make_char4(0, 0, 0, 0);
+        vv[k][0] = c.x; vv[k][1] = c.y; vv[k][2] = c.z; vv[k][3] = c.w;
+        uq[k] = ok ? reinterpret_cast<const float4*>(u + (int64_t)c0 * ldu)[q] : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    float2 sp = st_thr[c0];
+    __syncthreads();   // sums / s_done initialised
+    for (int j = 0; j < P; ++j) {
+        float2 spx = sp;
+        if (j + 1 < P) {   // prefetch the next hypothesis' query slice and scale
+#pragma unroll
+            for (int k = 0; k < AQ5; ++k) {
+                const int64_t q = threadIdx.x + (int64_t)AT * k;
+                ux[k] = q < A4 ? reinterpret_cast<const float4*>(u + (int64_t)(c0 + j + 1) * ldu)[q]
+                               : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+            spx = st_thr[c0 + j + 1];
+        }
+        const float st = sp.x, thr = sp.y, m2st = -2.0f * st;
+        int acc[APC5];
+#pragma unroll
+        for (int p = 0; p < APC5; ++p) acc[p] = 0;
+        if (st <= ATT_ST_FAST_MAX) {   // CTA-uniform
+            float dmx[APC5];   // per position: max distance of v to its rounding integer
+#pragma unroll
+            for (int p = 0; p < APC5; ++p) {
+                dmx[p] = 0.0f;
+                if (p >= np) break;   // CTA-uniform
+#pragma unroll
+                for (int k = 0; k < AQ5; ++k) {
+                    const float4 apq = sap[(p * AQ5 + k) * AT + threadIdx.x];
+                    const float ap4[4] = {apq.x, apq.y, apq.z, apq.w};
+                    const float u4[4] = {uq[k].x, uq[k].y, uq[k].z, uq[k].w};
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const float x = __fadd_rn(ap4[e], u4[e]);
+                        const float r = rcp_approx(__fadd_rn(ex2_approx(__fmul_rn(x, 2.8853900817779268f)), 1.0f));
+                        const float v = fmaf(m2st, r, st);
+                        const float mg = __fadd_rn(v, 12582912.0f);   // 1.5 * 2^23
+                        dmx[p] = fmaxf(dmx[p], fabsf(__fsub_rn(v, __fsub_rn(mg, 12582912.0f))));
+                        acc[p] += vv[k][e] * (__float_as_int(mg) - 0x4B400000);
+                    }
+                }
+            }
+            // rare: a position with an element within the window of a rounding boundary is
+            // recomputed, flagged elements exactly (fp64 tanh)
+#pragma unroll
+            for (int p = 0; p < APC5; ++p) {
+                if (p >= np) break;
+                if (dmx[p] <= thr) continue;
+                int d = 0;
+#pragma unroll
+                for (int k = 0; k < AQ5; ++k) {
+                    const float4 apq = sap[(p * AQ5 + k) * AT + threadIdx.x];
+                    const float ap4[4] = {apq.x, apq.y, apq.z, apq.w};
+                    const float u4[4] = {uq[k].x, uq[k].y, uq[k].z, uq[k].w};
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const float x = __fadd_rn(ap4[e], u4[e]);
+                        const float r = rcp_approx(__fadd_rn(ex2_approx(__fmul_rn(x, 2.8853900817779268f)), 1.0f));
+                        const float v = fmaf(m2st, r, st);
+                        const float mg = __fadd_rn(v, 12582912.0f);
+                        if (fabsf(__fsub_rn(v, __fsub_rn(mg, 12582912.0f))) > thr && vv[k][e] != 0)
+                            d += vv[k][e] * (att_code_exact(x, st) - (__float_as_int(mg) - 0x4B400000));
+                    }
+                }
+                acc[p] += d;
+            }
+        } else {   // degenerate scale (max |tanh| < 1.3e-4): exact codes throughout
+            for (int p = 0; p < np; ++p) {
+                int a_sum = 0;
+#pragma unroll
+                for (int k = 0; k < AQ5; ++k) {
+                    const float4 apq = sap[(p * AQ5 + k) * AT + threadIdx.x];
+                    const float ap4[4] = {apq.x, apq.y, apq.z, apq.w};
+                    const float u4[4] = {uq[k].x, uq[k].y, uq[k].z, uq[k].w};
+#pragma unroll
+                    for (int e = 0; e < 4; ++e)
+                        if (vv[k][e] != 0) a_sum += vv[k][e] * att_code_exact(__fadd_rn(ap4[e], u4[e]), st);
+                }
+#pragma unroll
+                for (int pp = 0; pp < APC5; ++pp)
+                    if (pp == p) acc[pp] += a_sum;
+            }
+        }
+#pragma unroll
+        for (int p = 0; p < APC5; ++p) {
+            const int t = __reduce_add_sync(0xffffffffu, acc[p]);
+            if (lane == 0 && p < np) atomicAdd(&sums[j][p], t);
+        }
+#pragma unroll
+        for (int k = 0; k < AQ5; ++k) uq[k] = ux[k];
+        sp = spx;
+    }
+    // the last warp to finish writes the scores
+    int last = 0;
+    if (lane == 0) {
+        __threadfence_block();
+        last = atomicAdd(&s_done, 1) == AT / 32 - 1;
+    }
+    if (!__shfl_sync(0xffffffffu, last, 0)) return;
+    __threadfence_block();
+    for (int idx = lane; idx < P * np; idx += 32) {
+        const int j = idx / np, p = idx % np;
+        scores[(int64_t)(c0 + j) * max_len + i0 + p] = dequant(sums[j][p], v_scale[0], st_thr[c0 + j].x);
+    }
+}
+
 // softmax over the l scores of every hypothesis of sentence s (fp64, fixed
 // sequential sum order) and the context sum for a 256-wide slice of 2H.
 // alpha lives in smem position-major ([i][AMAXP]) so the context loop reads it
@@ -362,10 +519,25 @@ int attention_launch(const float* u, int64_t ldu, int64_t N, const int32_t* sent
     k_att_scale<<<dim3((unsigned)n_sent, AMAXP), AT, 0, st>>>(u, ldu, sent_col_off, sent_ncols, att_minmax, A,
                                                               st_thr, err_flag);
     QNMT_CHECK_LAUNCH("k_att_scale");
-    dim3 g1((unsigned)cdiv(max_len, APC), (unsigned)n_sent);
-    k_att_score4<<<g1, AT, 0, st>>>(u, ldu, sent_col_off, sent_ncols, att_proj, st_thr, sent_row, sent_len, A,
-                                    v_codes, v_scale, scores, max_len);
-    QNMT_CHECK_LAUNCH("k_att_score4");
+    const bool quads = A % 4 == 0 && ldu % 4 == 0 && A <= 4 * AT * AQ5 && ((uintptr_t)u % 16) == 0 &&
+                       ((uintptr_t)att_proj % 16) == 0 && ((uintptr_t)v_codes % 4) == 0;
+    if (quads) {   // smem-staged tile, 3 CTAs / SM
+        const size_t smem5 = (size_t)APC5 * AQ5 * AT * sizeof(float4);
+        static size_t done = 0;
+        if (smem5 > 48 * 1024 && smem5 > done) {
+            QNMT_CUDA(cudaFuncSetAttribute(k_att_score5, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem5));
+            done = smem5;
+        }
+        dim3 g5((unsigned)cdiv(max_len, APC5), (unsigned)n_sent);
+        k_att_score5<<<g5, AT, smem5, st>>>(u, ldu, sent_col_off, sent_ncols, att_proj, st_thr, sent_row, sent_len,
+                                            A, v_codes, v_scale, scores, max_len);
+        QNMT_CHECK_LAUNCH("k_att_score5");
+    } else {
+        dim3 g1((unsigned)cdiv(max_len, APC), (unsigned)n_sent);
+        k_att_score4<<<g1, AT, 0, st>>>(u, ldu, sent_col_off, sent_ncols, att_proj, st_thr, sent_row, sent_len, A,
+                                        v_codes, v_scale, scores, max_len);
+        QNMT_CHECK_LAUNCH("k_att_score4");
+    }
     const size_t smem = (size_t)AMAXP * max_len * 2 * sizeof(double);
     const dim3 g2((unsigned)cdiv(H2, AT), (unsigned)n_sent);
 if (smem > 48 * 1024)
