@@ -249,7 +249,7 @@ k_att_score4(const float* __restrict__ u, int64_t ldu, const int32_t* __restrict
 // so no barrier), registers holding just the query slice, codes and
 // accumulators: 3 CTAs / SM instead of 2 to hide the MUFU / FMA latency.  Thread
 // t owns a-quads 4t + 4*AT*k; quads past A are zero (no bounds checks in the
-// hot loop).  Warps add their per-position sums into shared memory and the last
+// hot loop).  Warps store their per-position sums in shared memory and the last
 // warp to finish writes the scores (no end-of-CTA barrier wait).
 constexpr int APC5 = 8;        // positions per CTA
 constexpr int AQ5 = 2;         // a-quads per thread (A <= 4 * AT * AQ5 = 2048)
@@ -261,7 +261,7 @@ k_att_score5(const float* __restrict__ u, int64_t ldu, const int32_t* __restrict
              const int32_t* __restrict__ sent_len, int64_t A, const int8_t* __restrict__ v_codes,
              const float* __restrict__ v_scale, float* __restrict__ scores, int32_t max_len) {
     extern __shared__ float4 sap[];   // [APC5][AQ5][AT]
-    __shared__ int sums[AMAXP][APC5];
+    __shared__ int red5[AMAXP][APC5][AT / 32];
     __shared__ int s_done;
     const int s = blockIdx.y;
     const int P = sent_ncols[s];
@@ -273,7 +273,6 @@ k_att_score5(const float* __restrict__ u, int64_t ldu, const int32_t* __restrict
     const int c0 = sent_col_off[s];
     const int lane = threadIdx.x & 31;
     const int64_t A4 = A / 4;
-    if (threadIdx.x < AMAXP * APC5) (&sums[0][0])[threadIdx.x] = 0;
     if (threadIdx.x == 0) s_done = 0;
     {   // this thread's slots of the tile (positions past i1 and quads past A are zero)
         const float4* src = reinterpret_cast<const float4*>(att_proj + (sent_row[s] + i0) * A);
@@ -297,7 +296,7 @@ k_att_score5(const float* __restrict__ u, int64_t ldu, const int32_t* __restrict
         uq[k] = ok ? reinterpret_cast<const float4*>(u + (int64_t)c0 * ldu)[q] : make_float4(0.f, 0.f, 0.f, 0.f);
     }
     float2 sp = st_thr[c0];
-    __syncthreads();   // sums / s_done initialised
+    __syncthreads();   // s_done initialised
     for (int j = 0; j < P; ++j) {
         float2 spx = sp;
         if (j + 1 < P) {   // prefetch the next hypothesis' query slice and scale
@@ -379,7 +378,7 @@ k_att_score5(const float* __restrict__ u, int64_t ldu, const int32_t* __restrict
 #pragma unroll
         for (int p = 0; p < APC5; ++p) {
             const int t = __reduce_add_sync(0xffffffffu, acc[p]);
-            if (lane == 0 && p < np) atomicAdd(&sums[j][p], t);
+            if (lane == 0) red5[j][p][threadIdx.x >> 5] = t;
         }
 #pragma unroll
         for (int k = 0; k < AQ5; ++k) uq[k] = ux[k];
@@ -395,7 +394,10 @@ k_att_score5(const float* __restrict__ u, int64_t ldu, const int32_t* __restrict
     __threadfence_block();
     for (int idx = lane; idx < P * np; idx += 32) {
         const int j = idx / np, p = idx % np;
-        scores[(int64_t)(c0 + j) * max_len + i0 + p] = dequant(sums[j][p], v_scale[0], st_thr[c0 + j].x);
+        int t = 0;
+#pragma unroll
+        for (int w = 0; w < AT / 32; ++w) t += red5[j][p][w];
+        scores[(int64_t)(c0 + j) * max_len + i0 + p] = dequant(t, v_scale[0], st_thr[c0 + j].x);
     }
 }
 
