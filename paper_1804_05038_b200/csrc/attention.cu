@@ -402,21 +402,11 @@ k_att_score5(const float* __restrict__ u, int64_t ldu, const int32_t* __restrict
 }
 
 // softmax over the l scores of every hypothesis of sentence s (fp64, fixed
-// sequential sum order) and the context sum for a 256-wide slice of 2H.
-// alpha lives in smem position-major ([i][AMAXP]) so the context loop reads it
-// with broadcast loads; P is a template parameter (exactly P fp64 FMAs per i).
-template <int P>
-__device__ __forceinline__ void att_context_body(const float* __restrict__ scores, int32_t max_len,
-                                                 const int32_t* __restrict__ sent_col_off, const float* __restrict__ states,
-                                                 const int64_t* __restrict__ sent_row, const int32_t* __restrict__ sent_len,
-                                                 int64_t H2, float* __restrict__ ctx, int64_t ldc,
-                                                 float* __restrict__ alpha, int64_t lda, int32_t* err_flag,
-                                                 unsigned char* smem_raw, uint32_t* ctx_segmax) {
-    double* ex = reinterpret_cast<double*>(smem_raw);                   // [AMAXP][max_len]
-    double* al = ex + AMAXP * max_len;   // [max_len][AMAXP] f32 alpha widened once (no per-use F2F)
-    const int s = blockIdx.y;
-    const int l = sent_len[s];
-    const int c0 = sent_col_off[s];
+// sequential sum order) into smem alpha, position-major ([i][AMAXP]) so the
+// context loop reads it with broadcast loads, widened to f64 once.
+__device__ __forceinline__ void att_softmax(const float* __restrict__ scores, int32_t max_len, int P, int l, int c0,
+                                            double* ex, double* al, float* __restrict__ alpha, int64_t lda,
+                                            int32_t* err_flag) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (int j = warp; j < P; j += AT / 32) {
         const float* sc = scores + (int64_t)(c0 + j) * max_len;
@@ -429,7 +419,10 @@ __device__ __forceinline__ void att_context_body(const float* __restrict__ score
         }
         m = warp_max(m);
         if (__any_sync(0xffffffffu, bad) && lane == 0) set_flag(err_flag, QNMT_FLAG_NUMERIC);
-        for (int i = lane; i < l; i += 32) ex[j * max_len + i] = exp((double)sc[i] - (double)m);
+        for (int i = lane; i < l; i += 32) {   // exp below e^-700 contributes nothing (sum >= 1)
+            const double t = (double)sc[i] - (double)m;
+            ex[j * max_len + i] = t < -700.0 ? 0.0 : exp_f64(t);
+        }
         __syncwarp();
         double sum = 0.0;
         if (lane == 0)
@@ -441,62 +434,120 @@ __device__ __forceinline__ void att_context_body(const float* __restrict__ score
             if (alpha && blockIdx.x == 0) alpha[(int64_t)(c0 + j) * lda + i] = a;
         }
     }
-    __syncthreads();
-    const int64_t c = (int64_t)blockIdx.x * AT + threadIdx.x;
-    if (c >= H2) return;
-    const float* st = states + sent_row[s] * H2 + c;
-    double acc[P];
+}
+
+// ctx[c] = fl32(sum_i f64(states[R+i][c]) * f64(alpha_i)) for the features of
+// this thread: 4 consecutive (V4, float4 loads) or one; P fp64 FMAs per value.
+template <int P, bool V4>
+__device__ __forceinline__ uint32_t att_context_acc(const float* __restrict__ st_row0, int64_t H2, int l,
+                                                    const double* al, int64_t c, float* __restrict__ ctx,
+                                                    int64_t ldc, int c0) {
+    constexpr int W = V4 ? 4 : 1;
+    uint32_t mx = 0;
+    if (c >= H2) return 0;
+    const float* st = st_row0 + c;
+    double acc[P][W];
 #pragma unroll
-    for (int j = 0; j < P; ++j) acc[j] = 0.0;
+    for (int j = 0; j < P; ++j)
+#pragma unroll
+        for (int e = 0; e < W; ++e) acc[j][e] = 0.0;
+    auto load = [&](int i, float (&d)[W]) {   // widened to f64 at use
+        if (V4) {
+            const float4 q = *reinterpret_cast<const float4*>(st + (int64_t)i * H2);
+            d[0] = q.x;
+            if (W > 1) { d[W > 1 ? 1 : 0] = q.y; d[W > 2 ? 2 : 0] = q.z; d[W > 3 ? 3 : 0] = q.w; }
+        } else {
+            d[0] = st[(int64_t)i * H2];
+        }
+    };
     int i = 0;
     for (; i + 4 <= l; i += 4) {
-        float sv[4];
+        float d[4][W];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) sv[q] = st[(int64_t)(i + q) * H2];
+        for (int q = 0; q < 4; ++q) load(i + q, d[q]);
 #pragma unroll
         for (int q = 0; q < 4; ++q)
 #pragma unroll
-            for (int j = 0; j < P; ++j) acc[j] += (double)sv[q] * al[(i + q) * AMAXP + j];
+            for (int j = 0; j < P; ++j) {
+                const double aj = al[(i + q) * AMAXP + j];
+#pragma unroll
+                for (int e = 0; e < W; ++e) acc[j][e] += (double)d[q][e] * aj;
+            }
     }
     for (; i < l; ++i) {
-        const double sv = (double)st[(int64_t)i * H2];
+        float d[W];
+        load(i, d);
 #pragma unroll
-        for (int j = 0; j < P; ++j) acc[j] += sv * al[i * AMAXP + j];
+        for (int j = 0; j < P; ++j) {
+            const double aj = al[i * AMAXP + j];
+#pragma unroll
+            for (int e = 0; e < W; ++e) acc[j][e] += (double)d[e] * aj;
+        }
     }
-    uint32_t mx = 0;
 #pragma unroll
     for (int j = 0; j < P; ++j) {
-        const float v = __double2float_rn(acc[j]);
-        ctx[(int64_t)(c0 + j) * ldc + c] = v;
-        mx = max(mx, __float_as_uint(v) & 0x7fffffffu);
+        float v[W];
+#pragma unroll
+        for (int e = 0; e < W; ++e) {
+            v[e] = __double2float_rn(acc[j][e]);
+            mx = max(mx, __float_as_uint(v[e]) & 0x7fffffffu);
+        }
+        float* dst = ctx + (int64_t)(c0 + j) * ldc + c;
+        if (V4)
+            *reinterpret_cast<float4*>(dst) = make_float4(v[0], v[W > 1 ? 1 : 0], v[W > 2 ? 2 : 0], v[W > 3 ? 3 : 0]);
+        else
+            dst[0] = v[0];
     }
-    if (ctx_segmax) {   // per-sentence max |ctx| for the next quantization (segment = sentence)
-        const unsigned act = __activemask();   // threads with c >= H2 have returned
-        mx = __reduce_max_sync(act, mx);
-        if ((act & ((1u << lane) - 1u)) == 0 && mx) atomicMax(ctx_segmax + s, mx);
-    }
+    return mx;
 }
 
+// Grid (features / (V4 ? 4 AT : AT), sentences).  V4 CTAs of sentences with more
+// than 6 live hypotheses run the scalar accumulation 4 times (register bound).
 __global__ void __launch_bounds__(AT)
 k_att_context3(const float* __restrict__ scores, int32_t max_len, const int32_t* __restrict__ sent_col_off,
                const int32_t* __restrict__ sent_ncols, const float* __restrict__ states,
                const int64_t* __restrict__ sent_row, const int32_t* __restrict__ sent_len, int64_t H2,
                float* __restrict__ ctx, int64_t ldc, float* __restrict__ alpha, int64_t lda, int32_t* err_flag,
-               uint32_t* ctx_segmax) {
+               uint32_t* ctx_segmax, int v4) {
     extern __shared__ unsigned char smem_raw[];
-    const int P = sent_ncols[blockIdx.y];
-#define QNMT_CTX_P(P_)                                                                                      \
-    case P_:                                                                                               \
-        att_context_body<P_>(scores, max_len, sent_col_off, states, sent_row, sent_len, H2, ctx, ldc, alpha, \
-                             lda, err_flag, smem_raw, ctx_segmax);                                         \
-        break;
-    switch (P) {
-        QNMT_CTX_P(1) QNMT_CTX_P(2) QNMT_CTX_P(3) QNMT_CTX_P(4) QNMT_CTX_P(5) QNMT_CTX_P(6) QNMT_CTX_P(7)
-        QNMT_CTX_P(8) QNMT_CTX_P(9) QNMT_CTX_P(10) QNMT_CTX_P(11) QNMT_CTX_P(12) QNMT_CTX_P(13) QNMT_CTX_P(14)
-        QNMT_CTX_P(15) QNMT_CTX_P(16)
-        default: break;   // P == 0: sentence finished
+    const int s = blockIdx.y;
+    const int P = sent_ncols[s];
+    if (P == 0) return;   // sentence finished
+    const int l = sent_len[s];
+    const int c0 = sent_col_off[s];
+    double* ex = reinterpret_cast<double*>(smem_raw);   // [AMAXP][max_len]
+    double* al = ex + AMAXP * max_len;                 // [max_len][AMAXP]
+    att_softmax(scores, max_len, P, l, c0, ex, al, alpha, lda, err_flag);
+    __syncthreads();
+    const float* st0 = states + sent_row[s] * H2;
+    uint32_t mx = 0;
+#define QNMT_CTX_P(P_, V4_, C_) \
+    case P_: mx = max(mx, att_context_acc<P_, V4_>(st0, H2, l, al, (C_), ctx, ldc, c0)); break;
+    if (v4 && P <= 6) {
+        const int64_t c = ((int64_t)blockIdx.x * AT + threadIdx.x) * 4;
+        switch (P) {
+            QNMT_CTX_P(1, true, c) QNMT_CTX_P(2, true, c) QNMT_CTX_P(3, true, c) QNMT_CTX_P(4, true, c)
+            QNMT_CTX_P(5, true, c) QNMT_CTX_P(6, true, c)
+            default: break;
+        }
+    } else {
+        const int reps = v4 ? 4 : 1;
+        for (int r = 0; r < reps; ++r) {
+            const int64_t c = (int64_t)blockIdx.x * AT * reps + (int64_t)r * AT + threadIdx.x;
+            switch (P) {
+                QNMT_CTX_P(1, false, c) QNMT_CTX_P(2, false, c) QNMT_CTX_P(3, false, c) QNMT_CTX_P(4, false, c)
+                QNMT_CTX_P(5, false, c) QNMT_CTX_P(6, false, c) QNMT_CTX_P(7, false, c) QNMT_CTX_P(8, false, c)
+                QNMT_CTX_P(9, false, c) QNMT_CTX_P(10, false, c) QNMT_CTX_P(11, false, c) QNMT_CTX_P(12, false, c)
+                QNMT_CTX_P(13, false, c) QNMT_CTX_P(14, false, c) QNMT_CTX_P(15, false, c) QNMT_CTX_P(16, false, c)
+                default: break;
+            }
+        }
     }
 #undef QNMT_CTX_P
+    if (ctx_segmax) {   // per-sentence max |ctx| for the next quantization (segment = sentence)
+        mx = __reduce_max_sync(0xffffffffu, mx);
+        if ((threadIdx.x & 31) == 0 && mx) atomicMax(ctx_segmax + s, mx);
+    }
 }
 
 int attention_launch(const float* u, int64_t ldu, int64_t N, const int32_t* sent_col_off,
@@ -541,11 +592,12 @@ int attention_launch(const float* u, int64_t ldu, int64_t N, const int32_t* sent
         QNMT_CHECK_LAUNCH("k_att_score4");
     }
     const size_t smem = (size_t)AMAXP * max_len * 2 * sizeof(double);
-    const dim3 g2((unsigned)cdiv(H2, AT), (unsigned)n_sent);
-if (smem > 48 * 1024)
+    const bool v4 = H2 % 4 == 0 && ldc % 4 == 0 && ((uintptr_t)states % 16) == 0 && ((uintptr_t)ctx % 16) == 0;
+    const dim3 g2((unsigned)cdiv(H2, v4 ? 4 * AT : AT), (unsigned)n_sent);
+    if (smem > 48 * 1024)
         QNMT_CUDA(cudaFuncSetAttribute(k_att_context3, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     k_att_context3<<<g2, AT, smem, st>>>(scores, max_len, sent_col_off, sent_ncols, states, sent_row, sent_len, H2,
-                                          ctx, ldc, alpha, lda, err_flag, ctx_segmax);
+                                          ctx, ldc, alpha, lda, err_flag, ctx_segmax, v4 ? 1 : 0);
     QNMT_CHECK_LAUNCH("k_att_context3");
     return QNMT_OK;
 }
