@@ -81,6 +81,7 @@ __device__ __forceinline__ void load_ap(const float* __restrict__ ap, int64_t A,
 __global__ void __launch_bounds__(AT)
 k_att_minmax(const float* __restrict__ att_proj, const int64_t* __restrict__ sent_row,
              const int32_t* __restrict__ sent_len, int64_t A, float* __restrict__ mm) {
+    pdl_entry();
     const int s = blockIdx.y;
     const int64_t a = (int64_t)blockIdx.x * AT + threadIdx.x;
     if (a >= A) return;
@@ -99,7 +100,7 @@ k_att_minmax(const float* __restrict__ att_proj, const int64_t* __restrict__ sen
 int att_minmax_launch(const float* att_proj, const int64_t* sent_row, const int32_t* sent_len, int32_t n_sent,
                       int64_t A, float* mm, cudaStream_t st) {
     if (n_sent <= 0) return QNMT_OK;
-    k_att_minmax<<<dim3((unsigned)cdiv(A, AT), (unsigned)n_sent), AT, 0, st>>>(att_proj, sent_row, sent_len, A, mm);
+    QNMT_LAUNCH(k_att_minmax, dim3((unsigned)cdiv(A, AT), (unsigned)n_sent), AT, 0, st, att_proj, sent_row, sent_len, A, mm);
     QNMT_CHECK_LAUNCH("k_att_minmax");
     return QNMT_OK;
 }
@@ -111,6 +112,7 @@ __global__ void __launch_bounds__(AT)
 k_att_scale(const float* __restrict__ u, int64_t ldu, const int32_t* __restrict__ sent_col_off,
             const int32_t* __restrict__ sent_ncols, const float* __restrict__ mm, int64_t A,
             float2* __restrict__ st_thr, int32_t* err_flag) {
+    pdl_entry();
     __shared__ uint32_t mred[AT / 32];
     const int s = blockIdx.x, j = blockIdx.y;
     if (j >= sent_ncols[s]) return;
@@ -153,6 +155,7 @@ k_att_score4(const float* __restrict__ u, int64_t ldu, const int32_t* __restrict
              const float2* __restrict__ st_thr, const int64_t* __restrict__ sent_row,
              const int32_t* __restrict__ sent_len, int64_t A, const int8_t* __restrict__ v_codes,
              const float* __restrict__ v_scale, float* __restrict__ scores, int32_t max_len) {
+    pdl_entry();
     __shared__ int red[AMAXP][APC][AT / 32];
     const int s = blockIdx.y;
     const int P = sent_ncols[s];
@@ -260,6 +263,7 @@ k_att_score5(const float* __restrict__ u, int64_t ldu, const int32_t* __restrict
              const float2* __restrict__ st_thr, const int64_t* __restrict__ sent_row,
              const int32_t* __restrict__ sent_len, int64_t A, const int8_t* __restrict__ v_codes,
              const float* __restrict__ v_scale, float* __restrict__ scores, int32_t max_len) {
+    pdl_entry();
     extern __shared__ float4 sap[];   // [APC5][AQ5][AT]
     __shared__ int red5[AMAXP][APC5][AT / 32];
     __shared__ int s_done;
@@ -509,6 +513,7 @@ k_att_context3(const float* __restrict__ scores, int32_t max_len, const int32_t*
                const int64_t* __restrict__ sent_row, const int32_t* __restrict__ sent_len, int64_t H2,
                float* __restrict__ ctx, int64_t ldc, float* __restrict__ alpha, int64_t lda, int32_t* err_flag,
                uint32_t* ctx_segmax, int v4) {
+    pdl_entry();
     extern __shared__ unsigned char smem_raw[];
     const int s = blockIdx.y;
     const int P = sent_ncols[s];
@@ -569,7 +574,7 @@ int attention_launch(const float* u, int64_t ldu, int64_t N, const int32_t* sent
         TRY_LAUNCH(att_minmax_launch(att_proj, sent_row, sent_len, n_sent, A, mm, st));
         att_minmax = mm;
     }
-    k_att_scale<<<dim3((unsigned)n_sent, AMAXP), AT, 0, st>>>(u, ldu, sent_col_off, sent_ncols, att_minmax, A,
+    QNMT_LAUNCH(k_att_scale, dim3((unsigned)n_sent, AMAXP), AT, 0, st, u, ldu, sent_col_off, sent_ncols, att_minmax, A,
                                                               st_thr, err_flag);
     QNMT_CHECK_LAUNCH("k_att_scale");
     const bool quads = A % 4 == 0 && ldu % 4 == 0 && A <= 4 * AT * AQ5 && ((uintptr_t)u % 16) == 0 &&
@@ -582,12 +587,12 @@ int attention_launch(const float* u, int64_t ldu, int64_t N, const int32_t* sent
             done = smem5;
         }
         dim3 g5((unsigned)cdiv(max_len, APC5), (unsigned)n_sent);
-        k_att_score5<<<g5, AT, smem5, st>>>(u, ldu, sent_col_off, sent_ncols, att_proj, st_thr, sent_row, sent_len,
+        QNMT_LAUNCH(k_att_score5, g5, AT, smem5, st, u, ldu, sent_col_off, sent_ncols, att_proj, st_thr, sent_row, sent_len,
                                             A, v_codes, v_scale, scores, max_len);
         QNMT_CHECK_LAUNCH("k_att_score5");
     } else {
         dim3 g1((unsigned)cdiv(max_len, APC), (unsigned)n_sent);
-        k_att_score4<<<g1, AT, 0, st>>>(u, ldu, sent_col_off, sent_ncols, att_proj, st_thr, sent_row, sent_len, A,
+        QNMT_LAUNCH(k_att_score4, g1, AT, 0, st, u, ldu, sent_col_off, sent_ncols, att_proj, st_thr, sent_row, sent_len, A,
                                         v_codes, v_scale, scores, max_len);
         QNMT_CHECK_LAUNCH("k_att_score4");
     }
@@ -596,7 +601,7 @@ int attention_launch(const float* u, int64_t ldu, int64_t N, const int32_t* sent
     const dim3 g2((unsigned)cdiv(H2, v4 ? 4 * AT : AT), (unsigned)n_sent);
     if (smem > 48 * 1024)
         QNMT_CUDA(cudaFuncSetAttribute(k_att_context3, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_att_context3<<<g2, AT, smem, st>>>(scores, max_len, sent_col_off, sent_ncols, states, sent_row, sent_len, H2,
+    QNMT_LAUNCH(k_att_context3, g2, AT, smem, st, scores, max_len, sent_col_off, sent_ncols, states, sent_row, sent_len, H2,
                                           ctx, ldc, alpha, lda, err_flag, ctx_segmax, v4 ? 1 : 0);
     QNMT_CHECK_LAUNCH("k_att_context3");
     return QNMT_OK;

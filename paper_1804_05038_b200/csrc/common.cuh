@@ -10,6 +10,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <utility>
 #include <stdint.h>
 #include <stdio.h>
 
@@ -31,6 +32,42 @@ struct NdevScope {
     explicit NdevScope(const int32_t* p) : old(tl_ndev) { tl_ndev = p; }
     ~NdevScope() { tl_ndev = old; }
 };
+
+// Programmatic dependent launch (PDL): kernels of the decode path are launched
+// with programmatic stream serialization, so a kernel's CTAs are scheduled while
+// its predecessor's last CTAs still run; every such kernel calls pdl_entry()
+// (wait for the predecessor's completion + memory, then let the successor
+// launch) before touching data the predecessor wrote.  Both instructions are
+// no-ops for a normal launch.  QNMT_PDL=0 in the environment disables it.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_entry() {
+    pdl_wait();
+    pdl_trigger();
+}
+bool pdl_enabled();
+
+template <typename... KArgs, typename... Args>
+static inline cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                                   Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
+#define QNMT_LAUNCH(kern, grid, block, smem, st, ...)                                                   \
+    do {                                                                                              \
+        cudaError_t _le = ::qnmt::launch_k(kern, grid, block, smem, st, __VA_ARGS__);                  \
+        if (_le != cudaSuccess) return ::qnmt::cuda_status(_le, #kern);                               \
+    } while (0)
 
 #define QNMT_CHECK_LAUNCH(where)                                              \
     do {                                                                      \

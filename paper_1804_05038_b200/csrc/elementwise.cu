@@ -27,6 +27,7 @@ __global__ void k_gru_gates(const float* __restrict__ gx, int64_t ldgx, const in
                             int64_t ldh, int64_t N, int64_t H, float* __restrict__ z,
                             float* __restrict__ rh, int32_t* err_flag, const int32_t* n_dev,
                             uint32_t* segmax, const int32_t* __restrict__ col_seg) {
+    pdl_entry();
     int64_t n = blockIdx.y;
     if (beyond(n_dev, n)) return;
     int64_t rowx = gx_row ? gx_row[n] : n;
@@ -55,6 +56,7 @@ __global__ void k_gru_combine(const float* __restrict__ gx, int64_t ldgx, const 
                               float* __restrict__ h_out, int64_t ldo, float* __restrict__ out2,
                               int64_t ld2, const int32_t* __restrict__ out2_row, int32_t* err_flag,
                               const int32_t* n_dev, uint32_t* segmax, const int32_t* __restrict__ col_seg) {
+    pdl_entry();
     int64_t n = blockIdx.y;
     if (beyond(n_dev, n)) return;
     int64_t rowx = gx_row ? gx_row[n] : n;
@@ -79,6 +81,7 @@ __global__ void k_gru_combine(const float* __restrict__ gx, int64_t ldgx, const 
 __global__ void k_tanh(const float* __restrict__ x, int64_t N, int64_t D, int64_t ldx,
                        float* __restrict__ y, int64_t ldy, int32_t* err_flag, const int32_t* n_dev,
                        uint32_t* segmax, const int32_t* __restrict__ col_seg) {
+    pdl_entry();
     int64_t n = blockIdx.y;
     if (beyond(n_dev, n)) return;
     bool bad = false;
@@ -98,6 +101,7 @@ __global__ void k_embed_gather(const float* __restrict__ table, int64_t rows, in
                                const int32_t* __restrict__ ids, float* __restrict__ out,
                                int64_t ldo, int32_t* err_flag, const int32_t* n_dev,
                                uint32_t* segmax, const int32_t* __restrict__ col_seg) {
+    pdl_entry();
     int64_t n = blockIdx.x;
     if (beyond(n_dev, n)) return;
     int32_t id = ids[n];
@@ -123,7 +127,7 @@ int gru_gates_launch(const float* gx, int64_t ldgx, const int32_t* gx_row, const
                      float* rh, int32_t* err_flag, cudaStream_t st, uint32_t* segmax,
                      const int32_t* col_seg) {
     if (N <= 0) return QNMT_OK;
-    k_gru_gates<<<rows_grid(N, H, 256), 256, 0, st>>>(gx, ldgx, gx_row, gh, ldgh, h, ldh, N, H, z, rh, err_flag,
+    QNMT_LAUNCH(k_gru_gates, rows_grid(N, H, 256), 256, 0, st, gx, ldgx, gx_row, gh, ldgh, h, ldh, N, H, z, rh, err_flag,
                                                      tl_ndev, segmax, col_seg);
     QNMT_CHECK_LAUNCH("k_gru_gates");
     return QNMT_OK;
@@ -135,7 +139,7 @@ int gru_combine_launch(const float* gx, int64_t ldgx, const int32_t* gx_row, con
                        const int32_t* out2_row, int32_t* err_flag, cudaStream_t st,
                        uint32_t* segmax, const int32_t* col_seg) {
     if (N <= 0) return QNMT_OK;
-    k_gru_combine<<<rows_grid(N, H, 256), 256, 0, st>>>(gx, ldgx, gx_row, ghc, ldghc, z, h, ldh, N, H,
+    QNMT_LAUNCH(k_gru_combine, rows_grid(N, H, 256), 256, 0, st, gx, ldgx, gx_row, ghc, ldghc, z, h, ldh, N, H,
                                                         h_out, ldo, out2, ld2, out2_row, err_flag, tl_ndev,
                                                         segmax, col_seg);
     QNMT_CHECK_LAUNCH("k_gru_combine");
@@ -146,7 +150,7 @@ int tanh_launch(const float* x, int64_t N, int64_t D, int64_t ldx, float* y, int
                 int32_t* err_flag, cudaStream_t st, uint32_t* segmax,
                 const int32_t* col_seg) {
     if (N <= 0) return QNMT_OK;
-    k_tanh<<<rows_grid(N, D, 256), 256, 0, st>>>(x, N, D, ldx, y, ldy, err_flag, tl_ndev, segmax, col_seg);
+    QNMT_LAUNCH(k_tanh, rows_grid(N, D, 256), 256, 0, st, x, N, D, ldx, y, ldy, err_flag, tl_ndev, segmax, col_seg);
     QNMT_CHECK_LAUNCH("k_tanh");
     return QNMT_OK;
 }
@@ -155,7 +159,7 @@ int embed_gather_launch(const float* table, int64_t rows, int64_t E, const int32
                         float* out, int64_t ldo, int32_t* err_flag, cudaStream_t st,
                         uint32_t* segmax, const int32_t* col_seg) {
     if (n <= 0) return QNMT_OK;
-    k_embed_gather<<<(unsigned)n, 128, 0, st>>>(table, rows, E, ids, out, ldo, err_flag, tl_ndev, segmax,
+    QNMT_LAUNCH(k_embed_gather, (unsigned)n, 128, 0, st, table, rows, E, ids, out, ldo, err_flag, tl_ndev, segmax,
                                                 col_seg);
     QNMT_CHECK_LAUNCH("k_embed_gather");
     return QNMT_OK;

@@ -390,6 +390,7 @@ static_assert(ST_COLS == QNMT_STAMP_COLS, "stamp row layout");
 
 __global__ void k_stamp(long long* stamps, const int32_t* step_dev, int slot, int slot2, const int32_t* n_dev,
                         const int32_t* P, const int32_t* len, int n_sent) {
+    pdl_entry();
     const int t = *step_dev;
     long long* row = stamps + (int64_t)t * ST_COLS;
     if (slot == ST_ATT0) {   // also record the work descriptors of this step
@@ -427,7 +428,7 @@ __global__ void k_stamp(long long* stamps, const int32_t* step_dev, int slot, in
 
 static int stamp(qnmt_engine* e, int slot, const StepIO& io, cudaStream_t st, int slot2 = -1) {
     if (!e->stamp_on || !tl_ndev || !e->stamps) return QNMT_OK;   // graph-captured steps only
-    k_stamp<<<1, 256, 0, st>>>(e->stamps, e->d_step, slot, slot2, tl_ndev, io.sent_ncols, io.sent_len, io.nseg);
+    QNMT_LAUNCH(k_stamp, 1, 256, 0, st, e->stamps, e->d_step, slot, slot2, tl_ndev, io.sent_ncols, io.sent_len, io.nseg);
     QNMT_CHECK_LAUNCH("k_stamp");
     return QNMT_OK;
 }

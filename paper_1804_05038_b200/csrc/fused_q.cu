@@ -82,6 +82,7 @@ k_gates_q(const float* __restrict__ gx, int64_t ldgx, const float* __restrict__ 
           const float* __restrict__ h, int64_t ldh, int64_t H, const int32_t* __restrict__ off,
           const int32_t* __restrict__ cnt, float* __restrict__ z, int8_t* __restrict__ q_rh, float* sc_rh,
           int32_t* err_flag, int max_cols) {
+    pdl_entry();
     FQ_SEG_PROLOGUE
     uint32_t m = 0;
     bool bad = false;
@@ -113,6 +114,7 @@ k_combine_q(const float* __restrict__ gxc, int64_t ldgx, const float* __restrict
             const float* __restrict__ z, const float* __restrict__ h, int64_t ldh, int64_t H,
             const int32_t* __restrict__ off, const int32_t* __restrict__ cnt, float* __restrict__ h_out,
             int64_t ldo, int8_t* __restrict__ q_out, float* sc_out, int32_t* err_flag, int max_cols) {
+    pdl_entry();
     FQ_SEG_PROLOGUE
     uint32_t m = 0;
     bool bad = false;
@@ -143,6 +145,7 @@ __global__ void __launch_bounds__(FQ_T)
 k_embed_q(const float* __restrict__ table, int64_t rows, int64_t E, const int32_t* __restrict__ ids,
           const int32_t* __restrict__ off, const int32_t* __restrict__ cnt, int8_t* __restrict__ q_out,
           float* sc_out, int32_t* err_flag, int max_cols) {
+    pdl_entry();
     FQ_SEG_PROLOGUE
     uint32_t m = 0;
     const int64_t G = (int64_t)P * E / 4;
@@ -164,6 +167,7 @@ __global__ void __launch_bounds__(FQ_T)
 k_tanh_q(const float* __restrict__ x, int64_t ldx, int64_t D, const int32_t* __restrict__ off,
          const int32_t* __restrict__ cnt, int8_t* __restrict__ q_out, float* sc_out, int32_t* err_flag,
          int max_cols) {
+    pdl_entry();
     FQ_SEG_PROLOGUE
     uint32_t m = 0;
     bool bad = false;
@@ -188,6 +192,7 @@ k_gather_q(const float* __restrict__ a, const float* __restrict__ b, const int32
            int64_t H, const int32_t* __restrict__ off, const int32_t* __restrict__ cnt, float* __restrict__ a_out,
            float* __restrict__ b_out, int8_t* __restrict__ qa, float* sca, int8_t* __restrict__ qb, float* scb,
            int32_t* err_flag, int max_cols) {
+    pdl_entry();
     FQ_SEG_PROLOGUE
     float* va = vals;                    // [P][H]
     float* vb = vals + (int64_t)P * H;   // [P][H]
@@ -238,7 +243,7 @@ int gates_q_launch(const float* gx, int64_t ldgx, const float* gh, int64_t ldgh,
     const size_t smem = (size_t)max_cols * H * sizeof(float);
     static size_t done = 0;
     FQ_TRY(set_smem((const void*)k_gates_q, smem, done));
-    k_gates_q<<<(unsigned)n_seg, FQ_T, smem, st>>>(gx, ldgx, gh, ldgh, h, ldh, H, off, cnt, z, q_rh, sc_rh,
+    QNMT_LAUNCH(k_gates_q, (unsigned)n_seg, FQ_T, smem, st, gx, ldgx, gh, ldgh, h, ldh, H, off, cnt, z, q_rh, sc_rh,
                                                     err_flag, max_cols);
     QNMT_CHECK_LAUNCH("k_gates_q");
     return QNMT_OK;
@@ -252,7 +257,7 @@ int combine_q_launch(const float* gxc, int64_t ldgx, const float* ghc, int64_t l
     const size_t smem = (size_t)max_cols * H * sizeof(float);
     static size_t done = 0;
     FQ_TRY(set_smem((const void*)k_combine_q, smem, done));
-    k_combine_q<<<(unsigned)n_seg, FQ_T, smem, st>>>(gxc, ldgx, ghc, ldghc, z, h, ldh, H, off, cnt, h_out, ldo,
+    QNMT_LAUNCH(k_combine_q, (unsigned)n_seg, FQ_T, smem, st, gxc, ldgx, ghc, ldghc, z, h, ldh, H, off, cnt, h_out, ldo,
                                                       q_out, sc_out, err_flag, max_cols);
     QNMT_CHECK_LAUNCH("k_combine_q");
     return QNMT_OK;
@@ -265,7 +270,7 @@ int embed_q_launch(const float* table, int64_t rows, int64_t E, const int32_t* i
     const size_t smem = (size_t)max_cols * E * sizeof(float);
     static size_t done = 0;
     FQ_TRY(set_smem((const void*)k_embed_q, smem, done));
-    k_embed_q<<<(unsigned)n_seg, FQ_T, smem, st>>>(table, rows, E, ids, off, cnt, q_out, sc_out, err_flag, max_cols);
+    QNMT_LAUNCH(k_embed_q, (unsigned)n_seg, FQ_T, smem, st, table, rows, E, ids, off, cnt, q_out, sc_out, err_flag, max_cols);
     QNMT_CHECK_LAUNCH("k_embed_q");
     return QNMT_OK;
 }
@@ -276,7 +281,7 @@ int tanh_q_launch(const float* x, int64_t ldx, int64_t D, const int32_t* off, co
     const size_t smem = (size_t)max_cols * D * sizeof(float);
     static size_t done = 0;
     FQ_TRY(set_smem((const void*)k_tanh_q, smem, done));
-    k_tanh_q<<<(unsigned)n_seg, FQ_T, smem, st>>>(x, ldx, D, off, cnt, q_out, sc_out, err_flag, max_cols);
+    QNMT_LAUNCH(k_tanh_q, (unsigned)n_seg, FQ_T, smem, st, x, ldx, D, off, cnt, q_out, sc_out, err_flag, max_cols);
     QNMT_CHECK_LAUNCH("k_tanh_q");
     return QNMT_OK;
 }
@@ -288,7 +293,7 @@ int gather_q_launch(const float* a, const float* b, const int32_t* parent, int64
     const size_t smem = (size_t)2 * max_cols * H * sizeof(float);
     static size_t done = 0;
     FQ_TRY(set_smem((const void*)k_gather_q, smem, done));
-    k_gather_q<<<(unsigned)n_seg, FQ_T, smem, st>>>(a, b, parent, H, off, cnt, a_out, b_out, qa, sca, qb, scb,
+    QNMT_LAUNCH(k_gather_q, (unsigned)n_seg, FQ_T, smem, st, a, b, parent, H, off, cnt, a_out, b_out, qa, sca, qb, scb,
                                                      err_flag, max_cols);
     QNMT_CHECK_LAUNCH("k_gather_q");
     return QNMT_OK;

@@ -29,8 +29,9 @@ namespace qnmt {
 constexpr int TC_EPI_WARPS = 8;
 constexpr int TC_THREADS = 64 + 32 * TC_EPI_WARPS;
 
+// ring depth: as many stages as fit ~200 KB of smem, at most 8
 template <int BN>
-using TcCfg = TcRing<BN, (BN == 256) ? 4 : (BN == 128 ? 6 : 8)>;
+using TcCfg = TcRing<BN, (200 * 1024 / (TC_BM * TC_BK + BN * TC_BK)) < 8 ? (200 * 1024 / (TC_BM * TC_BK + BN * TC_BK)) : 8>;
 
 struct TcEpi {
     const float* w_scales;
@@ -51,7 +52,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N, int K,
           TcEpi e, const int32_t* n_dev) {
     using C = TcCfg<BN>;
-    if (n_dev) N = min(N, *n_dev);   // graph mode: live columns from the device
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* smem = (unsigned char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     const TcBars<C> bars(smem);
@@ -60,11 +60,14 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
+    pdl_trigger();
+    const uint32_t tmem_base = tc_setup<C>(&tmA, &tmB, bars, TC_EPI_WARPS);
+    pdl_wait();   // everything above overlaps the predecessor kernel (PDL)
+    if (n_dev) N = min(N, *n_dev);   // graph mode: live columns from the device
     const int m_blocks = (M + TC_BM - 1) / TC_BM;
     const int n_blocks = (N + BN - 1) / BN;
     const int tiles = m_blocks * n_blocks;
     const int k_blocks = (K + TC_BK - 1) / TC_BK;
-    const uint32_t tmem_base = tc_setup<C>(&tmA, &tmB, bars, TC_EPI_WARPS);
 
     if (warp == 0) {
         tc_produce<C, BN>(&tmA, &tmB, smem, bars, tiles, n_blocks, k_blocks);
@@ -259,7 +262,8 @@ static int launch_tc(const GemmArgs& g, cudaStream_t st) {
     TcEpi e{g.w_scales, g.w_rows_per_scale, g.x_scales, g.col_seg, g.bias, g.Y, g.ldy, g.acc_out, g.flags};
     int tiles = (int)(cdiv(g.M, TC_BM) * cdiv(g.N, BN));
     int grid = tiles < tc_sm_count() ? tiles : tc_sm_count();
-    k_gemm_tc<BN, EPI><<<grid, TC_THREADS, C::SMEM, st>>>(ta, tb, (int)g.M, (int)g.N, (int)g.K, e, tl_ndev);
+    auto kfn = k_gemm_tc<BN, EPI>;
+    QNMT_LAUNCH(kfn, grid, TC_THREADS, C::SMEM, st, ta, tb, (int)g.M, (int)g.N, (int)g.K, e, tl_ndev);
     QNMT_CHECK_LAUNCH("k_gemm_tc");
     return QNMT_OK;
 }
@@ -275,14 +279,31 @@ int gemm_tc_launch(const GemmArgs& g, cudaStream_t st) {
     const int sms = tc_sm_count();
     const int epi = (g.bias ? EPI_BIAS : 0) | ((g.flags & QNMT_GEMM_ACCUMULATE) ? EPI_ACCUMULATE : 0) |
                     (g.acc_out ? EPI_RAW : 0);
-    const int bn = (g.N > 128 && mb * cdiv(g.N, 256) >= sms) ? 256 : (g.N > 64 && mb * cdiv(g.N, 128) >= sms / 2) ? 128 : 64;
+    int bn;
+    if (epi & EPI_RAW) {   // op-API accumulator export: three tile widths
+        bn = (g.N > 128 && mb * cdiv(g.N, 256) >= sms) ? 256 : (g.N > 64 && mb * cdiv(g.N, 128) >= sms / 2) ? 128 : 64;
+    } else {
+        // fewest waves of tiles over the SMs, then the narrowest tile (less B data and epilogue
+        // per tile, more CTAs): e.g. N = 1280 -> M 2048: 160 (128 tiles), M 3072: 256, M 1024: 96
+        static const int cand[] = {64, 96, 128, 160, 192, 224, 256};
+        bn = 256;
+        int64_t best = INT64_MAX;
+        for (int b : cand) {
+            const int64_t waves = cdiv(mb * cdiv(g.N, b), sms);
+            if (waves < best) {
+                best = waves;
+                bn = b;
+            }
+        }
+    }
 #define QNMT_TC_CASE(BN_, E_) \
     if (bn == BN_ && epi == E_) return launch_tc<BN_, E_>(g, st);
-#define QNMT_TC_BN(BN_) \
-    QNMT_TC_CASE(BN_, 0) QNMT_TC_CASE(BN_, 1) QNMT_TC_CASE(BN_, 2) QNMT_TC_CASE(BN_, 3) \
-    QNMT_TC_CASE(BN_, 4) QNMT_TC_CASE(BN_, 5) QNMT_TC_CASE(BN_, 6) QNMT_TC_CASE(BN_, 7)
-    QNMT_TC_BN(256) QNMT_TC_BN(128) QNMT_TC_BN(64)
-#undef QNMT_TC_BN
+#define QNMT_TC_BN4(BN_) QNMT_TC_CASE(BN_, 0) QNMT_TC_CASE(BN_, 1) QNMT_TC_CASE(BN_, 2) QNMT_TC_CASE(BN_, 3)
+#define QNMT_TC_BN8(BN_) QNMT_TC_BN4(BN_) QNMT_TC_CASE(BN_, 4) QNMT_TC_CASE(BN_, 5) QNMT_TC_CASE(BN_, 6) QNMT_TC_CASE(BN_, 7)
+    QNMT_TC_BN8(256) QNMT_TC_BN8(128) QNMT_TC_BN8(64)
+    QNMT_TC_BN4(96) QNMT_TC_BN4(160) QNMT_TC_BN4(192) QNMT_TC_BN4(224)
+#undef QNMT_TC_BN4
+#undef QNMT_TC_BN8
 #undef QNMT_TC_CASE
     set_error("gemm_tc: no kernel for bn=%d epi=%d", bn, epi);
     return QNMT_ERR_CONFIG;

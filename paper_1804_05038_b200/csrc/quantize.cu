@@ -19,6 +19,7 @@ __global__ void k_seg_maxabs(const float* __restrict__ x, int64_t ncols, int64_t
                              int chunks_per_col, int64_t chunk_elems,
                              const int32_t* __restrict__ col_seg, uint32_t* seg_maxbits,
                              bool vec4, const int32_t* n_dev) {
+    pdl_entry();
     int64_t b = blockIdx.x;
     int64_t col = b / chunks_per_col;
     int64_t chunk = b % chunks_per_col;
@@ -51,6 +52,7 @@ __global__ void k_encode(const float* __restrict__ x, int64_t ncols, int64_t K, 
                          const int32_t* __restrict__ col_seg, const uint32_t* __restrict__ seg_maxbits,
                          int8_t* __restrict__ q, int64_t ldq, float* __restrict__ scales,
                          int32_t mode, int32_t* err_flag, bool vec4, const int32_t* n_dev) {
+    pdl_entry();
     int64_t b = blockIdx.x;
     int64_t col = b / chunks_per_col;
     int64_t chunk = b % chunks_per_col;
@@ -91,10 +93,10 @@ int quantize_launch(const float* x, int64_t ncols, int64_t K, int64_t ldx, const
     int64_t chunk_elems = 4096;
     int chunks = (int)cdiv(K, chunk_elems);
     int64_t blocks = ncols * chunks;
-    k_seg_maxabs<<<(unsigned)blocks, QT, 0, st>>>(x, ncols, K, ldx, chunks, chunk_elems, col_seg,
+    QNMT_LAUNCH(k_seg_maxabs, (unsigned)blocks, QT, 0, st, x, ncols, K, ldx, chunks, chunk_elems, col_seg,
                                                  seg_maxbits, vec4, tl_ndev);
     QNMT_CHECK_LAUNCH("k_seg_maxabs");
-    k_encode<<<(unsigned)blocks, QT, 0, st>>>(x, ncols, K, ldx, chunks, chunk_elems, col_seg,
+    QNMT_LAUNCH(k_encode, (unsigned)blocks, QT, 0, st, x, ncols, K, ldx, chunks, chunk_elems, col_seg,
                                              seg_maxbits, q, ldq, scales, mode, err_flag, vec4, tl_ndev);
     QNMT_CHECK_LAUNCH("k_encode");
     return QNMT_OK;
@@ -108,7 +110,7 @@ int quantize_encode_launch(const float* x, int64_t ncols, int64_t K, int64_t ldx
                 ((uintptr_t)x % 16 == 0) && ((uintptr_t)q % 4 == 0);
     int64_t chunk_elems = 4096;
     int chunks = (int)cdiv(K, chunk_elems);
-    k_encode<<<(unsigned)(ncols * chunks), QT, 0, st>>>(x, ncols, K, ldx, chunks, chunk_elems, col_seg,
+    QNMT_LAUNCH(k_encode, (unsigned)(ncols * chunks), QT, 0, st, x, ncols, K, ldx, chunks, chunk_elems, col_seg,
                                                        seg_maxbits, q, ldq, scales, mode, err_flag, vec4, tl_ndev);
     QNMT_CHECK_LAUNCH("k_encode");
     return QNMT_OK;
@@ -120,7 +122,7 @@ int quantize_max_launch(const float* x, int64_t ncols, int64_t K, int64_t ldx, c
     bool vec4 = (K % 4 == 0) && (ldx % 4 == 0) && ((uintptr_t)x % 16 == 0);
     int64_t chunk_elems = 4096;
     int chunks = (int)cdiv(K, chunk_elems);
-    k_seg_maxabs<<<(unsigned)(ncols * chunks), QT, 0, st>>>(x, ncols, K, ldx, chunks, chunk_elems, col_seg,
+    QNMT_LAUNCH(k_seg_maxabs, (unsigned)(ncols * chunks), QT, 0, st, x, ncols, K, ldx, chunks, chunk_elems, col_seg,
                                                            seg_maxbits, vec4, tl_ndev);
     QNMT_CHECK_LAUNCH("k_seg_maxabs");
     return QNMT_OK;

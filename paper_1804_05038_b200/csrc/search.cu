@@ -13,6 +13,8 @@
 // the final min-by-(-logp, tokens) selection (:157).
 #include <float.h>
 
+#include <algorithm>
+
 #include "common.cuh"
 #include "search.cuh"
 
@@ -29,7 +31,8 @@ __device__ __forceinline__ bool cand_better(double sa, int ta, int pa, double sb
 
 __global__ void __launch_bounds__(SEARCH_T)
 k_search_step(SearchState ss, int step, int n_sent, int beam, int k_list) {
-    __shared__ int s_cnt[SEARCH_T];
+    pdl_entry();
+    __shared__ int wsum[SEARCH_T / 32];
     const int tid = threadIdx.x;
     if (ss.step_dev) step = *ss.step_dev;   // graph-captured loop: step counter lives on the device
     int new_p = 0;
@@ -41,29 +44,47 @@ k_search_step(SearchState ss, int step, int n_sent, int beam, int k_list) {
     if (s < n_sent && !ss.done[s]) {
         const int P = ss.P[s];
         const int off = ss.col_off[s];
-        int ptr[16];
-        for (int p = 0; p < P; ++p) ptr[p] = 0;
+        // merge with each parent's current head kept in registers: one dependent load per round
+        const int kt = min(k_list, beam);
+        double hs[16];
+        int ht[16], ptr[16];
+#pragma unroll
+        for (int p = 0; p < 16; ++p) {
+            ptr[p] = 0;
+            if (p < P) {
+                const int64_t idx = (int64_t)(off + p) * k_list;
+                hs[p] = ss.cand_score[idx];
+                ht[p] = ss.cand_tok[idx];
+            }
+        }
         for (int r = 0; r < beam; ++r) {
             int bp = -1;
             double bs = 0.0;
             int bt = 0;
-            for (int p = 0; p < P; ++p) {
-                if (ptr[p] >= k_list) continue;
-                int64_t idx = (int64_t)(off + p) * k_list + ptr[p];
-                double cs = ss.cand_score[idx];
-                int ct = ss.cand_tok[idx];
-                if (bp < 0 || cand_better(cs, ct, p, bs, bt, bp)) {
+#pragma unroll
+            for (int p = 0; p < 16; ++p) {
+                if (p >= P || ptr[p] >= kt) continue;
+                if (bp < 0 || cand_better(hs[p], ht[p], p, bs, bt, bp)) {
                     bp = p;
-                    bs = cs;
-                    bt = ct;
+                    bs = hs[p];
+                    bt = ht[p];
                 }
             }
             if (bp < 0) break;
-            ptr[bp]++;
             sel_tok[nsel] = bt;
             sel_par[nsel] = bp;
             sel_sc[nsel] = bs;
             nsel++;
+#pragma unroll
+            for (int p = 0; p < 16; ++p)
+                if (p == bp) {
+                    ptr[p]++;
+                    if (ptr[p] < kt) {
+                        const int64_t idx = (int64_t)(off + p) * k_list + ptr[p];
+                        hs[p] = ss.cand_score[idx];
+                        ht[p] = ss.cand_tok[idx];
+                    }
+                }
         }
         // split into finished / live
         double best_live = -DBL_MAX;
@@ -109,17 +130,29 @@ k_search_step(SearchState ss, int step, int n_sent, int beam, int k_list) {
             new_p = 0;
         }
     }
-    // exclusive prefix sum of new_p over sentences
-    s_cnt[tid] = new_p;
-    __syncthreads();
-    for (int o = 1; o < SEARCH_T; o <<= 1) {
-        int v = tid >= o ? s_cnt[tid - o] : 0;
-        __syncthreads();
-        s_cnt[tid] += v;
-        __syncthreads();
+    // exclusive prefix sum of new_p over sentences: warp scans, then a scan of the warp sums
+    const int lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+    int incl = new_p;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
     }
-    int new_off = s_cnt[tid] - new_p;
-    if (tid == SEARCH_T - 1) *ss.n_live = s_cnt[tid];
+    if (lane == 31) wsum[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+        int w = lane < nwarps ? wsum[lane] : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(0xffffffffu, w, o);
+            if (lane >= o) w += t;
+        }
+        if (lane < nwarps) wsum[lane] = w;
+    }
+    __syncthreads();
+    incl += warp > 0 ? wsum[warp - 1] : 0;
+    const int new_off = incl - new_p;
+    if (tid == (int)blockDim.x - 1) *ss.n_live = incl;
     if (s < n_sent) {
         const int old_off = ss.col_off[s];
         for (int j = 0; j < new_p; ++j) {
@@ -144,6 +177,7 @@ __global__ void k_gather_rows(const float* __restrict__ a, const float* __restri
                               const int32_t* __restrict__ parent, int64_t H,
                               float* __restrict__ a_out, float* __restrict__ b_out, const int32_t* n_dev,
                               uint32_t* a_max, uint32_t* b_max, const int32_t* __restrict__ col_seg) {
+    pdl_entry();
     int64_t n = blockIdx.x;
     if (beyond(n_dev, n)) return;
     int64_t p = parent[n];
@@ -175,7 +209,8 @@ int search_step_launch(const SearchState& ss, int step, int n_sent, int beam, in
         set_error("search: n_sent=%d beam=%d exceed limits (%d, 16)", n_sent, beam, SEARCH_T);
         return QNMT_ERR_CONFIG;
     }
-    k_search_step<<<1, SEARCH_T, 0, st>>>(ss, step, n_sent, beam, k_list);
+    const int threads = (int)std::min<int64_t>(SEARCH_T, std::max<int64_t>(32, cdiv(n_sent, 32) * 32));
+    QNMT_LAUNCH(k_search_step, 1, threads, 0, st, ss, step, n_sent, beam, k_list);
     QNMT_CHECK_LAUNCH("k_search_step");
     return QNMT_OK;
 }
@@ -184,7 +219,7 @@ int gather_rows_launch(const float* a, const float* b, const int32_t* parent, in
                        float* a_out, float* b_out, cudaStream_t st, uint32_t* a_max, uint32_t* b_max,
                        const int32_t* col_seg) {
     if (N <= 0) return QNMT_OK;
-    k_gather_rows<<<(unsigned)N, 256, 0, st>>>(a, b, parent, H, a_out, b_out, tl_ndev, a_max, b_max, col_seg);
+    QNMT_LAUNCH(k_gather_rows, (unsigned)N, 256, 0, st, a, b, parent, H, a_out, b_out, tl_ndev, a_max, b_max, col_seg);
     QNMT_CHECK_LAUNCH("k_gather_rows");
     return QNMT_OK;
 }

@@ -1,3 +1,4 @@
+#include <stdlib.h>
 // status.cu -- error plumbing and small utilities of the C ABI.
 #include <stdarg.h>
 #include <string.h>
@@ -9,6 +10,14 @@ namespace qnmt {
 static thread_local char g_last_error[512] = "";
 thread_local const int32_t* tl_ndev = nullptr;
 static unsigned long long g_launches = 0;
+
+bool pdl_enabled() {
+    static const bool on = [] {
+        const char* v = getenv("QNMT_PDL");
+        return !(v && v[0] == '0');
+    }();
+    return on;
+}
 
 void count_launch() { __atomic_fetch_add(&g_launches, 1ULL, __ATOMIC_RELAXED); }
 

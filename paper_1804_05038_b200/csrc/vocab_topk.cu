@@ -57,7 +57,6 @@ __global__ void __launch_bounds__(VT_THREADS, 1)
 k_vocab_stats(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW, int M, int V,
               int K, VtArgs e, const int32_t* n_dev) {
     using C = VtRing;
-    if (n_dev) M = min(M, *n_dev);
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* smem = (unsigned char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     const TcBars<C> bars(smem);
@@ -69,13 +68,16 @@ k_vocab_stats(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ C
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
+    if (threadIdx.x < 16) tab[threadIdx.x] = exp2((double)threadIdx.x / 16.0);
+    if (threadIdx.x < 64) tab64[threadIdx.x] = exp2((double)threadIdx.x / 64.0);
+    pdl_trigger();
+    const uint32_t tmem_base = tc_setup<C>(&tmX, &tmW, bars, VT_EPI_WARPS);   // includes __syncthreads
+    pdl_wait();   // everything above overlaps the predecessor kernel (PDL)
+    if (n_dev) M = min(M, *n_dev);
     const int m_blocks = (M + TC_BM - 1) / TC_BM;
     const int n_blocks = (V + VT_BN - 1) / VT_BN;
     const int tiles = m_blocks * n_blocks;
     const int k_blocks = (K + TC_BK - 1) / TC_BK;
-    if (threadIdx.x < 16) tab[threadIdx.x] = exp2((double)threadIdx.x / 16.0);
-    if (threadIdx.x < 64) tab64[threadIdx.x] = exp2((double)threadIdx.x / 64.0);
-    const uint32_t tmem_base = tc_setup<C>(&tmX, &tmW, bars, VT_EPI_WARPS);   // includes __syncthreads
 
     if (warp == 0) {
         tc_produce<C, VT_BN>(&tmX, &tmW, smem, bars, tiles, n_blocks, k_blocks);
@@ -302,6 +304,7 @@ constexpr int VM_WARPS = 4;   // rows per merge CTA (one warp per row)
 template <int KM>
 __global__ void __launch_bounds__(32 * VM_WARPS)
 k_vocab_merge(VtMergeArgs a, int64_t N, const int32_t* n_dev) {
+    pdl_entry();
     __shared__ double tab[16];
     __shared__ Cand lst[VM_WARPS][KM];
     __shared__ int flagged[VM_WARPS][VT_RESCAN_MAX];
@@ -549,7 +552,7 @@ int vocab_stats_launch(const VocabTopk& p, cudaStream_t st) {
     const int n_blocks = (int)cdiv(V, VT_BN);
     const int tiles = (int)(cdiv(N, TC_BM) * n_blocks);
     const int grid = tiles < tc_sm_count() ? tiles : tc_sm_count();
-    k_vocab_stats<<<grid, VT_THREADS, VtRing::SMEM, st>>>(tx, tw, (int)N, (int)V, (int)K, e, tl_ndev);
+    QNMT_LAUNCH(k_vocab_stats, grid, VT_THREADS, VtRing::SMEM, st, tx, tw, (int)N, (int)V, (int)K, e, tl_ndev);
     QNMT_CHECK_LAUNCH("k_vocab_stats");
     return QNMT_OK;
 }
@@ -562,12 +565,8 @@ int vocab_merge_launch(const VocabTopk& p, cudaStream_t st) {
                    p.w_scales, p.w_rows_per_scale, p.bias, reinterpret_cast<VtPart*>(p.part), p.live, k,
                    p.cand_score, p.cand_tok};
     const unsigned g = (unsigned)cdiv(N, VM_WARPS);
-    if (k <= 6)
-        k_vocab_merge<8><<<g, 32 * VM_WARPS, 0, st>>>(ma, N, tl_ndev);
-    else if (k <= 13)
-        k_vocab_merge<16><<<g, 32 * VM_WARPS, 0, st>>>(ma, N, tl_ndev);
-    else
-        k_vocab_merge<32><<<g, 32 * VM_WARPS, 0, st>>>(ma, N, tl_ndev);
+    auto kfn = k <= 6 ? k_vocab_merge<8> : k <= 13 ? k_vocab_merge<16> : k_vocab_merge<32>;
+    QNMT_LAUNCH(kfn, g, 32 * VM_WARPS, 0, st, ma, N, tl_ndev);
     QNMT_CHECK_LAUNCH("k_vocab_merge");
     return QNMT_OK;
 }
