@@ -141,6 +141,17 @@ struct qnmt_engine {
     float* att_mm;           // [S][2][A] per-sentence column max / min of att_proj
     uint32_t* ctx_max;       // [S] max |ctx| bits per sentence (attention context -> its quantization)
     bool fq_ok = false;      // per-sentence fused op + quantize kernels fit in shared memory (fused_q.cu)
+    // Stacked weights (copied at engine creation) for GEMMs that share an input:
+    //   w2x = [cell2 W_x; W_e] x q(emb), w3x = [cell3 W_x; W_c] x q(ctx): the readout terms
+    //   W_e e and W_c c come out of the cells' input GEMMs and are added in the W_s epilogue;
+    //   wuq = [U_att; cell3 U_zr] x q(s') (current-state query only).  Per-row scales.
+    bool stack_ok = false, stack_u = false;
+    int8_t* w2x = nullptr; float* w2x_s = nullptr; float* b2x = nullptr;
+    int8_t* w3x = nullptr; float* w3x_s = nullptr; float* b3x = nullptr;
+    int8_t* wuq = nullptr; float* wuq_s = nullptr;
+    float* gxr = nullptr;    // [N][3H+R] cell2 input side + W_e e
+    float* gxq = nullptr;    // [N][3H+R] cell3 input side + W_c c
+    float* uq = nullptr;     // [N][A+2H] U_att q + cell3 U_zr s'
     // translate loop state
     float* st_s[2];          // [N][H] s
     float* st_sp[2];         // [N][H] s_prime
@@ -244,8 +255,13 @@ static int check_flag(qnmt_engine* e, cudaStream_t st) {
 
 static int gemm(const int8_t* W, int64_t M, int64_t K, const float* ws, int64_t rps, const int8_t* X,
                 int64_t N, int64_t ldx, const float* xs, const int32_t* seg, const float* bias, float* Y,
-                int64_t ldy, int32_t flags, cudaStream_t st) {
+                int64_t ldy, int32_t flags, cudaStream_t st, const float* add1 = nullptr, int64_t ld1 = 0,
+                const float* add2 = nullptr, int64_t ld2 = 0) {
     GemmArgs g{W, M, K, K, ws, rps, X, N, ldx, xs, seg, bias, Y, ldy, nullptr, flags};
+    g.add1 = add1;
+    g.ld1 = ld1;
+    g.add2 = add2;
+    g.ld2 = ld2;
     return gemm_i8_launch(g, st);
 }
 
@@ -436,31 +452,50 @@ static int stamp(qnmt_engine* e, int slot, const StepIO& io, cudaStream_t st, in
 // one GRU cell (layers.py:170-181) over the step's columns; h_out's codes -> q_out / sc_out.
 // fq: gates and combine are the per-sentence fused op+quantize kernels (fused_q.cu);
 // otherwise elementwise kernels followed by the two-pass quantization.
+// Optional stacking (see qnmt_engine::w2x): xs = {W, per-row scales, bias, rows, out, ld} replaces the
+// cell's own W_x GEMM; gh_pre (ld ldgh_pre) is a U_zr product already computed by a stacked GEMM.
+struct XSide {
+    const int8_t* w;
+    const float* ws;
+    const float* b;
+    int64_t rows;
+    float* out;
+    int64_t ld;
+};
+
 static int gru_cell(qnmt_engine* e, const Cell& c, const StepIO& io, const int8_t* qx, const float* sx,
                     const int8_t* qh, const float* sh, const float* h, float* h_out, int8_t* q_out, float* sc_out,
-                    cudaStream_t st) {
+                    cudaStream_t st, const XSide* xs = nullptr, const float* gh_pre = nullptr,
+                    int64_t ldgh_pre = 0) {
     const int64_t H = e->m->H, N = io.N;
     const int32_t* seg = io.col_sent;
     const int ns = io.nseg;
+    float* gx = xs ? xs->out : e->gx;
+    const int64_t ldgx = xs ? xs->ld : 3 * H;
+    const float* gh = gh_pre ? gh_pre : e->gh;
+    const int64_t ldgh = gh_pre ? ldgh_pre : 2 * H;
     prof_mark(e, PG_GEMM, st, 2.0 * N * (3 * H * c.in + 2 * H * H), 3.0 * H * c.in + 2.0 * H * H);
-    TRY(gemm(c.wx, 3 * H, c.in, c.wx_s, H, qx, N, c.in, sx, seg, c.bx, e->gx, 3 * H, 0, st));
-    TRY(gemm(c.uzr, 2 * H, H, c.uzr_s, H, qh, N, H, sh, seg, nullptr, e->gh, 2 * H, 0, st));
+    if (xs)
+        TRY(gemm(xs->w, xs->rows, c.in, xs->ws, 1, qx, N, c.in, sx, seg, xs->b, gx, ldgx, 0, st));
+    else
+        TRY(gemm(c.wx, 3 * H, c.in, c.wx_s, H, qx, N, c.in, sx, seg, c.bx, gx, ldgx, 0, st));
+    if (!gh_pre) TRY(gemm(c.uzr, 2 * H, H, c.uzr_s, H, qh, N, H, sh, seg, nullptr, e->gh, 2 * H, 0, st));
     prof_mark(e, PG_GRU, st);
     if (e->fq_ok) {
-        TRY(gates_q_launch(e->gx, 3 * H, e->gh, 2 * H, h, H, H, io.sent_col_off, io.sent_ncols, ns, io.max_cols,
+        TRY(gates_q_launch(gx, ldgx, gh, ldgh, h, H, H, io.sent_col_off, io.sent_ncols, ns, io.max_cols,
                            e->z, e->q_rh, e->sc_rh, e->err, st));
     } else {
-        TRY(gru_gates_launch(e->gx, 3 * H, nullptr, e->gh, 2 * H, h, H, N, H, e->z, e->rh, e->err, st));
+        TRY(gru_gates_launch(gx, ldgx, nullptr, gh, ldgh, h, H, N, H, e->z, e->rh, e->err, st));
         TRY(quantize_launch(e->rh, N, H, H, seg, ns, e->q_rh, H, e->sc_rh, e->seg_bits, 1, e->err, st));
     }
     prof_mark(e, PG_GEMM, st, 2.0 * N * H * H, (double)H * H);
     TRY(gemm(c.uc, H, H, c.uc_s, H, e->q_rh, N, H, e->sc_rh, seg, nullptr, e->ghc, H, 0, st));
     prof_mark(e, PG_GRU, st);
     if (e->fq_ok) {
-        TRY(combine_q_launch(e->gx + 2 * H, 3 * H, e->ghc, H, e->z, h, H, H, io.sent_col_off, io.sent_ncols, ns,
+        TRY(combine_q_launch(gx + 2 * H, ldgx, e->ghc, H, e->z, h, H, H, io.sent_col_off, io.sent_ncols, ns,
                              io.max_cols, h_out, H, q_out, sc_out, e->err, st));
     } else {
-        TRY(gru_combine_launch(e->gx, 3 * H, nullptr, e->ghc, H, e->z, h, H, N, H, h_out, H, nullptr, 0,
+        TRY(gru_combine_launch(gx, ldgx, nullptr, e->ghc, H, e->z, h, H, N, H, h_out, H, nullptr, 0,
                                nullptr, e->err, st));
         TRY(quantize_launch(h_out, N, H, H, seg, ns, q_out, H, sc_out, e->seg_bits, 1, e->err, st));
     }
@@ -488,16 +523,31 @@ static int step_core(qnmt_engine* e, const StepIO& io, cudaStream_t st) {
         TRY(embed_gather_launch(m->tgt_embed, V, E, io.y, N, e->emb, E, e->err, st));
         TRY(quantize_launch(e->emb, N, E, E, seg, ns, e->q_emb, E, e->sc_emb, e->seg_bits, 1, e->err, st));
     }
+    // stacked GEMMs (fq + tcgen05 only): W_e e / W_c c ride on the cells' W_x GEMMs, U_att on U_zr
+    const bool stk = fq && e->stack_ok && g_gemm_impl != 1;
+    const bool stk_u = stk && e->stack_u;
+    const int64_t LX = 3 * H + R, LU = A + 2 * H;
+    const XSide xs2{e->w2x, e->w2x_s, e->b2x, LX, e->gxr, LX};
+    const XSide xs3{e->w3x, e->w3x_s, e->b3x, LX, e->gxq, LX};
     // s' = GRU_r(emb, s) (layers.py:372); the query (layers.py:373) is s' or the previous s'
     int8_t* q_si = m->aq == 1 ? e->q_si : e->q_q;
     float* sc_si = m->aq == 1 ? e->sc_si : e->sc_q;
-    TRY(gru_cell(e, m->cell[2], io, e->q_emb, e->sc_emb, e->q_s, e->sc_s, io.s, io.s_int, q_si, sc_si, st));
+    TRY(gru_cell(e, m->cell[2], io, e->q_emb, e->sc_emb, e->q_s, e->sc_s, io.s, io.s_int, q_si, sc_si, st,
+                 stk ? &xs2 : nullptr));
     prof_mark(e, PG_GEMM, st, 2.0 * N * A * H, (double)A * H);
-    TRY(gemm(m->u_att, A, H, m->u_att_s, A, e->q_q, N, H, e->sc_q, seg, nullptr, e->u, A, 0, st));
+    const float* u = e->u;
+    int64_t ldu = A;
+    if (stk_u) {
+        TRY(gemm(e->wuq, LU, H, e->wuq_s, 1, e->q_q, N, H, e->sc_q, seg, nullptr, e->uq, LU, 0, st));
+        u = e->uq;
+        ldu = LU;
+    } else {
+        TRY(gemm(m->u_att, A, H, m->u_att_s, A, e->q_q, N, H, e->sc_q, seg, nullptr, e->u, A, 0, st));
+    }
     prof_mark(e, PG_ATT, st);
     TRY(stamp(e, ST_ATT0, io, st));
     if (fq) QNMT_CUDA(cudaMemsetAsync(e->ctx_max, 0, sizeof(uint32_t) * (size_t)ns, st));
-    TRY(attention_launch(e->u, A, N, io.sent_col_off, io.sent_ncols, io.nseg, io.att_proj, io.att_minmax, io.states,
+    TRY(attention_launch(u, ldu, N, io.sent_col_off, io.sent_ncols, io.nseg, io.att_proj, io.att_minmax, io.states,
                          io.sent_row, io.sent_len, io.max_len, A, 2 * H, m->v, m->v_s, e->ctx, 2 * H,
                          io.alpha, io.lda, e->att_scratch, e->err, st, fq ? e->ctx_max : nullptr));
     TRY(stamp(e, ST_ATT1, io, st));
@@ -510,14 +560,20 @@ static int step_core(qnmt_engine* e, const StepIO& io, cudaStream_t st) {
                             st));
     }
     // s = GRU_q(ctx, s')                                        (layers.py:375)
-    TRY(gru_cell(e, m->cell[3], io, e->q_ctx, e->sc_ctx, q_si, sc_si, io.s_int, io.s_new, e->q_sn, e->sc_sn, st));
+    TRY(gru_cell(e, m->cell[3], io, e->q_ctx, e->sc_ctx, q_si, sc_si, io.s_int, io.s_new, e->q_sn, e->sc_sn, st,
+                 stk ? &xs3 : nullptr, stk_u ? e->uq + A : nullptr, LU));
     // readout = tanh(((W_s s + b_r) + W_e emb) + W_c ctx)       (layers.py:255-265)
     prof_mark(e, PG_GEMM, st, 2.0 * N * R * (H + E + 2 * H), (double)R * (H + E + 2 * H));
-    TRY(gemm(m->w_state, R, H, m->w_state_s, R, e->q_sn, N, H, e->sc_sn, seg, m->b_r, e->ro, R, 0, st));
-    TRY(gemm(m->w_embed, R, E, m->w_embed_s, R, e->q_emb, N, E, e->sc_emb, seg, nullptr, e->ro, R,
-             QNMT_GEMM_ACCUMULATE, st));
-    TRY(gemm(m->w_ctx, R, 2 * H, m->w_ctx_s, R, e->q_ctx, N, 2 * H, e->sc_ctx, seg, nullptr, e->ro, R,
-             QNMT_GEMM_ACCUMULATE, st));
+    if (stk) {   // W_e emb and W_c ctx were computed with the cells' input GEMMs
+        TRY(gemm(m->w_state, R, H, m->w_state_s, R, e->q_sn, N, H, e->sc_sn, seg, m->b_r, e->ro, R, 0, st,
+                 e->gxr + 3 * H, LX, e->gxq + 3 * H, LX));
+    } else {
+        TRY(gemm(m->w_state, R, H, m->w_state_s, R, e->q_sn, N, H, e->sc_sn, seg, m->b_r, e->ro, R, 0, st));
+        TRY(gemm(m->w_embed, R, E, m->w_embed_s, R, e->q_emb, N, E, e->sc_emb, seg, nullptr, e->ro, R,
+                 QNMT_GEMM_ACCUMULATE, st));
+        TRY(gemm(m->w_ctx, R, 2 * H, m->w_ctx_s, R, e->q_ctx, N, 2 * H, e->sc_ctx, seg, nullptr, e->ro, R,
+                 QNMT_GEMM_ACCUMULATE, st));
+    }
     prof_mark(e, PG_MISC, st);
     if (fq) {
         TRY(tanh_q_launch(e->ro, R, R, io.sent_col_off, io.sent_ncols, ns, io.max_cols, e->q_ro, e->sc_ro, e->err,
@@ -725,6 +781,17 @@ int qnmt_engine_create(const qnmt_model* m, int32_t max_sentences, int32_t max_s
         e->att_scratch = a.take<char>(N * (L + 2) * 4 + 2 * S * A * 4 + 1024);
         e->att_mm = a.take<float>(2 * S * A);
         e->ctx_max = a.take<uint32_t>(S);
+        e->w2x = a.take<int8_t>((3 * H + R) * E);
+        e->w2x_s = a.take<float>(3 * H + R);
+        e->b2x = a.take<float>(3 * H + R);
+        e->w3x = a.take<int8_t>((3 * H + R) * 2 * H);
+        e->w3x_s = a.take<float>(3 * H + R);
+        e->b3x = a.take<float>(3 * H + R);
+        e->wuq = a.take<int8_t>((A + 2 * H) * H);
+        e->wuq_s = a.take<float>(A + 2 * H);
+        e->gxr = a.take<float>(N * (3 * H + R));
+        e->gxq = a.take<float>(N * (3 * H + R));
+        e->uq = a.take<float>(N * (A + 2 * H));
         for (int i = 0; i < 2; ++i) {
             e->st_s[i] = a.take<float>(N * H);
             e->st_sp[i] = a.take<float>(N * H);
@@ -767,6 +834,45 @@ int qnmt_engine_create(const qnmt_model* m, int32_t max_sentences, int32_t max_s
         const size_t d = std::max(E, std::max(H, R));
         e->fq_ok = 16 * d * 4 <= FQ_SMEM_MAX && 2 * B * H * 4 <= FQ_SMEM_MAX && E % 4 == 0 && H % 4 == 0 &&
                    R % 4 == 0 && ((uintptr_t)m->tgt_embed % 16) == 0;   // float4 groups (fused_q.cu)
+    }
+    if (E % 16 == 0 && H % 16 == 0 && A % 16 == 0 && R % 16 == 0) {   // stacked weights (tcgen05 path)
+        auto host_scale = [](const float* d) { float v = 0; cudaMemcpy(&v, d, 4, cudaMemcpyDeviceToHost); return v; };
+        std::vector<float> sc;
+        auto stack = [&](int8_t* dst, const int8_t* a0, size_t rows0, const int8_t* a1, size_t rows1, size_t K) {
+            cudaMemcpy(dst, a0, rows0 * K, cudaMemcpyDeviceToDevice);
+            cudaMemcpy(dst + rows0 * K, a1, rows1 * K, cudaMemcpyDeviceToDevice);
+        };
+        const qnmt::Cell& c2 = m->cell[2];
+        const qnmt::Cell& c3 = m->cell[3];
+        // [cell W_x (3 row-block scales); readout W (one scale)], bias [b_x; 0]
+        auto stack_x = [&](const qnmt::Cell& c, const int8_t* wr, const float* wr_s, size_t K, int8_t* w, float* ws,
+                           float* b) {
+            stack(w, c.wx, 3 * H, wr, R, K);
+            sc.assign(3 * H + R, 0.0f);
+            for (size_t g = 0; g < 3; ++g) {
+                const float v = host_scale(c.wx_s + g);
+                for (size_t i = 0; i < H; ++i) sc[g * H + i] = v;
+            }
+            const float vr = host_scale(wr_s);
+            for (size_t i = 0; i < R; ++i) sc[3 * H + i] = vr;
+            cudaMemcpy(ws, sc.data(), (3 * H + R) * 4, cudaMemcpyHostToDevice);
+            cudaMemset(b, 0, (3 * H + R) * 4);
+            cudaMemcpy(b, c.bx, 3 * H * 4, cudaMemcpyDeviceToDevice);
+        };
+        stack_x(c2, m->w_embed, m->w_embed_s, E, e->w2x, e->w2x_s, e->b2x);
+        stack_x(c3, m->w_ctx, m->w_ctx_s, 2 * H, e->w3x, e->w3x_s, e->b3x);
+        // [U_att (one scale); cell3 U_zr (z, r scales)]
+        stack(e->wuq, m->u_att, A, c3.uzr, 2 * H, H);
+        sc.assign(A + 2 * H, 0.0f);
+        const float va = host_scale(m->u_att_s);
+        for (size_t i = 0; i < A; ++i) sc[i] = va;
+        for (size_t g = 0; g < 2; ++g) {
+            const float v = host_scale(c3.uzr_s + g);
+            for (size_t i = 0; i < H; ++i) sc[A + g * H + i] = v;
+        }
+        cudaMemcpy(e->wuq_s, sc.data(), (A + 2 * H) * 4, cudaMemcpyHostToDevice);
+        e->stack_ok = true;
+        e->stack_u = m->aq == 0;
     }
     cudaStreamCreateWithFlags(&e->cap_stream, cudaStreamNonBlocking);
     cudaError_t ce = cudaMallocHost(&e->h_pinned, 64);

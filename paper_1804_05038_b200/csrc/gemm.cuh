@@ -18,6 +18,11 @@ struct GemmArgs {
     int64_t ldy;
     int64_t* acc_out;
     int32_t flags;
+    // optional epilogue addends (tcgen05 path only): y = ((dq + bias) + add1[n][m]) + add2[n][m]
+    const float* add1 = nullptr;
+    int64_t ld1 = 0;
+    const float* add2 = nullptr;
+    int64_t ld2 = 0;
 };
 
 int gemm_i8_launch(const GemmArgs& g, cudaStream_t st);

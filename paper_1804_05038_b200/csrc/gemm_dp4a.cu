@@ -212,6 +212,8 @@ int g_gemm_impl = 0;
 
 int gemm_i8_launch(const GemmArgs& g, cudaStream_t st) {
     if (g.M <= 0 || g.N <= 0) return QNMT_OK;
+    if (g.add1 && !tc_eligible(g)) { set_error("gemm: epilogue addends need the tcgen05 path"); return QNMT_ERR_CONFIG; }
+    if (g.add1) return gemm_tc_launch(g, st);
     if (tl_ndev) {   // graph-captured step: device-side N, only the tcgen05 kernel supports it
         if (!tc_eligible(g)) { set_error("graph mode needs tcgen05-eligible GEMM shapes"); return QNMT_ERR_CONFIG; }
         return gemm_tc_launch(g, st);

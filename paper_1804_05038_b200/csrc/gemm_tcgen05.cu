@@ -43,9 +43,15 @@ struct TcEpi {
     int64_t ldy;
     int64_t* acc_out;
     int32_t flags;
+    const float* add1;
+    int64_t ld1;
+    const float* add2;
+    int64_t ld2;
 };
 
-enum { EPI_BIAS = 1, EPI_ACCUMULATE = 2, EPI_RAW = 4 };
+// EPI_ADD2: two precomputed f32 terms added in order after the bias (the readout's
+// ((W_s s + b_r) + W_e e) + W_c c with W_e e and W_c c from stacked GEMMs)
+enum { EPI_BIAS = 1, EPI_ACCUMULATE = 2, EPI_RAW = 4, EPI_ADD2 = 8 };
 
 template <int BN, int EPI>
 __global__ void __launch_bounds__(TC_THREADS, 1)
@@ -119,10 +125,17 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
                     continue;
                 }
                 float* yrow = e.Y + (int64_t)nbase * e.ldy + m;
-                float yv[16];
+                float yv[16], a1v[16], a2v[16];
                 if (EPI & EPI_ACCUMULATE) {
 #pragma unroll
                     for (int j = 0; j < 16; ++j) yv[j] = (mok && j < ncols) ? yrow[(int64_t)j * e.ldy] : 0.0f;
+                }
+                if (EPI & EPI_ADD2) {
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) {
+                        a1v[j] = (mok && j < ncols) ? e.add1[(int64_t)(nbase + j) * e.ld1 + m] : 0.0f;
+                        a2v[j] = (mok && j < ncols) ? e.add2[(int64_t)(nbase + j) * e.ld2 + m] : 0.0f;
+                    }
                 }
                 tc::tmem_ld_wait();
                 if (EPI & EPI_RAW) {
@@ -150,6 +163,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
                     float y = yd[j];
                     if (EPI & EPI_BIAS) y = __fadd_rn(y, bias);
                     if (EPI & EPI_ACCUMULATE) y = __fadd_rn(yv[j], y);
+                    if (EPI & EPI_ADD2) y = __fadd_rn(__fadd_rn(y, a1v[j]), a2v[j]);
                     yd[j] = y;
                 }
                 if (mok && ncols == 16) {
@@ -259,7 +273,8 @@ static int launch_tc(const GemmArgs& g, cudaStream_t st) {
     if (rc) return rc;
     rc = tc_get_map(g.X, g.N, g.K, g.ldx, BN, &tb);
     if (rc) return rc;
-    TcEpi e{g.w_scales, g.w_rows_per_scale, g.x_scales, g.col_seg, g.bias, g.Y, g.ldy, g.acc_out, g.flags};
+    TcEpi e{g.w_scales, g.w_rows_per_scale, g.x_scales, g.col_seg, g.bias, g.Y, g.ldy, g.acc_out, g.flags,
+            g.add1, g.ld1, g.add2, g.ld2};
     int tiles = (int)(cdiv(g.M, TC_BM) * cdiv(g.N, BN));
     int grid = tiles < tc_sm_count() ? tiles : tc_sm_count();
     auto kfn = k_gemm_tc<BN, EPI>;
@@ -278,7 +293,7 @@ int gemm_tc_launch(const GemmArgs& g, cudaStream_t st) {
     const int64_t mb = cdiv(g.M, TC_BM);
     const int sms = tc_sm_count();
     const int epi = (g.bias ? EPI_BIAS : 0) | ((g.flags & QNMT_GEMM_ACCUMULATE) ? EPI_ACCUMULATE : 0) |
-                    (g.acc_out ? EPI_RAW : 0);
+                    (g.acc_out ? EPI_RAW : 0) | (g.add1 ? EPI_ADD2 : 0);
     int bn;
     if (epi & EPI_RAW) {   // op-API accumulator export: three tile widths
         bn = (g.N > 128 && mb * cdiv(g.N, 256) >= sms) ? 256 : (g.N > 64 && mb * cdiv(g.N, 128) >= sms / 2) ? 128 : 64;
@@ -302,6 +317,8 @@ int gemm_tc_launch(const GemmArgs& g, cudaStream_t st) {
 #define QNMT_TC_BN8(BN_) QNMT_TC_BN4(BN_) QNMT_TC_CASE(BN_, 4) QNMT_TC_CASE(BN_, 5) QNMT_TC_CASE(BN_, 6) QNMT_TC_CASE(BN_, 7)
     QNMT_TC_BN8(256) QNMT_TC_BN8(128) QNMT_TC_BN8(64)
     QNMT_TC_BN4(96) QNMT_TC_BN4(160) QNMT_TC_BN4(192) QNMT_TC_BN4(224)
+    QNMT_TC_CASE(64, 9) QNMT_TC_CASE(96, 9) QNMT_TC_CASE(128, 9) QNMT_TC_CASE(160, 9) QNMT_TC_CASE(192, 9)
+    QNMT_TC_CASE(224, 9) QNMT_TC_CASE(256, 9)
 #undef QNMT_TC_BN4
 #undef QNMT_TC_BN8
 #undef QNMT_TC_CASE

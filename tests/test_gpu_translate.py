@@ -258,3 +258,21 @@ def test_vocab_candidates_abi(V, k, dup):
               ct1.data_ptr(), f.data_ptr(), _dev.stream_ptr())
     _dev.raise_flag(f)
     assert torch.equal(ct0, ct1) and torch.equal(cs0, cs1)
+
+
+@pytest.mark.parametrize("query,s0", [("previous", "transform"), ("current", "zero"), ("previous", "zero")])
+def test_engine_variants_stacked(query, s0):
+    """Engine paths with stacked GEMMs (16-aligned dims): previous-state attention
+    query (W_x stacks only) and zero initial state, against the oracle."""
+    d = pb.Dims(150, 333, 48, 64, 80, 32)
+    params = pb.synthetic_model(d, 13, weight_std=0.3, bias_std=0.2, eos_bias=0.4, s0_mode=s0,
+                                attention_query=query)
+    qm = pb.quantize_model(params)
+    om = O.QModel(O.Dims(**d.as_dict()), params.tensors, s0_mode=s0, attention_query=query)
+    rng = np.random.default_rng(len(query) + len(s0))
+    sents = [rng.integers(3, 150, int(rng.integers(1, 18))).tolist() for _ in range(15)]
+    eng = pb.Engine(qm, 16, 32, 6)
+    out = eng.translate_ids(sents, 4, 1.5)
+    for i, s in enumerate(sents):
+        toks, lp = om.translate(s, 4, 1.5)
+        assert out[0][i] == toks and out[1][i] == lp, i
