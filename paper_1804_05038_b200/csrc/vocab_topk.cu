@@ -301,6 +301,32 @@ __device__ __forceinline__ float vt_logits32(const VtMergeArgs& a, const int8_t*
 
 constexpr int VM_WARPS = 4;   // rows per merge CTA (one warp per row)
 
+// (logit desc, token asc) as one descending u64 key: order-preserving f32 bits, then ~token
+__device__ __forceinline__ uint64_t cand_key(float x, int tok) {
+    const uint32_t b = __float_as_uint(x);
+    const uint32_t sb = (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+    return ((uint64_t)sb << 32) | (uint32_t)~(uint32_t)tok;
+}
+__device__ __forceinline__ Cand key_cand(uint64_t k) {
+    const uint32_t sb = (uint32_t)(k >> 32);
+    const uint32_t b = (sb & 0x80000000u) ? (sb & 0x7fffffffu) : ~sb;
+    return k == 0 ? Cand{-DBL_MAX, 0x7fffffff} : Cand{(double)__uint_as_float(b), (int)~(uint32_t)k};
+}
+// bitonic sort of one key per lane, descending (lane 0 = largest); 15 compare-exchange stages
+__device__ __forceinline__ uint64_t warp_sort_desc(uint64_t key) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int k = 2; k <= 32; k <<= 1)
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            const uint64_t other = __shfl_xor_sync(0xffffffffu, key, j);
+            const bool desc = (lane & k) == 0 || k == 32;
+            const bool take_max = ((lane & j) == 0) == desc;
+            key = take_max ? (key > other ? key : other) : (key < other ? key : other);
+        }
+    return key;
+}
+
 template <int KM>
 __global__ void __launch_bounds__(32 * VM_WARPS)
 k_vocab_merge(VtMergeArgs a, int64_t N, const int32_t* n_dev) {
@@ -308,6 +334,8 @@ k_vocab_merge(VtMergeArgs a, int64_t N, const int32_t* n_dev) {
     __shared__ double tab[16];
     __shared__ Cand lst[VM_WARPS][KM];
     __shared__ int flagged[VM_WARPS][VT_RESCAN_MAX];
+    __shared__ uint64_t clist[VM_WARPS][32];
+    __shared__ int ncand[VM_WARPS];
     const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x < 16) tab[threadIdx.x] = exp2((double)threadIdx.x / 16.0);
     __syncthreads();
@@ -357,41 +385,41 @@ k_vocab_merge(VtMergeArgs a, int64_t N, const int32_t* n_dev) {
     const float M = warp_max(ml);
     const double dM = (double)M;
     const double lse = log(warp_sum(ml == -FLT_MAX ? 0.0 : sl * exp_neg((double)ml - dM, tab)));
-    // tau = kk-th best of the 32 lane maxima: at least kk half-tile maxima are >= tau, so every
-    // member of the top-kk is too; only those candidates enter the per-lane lists
-    Cand tau{-DBL_MAX, 0x7fffffff};
-    {
-        Cand mine{ml == -FLT_MAX ? -DBL_MAX : (double)ml, ml == -FLT_MAX ? 0x7fffffff : tl};
-        for (int r = 0; r < kk; ++r) {
-            Cand bst = mine;
-            int bl = lane;
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                const double os = __shfl_xor_sync(0xffffffffu, bst.s, o);
-                const int ot = __shfl_xor_sync(0xffffffffu, bst.t, o);
-                const int ol = __shfl_xor_sync(0xffffffffu, bl, o);
-                const Cand oc{os, ot};
-                if (better(oc, bst) || (!better(bst, oc) && ol < bl)) {
-                    bst = oc;
-                    bl = ol;
-                }
-            }
-            tau = bst;
-            if (lane == bl) mine = Cand{-DBL_MAX, 0x7fffffff};
-        }
-    }
-    Cand L[KM];
-#pragma unroll
-    for (int i = 0; i < KM; ++i) L[i] = Cand{-DBL_MAX, 0x7fffffff};
-    for (int b = lane; b < np; b += 32) {   // pass 2 (L1-resident): the few candidates >= tau
-        const float pm = pr[b].m;
-        if ((double)pm >= tau.s && pm != -FLT_MAX) {
-            const Cand c{(double)pm, pr[b].i1};
-            if (!better(tau, c)) insert<KM>(L, c);
-        }
-    }
-    warp_merge<KM>(L, out, kk);
+    // tau = kk-th best of the 32 lane maxima (bitonic sort of (logit, token) keys): at least kk
+    // group maxima are >= tau, so every member of the top-kk is too
+    const uint64_t tau_key = __shfl_sync(0xffffffffu,
+                                         warp_sort_desc(ml == -FLT_MAX ? 0ull : cand_key(ml, tl)), kk - 1);
+    // pass 2 (L1-resident): the few group maxima with key >= tau -> a per-warp list
+    if (lane == 0) ncand[wib] = 0;
     __syncwarp();
+    for (int b = lane; b < np; b += 32) {
+        const float pm = pr[b].m;
+        if (pm != -FLT_MAX) {
+            const uint64_t k = cand_key(pm, pr[b].i1);
+            if (k >= tau_key) {
+                const int slot = atomicAdd(&ncand[wib], 1);
+                if (slot < 32) clist[wib][slot] = k;
+            }
+        }
+    }
+    __syncwarp();
+    const int nc = ncand[wib];
+    if (nc <= 32) {   // sort the list across the warp: lanes 0..kk-1 hold the top-kk
+        const uint64_t k = warp_sort_desc(lane < nc ? clist[wib][lane] : 0ull);
+        if (lane < kk) out[lane] = key_cand(k);
+    } else {          // many equal logits: per-lane lists and a k-way merge
+        Cand L0[KM];
+#pragma unroll
+        for (int i = 0; i < KM; ++i) L0[i] = Cand{-DBL_MAX, 0x7fffffff};
+        for (int b = lane; b < np; b += 32) {
+            const float pm = pr[b].m;
+            if (pm != -FLT_MAX && cand_key(pm, pr[b].i1) >= tau_key) insert<KM>(L0, Cand{(double)pm, pr[b].i1});
+        }
+        warp_merge<KM>(L0, out, kk);
+    }
+    __syncwarp();
+    const Cand tau = key_cand(tau_key);
+    Cand L[KM];
     // half-tiles whose runner-up reaches the KM-th value may hold more of the top-KM
     const Cand thr = out[kk - 1];
     int nf = 0;
