@@ -254,10 +254,10 @@ k_att_score4(const float* __restrict__ u, int64_t ldu, const int32_t* __restrict
 // t owns a-quads 4t + 4*AT*k; quads past A are zero (no bounds checks in the
 // hot loop).  Warps store their per-position sums in shared memory and the last
 // warp to finish writes the scores (no end-of-CTA barrier wait).
-constexpr int APC5 = 8;        // positions per CTA
+constexpr int APC5 = 6;        // positions per CTA (48 KB of tile slices: 4 CTAs / SM)
 constexpr int AQ5 = 2;         // a-quads per thread (A <= 4 * AT * AQ5 = 2048)
 
-__global__ void __launch_bounds__(AT, 3)
+__global__ void __launch_bounds__(AT, 4)
 k_att_score5(const float* __restrict__ u, int64_t ldu, const int32_t* __restrict__ sent_col_off,
              const int32_t* __restrict__ sent_ncols, const float* __restrict__ att_proj,
              const float2* __restrict__ st_thr, const int64_t* __restrict__ sent_row,
@@ -582,7 +582,7 @@ int attention_launch(const float* u, int64_t ldu, int64_t N, const int32_t* sent
     if (quads) {   // smem-staged tile, 3 CTAs / SM
         const size_t smem5 = (size_t)APC5 * AQ5 * AT * sizeof(float4);
         static size_t done = 0;
-        if (smem5 > 48 * 1024 && smem5 > done) {
+        if (smem5 > done) {   // (dynamic + static > 48 KB needs the opt-in)
             QNMT_CUDA(cudaFuncSetAttribute(k_att_score5, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem5));
             done = smem5;
         }
