@@ -65,6 +65,20 @@ def gemm_case(name, M, K, N, seg_count=256):
             "GBps": nbytes / t / 1e9}
 
 
+def int_mm_case(M, K, N):
+    """cuBLASLt int8 GEMM (torch._int_mm, int32 out) on the same shape: the library ceiling."""
+    a = torch.randint(-127, 128, (N, K), dtype=torch.int8, device="cuda")
+    b = torch.randint(-127, 128, (M, K), dtype=torch.int8, device="cuda").t()
+    c = torch.empty((N, M), dtype=torch.int32, device="cuda")
+    try:
+        t = graph_time(lambda: torch._int_mm(a, b, out=c), reps=5)
+    except Exception as ex:   # noqa: BLE001
+        return {"kernel": "cublasLt int8 (torch._int_mm)", "M": M, "N": N, "K": K, "error": str(ex)[:200]}
+    ops = 2.0 * M * N * K
+    return {"kernel": "cublasLt int8 (torch._int_mm)", "M": M, "N": N, "K": K, "us": t * 1e6, "TOPS": ops / t / 1e12,
+            "tensor_frac_of_spec": ops / t / 1e12 / PEAK["int8_tops_spec"]}
+
+
 def topk_case(N=1280, V=50000, k=5):
     x = torch.randn((N, V), device="cuda") * 0.2
     live = torch.randn(N, dtype=torch.float64, device="cuda")
@@ -158,14 +172,17 @@ def gemv_cold(bsz):
     Y = torch.empty((bsz, 3072), dtype=torch.float32, device="cuda")
     it = iter(range(10 ** 9))
 
-    def run():
+    def run(static):
         for c in copies:
-            pb.qmath.gemm_kmajor(c, ws, 3072, X, xs, Y=Y)
-    t = graph_time(run, reps=1) / len(copies)
+            pb.qmath.gemm_kmajor(c, ws, 3072, X, xs, Y=Y, w_static=static)
+    t_iso = graph_time(lambda: run(False), reps=1) / len(copies)
+    t = graph_time(lambda: run(True), reps=1) / len(copies)
     nbytes = 3072 * 1024 + 4 * 1024 * bsz + 4 * 3072 * bsz
     return {"kernel": "cfg1 qgemm_panel", "B": bsz, "us": t * 1e6, "GBps": nbytes / t / 1e9,
             "hbm_frac_of_measured": nbytes / t / 1e9 / PEAK["hbm_gbs"], "TOPS": 2 * 3072 * 1024 * bsz / t / 1e12,
-            "note": "64 rotating weight copies (201 MB > 126 MB L2)"}
+            "us_no_prefetch": t_iso * 1e6, "GBps_no_prefetch": nbytes / t_iso / 1e9,
+            "note": "64 rotating weight copies (201 MB > 126 MB L2) in one CUDA graph; 'us' with the PDL weight "
+                    "prefetch (W streams while the previous product drains), 'us_no_prefetch' without"}
 
 
 def main():
@@ -179,6 +196,10 @@ def main():
             out.append(gemm_case(name, M, K, N))
         out.append(gemm_case("enc x-side", 3072, 512, 13000, 13000))
         out.append(gemm_case("enc Uzr", 2048, 1024, 256))
+    if "big" in which:   # tensor-bound shapes: tcgen05 K3 vs cuBLASLt int8 (torch._int_mm) as the measured ceiling
+        for M, N, K in [(8192, 8192, 8192), (16384, 8192, 4096), (50000, 1280, 512)]:
+            out.append(gemm_case(f"big {M}x{N}x{K}", M, K, N))
+            out.append(int_mm_case(M, K, N))
     if "topk" in which:
         out.append(topk_case())
     if "vocab" in which:

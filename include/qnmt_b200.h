@@ -95,6 +95,10 @@ int qnmt_dequantize(const int8_t* q, int64_t n, float scale, float* y, void* str
  * seg(n) = col_seg[n] (col_seg NULL -> 0).  Scales are device f32 arrays.
  * ------------------------------------------------------------------------- */
 #define QNMT_GEMM_ACCUMULATE 1
+/* W is not written by the kernels immediately preceding this call on the stream
+ * (model weights): the CUDA-core GEMV may stream W before its programmatic-
+ * dependent-launch wait, overlapping the predecessor kernel. */
+#define QNMT_GEMM_W_STATIC 2
 int qnmt_gemm_i8(const int8_t* W, int64_t M, int64_t K, int64_t ldw,
                  const float* w_scales, int64_t w_rows_per_scale,
                  const int8_t* X, int64_t N, int64_t ldx,

@@ -30,7 +30,10 @@ from .model import (
     ModelParams,
     QuantizedModel,
     generate_model,
+    load_model,
+    load_quantized,
     quantize_model,
+    save_model,
     synthetic_model,
     tensor_specs,
 )
@@ -50,7 +53,7 @@ __all__ = [
     "AttentionNet", "BeamHypothesis", "DecodeConfig", "DecoderState", "Dims", "EncoderStates",
     "Engine", "GruCell", "INT8_MAX", "INT32_SAFE_K", "LinearOp", "ModelParams", "Network",
     "OutputNet", "QuantizationStats", "QuantizedMatrix", "QuantizedModel", "attend", "bpe_merge",
-    "build_network", "dequantize", "errors", "generate_model", "gru_step", "qgemm", "qgemm_panel",
-    "quantize", "quantize_activations", "quantize_model", "synthetic_model", "tensor_specs",
+    "build_network", "dequantize", "errors", "generate_model", "gru_step", "load_model", "load_quantized", "qgemm", "qgemm_panel",
+    "quantize", "quantize_activations", "quantize_model", "save_model", "synthetic_model", "tensor_specs",
     "translate", "translate_batch",
 ]

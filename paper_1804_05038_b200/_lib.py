@@ -63,6 +63,7 @@ SIGNATURES = {
 QNMT_OK, ERR_SHAPE, ERR_INVALID, ERR_NUMERIC, ERR_VOCAB, ERR_CONFIG, ERR_EMPTY, ERR_CUDA = range(8)
 FLAG_NUMERIC, FLAG_INVALID, FLAG_VOCAB = 1, 2, 4
 GEMM_ACCUMULATE = 1
+GEMM_W_STATIC = 2
 INT32_SAFE_K = 131_000
 
 _EXC = {

@@ -257,7 +257,7 @@ static int gemm(const int8_t* W, int64_t M, int64_t K, const float* ws, int64_t 
                 int64_t N, int64_t ldx, const float* xs, const int32_t* seg, const float* bias, float* Y,
                 int64_t ldy, int32_t flags, cudaStream_t st, const float* add1 = nullptr, int64_t ld1 = 0,
                 const float* add2 = nullptr, int64_t ld2 = 0) {
-    GemmArgs g{W, M, K, K, ws, rps, X, N, ldx, xs, seg, bias, Y, ldy, nullptr, flags};
+    GemmArgs g{W, M, K, K, ws, rps, X, N, ldx, xs, seg, bias, Y, ldy, nullptr, flags | QNMT_GEMM_W_STATIC};
     g.add1 = add1;
     g.ld1 = ld1;
     g.add2 = add2;

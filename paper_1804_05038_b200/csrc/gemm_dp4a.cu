@@ -58,24 +58,17 @@ __device__ __forceinline__ int dp4a16(int acc, const int4& a, const int4& b) {
 template <int ROWS, int NC>
 __global__ void __launch_bounds__(256)
 k_gemv(const int8_t* __restrict__ W, int64_t M, int64_t K, int64_t ldw,
-       const int8_t* __restrict__ X, int64_t ldx, EpiArgs e) {
+       const int8_t* __restrict__ X, int64_t ldx, EpiArgs e, int w_static) {
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
     const int64_t row0 = ((int64_t)blockIdx.x * 8 + warp) * ROWS;
-    if (row0 >= M) return;
     const int64_t nch = K >> 4;   // 16-byte chunks per row
-    int acc[ROWS][NC];
-#pragma unroll
-    for (int r = 0; r < ROWS; ++r)
-#pragma unroll
-        for (int j = 0; j < NC; ++j) acc[r][j] = 0;
-
-    constexpr int U = 2;   // chunk-iterations whose loads are issued together
-    for (int64_t c0 = lane; c0 < nch; c0 += 32 * U) {
-        int4 w[U][ROWS];
+    constexpr int U = 2;          // chunk-iterations whose loads are issued together
+    int4 w[U][ROWS];
+    auto load_w = [&](int64_t c0) {
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            int64_t c = c0 + 32 * u;
+            const int64_t c = c0 + 32 * u;
 #pragma unroll
             for (int r = 0; r < ROWS; ++r) {
                 if (c < nch && row0 + r < M)
@@ -84,9 +77,31 @@ k_gemv(const int8_t* __restrict__ W, int64_t M, int64_t K, int64_t ldw,
                     w[u][r] = make_int4(0, 0, 0, 0);
             }
         }
+    };
+    // PDL: model weights (w_static) do not depend on the predecessor kernel, so the
+    // first weight chunks stream from HBM while the predecessor drains; X and the
+    // epilogue operands are touched only after griddepcontrol.wait.  The early trigger
+    // lets a following GEMV start its own weight stream in turn (its wait still
+    // orders it after this grid's completion).
+    pdl_trigger();
+    if (w_static) {
+        load_w(lane);
+        pdl_wait();
+    } else {
+        pdl_wait();
+        load_w(lane);
+    }
+    if (row0 >= M) return;
+    int acc[ROWS][NC];
+#pragma unroll
+    for (int r = 0; r < ROWS; ++r)
+#pragma unroll
+        for (int j = 0; j < NC; ++j) acc[r][j] = 0;
+
+    for (int64_t c0 = lane; c0 < nch; c0 += 32 * U) {
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            int64_t c = c0 + 32 * u;
+            const int64_t c = c0 + 32 * u;
             if (c < nch) {
 #pragma unroll
                 for (int j = 0; j < NC; ++j) {
@@ -96,6 +111,7 @@ k_gemv(const int8_t* __restrict__ W, int64_t M, int64_t K, int64_t ldw,
                 }
             }
         }
+        if (c0 + 32 * U < nch) load_w(c0 + 32 * U);
     }
 #pragma unroll
     for (int r = 0; r < ROWS; ++r)
@@ -187,24 +203,26 @@ __global__ void k_gemm_generic(const int8_t* __restrict__ W, int64_t M, int64_t 
 }
 
 template <int ROWS, int NC>
-static void launch_gemv(const int8_t* W, int64_t M, int64_t K, int64_t ldw, const int8_t* X,
-                        int64_t ldx, const EpiArgs& e, cudaStream_t st) {
+static int launch_gemv(const int8_t* W, int64_t M, int64_t K, int64_t ldw, const int8_t* X,
+                       int64_t ldx, const EpiArgs& e, cudaStream_t st) {
     unsigned grid = (unsigned)cdiv(M, 8 * ROWS);
-    k_gemv<ROWS, NC><<<grid, 256, 0, st>>>(W, M, K, ldw, X, ldx, e);
+    const int w_static = (e.flags & QNMT_GEMM_W_STATIC) ? 1 : 0;
+    QNMT_LAUNCH(k_gemv<ROWS, NC>, grid, 256, 0, st, W, M, K, ldw, X, ldx, e, w_static);
+    return QNMT_OK;
 }
 
 template <int ROWS>
-static void dispatch_gemv(int64_t N, const int8_t* W, int64_t M, int64_t K, int64_t ldw,
-                          const int8_t* X, int64_t ldx, const EpiArgs& e, cudaStream_t st) {
+static int dispatch_gemv(int64_t N, const int8_t* W, int64_t M, int64_t K, int64_t ldw,
+                         const int8_t* X, int64_t ldx, const EpiArgs& e, cudaStream_t st) {
     switch (N) {
-        case 1: launch_gemv<ROWS, 1>(W, M, K, ldw, X, ldx, e, st); break;
-        case 2: launch_gemv<ROWS, 2>(W, M, K, ldw, X, ldx, e, st); break;
-        case 3: launch_gemv<ROWS, 3>(W, M, K, ldw, X, ldx, e, st); break;
-        case 4: launch_gemv<ROWS, 4>(W, M, K, ldw, X, ldx, e, st); break;
-        case 5: launch_gemv<ROWS, 5>(W, M, K, ldw, X, ldx, e, st); break;
-        case 6: launch_gemv<ROWS, 6>(W, M, K, ldw, X, ldx, e, st); break;
-        case 7: launch_gemv<ROWS, 7>(W, M, K, ldw, X, ldx, e, st); break;
-        default: launch_gemv<ROWS, 8>(W, M, K, ldw, X, ldx, e, st); break;
+        case 1: return launch_gemv<ROWS, 1>(W, M, K, ldw, X, ldx, e, st);
+        case 2: return launch_gemv<ROWS, 2>(W, M, K, ldw, X, ldx, e, st);
+        case 3: return launch_gemv<ROWS, 3>(W, M, K, ldw, X, ldx, e, st);
+        case 4: return launch_gemv<ROWS, 4>(W, M, K, ldw, X, ldx, e, st);
+        case 5: return launch_gemv<ROWS, 5>(W, M, K, ldw, X, ldx, e, st);
+        case 6: return launch_gemv<ROWS, 6>(W, M, K, ldw, X, ldx, e, st);
+        case 7: return launch_gemv<ROWS, 7>(W, M, K, ldw, X, ldx, e, st);
+        default: return launch_gemv<ROWS, 8>(W, M, K, ldw, X, ldx, e, st);
     }
 }
 
@@ -229,10 +247,9 @@ int gemm_i8_launch(const GemmArgs& g, cudaStream_t st) {
         return QNMT_OK;
     }
     if (g.N <= 8) {
-        if (g.K <= 512)
-            dispatch_gemv<4>(g.N, g.W, g.M, g.K, g.ldw, g.X, g.ldx, e, st);
-        else
-            dispatch_gemv<2>(g.N, g.W, g.M, g.K, g.ldw, g.X, g.ldx, e, st);
+        int rc = g.K <= 512 ? dispatch_gemv<4>(g.N, g.W, g.M, g.K, g.ldw, g.X, g.ldx, e, st)
+                            : dispatch_gemv<2>(g.N, g.W, g.M, g.K, g.ldw, g.X, g.ldx, e, st);
+        if (rc != QNMT_OK) return rc;
         QNMT_CHECK_LAUNCH("k_gemv");
         return QNMT_OK;
     }
@@ -249,7 +266,8 @@ int gemm_i8_launch(const GemmArgs& g, cudaStream_t st) {
         if (e2.Y) e2.Y += n0 * g.ldy;
         if (e2.acc_out) e2.acc_out += n0 * g.M;
         if (e2.col_seg) e2.col_seg += n0;
-        dispatch_gemv<2>(nn, g.W, g.M, g.K, g.ldw, g.X + n0 * g.ldx, g.ldx, e2, st);
+        const int rc = dispatch_gemv<2>(nn, g.W, g.M, g.K, g.ldw, g.X + n0 * g.ldx, g.ldx, e2, st);
+        if (rc != QNMT_OK) return rc;
         QNMT_CHECK_LAUNCH("k_gemv(panel)");
     }
     return QNMT_OK;

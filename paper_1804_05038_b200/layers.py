@@ -116,7 +116,8 @@ class LinearOp:
             raise ConfigError("the B200 path implements int8 LinearOps only")
         q, sx = _quant_k(x_k, col_seg, nseg)
         return gemm_kmajor(self.weight.device_data(), self.weight.device_scale(), self.out_dim, q, sx,
-                           col_seg=col_seg, bias=self._bias_dev(), Y=out, accumulate=accumulate)
+                           col_seg=col_seg, bias=self._bias_dev(), Y=out, accumulate=accumulate,
+                           w_static=True)
 
     def apply(self, x, timer=None):
         if len(np.shape(x)) != 2 or np.shape(x)[0] != self.in_dim:
@@ -174,8 +175,8 @@ def gru_step_k(cell: GruCell, x_k: torch.Tensor, h_k: torch.Tensor, col_seg=None
     P = x_k.shape[0]
     qx, sx = _quant_k(x_k, col_seg, nseg)
     qh, sh = _quant_k(h_k, col_seg, nseg)
-    gx = gemm_kmajor(wx, wxs, H, qx, sx, col_seg=col_seg, bias=bx)           # [P][3H]
-    gh = gemm_kmajor(uzr, uzrs, H, qh, sh, col_seg=col_seg)                  # [P][2H]
+    gx = gemm_kmajor(wx, wxs, H, qx, sx, col_seg=col_seg, bias=bx, w_static=True)   # [P][3H]
+    gh = gemm_kmajor(uzr, uzrs, H, qh, sh, col_seg=col_seg, w_static=True)   # [P][2H]
     z = torch.empty((P, H), dtype=torch.float32, device=x_k.device)
     rh = torch.empty_like(z)
     flag = _dev.flag()
@@ -183,7 +184,7 @@ def gru_step_k(cell: GruCell, x_k: torch.Tensor, h_k: torch.Tensor, col_seg=None
     _lib.call("qnmt_gru_gates", gx.data_ptr(), 3 * H, None, gh.data_ptr(), 2 * H, h_k.data_ptr(),
               _dev.ld(h_k), P, H, z.data_ptr(), rh.data_ptr(), flag.data_ptr(), st)
     qr, sr = _quant_k(rh, col_seg, nseg)
-    ghc = gemm_kmajor(uc, ucs, H, qr, sr, col_seg=col_seg)                   # [P][H]
+    ghc = gemm_kmajor(uc, ucs, H, qr, sr, col_seg=col_seg, w_static=True)    # [P][H]
     out = torch.empty_like(z)
     _lib.call("qnmt_gru_combine", gx.data_ptr(), 3 * H, None, ghc.data_ptr(), H, z.data_ptr(),
               h_k.data_ptr(), _dev.ld(h_k), P, H, out.data_ptr(), H, None, 0, None, flag.data_ptr(), st)

@@ -1,9 +1,15 @@
-"""Parameter containers, synthetic models and on-device weight quantization.
+"""Parameter containers, the QNMT model file, synthetic models and on-device
+weight quantization.
 
 Mirrors the reference ``model.py``: :class:`Dims` (:42-52), the canonical
 tensor directory :func:`tensor_specs` (:151-177), :class:`ModelParams`
 (fp32), :class:`QuantizedModel` (int8 codes + one f32 scale per tensor,
-embeddings and biases fp32, :394-437) and the seeded generators.
+embeddings and biases fp32, :394-437), the seeded generators, and the binary
+format (:1-17, ``save_model`` :275-310, ``load_model`` :313-387).
+
+:func:`load_quantized` is the B200 loader: it validates the file on the host,
+moves the whole payload to HBM in one copy and quantizes every weight matrix
+there, so no per-tensor host work sits between the file and the engine.
 
 B200 layout: :func:`quantize_model` uploads the fp32 tensors once, quantizes
 every weight matrix with the device K1 kernel (bit-identical to the
@@ -16,15 +22,19 @@ device tensors are referenced by the C engine handle (``qnmt_model_create``).
 from __future__ import annotations
 
 import ctypes as C
+import hashlib
+import json
 from dataclasses import dataclass, field
 
 import numpy as np
 import torch
 
 from . import _dev, _lib
-from .errors import ParameterError
+from .errors import FormatError, ParameterError, SchemaError
 from .qmath import QuantizedMatrix, quantization_stats, quantize
 
+MAGIC = b"QNMT"
+VERSION = 1
 PAD_ID, UNK_ID, EOS_ID = 0, 1, 2
 PAD_TOKEN, UNK_TOKEN, EOS_TOKEN = "<pad>", "<unk>", "</s>"
 DEFAULT_WEIGHT_SCALE = 0.08
@@ -238,19 +248,163 @@ class QuantizedModel:
             pass
 
 
-def quantize_model(params: ModelParams, with_stats: bool = False) -> QuantizedModel:
-    """Quantize every weight matrix once on the device (model.py:394-437);
-    biases and embeddings stay f32 (uploaded)."""
+def _quantize_tensors(dims: Dims, tensors: dict, src_tokens, tgt_tokens, s0_mode, attention_query,
+                      with_stats: bool) -> QuantizedModel:
     q, f, stats = {}, {}, {}
-    for name, shape in tensor_specs(params.dims):
-        arr = params.tensors[name]
+    for name, shape in tensor_specs(dims):
+        arr = tensors[name]
+        if isinstance(arr, torch.Tensor):
+            dev = arr
+        else:
+            dev = _dev.to_device(np.ascontiguousarray(arr, dtype=np.float32))
         if len(shape) == 2 and name not in ("src_embed", "tgt_embed"):
-            dev = _dev.to_device(np.ascontiguousarray(arr, dtype=np.float32)).contiguous()
+            dev = dev.contiguous()
             qm = quantize(dev)
             q[name] = qm
             if with_stats:
                 stats[name] = quantization_stats(name, dev, qm)
+        else:   # own allocation (not a view of a loader buffer): 16-byte aligned rows for the fused kernels
+            f[name] = dev.clone() if isinstance(arr, torch.Tensor) and arr._base is not None else dev.contiguous()
+    return QuantizedModel(dims, q, f, src_tokens, tgt_tokens, s0_mode, attention_query, stats)
+
+
+def quantize_model(params: ModelParams, with_stats: bool = False) -> QuantizedModel:
+    """Quantize every weight matrix once on the device (model.py:394-437);
+    biases and embeddings stay f32 (uploaded)."""
+    return _quantize_tensors(params.dims, params.tensors, params.src_tokens, params.tgt_tokens,
+                             params.s0_mode, params.attention_query, with_stats)
+
+
+# ---------------------------------------------------------------------------
+# QNMT model file (model.py:1-17): "QNMT", u32 version, u64 header length,
+# JSON header, f32 payload (C order, spec order), 8-byte SHA-256 prefix of the
+# payload.  Little-endian throughout.
+# ---------------------------------------------------------------------------
+
+_HEADER_KEYS = ("dims", "s0_mode", "attention_query", "source_vocab", "target_vocab",
+                "payload_bytes", "tensors")
+
+
+def _u(blob, lo, hi) -> int:
+    return int.from_bytes(blob[lo:hi], "little")
+
+
+def save_model(params: ModelParams, path: str) -> None:
+    """Write the canonical byte-exact QNMT file (model.py:275-310): tensors in
+    ``tensor_specs`` order, compact sorted-key JSON header, SHA-256 checksum."""
+    raw, directory, at = [], [], 0
+    for name, shape in tensor_specs(params.dims):
+        arr = params.tensors[name]
+        if isinstance(arr, torch.Tensor):
+            arr = arr.detach().cpu().numpy()
+        arr = np.ascontiguousarray(arr, dtype="<f4")
+        if tuple(arr.shape) != tuple(shape):
+            raise SchemaError(f"tensor {name} has shape {arr.shape}, expected {shape}")
+        directory.append({"name": name, "shape": list(shape), "offset": at})
+        raw.append(arr.tobytes())
+        at += arr.nbytes
+    payload = b"".join(raw)
+    header = json.dumps({"dims": params.dims.as_dict(), "s0_mode": params.s0_mode,
+                         "attention_query": params.attention_query,
+                         "source_vocab": params.src_tokens, "target_vocab": params.tgt_tokens,
+                         "payload_bytes": len(payload), "tensors": directory},
+                        sort_keys=True, separators=(",", ":")).encode("utf-8")
+    with open(path, "wb") as fh:
+        fh.write(MAGIC + VERSION.to_bytes(4, "little") + len(header).to_bytes(8, "little"))
+        fh.write(header)
+        fh.write(payload)
+        fh.write(hashlib.sha256(payload).digest()[:8])
+
+
+def _parse_model_file(blob: bytes):
+    """Validate a QNMT file (model.py:313-387, same checks, messages and byte
+    offsets).  Returns (dims, header, payload memoryview, {name: (offset, shape)})."""
+    n = len(blob)
+    if n < 16:
+        raise FormatError("file shorter than the fixed header", offset=n)
+    if blob[:4] != MAGIC:
+        raise FormatError(f"bad magic {blob[:4]!r}, expected {MAGIC!r}", offset=0)
+    version = _u(blob, 4, 8)
+    if version != VERSION:
+        raise FormatError(f"unsupported format version {version}", offset=4)
+    hdr_end = 16 + _u(blob, 8, 16)
+    if hdr_end + 8 > n:
+        raise FormatError("declared header overruns the file", offset=8)
+    try:
+        header = json.loads(blob[16:hdr_end].decode("utf-8"))
+    except (UnicodeDecodeError, json.JSONDecodeError) as exc:
+        raise FormatError(f"header is not valid JSON: {exc}", offset=16) from None
+    missing = [k for k in _HEADER_KEYS if k not in header]
+    if missing:
+        raise SchemaError(f"header is missing required key {missing[0]!r}", offset=16)
+    try:
+        dims = Dims(**header["dims"])
+    except TypeError as exc:
+        raise SchemaError(f"bad dims block: {exc}", offset=16) from None
+    plen = int(header["payload_bytes"])
+    pend = hdr_end + plen
+    if pend + 8 > n:
+        raise FormatError("payload truncated", offset=min(n, pend))
+    payload = memoryview(blob)[hdr_end:pend]
+    if hashlib.sha256(payload).digest()[:8] != blob[pend:pend + 8]:
+        raise FormatError("payload checksum mismatch", offset=pend)
+    for key, declared, what in (("source_vocab", dims.src_vocab, "source"),
+                                ("target_vocab", dims.tgt_vocab, "target")):
+        if len(header[key]) != declared:
+            raise SchemaError(f"{what} vocabulary lists {len(header[key])} tokens, dims declare {declared}",
+                              offset=16)
+    want = {name: tuple(shape) for name, shape in tensor_specs(dims)}
+    entries = {e["name"]: e for e in header["tensors"]}
+    if set(entries) != set(want):
+        raise SchemaError(f"tensor directory mismatch (missing {sorted(set(want) - set(entries))}, "
+                          f"extra {sorted(set(entries) - set(want))})", offset=16)
+    layout = {}
+    for name, shape in want.items():
+        ent = entries[name]
+        if tuple(ent["shape"]) != shape:
+            raise SchemaError(f"tensor {name} declares shape {ent['shape']}, dims imply {shape}", offset=16)
+        off = int(ent["offset"])
+        if off < 0 or off + 4 * int(np.prod(shape)) > plen:
+            raise SchemaError(f"tensor {name} overruns the payload", offset=hdr_end + max(off, 0))
+        layout[name] = (off, shape)
+    return dims, header, payload, layout
+
+
+def load_model(path: str) -> ModelParams:
+    """Read and validate a QNMT model file into host f32 tensors (model.py:313-387);
+    tensors are read-only views of the file bytes, as in the reference."""
+    with open(path, "rb") as fh:
+        blob = fh.read()
+    dims, header, payload, layout = _parse_model_file(blob)
+    tensors = {name: np.frombuffer(payload, dtype="<f4", count=int(np.prod(shape)), offset=off).reshape(shape)
+               for name, (off, shape) in layout.items()}
+    return ModelParams(dims, tensors, list(header["source_vocab"]), list(header["target_vocab"]),
+                       header["s0_mode"], header["attention_query"])
+
+
+def load_quantized(path: str, with_stats: bool = False) -> QuantizedModel:
+    """QNMT file -> device-resident int8 model.
+
+    The file is validated on the host exactly like :func:`load_model`; the
+    payload then crosses PCIe once (pinned staging, one H2D copy) and every
+    tensor is a view of that device buffer: weight matrices are quantized by
+    the device K1 kernel (bit-identical to ``quantize_model(load_model(path))``),
+    embeddings and biases are used in place."""
+    with open(path, "rb") as fh:
+        blob = fh.read()
+    dims, header, payload, layout = _parse_model_file(blob)
+    dev = _dev.require_cuda()
+    host = torch.empty(len(payload), dtype=torch.uint8, pin_memory=True)
+    host.numpy()[:] = np.frombuffer(payload, dtype=np.uint8)
+    buf = torch.empty(len(payload) + 16, dtype=torch.uint8, device=dev)
+    buf[:len(payload)].copy_(host, non_blocking=True)
+    views = {}
+    for name, (off, shape) in layout.items():
+        nbytes = 4 * int(np.prod(shape))
+        if off % 4:   # unaligned directory entry (legal in the format): realign on the device
+            views[name] = buf[off:off + nbytes].clone().view(torch.float32).view(shape)
         else:
-            f[name] = _dev.to_device(np.ascontiguousarray(arr, dtype=np.float32)).contiguous()
-    return QuantizedModel(params.dims, q, f, params.src_tokens, params.tgt_tokens, params.s0_mode,
-                          params.attention_query, stats)
+            views[name] = buf[off:off + nbytes].view(torch.float32).view(shape)
+    torch.cuda.current_stream().synchronize()   # the pinned staging buffer is released on return
+    return _quantize_tensors(dims, views, list(header["source_vocab"]), list(header["target_vocab"]),
+                             header["s0_mode"], header["attention_query"], with_stats)

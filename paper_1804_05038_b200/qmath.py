@@ -177,8 +177,10 @@ def _check_pair(a, b):
 
 def gemm_kmajor(W: torch.Tensor, w_scales: torch.Tensor, rows_per_scale: int, X: torch.Tensor,
                 x_scales: torch.Tensor, col_seg=None, bias=None, Y=None, accumulate=False,
-                acc_out=None) -> torch.Tensor:
-    """Device GEMM in kernel layout: Y[N][M] from W[M][K] and K-major X[N][K]."""
+                acc_out=None, w_static=False) -> torch.Tensor:
+    """Device GEMM in kernel layout: Y[N][M] from W[M][K] and K-major X[N][K].
+    ``w_static``: W is a model weight (not produced by the preceding kernels), so
+    the GEMV may prefetch it before its programmatic-dependent-launch wait."""
     M, K = W.shape
     N = X.shape[0]
     if X.shape[1] != K:
@@ -188,7 +190,8 @@ def gemm_kmajor(W: torch.Tensor, w_scales: torch.Tensor, rows_per_scale: int, X:
     _lib.call("qnmt_gemm_i8", W.data_ptr(), M, K, _dev.ld(W), w_scales.data_ptr(), rows_per_scale,
               X.data_ptr(), N, _dev.ld(X), x_scales.data_ptr(), _dev.ptr(col_seg), _dev.ptr(bias),
               _dev.ptr(Y), _dev.ld(Y) if Y is not None else M, _dev.ptr(acc_out),
-              _lib.GEMM_ACCUMULATE if accumulate else 0, _dev.stream_ptr())
+              (_lib.GEMM_ACCUMULATE if accumulate else 0) | (_lib.GEMM_W_STATIC if w_static else 0),
+              _dev.stream_ptr())
     return Y
 
 

@@ -323,8 +323,42 @@ def gen_baseline():
     print("baseline_dims.npz:", len(out), "arrays")
 
 
+MODELFILE_ARGS = dict(src_vocab=14, tgt_vocab=13, embed=4, hidden=6, seed=11, attn=5, readout=3)
+
+
+def gen_modelfile():
+    """A QNMT file written by the reference's save_model, and the reference
+    loader's verdict (exception type, byte offset) on each corruption of it."""
+    import tempfile
+
+    import modelfile_cases
+    from qnmt import errors as ref_errors
+
+    params = ref_model.generate_model(**MODELFILE_ARGS)
+    path = os.path.join(HERE, "model_tiny.qnmt")
+    ref_model.save_model(params, path)
+    blob = open(path, "rb").read()
+    verdicts = {"generate_model_args": MODELFILE_ARGS, "file_sha256": hashlib.sha256(blob).hexdigest(),
+                "cases": {}}
+    with tempfile.TemporaryDirectory() as d:
+        for name, data in modelfile_cases.cases(blob).items():
+            p = os.path.join(d, name)
+            with open(p, "wb") as fh:
+                fh.write(data)
+            try:
+                ref_model.load_model(p)
+                verdicts["cases"][name] = {"error": None}
+            except ref_errors.QnmtError as exc:
+                verdicts["cases"][name] = {"error": type(exc).__name__, "offset": getattr(exc, "offset", None)}
+    with open(os.path.join(HERE, "model_tiny_errors.json"), "w") as fh:
+        json.dump(verdicts, fh, indent=1, sort_keys=True)
+    print("model_tiny.qnmt:", len(blob), "bytes;", len(verdicts["cases"]), "corruption verdicts")
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["qmath", "small", "baseline"]
+    which = sys.argv[1:] or ["qmath", "small", "baseline", "modelfile"]
+    if "modelfile" in which:
+        gen_modelfile()
     if "qmath" in which:
         gen_qmath()
     if "small" in which:
