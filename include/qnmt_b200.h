@@ -257,6 +257,21 @@ int qnmt_translate_batch(qnmt_engine* e, const int32_t* src_ids, const int32_t* 
                          int32_t* out_tokens, int32_t out_stride, int32_t* out_len,
                          double* out_logp, void* stream);
 
+/* Ensemble translation (decoder.py:88-160 with several models, :115-120):
+ * per step every member runs its own decoder step on its own states; the
+ * per-column log-probs are summed in member order in f32 and divided by
+ * f32(n_members); search state lives in engines[0].  Every engine must come
+ * from a model with the same target vocabulary size and have the same
+ * capacity.  src_ids holds n_members x sum(src_len) ids, member-major (each
+ * member maps the tokens with its own source vocabulary, decoder.py:99).
+ * 1 <= n_members <= QNMT_ENS_MAX (1 = qnmt_translate_batch).  Same outputs as
+ * qnmt_translate_batch (replaces decoder.py:115-120 for ensembles). */
+#define QNMT_ENS_MAX 8
+int qnmt_translate_ensemble(qnmt_engine* const* engines, int32_t n_members, const int32_t* src_ids,
+                            const int32_t* src_len, int32_t n_sent, int32_t beam, double max_ratio,
+                            int32_t* out_tokens, int32_t out_stride, int32_t* out_len,
+                            double* out_logp, void* stream);
+
 /* Encoder only (layers.py:313-348) for a batch, device in/out:
  *   src_ids (device) concatenated, sent_row (host) row offsets, src_len (host).
  *   states [sum_l][2H] (backward half first, layers.py:342), att_proj [sum_l][A],

@@ -332,50 +332,63 @@ class QModel:
     # decoder.py:88-160 (single model)
     def translate(self, src_ids, beam=5, max_ratio=3.0):
         """Returns (token ids without final EOS, log_prob)."""
-        src_ids = list(src_ids)
-        if not src_ids:
-            raise OracleError("empty", "cannot translate an empty sentence")
-        if beam < 1 or not max_ratio > 0:
-            raise OracleError("config", "bad decode config")
-        vocab = self.dims.tgt_vocab
-        enc = self.encode(src_ids)
-        max_steps = math.ceil(max_ratio * len(src_ids)) + 1
-        live_tokens = [[]]
-        live_scores = np.zeros(1, dtype=F64)
-        s0 = enc[2]
-        s, s_prime = s0.copy(), s0.copy()
-        y_prev = np.array([EOS_ID], dtype=np.int64)
-        finished = []   # (tokens, score)
-        for _ in range(max_steps):
-            lp, s_new, s_int, _ = self.decoder_step(y_prev, s, s_prime, enc)
-            flat = (live_scores[:, None] + lp.T.astype(F64)).ravel()
-            chosen = select_candidates(flat, beam, vocab)
-            nt, ns, npar, nid = [], [], [], []
-            for f in chosen:
-                parent, tok = divmod(f, vocab)
-                score = float(flat[f])
-                if tok == EOS_ID:
-                    finished.append((live_tokens[parent] + [tok], score))
-                else:
-                    nt.append(live_tokens[parent] + [tok])
-                    ns.append(score)
-                    npar.append(parent)
-                    nid.append(tok)
-            if not nt:
-                break
-            live_tokens = nt
-            live_scores = np.array(ns, dtype=F64)
-            pidx = np.array(npar, dtype=np.int64)
-            s, s_prime = np.ascontiguousarray(s_new[:, pidx]), np.ascontiguousarray(s_int[:, pidx])
-            y_prev = np.array(nid, dtype=np.int64)
-            if finished and max(h[1] for h in finished) >= live_scores.max():
-                break
-        else:
-            for toks, score in zip(live_tokens, live_scores):
-                finished.append((list(toks), float(score)))
-        best = min(finished, key=lambda h: (-h[1], h[0]))
-        toks = best[0][:-1] if best[0] and best[0][-1] == EOS_ID else best[0]
-        return toks, best[1]
+        return translate_ensemble([self], [src_ids], beam, max_ratio)
+
+
+def translate_ensemble(models, src_ids_per_member, beam=5, max_ratio=3.0):
+    """decoder.py:88-160: beam search over one sentence; with several members the
+    per-step log-probs are summed in member order in f32 and divided by
+    f32(#members) (:115-120).  ``src_ids_per_member[i]``: the sentence under
+    member i's source vocabulary (:99).  Returns (ids without final EOS, log_prob)."""
+    srcs = [list(x) for x in src_ids_per_member]
+    if not srcs[0]:
+        raise OracleError("empty", "cannot translate an empty sentence")
+    if beam < 1 or not max_ratio > 0:
+        raise OracleError("config", "bad decode config")
+    vocab = models[0].dims.tgt_vocab
+    encs = [m.encode(x) for m, x in zip(models, srcs)]
+    max_steps = math.ceil(max_ratio * len(srcs[0])) + 1
+    live_tokens = [[]]
+    live_scores = np.zeros(1, dtype=F64)
+    states = [(e[2].copy(), e[2].copy()) for e in encs]        # (s, s_prime) per member
+    y_prev = np.array([EOS_ID], dtype=np.int64)
+    finished = []   # (tokens, score)
+    for _ in range(max_steps):
+        lps, nxt = None, []
+        for m, enc, (s, sp) in zip(models, encs, states):
+            lp, s_new, s_int, _ = m.decoder_step(y_prev, s, sp, enc)
+            nxt.append((s_new, s_int))
+            lps = lp if lps is None else lps + lp
+        if len(models) > 1:
+            lps = lps / F32(len(models))
+        flat = (live_scores[:, None] + lps.T.astype(F64)).ravel()
+        chosen = select_candidates(flat, beam, vocab)
+        nt, ns, npar, nid = [], [], [], []
+        for f in chosen:
+            parent, tok = divmod(f, vocab)
+            score = float(flat[f])
+            if tok == EOS_ID:
+                finished.append((live_tokens[parent] + [tok], score))
+            else:
+                nt.append(live_tokens[parent] + [tok])
+                ns.append(score)
+                npar.append(parent)
+                nid.append(tok)
+        if not nt:
+            break
+        live_tokens = nt
+        live_scores = np.array(ns, dtype=F64)
+        pidx = np.array(npar, dtype=np.int64)
+        states = [(np.ascontiguousarray(a[:, pidx]), np.ascontiguousarray(b[:, pidx])) for a, b in nxt]
+        y_prev = np.array(nid, dtype=np.int64)
+        if finished and max(h[1] for h in finished) >= live_scores.max():
+            break
+    else:
+        for toks, score in zip(live_tokens, live_scores):
+            finished.append((list(toks), float(score)))
+    best = min(finished, key=lambda h: (-h[1], h[0]))
+    toks = best[0][:-1] if best[0] and best[0][-1] == EOS_ID else best[0]
+    return toks, best[1]
 
 
 def select_candidates(flat: np.ndarray, beam: int, vocab: int) -> list:

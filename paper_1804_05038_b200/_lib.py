@@ -44,6 +44,7 @@ SIGNATURES = {
     "qnmt_engine_destroy": (I32, [P]),
     "qnmt_engine_bytes": (C.c_size_t, [P]),
     "qnmt_translate_batch": (I32, [P, P, P, I32, I32, F64, P, I32, P, P, P]),
+    "qnmt_translate_ensemble": (I32, [P, I32, P, P, I32, I32, F64, P, I32, P, P, P]),
     "qnmt_encode_batch": (I32, [P, P, P, I32, P, P, P, P]),
     "qnmt_decoder_step": (I32, [P, I64, P, I32, P, P, P, P, P, P, P, I32, P, P, P, P, I64, P]),
     "qnmt_decode_batch_device": (I32, [P, P, P, I32, I32, F64, P]),

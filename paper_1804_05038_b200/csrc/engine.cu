@@ -592,14 +592,17 @@ static int step_core(qnmt_engine* e, const StepIO& io, cudaStream_t st) {
 }
 
 // next-step state columns by parent (decoder.py:131-140) and, with fq, their codes
-static int gather_next(qnmt_engine* e, int cur, int64_t N2, int n, int beam, cudaStream_t st) {
+// (srch: the engine holding the search state -- e itself, or an ensemble's lead engine)
+static int gather_next(qnmt_engine* e, int cur, int64_t N2, int n, int beam, cudaStream_t st,
+                       const qnmt_engine* srch = nullptr) {
     const qnmt_model* m = e->m;
     const int64_t H = m->H;
+    if (!srch) srch = e;
     if (e->fq_ok)
-        return gather_q_launch(e->s_new, m->aq == 1 ? e->s_int : nullptr, e->parent_col, H, e->col_off, e->P, n,
-                               beam, e->st_s[cur ^ 1], e->st_sp[cur ^ 1], e->q_s, e->sc_s,
+        return gather_q_launch(e->s_new, m->aq == 1 ? e->s_int : nullptr, srch->parent_col, H, srch->col_off, srch->P,
+                               n, beam, e->st_s[cur ^ 1], e->st_sp[cur ^ 1], e->q_s, e->sc_s,
                                m->aq == 1 ? e->q_q : nullptr, m->aq == 1 ? e->sc_q : nullptr, e->err, st);
-    return gather_rows_launch(e->s_new, e->s_int, e->parent_col, N2, H, e->st_s[cur ^ 1], e->st_sp[cur ^ 1], st);
+    return gather_rows_launch(e->s_new, e->s_int, srch->parent_col, N2, H, e->st_s[cur ^ 1], e->st_sp[cur ^ 1], st);
 }
 
 static bool vocab_fusable(const qnmt_engine* e, int k) {
@@ -1057,46 +1060,70 @@ static void drop_graphs(qnmt_engine* e) {
     e->graphs.clear();
 }
 
-// device-resident decode of one batch; results stay in the engine until finalize.
-static int decode_core(qnmt_engine* e, const int32_t* src_ids, bool ids_on_device, const int32_t* src_len,
-                       int32_t n, int32_t beam, double max_ratio, cudaStream_t st) {
+// host-side batch layout: row offsets, per-sentence step caps (decoder.py:103)
+struct BatchPlan {
+    std::vector<int64_t> row;
+    std::vector<int32_t> msteps;
+    int64_t P = 0;
+    int Lmax = 0, Tmax = 0;
+};
+
+static int plan_batch(const qnmt_engine* e, const int32_t* src_ids, bool ids_on_device, const int32_t* src_len,
+                      int32_t n, int32_t beam, double max_ratio, BatchPlan& b) {
     const qnmt_model* m = e->m;
-    const int64_t H = m->H, V = m->Vt;
     if (n < 1) { set_error("no sentences"); return QNMT_ERR_EMPTY; }
     if (beam < 1 || beam > e->B || !(max_ratio > 0)) { set_error("bad beam/max_ratio"); return QNMT_ERR_CONFIG; }
     if (n > e->S) { set_error("batch of %d exceeds engine capacity %d", n, e->S); return QNMT_ERR_CONFIG; }
-    std::vector<int64_t> row(n);
-    std::vector<int32_t> msteps(n);
-    int64_t P = 0;
-    int Lmax = 0, Tmax = 0;
+    b.row.resize(n);
+    b.msteps.resize(n);
     for (int i = 0; i < n; ++i) {
         if (src_len[i] < 1) { set_error("cannot translate an empty sentence"); return QNMT_ERR_EMPTY; }
-        row[i] = P;
-        P += src_len[i];
-        Lmax = std::max(Lmax, src_len[i]);
-        msteps[i] = (int32_t)ceil(max_ratio * (double)src_len[i]) + 1;   // decoder.py:103
-        Tmax = std::max(Tmax, msteps[i]);
+        if (src_len[i] > e->L) { set_error("sentence of length %d exceeds engine capacity %d", src_len[i], e->L); return QNMT_ERR_CONFIG; }
+        b.row[i] = b.P;
+        b.P += src_len[i];
+        b.Lmax = std::max(b.Lmax, src_len[i]);
+        b.msteps[i] = (int32_t)ceil(max_ratio * (double)src_len[i]) + 1;   // decoder.py:103
+        b.Tmax = std::max(b.Tmax, b.msteps[i]);
     }
     if (!ids_on_device)
-        for (int64_t i = 0; i < P; ++i)
+        for (int64_t i = 0; i < b.P; ++i)
             if (src_ids[i] < 0 || src_ids[i] >= m->Vs) { set_error("source id outside [0, %d)", m->Vs); return QNMT_ERR_VOCAB; }
-    TRY(grow_history(e, Tmax));
-    e->last_n = n;
-    e->last_tmax = Tmax;
+    return QNMT_OK;
+}
+
+// encoder + per-model decoder state for a batch: s = s' = s0 and the first step's state codes
+static int init_member(qnmt_engine* e, const int32_t* src_ids, bool ids_on_device, const int32_t* src_len,
+                       const BatchPlan& b, int32_t n, cudaStream_t st) {
+    const qnmt_model* m = e->m;
+    const int64_t H = m->H;
     QNMT_CUDA(cudaMemsetAsync(e->err, 0, 4, st));
-    QNMT_CUDA(cudaMemcpyAsync(e->src_ids, src_ids, (size_t)P * 4,
+    QNMT_CUDA(cudaMemcpyAsync(e->src_ids, src_ids, (size_t)b.P * 4,
                               ids_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
     prof_mark(e, PG_ENCODER, st);
-    TRY(encode_core(e, e->src_ids, src_len, row.data(), n, e->enc_states, e->enc_att, e->enc_s0, st));
+    TRY(encode_core(e, e->src_ids, src_len, b.row.data(), n, e->enc_states, e->enc_att, e->enc_s0, st));
     prof_mark(e, PG_MISC, st);
-    // decoder init: one column per sentence, s = s' = s0, y = EOS (BOS), live score 0 (decoder.py:105-110)
+    QNMT_CUDA(cudaMemcpyAsync(e->sent_row, b.row.data(), (size_t)n * 8, cudaMemcpyHostToDevice, st));
+    QNMT_CUDA(cudaMemcpyAsync(e->sent_len, src_len, (size_t)n * 4, cudaMemcpyHostToDevice, st));
+    TRY(att_minmax_launch(e->enc_att, e->sent_row, e->sent_len, n, m->A, e->att_mm, st));
+    QNMT_CUDA(cudaMemcpyAsync(e->st_s[0], e->enc_s0, (size_t)n * H * 4, cudaMemcpyDeviceToDevice, st));
+    QNMT_CUDA(cudaMemcpyAsync(e->st_sp[0], e->enc_s0, (size_t)n * H * 4, cudaMemcpyDeviceToDevice, st));
+    if (e->fq_ok) {   // first step's state codes (later steps get them from gather_q); column n = sentence n
+        TRY(quantize_launch(e->enc_s0, n, H, H, e->iota, n, e->q_s, H, e->sc_s, e->seg_bits, 1, e->err, st));
+        if (m->aq == 1)
+            TRY(quantize_launch(e->enc_s0, n, H, H, e->iota, n, e->q_q, H, e->sc_q, e->seg_bits, 1, e->err, st));
+    }
+    return QNMT_OK;
+}
+
+// search state: one column per sentence, y = EOS (BOS), live score 0 (decoder.py:105-110)
+static int init_search(qnmt_engine* e, const BatchPlan& b, int32_t n, cudaStream_t st) {
+    TRY(grow_history(e, b.Tmax));
+    e->last_n = n;
+    e->last_tmax = b.Tmax;
     std::vector<int32_t> iota_n(n), y0(n, 2), ones(n, 1);
     std::iota(iota_n.begin(), iota_n.end(), 0);
     std::vector<double> dz(n, 0.0);
-    QNMT_CUDA(cudaMemcpyAsync(e->sent_row, row.data(), (size_t)n * 8, cudaMemcpyHostToDevice, st));
-    QNMT_CUDA(cudaMemcpyAsync(e->sent_len, src_len, (size_t)n * 4, cudaMemcpyHostToDevice, st));
-    QNMT_CUDA(cudaMemcpyAsync(e->max_steps, msteps.data(), (size_t)n * 4, cudaMemcpyHostToDevice, st));
-    TRY(att_minmax_launch(e->enc_att, e->sent_row, e->sent_len, n, m->A, e->att_mm, st));
+    QNMT_CUDA(cudaMemcpyAsync(e->max_steps, b.msteps.data(), (size_t)n * 4, cudaMemcpyHostToDevice, st));
     QNMT_CUDA(cudaMemcpyAsync(e->P, ones.data(), (size_t)n * 4, cudaMemcpyHostToDevice, st));
     QNMT_CUDA(cudaMemcpyAsync(e->col_off, iota_n.data(), (size_t)n * 4, cudaMemcpyHostToDevice, st));
     QNMT_CUDA(cudaMemcpyAsync(e->col_sent[0], iota_n.data(), (size_t)n * 4, cudaMemcpyHostToDevice, st));
@@ -1105,13 +1132,26 @@ static int decode_core(qnmt_engine* e, const int32_t* src_ids, bool ids_on_devic
     QNMT_CUDA(cudaMemsetAsync(e->done, 0, (size_t)n * 4, st));
     QNMT_CUDA(cudaMemsetAsync(e->fin_cnt, 0, (size_t)n * 4, st));
     QNMT_CUDA(cudaMemsetAsync(e->steps_run, 0, (size_t)n * 4, st));
-    QNMT_CUDA(cudaMemcpyAsync(e->st_s[0], e->enc_s0, (size_t)n * H * 4, cudaMemcpyDeviceToDevice, st));
-    QNMT_CUDA(cudaMemcpyAsync(e->st_sp[0], e->enc_s0, (size_t)n * H * 4, cudaMemcpyDeviceToDevice, st));
-    if (e->fq_ok) {   // first step's state codes (later steps get them from gather_q); column n = sentence n
-        TRY(quantize_launch(e->enc_s0, n, H, H, e->iota, n, e->q_s, H, e->sc_s, e->seg_bits, 1, e->err, st));
-        if (m->aq == 1)
-            TRY(quantize_launch(e->enc_s0, n, H, H, e->iota, n, e->q_q, H, e->sc_q, e->seg_bits, 1, e->err, st));
-    }
+    return QNMT_OK;   // (pageable H2D copies are staged before cudaMemcpyAsync returns)
+}
+
+static SearchState search_state(qnmt_engine* e, int cur, int32_t* n_out) {
+    return SearchState{e->P, e->col_off, e->done, e->max_steps, e->steps_run, e->fin_cnt, e->fin_best,
+                       e->fin_score, e->fin_step, e->fin_slot, e->fin_eos, e->hist_tok, e->hist_par,
+                       (e->hist_steps + 1) * e->B, e->hist_steps, e->B, e->cand_score, e->cand_tok,
+                       e->col_sent[cur ^ 1], e->parent_col, e->y[cur ^ 1], e->live[cur ^ 1], n_out};
+}
+
+// device-resident decode of one batch; results stay in the engine until finalize.
+static int decode_core(qnmt_engine* e, const int32_t* src_ids, bool ids_on_device, const int32_t* src_len,
+                       int32_t n, int32_t beam, double max_ratio, cudaStream_t st) {
+    const qnmt_model* m = e->m;
+    const int64_t V = m->Vt;
+    BatchPlan b;
+    TRY(plan_batch(e, src_ids, ids_on_device, src_len, n, beam, max_ratio, b));
+    TRY(init_search(e, b, n, st));
+    TRY(init_member(e, src_ids, ids_on_device, src_len, b, n, st));
+    const int Tmax = b.Tmax, Lmax = b.Lmax;
     const int k_list = (int)std::min<int64_t>(beam, V);
     if (graph_eligible(e)) {
         // device-resident loop: one graph launch per step, live count polled every POLL steps
@@ -1141,12 +1181,7 @@ static int decode_core(qnmt_engine* e, const int32_t* src_ids, bool ids_on_devic
         TRY(step_core(e, io, st));
         TRY(cands_launch(e, io, e->live[cur], k_list, st));
         prof_mark(e, PG_SEARCH, st);
-        SearchState ss{e->P, e->col_off, e->done, e->max_steps, e->steps_run, e->fin_cnt, e->fin_best,
-                       e->fin_score, e->fin_step, e->fin_slot, e->fin_eos, e->hist_tok, e->hist_par,
-                       (e->hist_steps + 1) * e->B, e->hist_steps, e->B,
-                       e->cand_score, e->cand_tok,
-                       e->col_sent[cur ^ 1], e->parent_col, e->y[cur ^ 1], e->live[cur ^ 1], e->n_live};
-        TRY(search_step_launch(ss, t, n, beam, k_list, st));
+        TRY(search_step_launch(search_state(e, cur, e->n_live), t, n, beam, k_list, st));
         QNMT_CUDA(cudaMemcpyAsync(e->h_pinned, e->n_live, 4, cudaMemcpyDeviceToHost, st));
         QNMT_CUDA(cudaStreamSynchronize(st));
         prof_collect(e);
@@ -1160,6 +1195,59 @@ static int decode_core(qnmt_engine* e, const int32_t* src_ids, bool ids_on_devic
     int rc = check_flag(e, st);
     prof_collect(e);
     return rc;
+}
+
+// Ensemble decode (decoder.py:88-160 with several members): eager steps, one host
+// sync per step.  es[0] holds the search state; every member steps its own
+// states against the shared column layout, tokens and parents.
+static int decode_ensemble(qnmt_engine* const* es, int nm, const int32_t* src_ids, const int32_t* src_len, int32_t n,
+                           int32_t beam, double max_ratio, cudaStream_t st) {
+    qnmt_engine* lead = es[0];
+    const int64_t V = lead->m->Vt;
+    if (nm < 2 || nm > QNMT_ENS_MAX) { set_error("ensemble of %d members outside [2, %d]", nm, QNMT_ENS_MAX); return QNMT_ERR_CONFIG; }
+    for (int i = 1; i < nm; ++i) {
+        if (es[i]->m->Vt != V) { set_error("ensemble members must share the target vocabulary"); return QNMT_ERR_CONFIG; }
+        if (es[i]->S != lead->S || es[i]->L != lead->L || es[i]->B != lead->B) {
+            set_error("ensemble engines must have the same capacity");
+            return QNMT_ERR_CONFIG;
+        }
+        for (int j = 0; j < i; ++j)
+            if (es[j] == es[i]) { set_error("ensemble members need distinct engines"); return QNMT_ERR_CONFIG; }
+    }
+    // members map the tokens with their own source vocabularies (decoder.py:99): ids are member-major
+    BatchPlan b;
+    TRY(plan_batch(lead, src_ids, false, src_len, n, beam, max_ratio, b));
+    for (int i = 1; i < nm; ++i) {
+        BatchPlan bi;
+        TRY(plan_batch(es[i], src_ids + (size_t)i * b.P, false, src_len, n, beam, max_ratio, bi));
+    }
+    TRY(init_search(lead, b, n, st));
+    for (int i = 0; i < nm; ++i) TRY(init_member(es[i], src_ids + (size_t)i * b.P, false, src_len, b, n, st));
+    const int k_list = (int)std::min<int64_t>(beam, V);
+    EnsRows rows{};
+    for (int i = 0; i < nm; ++i) rows.p[i] = es[i]->logits;
+    int64_t N = n;
+    int cur = 0;
+    for (int t = 0; t < b.Tmax && N > 0; ++t) {
+        for (int i = 0; i < nm; ++i) {
+            qnmt_engine* e = es[i];
+            StepIO io{N, n, lead->col_sent[cur], lead->y[cur], e->st_s[cur], e->st_sp[cur], e->enc_states,
+                      e->enc_att, e->sent_row, e->sent_len, b.Lmax, e->s_int, e->s_new, e->logits, nullptr, 0,
+                      lead->col_off, lead->P, e->att_mm, beam, e->fq_ok, false};
+            TRY(step_core(e, io, st));
+        }
+        TRY(ens_topk_launch(rows, nm, N, V, V, lead->live[cur], k_list, lead->cand_score, lead->cand_tok, lead->err,
+                            st));
+        TRY(search_step_launch(search_state(lead, cur, lead->n_live), t, n, beam, k_list, st));
+        QNMT_CUDA(cudaMemcpyAsync(lead->h_pinned, lead->n_live, 4, cudaMemcpyDeviceToHost, st));
+        QNMT_CUDA(cudaStreamSynchronize(st));
+        const int64_t N2 = lead->h_pinned[0];
+        for (int i = 0; i < nm; ++i) TRY(gather_next(es[i], cur, N2, n, beam, st, lead));
+        N = N2;
+        cur ^= 1;
+    }
+    for (int i = 0; i < nm; ++i) TRY(check_flag(es[i], st));
+    return QNMT_OK;
 }
 
 // D2H of the finished lists + history, then min by (-logp, tokens) (decoder.py:157-160)
@@ -1223,6 +1311,16 @@ int qnmt_translate_batch(qnmt_engine* e, const int32_t* src_ids, const int32_t* 
     cudaStream_t st = as_stream(stream);
     TRY(decode_core(e, src_ids, false, src_len, n, beam, max_ratio, st));
     return finalize(e, out_tokens, out_stride, out_len, out_logp, st);
+}
+
+int qnmt_translate_ensemble(qnmt_engine* const* engines, int32_t n_members, const int32_t* src_ids,
+                            const int32_t* src_len, int32_t n, int32_t beam, double max_ratio, int32_t* out_tokens,
+                            int32_t out_stride, int32_t* out_len, double* out_logp, void* stream) {
+    if (n_members == 1) return qnmt_translate_batch(engines[0], src_ids, src_len, n, beam, max_ratio, out_tokens,
+                                                    out_stride, out_len, out_logp, stream);
+    cudaStream_t st = as_stream(stream);
+    TRY(decode_ensemble(engines, n_members, src_ids, src_len, n, beam, max_ratio, st));
+    return finalize(engines[0], out_tokens, out_stride, out_len, out_logp, st);
 }
 
 int qnmt_decode_batch_device(qnmt_engine* e, const int32_t* src_ids_dev, const int32_t* src_len,

@@ -31,6 +31,11 @@ int att_minmax_launch(const float* att_proj, const int64_t* sent_row, const int3
                       int64_t A, float* mm, cudaStream_t st);
 int col_ranges_launch(const int32_t* col_sent, int64_t N, int32_t n_sent, int32_t* off, int32_t* cnt,
                       cudaStream_t st);
+struct EnsRows {
+    const float* p[QNMT_ENS_MAX];   // member logits [N][ld], same layout
+};
+int ens_topk_launch(const EnsRows& rows, int nm, int64_t N, int64_t V, int64_t ld, const double* live, int32_t k,
+                    double* cand_score, int32_t* cand_tok, int32_t* err_flag, cudaStream_t st);
 int topk_launch(const float* logits, int64_t N, int64_t V, int64_t ld, const double* live, int32_t k,
                 double* cand_score, int32_t* cand_tok, int32_t* err_flag, cudaStream_t st);
 // encode pass only: seg_maxbits already holds the per-segment max-abs bits

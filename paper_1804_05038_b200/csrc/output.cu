@@ -11,6 +11,7 @@
 #include <float.h>
 
 #include "cand.cuh"
+#include "kernels.cuh"
 
 namespace qnmt {
 
@@ -284,6 +285,73 @@ k_topk1(const float* __restrict__ logits, int64_t V, int64_t ld, const double* _
             cand_score[n * k + i] = lst[i].s;
             cand_tok[n * k + i] = lst[i].t;
         }
+}
+
+// ---------------------------------------------------------------------------
+// Ensemble candidates (decoder.py:115-120 + :125): every member's column
+// log-softmax (fp64, rounded once, as k_log_softmax), summed in member order in
+// f32, divided by f32(#members), then score = live + f64(lp) and the top-k by
+// (score desc, token asc).  One CTA per hypothesis column; members' logits are
+// read once for the statistics and once for the candidates.
+// ---------------------------------------------------------------------------
+template <int KM>
+__global__ void __launch_bounds__(LS_T)
+k_ens_topk(EnsRows rows, int nm, int64_t V, int64_t ld, const double* __restrict__ live, int k,
+           double* __restrict__ cand_score, int32_t* __restrict__ cand_tok, int32_t* err_flag) {
+    __shared__ float redf[32];
+    __shared__ double redd[32];
+    __shared__ Cand wl[LS_T / 32][KM];
+    __shared__ Cand lst[KM];
+    const int64_t n = blockIdx.x;
+    double dm[QNMT_ENS_MAX], lse[QNMT_ENS_MAX];
+#pragma unroll
+    for (int i = 0; i < QNMT_ENS_MAX; ++i) {
+        dm[i] = 0.0;
+        lse[i] = 0.0;
+        if (i < nm) {
+            float mx;
+            column_stats(rows.p[i] + n * ld, V, redf, redd, mx, lse[i], err_flag);
+            dm[i] = (double)mx;
+        }
+    }
+    const float fn = (float)nm;
+    const double base = live ? live[n] : 0.0;
+    Cand L[KM];
+#pragma unroll
+    for (int i = 0; i < KM; ++i) L[i] = Cand{-DBL_MAX, 0x7fffffff};
+    for (int64_t v = threadIdx.x; v < V; v += LS_T) {
+        float acc = __double2float_rn(((double)rows.p[0][n * ld + v] - dm[0]) - lse[0]);
+#pragma unroll
+        for (int i = 1; i < QNMT_ENS_MAX; ++i)
+            if (i < nm) acc = __fadd_rn(acc, __double2float_rn(((double)rows.p[i][n * ld + v] - dm[i]) - lse[i]));
+        acc = __fdiv_rn(acc, fn);
+        insert<KM>(L, Cand{base + (double)acc, (int)v});
+    }
+    block_merge_cands<KM>(L, wl, lst, k);
+    if (threadIdx.x == 0)
+        for (int i = 0; i < k; ++i) {
+            cand_score[n * k + i] = lst[i].s;
+            cand_tok[n * k + i] = lst[i].t;
+        }
+}
+
+int ens_topk_launch(const EnsRows& rows, int nm, int64_t N, int64_t V, int64_t ld, const double* live, int32_t k,
+                    double* cand_score, int32_t* cand_tok, int32_t* err_flag, cudaStream_t st) {
+    if (N <= 0) return QNMT_OK;
+    if (nm < 2 || nm > QNMT_ENS_MAX) {
+        set_error("ensemble of %d members outside [2, %d]", nm, QNMT_ENS_MAX);
+        return QNMT_ERR_CONFIG;
+    }
+    if (k < 1 || k > 16 || k > V) {
+        set_error("ensemble candidates: k=%d outside [1, min(16, V)]", k);
+        return QNMT_ERR_CONFIG;
+    }
+    if (k <= 8)
+        k_ens_topk<8><<<(unsigned)N, LS_T, 0, st>>>(rows, nm, V, ld, live, k, cand_score, cand_tok, err_flag);
+    else
+        k_ens_topk<16><<<(unsigned)N, LS_T, 0, st>>>(rows, nm, V, ld, live, k, cand_score, cand_tok, err_flag);
+    QNMT_CHECK_LAUNCH("k_ens_topk");
+    return QNMT_OK;
 }
 
 int log_softmax_launch(const float* logits, int64_t N, int64_t V, int64_t ld, float* lp, int64_t ldlp,

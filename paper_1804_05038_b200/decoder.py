@@ -15,7 +15,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from .errors import ConfigError, EmptyInputError
-from .engine import Engine
+from .engine import Engine, translate_ensemble_ids
 from .model import EOS_ID, ModelParams, QuantizedModel, quantize_model
 
 
@@ -44,19 +44,23 @@ class BeamHypothesis:
     finished: bool = False
 
 
-def _single_model(models) -> QuantizedModel:
+def _members(models) -> list:
+    """Ensemble members as device int8 models (decoder.py:46-71): a single model
+    or a non-empty list sharing one target vocabulary; float parameters are
+    quantized once and cached."""
     if isinstance(models, (ModelParams, QuantizedModel)):
         members = [models]
     else:
         members = list(models)
     if not members:
         raise ConfigError("at least one model is required")
-    if len(members) > 1:
-        raise ConfigError("ensemble decoding is not implemented on the B200 path")
-    m = members[0]
-    if isinstance(m, ModelParams):
-        m = _quantized_cache(m)
-    return m
+    first = members[0].tgt_tokens
+    for m in members[1:]:
+        if m.tgt_tokens != first:
+            raise ConfigError("ensemble members must share the target vocabulary")
+    if len(members) > 8:
+        raise ConfigError("ensembles of more than 8 members are not supported")
+    return [_quantized_cache(m) if isinstance(m, ModelParams) else m for m in members]
 
 
 def _quantized_cache(params: ModelParams) -> QuantizedModel:
@@ -67,16 +71,41 @@ def _quantized_cache(params: ModelParams) -> QuantizedModel:
     return qm
 
 
-def _engine_for(qm: QuantizedModel, n: int, length: int, beam: int) -> Engine:
-    e = getattr(qm, "_engine", None)
-    if e is None or not e.fits(n, length, beam):
+def _engine_for(qm: QuantizedModel, n: int, length: int, beam: int, slot: int = 0, exact=None) -> Engine:
+    """The model's cached engine number ``slot`` (an ensemble that lists one model
+    twice needs two), grown to fit; ``exact`` forces one (S, L, B) capacity."""
+    pool = getattr(qm, "_engines", None)
+    if pool is None:
+        pool = qm._engines = []
+    while len(pool) <= slot:
+        pool.append(None)
+    e = pool[slot]
+    if exact is not None:
+        ok = e is not None and (e.max_sentences, e.max_len, e.max_beam) == exact
+        cap = exact
+    else:
+        ok = e is not None and e.fits(n, length, beam)
         cap = (max(n, e.max_sentences if e else 0), max(length, 128, e.max_len if e else 0),
                max(beam, e.max_beam if e else 0))
+    if not ok:
         if e is not None:
             e.close()
         e = Engine(qm, *cap)
-        qm._engine = e
+        pool[slot] = e
     return e
+
+
+def _engines_for(members, n: int, length: int, beam: int) -> list:
+    """One engine per ensemble member, all with the same capacity."""
+    slots, seen = [], {}
+    for m in members:
+        slots.append(seen.get(id(m), 0))
+        seen[id(m)] = slots[-1] + 1
+    cur = [getattr(m, "_engines", [None] * (s + 1))[s] if len(getattr(m, "_engines", [])) > s else None
+           for m, s in zip(members, slots)]
+    cap = (max([n] + [e.max_sentences for e in cur if e]), max([length, 128] + [e.max_len for e in cur if e]),
+           max([beam] + [e.max_beam for e in cur if e]))
+    return [_engine_for(m, n, length, beam, s, exact=cap) for m, s in zip(members, slots)]
 
 
 def _check_cfg(cfg: DecodeConfig):
@@ -86,44 +115,59 @@ def _check_cfg(cfg: DecodeConfig):
         raise ConfigError("beam > 16 is not supported by the device search")
 
 
+def _decode_ids(members, per_member_ids, cfg: DecodeConfig, max_batch: int):
+    """Batched device decode of id lists (one list per member); yields (ids, logp)."""
+    n_all = len(per_member_ids[0])
+    max_len = max(len(x) for x in per_member_ids[0])
+    nb = min(max_batch, n_all)
+    if len(members) == 1:
+        e = _engine_for(members[0], nb, max_len, cfg.beam)
+        for b0 in range(0, n_all, max_batch):
+            toks, lps = e.translate_ids(per_member_ids[0][b0:b0 + max_batch], cfg.beam, cfg.max_ratio)
+            yield from zip(toks, lps)
+        return
+    engines = _engines_for(members, nb, max_len, cfg.beam)
+    for b0 in range(0, n_all, max_batch):
+        toks, lps = translate_ensemble_ids(engines, [ids[b0:b0 + max_batch] for ids in per_member_ids], cfg.beam,
+                                           cfg.max_ratio)
+        yield from zip(toks, lps)
+
+
 def translate(models, source_tokens, cfg: DecodeConfig, timer=None):
     """Beam-search translation of one pre-tokenized sentence (decoder.py:88-160).
 
     Returns ``(target_tokens, log_prob)``: the token list excludes the final
-    EOS; the score is the plain sum of per-step log-probs."""
+    EOS; the score is the plain sum of per-step log-probs (ensemble members
+    contribute the arithmetic mean of their log-probs per step)."""
     tokens = list(source_tokens)
     if not tokens:
         raise EmptyInputError("cannot translate an empty sentence")
     _check_cfg(cfg)
-    qm = _single_model(models)
-    ids = qm.src_ids(tokens)
-    e = _engine_for(qm, 1, len(ids), cfg.beam)
-    out, lps = e.translate_ids([ids], cfg.beam, cfg.max_ratio)
-    return [qm.tgt_tokens[i] for i in out[0]], lps[0]
+    members = _members(models)
+    ids = [[m.src_ids(tokens)] for m in members]
+    out, lp = next(_decode_ids(members, ids, cfg, 1))
+    return [members[0].tgt_tokens[i] for i in out], lp
 
 
-def translate_batch(model, sentences, cfg: DecodeConfig, max_batch: int = 256, return_ids=False):
+def translate_batch(models, sentences, cfg: DecodeConfig, max_batch: int = 256, return_ids=False):
     """Translate a corpus with batched device decoding (B200-native bulk path).
 
-    ``sentences``: token lists / whitespace strings, or (``return_ids``) id
-    lists.  Output order follows the input.  Each batch of up to
-    ``max_batch`` sentences is one engine call."""
+    ``models``: one model or an ensemble list.  ``sentences``: token lists /
+    whitespace strings, or (``return_ids``) id lists.  Output order follows
+    the input.  Each batch of up to ``max_batch`` sentences is one engine call."""
     _check_cfg(cfg)
-    qm = _single_model(model)
+    members = _members(models)
     sents = [s.split() if isinstance(s, str) else list(s) for s in sentences]
     if not sents:
         return []
     if any(len(s) == 0 for s in sents):
         raise EmptyInputError("cannot translate an empty sentence")
-    ids = [np.asarray(s, dtype=np.int64) if return_ids else qm.src_ids(s) for s in sents]
-    max_len = max(len(x) for x in ids)
-    e = _engine_for(qm, min(max_batch, len(ids)), max_len, cfg.beam)
-    results = []
-    for b0 in range(0, len(ids), max_batch):
-        toks, lps = e.translate_ids(ids[b0:b0 + max_batch], cfg.beam, cfg.max_ratio)
-        for t, lp in zip(toks, lps):
-            results.append((t if return_ids else [qm.tgt_tokens[i] for i in t], lp))
-    return results
+    if return_ids:
+        ids = [[np.asarray(s, dtype=np.int64) for s in sents]] * len(members)
+    else:
+        ids = [[m.src_ids(s) for s in sents] for m in members]
+    tgt = members[0].tgt_tokens
+    return [(t if return_ids else [tgt[i] for i in t], lp) for t, lp in _decode_ids(members, ids, cfg, max_batch)]
 
 
 def max_steps(length: int, max_ratio: float) -> int:

@@ -103,3 +103,29 @@ class Engine:
                   out_lp.ctypes.data, _dev.stream_ptr())
         toks = [out_tok[i, :out_len[i]].tolist() for i in range(n)]
         return toks, out_lp.tolist()
+
+
+def translate_ensemble_ids(engines, id_lists_per_member, beam: int, max_ratio: float):
+    """Ensemble translation (decoder.py:88-160, members averaged per step,
+    :115-120) of many sentences; ``id_lists_per_member[i]`` are the source ids
+    under member i's vocabulary.  Returns (token-id lists, log-probs)."""
+    nm = len(engines)
+    n = len(id_lists_per_member[0])
+    if n == 0:
+        return [], []
+    lens = np.array([len(x) for x in id_lists_per_member[0]], dtype=np.int32)
+    if (lens == 0).any():
+        raise EmptyInputError("cannot translate an empty sentence")
+    if any(not e.fits(n, int(lens.max()), beam) for e in engines):
+        raise ConfigError("batch exceeds engine capacity")
+    ids = np.ascontiguousarray(np.concatenate([np.asarray(x, dtype=np.int32)
+                                               for lists in id_lists_per_member for x in lists]))
+    stride = int(math.ceil(max_ratio * int(lens.max()))) + 1
+    out_tok = np.zeros((n, stride), dtype=np.int32)
+    out_len = np.zeros(n, dtype=np.int32)
+    out_lp = np.zeros(n, dtype=np.float64)
+    hs = (C.c_void_p * nm)(*[e._h.value for e in engines])
+    _lib.call("qnmt_translate_ensemble", C.cast(hs, C.c_void_p), nm, ids.ctypes.data, lens.ctypes.data, n, beam,
+              float(max_ratio), out_tok.ctypes.data, stride, out_len.ctypes.data, out_lp.ctypes.data,
+              _dev.stream_ptr())
+    return [out_tok[i, :out_len[i]].tolist() for i in range(n)], out_lp.tolist()

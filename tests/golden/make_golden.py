@@ -323,6 +323,53 @@ def gen_baseline():
     print("baseline_dims.npz:", len(out), "arrays")
 
 
+# ensembles (decoder.py:115-120): members share the target vocabulary; member 2 has a
+# smaller source vocabulary (its UNK mapping differs) and the "previous" query flags
+ENSEMBLES = [
+    ("ens2", [("e_a", dict(SMALL_DIMS), 21, 0.6, 0.1, 0.75, "transform", "current"),
+              ("e_b", dict(SMALL_DIMS), 22, 0.6, 0.1, 0.75, "transform", "current")]),
+    ("ens3", [("e_c", dict(SMALL_DIMS), 23, 0.5, 0.1, 0.6, "transform", "current"),
+              ("e_d", dict(SMALL_DIMS, src_vocab=SMALL_DIMS["src_vocab"] - 9), 24, 0.5, 0.1, 0.6, "zero", "previous"),
+              ("e_e", dict(SMALL_DIMS), 25, 0.05, 0.05, 0.0, "transform", "current")]),
+    ("ensdup", [("e_a", dict(SMALL_DIMS), 21, 0.6, 0.1, 0.75, "transform", "current"),
+                ("e_a", dict(SMALL_DIMS), 21, 0.6, 0.1, 0.75, "transform", "current")]),
+]
+
+
+def gen_ensemble():
+    """Tier-B (and Tier-A) ensemble translations by the reference's translate()."""
+    out = {"ensembles": {}, "cases": []}
+    for tag, members in ENSEMBLES:
+        qms, src_tokens = [], None
+        for mtag, dims_kw, seed, ws, bs, eb, s0m, aq in members:
+            params, _ = make_params(ref_model.Dims(**dims_kw), seed, bias_std=bs, weight_std=ws, eos_bias=eb,
+                                    s0_mode=s0m, attention_query=aq)
+            qms.append(ref_model.quantize_model(params))
+            src_tokens = src_tokens or params.src_tokens
+        out["ensembles"][tag] = [dict(tag=m[0], dims=m[1], seed=m[2], weight_std=m[3], bias_std=m[4], eos_bias=m[5],
+                                      s0_mode=m[6], attention_query=m[7]) for m in members]
+        rng = np.random.default_rng(300 + len(tag))
+        for n in range(10):
+            length = int(rng.integers(1, 10))
+            ids = rng.integers(3, len(src_tokens), length).tolist()
+            toks = [src_tokens[i] for i in ids]
+            beam = [1, 3, 5, 2, 8][n % 5]
+            ratio = [1.5, 3.0, 2.0][n % 3]
+            cfg = DecodeConfig(beam=beam, max_ratio=ratio, precision="int8")
+            case = {"ensemble": tag, "src_tokens": toks, "beam": beam, "max_ratio": ratio}
+            for tier in ("A", "B"):
+                ctx = tier_b() if tier == "B" else contextlib.nullcontext()
+                with ctx:
+                    words, logp = translate(qms, toks, cfg)
+                tgt_index = {t: i for i, t in enumerate(qms[0].tgt_tokens)}
+                case[f"out_{tier}"] = [tgt_index[w] for w in words]
+                case[f"logp_{tier}"] = logp
+            out["cases"].append(case)
+    with open(os.path.join(HERE, "ensemble_small.json"), "w") as fh:
+        json.dump(out, fh, indent=1)
+    print("ensemble_small.json:", len(out["cases"]), "cases")
+
+
 MODELFILE_ARGS = dict(src_vocab=14, tgt_vocab=13, embed=4, hidden=6, seed=11, attn=5, readout=3)
 
 
@@ -356,7 +403,9 @@ def gen_modelfile():
 
 
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["qmath", "small", "baseline", "modelfile"]
+    which = sys.argv[1:] or ["qmath", "small", "baseline", "modelfile", "ensemble"]
+    if "ensemble" in which:
+        gen_ensemble()
     if "modelfile" in which:
         gen_modelfile()
     if "qmath" in which:
