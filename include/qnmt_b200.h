@@ -111,6 +111,13 @@ int qnmt_gemm_i8(const int8_t* W, int64_t M, int64_t K, int64_t ldw,
  * 2 = tcgen05 whenever the shape is eligible.  Returns the previous value. */
 int qnmt_set_gemm_impl(int impl);
 
+/* fp32 precision path: replaces qmath.py:434-440
+ * (gemm_f32) in LinearOp's float branch (layers.py:138-145).
+ *   Y[n][m] = fl32(sum_k f64(W[m][k]) f64(X[n][k])) (+ bias[m]) (+ Y[n][m] if
+ *   flags & QNMT_GEMM_ACCUMULATE); W [M][ldw] f32, X K-major [N][ldx] f32. */
+int qnmt_gemm_f32(const float* W, int64_t M, int64_t K, int64_t ldw, const float* X, int64_t N,
+                  int64_t ldx, const float* bias, float* Y, int64_t ldy, int32_t flags, void* stream);
+
 /* ---------------------------------------------------------------------------
  * GRU gate arithmetic (layers.py:170-181), f32 ops in the reference's
  * association order, sigmoid/tanh evaluated in fp64 and rounded once.
@@ -151,6 +158,14 @@ int qnmt_tanh(const float* x, int64_t N, int64_t D, int64_t ldx, float* y, int64
  *   ctx: [N][2H] (ldc); alpha (nullable): [N][lda];
  *   scratch: >= 4*(N*max_len + 2*N + 128 + 2*n_sent*A) bytes
  * ------------------------------------------------------------------------- */
+/* fp32 attend (layers.py:214-241 with float LinearOps): scores
+ * fl32(sum_a f64(v_a) f64(tanh(att_proj + u))) then the same softmax/context as
+ * qnmt_attention.  v: f32 [A]; scratch >= 4*N*max_len bytes. */
+int qnmt_attention_f32(const float* u, int64_t ldu, int64_t N, const int32_t* sent_col_off,
+                       const int32_t* sent_ncols, int32_t n_sent, const float* att_proj,
+                       const float* states, const int64_t* sent_row, const int32_t* sent_len,
+                       int32_t max_len, int64_t A, int64_t H2, const float* v, float* ctx, int64_t ldc,
+                       float* alpha, int64_t lda, void* scratch, int32_t* err_flag, void* stream);
 int qnmt_attention_stats(const float* att_proj, const int64_t* sent_row, const int32_t* sent_len,
                          int32_t n_sent, int64_t A, float* att_minmax, void* stream);
 int qnmt_attention(const float* u, int64_t ldu, int64_t N, const int32_t* sent_col_off,
@@ -237,6 +252,10 @@ typedef struct qnmt_engine qnmt_engine;
 
 int qnmt_model_create(const int32_t* dims, const void* const* tensors, int32_t ntensors,
                       qnmt_model** out);
+/* fp32 model (same tensor table; weight slots hold f32 matrices, scale slots
+ * are ignored): engines built on it decode with the fp32 path. */
+int qnmt_model_create_f32(const int32_t* dims, const void* const* tensors, int32_t ntensors,
+                          qnmt_model** out);
 int qnmt_model_destroy(qnmt_model* m);
 
 /* Engine: scratch for up to max_sentences sentences of length <= max_src_len

@@ -185,6 +185,13 @@ def log_softmax_cols(v, tier="B"):
     return (t - lse).astype(F32)
 
 
+def gemm_f32(a, b, tier="B"):
+    """qmath.py:434-440 (numpy/OpenBLAS a @ b).  Tier B: fp64 product rounded once."""
+    if tier == "A":
+        return a @ b
+    return (a.astype(F64) @ b.astype(F64)).astype(F32)
+
+
 def context(states, alpha, tier="B"):
     """layers.py:237 (gemm_f32(enc.states, alpha))."""
     if tier == "A":
@@ -234,9 +241,10 @@ class QModel:
     embeddings becomes (int8 codes, f32 scale); embeddings and biases stay f32."""
 
     def __init__(self, dims: Dims, tensors: dict, s0_mode="transform",
-                 attention_query="current", tier="B"):
+                 attention_query="current", tier="B", precision="int8"):
         self.dims = dims
         self.tier = tier
+        self.precision = precision
         self.s0_mode = s0_mode
         self.attention_query = attention_query
         self.f = {}
@@ -244,13 +252,21 @@ class QModel:
         for name, shape in tensor_specs(dims):
             arr = np.ascontiguousarray(tensors[name], dtype=F32)
             assert tuple(arr.shape) == tuple(shape), (name, arr.shape, shape)
-            if len(shape) == 2 and name not in ("src_embed", "tgt_embed"):
+            if len(shape) == 2 and name not in ("src_embed", "tgt_embed") and precision == "int8":
                 self.q[name] = quantize(arr)
             else:
                 self.f[name] = arr
 
-    # layers.py:118-146 (LinearOp.apply, int8 branch)
+    # layers.py:118-146 (LinearOp.apply, int8 branch; float branch :138-143 -> gemm_f32)
     def linear(self, name, x, bias=None):
+        if self.precision == "fp32":
+            w = self.f[name]
+            if x.ndim != 2 or x.shape[0] != w.shape[1]:
+                raise OracleError("shape", f"LinearOp expects [{w.shape[1]}, P] input, got {x.shape}")
+            y = gemm_f32(w, x, self.tier)
+            if bias is not None:
+                y += self.f[bias][:, None]
+            return y
         codes, sw = self.q[name]
         if x.ndim != 2 or x.shape[0] != codes.shape[1]:
             raise OracleError("shape", f"LinearOp expects [{codes.shape[1]}, P] input, got {x.shape}")

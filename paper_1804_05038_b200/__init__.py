@@ -11,7 +11,17 @@ All arithmetic runs in hand-written sm_100a CUDA kernels behind the C ABI of
 __version__ = "0.1.0"
 
 from . import errors
-from .decoder import BeamHypothesis, DecodeConfig, bpe_merge, translate, translate_batch
+from .bleu import bleu
+from .decoder import (
+    BeamHypothesis,
+    DecodeConfig,
+    ParityReport,
+    bpe_merge,
+    compare_precisions,
+    edit_distance,
+    translate,
+    translate_batch,
+)
 from .engine import Engine
 from .layers import (
     AttentionNet,
@@ -27,6 +37,7 @@ from .layers import (
 )
 from .model import (
     Dims,
+    Float32Model,
     ModelParams,
     QuantizedModel,
     generate_model,
@@ -36,6 +47,7 @@ from .model import (
     save_model,
     synthetic_model,
     tensor_specs,
+    to_device_f32,
 )
 from .qmath import (
     INT8_MAX,
@@ -43,6 +55,7 @@ from .qmath import (
     QuantizationStats,
     QuantizedMatrix,
     dequantize,
+    gemm_f32,
     qgemm,
     qgemm_panel,
     quantize,
@@ -51,7 +64,8 @@ from .qmath import (
 
 __all__ = [
     "AttentionNet", "BeamHypothesis", "DecodeConfig", "DecoderState", "Dims", "EncoderStates",
-    "Engine", "GruCell", "INT8_MAX", "INT32_SAFE_K", "LinearOp", "ModelParams", "Network",
+    "Engine", "Float32Model", "GruCell", "ParityReport", "bleu", "compare_precisions", "edit_distance",
+    "gemm_f32", "to_device_f32", "INT8_MAX", "INT32_SAFE_K", "LinearOp", "ModelParams", "Network",
     "OutputNet", "QuantizationStats", "QuantizedMatrix", "QuantizedModel", "attend", "bpe_merge",
     "build_network", "dequantize", "errors", "generate_model", "gru_step", "load_model", "load_quantized", "qgemm", "qgemm_panel",
     "quantize", "quantize_activations", "quantize_model", "save_model", "synthetic_model", "tensor_specs",

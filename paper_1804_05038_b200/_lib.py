@@ -33,12 +33,15 @@ SIGNATURES = {
     "qnmt_tanh": (I32, [P, I64, I64, I64, P, I64, P, P]),
     "qnmt_attention": (I32, [P, I64, I64, P, P, I32, P, P, P, P, P, I32, I64, I64, P, P, P, I64, P, I64, P, P, P]),
     "qnmt_attention_stats": (I32, [P, P, P, I32, I64, P, P]),
+    "qnmt_attention_f32": (I32, [P, I64, I64, P, P, I32, P, P, P, P, I32, I64, I64, P, P, I64, P, I64, P, P, P]),
+    "qnmt_gemm_f32": (I32, [P, I64, I64, I64, P, I64, I64, P, P, I64, I32, P]),
     "qnmt_log_softmax": (I32, [P, I64, I64, I64, P, I64, P, P]),
     "qnmt_topk_candidates": (I32, [P, I64, I64, I64, P, I32, P, P, P, P]),
     "qnmt_vocab_candidates": (I32, [P, I64, I64, P, P, P, I64, I64, I64, P, I64, P, P, I32, P, P, P, P, P]),
     "qnmt_vocab_candidates_scratch": (I64, [I64, I64]),
     "qnmt_embed_gather": (I32, [P, I64, I64, P, I64, P, I64, P, P]),
     "qnmt_model_create": (I32, [P, P, I32, P]),
+    "qnmt_model_create_f32": (I32, [P, P, I32, P]),
     "qnmt_model_destroy": (I32, [P]),
     "qnmt_engine_create": (I32, [P, I32, I32, I32, P]),
     "qnmt_engine_destroy": (I32, [P]),

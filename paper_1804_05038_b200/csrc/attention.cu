@@ -608,6 +608,76 @@ int attention_launch(const float* u, int64_t ldu, int64_t N, const int32_t* sent
 }
 
 // column -> sentence ranges for callers that only have col_sent (columns grouped by sentence)
+// ---------------------------------------------------------------------------
+// fp32 precision path: the scorer is a float LinearOp, so
+//   score_i = fl32(sum_a f64(v_a) * f64(fl32(tanh(fl32(att_proj[R+i][a] + u[n][a])))))
+// (gemm_f32 of layers.py:226 under the Tier-B fp64 contract), then the same
+// softmax + context kernel as the int8 path.  One warp per (position, sentence)
+// covers every live hypothesis of the sentence, so att_proj is read once.
+// ---------------------------------------------------------------------------
+constexpr int AFW = 8;   // warps (positions) per CTA
+
+__global__ void __launch_bounds__(AFW * 32)
+k_att_score_f32(const float* __restrict__ u, int64_t ldu, const int32_t* __restrict__ sent_col_off,
+                const int32_t* __restrict__ sent_ncols, const float* __restrict__ att_proj,
+                const int64_t* __restrict__ sent_row, const int32_t* __restrict__ sent_len, int64_t A,
+                const float* __restrict__ v, float* __restrict__ scores, int32_t max_len, int32_t* err_flag) {
+    pdl_entry();
+    const int s = blockIdx.y;
+    const int i = blockIdx.x * AFW + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    const int P = sent_ncols[s];
+    if (P == 0 || i >= sent_len[s]) return;
+    const int c0 = sent_col_off[s];
+    const float* ap = att_proj + (sent_row[s] + i) * A;
+    double acc[AMAXP];
+#pragma unroll
+    for (int j = 0; j < AMAXP; ++j) acc[j] = 0.0;
+    bool bad = false;
+    for (int64_t a = lane; a < A; a += 32) {
+        const float at = ap[a];
+        const double va = (double)v[a];
+#pragma unroll
+        for (int j = 0; j < AMAXP; ++j) {
+            if (j < P) {
+                const float x = __fadd_rn(at, u[(int64_t)(c0 + j) * ldu + a]);
+                bad |= !is_finite_f(x);
+                acc[j] = fma(va, (double)tanh_b(x), acc[j]);
+            }
+        }
+    }
+    if (__any_sync(0xffffffffu, bad) && lane == 0) set_flag(err_flag, QNMT_FLAG_NUMERIC);
+#pragma unroll
+    for (int j = 0; j < AMAXP; ++j) {
+        if (j < P) {
+            const double t = warp_sum(acc[j]);
+            if (lane == 0) scores[(int64_t)(c0 + j) * max_len + i] = __double2float_rn(t);
+        }
+    }
+}
+
+int attention_f32_launch(const float* u, int64_t ldu, int64_t N, const int32_t* sent_col_off,
+                         const int32_t* sent_ncols, int32_t n_sent, const float* att_proj, const float* states,
+                         const int64_t* sent_row, const int32_t* sent_len, int32_t max_len, int64_t A, int64_t H2,
+                         const float* v, float* ctx, int64_t ldc, float* alpha, int64_t lda, void* scratch,
+                         int32_t* err_flag, cudaStream_t st) {
+    if (N <= 0 || n_sent <= 0) return QNMT_OK;
+    float* scores = reinterpret_cast<float*>(scratch);   // [N][max_len]
+    const dim3 g1((unsigned)cdiv(max_len, AFW), (unsigned)n_sent);
+    QNMT_LAUNCH(k_att_score_f32, g1, AFW * 32, 0, st, u, ldu, sent_col_off, sent_ncols, att_proj, sent_row, sent_len,
+                A, v, scores, max_len, err_flag);
+    QNMT_CHECK_LAUNCH("k_att_score_f32");
+    const size_t smem = (size_t)AMAXP * max_len * 2 * sizeof(double);
+    const bool v4 = H2 % 4 == 0 && ldc % 4 == 0 && ((uintptr_t)states % 16) == 0 && ((uintptr_t)ctx % 16) == 0;
+    const dim3 g2((unsigned)cdiv(H2, v4 ? 4 * AT : AT), (unsigned)n_sent);
+    if (smem > 48 * 1024)
+        QNMT_CUDA(cudaFuncSetAttribute(k_att_context3, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    QNMT_LAUNCH(k_att_context3, g2, AT, smem, st, scores, max_len, sent_col_off, sent_ncols, states, sent_row, sent_len,
+                H2, ctx, ldc, alpha, lda, err_flag, (uint32_t*)nullptr, v4 ? 1 : 0);
+    QNMT_CHECK_LAUNCH("k_att_context3");
+    return QNMT_OK;
+}
+
 __global__ void k_col_ranges(const int32_t* __restrict__ col_sent, int64_t N, int32_t* off, int32_t* cnt) {
     const int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (n >= N) return;
@@ -643,4 +713,14 @@ extern "C" int qnmt_attention(const float* u, int64_t ldu, int64_t N, const int3
 extern "C" int qnmt_attention_stats(const float* att_proj, const int64_t* sent_row, const int32_t* sent_len,
                                     int32_t n_sent, int64_t A, float* att_minmax, void* stream) {
     return qnmt::att_minmax_launch(att_proj, sent_row, sent_len, n_sent, A, att_minmax, qnmt::as_stream(stream));
+}
+
+extern "C" int qnmt_attention_f32(const float* u, int64_t ldu, int64_t N, const int32_t* sent_col_off,
+                                  const int32_t* sent_ncols, int32_t n_sent, const float* att_proj,
+                                  const float* states, const int64_t* sent_row, const int32_t* sent_len,
+                                  int32_t max_len, int64_t A, int64_t H2, const float* v, float* ctx, int64_t ldc,
+                                  float* alpha, int64_t lda, void* scratch, int32_t* err_flag, void* stream) {
+    return qnmt::attention_f32_launch(u, ldu, N, sent_col_off, sent_ncols, n_sent, att_proj, states, sent_row,
+                                      sent_len, max_len, A, H2, v, ctx, ldc, alpha, lda, scratch, err_flag,
+                                      qnmt::as_stream(stream));
 }

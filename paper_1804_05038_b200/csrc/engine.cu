@@ -49,6 +49,7 @@ struct qnmt_model {
     const int8_t* w_ctx; const float* w_ctx_s;
     const int8_t* w_vocab; const float* w_vocab_s; const float* b_vocab;
     const int8_t* s0_w; const float* s0_s; const float* s0_b;
+    int fp32 = 0;   // 1: the fp32 precision path -- every weight pointer above holds f32 values, no scales
 };
 
 namespace qnmt {
@@ -265,6 +266,10 @@ static int gemm(const int8_t* W, int64_t M, int64_t K, const float* ws, int64_t 
     return gemm_i8_launch(g, st);
 }
 
+static int encode_core_f32(qnmt_engine* e, const int32_t* ids_dev, const int32_t* len, int n, int Lmax, int64_t P,
+                           const std::vector<int>& perm, float* states, float* att_proj, float* s0,
+                           cudaStream_t st);
+
 // ---------------------------------------------------------------------------
 // encoder (layers.py:313-348) for n sentences in arbitrary order.
 //   ids: device, concatenated; len/row: host.  Outputs at caller pointers.
@@ -307,6 +312,7 @@ static int encode_core(qnmt_engine* e, const int32_t* ids_dev, const int32_t* le
     QNMT_CUDA(cudaMemcpyAsync(e->pos_sent, pos_sent.data(), (size_t)P * 4, cudaMemcpyHostToDevice, st));
     QNMT_CUDA(cudaMemcpyAsync(e->s0_dst, s0dst.data(), (size_t)n * 4, cudaMemcpyHostToDevice, st));
 
+    if (m->fp32) return encode_core_f32(e, ids_dev, len, n, Lmax, P, perm, states, att_proj, s0, st);
     // input side for every position at once (per-position scales; one GEMM per direction)
     TRY(embed_gather_launch(m->src_embed, m->Vs, E, ids_dev, P, e->emb_src, E, e->err, st));
     TRY(quantize_launch(e->emb_src, P, E, E, e->iota, (int32_t)P, e->q_emb_src, E, e->sc_pos,
@@ -502,8 +508,87 @@ static int gru_cell(qnmt_engine* e, const Cell& c, const StepIO& io, const int8_
     return QNMT_OK;
 }
 
+// ---------------------------------------------------------------------------
+// fp32 precision path (LinearOp's float branch,
+// layers.py:138-145): the same network with every LinearOp an f32 product
+// (gemm_f32.cu, fp64-evaluated and rounded once) and no quantization.
+// ---------------------------------------------------------------------------
+static inline const float* F(const int8_t* p) { return reinterpret_cast<const float*>(p); }
+
+static int gemm32(const int8_t* W, int64_t M, int64_t K, const float* X, int64_t N, int64_t ldx, const float* bias,
+                  float* Y, int64_t ldy, int32_t flags, cudaStream_t st) {
+    return gemm_f32_launch(F(W), M, K, K, X, N, ldx, bias, Y, ldy, flags, st);
+}
+
+static int encode_core_f32(qnmt_engine* e, const int32_t* ids_dev, const int32_t* len, int n, int Lmax, int64_t P,
+                           const std::vector<int>& perm, float* states, float* att_proj, float* s0,
+                           cudaStream_t st) {
+    const qnmt_model* m = e->m;
+    const int64_t E = m->E, H = m->H, A = m->A;
+    TRY(embed_gather_launch(m->src_embed, m->Vs, E, ids_dev, P, e->emb_src, E, e->err, st));
+    for (int d = 0; d < 2; ++d) {
+        const Cell& c = m->cell[d];
+        TRY(gemm32(c.wx, 3 * H, E, e->emb_src, P, E, c.bx, e->gx_enc + d * 3 * H, 6 * H, 0, st));
+    }
+    QNMT_CUDA(cudaMemsetAsync(e->h2, 0, sizeof(float) * (size_t)n * 2 * H, st));
+    for (int t = 0; t < Lmax; ++t) {
+        int na = 0;
+        while (na < n && len[perm[na]] > t) ++na;
+        const int64_t N2 = 2 * (int64_t)na;
+        const int32_t* gxr = e->enc_rows + (size_t)t * 2 * n;
+        const int32_t* outr = e->enc_out_rows + (size_t)t * 2 * n;
+        for (int d = 0; d < 2; ++d)   // rows of direction d: h2 + d*H with stride 2H
+            TRY(gemm32(m->cell[d].uzr, 2 * H, H, e->h2 + d * H, na, 2 * H, nullptr, e->gh2 + d * 2 * H, 4 * H, 0, st));
+        TRY(gru_gates_launch(e->gx_enc, 3 * H, gxr, e->gh2, 2 * H, e->h2, H, N2, H, e->z2, e->rh2, e->err, st));
+        for (int d = 0; d < 2; ++d)
+            TRY(gemm32(m->cell[d].uc, H, H, e->rh2 + d * H, na, 2 * H, nullptr, e->ghc2 + d * H, 2 * H, 0, st));
+        TRY(gru_combine_launch(e->gx_enc, 3 * H, gxr, e->ghc2, H, e->z2, e->h2, H, N2, H, e->h2, H, states, H, outr,
+                               e->err, st));
+    }
+    TRY(gemm32(m->w_enc, A, 2 * H, states, P, 2 * H, m->b_enc, att_proj, A, 0, st));   // layers.py:343
+    if (m->s0_mode == 1) {
+        QNMT_CUDA(cudaMemsetAsync(s0, 0, sizeof(float) * (size_t)n * H, st));
+    } else {   // s0 = tanh(W_s0 bwd[:, 0] + b): bwd final states are the odd rows of h2 (layers.py:347)
+        TRY(gemm32(m->s0_w, H, H, e->h2 + H, n, 2 * H, m->s0_b, e->s0tmp, H, 0, st));
+        TRY(tanh_launch(e->s0tmp, n, H, H, e->s0tmp, H, e->err, st));
+        TRY(gather_rows_launch(e->s0tmp, nullptr, e->s0_dst, n, H, s0, nullptr, st));
+    }
+    return QNMT_OK;
+}
+
+static int gru_cell_f32(qnmt_engine* e, const Cell& c, const StepIO& io, const float* x, const float* h, float* h_out,
+                        cudaStream_t st) {
+    const int64_t H = e->m->H, N = io.N;
+    TRY(gemm32(c.wx, 3 * H, c.in, x, N, c.in, c.bx, e->gx, 3 * H, 0, st));
+    TRY(gemm32(c.uzr, 2 * H, H, h, N, H, nullptr, e->gh, 2 * H, 0, st));
+    TRY(gru_gates_launch(e->gx, 3 * H, nullptr, e->gh, 2 * H, h, H, N, H, e->z, e->rh, e->err, st));
+    TRY(gemm32(c.uc, H, H, e->rh, N, H, nullptr, e->ghc, H, 0, st));
+    return gru_combine_launch(e->gx, 3 * H, nullptr, e->ghc, H, e->z, h, H, N, H, h_out, H, nullptr, 0, nullptr,
+                              e->err, st);
+}
+
+static int step_core_f32(qnmt_engine* e, const StepIO& io, cudaStream_t st) {
+    const qnmt_model* m = e->m;
+    const int64_t N = io.N, E = m->E, H = m->H, A = m->A, R = m->R, V = m->Vt;
+    TRY(embed_gather_launch(m->tgt_embed, V, E, io.y, N, e->emb, E, e->err, st));
+    TRY(gru_cell_f32(e, m->cell[2], io, e->emb, io.s, io.s_int, st));                  // s' (layers.py:372)
+    const float* query = m->aq == 1 ? io.sp : io.s_int;                                  // layers.py:373
+    TRY(gemm32(m->u_att, A, H, query, N, H, nullptr, e->u, A, 0, st));
+    TRY(attention_f32_launch(e->u, A, N, io.sent_col_off, io.sent_ncols, io.nseg, io.att_proj, io.states, io.sent_row,
+                             io.sent_len, io.max_len, A, 2 * H, F(m->v), e->ctx, 2 * H, io.alpha, io.lda,
+                             e->att_scratch, e->err, st));
+    TRY(gru_cell_f32(e, m->cell[3], io, e->ctx, io.s_int, io.s_new, st));                // s (layers.py:375)
+    // readout = tanh(((W_s s + b_r) + W_e emb) + W_c ctx), logits = W_v readout + b_v (layers.py:255-266)
+    TRY(gemm32(m->w_state, R, H, io.s_new, N, H, m->b_r, e->ro, R, 0, st));
+    TRY(gemm32(m->w_embed, R, E, e->emb, N, E, nullptr, e->ro, R, QNMT_GEMM_ACCUMULATE, st));
+    TRY(gemm32(m->w_ctx, R, 2 * H, e->ctx, N, 2 * H, nullptr, e->ro, R, QNMT_GEMM_ACCUMULATE, st));
+    TRY(tanh_launch(e->ro, N, R, R, e->ro, R, e->err, st));
+    return gemm32(m->w_vocab, V, R, e->ro, N, R, m->b_vocab, io.logits, V, 0, st);
+}
+
 static int step_core(qnmt_engine* e, const StepIO& io, cudaStream_t st) {
     const qnmt_model* m = e->m;
+    if (m->fp32) return io.N > 0 ? step_core_f32(e, io, st) : QNMT_OK;
     const int64_t N = io.N, E = m->E, H = m->H, A = m->A, R = m->R, V = m->Vt;
     const int32_t* seg = io.col_sent;
     const int ns = io.nseg;
@@ -607,7 +692,7 @@ static int gather_next(qnmt_engine* e, int cur, int64_t N2, int n, int beam, cud
 
 static bool vocab_fusable(const qnmt_engine* e, int k) {
     const qnmt_model* m = e->m;
-    return g_vocab_fused && g_gemm_impl != 1 && vocab_topk_eligible(m->R, m->R, m->R, e->q_ro, m->w_vocab, k);
+    return !m->fp32 && g_vocab_fused && g_gemm_impl != 1 && vocab_topk_eligible(m->R, m->R, m->R, e->q_ro, m->w_vocab, k);
 }
 
 // beam candidates of the step: fused vocab projection + statistics + merge, or
@@ -696,6 +781,12 @@ int qnmt_model_create(const int32_t* dims, const void* const* t, int32_t nt, qnm
     m->s0_w = (const int8_t*)t[QNMT_T_S0_W]; m->s0_s = (const float*)t[QNMT_T_S0_W_SCALE];
     m->s0_b = (const float*)t[QNMT_T_S0_B];
     *out = m;
+    return QNMT_OK;
+}
+
+int qnmt_model_create_f32(const int32_t* dims, const void* const* t, int32_t nt, qnmt_model** out) {
+    TRY(qnmt_model_create(dims, t, nt, out));
+    (*out)->fp32 = 1;
     return QNMT_OK;
 }
 
@@ -835,10 +926,10 @@ int qnmt_engine_create(const qnmt_model* m, int32_t max_sentences, int32_t max_s
     cudaMemset(e->err, 0, 16);
     {   // per-sentence fused op + quantize: [16 columns][max(E, H, R)] values, gather [2][B][H]
         const size_t d = std::max(E, std::max(H, R));
-        e->fq_ok = 16 * d * 4 <= FQ_SMEM_MAX && 2 * B * H * 4 <= FQ_SMEM_MAX && E % 4 == 0 && H % 4 == 0 &&
+        e->fq_ok = !m->fp32 && 16 * d * 4 <= FQ_SMEM_MAX && 2 * B * H * 4 <= FQ_SMEM_MAX && E % 4 == 0 && H % 4 == 0 &&
                    R % 4 == 0 && ((uintptr_t)m->tgt_embed % 16) == 0;   // float4 groups (fused_q.cu)
     }
-    if (E % 16 == 0 && H % 16 == 0 && A % 16 == 0 && R % 16 == 0) {   // stacked weights (tcgen05 path)
+    if (!m->fp32 && E % 16 == 0 && H % 16 == 0 && A % 16 == 0 && R % 16 == 0) {   // stacked weights (tcgen05 path)
         auto host_scale = [](const float* d) { float v = 0; cudaMemcpy(&v, d, 4, cudaMemcpyDeviceToHost); return v; };
         std::vector<float> sc;
         auto stack = [&](int8_t* dst, const int8_t* a0, size_t rows0, const int8_t* a1, size_t rows1, size_t K) {
@@ -980,7 +1071,7 @@ int qnmt_decoder_step(qnmt_engine* e, int64_t N, const int32_t* col_sent, int32_
 // ---------------------------------------------------------------------------
 static bool graph_eligible(const qnmt_engine* e) {
     const qnmt_model* m = e->m;
-    return e->use_graphs && !e->prof_on && g_gemm_impl != 1 && m->E % 16 == 0 && m->H % 16 == 0 &&
+    return e->use_graphs && !e->prof_on && !m->fp32 && g_gemm_impl != 1 && m->E % 16 == 0 && m->H % 16 == 0 &&
            m->A % 16 == 0 && m->R % 16 == 0;
 }
 

@@ -31,6 +31,13 @@ int att_minmax_launch(const float* att_proj, const int64_t* sent_row, const int3
                       int64_t A, float* mm, cudaStream_t st);
 int col_ranges_launch(const int32_t* col_sent, int64_t N, int32_t n_sent, int32_t* off, int32_t* cnt,
                       cudaStream_t st);
+int gemm_f32_launch(const float* W, int64_t M, int64_t K, int64_t ldw, const float* X, int64_t N, int64_t ldx,
+                    const float* bias, float* Y, int64_t ldy, int32_t flags, cudaStream_t st);
+int attention_f32_launch(const float* u, int64_t ldu, int64_t N, const int32_t* sent_col_off,
+                         const int32_t* sent_ncols, int32_t n_sent, const float* att_proj, const float* states,
+                         const int64_t* sent_row, const int32_t* sent_len, int32_t max_len, int64_t A, int64_t H2,
+                         const float* v, float* ctx, int64_t ldc, float* alpha, int64_t lda, void* scratch,
+                         int32_t* err_flag, cudaStream_t st);
 struct EnsRows {
     const float* p[QNMT_ENS_MAX];   // member logits [N][ld], same layout
 };

@@ -10,20 +10,21 @@ search state), so results are identical to a sentence-by-sentence loop.
 from __future__ import annotations
 
 import math
-from dataclasses import dataclass
+from dataclasses import dataclass, field
 
 import numpy as np
 
-from .errors import ConfigError, EmptyInputError
+from .bleu import bleu
+from .errors import ConfigError, EmptyInputError, QnmtError
 from .engine import Engine, translate_ensemble_ids
-from .model import EOS_ID, ModelParams, QuantizedModel, quantize_model
+from .model import EOS_ID, Float32Model, ModelParams, QuantizedModel, quantize_model, to_device_f32
 
 
 @dataclass
 class DecodeConfig:
     beam: int = 5
     max_ratio: float = 3.0        # max output length = ceil(ratio * source len) + 1
-    precision: str = "int8"       # the B200 path decodes int8 (fp32 is SURVEY 8(f) "next")
+    precision: str = "int8"       # "int8" (the B200 hot path) or "fp32"; the reference defaults to fp32
 
     def __post_init__(self):
         if self.beam < 1:
@@ -44,11 +45,11 @@ class BeamHypothesis:
     finished: bool = False
 
 
-def _members(models) -> list:
-    """Ensemble members as device int8 models (decoder.py:46-71): a single model
-    or a non-empty list sharing one target vocabulary; float parameters are
-    quantized once and cached."""
-    if isinstance(models, (ModelParams, QuantizedModel)):
+def _members(models, precision: str = "int8") -> list:
+    """Ensemble members as device models (decoder.py:46-71): a single model or a
+    non-empty list sharing one target vocabulary.  int8: float parameters are
+    quantized once and cached; fp32: float parameters only (uploaded once)."""
+    if isinstance(models, (ModelParams, QuantizedModel, Float32Model)):
         members = [models]
     else:
         members = list(models)
@@ -60,6 +61,12 @@ def _members(models) -> list:
             raise ConfigError("ensemble members must share the target vocabulary")
     if len(members) > 8:
         raise ConfigError("ensembles of more than 8 members are not supported")
+    if precision == "fp32":
+        if any(isinstance(m, QuantizedModel) for m in members):
+            raise ConfigError("fp32 decoding requires float parameters")
+        return [to_device_f32(m) if isinstance(m, ModelParams) else m for m in members]
+    if any(isinstance(m, Float32Model) for m in members):
+        raise ConfigError("int8 decoding needs ModelParams or QuantizedModel members")
     return [_quantized_cache(m) if isinstance(m, ModelParams) else m for m in members]
 
 
@@ -109,8 +116,6 @@ def _engines_for(members, n: int, length: int, beam: int) -> list:
 
 
 def _check_cfg(cfg: DecodeConfig):
-    if cfg.precision != "int8":
-        raise ConfigError("the B200 path decodes int8 only (fp32 decoding is not implemented)")
     if cfg.beam > 16:
         raise ConfigError("beam > 16 is not supported by the device search")
 
@@ -143,7 +148,7 @@ def translate(models, source_tokens, cfg: DecodeConfig, timer=None):
     if not tokens:
         raise EmptyInputError("cannot translate an empty sentence")
     _check_cfg(cfg)
-    members = _members(models)
+    members = _members(models, cfg.precision)
     ids = [[m.src_ids(tokens)] for m in members]
     out, lp = next(_decode_ids(members, ids, cfg, 1))
     return [members[0].tgt_tokens[i] for i in out], lp
@@ -156,7 +161,7 @@ def translate_batch(models, sentences, cfg: DecodeConfig, max_batch: int = 256, 
     whitespace strings, or (``return_ids``) id lists.  Output order follows
     the input.  Each batch of up to ``max_batch`` sentences is one engine call."""
     _check_cfg(cfg)
-    members = _members(models)
+    members = _members(models, cfg.precision)
     sents = [s.split() if isinstance(s, str) else list(s) for s in sentences]
     if not sents:
         return []
@@ -190,5 +195,60 @@ def bpe_merge(tokens) -> str:
     return " ".join(words)
 
 
+def edit_distance(a, b) -> int:
+    """Levenshtein distance between two token sequences (decoder.py:180-190)."""
+    if len(a) < len(b):
+        a, b = b, a
+    row = list(range(len(b) + 1))
+    for i, x in enumerate(a, 1):
+        prev_diag, row[0] = row[0], i
+        for j, y in enumerate(b, 1):
+            cur = min(row[j] + 1, row[j - 1] + 1, prev_diag + (x != y))
+            prev_diag, row[j] = row[j], cur
+    return row[-1]
+
+
+@dataclass
+class ParityReport:
+    """Output agreement between the two precision modes on one corpus (decoder.py:193-213)."""
+
+    sentences: int
+    identical: int
+    identical_fraction: float
+    edit_distances: list
+    mean_edit_distance: float
+    bleu_int8_vs_fp32: float
+    fp32_outputs: list = field(repr=False, default_factory=list)
+    int8_outputs: list = field(repr=False, default_factory=list)
+
+    def to_dict(self) -> dict:
+        return {"sentences": self.sentences, "identical": self.identical,
+                "identical_fraction": self.identical_fraction, "mean_edit_distance": self.mean_edit_distance,
+                "bleu_int8_vs_fp32": self.bleu_int8_vs_fp32, "edit_distances": list(self.edit_distances)}
+
+
+def compare_precisions(model: ModelParams, sentences, cfg: DecodeConfig, max_batch: int = 256) -> ParityReport:
+    """Decode every sentence under fp32 and int8 and measure agreement
+    (decoder.py:216-248).  Both precisions run batched on the device; results
+    are identical to the reference's sentence-by-sentence loop."""
+    sents = [s.split() if isinstance(s, str) else list(s) for s in sentences]
+    if not sents:
+        raise EmptyInputError("no sentences to compare")
+    for i, s in enumerate(sents):
+        if not s:
+            raise EmptyInputError(f"sentence {i}: cannot translate an empty sentence")
+    if not isinstance(model, ModelParams):
+        raise ConfigError("compare_precisions needs float parameters")
+    out32 = translate_batch(model, sents, DecodeConfig(cfg.beam, cfg.max_ratio, "fp32"), max_batch)
+    out8 = translate_batch(model, sents, DecodeConfig(cfg.beam, cfg.max_ratio, "int8"), max_batch)
+    d = [edit_distance(a[0], b[0]) for a, b in zip(out32, out8)]
+    same = sum(a[0] == b[0] for a, b in zip(out32, out8))
+    f32_txt = [bpe_merge(a[0]) for a in out32]
+    i8_txt = [bpe_merge(b[0]) for b in out8]
+    return ParityReport(sentences=len(sents), identical=same, identical_fraction=same / len(sents),
+                        edit_distances=d, mean_edit_distance=float(np.mean(d)),
+                        bleu_int8_vs_fp32=bleu(i8_txt, f32_txt), fp32_outputs=f32_txt, int8_outputs=i8_txt)
+
+
 __all__ = ["DecodeConfig", "BeamHypothesis", "translate", "translate_batch", "bpe_merge",
-           "max_steps", "EOS_ID"]
+           "max_steps", "EOS_ID", "edit_distance", "ParityReport", "compare_precisions"]

@@ -11,8 +11,9 @@ Two device compositions exist and are tested against the oracle:
   :meth:`OutputNet.logits`) -- one C-ABI op per reference operation;
 * the engine path (:meth:`Network.encode`, :meth:`Network.decoder_step`,
   and decoder.translate) -- csrc/engine.cu, the production path.
-Only the int8 precision is implemented on B200 (SURVEY.md 8(f) ranks the fp32
-path as next); fp32 LinearOps raise ConfigError.
+Both precisions run on B200: int8 LinearOps quantize + tcgen05/dp4a GEMM; float
+LinearOps (the fp32 path, layers.py:138-145) use csrc/gemm_f32.cu, evaluated in
+fp64 and rounded once (the Tier-B contract of gemm_f32).
 """
 
 from __future__ import annotations
@@ -25,7 +26,7 @@ import torch
 from . import _dev, _lib
 from .engine import Engine
 from .errors import ConfigError, ShapeError, VocabError, EmptyInputError
-from .qmath import QuantizedMatrix, gemm_kmajor
+from .qmath import QuantizedMatrix, gemm_f32_kmajor, gemm_kmajor
 
 F32 = np.float32
 
@@ -83,10 +84,21 @@ def _log_softmax_cols(v):
 
 @dataclass(eq=False)
 class LinearOp:
-    """A trained linear transform ``y = W x (+ b)`` (layers.py:94-146)."""
+    """A trained linear transform ``y = W x (+ b)`` (layers.py:94-146): ``weight``
+    is a :class:`QuantizedMatrix` (int8 path) or a float32 ``[out, in]`` matrix
+    (fp32 path, numpy or device tensor)."""
 
-    weight: QuantizedMatrix
+    weight: object
     bias: object = None
+
+    def _wdev(self) -> torch.Tensor:
+        w = getattr(self, "_wd", None)
+        if w is None:
+            if len(np.shape(self.weight)) != 2 or min(np.shape(self.weight)) < 1:
+                raise ShapeError(f"weight must be a non-empty 2-D matrix, got shape {tuple(np.shape(self.weight))}")
+            w = _dev.to_device(self.weight).contiguous()
+            self._wd = w
+        return w
 
     @property
     def is_quantized(self) -> bool:
@@ -111,9 +123,10 @@ class LinearOp:
 
     def apply_k(self, x_k: torch.Tensor, out: torch.Tensor | None = None, accumulate=False,
                 col_seg=None, nseg=1) -> torch.Tensor:
-        """K-major core: x_k [P][in] device f32 -> y_k [P][out] (quantize + GEMM + bias)."""
+        """K-major core: x_k [P][in] device f32 -> y_k [P][out] (quantize + GEMM + bias,
+        or the fp32 product + bias)."""
         if not self.is_quantized:
-            raise ConfigError("the B200 path implements int8 LinearOps only")
+            return gemm_f32_kmajor(self._wdev(), x_k, bias=self._bias_dev(), Y=out, accumulate=accumulate)
         q, sx = _quant_k(x_k, col_seg, nseg)
         return gemm_kmajor(self.weight.device_data(), self.weight.device_scale(), self.out_dim, q, sx,
                            col_seg=col_seg, bias=self._bias_dev(), Y=out, accumulate=accumulate,
@@ -151,6 +164,15 @@ class GruCell:
     def packed(self):
         """Stacked device weights: WX=[wz;wr;wc] (3 scales), BX, UZR=[uz;ur] (2 scales), UC."""
         p = getattr(self, "_packed", None)
+        if p is None and not self.update_in.is_quantized:   # fp32: WX, BX, UZR, UC without scales
+            ins = (self.update_in, self.reset_in, self.cand_in)
+            wx = torch.cat([o._wdev() for o in ins]).contiguous()
+            dev = wx.device
+            bx = torch.cat([o._bias_dev() if o.bias is not None
+                            else torch.zeros(self.hidden, dtype=torch.float32, device=dev) for o in ins])
+            uzr = torch.cat([self.update_state._wdev(), self.reset_state._wdev()]).contiguous()
+            p = (wx, None, bx.contiguous(), uzr, None, self.cand_state._wdev(), None)
+            self._packed = p
         if p is None:
             ins = (self.update_in, self.reset_in, self.cand_in)
             wx = torch.cat([o.weight.device_data() for o in ins]).contiguous()
@@ -173,18 +195,26 @@ def gru_step_k(cell: GruCell, x_k: torch.Tensor, h_k: torch.Tensor, col_seg=None
     wx, wxs, bx, uzr, uzrs, uc, ucs = cell.packed()
     H = cell.hidden
     P = x_k.shape[0]
-    qx, sx = _quant_k(x_k, col_seg, nseg)
-    qh, sh = _quant_k(h_k, col_seg, nseg)
-    gx = gemm_kmajor(wx, wxs, H, qx, sx, col_seg=col_seg, bias=bx, w_static=True)   # [P][3H]
-    gh = gemm_kmajor(uzr, uzrs, H, qh, sh, col_seg=col_seg, w_static=True)   # [P][2H]
+    f32 = wxs is None
+    if f32:   # fp32 path: float products, no quantization
+        gx = gemm_f32_kmajor(wx, x_k, bias=bx)
+        gh = gemm_f32_kmajor(uzr, h_k)
+    else:
+        qx, sx = _quant_k(x_k, col_seg, nseg)
+        qh, sh = _quant_k(h_k, col_seg, nseg)
+        gx = gemm_kmajor(wx, wxs, H, qx, sx, col_seg=col_seg, bias=bx, w_static=True)   # [P][3H]
+        gh = gemm_kmajor(uzr, uzrs, H, qh, sh, col_seg=col_seg, w_static=True)   # [P][2H]
     z = torch.empty((P, H), dtype=torch.float32, device=x_k.device)
     rh = torch.empty_like(z)
     flag = _dev.flag()
     st = _dev.stream_ptr()
     _lib.call("qnmt_gru_gates", gx.data_ptr(), 3 * H, None, gh.data_ptr(), 2 * H, h_k.data_ptr(),
               _dev.ld(h_k), P, H, z.data_ptr(), rh.data_ptr(), flag.data_ptr(), st)
-    qr, sr = _quant_k(rh, col_seg, nseg)
-    ghc = gemm_kmajor(uc, ucs, H, qr, sr, col_seg=col_seg, w_static=True)    # [P][H]
+    if f32:
+        ghc = gemm_f32_kmajor(uc, rh)
+    else:
+        qr, sr = _quant_k(rh, col_seg, nseg)
+        ghc = gemm_kmajor(uc, ucs, H, qr, sr, col_seg=col_seg, w_static=True)    # [P][H]
     out = torch.empty_like(z)
     _lib.call("qnmt_gru_combine", gx.data_ptr(), 3 * H, None, ghc.data_ptr(), H, z.data_ptr(),
               h_k.data_ptr(), _dev.ld(h_k), P, H, out.data_ptr(), H, None, 0, None, flag.data_ptr(), st)
@@ -280,6 +310,12 @@ def attend_k(att: AttentionNet, q_k: torch.Tensor, enc: EncoderStates):
     v = att.scorer.weight
     if P > 16:
         raise ShapeError("attend supports at most 16 query columns per call")
+    if not att.scorer.is_quantized:   # fp32 scorer (layers.py:226 with a float LinearOp)
+        _lib.call("qnmt_attention_f32", u.data_ptr(), A, P, col_off.data_ptr(), ncols.data_ptr(), 1,
+                  enc.att_proj_k.data_ptr(), enc.states_k.data_ptr(), sent_row.data_ptr(), sent_len.data_ptr(),
+                  length, A, H2, att.scorer._wdev().data_ptr(), ctx.data_ptr(), H2, alpha.data_ptr(), length,
+                  scratch.data_ptr(), _dev.flag().data_ptr(), _dev.stream_ptr())
+        return ctx, alpha
     _lib.call("qnmt_attention", u.data_ptr(), A, P, col_off.data_ptr(), ncols.data_ptr(), 1,
               enc.att_proj_k.data_ptr(), None,
               enc.states_k.data_ptr(), sent_row.data_ptr(), sent_len.data_ptr(), length, A, H2,
@@ -435,14 +471,23 @@ def decoder_step(network: Network, y_prev, state, enc, timer=None):
 
 
 def build_network(model, timer=None) -> Network:
-    """Wrap a :class:`QuantizedModel` in an inference network (layers.py:395-435)."""
-    from .model import QuantizedModel
-    if not isinstance(model, QuantizedModel):
-        raise ConfigError("the B200 path needs a QuantizedModel (see quantize_model)")
-    q, f = model.q, model.f
+    """Wrap a float (:class:`ModelParams`, fp32 path) or quantized parameter set
+    in an inference network (layers.py:395-435)."""
+    from .model import Float32Model, ModelParams, QuantizedModel, to_device_f32
+    if isinstance(model, ModelParams):
+        model = to_device_f32(model)
+    if isinstance(model, Float32Model):
+        f = model.f
 
-    def lin(name, bias=None):
-        return LinearOp(q[name], f[bias] if bias else None)
+        def lin(name, bias=None):
+            return LinearOp(f[name], f[bias] if bias else None)
+    elif isinstance(model, QuantizedModel):
+        q, f = model.q, model.f
+
+        def lin(name, bias=None):
+            return LinearOp(q[name], f[bias] if bias else None)
+    else:
+        raise ConfigError("build_network needs ModelParams or a QuantizedModel")
 
     def cell(p) -> GruCell:
         return GruCell(update_in=lin(f"{p}.wz", f"{p}.bz"), update_state=lin(f"{p}.uz"),

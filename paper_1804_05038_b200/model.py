@@ -248,6 +248,90 @@ class QuantizedModel:
             pass
 
 
+class Float32Model:
+    """Device-resident fp32 model for the fp32 precision path:
+    every tensor of ``tensor_specs`` as a device f32 tensor in ``f``, the GRU
+    gates packed like the int8 model (``WX = [wz; wr; wc]``, ``UZR``, ``UC``), and
+    a C model handle created with ``qnmt_model_create_f32``.  Built from (and
+    cached on) a :class:`ModelParams` by :func:`to_device_f32`."""
+
+    precision = "fp32"
+
+    def __init__(self, params: ModelParams):
+        self.dims = params.dims
+        self.src_tokens, self.tgt_tokens = params.src_tokens, params.tgt_tokens
+        self.s0_mode, self.attention_query = params.s0_mode, params.attention_query
+        self._src_index = None
+        self._handle = None
+        self._keep = []
+        self.f = {}
+        for name, _ in tensor_specs(params.dims):
+            arr = params.tensors[name]
+            t = arr if isinstance(arr, torch.Tensor) else _dev.to_device(np.ascontiguousarray(arr, dtype=np.float32))
+            self.f[name] = t.to(dtype=torch.float32).contiguous()
+
+    src_ids = ModelParams.src_ids
+    tgt_token = ModelParams.tgt_token
+
+    def packed_cell(self, cell: str):
+        """(WX [3H,in] f32, None, BX [3H], UZR [2H,H], None, UC, None) -- int8 layout without scales."""
+        key = f"_packed_{cell}"
+        if not hasattr(self, key):
+            f = self.f
+            wx = torch.cat([f[f"{cell}.w{g}"] for g in "zrc"]).contiguous()
+            bx = torch.cat([f[f"{cell}.b{g}"] for g in "zrc"]).contiguous()
+            uzr = torch.cat([f[f"{cell}.u{g}"] for g in "zr"]).contiguous()
+            setattr(self, key, (wx, None, bx, uzr, None, f[f"{cell}.uc"], None))
+        return getattr(self, key)
+
+    def handle(self):
+        if self._handle is None:
+            ptrs = [0] * 50
+            keep = []
+
+            def put(i, t):
+                if t is not None:
+                    keep.append(t)
+                    ptrs[i] = t.data_ptr()
+
+            f = self.f
+            put(0, f["src_embed"])
+            put(1, f["tgt_embed"])
+            for c, cell in enumerate(CELLS):
+                for j, t in enumerate(self.packed_cell(cell)):
+                    put(2 + 7 * c + j, t)
+            for i, name in ((30, "attn.w_enc"), (32, "attn.b_enc"), (33, "attn.u_state"), (35, "attn.v"),
+                            (37, "out.w_state"), (39, "out.b_readout"), (40, "out.w_embed"), (42, "out.w_ctx"),
+                            (44, "out.w_vocab"), (46, "out.b_vocab"), (47, "s0.w"), (49, "s0.b")):
+                put(i, f[name])
+            d = self.dims
+            dims = (C.c_int32 * 8)(d.src_vocab, d.tgt_vocab, d.embed, d.hidden, d.attn, d.readout,
+                                   1 if self.s0_mode == "zero" else 0,
+                                   1 if self.attention_query == "previous" else 0)
+            arr = (C.c_void_p * 50)(*ptrs)
+            h = C.c_void_p()
+            _lib.call("qnmt_model_create_f32", C.cast(dims, C.c_void_p), C.cast(arr, C.c_void_p), 50, C.byref(h))
+            self._keep = keep
+            self._handle = h
+        return self._handle
+
+    def __del__(self):
+        try:
+            if self._handle is not None:
+                _lib.load().qnmt_model_destroy(self._handle)
+        except Exception:
+            pass
+
+
+def to_device_f32(params: ModelParams) -> Float32Model:
+    """The fp32 device model of ``params`` (uploaded once, cached on ``params``)."""
+    m = getattr(params, "_b200_f32", None)
+    if m is None:
+        m = Float32Model(params)
+        params._b200_f32 = m
+    return m
+
+
 def _quantize_tensors(dims: Dims, tensors: dict, src_tokens, tgt_tokens, s0_mode, attention_query,
                       with_stats: bool) -> QuantizedModel:
     q, f, stats = {}, {}, {}

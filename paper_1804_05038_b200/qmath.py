@@ -195,6 +195,34 @@ def gemm_kmajor(W: torch.Tensor, w_scales: torch.Tensor, rows_per_scale: int, X:
     return Y
 
 
+def gemm_f32_kmajor(W: torch.Tensor, X: torch.Tensor, bias=None, Y=None, accumulate=False) -> torch.Tensor:
+    """fp32-path product in kernel layout: Y[N][M] = fl32(W[M][K] . X[N][K]) (fp64
+    evaluation, csrc/gemm_f32.cu) (+ bias) (+ Y)."""
+    M, K = W.shape
+    N = X.shape[0]
+    if X.shape[1] != K:
+        raise ShapeError(f"inner dimensions disagree: {M}x{K} @ {X.shape[1]}x{N}")
+    if Y is None:
+        Y = torch.empty((N, M), dtype=torch.float32, device=W.device)
+    _lib.call("qnmt_gemm_f32", W.data_ptr(), M, K, _dev.ld(W), X.data_ptr(), N, _dev.ld(X), _dev.ptr(bias),
+              Y.data_ptr(), _dev.ld(Y), _lib.GEMM_ACCUMULATE if accumulate else 0, _dev.stream_ptr())
+    return Y
+
+
+def gemm_f32(a, b):
+    """Standard float32 product (qmath.py:434-440), on the device: fp64-evaluated,
+    rounded once (numpy in -> numpy out)."""
+    for name, m in (("a", a), ("b", b)):
+        if len(np.shape(m)) != 2 or min(np.shape(m)) < 1:
+            raise ShapeError(f"{name} must be a non-empty 2-D matrix, got shape {tuple(np.shape(m))}")
+    if np.shape(a)[1] != np.shape(b)[0]:
+        raise ShapeError(f"inner dimensions disagree: {tuple(np.shape(a))} @ {tuple(np.shape(b))}")
+    W = _dev.to_device(a).contiguous()
+    X = _dev.kmajor(b)
+    Y = gemm_f32_kmajor(W, X).t()
+    return Y.contiguous().cpu().numpy() if _dev.is_numpy(a) or _dev.is_numpy(b) else Y
+
+
 def qgemm(a: QuantizedMatrix, b: QuantizedMatrix):
     """Quantized product with exact integer accumulation, emitted as float32.
 

@@ -370,6 +370,80 @@ def gen_ensemble():
     print("ensemble_small.json:", len(out["cases"]), "cases")
 
 
+def gen_fp32():
+    """The reference's fp32 path (precision="fp32": LinearOp's float branch,
+    layers.py:138-145): Tier-B / Tier-A translations, op-level outputs, a
+    compare_precisions report, and BLEU / edit-distance known answers."""
+    import importlib
+    ref_bleu = importlib.import_module("qnmt.bleu")
+    from qnmt import decoder as ref_decoder
+    out = {"cases": [], "ops": {}, "parity": {}, "bleu": [], "edit": []}
+    arrays = {}
+    for tag, dims_kw, seed, ws, bs, eb, s0m, aq in MODELS:
+        dims = ref_model.Dims(**dims_kw)
+        params, _ = make_params(dims, seed, bias_std=bs, weight_std=ws, eos_bias=eb, s0_mode=s0m,
+                                attention_query=aq)
+        rng = np.random.default_rng(400 + seed)
+        for n in range(8):
+            length = int(rng.integers(1, 10))
+            ids = rng.integers(3, dims.src_vocab, length).tolist()
+            beam = [1, 3, 5, 2][n % 4]
+            ratio = [1.5, 3.0, 2.0][n % 3]
+            toks = [params.src_tokens[i] for i in ids]
+            cfg = DecodeConfig(beam=beam, max_ratio=ratio, precision="fp32")
+            case = {"model": tag, "src": ids, "beam": beam, "max_ratio": ratio}
+            for tier in ("A", "B"):
+                ctx = tier_b() if tier == "B" else contextlib.nullcontext()
+                with ctx:
+                    words, logp = translate(params, toks, cfg)
+                tgt_index = {t: i for i, t in enumerate(params.tgt_tokens)}
+                case[f"out_{tier}"] = [tgt_index[w] for w in words]
+                case[f"logp_{tier}"] = logp
+            out["cases"].append(case)
+        # op level, Tier B: encoder outputs and one decoder step at P = 3
+        with tier_b():
+            net = ref_layers.build_network(params)
+            src = rng.integers(3, dims.src_vocab, 6)
+            enc = net.encode(src)
+            st = net.initial_state(enc, 3)
+            y = rng.integers(0, dims.tgt_vocab, 3)
+            lp, st2, alpha = net.decoder_step(y, st, enc)
+            x = rng.normal(0, 1, (dims.embed, 4)).astype(F32)
+            lin = net.dec_r.update_in.apply(x)
+        for k, v in (("src", src), ("states", enc.states), ("att_proj", enc.att_proj), ("s0", enc.s0), ("y", y),
+                     ("lp", lp), ("s_new", st2.s), ("s_int", st2.s_prime), ("alpha", alpha), ("x", x),
+                     ("lin_wz", lin)):
+            arrays[f"{tag}_{k}"] = np.asarray(v)
+        if tag in ("eos", "med"):   # compare_precisions (Tier B) over a small corpus
+            corpus = [[params.src_tokens[i] for i in rng.integers(3, dims.src_vocab, int(rng.integers(1, 9)))]
+                      for _ in range(12)]
+            with tier_b():
+                rep = ref_decoder.compare_precisions(params, corpus, DecodeConfig(beam=3, max_ratio=1.5))
+            out["parity"][tag] = {"corpus": corpus, "report": rep.to_dict(), "fp32": rep.fp32_outputs,
+                                  "int8": rep.int8_outputs}
+    rng = np.random.default_rng(77)
+    for _ in range(40):   # BLEU / edit distance known answers
+        nl = int(rng.integers(1, 5))
+        hyps = [[f"t{v}" for v in rng.integers(0, 6, int(rng.integers(0, 12)))] for _ in range(nl)]
+        refs = [[f"t{v}" for v in rng.integers(0, 6, int(rng.integers(0, 12)))] for _ in range(nl)]
+        if _ % 2:   # near-copies: non-zero scores
+            refs = [[f"t{v}" for v in rng.integers(0, 9, int(rng.integers(4, 14)))] for _ in range(nl)]
+            hyps = [r[:int(rng.integers(1, len(r) + 1))] + [f"t{int(rng.integers(0, 9))}"] for r in refs]
+        try:
+            b = ref_bleu.bleu([" ".join(h) for h in hyps], [" ".join(r) for r in refs])
+        except Exception as exc:   # noqa: BLE001
+            b = type(exc).__name__
+        out["bleu"].append({"hyps": hyps, "refs": refs, "bleu": b})
+        out["edit"].append({"a": hyps[0], "b": refs[0], "d": ref_decoder.edit_distance(hyps[0], refs[0])})
+    out["models"] = {m[0]: dict(dims=m[1], seed=m[2], weight_std=m[3], bias_std=m[4], eos_bias=m[5],
+                                s0_mode=m[6], attention_query=m[7]) for m in MODELS}
+    with open(os.path.join(HERE, "fp32_small.json"), "w") as fh:
+        json.dump(out, fh, indent=1)
+    np.savez_compressed(os.path.join(HERE, "fp32_ops.npz"), **arrays)
+    print("fp32_small.json:", len(out["cases"]), "translations,", len(out["parity"]), "parity reports;",
+          "fp32_ops.npz:", len(arrays), "arrays")
+
+
 MODELFILE_ARGS = dict(src_vocab=14, tgt_vocab=13, embed=4, hidden=6, seed=11, attn=5, readout=3)
 
 
@@ -403,7 +477,9 @@ def gen_modelfile():
 
 
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["qmath", "small", "baseline", "modelfile", "ensemble"]
+    which = sys.argv[1:] or ["qmath", "small", "baseline", "modelfile", "ensemble", "fp32"]
+    if "fp32" in which:
+        gen_fp32()
     if "ensemble" in which:
         gen_ensemble()
     if "modelfile" in which:
