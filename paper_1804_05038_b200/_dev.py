@@ -63,7 +63,10 @@ def to_device(x, dtype=torch.float32) -> torch.Tensor:
     dev = require_cuda()
     if isinstance(x, torch.Tensor):
         return x.to(device=dev, dtype=dtype)
-    return torch.from_numpy(np.ascontiguousarray(x)).to(device=dev, dtype=dtype)
+    a = np.ascontiguousarray(x)
+    if not a.flags.writeable:   # e.g. load_model's read-only views of the file bytes
+        a = a.copy()
+    return torch.from_numpy(a).to(device=dev, dtype=dtype)
 
 
 def kmajor(x, dtype=torch.float32) -> torch.Tensor:

@@ -43,6 +43,21 @@ class Engine:
         except Exception:
             pass
 
+    # -- phase profiler (eager steps, CUDA events per phase group) -------------
+    PHASE_GROUPS = ("encoder", "embedding", "quantize-activations", "matmul", "gru", "attention", "matmul-vocab",
+                    "topk", "search", "gather", "other")
+
+    def profile(self, enable: bool):
+        """Enable (resetting the totals) or disable the engine's phase profiler;
+        while enabled the decode loop runs eagerly (no CUDA graphs)."""
+        _lib.call("qnmt_engine_profile", self._h, 1 if enable else 0)
+
+    def profile_read(self) -> dict:
+        """{group: milliseconds} accumulated since :meth:`profile` (True)."""
+        ms, calls, ops, nb = ((C.c_double * 16)() for _ in range(4))
+        n = _lib.load().qnmt_engine_profile_read(self._h, ms, calls, ops, nb)
+        return {self.PHASE_GROUPS[i]: ms[i] for i in range(min(n, len(self.PHASE_GROUPS)))}
+
     # -- encoder -------------------------------------------------------------
     def encode_batch(self, id_lists):
         """Returns device (states [sum_l][2H], att_proj [sum_l][A], s0 [n][H], rows)."""
