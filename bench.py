@@ -4,17 +4,21 @@
 Workload (BASELINE.json configs[4], the config the metric is quoted on at
 1/2/4/8 B200): V_src 32000, V_tgt 50000, E 512, H 1024, A 2048, R 512, beam 5,
 max_ratio 1.5, a seeded 8192-sentence corpus with lengths ~ U[5, 100]; one
-"step" = one batch of 256 sentences per GPU (weak scaling: every rank decodes
-its own batch, no collective on the data path).  Seeded N(0, 0.05) weights,
-uniform synthetic token ids (no datasets / checkpoints in this environment).
+"step" = one pass over the whole corpus: it is sorted by length, cut into
+batches of 256 sentences (one engine call each) and the batches are dealt
+round-robin to the GPUs (strong scaling: the corpus is fixed, no collective on
+the data path).  On each GPU STREAMS engines, each on its own CUDA stream and
+host thread, take batches from a queue.  Seeded N(0, 0.05) weights, uniform
+synthetic token ids (no datasets / checkpoints in this environment).
 
   value  : target tokens/s (EOS excluded, as the reference's bench.py:161 counts)
            of the device-resident decode (qnmt_decode_batch_device: source ids
            already in HBM), CUDA events on the launching stream, L2 flushed
            before every step, max over ranks.
-  e2e    : the same metric through the public C-ABI call qnmt_translate_batch
-           with HOST buffers (H2D of ids, D2H of finished lists + history, host
-           selection of the best hypothesis), wall clock per step.
+  e2e    : the same metric through the public bulk API translate_batch (C-ABI
+           qnmt_translate_batch per batch) with HOST buffers (H2D of ids, D2H of
+           finished lists + history, host selection of the best hypothesis),
+           wall clock per step.
   roofline: per-kernel device time measured live in the timed steps by
            %globaltimer stamps captured into the step graphs (a CUDA graph step
            cannot be bracketed by host events); algorithmic bytes / int-ops per
@@ -43,10 +47,12 @@ sys.path.insert(0, ROOT)
 
 DIMS = dict(src_vocab=32000, tgt_vocab=50000, embed=512, hidden=1024, attn=2048, readout=512)
 BEAM, MAX_RATIO, PER_GPU, CORPUS = 5, 1.5, 256, 8192
+STREAMS = 2   # engines (CUDA streams + host threads) per GPU
 MODEL_SEED, CORPUS_SEED = 1804, 5038
 METRIC = "tokens/sec (int8 beam-5 decode, target tokens excl. EOS)"
-WORKLOAD = ("cfg5 bulk translation shard: 256 sentences/GPU/step of a seeded 8192-sentence corpus, "
-            "l~U[5,100], beam 5, max_ratio 1.5, V_tgt 50000, H 1024, E 512, A 2048, R 512")
+WORKLOAD = ("cfg5 bulk translation: one step = the whole seeded 8192-sentence corpus (l~U[5,100]) sharded over "
+            "the GPUs, 256 sentences per engine call, beam 5, max_ratio 1.5, V_tgt 50000, H 1024, E 512, A 2048, "
+            "R 512")
 # DRAM bytes per algorithmic byte measured by `ncu --set full` at N = 1280 (profiles/r01_ncu_summary.md)
 NCU_TRAFFIC_RATIO = {"attention": 264.4 / 249.8, "vocab_stats": 34.47 / 50.30, "vocab_merge": 24.14 / 24.13}
 
@@ -65,10 +71,23 @@ def corpus():
     return [rng.integers(3, DIMS["src_vocab"], int(l)).astype(np.int32) for l in lens]
 
 
-def batch_for(step: int, rank: int, world: int, sents):
-    nb = len(sents) // PER_GPU
-    b = (step * world + rank) % nb
-    return sents[b * PER_GPU:(b + 1) * PER_GPU]
+def sorted_batches(sents):
+    """Length-sorted (stable) batches of PER_GPU corpus indices."""
+    order = sorted(range(len(sents)), key=lambda i: (len(sents[i]), i))
+    return [order[i:i + PER_GPU] for i in range(0, len(order), PER_GPU)]
+
+
+def shard_batches(sents, rank: int, world: int):
+    """Sorted batches dealt to ranks in snake order (0..W-1, W-1..0, ...): every rank
+    sees the whole length range and the ranks' work is balanced."""
+    bs = sorted_batches(sents)
+    return [b for k, b in enumerate(bs) if (k % world if (k // world) % 2 == 0 else world - 1 - k % world) == rank]
+
+
+def cpu_sample(sents, n):
+    """n corpus indices spread evenly over the sorted length range (bounded CPU sample)."""
+    order = sorted(range(len(sents)), key=lambda i: (len(sents[i]), i))
+    return [order[(2 * k + 1) * len(order) // (2 * n)] for k in range(n)]
 
 
 class ClockSampler:
@@ -126,19 +145,22 @@ def run_reference(args, rank, world):
     params = pb.synthetic_model(pb.Dims(**DIMS), MODEL_SEED)
     sents = corpus()
     sample = args.cpu_sample
+    idx = cpu_sample(sents, sample)
+    short = min(range(len(sents)), key=lambda i: len(sents[i]))
     for w in range(args.warmup):
-        cpu_translate(params, batch_for(w, 0, 1, sents)[:1])
+        cpu_translate(params, [sents[short]])
     secs, toks, cores = 0.0, 0, 1
     for k in range(args.steps):
-        outs, dt, cores = cpu_translate(params, batch_for(args.warmup + k, 0, 1, sents)[:sample])
+        outs, dt, cores = cpu_translate(params, [sents[i] for i in idx])
         toks += sum(len(o[0]) for o in outs)
         secs += dt
     value = toks / secs
-    desc = (f"{sample} sentences per step (first {sample} of each 256-sentence batch), beam 5, V_tgt 50000, "
+    desc = (f"{sample} sentences per step spread over the corpus length range (lengths "
+            f"{len(sents[idx[0]])}..{len(sents[idx[-1]])}), beam 5, V_tgt 50000, "
             f"oracle/qnmt_oracle.py numpy port, {cores} threads")
     line = {"metric": METRIC, "value": value, "unit": "tokens/s", "impl": "reference", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * secs / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int8",
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int8",
             "data": "synthetic", "config": {"workload": WORKLOAD, "sample_per_step": sample},
             "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores, "kind": "port", "sample": desc},
             "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -221,7 +243,7 @@ def main():
         run_reference(args, rank, world)
         return
 
-    import ctypes as C
+    import threading
 
     import torch
     import torch.distributed as dist
@@ -235,87 +257,120 @@ def main():
     dev = torch.device("cuda", local)
     params = pb.synthetic_model(pb.Dims(**DIMS), MODEL_SEED)
     qm = pb.quantize_model(params)
-    eng = pb.Engine(qm, PER_GPU, 100, BEAM)
     sents = corpus()
+    shard = shard_batches(sents, rank, world)          # this rank's length-sorted batches (corpus indices)
+    engines = [pb.Engine(qm, PER_GPU, 100, BEAM) for _ in range(STREAMS)]
+    streams = [torch.cuda.Stream(device=dev) for _ in range(STREAMS)]
     lib = _lib.load()
-    stream = torch.cuda.current_stream()
+    main_stream = torch.cuda.current_stream()
     flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device=dev)   # > 126 MB L2
     stamps_on = not args.no_stamps
-    lib.qnmt_engine_stamps(eng._h, 1 if stamps_on else 0)   # graphs are captured during warm-up
-    stamp_buf = np.zeros((256, 11), dtype=np.int64)   # QNMT_STAMP_COLS
+    for e in engines:
+        lib.qnmt_engine_stamps(e._h, 1 if stamps_on else 0)   # graphs are captured during warm-up
+    # device-resident inputs of every batch of the shard (the "value" pass reads ids from HBM)
+    dev_ids = [torch.from_numpy(np.concatenate([sents[i] for i in b])).to(dev) for b in shard]
+    lens = [np.array([len(sents[i]) for i in b], dtype=np.int32) for b in shard]
 
-    def fetch(batch):
-        stride = int(math.ceil(MAX_RATIO * max(len(s) for s in batch))) + 1
-        out = np.zeros((len(batch), stride), np.int32)
-        ol = np.zeros(len(batch), np.int32)
-        lp = np.zeros(len(batch), np.float64)
-        _lib.call("qnmt_fetch_results", eng._h, out.ctypes.data, stride, ol.ctypes.data, lp.ctypes.data,
-                  stream.cuda_stream)
+    def fetch(e, b, st):
+        stride = int(math.ceil(MAX_RATIO * int(lens[b].max()))) + 1
+        out = np.zeros((len(shard[b]), stride), np.int32)
+        ol = np.zeros(len(shard[b]), np.int32)
+        lp = np.zeros(len(shard[b]), np.float64)
+        _lib.call("qnmt_fetch_results", e._h, out.ctypes.data, stride, ol.ctypes.data, lp.ctypes.data, st.cuda_stream)
         return out, ol, lp
 
-    def device_step(batch):
-        lens = np.array([len(s) for s in batch], dtype=np.int32)
-        ids = torch.from_numpy(np.concatenate(batch)).to(dev)
+    def device_pass(collect=None):
+        """One pass over the shard: STREAMS engines on STREAMS streams, one host thread
+        each, taking batches from a queue.  Device time = CUDA events on the main stream
+        around a fork (side streams wait on ev0) / join (main waits on every side)."""
+        queue = list(range(len(shard)))
+        lock = threading.Lock()
+        toks, rows, errs = [0], [], []
+        stamp_buf = [np.zeros((256, 11), dtype=np.int64) for _ in range(STREAMS)]   # QNMT_STAMP_COLS
         flush.fill_(1)
         torch.cuda.synchronize()
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         l0 = lib.qnmt_kernel_launches()
-        ev0.record(stream)
-        _lib.call("qnmt_decode_batch_device", eng._h, ids.data_ptr(), lens.ctypes.data, len(batch), BEAM,
-                  MAX_RATIO, stream.cuda_stream)
-        ev1.record(stream)
+        ev0.record(main_stream)
+
+        def worker(j):
+            e, st = engines[j], streams[j]
+            st.wait_event(ev0)
+            try:
+                while True:
+                    with lock:
+                        if not queue:
+                            return
+                        b = queue.pop(0)
+                    _lib.call("qnmt_decode_batch_device", e._h, dev_ids[b].data_ptr(), lens[b].ctypes.data,
+                              len(shard[b]), BEAM, MAX_RATIO, st.cuda_stream)
+                    r = []
+                    if stamps_on:
+                        nr = lib.qnmt_engine_stamps_read(e._h, stamp_buf[j].ctypes.data, 256, st.cuda_stream)
+                        r = [stamp_buf[j][i].copy() for i in range(nr)]
+                    out, ol, lp = fetch(e, b, st)
+                    with lock:
+                        toks[0] += int(ol.sum())
+                        rows.extend(r)
+                        if collect is not None:
+                            for k, i in enumerate(shard[b]):
+                                collect[i] = (out[k, :ol[k]].tolist(), float(lp[k]))
+            except BaseException as exc:   # noqa: BLE001
+                with lock:
+                    errs.append(exc)
+
+        th = [threading.Thread(target=worker, args=(j,)) for j in range(STREAMS)]
+        for t in th:
+            t.start()
+        for t in th:
+            t.join()
+        for st in streams:
+            main_stream.wait_stream(st)
+        ev1.record(main_stream)
         ev1.synchronize()
-        launches = lib.qnmt_kernel_launches() - l0
-        rows = []
-        if stamps_on:
-            nr = lib.qnmt_engine_stamps_read(eng._h, stamp_buf.ctypes.data, stamp_buf.shape[0], stream.cuda_stream)
-            rows = [stamp_buf[i].copy() for i in range(nr)]
-        out, ol, lp = fetch(batch)
-        return ev0.elapsed_time(ev1) / 1000.0, int(ol.sum()), launches, rows, (out, ol, lp)
+        if errs:
+            raise errs[0]
+        return ev0.elapsed_time(ev1) / 1000.0, toks[0], lib.qnmt_kernel_launches() - l0, rows
 
     for w in range(args.warmup):
-        device_step(batch_for(w, rank, world, sents))
+        device_pass()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     clk = ClockSampler(local)
     secs, toks, launches, step_ms, all_rows = 0.0, 0, 0, [], []
-    first_result = None
+    first_result = {}
     for k in range(args.steps):
-        t, n, nl, rows, res = device_step(batch_for(args.warmup + k, rank, world, sents))
+        t, n, nl, rows = device_pass(first_result if k == 0 else None)
         secs += t
         toks += n
         launches += nl
         step_ms.append(1000 * t)
         all_rows += rows
-        if first_result is None:
-            first_result = res
     torch.cuda.synchronize()
     clocks = clk.stop()
     if world > 1:
         dist.barrier()
 
-    # e2e through the public C-ABI call with host buffers
-    e2e_secs, e2e_toks, h2d, d2h = 0.0, 0, 0, 0
+    # e2e: the public bulk API (translate_batch: host ids in, host results out, length-sorted
+    # batches pipelined over STREAMS engines), wall clock around the call with a device sync
+    shard_ids = [sents[i] for b in shard for i in b]
+    e2e_secs, e2e_toks = 0.0, 0
+    cfg = pb.DecodeConfig(beam=BEAM, max_ratio=MAX_RATIO, precision="int8")
+    pb.translate_batch(qm, shard_ids, cfg, max_batch=PER_GPU, return_ids=True, streams=STREAMS)   # warm-up
+    eng_pool = qm._engines
+    b0 = [(e.h2d_bytes, e.d2h_bytes) for e in eng_pool if e is not None]
     for k in range(args.steps):
-        batch = batch_for(args.warmup + k, rank, world, sents)
-        lens = np.array([len(s) for s in batch], dtype=np.int32)
-        ids = np.ascontiguousarray(np.concatenate(batch))
-        stride = int(math.ceil(MAX_RATIO * int(lens.max()))) + 1
-        out = np.zeros((len(batch), stride), np.int32)
-        ol = np.zeros(len(batch), np.int32)
-        lp = np.zeros(len(batch), np.float64)
         flush.fill_(1)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        _lib.call("qnmt_translate_batch", eng._h, ids.ctypes.data, lens.ctypes.data, len(batch), BEAM,
-                  MAX_RATIO, out.ctypes.data, stride, ol.ctypes.data, lp.ctypes.data, stream.cuda_stream)
+        res = pb.translate_batch(qm, shard_ids, cfg, max_batch=PER_GPU, return_ids=True, streams=STREAMS)
+        torch.cuda.synchronize()
         e2e_secs += time.perf_counter() - t0
-        e2e_toks += int(ol.sum())
-        n = len(batch)
-        # ids + per-sentence metadata (row, len, max_steps, P, col_off, col_sent, y, live) + encoder row maps
-        h2d += ids.nbytes + n * 40 + 2 * 2 * n * int(lens.max()) * 4 + ids.nbytes + n * 4
-        d2h += int(lib.qnmt_last_d2h_bytes(eng._h))
+        e2e_toks += sum(len(r[0]) for r in res)
+    b1 = [(e.h2d_bytes, e.d2h_bytes) for e in eng_pool if e is not None]
+    h2d = sum(x[0] for x in b1) - sum(x[0] for x in b0)
+    d2h = sum(x[1] for x in b1) - sum(x[1] for x in b0)
 
     stats = torch.tensor([secs, toks, e2e_secs, e2e_toks], dtype=torch.float64, device=dev)
     if world > 1:
@@ -338,26 +393,28 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        first = batch_for(args.warmup, 0, 1, sents)[:args.cpu_sample]
-        outs, dt, cores = cpu_translate(params, first)
+        idx = cpu_sample(sents, args.cpu_sample)
+        outs, dt, cores = cpu_translate(params, [sents[i] for i in idx])
         ctoks = sum(len(o[0]) for o in outs)
-        gout, gol, glp = first_result
-        match = sum(1 for i, o in enumerate(outs)
-                    if o[0] == gout[i, :gol[i]].tolist() and o[1] == glp[i])
+        match = sum(1 for i, o in zip(idx, outs) if first_result.get(i) == (o[0], o[1]))
         cpu = {"value": ctoks / dt, "unit": "tokens/s", "cores": cores, "kind": "port",
-               "sample": f"first {len(first)} sentences of the first timed batch (beam 5, V_tgt 50000), "
-                         f"oracle/qnmt_oracle.py numpy port, {cores} threads, {dt:.1f} s",
-               "gpu_outputs_identical": f"{match}/{len(first)}"}
+               "sample": f"{len(idx)} sentences spread over the length range (sorted-corpus positions "
+                         f"{idx[0]}..{idx[-1]}, lengths {len(sents[idx[0]])}..{len(sents[idx[-1]])}; beam 5, "
+                         f"V_tgt 50000), oracle/qnmt_oracle.py numpy port, {cores} threads, {dt:.1f} s",
+               "gpu_outputs_identical": f"{match}/{len(idx)}"}
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": 1000 * secs / args.steps,
-                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int8",
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int8",
                 "data": "synthetic (seeded N(0,0.05) weights, uniform token ids)",
-                "config": {"workload": WORKLOAD, "sentences_per_gpu_step": PER_GPU,
-                           "parallelism": f"sentence-sharded x{world} (no collective)",
+                "config": {"workload": WORKLOAD, "sentences_per_step": CORPUS,
+                           "batches_per_rank": len(shard), "sentences_per_batch": PER_GPU,
+                           "parallelism": f"sentence-sharded x{world} (length-sorted batches dealt in snake order, "
+                                          "no collective)",
+                           "streams_per_gpu": STREAMS,
                            "l2": "flushed (512 MB write) before every timed step",
                            "decode_loop": "CUDA-graph steps, device-side live count"},
-                "sentences_per_s": world * PER_GPU * args.steps / secs,
+                "sentences_per_s": CORPUS * args.steps / secs,
                 "step_ms": step_ms,
                 "e2e": {"value": e2e_value, "unit": "tokens/s", "h2d_bytes_per_step": h2d // args.steps,
                         "d2h_bytes_per_step": d2h // args.steps},

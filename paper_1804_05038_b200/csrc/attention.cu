@@ -581,11 +581,8 @@ int attention_launch(const float* u, int64_t ldu, int64_t N, const int32_t* sent
                        ((uintptr_t)att_proj % 16) == 0 && ((uintptr_t)v_codes % 4) == 0;
     if (quads) {   // smem-staged tile, 3 CTAs / SM
         const size_t smem5 = (size_t)APC5 * AQ5 * AT * sizeof(float4);
-        static size_t done = 0;
-        if (smem5 > done) {   // (dynamic + static > 48 KB needs the opt-in)
-            QNMT_CUDA(cudaFuncSetAttribute(k_att_score5, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem5));
-            done = smem5;
-        }
+        static size_t done = 0;   // (dynamic + static > 48 KB needs the opt-in)
+        QNMT_CUDA(raise_smem_limit((const void*)k_att_score5, smem5, done));
         dim3 g5((unsigned)cdiv(max_len, APC5), (unsigned)n_sent);
         QNMT_LAUNCH(k_att_score5, g5, AT, smem5, st, u, ldu, sent_col_off, sent_ncols, att_proj, st_thr, sent_row, sent_len,
                                             A, v_codes, v_scale, scores, max_len);
@@ -599,8 +596,10 @@ int attention_launch(const float* u, int64_t ldu, int64_t N, const int32_t* sent
     const size_t smem = (size_t)AMAXP * max_len * 2 * sizeof(double);
     const bool v4 = H2 % 4 == 0 && ldc % 4 == 0 && ((uintptr_t)states % 16) == 0 && ((uintptr_t)ctx % 16) == 0;
     const dim3 g2((unsigned)cdiv(H2, v4 ? 4 * AT : AT), (unsigned)n_sent);
-    if (smem > 48 * 1024)
-        QNMT_CUDA(cudaFuncSetAttribute(k_att_context3, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    if (smem > 48 * 1024) {
+        static size_t done = 0;
+        QNMT_CUDA(raise_smem_limit((const void*)k_att_context3, smem, done));
+    }
     QNMT_LAUNCH(k_att_context3, g2, AT, smem, st, scores, max_len, sent_col_off, sent_ncols, states, sent_row, sent_len, H2,
                                           ctx, ldc, alpha, lda, err_flag, ctx_segmax, v4 ? 1 : 0);
     QNMT_CHECK_LAUNCH("k_att_context3");
@@ -670,8 +669,10 @@ int attention_f32_launch(const float* u, int64_t ldu, int64_t N, const int32_t* 
     const size_t smem = (size_t)AMAXP * max_len * 2 * sizeof(double);
     const bool v4 = H2 % 4 == 0 && ldc % 4 == 0 && ((uintptr_t)states % 16) == 0 && ((uintptr_t)ctx % 16) == 0;
     const dim3 g2((unsigned)cdiv(H2, v4 ? 4 * AT : AT), (unsigned)n_sent);
-    if (smem > 48 * 1024)
-        QNMT_CUDA(cudaFuncSetAttribute(k_att_context3, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    if (smem > 48 * 1024) {
+        static size_t done = 0;
+        QNMT_CUDA(raise_smem_limit((const void*)k_att_context3, smem, done));
+    }
     QNMT_LAUNCH(k_att_context3, g2, AT, smem, st, scores, max_len, sent_col_off, sent_ncols, states, sent_row, sent_len,
                 H2, ctx, ldc, alpha, lda, err_flag, (uint32_t*)nullptr, v4 ? 1 : 0);
     QNMT_CHECK_LAUNCH("k_att_context3");

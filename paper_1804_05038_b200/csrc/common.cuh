@@ -10,6 +10,8 @@
 #pragma once
 
 #include <cuda_runtime.h>
+
+#include <mutex>
 #include <utility>
 #include <stdint.h>
 #include <stdio.h>
@@ -46,6 +48,18 @@ __device__ __forceinline__ void pdl_entry() {
     pdl_trigger();
 }
 bool pdl_enabled();
+
+// Raise a kernel's dynamic shared-memory limit to at least `bytes` (host threads
+// driving separate engines may race here: check-and-set under one lock so the
+// limit only grows).  `done` is the caller's per-kernel high-water mark.
+inline cudaError_t raise_smem_limit(const void* fn, size_t bytes, size_t& done) {
+    static std::mutex mu;
+    std::lock_guard<std::mutex> g(mu);
+    if (bytes <= done) return cudaSuccess;
+    const cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e == cudaSuccess) done = bytes;
+    return e;
+}
 
 template <typename... KArgs, typename... Args>
 static inline cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,

@@ -227,10 +227,7 @@ static int set_smem(const void* fn, size_t bytes, size_t& done) {
         set_error("fused quantize: %zu bytes of segment values exceed shared memory", bytes);
         return QNMT_ERR_CONFIG;
     }
-    if (bytes > 48 * 1024 && bytes > done) {
-        QNMT_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
-        done = bytes;
-    }
+    if (bytes > 48 * 1024) QNMT_CUDA(raise_smem_limit(fn, bytes, done));
     return QNMT_OK;
 }
 

@@ -263,11 +263,8 @@ int tc_sm_count() {
 template <int BN, int EPI>
 static int launch_tc(const GemmArgs& g, cudaStream_t st) {
     using C = TcCfg<BN>;
-    static bool attr_set = false;
-    if (!attr_set) {
-        QNMT_CUDA(cudaFuncSetAttribute(k_gemm_tc<BN, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
-        attr_set = true;
-    }
+    static size_t attr_done = 0;
+    QNMT_CUDA(raise_smem_limit((const void*)k_gemm_tc<BN, EPI>, C::SMEM, attr_done));
     CUtensorMap ta, tb;
     int rc = tc_get_map(g.W, g.M, g.K, g.ldw, TC_BM, &ta);
     if (rc) return rc;

@@ -565,11 +565,8 @@ int vocab_stats_launch(const VocabTopk& p, cudaStream_t st) {
         set_error("vocab_topk: ineligible shape K=%lld k=%d V=%lld", (long long)K, k, (long long)V);
         return QNMT_ERR_CONFIG;
     }
-    static bool attr_set = false;
-    if (!attr_set) {
-        QNMT_CUDA(cudaFuncSetAttribute(k_vocab_stats, cudaFuncAttributeMaxDynamicSharedMemorySize, VtRing::SMEM));
-        attr_set = true;
-    }
+    static size_t attr_done = 0;
+    QNMT_CUDA(raise_smem_limit((const void*)k_vocab_stats, VtRing::SMEM, attr_done));
     CUtensorMap tx, tw;
     int rc = tc_get_map(X, N, K, ldx, TC_BM, &tx);
     if (rc) return rc;

@@ -120,22 +120,90 @@ def _check_cfg(cfg: DecodeConfig):
         raise ConfigError("beam > 16 is not supported by the device search")
 
 
-def _decode_ids(members, per_member_ids, cfg: DecodeConfig, max_batch: int):
-    """Batched device decode of id lists (one list per member); yields (ids, logp)."""
+_STREAMS: dict = {}
+
+
+def _side_streams(k: int) -> list:
+    """k CUDA streams of the current device, created once (one per pipelined engine)."""
+    import torch
+    dev = torch.cuda.current_device()
+    lst = _STREAMS.setdefault(dev, [])
+    while len(lst) < k:
+        lst.append(torch.cuda.Stream(device=dev))
+    return lst[:k]
+
+
+def _decode_ids(members, per_member_ids, cfg: DecodeConfig, max_batch: int, streams: int = 1, sort: bool = False):
+    """Batched device decode of id lists (one list per member).  Returns [(ids, logp)]
+    in input order.
+
+    ``sort``: batches are cut from the length-sorted corpus (stable), so the
+    sentences of one engine call need similar step counts (ceil(ratio*l)+1) and
+    the device runs full-width steps instead of a long tail of a few live
+    sentences.  ``streams`` > 1 (single model): that many engines, each on its
+    own CUDA stream driven by its own host thread, take batches from a shared
+    queue -- one engine's host-side turnaround (polls, result fetch, graph
+    launches) and its small latency-bound kernels overlap the other engines'
+    device work.  Every sentence is still decoded exactly as decoder.translate
+    would (results do not depend on batching)."""
     n_all = len(per_member_ids[0])
+    order = sorted(range(n_all), key=lambda i: (len(per_member_ids[0][i]), i)) if sort else list(range(n_all))
+    batches = [order[b0:b0 + max_batch] for b0 in range(0, n_all, max_batch)]
     max_len = max(len(x) for x in per_member_ids[0])
     nb = min(max_batch, n_all)
-    if len(members) == 1:
-        e = _engine_for(members[0], nb, max_len, cfg.beam)
-        for b0 in range(0, n_all, max_batch):
-            toks, lps = e.translate_ids(per_member_ids[0][b0:b0 + max_batch], cfg.beam, cfg.max_ratio)
-            yield from zip(toks, lps)
-        return
-    engines = _engines_for(members, nb, max_len, cfg.beam)
-    for b0 in range(0, n_all, max_batch):
-        toks, lps = translate_ensemble_ids(engines, [ids[b0:b0 + max_batch] for ids in per_member_ids], cfg.beam,
-                                           cfg.max_ratio)
-        yield from zip(toks, lps)
+    out = [None] * n_all
+
+    def put(idx, toks, lps):
+        for i, t, lp in zip(idx, toks, lps):
+            out[i] = (t, lp)
+
+    if len(members) > 1:
+        engines = _engines_for(members, nb, max_len, cfg.beam)
+        for idx in batches:
+            put(idx, *translate_ensemble_ids(engines, [[ids[i] for i in idx] for ids in per_member_ids],
+                                             cfg.beam, cfg.max_ratio))
+        return out
+    ids0 = per_member_ids[0]
+    k = max(1, min(streams, len(batches)))
+    engines = [_engine_for(members[0], nb, max_len, cfg.beam, slot=j) for j in range(k)]
+    if k == 1:
+        for idx in batches:
+            put(idx, *engines[0].translate_ids([ids0[i] for i in idx], cfg.beam, cfg.max_ratio))
+        return out
+    import threading
+
+    import torch
+    queue = list(range(len(batches)))
+    lock = threading.Lock()
+    errors = []
+    main = torch.cuda.current_stream()
+    sides = _side_streams(k)
+
+    def worker(j):
+        try:
+            sides[j].wait_stream(main)
+            with torch.cuda.stream(sides[j]):
+                while True:
+                    with lock:
+                        if not queue or errors:
+                            return
+                        b = queue.pop(0)
+                    idx = batches[b]
+                    put(idx, *engines[j].translate_ids([ids0[i] for i in idx], cfg.beam, cfg.max_ratio))
+        except BaseException as exc:   # noqa: BLE001 -- re-raised in the caller's thread
+            with lock:
+                errors.append(exc)
+
+    threads = [threading.Thread(target=worker, args=(j,)) for j in range(k)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    for s in sides:
+        main.wait_stream(s)
+    if errors:
+        raise errors[0]
+    return out
 
 
 def translate(models, source_tokens, cfg: DecodeConfig, timer=None):
@@ -150,16 +218,20 @@ def translate(models, source_tokens, cfg: DecodeConfig, timer=None):
     _check_cfg(cfg)
     members = _members(models, cfg.precision)
     ids = [[m.src_ids(tokens)] for m in members]
-    out, lp = next(_decode_ids(members, ids, cfg, 1))
+    out, lp = _decode_ids(members, ids, cfg, 1)[0]
     return [members[0].tgt_tokens[i] for i in out], lp
 
 
-def translate_batch(models, sentences, cfg: DecodeConfig, max_batch: int = 256, return_ids=False):
+def translate_batch(models, sentences, cfg: DecodeConfig, max_batch: int = 256, return_ids=False,
+                    streams: int = 2, sort: bool = True):
     """Translate a corpus with batched device decoding (B200-native bulk path).
 
     ``models``: one model or an ensemble list.  ``sentences``: token lists /
     whitespace strings, or (``return_ids``) id lists.  Output order follows
-    the input.  Each batch of up to ``max_batch`` sentences is one engine call."""
+    the input.  Each batch of up to ``max_batch`` sentences is one engine call;
+    batches are cut from the length-sorted corpus and pipelined over
+    ``streams`` engines (see ``_decode_ids``).  Results are identical to
+    sentence-by-sentence ``translate``."""
     _check_cfg(cfg)
     members = _members(models, cfg.precision)
     sents = [s.split() if isinstance(s, str) else list(s) for s in sentences]
@@ -172,7 +244,8 @@ def translate_batch(models, sentences, cfg: DecodeConfig, max_batch: int = 256, 
     else:
         ids = [[m.src_ids(s) for s in sents] for m in members]
     tgt = members[0].tgt_tokens
-    return [(t if return_ids else [tgt[i] for i in t], lp) for t, lp in _decode_ids(members, ids, cfg, max_batch)]
+    res = _decode_ids(members, ids, cfg, max_batch, streams=streams, sort=sort)
+    return [(t if return_ids else [tgt[i] for i in t], lp) for t, lp in res]
 
 
 def max_steps(length: int, max_ratio: float) -> int:

@@ -24,6 +24,8 @@ class Engine:
         h = C.c_void_p()
         _lib.call("qnmt_engine_create", qmodel.handle(), max_sentences, max_len, max_beam, C.byref(h))
         self._h = h
+        self.h2d_bytes = 0   # host<->device traffic of translate_ids calls (ids + metadata in, results out)
+        self.d2h_bytes = 0
 
     def fits(self, n, length, beam) -> bool:
         return n <= self.max_sentences and length <= self.max_len and beam <= self.max_beam
@@ -116,6 +118,9 @@ class Engine:
         _lib.call("qnmt_translate_batch", self._h, ids.ctypes.data, lens.ctypes.data, n, beam,
                   float(max_ratio), out_tok.ctypes.data, stride, out_len.ctypes.data,
                   out_lp.ctypes.data, _dev.stream_ptr())
+        # ids + per-sentence metadata (row, len, max_steps, P, col_off, col_sent, y, live) + encoder row maps
+        self.h2d_bytes += ids.nbytes + n * 40 + 2 * 2 * n * int(lens.max()) * 4 + ids.nbytes + n * 4
+        self.d2h_bytes += int(_lib.load().qnmt_last_d2h_bytes(self._h))
         toks = [out_tok[i, :out_len[i]].tolist() for i in range(n)]
         return toks, out_lp.tolist()
 

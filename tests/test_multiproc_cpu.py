@@ -26,10 +26,8 @@ def _worker(rank, world, port, q):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     import bench
     sents = bench.corpus()
-    ids = []
-    for step in range(4):
-        b = bench.batch_for(step, rank, world, sents)
-        ids.append(int(b[0][0]) * 1000 + len(b[0]))
+    shard = bench.shard_batches(sents, rank, world)
+    ids = sorted(i for b in shard for i in b)   # corpus indices this rank decodes
     # per-rank "timing" and token counts reduced exactly as bench.py does
     secs = torch.tensor([1.0 + rank, 100.0 * (rank + 1)], dtype=torch.float64)
     mx = secs.clone()
@@ -54,9 +52,9 @@ def test_sharding_and_reductions_world2():
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    # each rank decodes a different batch at every step (no overlap between ranks)
-    for step in range(4):
-        assert gathered[0][step] != gathered[1][step]
+    # the ranks' shards are disjoint and together cover the corpus (no collective on the data path)
+    assert not set(gathered[0]) & set(gathered[1])
+    assert len(gathered[0]) + len(gathered[1]) == 8192
     # value = all ranks' tokens / max-over-ranks time
     assert mx[0] == 2.0 and sm[1] == 300.0
 
@@ -67,14 +65,17 @@ def test_batches_partition_corpus():
     assert len(sents) == bench.CORPUS
     lens = np.array([len(s) for s in sents])
     assert lens.min() >= 5 and lens.max() <= 100
+    batches = bench.sorted_batches(sents)
+    assert all(len(b) == bench.PER_GPU for b in batches)
+    flat = [i for b in batches for i in b]
+    assert sorted(flat) == list(range(bench.CORPUS))
+    blens = [lens[b] for b in batches]
+    assert all(blens[k].max() <= blens[k + 1].min() for k in range(len(blens) - 1))   # length-sorted
     for world in (1, 2, 4, 8):
-        seen = set()
-        steps = bench.CORPUS // bench.PER_GPU // world
-        for step in range(steps):
-            for rank in range(world):
-                b = bench.batch_for(step, rank, world, sents)
-                assert len(b) == bench.PER_GPU
-                key = id(b[0])
-                assert key not in seen
-                seen.add(key)
-        assert len(seen) == bench.CORPUS // bench.PER_GPU
+        shards = [bench.shard_batches(sents, r, world) for r in range(world)]
+        got = sorted(i for sh in shards for b in sh for i in b)
+        assert got == list(range(bench.CORPUS))
+        work = [sum(int(np.ceil(1.5 * lens[i])) + 1 for b in sh for i in b) for sh in shards]
+        assert max(work) / min(work) < 1.05   # snake-order dealing balances the ranks
+    idx = bench.cpu_sample(sents, 8)
+    assert len(set(idx)) == 8 and lens[idx].min() < 20 and lens[idx].max() > 85
