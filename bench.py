@@ -47,7 +47,7 @@ sys.path.insert(0, ROOT)
 
 DIMS = dict(src_vocab=32000, tgt_vocab=50000, embed=512, hidden=1024, attn=2048, readout=512)
 BEAM, MAX_RATIO, PER_GPU, CORPUS = 5, 1.5, 256, 8192
-STREAMS = 2   # engines (CUDA streams + host threads) per GPU
+STREAMS = int(os.environ.get("QNMT_BENCH_STREAMS", "3"))   # engines (CUDA streams + host threads) per GPU
 MODEL_SEED, CORPUS_SEED = 1804, 5038
 METRIC = "tokens/sec (int8 beam-5 decode, target tokens excl. EOS)"
 WORKLOAD = ("cfg5 bulk translation: one step = the whole seeded 8192-sentence corpus (l~U[5,100]) sharded over "
@@ -398,8 +398,8 @@ def main():
         ctoks = sum(len(o[0]) for o in outs)
         match = sum(1 for i, o in zip(idx, outs) if first_result.get(i) == (o[0], o[1]))
         cpu = {"value": ctoks / dt, "unit": "tokens/s", "cores": cores, "kind": "port",
-               "sample": f"{len(idx)} sentences spread over the length range (sorted-corpus positions "
-                         f"{idx[0]}..{idx[-1]}, lengths {len(sents[idx[0]])}..{len(sents[idx[-1]])}; beam 5, "
+               "sample": f"{len(idx)} sentences spread evenly over the corpus length order (lengths "
+                         f"{len(sents[idx[0]])}..{len(sents[idx[-1]])}; beam 5, "
                          f"V_tgt 50000), oracle/qnmt_oracle.py numpy port, {cores} threads, {dt:.1f} s",
                "gpu_outputs_identical": f"{match}/{len(idx)}"}
     if rank == 0:
@@ -421,6 +421,9 @@ def main():
                 "gpu_launches": launches,
                 "roofline": roof,
                 "kernels": kern,
+                "kernels_note": (f"per-launch device times from %globaltimer stamps inside the timed passes; with "
+                                 f"{STREAMS} engines on {STREAMS} streams a kernel may share SMs with the other "
+                                 "stream's kernels, so these are lower bounds on kernel efficiency"),
                 "cpu_baseline": cpu,
                 "clocks": clocks}
         print(json.dumps(line), flush=True)

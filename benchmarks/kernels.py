@@ -185,6 +185,28 @@ def gemv_cold(bsz):
                     "prefetch (W streams while the previous product drains), 'us_no_prefetch' without"}
 
 
+def gemv_large(M, K):
+    """Batch-1 GEMV over one large weight matrix (the vocab projection, or 64 MB) with
+    rotating copies (> L2): the HBM-streaming rate of the GEMV kernel once the matrix
+    is big enough to hide the launch and DRAM latency that bound cfg1's 3 MB product."""
+    reps = max(2, int(256e6 // (M * K)))
+    w = torch.randint(-127, 128, (M, K), dtype=torch.int8, device="cuda")
+    copies = [w.clone() for _ in range(reps)]
+    X = torch.randint(-127, 128, (1, K), dtype=torch.int8, device="cuda")
+    ws = torch.ones(1, device="cuda")
+    xs = torch.ones(1, device="cuda")
+    Y = torch.empty((1, M), dtype=torch.float32, device="cuda")
+
+    def run():
+        for c in copies:
+            pb.qmath.gemm_kmajor(c, ws, M, X, xs, Y=Y, w_static=True)
+    t = graph_time(run, reps=1) / len(copies)
+    nbytes = M * K + K + 4 * M
+    return {"kernel": "gemv batch 1 (large)", "M": M, "K": K, "us": t * 1e6, "GBps": nbytes / t / 1e9,
+            "hbm_frac_of_measured": nbytes / t / 1e9 / PEAK["hbm_gbs"],
+            "note": f"{len(copies)} rotating weight copies ({len(copies) * M * K / 1e6:.0f} MB > L2)"}
+
+
 def main():
     which = sys.argv[1:] or ["gemm", "topk", "gemv"]
     out = []
@@ -207,7 +229,7 @@ def main():
     if "att" in which:
         out.append(attention_case())
     if "gemv" in which:
-        out += [gemv_cold(1), gemv_cold(64)]
+        out += [gemv_cold(1), gemv_cold(64), gemv_large(50000, 512), gemv_large(16384, 4096)]
     for r in out:
         print(json.dumps(r), flush=True)
 

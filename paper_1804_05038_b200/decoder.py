@@ -223,7 +223,7 @@ def translate(models, source_tokens, cfg: DecodeConfig, timer=None):
 
 
 def translate_batch(models, sentences, cfg: DecodeConfig, max_batch: int = 256, return_ids=False,
-                    streams: int = 2, sort: bool = True):
+                    streams: int = 3, sort: bool = True):
     """Translate a corpus with batched device decoding (B200-native bulk path).
 
     ``models``: one model or an ensemble list.  ``sentences``: token lists /
