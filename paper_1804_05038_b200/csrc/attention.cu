@@ -23,6 +23,7 @@
 #include <algorithm>
 
 #include "kernels.cuh"
+#include "tc_common.cuh"
 
 #define TRY_LAUNCH(x) do { int _r = (x); if (_r != QNMT_OK) return _r; } while (0)
 
@@ -32,6 +33,7 @@ constexpr int AT = 256;        // threads per CTA
 constexpr int APC = 4;         // encoder positions per CTA (max / score passes)
 constexpr int AMAXP = 16;      // max live hypotheses per sentence (beam <= 16)
 constexpr int AKA = 8;         // a-elements per thread kept in registers (A <= AT * AKA)
+int g_att_ctx_staged = 1;      // 0: k_att_context3 everywhere (A/B testing)
 
 // Fast tanh from two MUFU ops, signed form: t = 1 - 2 / (1 + 2^(2x log2 e)).
 // Exhaustive over every f32 x with 2^-24 <= |x| < 64 (benchmarks/tanh_err.cu,
@@ -555,12 +557,155 @@ k_att_context3(const float* __restrict__ scores, int32_t max_len, const int32_t*
     }
 }
 
+// ---------------------------------------------------------------------------
+// k_att_context4: the context sum with the encoder states staged by TMA bulk
+// copies (cp.async.bulk, one 4 KB row slice per position) into a 5-stage
+// shared-memory ring of 4 positions each, so HBM streams at full depth
+// instead of a few float4 loads per thread in flight.  The states do not
+// depend on the predecessor kernel (they are the batch's encoder output), so
+// the first stages are issued before the programmatic-dependent-launch wait
+// and overlap the scorer's tail.  Same arithmetic and summation order as
+// k_att_context3 (sequential over positions, fp64 FMAs).  Sentences with more
+// than 8 live hypotheses (register bound) drain the ring and use the direct
+// loads of k_att_context3.
+// ---------------------------------------------------------------------------
+constexpr int ACF = 4 * AT;   // features per CTA (one float4 per thread)
+constexpr int ACH = 4;        // positions per stage
+constexpr int ACS = 5;        // stages (80 KB ring + softmax arrays: 2 CTAs / SM)
+constexpr int ACP_MAX = 8;    // hypotheses per sentence supported by context4
+
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(tc::smem_u32(dst)), "l"(src), "r"(bytes), "r"(tc::smem_u32(bar)) : "memory");
+}
+
+template <int P>
+__device__ __forceinline__ uint32_t att_context_staged(const float* buf, uint64_t* full, const float* src0,
+                                                       int64_t H2, uint32_t row_bytes, int l, const double* al,
+                                                       int64_t c, bool cok, float* __restrict__ ctx, int64_t ldc,
+                                                       int c0) {
+    double acc[P][4];
+#pragma unroll
+    for (int j = 0; j < P; ++j)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) acc[j][e] = 0.0;
+    const int nst = (l + ACH - 1) / ACH;
+    for (int k = 0; k < nst; ++k) {
+        const int b = k % ACS;
+        tc::mbar_wait(&full[b], (uint32_t)(k / ACS) & 1u);
+        const int np = min(ACH, l - k * ACH);
+        const float4* bp = reinterpret_cast<const float4*>(buf + (size_t)b * ACH * ACF) + threadIdx.x;
+#pragma unroll 4
+        for (int p = 0; p < np; ++p) {
+            const float4 q = bp[p * (ACF / 4)];
+            const double d[4] = {(double)q.x, (double)q.y, (double)q.z, (double)q.w};
+            const double* ap = al + (k * ACH + p) * AMAXP;
+#pragma unroll
+            for (int j = 0; j < P; ++j) {
+                const double aj = ap[j];
+#pragma unroll
+                for (int e = 0; e < 4; ++e) acc[j][e] += d[e] * aj;
+            }
+        }
+        __syncthreads();   // every thread is done with buffer b
+        if (threadIdx.x == 0 && k + ACS < nst) {
+            const int k2 = k + ACS, n2 = min(ACH, l - k2 * ACH);
+            tc::mbar_arrive_expect_tx(&full[b], (uint32_t)n2 * row_bytes);
+            for (int p = 0; p < n2; ++p)
+                bulk_g2s(const_cast<float*>(buf) + ((size_t)b * ACH + p) * ACF, src0 + (int64_t)(k2 * ACH + p) * H2,
+                         row_bytes, &full[b]);
+        }
+    }
+    uint32_t mx = 0;
+    if (!cok) return 0;
+#pragma unroll
+    for (int j = 0; j < P; ++j) {
+        float v[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            v[e] = __double2float_rn(acc[j][e]);
+            mx = max(mx, __float_as_uint(v[e]) & 0x7fffffffu);
+        }
+        *reinterpret_cast<float4*>(ctx + (int64_t)(c0 + j) * ldc + c) = make_float4(v[0], v[1], v[2], v[3]);
+    }
+    return mx;
+}
+
+// Grid (ceil(H2 / ACF), sentences).  Requires H2 % 4 == 0, 16-byte aligned states/ctx rows.
+__global__ void __launch_bounds__(AT, 2)
+k_att_context4(const float* __restrict__ scores, int32_t max_len, const int32_t* __restrict__ sent_col_off,
+               const int32_t* __restrict__ sent_ncols, const float* __restrict__ states,
+               const int64_t* __restrict__ sent_row, const int32_t* __restrict__ sent_len, int64_t H2,
+               float* __restrict__ ctx, int64_t ldc, float* __restrict__ alpha, int64_t lda, int32_t* err_flag,
+               uint32_t* ctx_segmax) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    __shared__ __align__(8) uint64_t full[ACS];
+    float* buf = reinterpret_cast<float*>(smem_raw);                      // [ACS][ACH][ACF]
+    double* ex = reinterpret_cast<double*>(buf + (size_t)ACS * ACH * ACF);  // [AMAXP][max_len]
+    double* al = ex + AMAXP * max_len;                                    // [max_len][AMAXP]
+    const int s = blockIdx.y;
+    // sentence metadata and states were written >= 2 kernels ago (the scorer waits for its own
+    // predecessor before triggering us): safe to read before the PDL wait
+    const int P = sent_ncols[s];
+    const int l = sent_len[s];
+    const int64_t cb = (int64_t)blockIdx.x * ACF;
+    const int64_t nfeat = min((int64_t)ACF, H2 - cb);
+    const uint32_t row_bytes = (uint32_t)(nfeat * 4);
+    const float* src0 = states + sent_row[s] * H2 + cb;
+    const int nst = (l + ACH - 1) / ACH;
+    if (P > 0 && threadIdx.x == 0) {
+#pragma unroll
+        for (int b = 0; b < ACS; ++b) tc::mbar_init(&full[b], 1);
+        tc::fence_mbar_init();
+        for (int k = 0; k < min(ACS, nst); ++k) {
+            const int np = min(ACH, l - k * ACH);
+            tc::mbar_arrive_expect_tx(&full[k], (uint32_t)np * row_bytes);
+            for (int p = 0; p < np; ++p)
+                bulk_g2s(buf + ((size_t)k * ACH + p) * ACF, src0 + (int64_t)(k * ACH + p) * H2, row_bytes, &full[k]);
+        }
+    }
+    pdl_entry();
+    if (P == 0) return;   // sentence finished
+    const int c0 = sent_col_off[s];
+    att_softmax(scores, max_len, P, l, c0, ex, al, alpha, lda, err_flag);
+    __syncthreads();   // al ready; barriers initialised
+    const int64_t c = cb + 4 * threadIdx.x;
+    const bool cok = 4 * threadIdx.x < nfeat;
+    uint32_t mx = 0;
+#define QNMT_CTX4(P_) \
+    case P_: mx = att_context_staged<P_>(buf, full, src0, H2, row_bytes, l, al, c, cok, ctx, ldc, c0); break;
+    switch (P) {
+        QNMT_CTX4(1) QNMT_CTX4(2) QNMT_CTX4(3) QNMT_CTX4(4) QNMT_CTX4(5) QNMT_CTX4(6) QNMT_CTX4(7) QNMT_CTX4(8)
+        default: break;
+    }
+#undef QNMT_CTX4
+    if (P > ACP_MAX) {   // wide beams (register bound): drain the staged copies, read states directly
+        for (int k = 0; k < min(ACS, nst); ++k) tc::mbar_wait(&full[k], 0);
+        const float* st0 = states + sent_row[s] * H2;
+        for (int r = 0; r < 4; ++r) {
+            const int64_t cc = cb + (int64_t)r * AT + threadIdx.x;
+            if (cc >= cb + nfeat) break;
+            switch (P) {
+#define QNMT_CTX4W(P_) case P_: mx = max(mx, att_context_acc<P_, false>(st0, H2, l, al, cc, ctx, ldc, c0)); break;
+                QNMT_CTX4W(9) QNMT_CTX4W(10) QNMT_CTX4W(11) QNMT_CTX4W(12) QNMT_CTX4W(13) QNMT_CTX4W(14)
+                QNMT_CTX4W(15) QNMT_CTX4W(16)
+#undef QNMT_CTX4W
+                default: break;
+            }
+        }
+    }
+    if (ctx_segmax) {
+        mx = __reduce_max_sync(0xffffffffu, mx);
+        if ((threadIdx.x & 31) == 0 && mx) atomicMax(ctx_segmax + s, mx);
+    }
+}
+
 int attention_launch(const float* u, int64_t ldu, int64_t N, const int32_t* sent_col_off,
                      const int32_t* sent_ncols, int32_t n_sent, const float* att_proj, const float* att_minmax,
                      const float* states, const int64_t* sent_row, const int32_t* sent_len, int32_t max_len,
                      int64_t A, int64_t H2, const int8_t* v_codes, const float* v_scale, float* ctx, int64_t ldc,
                      float* alpha, int64_t lda, void* scratch, int32_t* err_flag, cudaStream_t st,
-                     uint32_t* ctx_segmax) {
+                     uint32_t* ctx_segmax, int max_p) {
     if (N <= 0 || n_sent <= 0) return QNMT_OK;
     if (A > (int64_t)AT * AKA) {
         set_error("qnmt_attention: attention dim %lld > %d", (long long)A, AT * AKA);
@@ -596,6 +741,15 @@ int attention_launch(const float* u, int64_t ldu, int64_t N, const int32_t* sent
     const size_t smem = (size_t)AMAXP * max_len * 2 * sizeof(double);
     const bool v4 = H2 % 4 == 0 && ldc % 4 == 0 && ((uintptr_t)states % 16) == 0 && ((uintptr_t)ctx % 16) == 0;
     const dim3 g2((unsigned)cdiv(H2, v4 ? 4 * AT : AT), (unsigned)n_sent);
+    const size_t smem4 = (size_t)ACS * ACH * ACF * sizeof(float) + smem;
+    if (v4 && g_att_ctx_staged && smem4 <= 200 * 1024) {
+        static size_t done4 = 0;
+        QNMT_CUDA(raise_smem_limit((const void*)k_att_context4, smem4, done4));
+        QNMT_LAUNCH(k_att_context4, g2, AT, smem4, st, scores, max_len, sent_col_off, sent_ncols, states, sent_row,
+                    sent_len, H2, ctx, ldc, alpha, lda, err_flag, ctx_segmax);
+        QNMT_CHECK_LAUNCH("k_att_context4");
+        return QNMT_OK;
+    }
     if (smem > 48 * 1024) {
         static size_t done = 0;
         QNMT_CUDA(raise_smem_limit((const void*)k_att_context3, smem, done));
