@@ -110,6 +110,10 @@ int qnmt_gemm_i8(const int8_t* W, int64_t M, int64_t K, int64_t ldw,
  * (tcgen05 for N > 8, dp4a GEMV otherwise), 1 = CUDA-core dp4a only,
  * 2 = tcgen05 whenever the shape is eligible.  Returns the previous value. */
 int qnmt_set_gemm_impl(int impl);
+/* 1 (default): products with at least one wave of 256 x 256 tiles use the
+ * CTA-pair tcgen05 kernel (cta_group::2, M = 256); 0: single-CTA tiles only.
+ * Results are identical.  Returns the old value. */
+int qnmt_set_tc_pair(int enable);
 
 /* fp32 precision path: replaces qmath.py:434-440
  * (gemm_f32) in LinearOp's float branch (layers.py:138-145).

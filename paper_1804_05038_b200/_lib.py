@@ -55,6 +55,7 @@ SIGNATURES = {
     "qnmt_last_d2h_bytes": (I64, [P]),
     "qnmt_kernel_launches": (I64, []),
     "qnmt_set_gemm_impl": (I32, [I32]),
+    "qnmt_set_tc_pair": (I32, [I32]),
     "qnmt_set_topk_exact": (I32, [I32]),
     "qnmt_set_vocab_fused": (I32, [I32]),
     "qnmt_engine_profile": (I32, [P, I32]),

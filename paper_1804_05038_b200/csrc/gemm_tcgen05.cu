@@ -53,40 +53,24 @@ struct TcEpi {
 // ((W_s s + b_r) + W_e e) + W_c c with W_e e and W_c c from stacked GEMMs)
 enum { EPI_BIAS = 1, EPI_ACCUMULATE = 2, EPI_RAW = 4, EPI_ADD2 = 8 };
 
+// Epilogue warps (2..9) of one CTA: every tile of the persistent schedule
+// (tile0, tile0 + tstep, ...) -> TMEM accumulator rows m_tile * mb + m_off + [0, 128)
+// -> exact dequant (+ bias / + Y / + addends) -> f32 stores.  Shared by the
+// 1-CTA kernel and the CTA-pair kernel (tempty_remote: shared::cluster address
+// of the leader CTA's tempty barriers, 0 = local).
 template <int BN, int EPI>
-__global__ void __launch_bounds__(TC_THREADS, 1)
-k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N, int K,
-          TcEpi e, const int32_t* n_dev) {
-    using C = TcCfg<BN>;
-    extern __shared__ __align__(1024) unsigned char smem_raw[];
-    unsigned char* smem = (unsigned char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-    const TcBars<C> bars(smem);
-    __shared__ float col_sx[2][256];      // per-column activation scale (double-buffered by tile)
-    __shared__ double col_isx[2][256];    // and its f64 reciprocal
-
+__device__ __forceinline__ void tc_epilogue(const TcEpi& e, uint32_t tmem_base, uint64_t* tfull, uint64_t* tempty,
+                                            uint32_t tempty_remote, int tile0, int tstep, int tiles, int n_blocks,
+                                            int m_tile, int m_off, int M, int N, float (*col_sx)[256],
+                                            double (*col_isx)[256]) {
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
-    pdl_trigger();
-    const uint32_t tmem_base = tc_setup<C>(&tmA, &tmB, bars, TC_EPI_WARPS);
-    pdl_wait();   // everything above overlaps the predecessor kernel (PDL)
-    if (n_dev) N = min(N, *n_dev);   // graph mode: live columns from the device
-    const int m_blocks = (M + TC_BM - 1) / TC_BM;
-    const int n_blocks = (N + BN - 1) / BN;
-    const int tiles = m_blocks * n_blocks;
-    const int k_blocks = (K + TC_BK - 1) / TC_BK;
-
-    if (warp == 0) {
-        tc_produce<C, BN>(&tmA, &tmB, smem, bars, tiles, n_blocks, k_blocks);
-    } else if (warp == 1) {
-        tc_issue<C, BN>(smem, bars, tmem_base, tiles, k_blocks);
-    } else {
-        // ---------------- epilogue ----------------
-        const int ew = warp - 2;                 // 0..7
+    const int ew = warp - 2;                 // 0..7
         const int lg = warp & 3;                 // TMEM lane group this warp may access
         const int half = ew >> 2;                // column half of the tile
         constexpr int COLS = BN / 2;
         int it = 0;
-        for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++it) {
+        for (int tile = tile0; tile < tiles; tile += tstep, ++it) {
             const int mb = tile / n_blocks, nb = tile % n_blocks;
             const int buf = it & 1;
             const uint32_t use = (uint32_t)(it >> 1) & 1u;
@@ -102,7 +86,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
                     col_isx[buf][c] = 1.0 / (double)sx;
                 }
             }
-            const int m = mb * TC_BM + lg * 32 + lane;
+            const int m = mb * m_tile + m_off + lg * 32 + lane;
             const bool mok = m < M;
             float sw = 1.0f, bias = 0.0f;
             if (mok) {
@@ -111,7 +95,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
             }
             const double isw = 1.0 / (double)sw;
             asm volatile("bar.sync 1, %0;" ::"n"(32 * TC_EPI_WARPS));   // epilogue warps only
-            tc::mbar_wait(&bars.tfull[buf], use);
+            tc::mbar_wait(&tfull[buf], use);
             tc::tc_fence_after();
 #pragma unroll 1
             for (int c0 = half * COLS; c0 < (half + 1) * COLS; c0 += 16) {
@@ -177,13 +161,211 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
             }
             tc::tc_fence_before();
             __syncwarp();
-            if (lane == 0) tc::mbar_arrive(&bars.tempty[buf]);
+            if (lane == 0) {
+                if (tempty_remote)   // 2-CTA pair: the leader's MMA warp waits for both CTAs' epilogues
+                    asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(tempty_remote + 8u * buf)
+                                 : "memory");
+                else
+                    tc::mbar_arrive(&tempty[buf]);
+            }
         }
+    }
+
+template <int BN, int EPI>
+__global__ void __launch_bounds__(TC_THREADS, 1)
+k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N, int K,
+          TcEpi e, const int32_t* n_dev) {
+    using C = TcCfg<BN>;
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char* smem = (unsigned char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    const TcBars<C> bars(smem);
+    __shared__ float col_sx[2][256];      // per-column activation scale (double-buffered by tile)
+    __shared__ double col_isx[2][256];    // and its f64 reciprocal
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    pdl_trigger();
+    const uint32_t tmem_base = tc_setup<C>(&tmA, &tmB, bars, TC_EPI_WARPS);
+    pdl_wait();   // everything above overlaps the predecessor kernel (PDL)
+    if (n_dev) N = min(N, *n_dev);   // graph mode: live columns from the device
+    const int m_blocks = (M + TC_BM - 1) / TC_BM;
+    const int n_blocks = (N + BN - 1) / BN;
+    const int tiles = m_blocks * n_blocks;
+    const int k_blocks = (K + TC_BK - 1) / TC_BK;
+
+    if (warp == 0) {
+        tc_produce<C, BN>(&tmA, &tmB, smem, bars, tiles, n_blocks, k_blocks);
+    } else if (warp == 1) {
+        tc_issue<C, BN>(smem, bars, tmem_base, tiles, k_blocks);
+    } else {
+        tc_epilogue<BN, EPI>(e, tmem_base, bars.tfull, bars.tempty, 0u, blockIdx.x, gridDim.x, tiles, n_blocks,
+                             TC_BM, 0, M, N, col_sx, col_isx);
     }
     __syncthreads();
     if (warp == 1) {
         tc::tc_fence_after();
         tc::tmem_dealloc<C::TMEM_COLS>(tmem_base);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// CTA-pair variant for large products (tcgen05.mma.cta_group::2, M = 256).
+// A cluster of two CTAs on one TPC computes a 256 x BN tile: CTA r loads A rows
+// [256 mb + 128 r, +128) and B rows [BN nb + BN/2 r, +BN/2) into its own
+// shared memory; the leader (rank 0) issues the M = 256 MMAs, which read A and
+// B from both CTAs and accumulate rows 128 r .. of the tile in CTA r's TMEM.
+// Per CTA the ring carries 32 KB per k-block instead of 48 KB for the same MMA
+// work (BN = 256), which is what lets the tensor pipe run at the int8 rate
+// (single-CTA M = 128 tiles are shared-memory-bandwidth bound).  TMA loads of
+// both CTAs complete on the leader's full barrier (cta_group::2 TMA); MMA
+// commits multicast to both CTAs' empty / tmem-full barriers; both CTAs'
+// epilogues release a TMEM buffer on the leader's tmem-empty barrier.
+// ---------------------------------------------------------------------------
+template <int BN>
+struct Tc2Ring {
+    static constexpr int A_BYTES = TC_BM * TC_BK;
+    static constexpr int B_BYTES = (BN / 2) * TC_BK;
+    static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+    static constexpr int STAGES = (200 * 1024 / STAGE_BYTES) < 8 ? (200 * 1024 / STAGE_BYTES) : 8;
+    static constexpr int TMEM_COLS = 2 * BN <= 256 ? 256 : 512;
+    static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
+};
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t smem_in_rank(const void* p, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(tc::smem_u32(p)), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* map, uint32_t leader_bar, int x, int y) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];"
+        ::"r"(tc::smem_u32(dst)), "l"(map), "r"(leader_bar), "r"(x), "r"(y)
+        : "memory");
+}
+__device__ __forceinline__ void mma_i8_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                            uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+__device__ __forceinline__ void mma_commit_pair(uint64_t* bar) {   // arrive on bar in both CTAs
+    asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
+                 ::"r"(tc::smem_u32(bar)), "h"((uint16_t)3)
+                 : "memory");
+}
+
+template <int BN, int EPI>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
+k_gemm_tc2(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N, int K,
+           TcEpi e) {
+    using C = Tc2Ring<BN>;
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char* smem = (unsigned char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    const TcBars<C> bars(smem);
+    __shared__ float col_sx[2][256];
+    __shared__ double col_isx[2][256];
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const uint32_t rank = cluster_rank();
+    pdl_trigger();
+    if (warp == 0 && lane == 0) {
+        tc::prefetch_tmap(&tmA);
+        tc::prefetch_tmap(&tmB);
+        for (int s = 0; s < C::STAGES; ++s) {
+            tc::mbar_init(&bars.full[s], 1);
+            tc::mbar_init(&bars.empty[s], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            tc::mbar_init(&bars.tfull[i], 1);
+            tc::mbar_init(&bars.tempty[i], 2 * TC_EPI_WARPS);
+        }
+        tc::fence_mbar_init();
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         tc::smem_u32(bars.tmem_slot)), "n"(C::TMEM_COLS)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    }
+    tc::tc_fence_before();
+    cluster_sync_all();
+    tc::tc_fence_after();
+    const uint32_t tmem_base = *bars.tmem_slot;
+    pdl_wait();
+    const int m_blocks = (M + 2 * TC_BM - 1) / (2 * TC_BM);
+    const int n_blocks = (N + BN - 1) / BN;
+    const int tiles = m_blocks * n_blocks;
+    const int k_blocks = (K + TC_BK - 1) / TC_BK;
+    const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+    if (warp == 0) {
+        if (lane == 0) {
+            const uint32_t full0 = smem_in_rank(bars.full, 0);
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int tile = cid; tile < tiles; tile += ncl) {
+                const int mb = tile / n_blocks, nb = tile % n_blocks;
+                for (int kb = 0; kb < k_blocks; ++kb) {
+                    tc::mbar_wait(&bars.empty[stage], phase ^ 1);
+                    unsigned char* sa = smem + stage * C::STAGE_BYTES;
+                    unsigned char* sb = sa + C::A_BYTES;
+                    if (rank == 0) tc::mbar_arrive_expect_tx(&bars.full[stage], 2 * C::STAGE_BYTES);
+                    tma_load_2d_pair(sa, &tmA, full0 + 8u * stage, kb * TC_BK, mb * 2 * TC_BM + (int)rank * TC_BM);
+                    tma_load_2d_pair(sb, &tmB, full0 + 8u * stage, kb * TC_BK, nb * BN + (int)rank * (BN / 2));
+                    if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (rank == 0) {
+            constexpr uint32_t IDESC = tc::idesc_i8(2 * TC_BM, BN);
+            int stage = 0;
+            uint32_t phase = 0;
+            int it = 0;
+            for (int tile = cid; tile < tiles; tile += ncl, ++it) {
+                const int buf = it & 1;
+                const uint32_t use = (uint32_t)(it >> 1) & 1u;
+                tc::mbar_wait(&bars.tempty[buf], use ^ 1);
+                tc::tc_fence_after();
+                const uint32_t d = tmem_base + (uint32_t)(buf * BN);
+                for (int kb = 0; kb < k_blocks; ++kb) {
+                    tc::mbar_wait(&bars.full[stage], phase);
+                    tc::tc_fence_after();
+                    if (lane == 0) {
+                        const uint32_t a0 = tc::smem_u32(smem + stage * C::STAGE_BYTES);
+                        const uint32_t b0 = a0 + C::A_BYTES;
+#pragma unroll
+                        for (int k = 0; k < TC_BK / 32; ++k)
+                            mma_i8_pair(d, tc::sw128_kmajor_desc(a0 + 32 * k), tc::sw128_kmajor_desc(b0 + 32 * k),
+                                        IDESC, (kb | k) != 0);
+                        mma_commit_pair(&bars.empty[stage]);
+                        if (kb == k_blocks - 1) mma_commit_pair(&bars.tfull[buf]);
+                    }
+                    __syncwarp();
+                    if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+                }
+            }
+        }
+    } else {
+        tc_epilogue<BN, EPI>(e, tmem_base, bars.tfull, bars.tempty, rank ? smem_in_rank(bars.tempty, 0) : 0u, cid, ncl,
+                             tiles, n_blocks, 2 * TC_BM, (int)rank * TC_BM, M, N, col_sx, col_isx);
+    }
+    tc::tc_fence_before();
+    cluster_sync_all();   // both CTAs finished: no MMA writes or remote arrivals pending
+    if (warp == 1) {
+        tc::tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(C::TMEM_COLS)
+                     : "memory");
     }
 }
 
@@ -280,6 +462,29 @@ static int launch_tc(const GemmArgs& g, cudaStream_t st) {
     return QNMT_OK;
 }
 
+int g_tc_pair = 1;   // 0: never use the CTA-pair kernel (A/B testing)
+
+template <int EPI>
+static int launch_tc2(const GemmArgs& g, cudaStream_t st) {
+    constexpr int BN = 256;
+    using C = Tc2Ring<BN>;
+    static size_t attr_done = 0;
+    QNMT_CUDA(raise_smem_limit((const void*)k_gemm_tc2<BN, EPI>, C::SMEM, attr_done));
+    CUtensorMap ta, tb;
+    int rc = tc_get_map(g.W, g.M, g.K, g.ldw, TC_BM, &ta);
+    if (rc) return rc;
+    rc = tc_get_map(g.X, g.N, g.K, g.ldx, BN / 2, &tb);
+    if (rc) return rc;
+    TcEpi e{g.w_scales, g.w_rows_per_scale, g.x_scales, g.col_seg, g.bias, g.Y, g.ldy, g.acc_out, g.flags,
+            g.add1, g.ld1, g.add2, g.ld2};
+    const int tiles = (int)(cdiv(g.M, 2 * TC_BM) * cdiv(g.N, BN));
+    const int pairs = tc_sm_count() / 2;
+    const int grid = 2 * (tiles < pairs ? tiles : pairs);
+    QNMT_LAUNCH(k_gemm_tc2<BN, EPI>, grid, TC_THREADS, C::SMEM, st, ta, tb, (int)g.M, (int)g.N, (int)g.K, e);
+    QNMT_CHECK_LAUNCH("k_gemm_tc2");
+    return QNMT_OK;
+}
+
 bool tc_eligible(const GemmArgs& g) {
     return g.K % 16 == 0 && g.ldw % 16 == 0 && g.ldx % 16 == 0 && ((uintptr_t)g.W % 16 == 0) &&
            ((uintptr_t)g.X % 16 == 0) && g.K <= QNMT_INT32_SAFE_K && g.K > 0 && g.M < (1 << 30) &&
@@ -291,6 +496,21 @@ int gemm_tc_launch(const GemmArgs& g, cudaStream_t st) {
     const int sms = tc_sm_count();
     const int epi = (g.bias ? EPI_BIAS : 0) | ((g.flags & QNMT_GEMM_ACCUMULATE) ? EPI_ACCUMULATE : 0) |
                     (g.acc_out ? EPI_RAW : 0) | (g.add1 ? EPI_ADD2 : 0);
+    // large products (at least two waves of 256 x 256 pair tiles, not graph-captured): CTA pairs
+    if (g_tc_pair && !tl_ndev && !(epi & EPI_ADD2) && g.M >= 2 * TC_BM && g.N >= 256 &&
+        cdiv(g.M, 2 * TC_BM) * cdiv(g.N, 256) >= sms) {
+        switch (epi) {
+            case 0: return launch_tc2<0>(g, st);
+            case 1: return launch_tc2<1>(g, st);
+            case 2: return launch_tc2<2>(g, st);
+            case 3: return launch_tc2<3>(g, st);
+            case 4: return launch_tc2<4>(g, st);
+            case 5: return launch_tc2<5>(g, st);
+            case 6: return launch_tc2<6>(g, st);
+            case 7: return launch_tc2<7>(g, st);
+            default: break;
+        }
+    }
     int bn;
     if (epi & EPI_RAW) {   // op-API accumulator export: three tile widths
         bn = (g.N > 128 && mb * cdiv(g.N, 256) >= sms) ? 256 : (g.N > 64 && mb * cdiv(g.N, 128) >= sms / 2) ? 128 : 64;
@@ -324,3 +544,9 @@ int gemm_tc_launch(const GemmArgs& g, cudaStream_t st) {
 }
 
 }  // namespace qnmt
+
+extern "C" int qnmt_set_tc_pair(int enable) {
+    const int old = qnmt::g_tc_pair;
+    qnmt::g_tc_pair = enable;
+    return old;
+}

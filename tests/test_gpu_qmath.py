@@ -233,3 +233,35 @@ def test_tcgen05_segmented_bias_accumulate():
             yv = O.scale_output(acc[rows, n], ws[blk], xs[seg[n]])
             ref[n, rows] = y0[n, rows] + (yv + bias[rows])
     assert np.array_equal(Y.cpu().numpy(), ref)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("M,K,N", [(4096, 1024, 2560), (4100, 1040, 2600), (8192, 512, 4864)])
+def test_gpu_tc_pair_kernel_matches_single_cta(M, K, N):
+    """CTA-pair tcgen05 GEMM (cta_group::2, M = 256 tiles) == single-CTA kernel and the
+    exact integer product (torch._int_mm on the device, int32), incl. M/N/K tails."""
+    import torch
+    from paper_1804_05038_b200 import _lib
+    import paper_1804_05038_b200 as pb
+    g = torch.Generator(device="cuda").manual_seed(M + K + N)
+    W = torch.randint(-127, 128, (M, K), dtype=torch.int8, device="cuda", generator=g)
+    X = torch.randint(-127, 128, (N, K), dtype=torch.int8, device="cuda", generator=g)
+    ws = torch.rand(1, device="cuda", generator=g) * 100 + 1
+    xs = torch.rand(16, device="cuda", generator=g) * 100 + 1
+    seg = (torch.arange(N, device="cuda", dtype=torch.int32) * 16) // N
+    bias = torch.randn(M, device="cuda", generator=g)
+    lib = _lib.load()
+    outs = []
+    for pair in (1, 0):
+        old = lib.qnmt_set_tc_pair(pair)
+        acc = torch.empty((N, M), dtype=torch.int64, device="cuda")
+        Y = pb.qmath.gemm_kmajor(W, ws, M, X, xs, col_seg=seg, bias=bias, acc_out=acc,
+                                 Y=torch.empty((N, M), dtype=torch.float32, device="cuda"))
+        lib.qnmt_set_tc_pair(old)
+        outs.append((acc, Y))
+    torch.cuda.synchronize()
+    assert torch.equal(outs[0][0], outs[1][0])
+    assert torch.equal(outs[0][1], outs[1][1])
+    if K % 8 == 0 and N % 8 == 0 and M % 8 == 0:
+        ref = torch._int_mm(X, W.t())
+        assert torch.equal(outs[0][0], ref.to(torch.int64))
