@@ -30,6 +30,10 @@ struct EpiArgs {
     int64_t* acc_out;
     int64_t M;
     int32_t flags;
+    const float* add1 = nullptr;   // y = ((dq + bias) + add1[n][m]) + add2[n][m] (stacked readout terms)
+    int64_t ld1 = 0;
+    const float* add2 = nullptr;
+    int64_t ld2 = 0;
 };
 
 __device__ __forceinline__ void epilogue(const EpiArgs& e, int64_t m, int64_t n, long long acc) {
@@ -41,6 +45,7 @@ __device__ __forceinline__ void epilogue(const EpiArgs& e, int64_t m, int64_t n,
     if (e.bias) y = __fadd_rn(y, e.bias[m]);
     float* dst = e.Y + n * e.ldy + m;
     if (e.flags & QNMT_GEMM_ACCUMULATE) y = __fadd_rn(*dst, y);
+    if (e.add1) y = __fadd_rn(__fadd_rn(y, e.add1[n * e.ld1 + m]), e.add2[n * e.ld2 + m]);
     *dst = y;
 }
 
@@ -58,7 +63,7 @@ __device__ __forceinline__ int dp4a16(int acc, const int4& a, const int4& b) {
 template <int ROWS, int NC>
 __global__ void __launch_bounds__(256)
 k_gemv(const int8_t* __restrict__ W, int64_t M, int64_t K, int64_t ldw,
-       const int8_t* __restrict__ X, int64_t ldx, EpiArgs e, int w_static) {
+       const int8_t* __restrict__ X, int64_t ldx, EpiArgs e, int w_static, const int32_t* n_dev) {
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
     const int64_t row0 = ((int64_t)blockIdx.x * 8 + warp) * ROWS;
@@ -92,6 +97,8 @@ k_gemv(const int8_t* __restrict__ W, int64_t M, int64_t K, int64_t ldw,
         load_w(lane);
     }
     if (row0 >= M) return;
+    // graph-captured decode step: NC is the host-side maximum, the live column count is on the device
+    const int nlive = n_dev ? min(NC, *n_dev) : NC;
     int acc[ROWS][NC];
 #pragma unroll
     for (int r = 0; r < ROWS; ++r)
@@ -121,7 +128,7 @@ k_gemv(const int8_t* __restrict__ W, int64_t M, int64_t K, int64_t ldw,
     for (int t = 0; t < ROWS * NC; ++t) {
         if ((t & 31) == lane) {
             int r = t / NC, j = t % NC;
-            if (row0 + r < M) epilogue(e, row0 + r, j, (long long)acc[r][j]);
+            if (row0 + r < M && j < nlive) epilogue(e, row0 + r, j, (long long)acc[r][j]);
         }
     }
 }
@@ -207,7 +214,7 @@ static int launch_gemv(const int8_t* W, int64_t M, int64_t K, int64_t ldw, const
                        int64_t ldx, const EpiArgs& e, cudaStream_t st) {
     unsigned grid = (unsigned)cdiv(M, 8 * ROWS);
     const int w_static = (e.flags & QNMT_GEMM_W_STATIC) ? 1 : 0;
-    QNMT_LAUNCH(k_gemv<ROWS, NC>, grid, 256, 0, st, W, M, K, ldw, X, ldx, e, w_static);
+    QNMT_LAUNCH(k_gemv<ROWS, NC>, grid, 256, 0, st, W, M, K, ldw, X, ldx, e, w_static, tl_ndev);
     return QNMT_OK;
 }
 
@@ -230,17 +237,24 @@ int g_gemm_impl = 0;
 
 int gemm_i8_launch(const GemmArgs& g, cudaStream_t st) {
     if (g.M <= 0 || g.N <= 0) return QNMT_OK;
-    if (g.add1 && !tc_eligible(g)) { set_error("gemm: epilogue addends need the tcgen05 path"); return QNMT_ERR_CONFIG; }
-    if (g.add1) return gemm_tc_launch(g, st);
-    if (tl_ndev) {   // graph-captured step: device-side N, only the tcgen05 kernel supports it
+    EpiArgs e{g.w_scales, g.w_rows_per_scale, g.x_scales, g.col_seg, g.bias, g.Y, g.ldy,
+              g.acc_out, g.M, g.flags, g.add1, g.ld1, g.add2, g.ld2};
+    bool aligned = (g.K % 16 == 0) && (g.ldw % 16 == 0) && (g.ldx % 16 == 0) &&
+                   ((uintptr_t)g.W % 16 == 0) && ((uintptr_t)g.X % 16 == 0);
+    // batch-sized panels (latency path, N <= 8 incl. graph-captured steps with a device-side N):
+    // the HBM-streaming GEMV, weights prefetched before the PDL wait
+    // (in graph mode only for N <= 2: at beam-size N the tcgen05 tile is faster, measured cfg3 beam 5)
+    const bool gemv_ok = g_gemm_impl != 2 && g.N <= (tl_ndev ? 2 : 8) && aligned && g.K <= QNMT_INT32_SAFE_K &&
+                         g.K > 0;
+    if (g.add1 && !gemv_ok) {
+        if (!tc_eligible(g)) { set_error("gemm: epilogue addends need the tcgen05 path"); return QNMT_ERR_CONFIG; }
+        return gemm_tc_launch(g, st);
+    }
+    if (tl_ndev && !gemv_ok) {   // graph-captured step: device-side N (tcgen05 or GEMV kernels)
         if (!tc_eligible(g)) { set_error("graph mode needs tcgen05-eligible GEMM shapes"); return QNMT_ERR_CONFIG; }
         return gemm_tc_launch(g, st);
     }
     if (g_gemm_impl != 1 && tc_eligible(g) && (g.N > 8 || g_gemm_impl == 2)) return gemm_tc_launch(g, st);
-    EpiArgs e{g.w_scales, g.w_rows_per_scale, g.x_scales, g.col_seg, g.bias, g.Y, g.ldy,
-              g.acc_out, g.M, g.flags};
-    bool aligned = (g.K % 16 == 0) && (g.ldw % 16 == 0) && (g.ldx % 16 == 0) &&
-                   ((uintptr_t)g.W % 16 == 0) && ((uintptr_t)g.X % 16 == 0);
     if (g.K > QNMT_INT32_SAFE_K || !aligned || g.K == 0) {
         k_gemm_generic<<<(unsigned)(g.M * g.N), 128, 0, st>>>(g.W, g.M, g.K, g.ldw, g.X, g.N, g.ldx, e);
         QNMT_CHECK_LAUNCH("k_gemm_generic");
