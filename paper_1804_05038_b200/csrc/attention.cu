@@ -302,6 +302,10 @@ k_att_score5(const float* __restrict__ u, int64_t ldu, const int32_t* __restrict
         uq[k] = ok ? reinterpret_cast<const float4*>(u + (int64_t)c0 * ldu)[q] : make_float4(0.f, 0.f, 0.f, 0.f);
     }
     float2 sp = st_thr[c0];
+    int vsum = 0;
+#pragma unroll
+    for (int k = 0; k < AQ5; ++k) vsum += vv[k][0] + vv[k][1] + vv[k][2] + vv[k][3];
+    const int vsum_off = (int)((unsigned)vsum * 0x4B400000u);
     __syncthreads();   // s_done initialised
     for (int j = 0; j < P; ++j) {
         float2 spx = sp;
@@ -336,10 +340,14 @@ k_att_score5(const float* __restrict__ u, int64_t ldu, const int32_t* __restrict
                         const float v = fmaf(m2st, r, st);
                         const float mg = __fadd_rn(v, 12582912.0f);   // 1.5 * 2^23
                         dmx[p] = fmaxf(dmx[p], fabsf(__fsub_rn(v, __fsub_rn(mg, 12582912.0f))));
-                        acc[p] += vv[k][e] * (__float_as_int(mg) - 0x4B400000);
+                        // code = bits - 0x4B400000: the offset is removed once per position below
+                        acc[p] = (int)((unsigned)acc[p] + (unsigned)vv[k][e] * (unsigned)__float_as_int(mg));
                     }
                 }
             }
+#pragma unroll
+            for (int p = 0; p < APC5; ++p)   // sum_a v_a * code_a = sum_a v_a * bits_a - 0x4B400000 * sum_a v_a (mod 2^32)
+                if (p < np) acc[p] = (int)((unsigned)acc[p] - (unsigned)vsum_off);
             // rare: a position with an element within the window of a rounding boundary is
             // recomputed, flagged elements exactly (fp64 tanh)
 #pragma unroll
