@@ -165,7 +165,7 @@ struct qnmt_engine {
     double* cand_score;      // [N][B]
     int32_t* cand_tok;
     int32_t* n_live;
-    int32_t* P; int32_t* col_off; int32_t* done; int32_t* max_steps; int32_t* steps_run;
+    int32_t* P; int32_t* col_off; int32_t* done; int32_t* max_steps; int32_t* steps_run; int32_t* np_tmp;
     int32_t* fin_cnt; double* fin_best;
     // history/finished (grown on demand)
     char* hblock = nullptr;
@@ -908,6 +908,7 @@ int qnmt_engine_create(const qnmt_model* m, int32_t max_sentences, int32_t max_s
         e->done = a.take<int32_t>(S);
         e->max_steps = a.take<int32_t>(S);
         e->steps_run = a.take<int32_t>(S);
+        e->np_tmp = a.take<int32_t>(S);
         e->fin_cnt = a.take<int32_t>(S);
         e->fin_best = a.take<double>(S);
         if (pass == 0) {
@@ -1096,6 +1097,7 @@ static int capture_step(qnmt_engine* e, int cur, int n, int beam, int k_list, cu
                            (e->hist_steps + 1) * e->B, e->hist_steps, e->B, e->cand_score, e->cand_tok,
                            e->col_sent[cur ^ 1], e->parent_col, e->y[cur ^ 1], e->live[cur ^ 1],
                            e->d_N + (cur ^ 1), e->d_step};
+            ss.np_tmp = e->np_tmp;
             rc = search_step_launch(ss, 0, n, beam, k_list, cs);
         }
     }
@@ -1227,10 +1229,12 @@ static int init_search(qnmt_engine* e, const BatchPlan& b, int32_t n, cudaStream
 }
 
 static SearchState search_state(qnmt_engine* e, int cur, int32_t* n_out) {
-    return SearchState{e->P, e->col_off, e->done, e->max_steps, e->steps_run, e->fin_cnt, e->fin_best,
-                       e->fin_score, e->fin_step, e->fin_slot, e->fin_eos, e->hist_tok, e->hist_par,
-                       (e->hist_steps + 1) * e->B, e->hist_steps, e->B, e->cand_score, e->cand_tok,
-                       e->col_sent[cur ^ 1], e->parent_col, e->y[cur ^ 1], e->live[cur ^ 1], n_out};
+    SearchState ss{e->P, e->col_off, e->done, e->max_steps, e->steps_run, e->fin_cnt, e->fin_best,
+                   e->fin_score, e->fin_step, e->fin_slot, e->fin_eos, e->hist_tok, e->hist_par,
+                   (e->hist_steps + 1) * e->B, e->hist_steps, e->B, e->cand_score, e->cand_tok,
+                   e->col_sent[cur ^ 1], e->parent_col, e->y[cur ^ 1], e->live[cur ^ 1], n_out};
+    ss.np_tmp = e->np_tmp;
+    return ss;
 }
 
 // device-resident decode of one batch; results stay in the engine until finalize.

@@ -18,7 +18,7 @@
 
 namespace qnmt {
 
-constexpr int FQ_T = 1024;   // threads per segment CTA (the fp64 sigmoid/tanh work needs the occupancy)
+constexpr int FQ_T = 640;    // threads per segment CTA: 5 x 1024 / 4 = 1280 float4 groups -> 2 per thread at beam 5, 2 CTAs / SM
 
 // block max of |v| bits -> scale of the segment (non-finite: flag, scale 1 as k_encode)
 __device__ __forceinline__ float seg_scale(uint32_t m, uint32_t* red, int32_t* err_flag, float* sc_out) {
@@ -77,7 +77,7 @@ __device__ __forceinline__ bool fin4(float4 v) {
     }                                                                    \
     const int c0 = off[s];
 
-__global__ void __launch_bounds__(FQ_T)
+__global__ void __launch_bounds__(FQ_T, 2)
 k_gates_q(const float* __restrict__ gx, int64_t ldgx, const float* __restrict__ gh, int64_t ldgh,
           const float* __restrict__ h, int64_t ldh, int64_t H, const int32_t* __restrict__ off,
           const int32_t* __restrict__ cnt, float* __restrict__ z, int8_t* __restrict__ q_rh, float* sc_rh,
@@ -109,7 +109,7 @@ k_gates_q(const float* __restrict__ gx, int64_t ldgx, const float* __restrict__ 
     seg_encode(vals, P, H, c0, sc, q_rh, H);
 }
 
-__global__ void __launch_bounds__(FQ_T)
+__global__ void __launch_bounds__(FQ_T, 2)
 k_combine_q(const float* __restrict__ gxc, int64_t ldgx, const float* __restrict__ ghc, int64_t ldghc,
             const float* __restrict__ z, const float* __restrict__ h, int64_t ldh, int64_t H,
             const int32_t* __restrict__ off, const int32_t* __restrict__ cnt, float* __restrict__ h_out,
@@ -141,7 +141,7 @@ k_combine_q(const float* __restrict__ gxc, int64_t ldgx, const float* __restrict
     seg_encode(vals, P, H, c0, sc, q_out, H);
 }
 
-__global__ void __launch_bounds__(FQ_T)
+__global__ void __launch_bounds__(FQ_T, 2)
 k_embed_q(const float* __restrict__ table, int64_t rows, int64_t E, const int32_t* __restrict__ ids,
           const int32_t* __restrict__ off, const int32_t* __restrict__ cnt, int8_t* __restrict__ q_out,
           float* sc_out, int32_t* err_flag, int max_cols) {
@@ -163,7 +163,7 @@ k_embed_q(const float* __restrict__ table, int64_t rows, int64_t E, const int32_
     seg_encode(vals, P, E, c0, sc, q_out, E);
 }
 
-__global__ void __launch_bounds__(FQ_T)
+__global__ void __launch_bounds__(FQ_T, 2)
 k_tanh_q(const float* __restrict__ x, int64_t ldx, int64_t D, const int32_t* __restrict__ off,
          const int32_t* __restrict__ cnt, int8_t* __restrict__ q_out, float* sc_out, int32_t* err_flag,
          int max_cols) {
@@ -187,7 +187,7 @@ k_tanh_q(const float* __restrict__ x, int64_t ldx, int64_t D, const int32_t* __r
 }
 
 // a_out[n] = a[parent[n]] (+ codes qa); optionally the same for b (second state)
-__global__ void __launch_bounds__(FQ_T)
+__global__ void __launch_bounds__(FQ_T, 2)
 k_gather_q(const float* __restrict__ a, const float* __restrict__ b, const int32_t* __restrict__ parent,
            int64_t H, const int32_t* __restrict__ off, const int32_t* __restrict__ cnt, float* __restrict__ a_out,
            float* __restrict__ b_out, int8_t* __restrict__ qa, float* sca, int8_t* __restrict__ qb, float* scb,

@@ -1,6 +1,6 @@
 // search.cu -- device-resident beam bookkeeping for a batch of sentences.
 //
-// One thread per sentence executes one iteration of decoder.py:112-155:
+// One iteration of decoder.py:112-155 for every live sentence of the batch:
 //   chosen  = top-`beam` of the parent-major candidates under
 //             (score desc, token asc, parent asc)            (_select_candidates :74-85)
 //   EOS candidates -> finished list; others -> next live set  (:127-141)
@@ -29,109 +29,143 @@ __device__ __forceinline__ bool cand_better(double sa, int ta, int pa, double sb
     return pa < pb;
 }
 
-__global__ void __launch_bounds__(SEARCH_T)
-k_search_step(SearchState ss, int step, int n_sent, int beam, int k_list) {
+// Two kernels per step.
+//  k_search_select (one warp per sentence, many CTAs): the sentence's P * kt
+//    candidates (kt = min(k_list, beam) per parent list, each sorted by (score
+//    desc, token asc)) are spread over the lanes; a candidate's rank under
+//    (score desc, token asc, parent asc) is the number of better candidates, so
+//    the selection is ranks < beam -- the same set and order as the P-way merge
+//    of decoder.py:74-85.  Lane 0 applies the finished / live rules in rank order
+//    and parks the live selections (token | parent << 26, score) in the
+//    sentence's consumed candidate slots (P * k_list >= selections).
+//  k_search_layout (one CTA): prefix sum of the live counts over sentences and
+//    the next step's column layout from the parked selections.
+constexpr int SEL_WARPS = 8;
+constexpr int SLOTS = 8;   // candidates per lane (P * kt <= 16 * 16 = 256)
+
+__global__ void __launch_bounds__(32 * SEL_WARPS)
+k_search_select(SearchState ss, int step, int n_sent, int beam, int k_list) {
     pdl_entry();
-    __shared__ int wsum[SEARCH_T / 32];
-    const int tid = threadIdx.x;
+    __shared__ double sel_sc[SEL_WARPS][16];
+    __shared__ int sel_tok[SEL_WARPS][16], sel_par[SEL_WARPS][16];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int s = blockIdx.x * SEL_WARPS + warp;
+    if (s >= n_sent) return;   // warp-uniform
     if (ss.step_dev) step = *ss.step_dev;   // graph-captured loop: step counter lives on the device
-    int new_p = 0;
-    // per-thread selection results
-    int sel_tok[16], sel_par[16];
-    double sel_sc[16];
-    int nsel = 0;
-    const int s = tid;
-    if (s < n_sent && !ss.done[s]) {
-        const int P = ss.P[s];
-        const int off = ss.col_off[s];
-        // merge with each parent's current head kept in registers: one dependent load per round
-        const int kt = min(k_list, beam);
-        double hs[16];
-        int ht[16], ptr[16];
+    if (ss.done[s]) {
+        if (lane == 0) ss.np_tmp[s] = 0;
+        return;
+    }
+    const int kt = min(k_list, beam);
+    const int P = ss.P[s];
+    const int off = ss.col_off[s];
+    const int C = P * kt;
+    const int nslot = (C + 31) >> 5;   // warp-uniform
+    double cs[SLOTS];
+    int ct[SLOTS], cp[SLOTS], rk[SLOTS];
 #pragma unroll
-        for (int p = 0; p < 16; ++p) {
-            ptr[p] = 0;
-            if (p < P) {
-                const int64_t idx = (int64_t)(off + p) * k_list;
-                hs[p] = ss.cand_score[idx];
-                ht[p] = ss.cand_tok[idx];
-            }
-        }
-        for (int r = 0; r < beam; ++r) {
-            int bp = -1;
-            double bs = 0.0;
-            int bt = 0;
-#pragma unroll
-            for (int p = 0; p < 16; ++p) {
-                if (p >= P || ptr[p] >= kt) continue;
-                if (bp < 0 || cand_better(hs[p], ht[p], p, bs, bt, bp)) {
-                    bp = p;
-                    bs = hs[p];
-                    bt = ht[p];
-                }
-            }
-            if (bp < 0) break;
-            sel_tok[nsel] = bt;
-            sel_par[nsel] = bp;
-            sel_sc[nsel] = bs;
-            nsel++;
-#pragma unroll
-            for (int p = 0; p < 16; ++p)
-                if (p == bp) {
-                    ptr[p]++;
-                    if (ptr[p] < kt) {
-                        const int64_t idx = (int64_t)(off + p) * k_list + ptr[p];
-                        hs[p] = ss.cand_score[idx];
-                        ht[p] = ss.cand_tok[idx];
-                    }
-                }
-        }
-        // split into finished / live
-        double best_live = -DBL_MAX;
-        int64_t hbase = ((int64_t)s * ss.max_steps_cap + step) * ss.beam_cap;
-        for (int i = 0; i < nsel; ++i) {
-            if (sel_tok[i] == EOS) {
-                int f = ss.fin_cnt[s]++;
-                int64_t fb = (int64_t)s * ss.fin_cap + f;
-                ss.fin_score[fb] = sel_sc[i];
-                ss.fin_step[fb] = step;
-                ss.fin_slot[fb] = sel_par[i];
-                ss.fin_eos[fb] = 1;
-                if (f == 0 || sel_sc[i] > ss.fin_best[s]) ss.fin_best[s] = sel_sc[i];
-            } else {
-                ss.hist_tok[hbase + new_p] = sel_tok[i];
-                ss.hist_par[hbase + new_p] = sel_par[i];
-                if (sel_sc[i] > best_live) best_live = sel_sc[i];
-                sel_tok[new_p] = sel_tok[i];
-                sel_par[new_p] = sel_par[i];
-                sel_sc[new_p] = sel_sc[i];
-                new_p++;
-            }
-        }
-        bool stop = false;
-        if (new_p == 0) {
-            stop = true;                                   // :143-144
-        } else if (ss.fin_cnt[s] > 0 && ss.fin_best[s] >= best_live) {
-            stop = true;                                   // :150-151
-        } else if (step == ss.max_steps[s] - 1) {
-            for (int j = 0; j < new_p; ++j) {              // :152-155
-                int f = ss.fin_cnt[s]++;
-                int64_t fb = (int64_t)s * ss.fin_cap + f;
-                ss.fin_score[fb] = sel_sc[j];
-                ss.fin_step[fb] = step;
-                ss.fin_slot[fb] = j;
-                ss.fin_eos[fb] = 0;
-            }
-            stop = true;
-        }
-        ss.steps_run[s] = step + 1;
-        if (stop) {
-            ss.done[s] = 1;
-            new_p = 0;
+    for (int q = 0; q < SLOTS; ++q) {
+        const int c = q * 32 + lane;
+        rk[q] = 0;
+        if (q < nslot && c < C) {
+            const int p = c / kt, r = c - p * kt;
+            const int64_t idx = (int64_t)(off + p) * k_list + r;
+            cs[q] = ss.cand_score[idx];
+            ct[q] = ss.cand_tok[idx];
+            cp[q] = p;
+        } else {
+            cs[q] = -DBL_MAX;
+            ct[q] = 0x7fffffff;
+            cp[q] = 0x7fffffff;
         }
     }
+#pragma unroll
+    for (int q2 = 0; q2 < SLOTS; ++q2) {
+        if (q2 >= nslot) break;
+        const int nsrc = min(32, C - q2 * 32);   // warp-uniform
+        for (int src = 0; src < nsrc; ++src) {
+            const double os = __shfl_sync(0xffffffffu, cs[q2], src);
+            const int ot = __shfl_sync(0xffffffffu, ct[q2], src);
+            const int op = __shfl_sync(0xffffffffu, cp[q2], src);
+#pragma unroll
+            for (int q = 0; q < SLOTS; ++q)
+                if (q < nslot) rk[q] += cand_better(os, ot, op, cs[q], ct[q], cp[q]) ? 1 : 0;
+        }
+    }
+    const int nsel = min(beam, C);
+#pragma unroll
+    for (int q = 0; q < SLOTS; ++q) {
+        const int c = q * 32 + lane;
+        if (q < nslot && c < C && rk[q] < beam) {
+            sel_sc[warp][rk[q]] = cs[q];
+            sel_tok[warp][rk[q]] = ct[q];
+            sel_par[warp][rk[q]] = cp[q];
+        }
+    }
+    __syncwarp();
+    if (lane != 0) return;
+    // finished / live split (decoder.py:127-141), in selection order
+    double best_live = -DBL_MAX;
+    int new_p = 0;
+    const int64_t hbase = ((int64_t)s * ss.max_steps_cap + step) * ss.beam_cap;
+    int fin = ss.fin_cnt[s];
+    double fbest = ss.fin_best[s];
+    for (int i = 0; i < nsel; ++i) {
+        const double sc = sel_sc[warp][i];
+        const int tok = sel_tok[warp][i], par = sel_par[warp][i];
+        if (tok == EOS) {
+            const int64_t fb = (int64_t)s * ss.fin_cap + fin;
+            ss.fin_score[fb] = sc;
+            ss.fin_step[fb] = step;
+            ss.fin_slot[fb] = par;
+            ss.fin_eos[fb] = 1;
+            if (fin == 0 || sc > fbest) fbest = sc;
+            ++fin;
+        } else {
+            ss.hist_tok[hbase + new_p] = tok;
+            ss.hist_par[hbase + new_p] = par;
+            if (sc > best_live) best_live = sc;
+            const int64_t idx = (int64_t)off * k_list + new_p;
+            ss.cand_score[idx] = sc;
+            ss.cand_tok[idx] = tok | (par << 26);
+            ++new_p;
+        }
+    }
+    bool stop = false;
+    if (new_p == 0) {
+        stop = true;                                   // :143-144
+    } else if (fin > 0 && fbest >= best_live) {
+        stop = true;                                   // :150-151
+    } else if (step == ss.max_steps[s] - 1) {
+        for (int j = 0; j < new_p; ++j) {              // :152-155
+            const int64_t fb = (int64_t)s * ss.fin_cap + fin;
+            ss.fin_score[fb] = ss.cand_score[(int64_t)off * k_list + j];
+            ss.fin_step[fb] = step;
+            ss.fin_slot[fb] = j;
+            ss.fin_eos[fb] = 0;
+            ++fin;
+        }
+        stop = true;
+    }
+    ss.fin_cnt[s] = fin;
+    ss.fin_best[s] = fbest;
+    ss.steps_run[s] = step + 1;
+    if (stop) {
+        ss.done[s] = 1;
+        new_p = 0;
+    }
+    ss.np_tmp[s] = new_p;
+}
+
+__global__ void __launch_bounds__(SEARCH_T)
+k_search_layout(SearchState ss, int step, int n_sent, int k_list) {
+    pdl_entry();
+    __shared__ int wsum[SEARCH_T / 32];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+    if (ss.step_dev) step = *ss.step_dev;
+    const int s = tid;
+    const int new_p = s < n_sent ? ss.np_tmp[s] : 0;
     // exclusive prefix sum of new_p over sentences: warp scans, then a scan of the warp sums
-    const int lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
     int incl = new_p;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -153,14 +187,16 @@ k_search_step(SearchState ss, int step, int n_sent, int beam, int k_list) {
     incl += warp > 0 ? wsum[warp - 1] : 0;
     const int new_off = incl - new_p;
     if (tid == (int)blockDim.x - 1) *ss.n_live = incl;
-    if (s < n_sent) {
+    if (s < n_sent) {   // only this thread touches col_off[s] / P[s]; only cand_* slots of s are read
         const int old_off = ss.col_off[s];
         for (int j = 0; j < new_p; ++j) {
-            int n = new_off + j;
+            const int64_t idx = (int64_t)old_off * k_list + j;
+            const int v = ss.cand_tok[idx];
+            const int n = new_off + j;
             ss.col_sent_next[n] = s;
-            ss.parent_col[n] = old_off + sel_par[j];
-            ss.y_next[n] = sel_tok[j];
-            ss.live_next[n] = sel_sc[j];
+            ss.parent_col[n] = old_off + (v >> 26);
+            ss.y_next[n] = v & ((1 << 26) - 1);
+            ss.live_next[n] = ss.cand_score[idx];
         }
         ss.P[s] = new_p;
         ss.col_off[s] = new_off;
@@ -205,13 +241,17 @@ __global__ void k_gather_rows(const float* __restrict__ a, const float* __restri
 
 int search_step_launch(const SearchState& ss, int step, int n_sent, int beam, int k_list,
                        cudaStream_t st) {
-    if (n_sent > SEARCH_T || beam > 16) {
+    if (n_sent > SEARCH_T || beam > 16 || k_list > 16) {
         set_error("search: n_sent=%d beam=%d exceed limits (%d, 16)", n_sent, beam, SEARCH_T);
         return QNMT_ERR_CONFIG;
     }
+    if (!ss.np_tmp) { set_error("search: no per-sentence scratch"); return QNMT_ERR_CONFIG; }
+    QNMT_LAUNCH(k_search_select, (unsigned)cdiv(n_sent, SEL_WARPS), 32 * SEL_WARPS, 0, st, ss, step, n_sent, beam,
+                k_list);
+    QNMT_CHECK_LAUNCH("k_search_select");
     const int threads = (int)std::min<int64_t>(SEARCH_T, std::max<int64_t>(32, cdiv(n_sent, 32) * 32));
-    QNMT_LAUNCH(k_search_step, 1, threads, 0, st, ss, step, n_sent, beam, k_list);
-    QNMT_CHECK_LAUNCH("k_search_step");
+    QNMT_LAUNCH(k_search_layout, 1, threads, 0, st, ss, step, n_sent, k_list);
+    QNMT_CHECK_LAUNCH("k_search_layout");
     return QNMT_OK;
 }
 

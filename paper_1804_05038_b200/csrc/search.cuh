@@ -20,9 +20,9 @@ struct SearchState {
     int32_t* hist_tok;     // [S][max_steps_cap][beam_cap]
     int32_t* hist_par;
     int32_t fin_cap, max_steps_cap, beam_cap;
-    // per column (current step)
-    const double* cand_score;   // [N][k_list]
-    const int32_t* cand_tok;
+    // per column (current step); the search parks its selections in the consumed slots
+    double* cand_score;    // [N][k_list]
+    int32_t* cand_tok;
     // per column (next step)
     int32_t* col_sent_next;
     int32_t* parent_col;
@@ -30,6 +30,7 @@ struct SearchState {
     double* live_next;
     int32_t* n_live;       // device scalar: columns of the next step
     int32_t* step_dev;     // device step counter (graph mode) or nullptr (host passes step)
+    int32_t* np_tmp = nullptr;   // [S] live selections per sentence (select -> layout)
 };
 
 int search_step_launch(const SearchState& ss, int step, int n_sent, int beam, int k_list,
