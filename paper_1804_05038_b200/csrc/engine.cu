@@ -649,9 +649,8 @@ static int step_core(qnmt_engine* e, const StepIO& io, cudaStream_t st) {
                  stk ? &xs3 : nullptr, stk_u ? e->uq + A : nullptr, LU));
     // readout = tanh(((W_s s + b_r) + W_e emb) + W_c ctx)       (layers.py:255-265)
     prof_mark(e, PG_GEMM, st, 2.0 * N * R * (H + E + 2 * H), (double)R * (H + E + 2 * H));
-    if (stk) {   // W_e emb and W_c ctx were computed with the cells' input GEMMs
-        TRY(gemm(m->w_state, R, H, m->w_state_s, R, e->q_sn, N, H, e->sc_sn, seg, m->b_r, e->ro, R, 0, st,
-                 e->gxr + 3 * H, LX, e->gxq + 3 * H, LX));
+    if (stk) {   // W_e emb and W_c ctx were computed with the cells' input GEMMs; added in tanh_q below
+        TRY(gemm(m->w_state, R, H, m->w_state_s, R, e->q_sn, N, H, e->sc_sn, seg, m->b_r, e->ro, R, 0, st));
     } else {
         TRY(gemm(m->w_state, R, H, m->w_state_s, R, e->q_sn, N, H, e->sc_sn, seg, m->b_r, e->ro, R, 0, st));
         TRY(gemm(m->w_embed, R, E, m->w_embed_s, R, e->q_emb, N, E, e->sc_emb, seg, nullptr, e->ro, R,
@@ -662,7 +661,7 @@ static int step_core(qnmt_engine* e, const StepIO& io, cudaStream_t st) {
     prof_mark(e, PG_MISC, st);
     if (fq) {
         TRY(tanh_q_launch(e->ro, R, R, io.sent_col_off, io.sent_ncols, ns, io.max_cols, e->q_ro, e->sc_ro, e->err,
-                          st));
+                          st, stk ? e->gxr + 3 * H : nullptr, LX, stk ? e->gxq + 3 * H : nullptr, LX));
     } else {
         TRY(tanh_launch(e->ro, N, R, R, e->ro, R, e->err, st));
         TRY(quantize_launch(e->ro, N, R, R, seg, ns, e->q_ro, R, e->sc_ro, e->seg_bits, 1, e->err, st));

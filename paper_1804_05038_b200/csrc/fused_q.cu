@@ -166,7 +166,7 @@ k_embed_q(const float* __restrict__ table, int64_t rows, int64_t E, const int32_
 __global__ void __launch_bounds__(FQ_T, 2)
 k_tanh_q(const float* __restrict__ x, int64_t ldx, int64_t D, const int32_t* __restrict__ off,
          const int32_t* __restrict__ cnt, int8_t* __restrict__ q_out, float* sc_out, int32_t* err_flag,
-         int max_cols) {
+         int max_cols, const float* __restrict__ a1, int64_t ld1, const float* __restrict__ a2, int64_t ld2) {
     pdl_entry();
     FQ_SEG_PROLOGUE
     uint32_t m = 0;
@@ -175,7 +175,12 @@ k_tanh_q(const float* __restrict__ x, int64_t ldx, int64_t D, const int32_t* __r
 #pragma unroll 2
     for (int64_t g = threadIdx.x; g < G; g += FQ_T) {
         const int64_t c = (4 * g) / D, j = 4 * g - c * D;
-        const float4 xv = ld4(x + (int64_t)(c0 + c) * ldx + j);
+        float4 xv = ld4(x + (int64_t)(c0 + c) * ldx + j);
+        if (a1) {   // readout terms of stacked GEMMs: ((W_s s + b_r) + W_e e) + W_c c (layers.py:255-265)
+            const float4 u = ld4(a1 + (int64_t)(c0 + c) * ld1 + j), w = ld4(a2 + (int64_t)(c0 + c) * ld2 + j);
+            xv = make_float4(__fadd_rn(__fadd_rn(xv.x, u.x), w.x), __fadd_rn(__fadd_rn(xv.y, u.y), w.y),
+                             __fadd_rn(__fadd_rn(xv.z, u.z), w.z), __fadd_rn(__fadd_rn(xv.w, u.w), w.w));
+        }
         bad |= !fin4(xv);
         const float4 v = make_float4(tanh_b(xv.x), tanh_b(xv.y), tanh_b(xv.z), tanh_b(xv.w));
         st4(vals + 4 * g, v);
@@ -273,12 +278,14 @@ int embed_q_launch(const float* table, int64_t rows, int64_t E, const int32_t* i
 }
 
 int tanh_q_launch(const float* x, int64_t ldx, int64_t D, const int32_t* off, const int32_t* cnt, int n_seg,
-                  int max_cols, int8_t* q_out, float* sc_out, int32_t* err_flag, cudaStream_t st) {
+                  int max_cols, int8_t* q_out, float* sc_out, int32_t* err_flag, cudaStream_t st, const float* a1,
+                  int64_t ld1, const float* a2, int64_t ld2) {
     if (n_seg <= 0) return QNMT_OK;
     const size_t smem = (size_t)max_cols * D * sizeof(float);
     static size_t done = 0;
     FQ_TRY(set_smem((const void*)k_tanh_q, smem, done));
-    QNMT_LAUNCH(k_tanh_q, (unsigned)n_seg, FQ_T, smem, st, x, ldx, D, off, cnt, q_out, sc_out, err_flag, max_cols);
+    QNMT_LAUNCH(k_tanh_q, (unsigned)n_seg, FQ_T, smem, st, x, ldx, D, off, cnt, q_out, sc_out, err_flag, max_cols, a1,
+                ld1, a2, ld2);
     QNMT_CHECK_LAUNCH("k_tanh_q");
     return QNMT_OK;
 }

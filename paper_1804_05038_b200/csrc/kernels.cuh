@@ -91,7 +91,8 @@ int embed_q_launch(const float* table, int64_t rows, int64_t E, const int32_t* i
                    const int32_t* cnt, int n_seg, int max_cols, int8_t* q_out, float* sc_out, int32_t* err_flag,
                    cudaStream_t st);
 int tanh_q_launch(const float* x, int64_t ldx, int64_t D, const int32_t* off, const int32_t* cnt, int n_seg,
-                  int max_cols, int8_t* q_out, float* sc_out, int32_t* err_flag, cudaStream_t st);
+                  int max_cols, int8_t* q_out, float* sc_out, int32_t* err_flag, cudaStream_t st,
+                  const float* a1 = nullptr, int64_t ld1 = 0, const float* a2 = nullptr, int64_t ld2 = 0);
 int gather_q_launch(const float* a, const float* b, const int32_t* parent, int64_t H, const int32_t* off,
                     const int32_t* cnt, int n_seg, int max_cols, float* a_out, float* b_out, int8_t* qa,
                     float* sca, int8_t* qb, float* scb, int32_t* err_flag, cudaStream_t st);
