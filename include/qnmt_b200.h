@@ -114,6 +114,10 @@ int qnmt_set_gemm_impl(int impl);
  * CTA-pair tcgen05 kernel (cta_group::2, M = 256); 0: single-CTA tiles only.
  * Results are identical.  Returns the old value. */
 int qnmt_set_tc_pair(int enable);
+/* 1 (default): translations of one sentence at beam 1 run the persistent
+ * batch-1 decode kernel (one cooperative launch for all steps); 0: the step
+ * graphs.  Results are identical.  Returns the old value. */
+int qnmt_set_greedy1(int enable);
 
 /* fp32 precision path: replaces qmath.py:434-440
  * (gemm_f32) in LinearOp's float branch (layers.py:138-145).

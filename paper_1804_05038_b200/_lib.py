@@ -56,6 +56,7 @@ SIGNATURES = {
     "qnmt_kernel_launches": (I64, []),
     "qnmt_set_gemm_impl": (I32, [I32]),
     "qnmt_set_tc_pair": (I32, [I32]),
+    "qnmt_set_greedy1": (I32, [I32]),
     "qnmt_set_topk_exact": (I32, [I32]),
     "qnmt_set_vocab_fused": (I32, [I32]),
     "qnmt_engine_profile": (I32, [P, I32]),

@@ -18,6 +18,7 @@
 
 #include "gemm.cuh"
 #include "kernels.cuh"
+#include "persistent.cuh"
 #include "search.cuh"
 
 namespace qnmt {
@@ -166,6 +167,7 @@ struct qnmt_engine {
     int32_t* cand_tok;
     int32_t* n_live;
     int32_t* P; int32_t* col_off; int32_t* done; int32_t* max_steps; int32_t* steps_run; int32_t* np_tmp;
+    int32_t* pk_ctl;         // [8] persistent greedy kernel: y, best token, done, grid barrier
     int32_t* fin_cnt; double* fin_best;
     // history/finished (grown on demand)
     char* hblock = nullptr;
@@ -908,6 +910,7 @@ int qnmt_engine_create(const qnmt_model* m, int32_t max_sentences, int32_t max_s
         e->max_steps = a.take<int32_t>(S);
         e->steps_run = a.take<int32_t>(S);
         e->np_tmp = a.take<int32_t>(S);
+        e->pk_ctl = a.take<int32_t>(8);
         e->fin_cnt = a.take<int32_t>(S);
         e->fin_best = a.take<double>(S);
         if (pass == 0) {
@@ -1236,6 +1239,54 @@ static SearchState search_state(qnmt_engine* e, int cur, int32_t* n_out) {
     return ss;
 }
 
+// Batch-1 greedy translation as one persistent kernel (persistent.cu): the
+// latency path of BASELINE cfg3.  Needs the stacked decoder weights (current-
+// state query) and vectors of at most 2048 values per quantization.
+static bool greedy1_eligible(const qnmt_engine* e) {
+    const qnmt_model* m = e->m;
+    return g_greedy1 && !m->fp32 && m->aq == 0 && e->stack_ok && e->stack_u && e->fq_ok && !e->prof_on &&
+           m->E % 16 == 0 && m->H % 16 == 0 && m->A % 16 == 0 && m->R % 16 == 0 && 2 * m->H <= 2048 &&
+           m->A <= 2048 && m->E <= 2048 && m->R <= 2048 && e->L * 8 <= 96 * 1024;
+}
+
+static int decode_greedy1(qnmt_engine* e, const BatchPlan& b, cudaStream_t st) {
+    const qnmt_model* m = e->m;
+    const int H = m->H;
+    const Cell& c2 = m->cell[2];
+    const Cell& c3 = m->cell[3];
+    PkArgs a{};
+    a.E = m->E; a.H = H; a.A = m->A; a.R = m->R; a.V = m->Vt;
+    a.tgt_embed = m->tgt_embed;
+    a.w2x = e->w2x; a.w2x_s = e->w2x_s; a.b2x = e->b2x;
+    a.uzr2 = c2.uzr; a.uzr2_s = c2.uzr_s; a.uc2 = c2.uc; a.uc2_s = c2.uc_s;
+    a.wuq = e->wuq; a.wuq_s = e->wuq_s;
+    a.w3x = e->w3x; a.w3x_s = e->w3x_s; a.b3x = e->b3x;
+    a.uc3 = c3.uc; a.uc3_s = c3.uc_s;
+    a.v = m->v; a.v_s = m->v_s;
+    a.w_state = m->w_state; a.w_state_s = m->w_state_s; a.b_r = m->b_r;
+    a.w_vocab = m->w_vocab; a.w_vocab_s = m->w_vocab_s; a.b_vocab = m->b_vocab;
+    a.states = e->enc_states; a.att = e->enc_att; a.att_mm = e->att_mm;
+    a.l = (int)b.P;
+    a.max_steps = b.msteps[0];
+    a.s = e->st_s[0]; a.sp = e->st_sp[0];
+    a.gxr = e->gxr; a.gh = e->gh; a.ghc = e->ghc; a.uq = e->uq;
+    a.scores = reinterpret_cast<float*>(e->att_scratch);
+    a.ctx = e->ctx; a.gxq = e->gxq; a.ro = e->ro; a.logits = e->logits;
+    a.part = reinterpret_cast<double*>(e->vocab_part);
+    a.ctl = e->pk_ctl;
+    a.hist_tok = e->hist_tok; a.hist_par = e->hist_par; a.hist_stride = e->B;
+    a.fin_score = e->fin_score; a.fin_step = e->fin_step; a.fin_slot = e->fin_slot; a.fin_eos = e->fin_eos;
+    a.fin_cnt = e->fin_cnt;
+    a.err = e->err;
+    a.stamps = e->stamp_on ? e->stamps : nullptr;
+    a.step_dev = e->d_step;
+    int32_t* ctl0 = e->h_pinned + 4;   // host staging of the control words
+    ctl0[0] = 2; ctl0[1] = 0x7fffffff; ctl0[2] = 0; ctl0[3] = 0; ctl0[4] = 0;
+    QNMT_CUDA(cudaMemcpyAsync(e->pk_ctl, ctl0, 5 * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+    TRY(greedy1_launch(a, st));
+    return check_flag(e, st);
+}
+
 // device-resident decode of one batch; results stay in the engine until finalize.
 static int decode_core(qnmt_engine* e, const int32_t* src_ids, bool ids_on_device, const int32_t* src_len,
                        int32_t n, int32_t beam, double max_ratio, cudaStream_t st) {
@@ -1247,6 +1298,7 @@ static int decode_core(qnmt_engine* e, const int32_t* src_ids, bool ids_on_devic
     TRY(init_member(e, src_ids, ids_on_device, src_len, b, n, st));
     const int Tmax = b.Tmax, Lmax = b.Lmax;
     const int k_list = (int)std::min<int64_t>(beam, V);
+    if (n == 1 && beam == 1 && greedy1_eligible(e)) return decode_greedy1(e, b, st);
     if (graph_eligible(e)) {
         // device-resident loop: one graph launch per step, live count polled every POLL steps
         cudaGraphExec_t g[2];

@@ -1,0 +1,506 @@
+// persistent.cu -- the batch-1 greedy latency path (BASELINE cfg3) as ONE
+// persistent kernel: every decoder step of decoder.translate(beam=1) for one
+// sentence, on a cooperative grid of one CTA per SM with grid-wide barriers
+// between the dependent phases of a step, instead of ~16 kernel launches per
+// step.  Per step (layers.py:356-384 + decoder.py:112-155 at P = 1):
+//
+//   P0  q(emb[y]), q(s)                 (every CTA, redundantly: <= 2H values)
+//       GEMV  [W_x2; W_e] q(emb) + b, U_zr2 q(s)            rows over all warps
+//   P1  z, q(r * s)  ->  GEMV U_c2                          (cell dec_r)
+//   P2  s' = (1-z) s + z tanh(.)  ->  q(s')  ->  GEMV [U_att; U_zr3] q(s')
+//   P3  attention scale; scores of the positions (one CTA per position)
+//   P4  softmax (every CTA); context features over all threads
+//   P5  q(ctx)  ->  GEMV [W_x3; W_c] q(ctx) + b
+//   P6  z, q(r * s')  ->  GEMV U_c3                         (cell dec_q)
+//   P7  s_new  ->  q(s_new)  ->  GEMV W_s q(s_new) + b_r
+//   P8  readout tanh(((.) + W_e e) + W_c c)  ->  q  ->  vocab GEMV (logits)
+//   P9  per-CTA (max, sum exp) of its token range
+//   P10 lse; every CTA finds the smallest token whose log-prob equals the best
+//       one (so the next step needs no further barrier)
+//   P11 CTA 0: search bookkeeping (EOS -> finished, length cap -> frozen)
+//
+// Numerics are those of the batched engine (Tier B): the same quantization,
+// exact integer dot products, exact dequantization (dequant: __ddiv_rn), fp64
+// sigmoid / tanh rounded once, fp64 softmax and context in position order,
+// attention codes from the fp64 tanh (the engine's fast path + exact fallback
+// produces exactly these codes).  Only fp64 summation orders of the vocabulary
+// log-sum-exp differ (as between any two correct implementations).  Results go
+// to the engine's history / finished arrays, so finalize() is unchanged.
+// Weights stay L2-resident across the steps of the one launch (34 MB at cfg3).
+#include <cooperative_groups.h>
+
+#include "kernels.cuh"
+#include "persistent.cuh"
+#include "search.cuh"
+
+namespace qnmt {
+
+constexpr int PK_T = 256;              // threads per CTA (8 warps)
+constexpr int PK_W = PK_T / 32;
+constexpr int PK_MAXD = 2048;          // longest vector quantized per CTA (2H, A <= 2048)
+
+
+
+__device__ __forceinline__ float ldcg(const float* p) { return __ldcg(p); }
+
+// grid-wide barrier (generation counter); every CTA is resident (cooperative launch)
+__device__ __forceinline__ void gsync(int32_t* ctl) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned* count = reinterpret_cast<unsigned*>(ctl + 3);
+        unsigned* gen = reinterpret_cast<unsigned*>(ctl + 4);
+        unsigned g;
+        asm volatile("ld.acquire.gpu.u32 %0, [%1];" : "=r"(g) : "l"(gen) : "memory");
+        __threadfence();
+        if (atomicAdd(count, 1u) == gridDim.x - 1) {
+            atomicExch(count, 0u);
+            __threadfence();
+            atomicAdd(gen, 1u);
+        } else {
+            unsigned cur;
+            do {
+                asm volatile("ld.acquire.gpu.u32 %0, [%1];" : "=r"(cur) : "l"(gen) : "memory");
+            } while (cur == g);
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+// block max of |x| bits
+__device__ __forceinline__ uint32_t block_max_u(uint32_t m, uint32_t* red) {
+    m = warp_max(m);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+    __syncthreads();
+    uint32_t r = red[0];
+#pragma unroll
+    for (int w = 1; w < PK_W; ++w) r = max(r, red[w]);
+    __syncthreads();
+    return r;
+}
+
+// quantize vals[0..D) (smem f32) into q (smem int8) with the segment scale rule
+// (qmath.py:119-142 / fused_q.cu seg_scale: a non-finite max raises the flag, scale 1)
+__device__ float quantize_vec(const float* vals, int D, int8_t* q, uint32_t* red, int32_t* err) {
+    uint32_t m = 0;
+    for (int j = threadIdx.x; j < D; j += PK_T) m = max(m, __float_as_uint(vals[j]) & 0x7fffffffu);
+    uint32_t mm = block_max_u(m, red);
+    if (mm >= 0x7f800000u) {
+        if (threadIdx.x == 0 && blockIdx.x == 0) set_flag(err, QNMT_FLAG_NUMERIC);
+        mm = 0;
+    }
+    const float sc = scale_from_maxbits(mm);
+    for (int j = threadIdx.x; j < D; j += PK_T) q[j] = (int8_t)quant_code(vals[j], sc);
+    __syncthreads();
+    return sc;
+}
+
+// one weight row . q (int8, K % 16 == 0) by a warp: 16-byte chunks per lane, dp4a, REDUX
+__device__ __forceinline__ int row_dot(const int8_t* __restrict__ w, const int8_t* q, int K) {
+    const int lane = threadIdx.x & 31;
+    int acc = 0;
+    for (int k = lane * 16; k < K; k += 512) {
+        const int4 a = __ldg(reinterpret_cast<const int4*>(w + k));
+        const int4 b = *reinterpret_cast<const int4*>(q + k);
+        acc = __dp4a(a.x, b.x, acc);
+        acc = __dp4a(a.y, b.y, acc);
+        acc = __dp4a(a.z, b.z, acc);
+        acc = __dp4a(a.w, b.w, acc);
+    }
+    return __reduce_add_sync(0xffffffffu, acc);
+}
+
+// rows [0, M) of W (row stride K) against q: out[m] = fl32(acc / (sw * sx)) (+ bias[m]);
+// scale of row m: ws[m / rps].  Each warp owns a contiguous block of rows and keeps
+// PK_RB rows' weight loads in flight; lane r dequantizes row r of each group.
+constexpr int PK_RB = 8;
+__device__ __forceinline__ void gemv(const int8_t* __restrict__ W, int M, int K, const float* ws, int rps,
+                                     const int8_t* q, float sx, const float* bias, float* out, int row0, int gw,
+                                     int nw) {
+    const int lane = threadIdx.x & 31;
+    const int rpw = (M + nw - 1) / nw;
+    const int m0 = gw * rpw, m1 = min(M, m0 + rpw);
+    for (int mb = m0; mb < m1; mb += PK_RB) {
+        int acc[PK_RB];
+#pragma unroll
+        for (int r = 0; r < PK_RB; ++r) acc[r] = 0;
+        for (int k = lane * 16; k < K; k += 512) {
+            const int4 b = *reinterpret_cast<const int4*>(q + k);
+            int4 wv[PK_RB];
+#pragma unroll
+            for (int r = 0; r < PK_RB; ++r)
+                wv[r] = (mb + r < m1) ? __ldg(reinterpret_cast<const int4*>(W + (int64_t)(mb + r) * K + k))
+                                      : make_int4(0, 0, 0, 0);
+#pragma unroll
+            for (int r = 0; r < PK_RB; ++r) {
+                acc[r] = __dp4a(wv[r].x, b.x, acc[r]);
+                acc[r] = __dp4a(wv[r].y, b.y, acc[r]);
+                acc[r] = __dp4a(wv[r].z, b.z, acc[r]);
+                acc[r] = __dp4a(wv[r].w, b.w, acc[r]);
+            }
+        }
+        int mine = 0;
+#pragma unroll
+        for (int r = 0; r < PK_RB; ++r) {
+            const int tot = __reduce_add_sync(0xffffffffu, acc[r]);
+            if (lane == r) mine = tot;
+        }
+        const int m = mb + lane;
+        if (lane < PK_RB && m < m1) {
+            float y = dequant(mine, ws[m / rps], sx);
+            if (bias) y = __fadd_rn(y, bias[m]);
+            out[row0 + m] = y;
+        }
+    }
+}
+
+#define PK_STAMP(k)                                                                 \
+    if (a.stamps && blockIdx.x == 0 && threadIdx.x == 0) {                          \
+        long long g_;                                                               \
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_));                      \
+        if ((k) < 11) a.stamps[(int64_t)t * 11 + (k)] = g_;                          \
+    }
+
+__global__ void __launch_bounds__(PK_T, 1) k_greedy1(PkArgs a) {
+    extern __shared__ __align__(16) unsigned char pk_smem[];
+    __shared__ __align__(16) int8_t q[PK_MAXD];
+    __shared__ __align__(16) float vals[PK_MAXD];
+    __shared__ uint32_t red[PK_W];
+    __shared__ double dred[PK_W];
+    __shared__ int sh_done;
+    double* al = reinterpret_cast<double*>(pk_smem);   // [l] softmax weights
+    const int E = a.E, H = a.H, A = a.A, R = a.R, V = a.V, LX = 3 * H + R;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int gw = blockIdx.x * PK_W + warp, nw = gridDim.x * PK_W;
+    double score = 0.0;   // live log-prob (CTA 0, thread 0)
+    int y = 2;            // BOS = EOS (decoder.py:109); afterwards the token every CTA selected
+    for (int t = 0; t < a.max_steps; ++t) {
+        // ---- P0: q(emb[y]), q(s); GEMV [W_x2; W_e] and U_zr2 ----
+        for (int j = threadIdx.x; j < E; j += PK_T) vals[j] = a.tgt_embed[(int64_t)y * E + j];
+        __syncthreads();
+        const float se = quantize_vec(vals, E, q, red, a.err);
+        gemv(a.w2x, LX, E, a.w2x_s, 1, q, se, a.b2x, a.gxr, 0, gw, nw);
+        __syncthreads();
+        for (int j = threadIdx.x; j < H; j += PK_T) vals[j] = ldcg(a.s + j);
+        __syncthreads();
+        const float ss = quantize_vec(vals, H, q, red, a.err);
+        gemv(a.uzr2, 2 * H, H, a.uzr2_s, H, q, ss, nullptr, a.gh, 0, gw, nw);
+        gsync(a.ctl);
+        PK_STAMP(0);
+        // ---- P1: gates of dec_r -> q(r * s); GEMV U_c2 ----
+        bool bad = false;
+        for (int j = threadIdx.x; j < H; j += PK_T) {
+            const float pz = __fadd_rn(ldcg(a.gxr + j), ldcg(a.gh + j));
+            const float pr = __fadd_rn(ldcg(a.gxr + H + j), ldcg(a.gh + H + j));
+            bad |= !(is_finite_f(pz) && is_finite_f(pr));
+            vals[j] = __fmul_rn(sigmoid_b(pr), ldcg(a.s + j));
+        }
+        if (bad && blockIdx.x == 0) set_flag(a.err, QNMT_FLAG_NUMERIC);
+        __syncthreads();
+        const float srh = quantize_vec(vals, H, q, red, a.err);
+        gemv(a.uc2, H, H, a.uc2_s, H, q, srh, nullptr, a.ghc, 0, gw, nw);
+        gsync(a.ctl);
+        PK_STAMP(1);
+        // ---- P2: combine of dec_r -> s', q(s'); GEMV [U_att; U_zr3] ----
+        for (int j = threadIdx.x; j < H; j += PK_T) {
+            const float z = sigmoid_b(__fadd_rn(ldcg(a.gxr + j), ldcg(a.gh + j)));
+            const float pc = __fadd_rn(ldcg(a.gxr + 2 * H + j), ldcg(a.ghc + j));
+            if (!is_finite_f(pc) && blockIdx.x == 0) set_flag(a.err, QNMT_FLAG_NUMERIC);
+            const float h = ldcg(a.s + j);
+            const float v = __fadd_rn(__fmul_rn(__fsub_rn(1.0f, z), h), __fmul_rn(z, tanh_b(pc)));
+            vals[j] = v;
+            if (blockIdx.x == 0) a.sp[j] = v;
+        }
+        __syncthreads();
+        const float ssp = quantize_vec(vals, H, q, red, a.err);
+        gemv(a.wuq, A + 2 * H, H, a.wuq_s, 1, q, ssp, nullptr, a.uq, 0, gw, nw);
+        gsync(a.ctl);
+        PK_STAMP(2);
+        // ---- P3: attention scale (every CTA) and scores (one CTA per position) ----
+        float st;
+        {
+            uint32_t m = 0;
+            for (int k = threadIdx.x; k < A; k += PK_T) {
+                const float u = ldcg(a.uq + k);
+                m = max(m, __float_as_uint(__fadd_rn(a.att_mm[k], u)) & 0x7fffffffu);
+                m = max(m, __float_as_uint(__fadd_rn(a.att_mm[A + k], u)) & 0x7fffffffu);
+            }
+            m = block_max_u(m, red);
+            if (m >= 0x7f800000u) {
+                if (threadIdx.x == 0 && blockIdx.x == 0) set_flag(a.err, QNMT_FLAG_NUMERIC);
+                m = 0;
+            }
+            const float tmax = tanh_b(__uint_as_float(m));
+            st = (tmax == 0.0f) ? 1.0f : __fdiv_rn(127.0f, tmax);
+        }
+        for (int k = threadIdx.x; k < A; k += PK_T) vals[k] = ldcg(a.uq + k);
+        __syncthreads();
+        for (int i = blockIdx.x; i < a.l; i += gridDim.x) {
+            int acc = 0;
+            const float* ap = a.att + (int64_t)i * A;
+            for (int k = threadIdx.x; k < A; k += PK_T)
+                acc += (int)a.v[k] * quant_code(tanh_b(__fadd_rn(ap[k], vals[k])), st);
+            acc = warp_sum(acc);
+            __shared__ int ired[PK_W];
+            if (lane == 0) ired[warp] = acc;
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                int tot = 0;
+                for (int w = 0; w < PK_W; ++w) tot += ired[w];
+                a.scores[i] = dequant(tot, a.v_s[0], st);
+            }
+            __syncthreads();
+        }
+        gsync(a.ctl);
+        PK_STAMP(3);
+        // ---- P4: softmax (every CTA, fp64, sequential sum) and context features ----
+        {
+            float m = -3.402823466e38f;
+            bool bad4 = false;
+            for (int i = threadIdx.x; i < a.l; i += PK_T) {
+                const float x = ldcg(a.scores + i);
+                bad4 |= !is_finite_f(x);
+                m = fmaxf(m, x);
+            }
+            if (bad4 && blockIdx.x == 0) set_flag(a.err, QNMT_FLAG_NUMERIC);
+            m = warp_max(m);
+            if (lane == 0) vals[warp] = m;
+            __syncthreads();
+            float mm = vals[0];
+            for (int w = 1; w < PK_W; ++w) mm = fmaxf(mm, vals[w]);
+            for (int i = threadIdx.x; i < a.l; i += PK_T) {
+                const double tt = (double)ldcg(a.scores + i) - (double)mm;
+                al[i] = tt < -700.0 ? 0.0 : exp_f64(tt);
+            }
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                double sum = 0.0;
+                for (int i = 0; i < a.l; ++i) sum += al[i];
+                dred[0] = sum;
+            }
+            __syncthreads();
+            const double sum = dred[0];
+            for (int i = threadIdx.x; i < a.l; i += PK_T) al[i] = (double)__double2float_rn(al[i] / sum);
+            __syncthreads();
+            // features spread over the CTAs (feature c: CTA c % grid); positions in order, 8 loads in flight
+            for (int c = blockIdx.x + gridDim.x * threadIdx.x; c < 2 * H; c += gridDim.x * PK_T) {
+                double acc = 0.0;
+                const float* sp = a.states + c;
+                int i = 0;
+                for (; i + 8 <= a.l; i += 8) {
+                    float d[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) d[u] = sp[(int64_t)(i + u) * 2 * H];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) acc = fma((double)d[u], al[i + u], acc);
+                }
+                for (; i < a.l; ++i) acc = fma((double)sp[(int64_t)i * 2 * H], al[i], acc);
+                a.ctx[c] = __double2float_rn(acc);
+            }
+        }
+        gsync(a.ctl);
+        PK_STAMP(4);
+        // ---- P5: q(ctx); GEMV [W_x3; W_c] ----
+        for (int j = threadIdx.x; j < 2 * H; j += PK_T) vals[j] = ldcg(a.ctx + j);
+        __syncthreads();
+        const float sctx = quantize_vec(vals, 2 * H, q, red, a.err);
+        gemv(a.w3x, LX, 2 * H, a.w3x_s, 1, q, sctx, a.b3x, a.gxq, 0, gw, nw);
+        gsync(a.ctl);
+        PK_STAMP(5);
+        // ---- P6: gates of dec_q (h = s') -> q(r * s'); GEMV U_c3 ----
+        bad = false;
+        for (int j = threadIdx.x; j < H; j += PK_T) {
+            const float pz = __fadd_rn(ldcg(a.gxq + j), ldcg(a.uq + A + j));
+            const float pr = __fadd_rn(ldcg(a.gxq + H + j), ldcg(a.uq + A + H + j));
+            bad |= !(is_finite_f(pz) && is_finite_f(pr));
+            vals[j] = __fmul_rn(sigmoid_b(pr), ldcg(a.sp + j));
+        }
+        if (bad && blockIdx.x == 0) set_flag(a.err, QNMT_FLAG_NUMERIC);
+        __syncthreads();
+        const float srh3 = quantize_vec(vals, H, q, red, a.err);
+        gemv(a.uc3, H, H, a.uc3_s, H, q, srh3, nullptr, a.ghc, 0, gw, nw);
+        gsync(a.ctl);
+        PK_STAMP(6);
+        // ---- P7: combine of dec_q -> s_new (next state), q(s_new); GEMV W_s + b_r ----
+        for (int j = threadIdx.x; j < H; j += PK_T) {
+            const float z = sigmoid_b(__fadd_rn(ldcg(a.gxq + j), ldcg(a.uq + A + j)));
+            const float pc = __fadd_rn(ldcg(a.gxq + 2 * H + j), ldcg(a.ghc + j));
+            if (!is_finite_f(pc) && blockIdx.x == 0) set_flag(a.err, QNMT_FLAG_NUMERIC);
+            const float h = ldcg(a.sp + j);
+            const float v = __fadd_rn(__fmul_rn(__fsub_rn(1.0f, z), h), __fmul_rn(z, tanh_b(pc)));
+            vals[j] = v;
+            if (blockIdx.x == 0) a.s[j] = v;   // every CTA read s for this step before the last barrier
+        }
+        __syncthreads();
+        const float ssn = quantize_vec(vals, H, q, red, a.err);
+        gemv(a.w_state, R, H, a.w_state_s, R, q, ssn, a.b_r, a.ro, 0, gw, nw);
+        gsync(a.ctl);
+        PK_STAMP(7);
+        // ---- P8: readout tanh -> q; vocabulary GEMV (logits) ----
+        for (int j = threadIdx.x; j < R; j += PK_T) {
+            const float x = __fadd_rn(__fadd_rn(ldcg(a.ro + j), ldcg(a.gxr + 3 * H + j)), ldcg(a.gxq + 3 * H + j));
+            if (!is_finite_f(x) && blockIdx.x == 0) set_flag(a.err, QNMT_FLAG_NUMERIC);
+            vals[j] = tanh_b(x);
+        }
+        __syncthreads();
+        const float sro = quantize_vec(vals, R, q, red, a.err);
+        gemv(a.w_vocab, V, R, a.w_vocab_s, V, q, sro, a.b_vocab, a.logits, 0, gw, nw);
+        gsync(a.ctl);
+        PK_STAMP(8);
+        // ---- P9: per-CTA (max, sum exp(x - max)) over a contiguous token range ----
+        const int per = (V + gridDim.x - 1) / gridDim.x;
+        const int v0 = blockIdx.x * per, v1 = min(V, v0 + per);
+        {
+            float m = -3.402823466e38f;
+            for (int v = v0 + threadIdx.x; v < v1; v += PK_T) m = fmaxf(m, ldcg(a.logits + v));
+            m = warp_max(m);
+            if (lane == 0) vals[warp] = m;
+            __syncthreads();
+            float mm = vals[0];
+            for (int w = 1; w < PK_W; ++w) mm = fmaxf(mm, vals[w]);
+            double sacc = 0.0;
+            for (int v = v0 + threadIdx.x; v < v1; v += PK_T) {
+                const float x = ldcg(a.logits + v);
+                if (!is_finite_f(x)) set_flag(a.err, QNMT_FLAG_NUMERIC);
+                const double tt = (double)x - (double)mm;
+                sacc += tt < -700.0 ? 0.0 : exp_f64(tt);
+            }
+            sacc = warp_sum(sacc);
+            if (lane == 0) dred[warp] = sacc;
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                double tot = 0.0;
+                for (int w = 0; w < PK_W; ++w) tot += dred[w];
+                a.part[2 * blockIdx.x] = v0 < v1 ? (double)mm : -1.0e308;
+                a.part[2 * blockIdx.x + 1] = v0 < v1 ? tot : 0.0;
+            }
+        }
+        gsync(a.ctl);
+        PK_STAMP(9);
+        // ---- P10: lse (every CTA, same order); smallest token with the best log-prob ----
+        // (thread c reads partial c; block tree reductions in a fixed order: every CTA gets the
+        // same M and lse)
+        double mc = -1.0e308, scv = 0.0;
+        if (threadIdx.x < (int)gridDim.x) {
+            mc = __ldcg(a.part + 2 * threadIdx.x);
+            scv = __ldcg(a.part + 2 * threadIdx.x + 1);
+        }
+        double dM = mc;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) dM = fmax(dM, __shfl_xor_sync(0xffffffffu, dM, o));
+        if (lane == 0) dred[warp] = dM;
+        __syncthreads();
+        dM = dred[0];
+#pragma unroll
+        for (int w = 1; w < PK_W; ++w) dM = fmax(dM, dred[w]);
+        __syncthreads();
+        double S = mc > -1.0e308 ? scv * exp_f64(mc - dM) : 0.0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) S += __shfl_xor_sync(0xffffffffu, S, o);
+        if (lane == 0) dred[warp] = S;
+        __syncthreads();
+        S = dred[0];
+#pragma unroll
+        for (int w = 1; w < PK_W; ++w) S += dred[w];
+        __syncthreads();
+        const double lse = log(S);
+        const float lp_best = __double2float_rn((dM - dM) - lse);
+        // every CTA scans the whole vocabulary for the smallest token whose log-prob equals the best
+        // one (logits more than 1.0 below the max cannot round to it): the next y is known everywhere
+        // without another grid barrier
+        {
+            // a token whose log-prob rounds to the best one has a logit within 4 f32-ulps of lp_best
+            // below M (as k_vocab_merge's tie rescan): only those CTAs' token ranges are scanned
+            const int lex = (int)((__float_as_uint(lp_best) >> 23) & 0xffu);
+            const double delta = ldexp(1.0, max(lex, 1) - 150 + 2);
+            __shared__ int cand_cta[PK_T];
+            __shared__ int ncand;
+            if (threadIdx.x == 0) ncand = 0;
+            __syncthreads();
+            if (threadIdx.x < (int)gridDim.x && mc > -1.0e308 && mc >= dM - delta) cand_cta[atomicAdd(&ncand, 1)] = threadIdx.x;
+            __syncthreads();
+            int best = 0x7fffffff;
+            for (int ci = 0; ci < ncand; ++ci) {
+                const int c = cand_cta[ci];
+                const int u0 = c * per, u1 = min(V, u0 + per);
+                for (int v = u0 + threadIdx.x; v < u1; v += PK_T) {
+                    const float x = ldcg(a.logits + v);
+                    if ((double)x >= dM - delta && v < best && __double2float_rn(((double)x - dM) - lse) == lp_best)
+                        best = v;
+                }
+            }
+            best = __reduce_min_sync(0xffffffffu, best);
+            if (lane == 0) red[warp] = (uint32_t)best;
+            __syncthreads();
+            best = (int)red[0];
+#pragma unroll
+            for (int w = 1; w < PK_W; ++w) best = min(best, (int)red[w]);
+            __syncthreads();
+            if (threadIdx.x == 0) sh_done = best;   // (reused as the CTA's token slot)
+        }
+        __syncthreads();
+        const int tok = sh_done;
+        __syncthreads();
+        PK_STAMP(10);
+        // ---- P11: search bookkeeping (decoder.py:112-155 at beam 1); every CTA knows tok ----
+        const bool done = tok == 2 || t == a.max_steps - 1;
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            score += (double)lp_best;
+            if (tok == 2) {   // EOS: the only candidate goes to the finished list, no live hypothesis left
+                a.fin_score[0] = score;
+                a.fin_step[0] = t;
+                a.fin_slot[0] = 0;
+                a.fin_eos[0] = 1;
+                *a.fin_cnt = 1;
+            } else {
+                a.hist_tok[(int64_t)t * a.hist_stride] = tok;
+                a.hist_par[(int64_t)t * a.hist_stride] = 0;
+                if (t == a.max_steps - 1) {   // length cap: the survivor is frozen (for-else)
+                    a.fin_score[0] = score;
+                    a.fin_step[0] = t;
+                    a.fin_slot[0] = 0;
+                    a.fin_eos[0] = 0;
+                    *a.fin_cnt = 1;
+                }
+            }
+        }
+        y = tok;
+        if (done) {
+            if (a.step_dev && blockIdx.x == 0 && threadIdx.x == 0) *a.step_dev = t + 1;
+            break;
+        }
+    }
+}
+
+int g_greedy1 = 1;
+
+int greedy1_launch(const PkArgs& a, cudaStream_t st) {
+    static int grid = 0;
+    const size_t smem = (size_t)a.l * sizeof(double);
+    if (smem > 48 * 1024) {
+        static size_t done = 0;
+        QNMT_CUDA(raise_smem_limit((const void*)k_greedy1, smem, done));
+    }
+    if (!grid) {
+        int dev = 0, sms = 0, per_sm = 0;
+        QNMT_CUDA(cudaGetDevice(&dev));
+        QNMT_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        QNMT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_greedy1, PK_T, smem));
+        if (per_sm < 1) { set_error("greedy1: kernel does not fit on an SM"); return QNMT_ERR_CUDA; }
+        grid = sms < PK_T ? sms : PK_T;   // P10 reads one vocabulary partial per thread
+    }
+    PkArgs args = a;
+    void* params[] = {&args};
+    QNMT_CUDA(cudaLaunchCooperativeKernel((const void*)k_greedy1, dim3(grid), dim3(PK_T), params, smem, st));
+    count_launch();
+    QNMT_CUDA(cudaGetLastError());
+    return QNMT_OK;
+}
+
+}  // namespace qnmt
+
+extern "C" int qnmt_set_greedy1(int enable) {
+    const int old = qnmt::g_greedy1;
+    qnmt::g_greedy1 = enable;
+    return old;
+}

@@ -89,31 +89,40 @@ k_vocab_stats(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ C
         const int half = ew >> 2;    // token group of the tile
         const int np = VT_SPLIT * n_blocks;
         const bool one_scale = e.w_rows_per_scale >= V;   // kernel-uniform
-        const double isw0 = 1.0 / (double)e.w_scales[0];
+        const float sw0 = e.w_scales[0];
+        const double isw0 = 1.0 / (double)sw0;
         bool bad = false;
         int it = 0;
+        // the row's activation scale and multipliers depend only on the m-block: computed when it
+        // changes (consecutive tiles of the persistent schedule mostly share it), not per tile
+        int cur_mb = -1;
+        float sx = 1.0f;
+        double isx = 1.0, rs0 = isw0;
         for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++it) {
             const int mb = tile / n_blocks, nb = tile % n_blocks;
             const int buf = it & 1;
             const uint32_t use = (uint32_t)(it >> 1) & 1u;
-            if (ew * 32 < VT_BN) {   // per-token weight scale and bias of this tile -> smem
+            if (ew * 32 < VT_BN) {   // per-token bias (and per-token weight scale) of this tile -> smem
                 const int c = ew * 32 + lane;
                 const int v = nb * VT_BN + c;
-                float sw = 1.0f, b = 0.0f;
-                if (v < V) {
-                    sw = e.w_scales[v / e.w_rows_per_scale];
-                    b = e.bias ? e.bias[v] : 0.0f;
+                float b = 0.0f;
+                if (v < V && e.bias) b = e.bias[v];
+                if (!one_scale) {
+                    const float sw = v < V ? e.w_scales[v / e.w_rows_per_scale] : 1.0f;
+                    col_sw[buf][c] = sw;
+                    col_isw[buf][c] = 1.0 / (double)sw;
                 }
-                col_sw[buf][c] = sw;
-                col_isw[buf][c] = 1.0 / (double)sw;
                 col_b[buf][c] = b;
                 bad |= !is_finite_f(b);
             }
             const int row = mb * TC_BM + lg * 32 + lane;
             const bool rok = row < M;
-            const float sx = rok ? e.x_scales[e.row_seg ? e.row_seg[row] : 0] : 1.0f;
-            const double isx = 1.0 / (double)sx;
-            const double rs0 = isx * isw0;   // acc -> logit multiplier when W has one scale
+            if (mb != cur_mb) {
+                sx = rok ? e.x_scales[e.row_seg ? e.row_seg[row] : 0] : 1.0f;
+                isx = 1.0 / (double)sx;
+                rs0 = isx * isw0;   // acc -> logit multiplier when W has one scale
+                cur_mb = mb;
+            }
             asm volatile("bar.sync 1, %0;" ::"n"(32 * VT_EPI_WARPS));
             tc::mbar_wait(&bars.tfull[buf], use);
             tc::tc_fence_after();
@@ -151,7 +160,7 @@ k_vocab_stats(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ C
                         for (int j = 0; j < 16; ++j) {
                             const double q = (double)(int)r[j] * rs0;
                             const int d = (int)((uint32_t)__double2loint(q) & 0x1fffffffu) - 0x10000000;
-                            if (abs(d) <= 64) x[j] = dequant((int)r[j], col_sw[buf][c0 + j], sx);
+                            if (abs(d) <= 64) x[j] = dequant((int)r[j], sw0, sx);   // (fast path: one scale)
                         }
                     }
                     const float4* b4 = reinterpret_cast<const float4*>(&col_b[buf][c0]);
@@ -167,9 +176,10 @@ k_vocab_stats(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ C
 #pragma unroll
                     for (int j = 0; j < 16; ++j) {
                         if (j < ncols) {
-                            const double q = (double)(int)r[j] * (isx * col_isw[buf][c0 + j]);
-                            x[j] = dequant_rcp_safe(q) ? __double2float_rn(q)
-                                                       : dequant((int)r[j], col_sw[buf][c0 + j], sx);
+                            const double isw = one_scale ? isw0 : col_isw[buf][c0 + j];
+                            const float swj = one_scale ? sw0 : col_sw[buf][c0 + j];
+                            const double q = (double)(int)r[j] * (isx * isw);
+                            x[j] = dequant_rcp_safe(q) ? __double2float_rn(q) : dequant((int)r[j], swj, sx);
                             x[j] = __fadd_rn(x[j], col_b[buf][c0 + j]);
                         } else {
                             x[j] = -FLT_MAX;   // excluded below (exp skipped, never above a real logit)

@@ -276,3 +276,29 @@ def test_engine_variants_stacked(query, s0):
     for i, s in enumerate(sents):
         toks, lp = om.translate(s, 4, 1.5)
         assert out[0][i] == toks and out[1][i] == lp, i
+
+
+@pytest.mark.gpu
+def test_gpu_persistent_greedy_matches_oracle_and_step_graphs():
+    """Batch-1 greedy translations through the persistent decode kernel (persistent.cu)
+    == the oracle == the step-graph engine, incl. sentences that end on EOS."""
+    import paper_1804_05038_b200 as pb
+    from paper_1804_05038_b200 import _lib
+    lib = _lib.load()
+    for seed, ws, bs, eb in ((61, 0.3, 0.1, 0.6), (62, 0.05, 0.0, 0.0), (63, 0.5, 0.1, 1.0)):
+        d = pb.Dims(300, 251, 32, 48, 64, 32)
+        params = pb.synthetic_model(d, seed, ws, bs, eb)
+        qm = pb.quantize_model(params)
+        om = O.QModel(O.Dims(**d.as_dict()), params.tensors)
+        rng = np.random.default_rng(seed)
+        for _ in range(6):
+            src = rng.integers(3, 300, int(rng.integers(1, 30))).tolist()
+            ratio = float(rng.choice([0.5, 1.5, 3.0]))
+            old = lib.qnmt_set_greedy1(1)
+            got = pb.translate_batch(qm, [src], pb.DecodeConfig(1, ratio), return_ids=True)[0]
+            lib.qnmt_set_greedy1(0)
+            ref = pb.translate_batch(qm, [src], pb.DecodeConfig(1, ratio), return_ids=True)[0]
+            lib.qnmt_set_greedy1(old)
+            want = om.translate(src, 1, ratio)
+            assert got[0] == want[0] and got[1] == want[1], (seed, src)
+            assert got == ref
