@@ -324,6 +324,24 @@ static int encode_core(qnmt_engine* e, const int32_t* ids_dev, const int32_t* le
         TRY(gemm(c.wx, 3 * H, E, c.wx_s, H, e->q_emb_src, P, E, e->sc_pos, e->iota, c.bx,
                  e->gx_enc + d * 3 * H, 6 * H, 0, st));
     }
+    if (n == 1 && g_enc1 && H % 16 == 0 && 2 * H <= 4096 && !e->prof_on) {
+        // one sentence: the recurrence as one persistent kernel (persistent.cu)
+        PeArgs pa{};
+        pa.H = (int)H;
+        pa.l = len[0];
+        pa.gx = e->gx_enc;
+        for (int d = 0; d < 2; ++d) {
+            pa.uzr[d] = m->cell[d].uzr; pa.uzr_s[d] = m->cell[d].uzr_s;
+            pa.uc[d] = m->cell[d].uc; pa.uc_s[d] = m->cell[d].uc_s;
+        }
+        pa.gh = e->gh2; pa.ghc = e->ghc2;
+        pa.states = states + row[0] * 2 * H;
+        pa.h2 = e->h2;
+        pa.ctl = e->pk_ctl;
+        pa.err = e->err;
+        QNMT_CUDA(cudaMemsetAsync(e->pk_ctl, 0, 8 * sizeof(int32_t), st));
+        TRY(enc1_launch(pa, st));
+    } else {
     QNMT_CUDA(cudaMemsetAsync(e->h2, 0, sizeof(float) * (size_t)n * 2 * H, st));
     // per-step max-abs bits (column c = its own segment): the gates kernel of step t
     // produces rh2's, the combine kernel of step t the next step's h2's
@@ -354,6 +372,7 @@ static int encode_core(qnmt_engine* e, const int32_t* ids_dev, const int32_t* le
         TRY(gru_combine_launch(e->gx_enc, 3 * H, gxr, e->ghc2, H, e->z2, e->h2, H, N2, H, e->h2, H,
                                states, H, outr, e->err, st, qm_hn, nullptr));
     }
+    }   // per-step kernels
     // att_proj = enc_proj(states) with one scale per sentence over [2H, l] (layers.py:343)
     TRY(quantize_launch(states, P, 2 * H, 2 * H, e->pos_sent, n, e->q_states, 2 * H, e->sc_sent,
                         e->seg_bits, 1, e->err, st));

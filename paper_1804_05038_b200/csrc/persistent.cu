@@ -497,10 +497,99 @@ int greedy1_launch(const PkArgs& a, cudaStream_t st) {
     return QNMT_OK;
 }
 
+// ---------------------------------------------------------------------------
+// Batch-1 encoder recurrence: both directions advance together, one step per
+// iteration: S1 q(h_d) -> GEMV U_zr_d; barrier; S2 gates -> q(r * h_d) -> GEMV
+// U_c_d; barrier; S3 combine (every CTA keeps both h_d in shared memory, so the
+// next step needs no barrier).  Same arithmetic as encode_core's per-step
+// kernels (k_gru_gates / k_gru_combine, per-(sentence, direction) scales).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(PK_T, 1) k_enc1(PeArgs a) {
+    extern __shared__ __align__(16) unsigned char pe_smem[];
+    const int H = a.H;
+    float* h = reinterpret_cast<float*>(pe_smem);   // [2][H]
+    float* zb = h + 2 * H;                          // [2][H]
+    float* vals = zb + 2 * H;                       // [H]
+    int8_t* q = reinterpret_cast<int8_t*>(vals + H);   // [2][H]
+    __shared__ uint32_t red[PK_W];
+    const int warp = threadIdx.x >> 5;
+    const int gw = blockIdx.x * PK_W + warp, nw = gridDim.x * PK_W;
+    for (int j = threadIdx.x; j < 2 * H; j += PK_T) h[j] = 0.0f;   // layers.py:330
+    __syncthreads();
+    for (int t = 0; t < a.l; ++t) {
+        const int pos[2] = {t, a.l - 1 - t};
+        // S1: q(h_d) and U_zr_d q(h_d)
+        float sh[2];
+#pragma unroll
+        for (int d = 0; d < 2; ++d) sh[d] = quantize_vec(h + d * H, H, q + d * H, red, a.err);
+#pragma unroll
+        for (int d = 0; d < 2; ++d)
+            gemv(a.uzr[d], 2 * H, H, a.uzr_s[d], H, q + d * H, sh[d], nullptr, a.gh + d * 2 * H, 0, gw, nw);
+        gsync(a.ctl);
+        // S2: gates -> q(r * h_d) -> U_c_d
+        float srh[2];
+#pragma unroll
+        for (int d = 0; d < 2; ++d) {
+            const float* gx = a.gx + ((int64_t)pos[d] * 2 + d) * 3 * H;
+            bool bad = false;
+            for (int j = threadIdx.x; j < H; j += PK_T) {
+                const float pz = __fadd_rn(gx[j], ldcg(a.gh + d * 2 * H + j));
+                const float pr = __fadd_rn(gx[H + j], ldcg(a.gh + d * 2 * H + H + j));
+                bad |= !(is_finite_f(pz) && is_finite_f(pr));
+                zb[d * H + j] = sigmoid_b(pz);
+                vals[j] = __fmul_rn(sigmoid_b(pr), h[d * H + j]);
+            }
+            if (bad && blockIdx.x == 0) set_flag(a.err, QNMT_FLAG_NUMERIC);
+            __syncthreads();
+            srh[d] = quantize_vec(vals, H, q + d * H, red, a.err);
+        }
+#pragma unroll
+        for (int d = 0; d < 2; ++d)
+            gemv(a.uc[d], H, H, a.uc_s[d], H, q + d * H, srh[d], nullptr, a.ghc + d * H, 0, gw, nw);
+        gsync(a.ctl);
+        // S3: combine; the new states stay in this CTA's shared memory
+#pragma unroll
+        for (int d = 0; d < 2; ++d) {
+            const float* gx = a.gx + ((int64_t)pos[d] * 2 + d) * 3 * H + 2 * H;
+            for (int j = threadIdx.x; j < H; j += PK_T) {
+                const float pc = __fadd_rn(gx[j], ldcg(a.ghc + d * H + j));
+                if (!is_finite_f(pc) && blockIdx.x == 0) set_flag(a.err, QNMT_FLAG_NUMERIC);
+                const float z = zb[d * H + j];
+                const float v = __fadd_rn(__fmul_rn(__fsub_rn(1.0f, z), h[d * H + j]), __fmul_rn(z, tanh_b(pc)));
+                h[d * H + j] = v;
+                if (blockIdx.x == 0) a.states[(int64_t)pos[d] * 2 * H + (d == 0 ? H : 0) + j] = v;
+            }
+        }
+        __syncthreads();
+    }
+    if (blockIdx.x == 0)
+        for (int j = threadIdx.x; j < 2 * H; j += PK_T) a.h2[j] = h[j];
+}
+
+int g_enc1 = 1;
+
+int enc1_launch(const PeArgs& a, cudaStream_t st) {
+    const size_t smem = (size_t)a.H * (2 + 2 + 1) * sizeof(float) + 2 * (size_t)a.H;
+    if (smem > 48 * 1024) {
+        static size_t done = 0;
+        QNMT_CUDA(raise_smem_limit((const void*)k_enc1, smem, done));
+    }
+    int dev = 0, sms = 0;
+    QNMT_CUDA(cudaGetDevice(&dev));
+    QNMT_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    PeArgs args = a;
+    void* params[] = {&args};
+    QNMT_CUDA(cudaLaunchCooperativeKernel((const void*)k_enc1, dim3(sms), dim3(PK_T), params, smem, st));
+    count_launch();
+    QNMT_CUDA(cudaGetLastError());
+    return QNMT_OK;
+}
+
 }  // namespace qnmt
 
 extern "C" int qnmt_set_greedy1(int enable) {
     const int old = qnmt::g_greedy1;
     qnmt::g_greedy1 = enable;
+    qnmt::g_enc1 = enable;
     return old;
 }

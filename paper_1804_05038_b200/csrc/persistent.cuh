@@ -46,4 +46,20 @@ struct PkArgs {
 int greedy1_launch(const PkArgs& a, cudaStream_t st);
 extern int g_greedy1;
 
+// batch-1 bidirectional GRU recurrence (layers.py:331-340) as one persistent kernel
+struct PeArgs {
+    int H, l;
+    const float* gx;            // [l][2][3H]: W_x q(emb_i) + b_x per position and direction
+    const int8_t* uzr[2]; const float* uzr_s[2];   // per direction (0 fwd, 1 bwd): [2H][H], 2 block scales
+    const int8_t* uc[2]; const float* uc_s[2];
+    float* gh;       // [2][2H] scratch
+    float* ghc;      // [2][H] scratch
+    float* states;   // [l][2H] output, backward half first (layers.py:342)
+    float* h2;       // [2][H] final states (fwd, bwd)
+    int32_t* ctl;    // [3..4] grid barrier
+    int32_t* err;
+};
+int enc1_launch(const PeArgs& a, cudaStream_t st);
+extern int g_enc1;
+
 }  // namespace qnmt
