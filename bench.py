@@ -19,10 +19,11 @@ synthetic token ids (no datasets / checkpoints in this environment).
            qnmt_translate_batch per batch) with HOST buffers (H2D of ids, D2H of
            finished lists + history, host selection of the best hypothesis),
            wall clock per step.
-  roofline: per-kernel device time measured live in the timed steps by
-           %globaltimer stamps captured into the step graphs (a CUDA graph step
-           cannot be bracketed by host events); algorithmic bytes / int-ops per
-           launch from the live column count of each step.
+  roofline: per-kernel device time measured live by %globaltimer stamps
+           captured into the step graphs (a CUDA graph step cannot be bracketed
+           by host events) of an untimed single-stream pass over the same shard
+           right after the timed passes; algorithmic bytes / int-ops per launch
+           from the live column count of each step.
   --impl reference : the reference algorithm on the host CPU.  The reference is
            a Python package that cannot travel to the GPU box, so this arm runs
            the numpy port oracle/qnmt_oracle.py (pinned bit-exact against the
@@ -264,9 +265,9 @@ def main():
     lib = _lib.load()
     main_stream = torch.cuda.current_stream()
     flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device=dev)   # > 126 MB L2
-    stamps_on = not args.no_stamps
+    stamps_on = False   # timed passes run without device-clock stamps (see roofline_pass)
     for e in engines:
-        lib.qnmt_engine_stamps(e._h, 1 if stamps_on else 0)   # graphs are captured during warm-up
+        lib.qnmt_engine_stamps(e._h, 0)
     # device-resident inputs of every batch of the shard (the "value" pass reads ids from HBM)
     dev_ids = [torch.from_numpy(np.concatenate([sents[i] for i in b])).to(dev) for b in shard]
     lens = [np.array([len(sents[i]) for i in b], dtype=np.int32) for b in shard]
@@ -278,6 +279,24 @@ def main():
         lp = np.zeros(len(shard[b]), np.float64)
         _lib.call("qnmt_fetch_results", e._h, out.ctypes.data, stride, ol.ctypes.data, lp.ctypes.data, st.cuda_stream)
         return out, ol, lp
+
+    def roofline_pass():
+        """Untimed single-engine pass over the shard with %globaltimer stamps captured into
+        the step graphs: per-kernel device times of kernels running alone (the timed passes
+        overlap three streams, where a kernel's duration includes sharing SMs)."""
+        e, st = engines[0], streams[0]
+        buf = np.zeros((256, 11), dtype=np.int64)   # QNMT_STAMP_COLS
+        lib.qnmt_engine_stamps(e._h, 1)
+        rows = []
+        with torch.cuda.stream(st):
+            for b in range(len(shard)):
+                _lib.call("qnmt_decode_batch_device", e._h, dev_ids[b].data_ptr(), lens[b].ctypes.data,
+                          len(shard[b]), BEAM, MAX_RATIO, st.cuda_stream)
+                nr = lib.qnmt_engine_stamps_read(e._h, buf.ctypes.data, 256, st.cuda_stream)
+                rows += [buf[i].copy() for i in range(nr)]
+        lib.qnmt_engine_stamps(e._h, 0)
+        torch.cuda.synchronize()
+        return rows
 
     def device_pass(collect=None):
         """One pass over the shard: STREAMS engines on STREAMS streams, one host thread
@@ -351,6 +370,9 @@ def main():
     clocks = clk.stop()
     if world > 1:
         dist.barrier()
+    if not args.no_stamps:
+        roofline_pass()                 # captures the stamped step graphs
+        all_rows = roofline_pass()
 
     # e2e: the public bulk API (translate_batch: host ids in, host results out, length-sorted
     # batches pipelined over STREAMS engines), wall clock around the call with a device sync
@@ -421,9 +443,10 @@ def main():
                 "gpu_launches": launches,
                 "roofline": roof,
                 "kernels": kern,
-                "kernels_note": (f"per-launch device times from %globaltimer stamps inside the timed passes; with "
-                                 f"{STREAMS} engines on {STREAMS} streams a kernel may share SMs with the other "
-                                 "stream's kernels, so these are lower bounds on kernel efficiency"),
+                "kernels_note": ("per-launch device times from %globaltimer stamps captured into the step graphs of "
+                                 "an untimed single-stream pass over the same shard right after the timed passes "
+                                 f"(the timed passes overlap {STREAMS} streams, where a kernel's duration includes "
+                                 "sharing SMs with the other streams' kernels)"),
                 "cpu_baseline": cpu,
                 "clocks": clocks}
         print(json.dumps(line), flush=True)

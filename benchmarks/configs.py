@@ -6,6 +6,7 @@
         ~200 MB > 126 MB L2), GB/s over the algorithmic bytes and int-op/s.
   cfg2  Network.encode, l = 50 (latency).
   cfg3  translate, greedy, 50 steps, V = 32000 (latency, tokens/s).
+  cfg4  64 sentences, l ~ U[10, 80], beam 5 (sentences/s, tokens/s).
   host  per-step floor: one sentence, l = 100, beam 5 (151 steps).
 """
 
@@ -94,6 +95,19 @@ def main():
     t = timed(lambda: pb.translate(qm, toks, cfg))
     res.append({"config": "cfg3 greedy 50 steps (encoder + decoder)", "ms": t * 1e3,
                 "tokens_per_s": 50 / t, "ms_per_step": t * 1e3 / 51})
+    # cfg4: 64 sentences, l ~ U[10, 80], beam 5, max_ratio 1.5 (batched, tcgen05 path)
+    rng4 = np.random.default_rng(4)
+    c4 = [rng4.integers(3, 32000, int(rng4.integers(10, 81))).tolist() for _ in range(64)]
+    cfg4 = pb.DecodeConfig(beam=5, max_ratio=1.5)
+    for mb, ns in ((64, 1), (32, 2), (16, 3)):
+        toks = []
+
+        def run4():
+            toks[:] = pb.translate_batch(qm, c4, cfg4, max_batch=mb, return_ids=True, streams=ns)
+        t = timed(run4, 3)
+        ntok = sum(len(r[0]) for r in toks)
+        res.append({"config": f"cfg4 64 sentences beam 5 (batches of {mb}, {ns} streams)", "ms": t * 1e3,
+                    "sentences_per_s": 64 / t, "tokens_per_s": ntok / t})
     src100 = np.random.default_rng(7).integers(3, 32000, 100)
     t = timed(lambda: pb.translate(qm, [params.src_tokens[i] for i in src100], pb.DecodeConfig(5, 1.5)), 3)
     res.append({"config": "1 sentence l=100 beam 5 (151 steps)", "ms": t * 1e3, "ms_per_step": t * 1e3 / 151})
