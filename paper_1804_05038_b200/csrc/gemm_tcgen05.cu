@@ -18,6 +18,7 @@
 //               fl32(acc / (sw*sx)) (reciprocal fast path, __ddiv_rn near f32
 //               midpoints) -> +bias -> (+Y) -> coalesced f32 stores of Y[n][m].
 // Tiles are visited n-fastest so consecutive CTAs share the W block in L2.
+#include <cstdlib>
 #include <mutex>
 #include <unordered_map>
 
@@ -58,11 +59,30 @@ enum { EPI_BIAS = 1, EPI_ACCUMULATE = 2, EPI_RAW = 4, EPI_ADD2 = 8 };
 // -> exact dequant (+ bias / + Y / + addends) -> f32 stores.  Shared by the
 // 1-CTA kernel and the CTA-pair kernel (tempty_remote: shared::cluster address
 // of the leader CTA's tempty barriers, 0 = local).
+// Tile t -> (m-block, n-block).  group_m == 0: n fastest (consecutive CTAs share the
+// weight block).  group_m > 0: bands of group_m m-blocks with the m-block fastest, so
+// the tiles in flight at once touch ~group_m A blocks and ~(grid / group_m) B blocks
+// -- an L2-resident working set for large products instead of one B block per tile.
+__device__ __forceinline__ void tile_coords(int tile, int m_blocks, int n_blocks, int group_m, int& mb, int& nb) {
+    if (group_m <= 0) {
+        mb = tile / n_blocks;
+        nb = tile % n_blocks;
+        return;
+    }
+    const int band_tiles = group_m * n_blocks;
+    const int band = tile / band_tiles;
+    const int r = tile - band * band_tiles;
+    const int m_base = band * group_m;
+    const int gm = min(group_m, m_blocks - m_base);
+    mb = m_base + r % gm;
+    nb = r / gm;
+}
+
 template <int BN, int EPI>
 __device__ __forceinline__ void tc_epilogue(const TcEpi& e, uint32_t tmem_base, uint64_t* tfull, uint64_t* tempty,
                                             uint32_t tempty_remote, int tile0, int tstep, int tiles, int n_blocks,
                                             int m_tile, int m_off, int M, int N, float (*col_sx)[256],
-                                            double (*col_isx)[256]) {
+                                            double (*col_isx)[256], int m_blocks = 0, int group_m = 0) {
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     const int ew = warp - 2;                 // 0..7
@@ -71,7 +91,8 @@ __device__ __forceinline__ void tc_epilogue(const TcEpi& e, uint32_t tmem_base, 
         constexpr int COLS = BN / 2;
         int it = 0;
         for (int tile = tile0; tile < tiles; tile += tstep, ++it) {
-            const int mb = tile / n_blocks, nb = tile % n_blocks;
+            int mb, nb;
+            tile_coords(tile, m_blocks, n_blocks, group_m, mb, nb);
             const int buf = it & 1;
             const uint32_t use = (uint32_t)(it >> 1) & 1u;
             // Column scales of this tile -> smem (x scale and its f64 reciprocal), row scale and
@@ -221,6 +242,8 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
 // commits multicast to both CTAs' empty / tmem-full barriers; both CTAs'
 // epilogues release a TMEM buffer on the leader's tmem-empty barrier.
 // ---------------------------------------------------------------------------
+constexpr int TC2_GROUP_M = 16;  // tile rasterization band of the pair kernel (see tile_coords; swept 0..32)
+
 template <int BN>
 struct Tc2Ring {
     static constexpr int A_BYTES = TC_BM * TC_BK;
@@ -268,7 +291,7 @@ __device__ __forceinline__ void mma_commit_pair(uint64_t* bar) {   // arrive on 
 template <int BN, int EPI>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
 k_gemm_tc2(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N, int K,
-           TcEpi e) {
+           TcEpi e, int group_m) {
     using C = Tc2Ring<BN>;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* smem = (unsigned char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -314,7 +337,8 @@ k_gemm_tc2(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUte
             int stage = 0;
             uint32_t phase = 0;
             for (int tile = cid; tile < tiles; tile += ncl) {
-                const int mb = tile / n_blocks, nb = tile % n_blocks;
+                int mb, nb;
+                tile_coords(tile, m_blocks, n_blocks, group_m, mb, nb);
                 for (int kb = 0; kb < k_blocks; ++kb) {
                     tc::mbar_wait(&bars.empty[stage], phase ^ 1);
                     unsigned char* sa = smem + stage * C::STAGE_BYTES;
@@ -358,7 +382,8 @@ k_gemm_tc2(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUte
         }
     } else {
         tc_epilogue<BN, EPI>(e, tmem_base, bars.tfull, bars.tempty, rank ? smem_in_rank(bars.tempty, 0) : 0u, cid, ncl,
-                             tiles, n_blocks, 2 * TC_BM, (int)rank * TC_BM, M, N, col_sx, col_isx);
+                             tiles, n_blocks, 2 * TC_BM, (int)rank * TC_BM, M, N, col_sx, col_isx, m_blocks,
+                             group_m);
     }
     tc::tc_fence_before();
     cluster_sync_all();   // both CTAs finished: no MMA writes or remote arrivals pending
@@ -480,7 +505,11 @@ static int launch_tc2(const GemmArgs& g, cudaStream_t st) {
     const int tiles = (int)(cdiv(g.M, 2 * TC_BM) * cdiv(g.N, BN));
     const int pairs = tc_sm_count() / 2;
     const int grid = 2 * (tiles < pairs ? tiles : pairs);
-    QNMT_LAUNCH(k_gemm_tc2<BN, EPI>, grid, TC_THREADS, C::SMEM, st, ta, tb, (int)g.M, (int)g.N, (int)g.K, e);
+    static const int group_m = [] {
+        const char* v = getenv("QNMT_TC2_GROUP_M");   // (tuning knob; default TC2_GROUP_M)
+        return v ? atoi(v) : TC2_GROUP_M;
+    }();
+    QNMT_LAUNCH(k_gemm_tc2<BN, EPI>, grid, TC_THREADS, C::SMEM, st, ta, tb, (int)g.M, (int)g.N, (int)g.K, e, group_m);
     QNMT_CHECK_LAUNCH("k_gemm_tc2");
     return QNMT_OK;
 }
