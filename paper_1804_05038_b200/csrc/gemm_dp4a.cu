@@ -60,15 +60,14 @@ __device__ __forceinline__ int dp4a16(int acc, const int4& a, const int4& b) {
 // ---------------------------------------------------------------------------
 // GEMV-class kernel: N <= 8
 // ---------------------------------------------------------------------------
-template <int ROWS, int NC>
+template <int ROWS, int NC, int U = 2>
 __global__ void __launch_bounds__(256)
 k_gemv(const int8_t* __restrict__ W, int64_t M, int64_t K, int64_t ldw,
        const int8_t* __restrict__ X, int64_t ldx, EpiArgs e, int w_static, const int32_t* n_dev) {
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
     const int64_t row0 = ((int64_t)blockIdx.x * 8 + warp) * ROWS;
-    const int64_t nch = K >> 4;   // 16-byte chunks per row
-    constexpr int U = 2;          // chunk-iterations whose loads are issued together
+    const int64_t nch = K >> 4;   // 16-byte chunks per row (U chunk-iterations' loads issued together)
     int4 w[U][ROWS];
     auto load_w = [&](int64_t c0) {
 #pragma unroll
@@ -214,7 +213,10 @@ static int launch_gemv(const int8_t* W, int64_t M, int64_t K, int64_t ldw, const
                        int64_t ldx, const EpiArgs& e, cudaStream_t st) {
     unsigned grid = (unsigned)cdiv(M, 8 * ROWS);
     const int w_static = (e.flags & QNMT_GEMM_W_STATIC) ? 1 : 0;
-    QNMT_LAUNCH(k_gemv<ROWS, NC>, grid, 256, 0, st, W, M, K, ldw, X, ldx, e, w_static, tl_ndev);
+    if (K >= 2048 && NC <= 2)   // long rows: four 16-byte chunks per lane and row in flight
+        QNMT_LAUNCH((k_gemv<ROWS, NC, 4>), grid, 256, 0, st, W, M, K, ldw, X, ldx, e, w_static, tl_ndev);
+    else
+        QNMT_LAUNCH((k_gemv<ROWS, NC, 2>), grid, 256, 0, st, W, M, K, ldw, X, ldx, e, w_static, tl_ndev);
     return QNMT_OK;
 }
 
