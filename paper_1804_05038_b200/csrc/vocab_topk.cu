@@ -147,20 +147,23 @@ k_vocab_stats(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ C
                 if (__all_sync(0xffffffffu, fast_row) && ncols == 16) {
                     // exact dequant fl32(acc * rs): safe unless q's bits below f32 precision lie
                     // within 64 f64-ulps of the rounding midpoint (0x10000000)
+                    // (int32 -> f64 through the exponent field on the fp64 pipe instead of the XU
+                    // conversion: 2^52 + (acc + 2^31) - (2^52 + 2^31), exact; |d| <= 64 test as one
+                    // wrapped unsigned range check)
                     uint32_t dmin = 0xffffffffu;
 #pragma unroll
                     for (int j = 0; j < 16; ++j) {
-                        const double q = (double)(int)r[j] * rs0;
+                        const double av = __hiloint2double(0x43300000, (int)(r[j] ^ 0x80000000u)) - 4503601774854144.0;
+                        const double q = av * rs0;
                         x[j] = __double2float_rn(q);
-                        const int d = (int)((uint32_t)__double2loint(q) & 0x1fffffffu) - 0x10000000;
-                        dmin = min(dmin, (uint32_t)abs(d));
+                        dmin = min(dmin, ((uint32_t)__double2loint(q) + (64u - 0x10000000u)) & 0x1fffffffu);
                     }
-                    if (__any_sync(0xffffffffu, dmin <= 64u)) {   // rare: exact division where needed
+                    if (__any_sync(0xffffffffu, dmin <= 128u)) {   // rare: exact division where needed
 #pragma unroll
                         for (int j = 0; j < 16; ++j) {
                             const double q = (double)(int)r[j] * rs0;
-                            const int d = (int)((uint32_t)__double2loint(q) & 0x1fffffffu) - 0x10000000;
-                            if (abs(d) <= 64) x[j] = dequant((int)r[j], sw0, sx);   // (fast path: one scale)
+                            if ((((uint32_t)__double2loint(q) + (64u - 0x10000000u)) & 0x1fffffffu) <= 128u)
+                                x[j] = dequant((int)r[j], sw0, sx);   // (fast path: one scale)
                         }
                     }
                     const float4* b4 = reinterpret_cast<const float4*>(&col_b[buf][c0]);
