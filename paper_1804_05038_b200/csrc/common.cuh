@@ -152,6 +152,12 @@ __device__ __forceinline__ float dequant_rcp(long long acc, double rcp, float sa
 
 // Predicate of dequant_rcp's fast path for q = acc * rcp: zero, or a normal-range
 // value whose bits are more than 64 f64-ulps away from an f32 rounding midpoint.
+// (double)v for an int32 v through the exponent field (fp64 pipe, exact):
+// 2^52 + (v + 2^31) - (2^52 + 2^31) -- the XU conversion is the scarcer pipe in epilogues.
+__device__ __forceinline__ double i2d_exact(int v) {
+    return __hiloint2double(0x43300000, (int)((unsigned)v ^ 0x80000000u)) - 4503601774854144.0;
+}
+
 __device__ __forceinline__ bool dequant_rcp_safe(double q) {
     unsigned long long b = (unsigned long long)__double_as_longlong(q);
     int low = (int)(b & 0x1fffffffull);

@@ -154,7 +154,7 @@ __device__ __forceinline__ void tc_epilogue(const TcEpi& e, uint32_t tmem_base, 
                 float yd[16];
 #pragma unroll
                 for (int j = 0; j < 16; ++j) {
-                    const double q = (double)(int)r[j] * (isw * col_isx[buf][c0 + j]);
+                    const double q = i2d_exact((int)r[j]) * (isw * col_isx[buf][c0 + j]);
                     yd[j] = __double2float_rn(q);
                     unsafe |= (uint32_t)(!dequant_rcp_safe(q)) << j;
                 }
