@@ -113,10 +113,13 @@ int att_minmax_launch(const float* att_proj, const int64_t* sent_row, const int3
 __global__ void __launch_bounds__(AT)
 k_att_scale(const float* __restrict__ u, int64_t ldu, const int32_t* __restrict__ sent_col_off,
             const int32_t* __restrict__ sent_ncols, const float* __restrict__ mm, int64_t A,
-            float2* __restrict__ st_thr, int32_t* err_flag) {
+            float2* __restrict__ st_thr, int32_t* err_flag, uint32_t* zero_seg) {
     pdl_entry();
     __shared__ uint32_t mred[AT / 32];
     const int s = blockIdx.x, j = blockIdx.y;
+    // the context kernel of this step max-reduces |ctx| per sentence into zero_seg[s]
+    // (replaces a memset node, which would break the programmatic-dependent-launch chain)
+    if (zero_seg && j == 0 && threadIdx.x == 0) zero_seg[s] = 0u;
     if (j >= sent_ncols[s]) return;
     const int c = sent_col_off[s] + j;
     const float* un = u + (int64_t)c * ldu;
@@ -728,7 +731,7 @@ int attention_launch(const float* u, int64_t ldu, int64_t N, const int32_t* sent
         att_minmax = mm;
     }
     QNMT_LAUNCH(k_att_scale, dim3((unsigned)n_sent, AMAXP), AT, 0, st, u, ldu, sent_col_off, sent_ncols, att_minmax, A,
-                                                              st_thr, err_flag);
+                                                              st_thr, err_flag, ctx_segmax);
     QNMT_CHECK_LAUNCH("k_att_scale");
     const bool quads = A % 4 == 0 && ldu % 4 == 0 && A <= 4 * AT * AQ5 && ((uintptr_t)u % 16) == 0 &&
                        ((uintptr_t)att_proj % 16) == 0 && ((uintptr_t)v_codes % 4) == 0;

@@ -652,7 +652,7 @@ static int step_core(qnmt_engine* e, const StepIO& io, cudaStream_t st) {
     }
     prof_mark(e, PG_ATT, st);
     TRY(stamp(e, ST_ATT0, io, st));
-    if (fq) QNMT_CUDA(cudaMemsetAsync(e->ctx_max, 0, sizeof(uint32_t) * (size_t)ns, st));
+    // (ctx_max is zeroed by the attention scale kernel)
     TRY(attention_launch(u, ldu, N, io.sent_col_off, io.sent_ncols, io.nseg, io.att_proj, io.att_minmax, io.states,
                          io.sent_row, io.sent_len, io.max_len, A, 2 * H, m->v, m->v_s, e->ctx, 2 * H,
                          io.alpha, io.lda, e->att_scratch, e->err, st, fq ? e->ctx_max : nullptr, io.max_cols));

@@ -547,6 +547,10 @@ int gemm_tc_launch(const GemmArgs& g, cudaStream_t st) {
         // fewest waves of tiles over the SMs, then the narrowest tile (less B data and epilogue
         // per tile, more CTAs): e.g. N = 1280 -> M 2048: 160 (128 tiles), M 3072: 256, M 1024: 96
         static const int cand[] = {64, 96, 128, 160, 192, 224, 256};
+        static const int forced = [] {   // (tuning knob: QNMT_TC_BN forces one tile width)
+            const char* v = getenv("QNMT_TC_BN");
+            return v ? atoi(v) : 0;
+        }();
         bn = 256;
         int64_t best = INT64_MAX;
         for (int b : cand) {
@@ -556,6 +560,7 @@ int gemm_tc_launch(const GemmArgs& g, cudaStream_t st) {
                 bn = b;
             }
         }
+        if (forced) bn = forced;
     }
 #define QNMT_TC_CASE(BN_, E_) \
     if (bn == BN_ && epi == E_) return launch_tc<BN_, E_>(g, st);
