@@ -4,6 +4,7 @@ reference goldens (Tier B): identical token ids and identical f64 log-probs."""
 import math
 
 import numpy as np
+import torch
 import pytest
 
 from oracle import qnmt_oracle as O
@@ -285,14 +286,15 @@ def test_gpu_persistent_greedy_matches_oracle_and_step_graphs():
     import paper_1804_05038_b200 as pb
     from paper_1804_05038_b200 import _lib
     lib = _lib.load()
-    for seed, ws, bs, eb in ((61, 0.3, 0.1, 0.6), (62, 0.05, 0.0, 0.0), (63, 0.5, 0.1, 1.0)):
+    for seed, ws, bs, eb, s0m in ((61, 0.3, 0.1, 0.6, "transform"), (62, 0.05, 0.0, 0.0, "transform"),
+                                  (63, 0.5, 0.1, 1.0, "transform"), (64, 0.3, 0.1, 0.6, "zero")):
         d = pb.Dims(300, 251, 32, 48, 64, 32)
-        params = pb.synthetic_model(d, seed, ws, bs, eb)
+        params = pb.synthetic_model(d, seed, ws, bs, eb, s0_mode=s0m)
         qm = pb.quantize_model(params)
-        om = O.QModel(O.Dims(**d.as_dict()), params.tensors)
+        om = O.QModel(O.Dims(**d.as_dict()), params.tensors, s0_mode=s0m)
         rng = np.random.default_rng(seed)
-        for _ in range(6):
-            src = rng.integers(3, 300, int(rng.integers(1, 30))).tolist()
+        for k in range(6):
+            src = rng.integers(3, 300, 1 if k == 0 else int(rng.integers(1, 30))).tolist()
             ratio = float(rng.choice([0.5, 1.5, 3.0]))
             old = lib.qnmt_set_greedy1(1)
             got = pb.translate_batch(qm, [src], pb.DecodeConfig(1, ratio), return_ids=True)[0]
@@ -302,3 +304,27 @@ def test_gpu_persistent_greedy_matches_oracle_and_step_graphs():
             want = om.translate(src, 1, ratio)
             assert got[0] == want[0] and got[1] == want[1], (seed, src)
             assert got == ref
+
+
+
+@pytest.mark.gpu
+def test_gpu_persistent_encoder_matches_batched_encoder():
+    """One-sentence encodes (persistent recurrence kernel) == the batched encoder's states,
+    att_proj and s0 for the same sentence inside a multi-sentence batch, and == the oracle."""
+    import paper_1804_05038_b200 as pb
+    d = pb.Dims(300, 251, 32, 48, 64, 32)
+    params = pb.synthetic_model(d, 71, 0.3, 0.1, 0.6)
+    qm = pb.quantize_model(params)
+    om = O.QModel(O.Dims(**d.as_dict()), params.tensors)
+    eng = pb.Engine(qm, 8, 64, 4)
+    rng = np.random.default_rng(71)
+    sents = [rng.integers(3, 300, n).tolist() for n in (1, 2, 7, 33, 64)]
+    st_b, att_b, s0_b, rows, lens = eng.encode_batch(sents)
+    for k, src in enumerate(sents):
+        st1, att1, s01, _, _ = eng.encode_batch([src])
+        r0, l = int(rows[k]), len(src)
+        assert torch.equal(st1, st_b[r0:r0 + l]) and torch.equal(att1, att_b[r0:r0 + l])
+        assert torch.equal(s01[0], s0_b[k])
+        ost, oatt, os0 = om.encode(src)
+        assert np.array_equal(st1.t().cpu().numpy(), ost) and np.array_equal(att1.t().cpu().numpy(), oatt)
+        assert np.array_equal(s01.t().cpu().numpy(), os0)
