@@ -226,15 +226,17 @@ def test_vocab_fused_ties(dup):
         assert fused[0][i] == toks and fused[1][i] == lp, i
 
 
-@pytest.mark.parametrize("V,k,dup", [(50000, 5, 0), (50000, 5, 97), (3001, 8, 7), (700, 16, 0), (300, 12, 2),
-                                     (20, 5, 0)])
-def test_vocab_candidates_abi(V, k, dup):
+@pytest.mark.parametrize("V,k,dup,N", [(50000, 5, 0, 37), (50000, 5, 97, 37), (3001, 8, 7, 37), (700, 16, 0, 37),
+                                       (300, 12, 2, 37), (20, 5, 0, 37), (50000, 5, 0, 300), (50000, 3, 5000, 300),
+                                       (50000, 6, 11, 1280), (5000, 1, 2, 700), (1, 1, 0, 9)])
+def test_vocab_candidates_abi(V, k, dup, N):
     """qnmt_vocab_candidates (fused) == qnmt_gemm_i8 + qnmt_topk_candidates on
-    the same codes, including vocabularies with repeated rows (exact ties)."""
+    the same codes, including vocabularies with repeated rows (exact ties), over
+    1..10 row blocks of the fused kernel."""
     import torch
     from paper_1804_05038_b200 import _lib, _dev
-    rng = np.random.default_rng(V + 31 * k + dup)
-    N, K = 37, 64
+    rng = np.random.default_rng(V + 31 * k + dup + N)
+    K = 64
     w = rng.integers(-127, 128, (V, K)).astype(np.int8)
     if dup:
         w = w[np.arange(V) % dup]
