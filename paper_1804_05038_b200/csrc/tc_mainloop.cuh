@@ -7,7 +7,8 @@
 // warp 0 lane 0: TMA producer into a STAGES-deep ring (SWIZZLE_128B, K-major);
 // warp 1 lane 0: tcgen05.mma.cta_group::1.kind::i8 issuer, int32 accumulators in
 //   TMEM, double-buffered (buffer b at column b*BN) so the epilogue of tile t
-//   overlaps the MMAs of tile t+1.  Tiles t = blockIdx.x, +gridDim.x, ...;
+//   overlaps the MMAs of tile t+1.  Tiles t = blockIdx.x, +gridDim.x, ... (or a given
+//   [t0, tiles) range with stride tstep);
 //   t -> (a-block t / n_blocks, b-block t % n_blocks).
 #pragma once
 #include "tc_common.cuh"
@@ -71,11 +72,16 @@ __device__ __forceinline__ uint32_t tc_setup(const CUtensorMap* tmA, const CUten
 
 template <class R, int BN>
 __device__ __forceinline__ void tc_produce(const CUtensorMap* tmA, const CUtensorMap* tmB, unsigned char* smem,
-                                           const TcBars<R>& b, int tiles, int n_blocks, int k_blocks) {
+                                           const TcBars<R>& b, int tiles, int n_blocks, int k_blocks,
+                                           int t0 = -1, int tstep = 0) {
     if ((threadIdx.x & 31) != 0) return;
     int stage = 0;
     uint32_t phase = 0;
-    for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+    if (t0 < 0) {   // default: persistent round-robin
+        t0 = blockIdx.x;
+        tstep = gridDim.x;
+    }
+    for (int tile = t0; tile < tiles; tile += tstep) {
         const int ab = tile / n_blocks, bb = tile % n_blocks;
         for (int kb = 0; kb < k_blocks; ++kb) {
             tc::mbar_wait(&b.empty[stage], phase ^ 1);
@@ -91,13 +97,17 @@ __device__ __forceinline__ void tc_produce(const CUtensorMap* tmA, const CUtenso
 
 template <class R, int BN>
 __device__ __forceinline__ void tc_issue(unsigned char* smem, const TcBars<R>& b, uint32_t tmem_base, int tiles,
-                                         int k_blocks) {
+                                         int k_blocks, int t0 = -1, int tstep = 0) {
     constexpr uint32_t IDESC = tc::idesc_i8(TC_BM, BN);
     const int lane = threadIdx.x & 31;
     int stage = 0;
     uint32_t phase = 0;
     int it = 0;
-    for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++it) {
+    if (t0 < 0) {
+        t0 = blockIdx.x;
+        tstep = gridDim.x;
+    }
+    for (int tile = t0; tile < tiles; tile += tstep, ++it) {
         const int buf = it & 1;
         const uint32_t use = (uint32_t)(it >> 1) & 1u;
         tc::mbar_wait(&b.tempty[buf], use ^ 1);

@@ -77,12 +77,16 @@ k_vocab_stats(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ C
     const int m_blocks = (M + TC_BM - 1) / TC_BM;
     const int n_blocks = (V + VT_BN - 1) / VT_BN;
     const int tiles = m_blocks * n_blocks;
+    // contiguous tile range per CTA (row block changes at most a few times per CTA, and the
+    // next tile's bias is known one tile ahead); equal shares +-1 tile
+    const int t_begin = (int)((int64_t)blockIdx.x * tiles / gridDim.x);
+    const int t_end = (int)((int64_t)(blockIdx.x + 1) * tiles / gridDim.x);
     const int k_blocks = (K + TC_BK - 1) / TC_BK;
 
     if (warp == 0) {
-        tc_produce<C, VT_BN>(&tmX, &tmW, smem, bars, tiles, n_blocks, k_blocks);
+        tc_produce<C, VT_BN>(&tmX, &tmW, smem, bars, t_end, n_blocks, k_blocks, t_begin, 1);
     } else if (warp == 1) {
-        tc_issue<C, VT_BN>(smem, bars, tmem_base, tiles, k_blocks);
+        tc_issue<C, VT_BN>(smem, bars, tmem_base, t_end, k_blocks, t_begin, 1);
     } else {
         const int ew = warp - 2;
         const int lg = warp & 3;     // TMEM lane group
@@ -94,19 +98,27 @@ k_vocab_stats(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ C
         bool bad = false;
         int it = 0;
         // the row's activation scale and multipliers depend only on the m-block: computed when it
-        // changes (consecutive tiles of the persistent schedule mostly share it), not per tile
+        // changes (at most a few times in a CTA's contiguous tile range), not per tile
         int cur_mb = -1;
         float sx = 1.0f;
         double isx = 1.0, rs0 = isw0;
-        for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++it) {
-            const int mb = tile / n_blocks, nb = tile % n_blocks;
+        int mb = t_begin / n_blocks, nb = t_begin % n_blocks;
+        float b_pre = 0.0f;   // this tile's bias (loaded during the previous tile)
+        if (ew * 32 < VT_BN && t_begin < t_end && e.bias) {
+            const int v = nb * VT_BN + ew * 32 + lane;
+            if (v < V) b_pre = e.bias[v];
+        }
+        for (int tile = t_begin; tile < t_end; ++tile, ++it) {
             const int buf = it & 1;
             const uint32_t use = (uint32_t)(it >> 1) & 1u;
             if (ew * 32 < VT_BN) {   // per-token bias (and per-token weight scale) of this tile -> smem
                 const int c = ew * 32 + lane;
                 const int v = nb * VT_BN + c;
-                float b = 0.0f;
-                if (v < V && e.bias) b = e.bias[v];
+                const float b = b_pre;
+                {   // prefetch the next tile's
+                    const int vn = (nb + 1 == n_blocks ? 0 : nb + 1) * VT_BN + c;
+                    b_pre = (tile + 1 < t_end && e.bias && vn < V) ? e.bias[vn] : 0.0f;
+                }
                 if (!one_scale) {
                     const float sw = v < V ? e.w_scales[v / e.w_rows_per_scale] : 1.0f;
                     col_sw[buf][c] = sw;
@@ -248,6 +260,10 @@ k_vocab_stats(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ C
                 p.i1 = i1;
                 p.pad = 0;
                 e.part[(int64_t)row * np + nb * VT_SPLIT + half] = p;
+            }
+            if (++nb == n_blocks) {
+                nb = 0;
+                ++mb;
             }
         }
         if (bad) set_flag(e.err_flag, QNMT_FLAG_NUMERIC);
