@@ -236,6 +236,9 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-stamps", action="store_true", help="no device-clock stamps (no roofline)")
     ap.add_argument("--no-profile", action="store_true", help="(kept for compatibility)")
+    ap.add_argument("--emulate-shard", default=None, metavar="R/W",
+                    help="development: run rank R's shard of a W-way split on this one GPU (no process "
+                         "group; the line reports that rank alone)")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
@@ -259,7 +262,11 @@ def main():
     params = pb.synthetic_model(pb.Dims(**DIMS), MODEL_SEED)
     qm = pb.quantize_model(params)
     sents = corpus()
-    shard = shard_batches(sents, rank, world)          # this rank's length-sorted batches (corpus indices)
+    if args.emulate_shard and world == 1:
+        er, ew = (int(x) for x in args.emulate_shard.split("/"))
+        shard = shard_batches(sents, er, ew)
+    else:
+        shard = shard_batches(sents, rank, world)      # this rank's length-sorted batches (corpus indices)
     engines = [pb.Engine(qm, PER_GPU, 100, BEAM) for _ in range(STREAMS)]
     streams = [torch.cuda.Stream(device=dev) for _ in range(STREAMS)]
     lib = _lib.load()
@@ -302,7 +309,7 @@ def main():
         """One pass over the shard: STREAMS engines on STREAMS streams, one host thread
         each, taking batches from a queue.  Device time = CUDA events on the main stream
         around a fork (side streams wait on ev0) / join (main waits on every side)."""
-        queue = list(range(len(shard)))
+        queue = sorted(range(len(shard)), key=lambda b: (-int(lens[b].max()), b))   # longest first
         lock = threading.Lock()
         toks, rows, errs = [0], [], []
         stamp_buf = [np.zeros((256, 11), dtype=np.int64) for _ in range(STREAMS)]   # QNMT_STAMP_COLS
@@ -437,6 +444,7 @@ def main():
                            "l2": "flushed (512 MB write) before every timed step",
                            "decode_loop": "CUDA-graph steps, device-side live count"},
                 "sentences_per_s": CORPUS * args.steps / secs,
+                **({"emulated_shard": args.emulate_shard} if args.emulate_shard and world == 1 else {}),
                 "step_ms": step_ms,
                 "e2e": {"value": e2e_value, "unit": "tokens/s", "h2d_bytes_per_step": h2d // args.steps,
                         "d2h_bytes_per_step": d2h // args.steps},

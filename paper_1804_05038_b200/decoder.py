@@ -145,7 +145,8 @@ def _decode_ids(members, per_member_ids, cfg: DecodeConfig, max_batch: int, stre
     queue -- one engine's host-side turnaround (polls, result fetch, graph
     launches) and its small latency-bound kernels overlap the other engines'
     device work.  Every sentence is still decoded exactly as decoder.translate
-    would (results do not depend on batching)."""
+    would (results do not depend on batching).  The queue hands out the longest
+    batches first."""
     n_all = len(per_member_ids[0])
     order = sorted(range(n_all), key=lambda i: (len(per_member_ids[0][i]), i)) if sort else list(range(n_all))
     batches = [order[b0:b0 + max_batch] for b0 in range(0, n_all, max_batch)]
@@ -173,7 +174,9 @@ def _decode_ids(members, per_member_ids, cfg: DecodeConfig, max_batch: int, stre
     import threading
 
     import torch
-    queue = list(range(len(batches)))
+    # longest batches first (LPT): the engines drain the short ones together at the end
+    # instead of one engine finishing the longest batch alone
+    queue = sorted(range(len(batches)), key=lambda b: (-max(len(ids0[i]) for i in batches[b]), b))
     lock = threading.Lock()
     errors = []
     main = torch.cuda.current_stream()
