@@ -65,6 +65,9 @@ k_vocab_stats(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ C
     __shared__ float col_b[2][VT_BN];
     __shared__ double tab[16];
     __shared__ double tab64[64];
+    // per epilogue thread: the 16 logits of the chunk holding its group's running max
+    // ([slot][thread]: consecutive lanes hit consecutive 16-byte words)
+    __shared__ float4 xbest[4][VT_EPI_WARPS * 32];
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -141,10 +144,12 @@ k_vocab_stats(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ C
             // fast-path preconditions, per thread and tile: one weight scale, and every
             // nonzero |q| = |acc| * rs in [2^-124, 2^127) (f32 normal range for |acc| < 2^31)
             const bool fast_row = one_scale && rs0 >= 0x1p-124 && rs0 * 2147483648.0 < 0x1p127;
-            // top-1 (value, smallest token) and runner-up value, as 4 interleaved chains
-            // (token j of a chunk goes to chain j & 3) to keep the dependency chains short
-            float cm4[4] = {-FLT_MAX, -FLT_MAX, -FLT_MAX, -FLT_MAX}, ca4[4] = {-FLT_MAX, -FLT_MAX, -FLT_MAX, -FLT_MAX};
-            int ci4[4] = {0x7fffffff, 0x7fffffff, 0x7fffffff, 0x7fffffff};
+            // top-1 (value, smallest token) and runner-up value from chunk maxima: the chunk that
+            // raised the running max is parked in shared memory; after the group, its token and
+            // the runner-up (its own second value vs the other chunks' maxima) are resolved
+            const int et = ew * 32 + lane;
+            float om = -FLT_MAX;   // max of the chunk maxima other than the best chunk's
+            int bc0 = -1;          // first token of the best chunk (-1: none)
             float m = -FLT_MAX;   // running max of the half-tile (the exp reference)
             double s = 0.0;
 #pragma unroll 1
@@ -168,9 +173,10 @@ k_vocab_stats(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ C
                         const double av = __hiloint2double(0x43300000, (int)(r[j] ^ 0x80000000u)) - 4503601774854144.0;
                         const double q = av * rs0;
                         x[j] = __double2float_rn(q);
-                        dmin = min(dmin, ((uint32_t)__double2loint(q) + (64u - 0x10000000u)) & 0x1fffffffu);
+                        // (low 29 bits of q + 64 - 2^28, times 8 so the wrap is the u32 one: one IMAD)
+                        dmin = min(dmin, (uint32_t)__double2loint(q) * 8u + (64u - 0x10000000u) * 8u);
                     }
-                    if (__any_sync(0xffffffffu, dmin <= 128u)) {   // rare: exact division where needed
+                    if (__any_sync(0xffffffffu, dmin <= 1024u)) {   // rare: exact division where needed
 #pragma unroll
                         for (int j = 0; j < 16; ++j) {
                             const double q = (double)(int)r[j] * rs0;
@@ -202,17 +208,28 @@ k_vocab_stats(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ C
                     }
                 }
                 float cm, cn;
-                {   // chunk max / min as shallow trees (invalid tail tokens are -FLT_MAX: skipped for min)
+                {   // chunk max / min as shallow trees (invalid tail tokens are -FLT_MAX: a tail chunk's
+                    // min is then -FLT_MAX, harmless: tail chunks take the range-guarded exp anyway)
                     float t[8], u[8];
 #pragma unroll
                     for (int j = 0; j < 8; ++j) {
                         t[j] = fmaxf(x[2 * j], x[2 * j + 1]);
-                        u[j] = fminf(2 * j < ncols ? x[2 * j] : FLT_MAX, 2 * j + 1 < ncols ? x[2 * j + 1] : FLT_MAX);
+                        u[j] = fminf(x[2 * j], x[2 * j + 1]);
                     }
                     cm = fmaxf(fmaxf(fmaxf(t[0], t[1]), fmaxf(t[2], t[3])), fmaxf(fmaxf(t[4], t[5]), fmaxf(t[6], t[7])));
                     cn = fminf(fminf(fminf(u[0], u[1]), fminf(u[2], u[3])), fminf(fminf(u[4], u[5]), fminf(u[6], u[7])));
                 }
                 bad |= !(is_finite_f(cm) && is_finite_f(cn));   // +-inf (NaN only from non-finite bias)
+                {   // strict '>': on equal maxima the earlier chunk (smaller tokens) stays best
+                    const bool nbst = cm > m;
+                    om = fmaxf(om, nbst ? m : cm);
+                    if (nbst) {
+                        bc0 = vbase;
+#pragma unroll
+                        for (int q4 = 0; q4 < 4; ++q4)
+                            xbest[q4][et] = make_float4(x[4 * q4], x[4 * q4 + 1], x[4 * q4 + 2], x[4 * q4 + 3]);
+                    }
+                }
                 if (cm > m) {   // rescale the running sum (first chunk, then rare)
                     s = (m == -FLT_MAX) ? 0.0 : s * exp_neg((double)m - (double)cm, tab);
                     m = cm;
@@ -228,26 +245,27 @@ k_vocab_stats(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ C
                         if (j < ncols) e4[j & 3] += exp_neg((double)x[j] - dm, tab);
                 }
                 s += (e4[0] + e4[1]) + (e4[2] + e4[3]);
-#pragma unroll
-                for (int j = 0; j < 16; ++j) {   // strict '>': the first (smallest) token wins ties
-                    const int k = j & 3;
-                    const bool g = x[j] > cm4[k];
-                    ca4[k] = fmaxf(ca4[k], fminf(cm4[k], x[j]));
-                    cm4[k] = fmaxf(cm4[k], x[j]);
-                    ci4[k] = g ? vbase + j : ci4[k];
-                }
             }
-            // merge the 4 chains: larger value, then smaller token; runner-up = max(min of maxima, runner-ups)
-            float a2 = -FLT_MAX;
-            int i1 = ci4[0];
-            float mm = cm4[0];
-            a2 = ca4[0];
+            float a2 = om;
+            int i1 = 0x7fffffff;
+            if (bc0 >= 0) {   // first token of the best chunk equal to m; the chunk's second value
+                float xb[16];
 #pragma unroll
-            for (int k = 1; k < 4; ++k) {
-                a2 = fmaxf(fmaxf(a2, ca4[k]), fminf(mm, cm4[k]));
-                const bool g = cm4[k] > mm || (cm4[k] == mm && ci4[k] < i1);
-                i1 = g ? ci4[k] : i1;
-                mm = fmaxf(mm, cm4[k]);
+                for (int q4 = 0; q4 < 4; ++q4) {
+                    const float4 v4 = xbest[q4][et];
+                    xb[4 * q4] = v4.x;
+                    xb[4 * q4 + 1] = v4.y;
+                    xb[4 * q4 + 2] = v4.z;
+                    xb[4 * q4 + 3] = v4.w;
+                }
+                int idx = 15;
+#pragma unroll
+                for (int j = 14; j >= 0; --j) idx = xb[j] == m ? j : idx;
+                float sm = -FLT_MAX;
+#pragma unroll
+                for (int j = 0; j < 16; ++j) sm = fmaxf(sm, j == idx ? -FLT_MAX : xb[j]);
+                a2 = fmaxf(a2, sm);
+                i1 = bc0 + idx;
             }
             tc::tc_fence_before();
             __syncwarp();
