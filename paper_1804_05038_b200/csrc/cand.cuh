@@ -130,7 +130,11 @@ __device__ __forceinline__ double exp_neg64(double t, const double* __restrict__
     p = fma(p, r, 1.0);
     p = fma(p, r, 1.0);
     const double v = p * tab64[k & 63];
-    return __hiloint2double(__double2hiint(v) + ((k >> 6) << 20), __double2loint(v));   // * 2^(k >> 6)
+    // * 2^(k >> 6): shift then shift-add (SHF + LEA) rather than the compiler's
+    // shift / mask / add form of (k >> 6) << 20
+    int kk;
+    asm("shr.s32 %0, %1, 6;" : "=r"(kk) : "r"(k));
+    return __hiloint2double(__double2hiint(v) + kk * (1 << 20), __double2loint(v));
 }
 
 template <int KM>
