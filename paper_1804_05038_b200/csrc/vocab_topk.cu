@@ -63,6 +63,7 @@ k_vocab_stats(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ C
     __shared__ double col_isw[2][VT_BN];   // 1 / s_w per token (double-buffered by tile)
     __shared__ float col_sw[2][VT_BN];
     __shared__ float col_b[2][VT_BN];
+    __shared__ float col_bmax[2][VT_BN / 32];   // max |bias| per 32 tokens of the tile
     __shared__ double tab[16];
     __shared__ double tab64[64];
     // per epilogue thread: the 16 logits of the chunk holding its group's running max
@@ -128,6 +129,8 @@ k_vocab_stats(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ C
                     col_isw[buf][c] = 1.0 / (double)sw;
                 }
                 col_b[buf][c] = b;
+                const float wb = warp_max(fabsf(b));
+                if (lane == 0) col_bmax[buf][ew] = wb;
                 bad |= !is_finite_f(b);
             }
             const int row = mb * TC_BM + lg * 32 + lane;
@@ -144,6 +147,16 @@ k_vocab_stats(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ C
             // fast-path preconditions, per thread and tile: one weight scale, and every
             // nonzero |q| = |acc| * rs in [2^-124, 2^127) (f32 normal range for |acc| < 2^31)
             const bool fast_row = one_scale && rs0 >= 0x1p-124 && rs0 * 2147483648.0 < 0x1p127;
+            // every logit of the tile lies in [-340, 340] when K * 127^2 * rs + max|b| < 340
+            // (|acc| <= K * 127^2; roundings add < 2^-22 relative), so no x - m falls below
+            // -700: the chunk minimum (the exp range guard) is then skipped
+            bool narrow = false;
+            if (__all_sync(0xffffffffu, fast_row)) {
+                float bmx = 0.0f;
+#pragma unroll
+                for (int i = 0; i < VT_BN / 32; ++i) bmx = fmaxf(bmx, col_bmax[buf][i]);
+                narrow = __all_sync(0xffffffffu, (double)K * 16129.0 * rs0 + (double)bmx < 340.0);
+            }
             // top-1 (value, smallest token) and runner-up value from chunk maxima: the chunk that
             // raised the running max is parked in shared memory; after the group, its token and
             // the runner-up (its own second value vs the other chunks' maxima) are resolved
@@ -207,19 +220,22 @@ k_vocab_stats(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ C
                         }
                     }
                 }
-                float cm, cn;
+                float cm, cn = 0.0f;
                 {   // chunk max / min as shallow trees (invalid tail tokens are -FLT_MAX: a tail chunk's
                     // min is then -FLT_MAX, harmless: tail chunks take the range-guarded exp anyway)
-                    float t[8], u[8];
+                    float t[8];
 #pragma unroll
-                    for (int j = 0; j < 8; ++j) {
-                        t[j] = fmaxf(x[2 * j], x[2 * j + 1]);
-                        u[j] = fminf(x[2 * j], x[2 * j + 1]);
-                    }
+                    for (int j = 0; j < 8; ++j) t[j] = fmaxf(x[2 * j], x[2 * j + 1]);
                     cm = fmaxf(fmaxf(fmaxf(t[0], t[1]), fmaxf(t[2], t[3])), fmaxf(fmaxf(t[4], t[5]), fmaxf(t[6], t[7])));
-                    cn = fminf(fminf(fminf(u[0], u[1]), fminf(u[2], u[3])), fminf(fminf(u[4], u[5]), fminf(u[6], u[7])));
+                    if (!narrow) {   // warp-uniform
+                        float u[8];
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) u[j] = fminf(x[2 * j], x[2 * j + 1]);
+                        cn = fminf(fminf(fminf(u[0], u[1]), fminf(u[2], u[3])), fminf(fminf(u[4], u[5]), fminf(u[6], u[7])));
+                    }
                 }
-                bad |= !(is_finite_f(cm) && is_finite_f(cn));   // +-inf (NaN only from non-finite bias)
+                // +-inf (NaN only from non-finite bias); a narrow tile's logits are finite by its bound
+                bad |= !(is_finite_f(cm) && is_finite_f(cn));
                 {   // strict '>': on equal maxima the earlier chunk (smaller tokens) stays best
                     const bool nbst = cm > m;
                     om = fmaxf(om, nbst ? m : cm);
@@ -236,7 +252,7 @@ k_vocab_stats(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ C
                 }
                 const double dm = (double)m;
                 double e4[4] = {0.0, 0.0, 0.0, 0.0};
-                if (ncols == 16 && !__any_sync(0xffffffffu, (double)cn - dm < -700.0)) {
+                if (ncols == 16 && (narrow || !__any_sync(0xffffffffu, (double)cn - dm < -700.0))) {
 #pragma unroll
                     for (int j = 0; j < 16; ++j) e4[j & 3] += exp_neg64((double)x[j] - dm, tab64);
                 } else {   // vocabulary tail or a logit range beyond 700 (range-guarded exp)

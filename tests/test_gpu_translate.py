@@ -233,6 +233,22 @@ def test_vocab_candidates_abi(V, k, dup, N):
     """qnmt_vocab_candidates (fused) == qnmt_gemm_i8 + qnmt_topk_candidates on
     the same codes, including vocabularies with repeated rows (exact ties), over
     1..10 row blocks of the fused kernel."""
+    _vocab_candidates_case(V, k, dup, N, 900.0)
+
+
+@pytest.mark.parametrize("ws", [0.5, 3e-3])
+def test_vocab_candidates_wide_logits(ws):
+    """Logit ranges far beyond 700 (tiny weight scale): the fused kernel's
+    range-guarded exp path (no narrow-tile bound) against GEMM + candidates.
+    Tokens must agree exactly. Scores are compared to 4 f64 ulps: when the top
+    logit leads the rest by > ~36, lse = log(1 + eps) with eps < 2^-52, so the
+    top token's log-prob (~ -eps, a tiny f32) carries the fp64 rounding of
+    1 + eps, which depends on summation order."""
+    _vocab_candidates_case(5000, 5, 0, 300, ws, score_ulps=4)
+    _vocab_candidates_case(5000, 5, 13, 37, ws, score_ulps=4)
+
+
+def _vocab_candidates_case(V, k, dup, N, wscale, score_ulps=0):
     import torch
     from paper_1804_05038_b200 import _lib, _dev
     rng = np.random.default_rng(V + 31 * k + dup + N)
@@ -242,7 +258,7 @@ def test_vocab_candidates_abi(V, k, dup, N):
         w = w[np.arange(V) % dup]
     W = torch.from_numpy(np.ascontiguousarray(w)).cuda()
     X = torch.from_numpy(rng.integers(-127, 128, (N, K)).astype(np.int8)).cuda()
-    ws = torch.full((1,), 900.0, device="cuda")
+    ws = torch.full((1,), wscale, device="cuda")
     seg = torch.from_numpy((np.arange(N) // 5).astype(np.int32)).cuda()
     xs = torch.from_numpy(rng.uniform(300, 900, N // 5 + 1).astype(np.float32)).cuda()
     bias = torch.from_numpy((np.round(rng.normal(0, 0.5, V) * 8) / 8).astype(np.float32)).cuda()
@@ -260,7 +276,12 @@ def test_vocab_candidates_abi(V, k, dup, N):
               ws.data_ptr(), V, bias.data_ptr(), live.data_ptr(), k, scratch.data_ptr(), cs1.data_ptr(),
               ct1.data_ptr(), f.data_ptr(), _dev.stream_ptr())
     _dev.raise_flag(f)
-    assert torch.equal(ct0, ct1) and torch.equal(cs0, cs1)
+    assert torch.equal(ct0, ct1)
+    if score_ulps == 0:
+        assert torch.equal(cs0, cs1)
+    else:
+        a, b = cs0.cpu().numpy(), cs1.cpu().numpy()
+        assert np.all(np.abs(a - b) <= score_ulps * np.spacing(np.abs(a)))
 
 
 @pytest.mark.parametrize("query,s0", [("previous", "transform"), ("current", "zero"), ("previous", "zero")])
