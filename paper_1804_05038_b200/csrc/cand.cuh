@@ -137,6 +137,27 @@ __device__ __forceinline__ double exp_neg64(double t, const double* __restrict__
     return __hiloint2double(__double2hiint(v) + kk * (1 << 20), __double2loint(v));
 }
 
+// acc + exp_neg64(t) with the 2^(k >> 6) scaling applied to the table entry (exact: a
+// power of two, result normal for t >= -700) so the final multiply and the add fuse into
+// one DFMA (one rounding instead of two)
+__device__ __forceinline__ double exp_neg64_acc(double t, const double* __restrict__ tab64, double acc) {
+    const double kd_m = fma(t, 92.33248261689366, 6755399441055744.0);    // t * 64/ln2 + 1.5*2^52
+    const int k = __double2loint(kd_m);
+    const double kd = kd_m - 6755399441055744.0;
+    double r = fma(kd, -0.010830424696249145, t);
+    r = fma(kd, -3.623510646634843e-19, r);
+    double p = fma(r, 1.0 / 120.0, 1.0 / 24.0);
+    p = fma(p, r, 1.0 / 6.0);
+    p = fma(p, r, 0.5);
+    p = fma(p, r, 1.0);
+    p = fma(p, r, 1.0);
+    const double tb = tab64[k & 63];
+    int kk;
+    asm("shr.s32 %0, %1, 6;" : "=r"(kk) : "r"(k));
+    const double ts = __hiloint2double(__double2hiint(tb) + kk * (1 << 20), __double2loint(tb));
+    return fma(p, ts, acc);
+}
+
 template <int KM>
 __device__ void block_merge_cands(Cand (&L)[KM], Cand (*wl)[KM], Cand* out, int kk) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;

@@ -254,7 +254,7 @@ k_vocab_stats(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ C
                 double e4[4] = {0.0, 0.0, 0.0, 0.0};
                 if (ncols == 16 && (narrow || !__any_sync(0xffffffffu, (double)cn - dm < -700.0))) {
 #pragma unroll
-                    for (int j = 0; j < 16; ++j) e4[j & 3] += exp_neg64((double)x[j] - dm, tab64);
+                    for (int j = 0; j < 16; ++j) e4[j & 3] = exp_neg64_acc((double)x[j] - dm, tab64, e4[j & 3]);
                 } else {   // vocabulary tail or a logit range beyond 700 (range-guarded exp)
 #pragma unroll
                     for (int j = 0; j < 16; ++j)
