@@ -60,10 +60,11 @@ k_vocab_stats(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ C
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* smem = (unsigned char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     const TcBars<C> bars(smem);
-    __shared__ double col_isw[2][VT_BN];   // 1 / s_w per token (double-buffered by tile)
-    __shared__ float col_sw[2][VT_BN];
-    __shared__ float col_b[2][VT_BN];
-    __shared__ float col_bmax[2][VT_BN / 32];   // max |bias| per 32 tokens of the tile
+    // per epilogue warp: bias (and weight scale, 1/scale) of its 64-token group of the current
+    // tile -- warp-private, so __syncwarp orders the writes and reads (no barrier across warps)
+    __shared__ double col_isw[VT_EPI_WARPS][VT_HALF];
+    __shared__ float col_sw[VT_EPI_WARPS][VT_HALF];
+    __shared__ __align__(16) float col_b[VT_EPI_WARPS][VT_HALF];
     __shared__ double tab[16];
     __shared__ double tab64[64];
     // per epilogue thread: the 16 logits of the chunk holding its group's running max
@@ -107,31 +108,41 @@ k_vocab_stats(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ C
         float sx = 1.0f;
         double isx = 1.0, rs0 = isw0;
         int mb = t_begin / n_blocks, nb = t_begin % n_blocks;
-        float b_pre = 0.0f;   // this tile's bias (loaded during the previous tile)
-        if (ew * 32 < VT_BN && t_begin < t_end && e.bias) {
-            const int v = nb * VT_BN + ew * 32 + lane;
-            if (v < V) b_pre = e.bias[v];
+        // this tile's bias for tokens lane and lane + 32 of the group (loaded one tile ahead)
+        float bp0 = 0.0f, bp1 = 0.0f;
+        if (t_begin < t_end && e.bias) {
+            const int v = nb * VT_BN + half * VT_HALF + lane;
+            if (v < V) bp0 = e.bias[v];
+            if (v + 32 < V) bp1 = e.bias[v + 32];
         }
         for (int tile = t_begin; tile < t_end; ++tile, ++it) {
             const int buf = it & 1;
             const uint32_t use = (uint32_t)(it >> 1) & 1u;
-            if (ew * 32 < VT_BN) {   // per-token bias (and per-token weight scale) of this tile -> smem
-                const int c = ew * 32 + lane;
-                const int v = nb * VT_BN + c;
-                const float b = b_pre;
+            float bmx;   // max |bias| over the group
+            {   // this warp's group: bias (and per-token weight scale) -> its smem slice
+                const int vg = nb * VT_BN + half * VT_HALF;
+                const float b0 = bp0, b1 = bp1;
                 {   // prefetch the next tile's
-                    const int vn = (nb + 1 == n_blocks ? 0 : nb + 1) * VT_BN + c;
-                    b_pre = (tile + 1 < t_end && e.bias && vn < V) ? e.bias[vn] : 0.0f;
+                    const int vn = (nb + 1 == n_blocks ? 0 : nb + 1) * VT_BN + half * VT_HALF + lane;
+                    const bool more = tile + 1 < t_end && e.bias;
+                    bp0 = (more && vn < V) ? e.bias[vn] : 0.0f;
+                    bp1 = (more && vn + 32 < V) ? e.bias[vn + 32] : 0.0f;
                 }
+                __syncwarp();   // the previous tile's reads of the slice are done
                 if (!one_scale) {
-                    const float sw = v < V ? e.w_scales[v / e.w_rows_per_scale] : 1.0f;
-                    col_sw[buf][c] = sw;
-                    col_isw[buf][c] = 1.0 / (double)sw;
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const int v = vg + lane + 32 * h;
+                        const float sw = v < V ? e.w_scales[v / e.w_rows_per_scale] : 1.0f;
+                        col_sw[ew][lane + 32 * h] = sw;
+                        col_isw[ew][lane + 32 * h] = 1.0 / (double)sw;
+                    }
                 }
-                col_b[buf][c] = b;
-                const float wb = warp_max(fabsf(b));
-                if (lane == 0) col_bmax[buf][ew] = wb;
-                bad |= !is_finite_f(b);
+                col_b[ew][lane] = b0;
+                col_b[ew][lane + 32] = b1;
+                bmx = warp_max(fmaxf(fabsf(b0), fabsf(b1)));
+                bad |= !(is_finite_f(b0) && is_finite_f(b1));
+                __syncwarp();
             }
             const int row = mb * TC_BM + lg * 32 + lane;
             const bool rok = row < M;
@@ -141,7 +152,6 @@ k_vocab_stats(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ C
                 rs0 = isx * isw0;   // acc -> logit multiplier when W has one scale
                 cur_mb = mb;
             }
-            asm volatile("bar.sync 1, %0;" ::"n"(32 * VT_EPI_WARPS));
             tc::mbar_wait(&bars.tfull[buf], use);
             tc::tc_fence_after();
             // fast-path preconditions, per thread and tile: one weight scale, and every
@@ -151,12 +161,8 @@ k_vocab_stats(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ C
             // (|acc| <= K * 127^2; roundings add < 2^-22 relative), so no x - m falls below
             // -700: the chunk minimum (the exp range guard) is then skipped
             bool narrow = false;
-            if (__all_sync(0xffffffffu, fast_row)) {
-                float bmx = 0.0f;
-#pragma unroll
-                for (int i = 0; i < VT_BN / 32; ++i) bmx = fmaxf(bmx, col_bmax[buf][i]);
+            if (__all_sync(0xffffffffu, fast_row))
                 narrow = __all_sync(0xffffffffu, (double)K * 16129.0 * rs0 + (double)bmx < 340.0);
-            }
             // top-1 (value, smallest token) and runner-up value from chunk maxima: the chunk that
             // raised the running max is parked in shared memory; after the group, its token and
             // the runner-up (its own second value vs the other chunks' maxima) are resolved
@@ -197,7 +203,7 @@ k_vocab_stats(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ C
                                 x[j] = dequant((int)r[j], sw0, sx);   // (fast path: one scale)
                         }
                     }
-                    const float4* b4 = reinterpret_cast<const float4*>(&col_b[buf][c0]);
+                    const float4* b4 = reinterpret_cast<const float4*>(&col_b[ew][c0 - half * VT_HALF]);
 #pragma unroll
                     for (int q4 = 0; q4 < 4; ++q4) {
                         const float4 bb = b4[q4];
@@ -210,11 +216,11 @@ k_vocab_stats(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ C
 #pragma unroll
                     for (int j = 0; j < 16; ++j) {
                         if (j < ncols) {
-                            const double isw = one_scale ? isw0 : col_isw[buf][c0 + j];
-                            const float swj = one_scale ? sw0 : col_sw[buf][c0 + j];
+                            const double isw = one_scale ? isw0 : col_isw[ew][c0 - half * VT_HALF + j];
+                            const float swj = one_scale ? sw0 : col_sw[ew][c0 - half * VT_HALF + j];
                             const double q = (double)(int)r[j] * (isx * isw);
                             x[j] = dequant_rcp_safe(q) ? __double2float_rn(q) : dequant((int)r[j], swj, sx);
-                            x[j] = __fadd_rn(x[j], col_b[buf][c0 + j]);
+                            x[j] = __fadd_rn(x[j], col_b[ew][c0 - half * VT_HALF + j]);
                         } else {
                             x[j] = -FLT_MAX;   // excluded below (exp skipped, never above a real logit)
                         }
