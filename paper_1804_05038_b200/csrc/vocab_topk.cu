@@ -170,7 +170,7 @@ k_vocab_stats(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ C
             float om = -FLT_MAX;   // max of the chunk maxima other than the best chunk's
             int bc0 = -1;          // first token of the best chunk (-1: none)
             float m = -FLT_MAX;   // running max of the half-tile (the exp reference)
-            double s = 0.0;
+            double e4[4] = {0.0, 0.0, 0.0, 0.0};   // sum exp(x - m) as 4 interleaved chains over the group
 #pragma unroll 1
             for (int c0 = half * VT_HALF; c0 < (half + 1) * VT_HALF; c0 += 16) {
                 uint32_t r[16];
@@ -253,11 +253,12 @@ k_vocab_stats(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ C
                     }
                 }
                 if (cm > m) {   // rescale the running sum (first chunk, then rare)
-                    s = (m == -FLT_MAX) ? 0.0 : s * exp_neg((double)m - (double)cm, tab);
+                    const double f = (m == -FLT_MAX) ? 0.0 : exp_neg((double)m - (double)cm, tab);
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) e4[q] *= f;
                     m = cm;
                 }
                 const double dm = (double)m;
-                double e4[4] = {0.0, 0.0, 0.0, 0.0};
                 if (ncols == 16 && (narrow || !__any_sync(0xffffffffu, (double)cn - dm < -700.0))) {
 #pragma unroll
                     for (int j = 0; j < 16; ++j) e4[j & 3] = exp_neg64_acc((double)x[j] - dm, tab64, e4[j & 3]);
@@ -266,7 +267,6 @@ k_vocab_stats(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ C
                     for (int j = 0; j < 16; ++j)
                         if (j < ncols) e4[j & 3] += exp_neg((double)x[j] - dm, tab);
                 }
-                s += (e4[0] + e4[1]) + (e4[2] + e4[3]);
             }
             float a2 = om;
             int i1 = 0x7fffffff;
@@ -294,7 +294,7 @@ k_vocab_stats(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ C
             if (lane == 0) tc::mbar_arrive(&bars.tempty[buf]);
             if (rok) {
                 VtPart p;
-                p.s = s;
+                p.s = (e4[0] + e4[1]) + (e4[2] + e4[3]);
                 p.m = m;
                 p.a2 = a2;
                 p.i1 = i1;
