@@ -55,7 +55,7 @@ WORKLOAD = ("cfg5 bulk translation: one step = the whole seeded 8192-sentence co
             "the GPUs, 256 sentences per engine call, beam 5, max_ratio 1.5, V_tgt 50000, H 1024, E 512, A 2048, "
             "R 512")
 # DRAM bytes per algorithmic byte measured by `ncu --set full` at N = 1280 (profiles/r01_ncu_summary.md)
-NCU_TRAFFIC_RATIO = {"attention": 264.4 / 249.8, "vocab_stats": 34.47 / 50.30, "vocab_merge": 24.14 / 24.13}
+NCU_TRAFFIC_RATIO = {"attention": 264.4 / 249.8, "vocab_stats": 27.72 / 50.30, "vocab_merge": 24.14 / 24.13}
 
 
 def peaks():
