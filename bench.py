@@ -254,6 +254,7 @@ def main():
 
     import paper_1804_05038_b200 as pb
     from paper_1804_05038_b200 import _lib
+    from paper_1804_05038_b200.engine import engine_pool
 
     torch.cuda.set_device(local)
     if world > 1:
@@ -387,7 +388,7 @@ def main():
     e2e_secs, e2e_toks = 0.0, 0
     cfg = pb.DecodeConfig(beam=BEAM, max_ratio=MAX_RATIO, precision="int8")
     pb.translate_batch(qm, shard_ids, cfg, max_batch=PER_GPU, return_ids=True, streams=STREAMS)   # warm-up
-    eng_pool = qm._engines
+    eng_pool = engine_pool(qm).all
     b0 = [(e.h2d_bytes, e.d2h_bytes) for e in eng_pool if e is not None]
     for k in range(args.steps):
         flush.fill_(1)

@@ -88,17 +88,17 @@ def main():
     qm = pb.quantize_model(params)
     net = pb.build_network(qm)
     src50 = np.random.default_rng(5038).integers(3, 32000, 50)
-    t = timed(lambda: net.engine(1, 50, 1).encode_batch([src50]))
+    t = timed(lambda: net.encode(src50))
     res.append({"config": "cfg2 encode l=50", "ms": t * 1e3})
     toks = [params.src_tokens[i] for i in src50]
-    cfg = pb.DecodeConfig(beam=1, max_ratio=0.98)
+    cfg = pb.DecodeConfig(beam=1, max_ratio=0.98, precision="int8")
     t = timed(lambda: pb.translate(qm, toks, cfg))
     res.append({"config": "cfg3 greedy 50 steps (encoder + decoder)", "ms": t * 1e3,
                 "tokens_per_s": 50 / t, "ms_per_step": t * 1e3 / 51})
     # cfg4: 64 sentences, l ~ U[10, 80], beam 5, max_ratio 1.5 (batched, tcgen05 path)
     rng4 = np.random.default_rng(4)
     c4 = [rng4.integers(3, 32000, int(rng4.integers(10, 81))).tolist() for _ in range(64)]
-    cfg4 = pb.DecodeConfig(beam=5, max_ratio=1.5)
+    cfg4 = pb.DecodeConfig(beam=5, max_ratio=1.5, precision="int8")
     for mb, ns in ((64, 1), (32, 2), (16, 3)):
         toks = []
 
@@ -109,7 +109,7 @@ def main():
         res.append({"config": f"cfg4 64 sentences beam 5 (batches of {mb}, {ns} streams)", "ms": t * 1e3,
                     "sentences_per_s": 64 / t, "tokens_per_s": ntok / t})
     src100 = np.random.default_rng(7).integers(3, 32000, 100)
-    t = timed(lambda: pb.translate(qm, [params.src_tokens[i] for i in src100], pb.DecodeConfig(5, 1.5)), 3)
+    t = timed(lambda: pb.translate(qm, [params.src_tokens[i] for i in src100], pb.DecodeConfig(5, 1.5, "int8")), 3)
     res.append({"config": "1 sentence l=100 beam 5 (151 steps)", "ms": t * 1e3, "ms_per_step": t * 1e3 / 151})
     for r in res:
         print(json.dumps(r), flush=True)

@@ -26,7 +26,7 @@ def main():
     params = pb.synthetic_model(pb.Dims(32000, 32000, 512, 1024, 2048, 512), 1804)
     qm = pb.quantize_model(params)
     src = [params.src_tokens[i] for i in np.random.default_rng(5038).integers(3, 32000, 50)]
-    cfg = pb.DecodeConfig(beam=beam, max_ratio=0.98)
+    cfg = pb.DecodeConfig(beam=beam, max_ratio=0.98, precision="int8")
     for _ in range(3):
         pb.translate(qm, src, cfg)
     torch.cuda.synchronize()

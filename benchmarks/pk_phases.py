@@ -21,9 +21,9 @@ def main():
     params = pb.synthetic_model(pb.Dims(32000, 32000, 512, 1024, 2048, 512), 1804)
     qm = pb.quantize_model(params)
     src = [params.src_tokens[i] for i in np.random.default_rng(5038).integers(3, 32000, 50)]
-    cfg = pb.DecodeConfig(beam=1, max_ratio=0.98)
+    cfg = pb.DecodeConfig(beam=1, max_ratio=0.98, precision="int8")
     pb.translate(qm, src, cfg)
-    e = qm._engines[0]
+    e = engine_pool(qm).all[0]
     lib = _lib.load()
     lib.qnmt_engine_stamps(e._h, 1)
     pb.translate(qm, src, cfg)

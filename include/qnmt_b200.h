@@ -322,14 +322,17 @@ int qnmt_decoder_step(qnmt_engine* e, int64_t N, const int32_t* col_sent, int32_
                       int64_t lda, void* stream);
 
 /* Device-resident variant for benchmarking / pipelines: src_ids already on the
- * device, results kept in the engine until qnmt_fetch_results (D2H + the
- * final host-side min-by-(-logp, tokens) selection of decoder.py:157). */
+ * device, results kept in the engine until qnmt_fetch_results (the final
+ * min-by-(-logp, tokens) selection of decoder.py:157 runs on the device, then
+ * one D2H of n * (max_steps + 3) words). */
 int qnmt_decode_batch_device(qnmt_engine* e, const int32_t* src_ids_dev, const int32_t* src_len,
                              int32_t n_sent, int32_t beam, double max_ratio, void* stream);
 int qnmt_fetch_results(qnmt_engine* e, int32_t* out_tokens, int32_t out_stride, int32_t* out_len,
                        double* out_logp, void* stream);
 /* bytes copied device->host by the last fetch */
 int64_t qnmt_last_d2h_bytes(const qnmt_engine* e);
+/* bytes copied host->device by the last decode call (ids, lengths, batch plan, search init) */
+int64_t qnmt_last_h2d_bytes(const qnmt_engine* e);
 /* kernels launched by this library since load (process-wide counter) */
 int64_t qnmt_kernel_launches(void);
 

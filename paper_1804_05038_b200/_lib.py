@@ -53,6 +53,7 @@ SIGNATURES = {
     "qnmt_decode_batch_device": (I32, [P, P, P, I32, I32, F64, P]),
     "qnmt_fetch_results": (I32, [P, P, I32, P, P, P]),
     "qnmt_last_d2h_bytes": (I64, [P]),
+    "qnmt_last_h2d_bytes": (I64, [P]),
     "qnmt_kernel_launches": (I64, []),
     "qnmt_set_gemm_impl": (I32, [I32]),
     "qnmt_set_tc_pair": (I32, [I32]),

@@ -21,18 +21,11 @@ import json
 import time
 from dataclasses import dataclass, field
 
-from .decoder import DecodeConfig, _engine_for, _members, translate_batch
+from .decoder import DecodeConfig, _decode_ids, _members, translate_batch
 from .errors import ConfigError
 from .model import ModelParams, QuantizedModel
 
 PHASES = ("quantize-activations", "matmul", "transcendental", "embedding", "search-overhead", "other")
-
-# engine phase groups (csrc/engine.cu PG_*) -> reference phase names (bench.py:23-24)
-_GROUP_TO_PHASE = {"quantize-activations": "quantize-activations", "matmul": "matmul", "matmul-vocab": "matmul",
-                   "gru": "transcendental", "attention": "transcendental", "embedding": "embedding",
-                   "topk": "search-overhead", "search": "search-overhead", "gather": "search-overhead",
-                   "encoder": "encoder", "other": "other"}
-
 
 class PhaseTimer:
     """Wall-clock accumulator per named phase (bench.py:27-57): phases nest and
@@ -110,18 +103,10 @@ def _device_phases(model, corpus, cfg: DecodeConfig, batch: int) -> dict:
     members = _members(model, cfg.precision)
     if len(members) != 1:
         return {}
-    max_len = max(len(s) for s in corpus)
-    e = _engine_for(members[0], min(batch, len(corpus)), max_len, cfg.beam)
-    e.profile(True)
-    try:
-        translate_batch(model, corpus, cfg, max_batch=batch)
-        groups = e.profile_read()
-    finally:
-        e.profile(False)
+    m = members[0]
+    ids = [[m.src_ids(s) for s in corpus]]
     out: dict = {}
-    for g, ms in groups.items():
-        ph = _GROUP_TO_PHASE.get(g, "other")
-        out[ph] = out.get(ph, 0.0) + ms * 1e-3
+    _decode_ids(members, ids, cfg, batch, sort=True, phases=out)
     return out
 
 

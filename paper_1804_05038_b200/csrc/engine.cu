@@ -176,8 +176,12 @@ struct qnmt_engine {
     double* fin_score; int32_t* fin_step; int32_t* fin_slot; int32_t* fin_eos;
     int32_t* hist_tok; int32_t* hist_par;
     int32_t* h_pinned = nullptr;   // host pinned scalar
+    int32_t* res_dev = nullptr;    // [S][hist_steps + 3] packed results (k_finalize)
+    int32_t* fin_scratch = nullptr;
+    int32_t* res_host = nullptr;   // pinned staging of res_dev
     int last_n = 0, last_tmax = 0;
-    int64_t d2h_bytes = 0;
+    int64_t d2h_bytes = 0;         // last batch: result bytes copied device -> host
+    int64_t h2d_bytes = 0;         // last batch: host -> device bytes (ids, lengths, batch plan, search init)
     // phase profiler (CUDA events on the engine stream; off by default)
     bool prof_on = false;
     int prof_group = -1;
@@ -256,6 +260,12 @@ static int check_flag(qnmt_engine* e, cudaStream_t st) {
 
 #define TRY(x) do { int _r = (x); if (_r != QNMT_OK) return _r; } while (0)
 
+// host -> device copy of per-batch inputs, counted for the e2e traffic report
+static cudaError_t h2d(qnmt_engine* e, void* dst, const void* src, size_t bytes, cudaStream_t st) {
+    e->h2d_bytes += (int64_t)bytes;
+    return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st);
+}
+
 static int gemm(const int8_t* W, int64_t M, int64_t K, const float* ws, int64_t rps, const int8_t* X,
                 int64_t N, int64_t ldx, const float* xs, const int32_t* seg, const float* bias, float* Y,
                 int64_t ldy, int32_t flags, cudaStream_t st, const float* add1 = nullptr, int64_t ld1 = 0,
@@ -309,10 +319,10 @@ static int encode_core(qnmt_engine* e, const int32_t* ids_dev, const int32_t* le
         for (int i = 0; i < len[s]; ++i) pos_sent[row[s] + i] = s;
     std::vector<int32_t> s0dst(n);   // slot of each sentence (inverse permutation)
     for (int k = 0; k < n; ++k) s0dst[perm[k]] = k;
-    QNMT_CUDA(cudaMemcpyAsync(e->enc_rows, rows.data(), rows.size() * 4, cudaMemcpyHostToDevice, st));
-    QNMT_CUDA(cudaMemcpyAsync(e->enc_out_rows, orows.data(), orows.size() * 4, cudaMemcpyHostToDevice, st));
-    QNMT_CUDA(cudaMemcpyAsync(e->pos_sent, pos_sent.data(), (size_t)P * 4, cudaMemcpyHostToDevice, st));
-    QNMT_CUDA(cudaMemcpyAsync(e->s0_dst, s0dst.data(), (size_t)n * 4, cudaMemcpyHostToDevice, st));
+    QNMT_CUDA(h2d(e, e->enc_rows, rows.data(), rows.size() * 4, st));
+    QNMT_CUDA(h2d(e, e->enc_out_rows, orows.data(), orows.size() * 4, st));
+    QNMT_CUDA(h2d(e, e->pos_sent, pos_sent.data(), (size_t)P * 4, st));
+    QNMT_CUDA(h2d(e, e->s0_dst, s0dst.data(), (size_t)n * 4, st));
 
     if (m->fp32) return encode_core_f32(e, ids_dev, len, n, Lmax, P, perm, states, att_proj, s0, st);
     // input side for every position at once (per-position scales; one GEMM per direction)
@@ -748,8 +758,13 @@ static int grow_history(qnmt_engine* e, int steps) {
     if (e->hblock) cudaFree(e->hblock);
     size_t S = e->S, B = e->B, T = steps;
     size_t fin_cap = (T + 1) * B;
-    size_t bytes = S * fin_cap * (8 + 4 + 4 + 4) + 2 * S * T * B * 4 + (T + 1) * ST_COLS * 8 + 4096;
+    size_t res_w = T + 3;   // packed result row: len, logp (2 words), up to T tokens
+    size_t bytes = S * fin_cap * (8 + 4 + 4 + 4) + 2 * S * T * B * 4 + (T + 1) * ST_COLS * 8 +
+                   S * res_w * 4 + S * 2 * (T + 2) * 4 + 8192;
     QNMT_CUDA(cudaMalloc(&e->hblock, bytes));
+    if (e->res_host) cudaFreeHost(e->res_host);
+    e->res_host = nullptr;
+    QNMT_CUDA(cudaMallocHost(&e->res_host, S * res_w * 4));
     e->hblock_bytes = bytes;
     Arena a{e->hblock, bytes, 0};
     e->stamps = a.take<long long>((T + 1) * ST_COLS);
@@ -759,6 +774,8 @@ static int grow_history(qnmt_engine* e, int steps) {
     e->fin_eos = a.take<int32_t>(S * fin_cap);
     e->hist_tok = a.take<int32_t>(S * T * B);
     e->hist_par = a.take<int32_t>(S * T * B);
+    e->res_dev = a.take<int32_t>(S * res_w);
+    e->fin_scratch = a.take<int32_t>(S * 2 * (T + 2));
     e->hist_steps = steps;
     return QNMT_OK;
 }
@@ -1003,6 +1020,7 @@ int qnmt_engine_destroy(qnmt_engine* e) {
     if (e->block) cudaFree(e->block);
     if (e->hblock) cudaFree(e->hblock);
     if (e->h_pinned) cudaFreeHost(e->h_pinned);
+    if (e->res_host) cudaFreeHost(e->res_host);
     for (auto& kv : e->graphs) {
         cudaGraphExecDestroy(kv.second.first);
         cudaGraphExecDestroy(kv.second.second);
@@ -1211,13 +1229,15 @@ static int init_member(qnmt_engine* e, const int32_t* src_ids, bool ids_on_devic
     const qnmt_model* m = e->m;
     const int64_t H = m->H;
     QNMT_CUDA(cudaMemsetAsync(e->err, 0, 4, st));
-    QNMT_CUDA(cudaMemcpyAsync(e->src_ids, src_ids, (size_t)b.P * 4,
-                              ids_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
+    if (ids_on_device)
+        QNMT_CUDA(cudaMemcpyAsync(e->src_ids, src_ids, (size_t)b.P * 4, cudaMemcpyDeviceToDevice, st));
+    else
+        QNMT_CUDA(h2d(e, e->src_ids, src_ids, (size_t)b.P * 4, st));
     prof_mark(e, PG_ENCODER, st);
     TRY(encode_core(e, e->src_ids, src_len, b.row.data(), n, e->enc_states, e->enc_att, e->enc_s0, st));
     prof_mark(e, PG_MISC, st);
-    QNMT_CUDA(cudaMemcpyAsync(e->sent_row, b.row.data(), (size_t)n * 8, cudaMemcpyHostToDevice, st));
-    QNMT_CUDA(cudaMemcpyAsync(e->sent_len, src_len, (size_t)n * 4, cudaMemcpyHostToDevice, st));
+    QNMT_CUDA(h2d(e, e->sent_row, b.row.data(), (size_t)n * 8, st));
+    QNMT_CUDA(h2d(e, e->sent_len, src_len, (size_t)n * 4, st));
     TRY(att_minmax_launch(e->enc_att, e->sent_row, e->sent_len, n, m->A, e->att_mm, st));
     QNMT_CUDA(cudaMemcpyAsync(e->st_s[0], e->enc_s0, (size_t)n * H * 4, cudaMemcpyDeviceToDevice, st));
     QNMT_CUDA(cudaMemcpyAsync(e->st_sp[0], e->enc_s0, (size_t)n * H * 4, cudaMemcpyDeviceToDevice, st));
@@ -1237,12 +1257,12 @@ static int init_search(qnmt_engine* e, const BatchPlan& b, int32_t n, cudaStream
     std::vector<int32_t> iota_n(n), y0(n, 2), ones(n, 1);
     std::iota(iota_n.begin(), iota_n.end(), 0);
     std::vector<double> dz(n, 0.0);
-    QNMT_CUDA(cudaMemcpyAsync(e->max_steps, b.msteps.data(), (size_t)n * 4, cudaMemcpyHostToDevice, st));
-    QNMT_CUDA(cudaMemcpyAsync(e->P, ones.data(), (size_t)n * 4, cudaMemcpyHostToDevice, st));
-    QNMT_CUDA(cudaMemcpyAsync(e->col_off, iota_n.data(), (size_t)n * 4, cudaMemcpyHostToDevice, st));
-    QNMT_CUDA(cudaMemcpyAsync(e->col_sent[0], iota_n.data(), (size_t)n * 4, cudaMemcpyHostToDevice, st));
-    QNMT_CUDA(cudaMemcpyAsync(e->y[0], y0.data(), (size_t)n * 4, cudaMemcpyHostToDevice, st));
-    QNMT_CUDA(cudaMemcpyAsync(e->live[0], dz.data(), (size_t)n * 8, cudaMemcpyHostToDevice, st));
+    QNMT_CUDA(h2d(e, e->max_steps, b.msteps.data(), (size_t)n * 4, st));
+    QNMT_CUDA(h2d(e, e->P, ones.data(), (size_t)n * 4, st));
+    QNMT_CUDA(h2d(e, e->col_off, iota_n.data(), (size_t)n * 4, st));
+    QNMT_CUDA(h2d(e, e->col_sent[0], iota_n.data(), (size_t)n * 4, st));
+    QNMT_CUDA(h2d(e, e->y[0], y0.data(), (size_t)n * 4, st));
+    QNMT_CUDA(h2d(e, e->live[0], dz.data(), (size_t)n * 8, st));
     QNMT_CUDA(cudaMemsetAsync(e->done, 0, (size_t)n * 4, st));
     QNMT_CUDA(cudaMemsetAsync(e->fin_cnt, 0, (size_t)n * 4, st));
     QNMT_CUDA(cudaMemsetAsync(e->steps_run, 0, (size_t)n * 4, st));
@@ -1301,7 +1321,7 @@ static int decode_greedy1(qnmt_engine* e, const BatchPlan& b, cudaStream_t st) {
     a.step_dev = e->d_step;
     int32_t* ctl0 = e->h_pinned + 4;   // host staging of the control words
     ctl0[0] = 2; ctl0[1] = 0x7fffffff; ctl0[2] = 0; ctl0[3] = 0; ctl0[4] = 0;
-    QNMT_CUDA(cudaMemcpyAsync(e->pk_ctl, ctl0, 5 * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+    QNMT_CUDA(h2d(e, e->pk_ctl, ctl0, 5 * sizeof(int32_t), st));
     TRY(greedy1_launch(a, st));
     return check_flag(e, st);
 }
@@ -1312,6 +1332,7 @@ static int decode_core(qnmt_engine* e, const int32_t* src_ids, bool ids_on_devic
     const qnmt_model* m = e->m;
     const int64_t V = m->Vt;
     BatchPlan b;
+    e->h2d_bytes = 0;
     TRY(plan_batch(e, src_ids, ids_on_device, src_len, n, beam, max_ratio, b));
     TRY(init_search(e, b, n, st));
     TRY(init_member(e, src_ids, ids_on_device, src_len, b, n, st));
@@ -1323,7 +1344,7 @@ static int decode_core(qnmt_engine* e, const int32_t* src_ids, bool ids_on_devic
         cudaGraphExec_t g[2];
         TRY(get_step_graphs(e, n, beam, k_list, g));
         e->h_pinned[1] = n;
-        QNMT_CUDA(cudaMemcpyAsync(e->d_N, e->h_pinned + 1, 4, cudaMemcpyHostToDevice, st));
+        QNMT_CUDA(h2d(e, e->d_N, e->h_pinned + 1, 4, st));
         QNMT_CUDA(cudaMemsetAsync(e->d_step, 0, 4, st));
         constexpr int POLL = 16;
         for (int t = 0; t < Tmax; ++t) {
@@ -1386,6 +1407,7 @@ static int decode_ensemble(qnmt_engine* const* es, int nm, const int32_t* src_id
         BatchPlan bi;
         TRY(plan_batch(es[i], src_ids + (size_t)i * b.P, false, src_len, n, beam, max_ratio, bi));
     }
+    for (int i = 0; i < nm; ++i) es[i]->h2d_bytes = 0;
     TRY(init_search(lead, b, n, st));
     for (int i = 0; i < nm; ++i) TRY(init_member(es[i], src_ids + (size_t)i * b.P, false, src_len, b, n, st));
     const int k_list = (int)std::min<int64_t>(beam, V);
@@ -1415,57 +1437,28 @@ static int decode_ensemble(qnmt_engine* const* es, int nm, const int32_t* src_id
     return QNMT_OK;
 }
 
-// D2H of the finished lists + history, then min by (-logp, tokens) (decoder.py:157-160)
+// min by (-logp, tokens) on the device (k_finalize, decoder.py:157-160), then one
+// D2H of the packed rows [len, logp, tokens] -- n * (Tmax + 3) words per batch
 static int finalize(qnmt_engine* e, int32_t* out_tokens, int32_t out_stride, int32_t* out_len,
                     double* out_logp, cudaStream_t st) {
     const int n = e->last_n;
     if (out_stride < e->last_tmax) { set_error("out_stride %d < max steps %d", out_stride, e->last_tmax); return QNMT_ERR_CONFIG; }
-    const int B = e->B, T = e->hist_steps, FC = (T + 1) * B;
-    std::vector<int32_t> fin_cnt(n), hist_tok((size_t)n * T * B), hist_par((size_t)n * T * B);
-    std::vector<double> fin_score((size_t)n * FC);
-    std::vector<int32_t> fin_step((size_t)n * FC), fin_slot((size_t)n * FC), fin_eos((size_t)n * FC);
-    QNMT_CUDA(cudaMemcpyAsync(fin_cnt.data(), e->fin_cnt, (size_t)n * 4, cudaMemcpyDeviceToHost, st));
-    QNMT_CUDA(cudaMemcpyAsync(fin_score.data(), e->fin_score, fin_score.size() * 8, cudaMemcpyDeviceToHost, st));
-    QNMT_CUDA(cudaMemcpyAsync(fin_step.data(), e->fin_step, fin_step.size() * 4, cudaMemcpyDeviceToHost, st));
-    QNMT_CUDA(cudaMemcpyAsync(fin_slot.data(), e->fin_slot, fin_slot.size() * 4, cudaMemcpyDeviceToHost, st));
-    QNMT_CUDA(cudaMemcpyAsync(fin_eos.data(), e->fin_eos, fin_eos.size() * 4, cudaMemcpyDeviceToHost, st));
-    QNMT_CUDA(cudaMemcpyAsync(hist_tok.data(), e->hist_tok, hist_tok.size() * 4, cudaMemcpyDeviceToHost, st));
-    QNMT_CUDA(cudaMemcpyAsync(hist_par.data(), e->hist_par, hist_par.size() * 4, cudaMemcpyDeviceToHost, st));
+    if (n <= 0) return QNMT_OK;
+    const int T = e->hist_steps, W = T + 3, Wc = e->last_tmax + 3;
+    FinalizeArgs a{e->fin_cnt, e->fin_score, e->fin_step, e->fin_slot, e->fin_eos, e->hist_tok, e->hist_par,
+                   (T + 1) * e->B, T, e->B, e->res_dev, W, e->fin_scratch, 0};
+    TRY(finalize_launch(a, n, st));
+    QNMT_CUDA(cudaMemcpy2DAsync(e->res_host, (size_t)Wc * 4, e->res_dev, (size_t)W * 4, (size_t)Wc * 4, n,
+                                cudaMemcpyDeviceToHost, st));
     QNMT_CUDA(cudaStreamSynchronize(st));
-    e->d2h_bytes = (int64_t)(fin_cnt.size() + hist_tok.size() + hist_par.size() + fin_step.size() +
-                             fin_slot.size() + fin_eos.size()) * 4 + (int64_t)fin_score.size() * 8;
+    e->d2h_bytes = (int64_t)n * Wc * 4;
     for (int s = 0; s < n; ++s) {
-        auto backtrack = [&](int t, int j, std::vector<int32_t>& out) {
-            out.clear();
-            for (int tt = t; tt >= 0; --tt) {
-                size_t h = ((size_t)s * T + tt) * B + j;
-                out.push_back(hist_tok[h]);
-                j = hist_par[h];
-            }
-            std::reverse(out.begin(), out.end());
-        };
-        std::vector<int32_t> best, cand;
-        double best_s = 0;
-        bool have = false;
-        for (int f = 0; f < fin_cnt[s]; ++f) {
-            size_t fb = (size_t)s * FC + f;
-            if (fin_eos[fb]) {
-                backtrack(fin_step[fb] - 1, fin_slot[fb], cand);
-                cand.push_back(2);
-            } else {
-                backtrack(fin_step[fb], fin_slot[fb], cand);
-            }
-            double sc = fin_score[fb];
-            if (!have || sc > best_s || (sc == best_s && cand < best)) {
-                best = cand;
-                best_s = sc;
-                have = true;
-            }
-        }
-        if (!best.empty() && best.back() == 2) best.pop_back();
-        out_len[s] = (int32_t)best.size();
-        out_logp[s] = best_s;
-        for (size_t i = 0; i < best.size(); ++i) out_tokens[(size_t)s * out_stride + i] = best[i];
+        const int32_t* row = e->res_host + (size_t)s * Wc;
+        const int len = row[0];
+        out_len[s] = len;
+        const uint64_t bits = (uint64_t)(uint32_t)row[1] | ((uint64_t)(uint32_t)row[2] << 32);
+        memcpy(&out_logp[s], &bits, 8);
+        memcpy(out_tokens + (size_t)s * out_stride, row + 3, (size_t)len * 4);
     }
     return QNMT_OK;
 }
@@ -1499,5 +1492,7 @@ int qnmt_fetch_results(qnmt_engine* e, int32_t* out_tokens, int32_t out_stride, 
 }
 
 int64_t qnmt_last_d2h_bytes(const qnmt_engine* e) { return e ? e->d2h_bytes : 0; }
+
+int64_t qnmt_last_h2d_bytes(const qnmt_engine* e) { return e ? e->h2d_bytes : 0; }
 
 }  // extern "C"

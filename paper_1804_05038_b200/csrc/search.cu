@@ -239,6 +239,108 @@ __global__ void k_gather_rows(const float* __restrict__ a, const float* __restri
     }
 }
 
+// ---------------------------------------------------------------------------
+// Final selection on the device (decoder.py:157-160): the answer is the
+// finished hypothesis minimising (-log_prob, token list), EOS stripped.  One
+// warp per sentence: the lanes stage the sentence's (token, parent) history
+// in shared memory (coalesced) and find the best score; lane 0 backtracks the
+// hypotheses holding that score (Python's list order breaks exact ties) and
+// writes one packed row [len, logp lo, logp hi, tokens...] per sentence, so
+// the host copies n * (Tmax + 3) words instead of the whole history block.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ int fin_backtrack(const int32_t* ht, const int32_t* hp, int B, int step, int slot, int eos,
+                                             int32_t* out) {
+    // tokens 0..t of the hypothesis ending in `slot` at step t (t = step - 1 for an EOS entry)
+    const int t = eos ? step - 1 : step;
+    int j = slot;
+    for (int tt = t; tt >= 0; --tt) {
+        out[tt] = ht[tt * B + j];
+        j = hp[tt * B + j];
+    }
+    if (eos) out[t + 1] = EOS;
+    return t + 2 - (eos ? 0 : 1);   // EOS entries: t + 2 tokens incl. the EOS; survivors: t + 1
+}
+
+__global__ void __launch_bounds__(32)
+k_finalize(FinalizeArgs a) {
+    extern __shared__ int32_t fsm[];
+    const int s = blockIdx.x, lane = threadIdx.x;
+    const int B = a.B, T = a.T;
+    const int64_t hb = (int64_t)s * T * B;
+    const int fc = a.fin_cnt[s];
+    const int64_t fb = (int64_t)s * a.fin_cap;
+    int rows = 0;   // history rows any finished hypothesis reaches
+    for (int f = lane; f < fc; f += 32) rows = max(rows, a.fin_step[fb + f] + 1);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) rows = max(rows, __shfl_xor_sync(0xffffffffu, rows, o));
+    rows = min(rows, T);
+    const int32_t* ht = a.hist_tok + hb;
+    const int32_t* hp = a.hist_par + hb;
+    int32_t* bufA = fsm;
+    int32_t* bufB = fsm + (T + 2);
+    if (a.stage) {   // generic pointers: the backtrack reads shared memory when the history fits
+        int32_t* st = fsm + 2 * (T + 2);
+        for (int i = lane; i < rows * B; i += 32) {
+            st[i] = ht[i];
+            st[T * B + i] = hp[i];
+        }
+        __syncwarp();
+        ht = st;
+        hp = st + T * B;
+    } else {
+        bufA = a.scratch + (int64_t)s * 2 * (T + 2);
+        bufB = bufA + (T + 2);
+    }
+    double best = -DBL_MAX;
+    for (int f = lane; f < fc; f += 32) best = fmax(best, a.fin_score[fb + f]);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) best = fmax(best, __shfl_xor_sync(0xffffffffu, best, o));
+    if (lane != 0) return;
+    int32_t* row = a.res + (int64_t)s * a.res_stride;
+    int la = -1, fa = -1;
+    for (int f = 0; f < fc; ++f) {
+        if (a.fin_score[fb + f] != best) continue;
+        const int st_ = a.fin_step[fb + f], sl = a.fin_slot[fb + f], eo = a.fin_eos[fb + f];
+        if (la < 0) {
+            la = fin_backtrack(ht, hp, B, st_, sl, eo, bufA);
+            fa = f;
+            continue;
+        }
+        const int lb = fin_backtrack(ht, hp, B, st_, sl, eo, bufB);
+        int i = 0;
+        while (i < la && i < lb && bufA[i] == bufB[i]) ++i;
+        const bool less = (i < la && i < lb) ? bufB[i] < bufA[i] : lb < la;
+        if (less) {
+            int32_t* t = bufA; bufA = bufB; bufB = t;
+            la = lb;
+            fa = f;
+        }
+    }
+    int len = 0;
+    double lp = 0.0;
+    if (fa >= 0) {
+        len = (la > 0 && bufA[la - 1] == EOS) ? la - 1 : la;   // decoder.py:158
+        lp = best;
+    }
+    row[0] = len;
+    const long long bits = __double_as_longlong(lp);
+    row[1] = (int32_t)(bits & 0xffffffffll);
+    row[2] = (int32_t)(bits >> 32);
+    for (int i = 0; i < len; ++i) row[3 + i] = bufA[i];
+}
+
+int finalize_launch(const FinalizeArgs& a, int n, cudaStream_t st) {
+    if (n <= 0) return QNMT_OK;
+    FinalizeArgs b = a;
+    const size_t bufs = (size_t)2 * (a.T + 2) * 4, hist = (size_t)2 * a.T * a.B * 4;
+    b.stage = bufs + hist <= 48 * 1024 ? 1 : 0;
+    if (!b.stage && !a.scratch) { set_error("finalize: no global scratch for a %d-step history", a.T); return QNMT_ERR_CONFIG; }
+    const size_t smem = b.stage ? bufs + hist : 0;
+    k_finalize<<<(unsigned)n, 32, smem, st>>>(b);
+    QNMT_CHECK_LAUNCH("k_finalize");
+    return QNMT_OK;
+}
+
 int search_step_launch(const SearchState& ss, int step, int n_sent, int beam, int k_list,
                        cudaStream_t st) {
     if (n_sent > SEARCH_T || beam > 16 || k_list > 16) {

@@ -33,6 +33,23 @@ struct SearchState {
     int32_t* np_tmp = nullptr;   // [S] live selections per sentence (select -> layout)
 };
 
+// device-side final selection (decoder.py:157-160), one packed row per sentence
+struct FinalizeArgs {
+    const int32_t* fin_cnt;
+    const double* fin_score;
+    const int32_t* fin_step;
+    const int32_t* fin_slot;
+    const int32_t* fin_eos;
+    const int32_t* hist_tok;   // [S][T][B]
+    const int32_t* hist_par;
+    int32_t fin_cap, T, B;
+    int32_t* res;              // [n][res_stride]: len, logp (2 words), tokens
+    int32_t res_stride;
+    int32_t* scratch;          // [n][2][T + 2] when the history does not fit in shared memory
+    int32_t stage;             // set by finalize_launch
+};
+int finalize_launch(const FinalizeArgs& a, int n, cudaStream_t st);
+
 int search_step_launch(const SearchState& ss, int step, int n_sent, int beam, int k_list,
                        cudaStream_t st);
 // optional a_max/b_max: per-segment max |a_out| / |b_out| (segment = col_seg[n]) for the next step

@@ -10,13 +10,14 @@ search state), so results are identical to a sentence-by-sentence loop.
 from __future__ import annotations
 
 import math
+import threading
 from dataclasses import dataclass, field
 
 import numpy as np
 
 from .bleu import bleu
 from .errors import ConfigError, EmptyInputError, QnmtError
-from .engine import Engine, translate_ensemble_ids
+from .engine import engine_pool, translate_ensemble_ids
 from .model import EOS_ID, Float32Model, ModelParams, QuantizedModel, quantize_model, to_device_f32
 
 
@@ -24,7 +25,7 @@ from .model import EOS_ID, Float32Model, ModelParams, QuantizedModel, quantize_m
 class DecodeConfig:
     beam: int = 5
     max_ratio: float = 3.0        # max output length = ceil(ratio * source len) + 1
-    precision: str = "int8"       # "int8" (the B200 hot path) or "fp32"; the reference defaults to fp32
+    precision: str = "fp32"       # "fp32" or "int8" (the B200 hot path; bulk callers pass it)
 
     def __post_init__(self):
         if self.beam < 1:
@@ -70,49 +71,42 @@ def _members(models, precision: str = "int8") -> list:
     return [_quantized_cache(m) if isinstance(m, ModelParams) else m for m in members]
 
 
+_CACHE_LOCK = threading.Lock()
+
+
 def _quantized_cache(params: ModelParams) -> QuantizedModel:
     qm = getattr(params, "_b200_quantized", None)
     if qm is None:
-        qm = quantize_model(params)
-        params._b200_quantized = qm
+        with _CACHE_LOCK:   # concurrent translate() calls on one ModelParams quantize it once
+            qm = getattr(params, "_b200_quantized", None)
+            if qm is None:
+                qm = quantize_model(params)
+                params._b200_quantized = qm
     return qm
 
 
-def _engine_for(qm: QuantizedModel, n: int, length: int, beam: int, slot: int = 0, exact=None) -> Engine:
-    """The model's cached engine number ``slot`` (an ensemble that lists one model
-    twice needs two), grown to fit; ``exact`` forces one (S, L, B) capacity."""
-    pool = getattr(qm, "_engines", None)
-    if pool is None:
-        pool = qm._engines = []
-    while len(pool) <= slot:
-        pool.append(None)
-    e = pool[slot]
-    if exact is not None:
-        ok = e is not None and (e.max_sentences, e.max_len, e.max_beam) == exact
-        cap = exact
-    else:
-        ok = e is not None and e.fits(n, length, beam)
-        cap = (max(n, e.max_sentences if e else 0), max(length, 128, e.max_len if e else 0),
-               max(beam, e.max_beam if e else 0))
-    if not ok:
-        if e is not None:
-            e.close()
-        e = Engine(qm, *cap)
-        pool[slot] = e
-    return e
-
-
-def _engines_for(members, n: int, length: int, beam: int) -> list:
-    """One engine per ensemble member, all with the same capacity."""
-    slots, seen = [], {}
+def _acquire(members, n: int, length: int, beam: int) -> list:
+    """Check out one engine per member (a model listed twice gets two); an
+    ensemble's engines share one capacity.  Release with :func:`_release`."""
+    if len(members) == 1:
+        return [engine_pool(members[0]).acquire(members[0], n, length, beam)]
+    cap = (n, max(length, 128), beam)
     for m in members:
-        slots.append(seen.get(id(m), 0))
-        seen[id(m)] = slots[-1] + 1
-    cur = [getattr(m, "_engines", [None] * (s + 1))[s] if len(getattr(m, "_engines", [])) > s else None
-           for m, s in zip(members, slots)]
-    cap = (max([n] + [e.max_sentences for e in cur if e]), max([length, 128] + [e.max_len for e in cur if e]),
-           max([beam] + [e.max_beam for e in cur if e]))
-    return [_engine_for(m, n, length, beam, s, exact=cap) for m, s in zip(members, slots)]
+        c = engine_pool(m).capacity(n, length, beam)
+        cap = tuple(max(a, b) for a, b in zip(cap, c))
+    got = []
+    try:
+        for m in members:
+            got.append(engine_pool(m).acquire(m, n, length, beam, exact=cap))
+    except BaseException:
+        _release(members, got)
+        raise
+    return got
+
+
+def _release(members, engines):
+    for m, e in zip(members, engines):
+        engine_pool(m).release(e)
 
 
 def _check_cfg(cfg: DecodeConfig):
@@ -133,7 +127,25 @@ def _side_streams(k: int) -> list:
     return lst[:k]
 
 
-def _decode_ids(members, per_member_ids, cfg: DecodeConfig, max_batch: int, streams: int = 1, sort: bool = False):
+# engine phase groups (csrc/engine.cu PG_*) -> reference phase names (bench.py:23-24)
+GROUP_TO_PHASE = {"quantize-activations": "quantize-activations", "matmul": "matmul", "matmul-vocab": "matmul",
+                  "gru": "transcendental", "attention": "transcendental", "embedding": "embedding",
+                  "topk": "search-overhead", "search": "search-overhead", "gather": "search-overhead",
+                  "encoder": "encoder", "other": "other"}
+
+
+def _charge_timer(timer, phases: dict):
+    """Add device-measured phase seconds to a reference PhaseTimer (its
+    ``seconds`` dict, bench.py:27-57)."""
+    sec = getattr(timer, "seconds", None)
+    if not isinstance(sec, dict):
+        raise ConfigError("timer must be a PhaseTimer (an object with a 'seconds' dict)")
+    for k, v in phases.items():
+        sec[k] = sec.get(k, 0.0) + v
+
+
+def _decode_ids(members, per_member_ids, cfg: DecodeConfig, max_batch: int, streams: int = 1, sort: bool = False,
+                phases: dict = None):
     """Batched device decode of id lists (one list per member).  Returns [(ids, logp)]
     in input order.
 
@@ -146,7 +158,11 @@ def _decode_ids(members, per_member_ids, cfg: DecodeConfig, max_batch: int, stre
     launches) and its small latency-bound kernels overlap the other engines'
     device work.  Every sentence is still decoded exactly as decoder.translate
     would (results do not depend on batching).  The queue hands out the longest
-    batches first."""
+    batches first.
+
+    ``phases`` (a dict): the decode runs with the engine's device phase
+    profiler (eager steps, CUDA events per phase group, one stream) and adds
+    {reference phase name: seconds} into it."""
     n_all = len(per_member_ids[0])
     order = sorted(range(n_all), key=lambda i: (len(per_member_ids[0][i]), i)) if sort else list(range(n_all))
     batches = [order[b0:b0 + max_batch] for b0 in range(0, n_all, max_batch)]
@@ -159,21 +175,52 @@ def _decode_ids(members, per_member_ids, cfg: DecodeConfig, max_batch: int, stre
             out[i] = (t, lp)
 
     if len(members) > 1:
-        engines = _engines_for(members, nb, max_len, cfg.beam)
-        for idx in batches:
-            put(idx, *translate_ensemble_ids(engines, [[ids[i] for i in idx] for ids in per_member_ids],
-                                             cfg.beam, cfg.max_ratio))
+        engines = _acquire(members, nb, max_len, cfg.beam)
+        try:
+            for idx in batches:
+                put(idx, *translate_ensemble_ids(engines, [[ids[i] for i in idx] for ids in per_member_ids],
+                                                 cfg.beam, cfg.max_ratio))
+        finally:
+            _release(members, engines)
         return out
     ids0 = per_member_ids[0]
     k = max(1, min(streams, len(batches)))
-    engines = [_engine_for(members[0], nb, max_len, cfg.beam, slot=j) for j in range(k)]
-    if k == 1:
-        for idx in batches:
-            put(idx, *engines[0].translate_ids([ids0[i] for i in idx], cfg.beam, cfg.max_ratio))
-        return out
-    import threading
+    pool = engine_pool(members[0])
+    engines = []
+    try:
+        if phases is not None:
+            k = 1
+        for _ in range(k):
+            engines.append(pool.acquire(members[0], nb, max_len, cfg.beam))
+        if phases is not None:
+            e = engines[0]
+            e.profile(True)
+            try:
+                for idx in batches:
+                    put(idx, *e.translate_ids([ids0[i] for i in idx], cfg.beam, cfg.max_ratio))
+                groups = e.profile_read()
+            finally:
+                e.profile(False)
+            for g, ms in groups.items():
+                ph = GROUP_TO_PHASE.get(g, "other")
+                phases[ph] = phases.get(ph, 0.0) + ms * 1e-3
+            return out
+        if k == 1:
+            for idx in batches:
+                put(idx, *engines[0].translate_ids([ids0[i] for i in idx], cfg.beam, cfg.max_ratio))
+            return out
+        _run_streams(engines, batches, ids0, cfg, put)
+    finally:
+        for e in engines:
+            pool.release(e)
+    return out
 
+
+def _run_streams(engines, batches, ids0, cfg, put):
+    """Engines on their own CUDA streams and host threads take batches from a
+    shared queue (see _decode_ids)."""
     import torch
+    k = len(engines)
     # longest batches first (LPT): the engines drain the short ones together at the end
     # instead of one engine finishing the longest batch alone
     queue = sorted(range(len(batches)), key=lambda b: (-max(len(ids0[i]) for i in batches[b]), b))
@@ -206,7 +253,6 @@ def _decode_ids(members, per_member_ids, cfg: DecodeConfig, max_batch: int, stre
         main.wait_stream(s)
     if errors:
         raise errors[0]
-    return out
 
 
 def translate(models, source_tokens, cfg: DecodeConfig, timer=None):
@@ -214,14 +260,23 @@ def translate(models, source_tokens, cfg: DecodeConfig, timer=None):
 
     Returns ``(target_tokens, log_prob)``: the token list excludes the final
     EOS; the score is the plain sum of per-step log-probs (ensemble members
-    contribute the arithmetic mean of their log-probs per step)."""
+    contribute the arithmetic mean of their log-probs per step).
+
+    ``timer`` (a reference PhaseTimer): the decode runs with the engine's
+    device phase profiler and the measured seconds are added to the timer's
+    phases (device time per phase group instead of host wall-clock spans)."""
     tokens = list(source_tokens)
     if not tokens:
         raise EmptyInputError("cannot translate an empty sentence")
     _check_cfg(cfg)
     members = _members(models, cfg.precision)
     ids = [[m.src_ids(tokens)] for m in members]
-    out, lp = _decode_ids(members, ids, cfg, 1)[0]
+    phases = {} if timer is not None and len(members) == 1 else None
+    if timer is not None and phases is None:
+        raise ConfigError("phase timing of ensemble decodes is not supported")
+    out, lp = _decode_ids(members, ids, cfg, 1, phases=phases)[0]
+    if timer is not None:
+        _charge_timer(timer, phases)
     return [members[0].tgt_tokens[i] for i in out], lp
 
 
@@ -315,8 +370,21 @@ def compare_precisions(model: ModelParams, sentences, cfg: DecodeConfig, max_bat
             raise EmptyInputError(f"sentence {i}: cannot translate an empty sentence")
     if not isinstance(model, ModelParams):
         raise ConfigError("compare_precisions needs float parameters")
-    out32 = translate_batch(model, sents, DecodeConfig(cfg.beam, cfg.max_ratio, "fp32"), max_batch)
-    out8 = translate_batch(model, sents, DecodeConfig(cfg.beam, cfg.max_ratio, "int8"), max_batch)
+    cfg32 = DecodeConfig(cfg.beam, cfg.max_ratio, "fp32")
+    cfg8 = DecodeConfig(cfg.beam, cfg.max_ratio, "int8")
+    try:
+        out32 = translate_batch(model, sents, cfg32, max_batch)
+        out8 = translate_batch(model, sents, cfg8, max_batch)
+    except QnmtError:
+        # a batch failed: find the sentence as the reference's per-sentence loop would
+        # and name it (decoder.py:227-232)
+        for i, s in enumerate(sents):
+            try:
+                translate(model, s, cfg32)
+                translate(model, s, cfg8)
+            except QnmtError as exc:
+                raise type(exc)(f"sentence {i}: {exc}") from exc
+        raise
     d = [edit_distance(a[0], b[0]) for a, b in zip(out32, out8)]
     same = sum(a[0] == b[0] for a, b in zip(out32, out8))
     f32_txt = [bpe_merge(a[0]) for a in out32]

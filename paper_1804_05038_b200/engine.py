@@ -5,6 +5,7 @@ from __future__ import annotations
 
 import ctypes as C
 import math
+import threading
 
 import numpy as np
 import torch
@@ -118,9 +119,9 @@ class Engine:
         _lib.call("qnmt_translate_batch", self._h, ids.ctypes.data, lens.ctypes.data, n, beam,
                   float(max_ratio), out_tok.ctypes.data, stride, out_len.ctypes.data,
                   out_lp.ctypes.data, _dev.stream_ptr())
-        # ids + per-sentence metadata (row, len, max_steps, P, col_off, col_sent, y, live) + encoder row maps
-        self.h2d_bytes += ids.nbytes + n * 40 + 2 * 2 * n * int(lens.max()) * 4 + ids.nbytes + n * 4
-        self.d2h_bytes += int(_lib.load().qnmt_last_d2h_bytes(self._h))
+        lib = _lib.load()   # byte counts of the copies the C engine issued for this batch
+        self.h2d_bytes += int(lib.qnmt_last_h2d_bytes(self._h))
+        self.d2h_bytes += int(lib.qnmt_last_d2h_bytes(self._h))
         toks = [out_tok[i, :out_len[i]].tolist() for i in range(n)]
         return toks, out_lp.tolist()
 
@@ -149,3 +150,77 @@ def translate_ensemble_ids(engines, id_lists_per_member, beam: int, max_ratio: f
               float(max_ratio), out_tok.ctypes.data, stride, out_len.ctypes.data, out_lp.ctypes.data,
               _dev.stream_ptr())
     return [out_tok[i, :out_len[i]].tolist() for i in range(n)], out_lp.tolist()
+
+
+_POOL_LOCK = threading.Lock()
+
+
+class EnginePool:
+    """The engines of one device model, handed to one caller at a time.
+
+    The reference's API is safe to call concurrently (bench.py:129-132 and
+    cli.py:58-63 run ``translate`` from a thread pool on one model).  An engine
+    owns device scratch, pinned staging and the search history of the batch it
+    is decoding, so two threads must never share one: :meth:`acquire` checks an
+    idle engine out (or creates one) under a lock and :meth:`release` returns
+    it.  Engines are only closed while idle, so a decode in flight never loses
+    its engine; an engine that is outgrown is closed when a larger one is made."""
+
+    def __init__(self):
+        self._lock = threading.Lock()
+        self._idle: list = []
+        self.all: list = []       # every live engine (per-engine traffic counters)
+
+    def _cap(self, n, length, beam):
+        big = self.all
+        return (max([n] + [e.max_sentences for e in big]), max([length, 128] + [e.max_len for e in big]),
+                max([beam] + [e.max_beam for e in big]))
+
+    def capacity(self, n, length, beam):
+        """The capacity a new engine for (n, length, beam) gets: at least every existing engine's."""
+        with self._lock:
+            return self._cap(n, length, beam)
+
+    def acquire(self, qmodel, n: int, length: int, beam: int, exact=None) -> Engine:
+        with self._lock:
+            for i, e in enumerate(self._idle):
+                ok = ((e.max_sentences, e.max_len, e.max_beam) == tuple(exact)) if exact else e.fits(n, length, beam)
+                if ok:
+                    return self._idle.pop(i)
+            cap = tuple(exact) if exact else self._cap(n, length, beam)
+            # idle engines that the new one covers are closed (bounded device memory)
+            keep = []
+            for e in self._idle:
+                if e.max_sentences <= cap[0] and e.max_len <= cap[1] and e.max_beam <= cap[2]:
+                    e.close()
+                    self.all.remove(e)
+                else:
+                    keep.append(e)
+            self._idle = keep
+            e = Engine(qmodel, *cap)
+            self.all.append(e)
+            return e
+
+    def release(self, e: Engine):
+        with self._lock:
+            if e._h is not None:
+                self._idle.append(e)
+
+    def close(self):
+        with self._lock:
+            for e in self._idle:
+                e.close()
+            self.all = [e for e in self.all if e not in self._idle]
+            self._idle = []
+
+
+def engine_pool(qmodel) -> EnginePool:
+    """The model's engine pool (created once, thread-safe)."""
+    pool = getattr(qmodel, "_engine_pool", None)
+    if pool is None:
+        with _POOL_LOCK:
+            pool = getattr(qmodel, "_engine_pool", None)
+            if pool is None:
+                pool = EnginePool()
+                qmodel._engine_pool = pool
+    return pool

@@ -18,13 +18,14 @@ fp64 and rounded once (the Tier-B contract of gemm_f32).
 
 from __future__ import annotations
 
+import contextlib
 from dataclasses import dataclass
 
 import numpy as np
 import torch
 
 from . import _dev, _lib
-from .engine import Engine
+from .engine import engine_pool
 from .errors import ConfigError, ShapeError, VocabError, EmptyInputError
 from .qmath import QuantizedMatrix, gemm_f32_kmajor, gemm_kmajor
 
@@ -406,19 +407,21 @@ class Network:
         self.precision = precision
         self.src_ids = src_ids_fn
         self.tgt_tokens = tgt_tokens
-        self._engine = None
 
-    def engine(self, n=1, length=1, beam=1) -> Engine:
-        e = self._engine
-        if e is None or not e.fits(n, length, beam):
-            cap_len = max(length, 128, e.max_len if e else 0)
-            cap_beam = max(beam, 8, e.max_beam if e else 0)
-            cap_n = max(n, e.max_sentences if e else 1)
-            if e is not None:
-                e.close()
-            e = Engine(self.qmodel, cap_n, cap_len, min(cap_beam, 16))
-            self._engine = e
-        return e
+    @contextlib.contextmanager
+    def engine(self, n=1, length=1, beam=1):
+        """An engine of the model's pool, checked out for one call (networks are
+        shared between threads, layers.py:285-290); the stream is synchronised
+        before the engine goes back, so its scratch is free for the next caller."""
+        pool = engine_pool(self.qmodel)
+        e = pool.acquire(self.qmodel, n, length, min(max(beam, 8), 16))
+        try:
+            yield e
+        finally:
+            try:
+                torch.cuda.current_stream().synchronize()
+            finally:
+                pool.release(e)
 
     def encode(self, src_ids, timer=None) -> EncoderStates:
         ids = np.asarray(src_ids, dtype=np.int64)
@@ -426,7 +429,8 @@ class Network:
             raise EmptyInputError("cannot encode an empty sentence")
         if ids.min() < 0 or ids.max() >= self.dims.src_vocab:
             raise VocabError(f"source id outside [0, {self.dims.src_vocab})")
-        states, att, s0, _, _ = self.engine(1, ids.size, 1).encode_batch([ids])
+        with self.engine(1, ids.size, 1) as e:
+            states, att, s0, _, _ = e.encode_batch([ids])
         enc = EncoderStates(states, att, s0, _kmajor=True)
         enc._numpy = True
         return enc
@@ -446,13 +450,13 @@ class Network:
         if ids.min() < 0 or ids.max() >= self.dims.tgt_vocab:
             raise VocabError(f"target id outside [0, {self.dims.tgt_vocab})")
         P = ids.size
-        e = self.engine(1, enc.length, P)
         s_k, sp_k = _dev.kmajor(state.s), _dev.kmajor(state.s_prime)
         dev = s_k.device
         y = torch.from_numpy(ids.astype(np.int32)).to(dev)
         sent_row, sent_len, col_sent = _one_sentence_meta(enc.length, P, dev)
-        logits, s_int, s_new, alpha = e.decoder_step(y, s_k, sp_k, enc.states_k, enc.att_proj_k,
-                                                     sent_row, sent_len, col_sent)
+        with self.engine(1, enc.length, P) as e:
+            logits, s_int, s_new, alpha = e.decoder_step(y, s_k, sp_k, enc.states_k, enc.att_proj_k,
+                                                         sent_row, sent_len, col_sent)
         lp = torch.empty_like(logits)
         f = _dev.reset_flag()
         _lib.call("qnmt_log_softmax", logits.data_ptr(), P, logits.shape[1], _dev.ld(logits),

@@ -476,8 +476,209 @@ def gen_modelfile():
     print("model_tiny.qnmt:", len(blob), "bytes;", len(verdicts["cases"]), "corruption verdicts")
 
 
+
+# ---------------------------------------------------------------------------
+# 4. BASELINE configs: Tier-A teacher-forced ops at full dims, the cfg4 corpus,
+#    a cfg5 sample, and the Tier-A vs Tier-B agreement report
+# ---------------------------------------------------------------------------
+
+CFG5_DIMS = dict(BASE_DIMS, tgt_vocab=50000)
+
+
+def _decode_many(qm, corpora, cfg, threads=8):
+    """The reference's translate() over many sentences (one per thread, as the
+    reference's own bench.py:129-132 does): [(ids, logp)]."""
+    from concurrent.futures import ThreadPoolExecutor
+    idx = {t: i for i, t in enumerate(qm.tgt_tokens)}
+
+    def one(toks):
+        words, lp = translate(qm, toks, cfg)
+        return [idx[w] for w in words], lp
+
+    with ThreadPoolExecutor(threads) as pool:
+        return list(pool.map(one, corpora))
+
+
+def _trace_search(net, toks, beam, ratio):
+    """decoder.py:88-160 for one model, recording each step's chosen candidates
+    {token path: score} and every candidate's score by path (for the first step
+    at which two tiers' selections differ).  Returns (steps, final ids, logp)."""
+    from qnmt.decoder import _select_candidates
+    ids = net.src_ids(toks)
+    enc = net.encode(ids)
+    V = net.dims.tgt_vocab
+    max_steps = int(np.ceil(ratio * len(toks))) + 1
+    live = [()]
+    scores = np.zeros(1, F64)
+    st = net.initial_state(enc, 1)
+    y = np.array([2], np.int64)
+    fin = []
+    steps = []
+    for _ in range(max_steps):
+        lp, st2, _ = net.decoder_step(y, st, enc)
+        flat = (scores[:, None] + lp.T.astype(F64)).ravel()
+        chosen = _select_candidates(flat, beam, V)
+        top = np.argsort(-flat, kind="stable")[:4 * beam]
+        steps.append({"chosen": {live[f // V] + (f % V,): float(flat[f]) for f in chosen},
+                      "cand": {live[f // V] + (f % V,): float(flat[f]) for f in top}})
+        nl, ns, npar, ny = [], [], [], []
+        for f in chosen:
+            par, tok = divmod(f, V)
+            if tok == 2:
+                fin.append((live[par] + (tok,), float(flat[f])))
+            else:
+                nl.append(live[par] + (tok,)); ns.append(float(flat[f])); npar.append(par); ny.append(tok)
+        if not nl:
+            break
+        live, scores = nl, np.array(ns, F64)
+        st = st2.select(np.array(npar, np.int64))
+        y = np.array(ny, np.int64)
+        if fin and max(h[1] for h in fin) >= scores.max():
+            break
+    else:
+        fin += [(p, float(s)) for p, s in zip(live, scores)]
+    best = min(fin, key=lambda h: (-h[1], list(h[0])))
+    out = list(best[0][:-1]) if best[0] and best[0][-1] == 2 else list(best[0])
+    return steps, out, best[1]
+
+
+def _divergence(net, toks, beam, ratio):
+    """First step where Tier A and Tier B select different candidates, with the
+    score gap (under each tier) between the candidates that swapped places."""
+    ta, outa, lpa = _trace_search(net, toks, beam, ratio)
+    with tier_b():
+        tb, outb, lpb = _trace_search(net, toks, beam, ratio)
+    for t, (sa, sb) in enumerate(zip(ta, tb)):
+        ka, kb = set(sa["chosen"]), set(sb["chosen"])
+        if ka == kb:
+            continue
+        only_a, only_b = sorted(ka - kb), sorted(kb - ka)
+        # under tier B: best B-only pick vs the A-only pick B ranked highest (and vice versa)
+        gap_b = min(sb["chosen"][p] for p in only_b) - max(sb["cand"].get(p, -np.inf) for p in only_a)
+        gap_a = min(sa["chosen"][p] for p in only_a) - max(sa["cand"].get(p, -np.inf) for p in only_b)
+        shared = [p for p in sa["cand"] if p in sb["cand"]]
+        disc = max(abs(sa["cand"][p] - sb["cand"][p]) for p in shared) if shared else float("nan")
+        return {"step": t, "gap_B": float(gap_b), "gap_A": float(gap_a), "tier_discrepancy": float(disc),
+                "score_at_step": float(max(sb["chosen"].values())), "out_A": outa, "out_B": outb,
+                "logp_A": lpa, "logp_B": lpb}
+    return {"step": None, "out_A": outa, "out_B": outb, "logp_A": lpa, "logp_B": lpb}
+
+
+def _first_diff(a, b):
+    for i, (x, y) in enumerate(zip(a, b)):
+        if x != y:
+            return i
+    return None if len(a) == len(b) else min(len(a), len(b))
+
+
+def gen_baseline_parity():
+    """cfg3/cfg4/cfg5 outputs of the reference in both tiers, Tier-A op outputs at
+    BASELINE dims on fixed inputs, and the agreement report (tier_agreement.json)."""
+    out = {}
+    report = {"note": "Tier A = unmodified reference, Tier B = reference with its five elementwise functions in "
+                      "fp64 rounded once (the GPU contract). For each sentence whose outputs differ: the first "
+                      "decode step at which the two tiers select different candidates, and the score gap between "
+                      "the swapped candidates under each tier.",
+              "configs": {}}
+    dims = ref_model.Dims(**BASE_DIMS)
+    params, _ = make_params(dims, 1804)
+    qm = ref_model.quantize_model(params)
+    net = ref_layers.build_network(qm)
+    rng = np.random.default_rng(5038)
+    src50 = rng.integers(3, 32000, 50)
+    # -- Tier A (and B) teacher-forced ops at full dims, l = 20, P = 3 ------------
+    src20 = src50[:20]
+    enc_a = net.encode(src20)
+    out["tf_src"] = src20
+    out["tf_states"], out["tf_att_proj"], out["tf_s0"] = enc_a.states, enc_a.att_proj, enc_a.s0
+    r = np.random.default_rng(77)
+    s = (np.repeat(enc_a.s0, 3, axis=1) + r.normal(0, 0.05, (1024, 3))).astype(F32)
+    sp = (s + r.normal(0, 0.05, (1024, 3))).astype(F32)
+    y = np.array([2, 77, 31999])
+    out["tf_s"], out["tf_sp"], out["tf_y"] = s, sp, y
+    x = r.normal(0, 1, (512, 3)).astype(F32)
+    xq = r.normal(0, 0.3, (2048, 3)).astype(F32)
+    h = r.normal(0, 0.5, (1024, 3)).astype(F32)
+    out["tf_x"], out["tf_xq"], out["tf_h"] = x, xq, h
+    encs = ref_layers.EncoderStates(states=enc_a.states, att_proj=enc_a.att_proj, s0=enc_a.s0)
+    for tier in ("A", "B"):
+        ctx = tier_b() if tier == "B" else contextlib.nullcontext()
+        with ctx:
+            lp, st2, alpha = net.decoder_step(y, ref_layers.DecoderState(s=s, s_prime=sp), encs)
+            out[f"tf{tier}_lp"] = lp
+            out[f"tf{tier}_snew"], out[f"tf{tier}_sint"], out[f"tf{tier}_alpha"] = st2.s, st2.s_prime, alpha
+            out[f"tf{tier}_gru_r"] = ref_layers.gru_step(net.dec_r, x, h)
+            out[f"tf{tier}_gru_q"] = ref_layers.gru_step(net.dec_q, xq, h)
+            c, a = ref_layers.attend(net.attention, h, encs)
+            out[f"tf{tier}_att_ctx"], out[f"tf{tier}_att_alpha"] = c, a
+    # -- cfg3 greedy 50 steps, Tier A ------------------------------------------------
+    toks50 = [params.src_tokens[i] for i in src50]
+    cfg3 = DecodeConfig(beam=1, max_ratio=0.98, precision="int8")
+    words, lpa = translate(qm, toks50, cfg3)
+    idx = {t: i for i, t in enumerate(params.tgt_tokens)}
+    out["A_greedy50"], out["A_greedy50_logp"] = np.array([idx[w] for w in words]), np.array(lpa, F64)
+    gold = np.load(os.path.join(HERE, "baseline_dims.npz"))
+    rep3 = {"sentences": 1, "beam": 1, "rows": []}
+    fd = _first_diff(list(out["A_greedy50"]), list(gold["B_greedy50"]))
+    rep3["rows"].append({"i": 0, "len": 50, "identical": fd is None, "first_token_diff": fd,
+                         "logp_A": float(lpa), "logp_B": float(gold["B_greedy50_logp"])})
+    report["configs"]["cfg3"] = rep3
+    # -- cfg4: 64 sentences, l ~ U[10, 80], beam 5, max_ratio 1.5, V = 32000 -----------
+    rng4 = np.random.default_rng(5042)
+    corpus4 = [rng4.integers(3, 32000, int(rng4.integers(10, 81))) for _ in range(64)]
+    toks4 = [[params.src_tokens[i] for i in c] for c in corpus4]
+    cfg4 = DecodeConfig(beam=5, max_ratio=1.5, precision="int8")
+    with tier_b():
+        res_b = _decode_many(qm, toks4, cfg4)
+    res_a = _decode_many(qm, toks4, cfg4)
+    cases4 = []
+    for i, (c, rb, ra) in enumerate(zip(corpus4, res_b, res_a)):
+        cases4.append({"src": c.tolist(), "out_B": rb[0], "logp_B": rb[1], "out_A": ra[0], "logp_A": ra[1]})
+    report["configs"]["cfg4"] = _agreement(net, params, corpus4, res_a, res_b, 5, 1.5)
+    # -- cfg5 sample: 16 sentences of the bench corpus (l ~ U[5, 100]), V = 50000 ------
+    dims5 = ref_model.Dims(**CFG5_DIMS)
+    params5, _ = make_params(dims5, 1804)
+    qm5 = ref_model.quantize_model(params5)
+    net5 = ref_layers.build_network(qm5)
+    r5 = np.random.default_rng(5038)
+    lens5 = r5.integers(5, 101, 8192)
+    corpus5_all = [r5.integers(3, 32000, int(n)) for n in lens5]
+    order = sorted(range(8192), key=lambda i: (len(corpus5_all[i]), i))
+    pick = [order[(2 * k + 1) * 8192 // 32] for k in range(16)]
+    corpus5 = [corpus5_all[i] for i in pick]
+    toks5 = [[params5.src_tokens[i] for i in c] for c in corpus5]
+    with tier_b():
+        res5_b = _decode_many(qm5, toks5, cfg4)
+    res5_a = _decode_many(qm5, toks5, cfg4)
+    cases5 = [{"corpus_index": int(i), "src": c.tolist(), "out_B": rb[0], "logp_B": rb[1], "out_A": ra[0],
+               "logp_A": ra[1]} for i, c, rb, ra in zip(pick, corpus5, res5_b, res5_a)]
+    report["configs"]["cfg5"] = _agreement(net5, params5, corpus5, res5_a, res5_b, 5, 1.5)
+    np.savez_compressed(os.path.join(HERE, "baseline_parity.npz"), **out)
+    with open(os.path.join(HERE, "baseline_corpora.json"), "w") as fh:
+        json.dump({"cfg4": {"seed": 5042, "beam": 5, "max_ratio": 1.5, "model_seed": 1804, "dims": BASE_DIMS,
+                            "cases": cases4},
+                   "cfg5": {"corpus_seed": 5038, "beam": 5, "max_ratio": 1.5, "model_seed": 1804, "dims": CFG5_DIMS,
+                            "cases": cases5}}, fh)
+    with open(os.path.join(HERE, "tier_agreement.json"), "w") as fh:
+        json.dump(report, fh, indent=1)
+    print("baseline_parity.npz:", len(out), "arrays; cfg4", len(cases4), "cfg5", len(cases5), "sentences")
+
+
+def _agreement(net, params, corpus, res_a, res_b, beam, ratio):
+    rows = []
+    for i, (c, ra, rb) in enumerate(zip(corpus, res_a, res_b)):
+        row = {"i": i, "len": len(c), "identical": ra[0] == rb[0], "first_token_diff": _first_diff(ra[0], rb[0]),
+               "logp_A": ra[1], "logp_B": rb[1]}
+        if not row["identical"]:
+            d = _divergence(net, [params.src_tokens[j] for j in c], beam, ratio)
+            assert d["out_A"] == ra[0] and d["out_B"] == rb[0], "traced search != translate()"
+            row.update({k: d[k] for k in ("step", "gap_B", "gap_A", "tier_discrepancy", "score_at_step")})
+        rows.append(row)
+    same = sum(r["identical"] for r in rows)
+    return {"sentences": len(rows), "identical": same, "beam": beam, "max_ratio": ratio, "rows": rows}
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["qmath", "small", "baseline", "modelfile", "ensemble", "fp32"]
+    which = sys.argv[1:] or ["qmath", "small", "baseline", "modelfile", "ensemble", "fp32", "parity"]
     if "fp32" in which:
         gen_fp32()
     if "ensemble" in which:
@@ -490,3 +691,5 @@ if __name__ == "__main__":
         gen_small()
     if "baseline" in which:
         gen_baseline()
+    if "parity" in which:
+        gen_baseline_parity()

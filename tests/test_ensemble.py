@@ -74,7 +74,7 @@ def test_gpu_ensembles_match_reference(gold):
             ms.append(cache[key])
         models[tag] = ms
     for c in gold["cases"]:
-        words, lp = pb.translate(models[c["ensemble"]], c["src_tokens"], pb.DecodeConfig(c["beam"], c["max_ratio"]))
+        words, lp = pb.translate(models[c["ensemble"]], c["src_tokens"], pb.DecodeConfig(c["beam"], c["max_ratio"], "int8"))
         ids = [int(w[1:]) + 2 if w.startswith("w") else {"<pad>": 0, "<unk>": 1, "</s>": 2}[w] for w in words]
         assert ids == c["out_B"], c
         assert lp == c["logp_B"], c
@@ -92,7 +92,7 @@ def test_gpu_ensemble_batch_equals_oracle():
     oms = [O.QModel(O.Dims(**d.as_dict()), p.tensors) for p in ps]
     rng = np.random.default_rng(9)
     srcs = [rng.integers(3, 300, int(rng.integers(1, 20))).tolist() for _ in range(24)]
-    got = pb.translate_batch(qms, srcs, pb.DecodeConfig(beam=4, max_ratio=1.5), max_batch=16, return_ids=True)
+    got = pb.translate_batch(qms, srcs, pb.DecodeConfig(beam=4, max_ratio=1.5, precision="int8"), max_batch=16, return_ids=True)
     for s, g in zip(srcs, got):
         want = O.translate_ensemble(oms, [s, s], 4, 1.5)
         assert g[0] == want[0] and g[1] == want[1], s

@@ -43,7 +43,7 @@ def test_batch_equals_sentence_by_sentence(tag, beam):
     qm, om, params = qmodel(tr["models"][tag], tag)
     rng = np.random.default_rng(beam * 31 + len(tag))
     sents = [rng.integers(3, params.dims.src_vocab, int(rng.integers(1, 14))).tolist() for _ in range(23)]
-    cfg = pb.DecodeConfig(beam=beam, max_ratio=1.5)
+    cfg = pb.DecodeConfig(beam=beam, max_ratio=1.5, precision="int8")
     got = pb.translate_batch(qm, sents, cfg, max_batch=16, return_ids=True)
     for s, (toks, lp) in zip(sents, got):
         et, elp = om.translate(s, beam, 1.5)
@@ -54,11 +54,11 @@ def test_errors():
     tr = translate_specs()
     qm, _, params = qmodel(tr["models"]["small"], "small")
     with pytest.raises(pb.errors.EmptyInputError):
-        pb.translate(qm, [], pb.DecodeConfig())
+        pb.translate(qm, [], pb.DecodeConfig(precision="int8"))
     with pytest.raises(pb.errors.ConfigError):
         pb.translate(qm, ["w0001"], pb.DecodeConfig(precision="fp32"))
     # unknown source tokens map to UNK (model.py:110-115) and decode fine
-    words, lp = pb.translate(qm, ["nope", "w0003"], pb.DecodeConfig(beam=2))
+    words, lp = pb.translate(qm, ["nope", "w0003"], pb.DecodeConfig(beam=2, precision="int8"))
     assert isinstance(words, list) and math.isfinite(lp)
 
 
@@ -89,7 +89,7 @@ def test_cfg3_greedy_bit_exact(base):
     """BASELINE cfg3: encoder + 50 greedy steps, V = 32000 (latency path)."""
     params, qm, g = base
     toks = [params.src_tokens[i] for i in g["src50"]]
-    words, logp = pb.translate(qm, toks, pb.DecodeConfig(beam=1, max_ratio=0.98))
+    words, logp = pb.translate(qm, toks, pb.DecodeConfig(beam=1, max_ratio=0.98, precision="int8"))
     idx = {t: i for i, t in enumerate(params.tgt_tokens)}
     assert [idx[w] for w in words] == g["B_greedy50"].tolist()
     assert logp == float(g["B_greedy50_logp"])
@@ -103,7 +103,7 @@ def test_cfg3_greedy_bit_exact(base):
 def test_beam5_baseline_dims(base):
     params, qm, g = base
     toks = [params.src_tokens[i] for i in g["B_beam5_src"]]
-    words, logp = pb.translate(qm, toks, pb.DecodeConfig(beam=5, max_ratio=1.5))
+    words, logp = pb.translate(qm, toks, pb.DecodeConfig(beam=5, max_ratio=1.5, precision="int8"))
     idx = {t: i for i, t in enumerate(params.tgt_tokens)}
     assert [idx[w] for w in words] == g["B_beam5"].tolist()
     assert logp == float(g["B_beam5_logp"])
@@ -320,9 +320,9 @@ def test_gpu_persistent_greedy_matches_oracle_and_step_graphs():
             src = rng.integers(3, 300, 1 if k == 0 else int(rng.integers(1, 30))).tolist()
             ratio = float(rng.choice([0.5, 1.5, 3.0]))
             old = lib.qnmt_set_greedy1(1)
-            got = pb.translate_batch(qm, [src], pb.DecodeConfig(1, ratio), return_ids=True)[0]
+            got = pb.translate_batch(qm, [src], pb.DecodeConfig(1, ratio, "int8"), return_ids=True)[0]
             lib.qnmt_set_greedy1(0)
-            ref = pb.translate_batch(qm, [src], pb.DecodeConfig(1, ratio), return_ids=True)[0]
+            ref = pb.translate_batch(qm, [src], pb.DecodeConfig(1, ratio, "int8"), return_ids=True)[0]
             lib.qnmt_set_greedy1(old)
             want = om.translate(src, 1, ratio)
             assert got[0] == want[0] and got[1] == want[1], (seed, src)

@@ -103,7 +103,7 @@ def test_load_quantized_translates_like_the_oracle(tmp_path):
     qm = pb.load_quantized(str(p))
     om = O.QModel(O.Dims(**params.dims.as_dict()), params.tensors)
     srcs = [[5, 9, 17, 33, 40], [3, 4, 60, 11]]
-    got = pb.translate_batch(qm, srcs, pb.DecodeConfig(beam=3, max_ratio=2.0), return_ids=True)
+    got = pb.translate_batch(qm, srcs, pb.DecodeConfig(beam=3, max_ratio=2.0, precision="int8"), return_ids=True)
     for s, g in zip(srcs, got):
         want = om.translate(s, beam=3, max_ratio=2.0)
         assert g[0] == want[0] and g[1] == want[1]
