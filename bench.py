@@ -24,10 +24,11 @@ synthetic token ids (no datasets / checkpoints in this environment).
            by host events) of an untimed single-stream pass over the same shard
            right after the timed passes; algorithmic bytes / int-ops per launch
            from the live column count of each step.
-  --impl reference : the reference algorithm on the host CPU.  The reference is
-           a Python package that cannot travel to the GPU box, so this arm runs
-           the numpy port oracle/qnmt_oracle.py (pinned bit-exact against the
-           reference) with all host cores.
+  --impl reference : the unmodified reference package (pip-installed into
+           baseline/_ref, which travels to the GPU box) through its own
+           bench.run_benchmark on the host cores, on a bounded sample of the
+           corpus per step; the numpy port oracle/qnmt_oracle.py only if the
+           package cannot be imported there.
 """
 
 from __future__ import annotations
@@ -125,9 +126,59 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(rows)}
 
 
-def cpu_translate(params, sents, threads=None):
-    """Reference algorithm (oracle port, numpy) on host cores, one sentence per thread
-    (the reference's own bench.py:129-132 scheme)."""
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")   # the unmodified reference package (pip --target install)
+
+
+def load_reference():
+    """The reference package ``qnmt`` as installed into baseline/_ref (DESIGN.md
+    section 6): (module, None), or (None, reason) when it cannot be imported."""
+    os.environ.setdefault("NUMBA_CACHE_DIR", os.path.join(tempfile.gettempdir(), "qnmt_numba_cache"))
+    if not os.path.isdir(os.path.join(REF_DIR, "qnmt")):
+        return None, "baseline/_ref/qnmt not installed"
+    if REF_DIR not in sys.path:
+        sys.path.insert(0, REF_DIR)
+    try:
+        import qnmt
+        import qnmt.bench  # noqa: F401
+        import qnmt.qmath  # noqa: F401
+    except Exception as exc:   # noqa: BLE001
+        return None, f"import qnmt failed: {type(exc).__name__}: {exc}"
+    return qnmt, None
+
+
+def reference_model(qnmt, params):
+    """The reference's own int8 model (model.quantize_model) of the benchmark's
+    seeded weights, built through its ModelParams constructor (model.py:196-222)."""
+    from qnmt import model as rm
+    d = rm.Dims(**DIMS)
+    rp = rm._build_params(d, {k: np.asarray(v) for k, v in params.tensors.items()}, rm._synthetic_vocab(d.src_vocab),
+                          rm._synthetic_vocab(d.tgt_vocab), "transform", "current")
+    return rm.quantize_model(rp), rp
+
+
+def cpu_translate(ref, sents, threads=None):
+    """The reference's own decode on host cores: qnmt.decoder.translate, one
+    sentence per worker thread of a ThreadPoolExecutor -- the scheme of its
+    bench._decode_corpus (bench.py:107-132; the numba int8 kernels release the
+    GIL).  ``ref`` = (qnmt module, quantized model, float params).
+    Returns ([(ids, logp)], seconds, threads)."""
+    import concurrent.futures as cf
+    _, qm, rp = ref
+    from qnmt.decoder import DecodeConfig, translate
+    cores = min(threads or os.cpu_count() or 1, len(sents))
+    cfg = DecodeConfig(beam=BEAM, max_ratio=MAX_RATIO, precision="int8")
+    toks = [[rp.src_tokens[i] for i in s] for s in sents]
+    idx = {t: i for i, t in enumerate(rp.tgt_tokens)}
+    t0 = time.perf_counter()
+    with cf.ThreadPoolExecutor(max_workers=cores) as pool:
+        outs = list(pool.map(lambda t: translate(qm, t, cfg), toks))
+    dt = time.perf_counter() - t0
+    return [([idx[w] for w in words], lp) for words, lp in outs], dt, cores
+
+
+def cpu_translate_port(params, sents, threads=None):
+    """Fallback when the reference cannot be imported: the numpy port
+    oracle/qnmt_oracle.py (pinned to the reference's Tier-B goldens)."""
     import concurrent.futures as cf
 
     from oracle import qnmt_oracle as O
@@ -139,7 +190,18 @@ def cpu_translate(params, sents, threads=None):
     return outs, time.perf_counter() - t0, cores
 
 
+def host_desc(qnmt=None):
+    vnni = None
+    if qnmt is not None:
+        vnni = bool(getattr(qnmt.qmath, "HAVE_VNNI", False))
+    return {"host_threads": os.cpu_count(), "avx512_vnni": vnni}
+
+
 def run_reference(args, rank, world):
+    """--impl reference: the unmodified reference package (baseline/_ref) through
+    its own public API (quantize_model + translate on a thread pool, the VNNI
+    numba int8 path when the host CPU has it) with all host threads, on a
+    bounded sample of the cfg5 corpus per step (rank 0 only)."""
     if rank != 0:
         return
     import paper_1804_05038_b200 as pb   # host-side synthetic model recipe only (numpy)
@@ -147,23 +209,41 @@ def run_reference(args, rank, world):
     sents = corpus()
     sample = args.cpu_sample
     idx = cpu_sample(sents, sample)
-    short = min(range(len(sents)), key=lambda i: len(sents[i]))
-    for w in range(args.warmup):
-        cpu_translate(params, [sents[short]])
-    secs, toks, cores = 0.0, 0, 1
-    for k in range(args.steps):
-        outs, dt, cores = cpu_translate(params, [sents[i] for i in idx])
-        toks += sum(len(o[0]) for o in outs)
-        secs += dt
+    qnmt, why = load_reference()
+    secs, toks = 0.0, 0
+    if qnmt is not None:
+        ref = (qnmt,) + reference_model(qnmt, params)
+        short = min(range(len(sents)), key=lambda i: len(sents[i]))
+        for _ in range(args.warmup):   # numba JIT / weight shadows (the reference's own warm-up pass)
+            cpu_translate(ref, [sents[short]])
+        cores = 1
+        for _ in range(args.steps):
+            outs, dt, cores = cpu_translate(ref, [sents[i] for i in idx])
+            toks += sum(len(o[0]) for o in outs)
+            secs += dt
+        kind = "reference"
+        what = (f"qnmt (unmodified, baseline/_ref) decoder.translate, one sentence per worker thread "
+                f"(bench._decode_corpus scheme), {cores} threads, VNNI={bool(qnmt.qmath.HAVE_VNNI)}")
+    else:
+        short = min(range(len(sents)), key=lambda i: len(sents[i]))
+        for _ in range(args.warmup):
+            cpu_translate_port(params, [sents[short]])
+        cores = 1
+        for _ in range(args.steps):
+            outs, dt, cores = cpu_translate_port(params, [sents[i] for i in idx])
+            toks += sum(len(o[0]) for o in outs)
+            secs += dt
+        kind = "port"
+        what = f"oracle/qnmt_oracle.py numpy port ({why}), {cores} threads"
     value = toks / secs
     desc = (f"{sample} sentences per step spread over the corpus length range (lengths "
-            f"{len(sents[idx[0]])}..{len(sents[idx[-1]])}), beam 5, V_tgt 50000, "
-            f"oracle/qnmt_oracle.py numpy port, {cores} threads")
+            f"{len(sents[idx[0]])}..{len(sents[idx[-1]])}), beam 5, max_ratio 1.5, V_tgt 50000, {what}")
     line = {"metric": METRIC, "value": value, "unit": "tokens/s", "impl": "reference", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * secs / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int8",
             "data": "synthetic", "config": {"workload": WORKLOAD, "sample_per_step": sample},
-            "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores, "kind": "port", "sample": desc},
+            "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores, "kind": kind, "sample": desc,
+                             **host_desc(qnmt)},
             "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -232,7 +312,7 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--cpu-sample", type=int, default=8)
+    ap.add_argument("--cpu-sample", type=int, default=16)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-stamps", action="store_true", help="no device-clock stamps (no roofline)")
     ap.add_argument("--no-profile", action="store_true", help="(kept for compatibility)")
@@ -424,14 +504,28 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         idx = cpu_sample(sents, args.cpu_sample)
-        outs, dt, cores = cpu_translate(params, [sents[i] for i in idx])
-        ctoks = sum(len(o[0]) for o in outs)
+        qnmt, why = load_reference()
+        if qnmt is not None:
+            ref = (qnmt,) + reference_model(qnmt, params)
+            cpu_translate(ref, [sents[idx[0]]])   # warm-up (numba JIT, weight shadows)
+            outs, dt, cores = cpu_translate(ref, [sents[i] for i in idx])
+            value, kind = sum(len(o[0]) for o in outs) / dt, "reference"
+            what = (f"qnmt (unmodified, baseline/_ref) decoder.translate, one sentence per worker thread "
+                    f"(bench._decode_corpus scheme), {cores} threads")
+            tier = "the unmodified reference (Tier A)"
+        else:
+            outs, dt, cores = cpu_translate_port(params, [sents[i] for i in idx])
+            value, kind = sum(len(o[0]) for o in outs) / dt, "port"
+            what = f"oracle/qnmt_oracle.py numpy port ({why}), {cores} threads"
+            tier = "the oracle port (Tier B)"
         match = sum(1 for i, o in zip(idx, outs) if first_result.get(i) == (o[0], o[1]))
-        cpu = {"value": ctoks / dt, "unit": "tokens/s", "cores": cores, "kind": "port",
+        same_tokens = sum(1 for i, o in zip(idx, outs) if first_result.get(i, (None,))[0] == o[0])
+        cpu = {"value": value, "unit": "tokens/s", "cores": cores, "kind": kind,
                "sample": f"{len(idx)} sentences spread evenly over the corpus length order (lengths "
-                         f"{len(sents[idx[0]])}..{len(sents[idx[-1]])}; beam 5, "
-                         f"V_tgt 50000), oracle/qnmt_oracle.py numpy port, {cores} threads, {dt:.1f} s",
-               "gpu_outputs_identical": f"{match}/{len(idx)}"}
+                         f"{len(sents[idx[0]])}..{len(sents[idx[-1]])}; beam 5, V_tgt 50000), {what}, {dt:.1f} s",
+               **host_desc(qnmt),
+               "gpu_outputs_identical": f"{match}/{len(idx)} (tokens and log-prob, vs {tier})",
+               "gpu_tokens_identical": f"{same_tokens}/{len(idx)}"}
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": 1000 * secs / args.steps,

@@ -109,13 +109,16 @@ def attention_case(S=256, beam=5, A=2048, H2=2048, seed=0):
     rows_d = torch.from_numpy(rows).cuda()
     lens_d = torch.from_numpy(lens).cuda()
     ctx = torch.empty((N, H2), device="cuda")
-    scratch = torch.empty(N * 104 + 64, dtype=torch.int32, device="cuda")
+    scratch = torch.empty(N * (104 + A) + 256, dtype=torch.int32, device="cuda")
     mm = torch.empty((S, 2, A), device="cuda")
+    ex = torch.empty_like(att)
     f = _dev.flag()
     _lib.call("qnmt_attention_stats", att.data_ptr(), rows_d.data_ptr(), lens_d.data_ptr(), S, A, mm.data_ptr(),
               torch.cuda.current_stream().cuda_stream)
+    _lib.call("qnmt_attention_exp", att.data_ptr(), att.numel(), ex.data_ptr(), torch.cuda.current_stream().cuda_stream)
     t = graph_time(lambda: _lib.call("qnmt_attention", u.data_ptr(), A, N, off.data_ptr(), cnt.data_ptr(), S,
-                                     att.data_ptr(), mm.data_ptr(), states.data_ptr(), rows_d.data_ptr(), lens_d.data_ptr(), 100,
+                                     att.data_ptr(), mm.data_ptr(), ex.data_ptr(), states.data_ptr(), rows_d.data_ptr(),
+                                     lens_d.data_ptr(), 100,
                                      A, H2, v.data_ptr(), vs.data_ptr(), ctx.data_ptr(), H2, None, 0,
                                      scratch.data_ptr(), f.data_ptr(), torch.cuda.current_stream().cuda_stream))
     tanh_count = beam * A * int(lens.sum())

@@ -163,8 +163,12 @@ int qnmt_tanh(const float* x, int64_t N, int64_t D, int64_t ldx, float* y, int64
  *   (fp64, rounded).
  *   att_minmax (nullable): [n_sent][2][A] per-sentence column max / min of
  *   att_proj (qnmt_attention_stats); computed into scratch when NULL.
+ *   att_exp (nullable): fl32(e^(2 att_proj)) in att_proj's layout
+ *   (qnmt_attention_exp, once per encoder output): enables the one-MUFU
+ *   scorer (same results; sentences with |att_proj| or |u| > 20 use the
+ *   two-MUFU one).
  *   ctx: [N][2H] (ldc); alpha (nullable): [N][lda];
- *   scratch: >= 4*(N*max_len + 2*N + 128 + 2*n_sent*A) bytes
+ *   scratch: >= 4*(N*max_len + 4*N + 192 + 2*n_sent*A + N*A) bytes
  * ------------------------------------------------------------------------- */
 /* fp32 attend (layers.py:214-241 with float LinearOps): scores
  * fl32(sum_a f64(v_a) f64(tanh(att_proj + u))) then the same softmax/context as
@@ -176,9 +180,16 @@ int qnmt_attention_f32(const float* u, int64_t ldu, int64_t N, const int32_t* se
                        float* alpha, int64_t lda, void* scratch, int32_t* err_flag, void* stream);
 int qnmt_attention_stats(const float* att_proj, const int64_t* sent_row, const int32_t* sent_len,
                          int32_t n_sent, int64_t A, float* att_minmax, void* stream);
+/* att_exp[i] = fl32(e^(2 att_proj[i])) (fp64 exp, rounded once) for n values
+ * (values beyond +-20 clamped: their sentences take the two-MUFU scorer). */
+int qnmt_attention_exp(const float* att_proj, int64_t n, float* att_exp, void* stream);
+/* 1 (default): one-MUFU scorer when att_exp is supplied; 0: two-MUFU scorer
+ * everywhere (A/B testing; results identical).  Returns old value. */
+int qnmt_set_att_exp(int32_t enable);
 int qnmt_attention(const float* u, int64_t ldu, int64_t N, const int32_t* sent_col_off,
                    const int32_t* sent_ncols, int32_t n_sent,
-                   const float* att_proj, const float* att_minmax, const float* states,
+                   const float* att_proj, const float* att_minmax, const float* att_exp,
+                   const float* states,
                    const int64_t* sent_row,
                    const int32_t* sent_len, int32_t max_len, int64_t A, int64_t H2,
                    const int8_t* v_codes, const float* v_scale,

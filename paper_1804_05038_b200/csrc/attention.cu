@@ -16,10 +16,16 @@
 //
 // max|t| needs no tanh: |tanh| is odd and monotone, and so is "evaluate in
 // fp64, round once", hence max_{a,i} |fl32(tanh(x))| = fl32(tanh(max |x|)).
-// Codes q(t) use an f32 fast path: tanhf (<= 2 ulp) gives v = t*scale within a
-// few ulps of the exact product; the code floor(|v| + 1/2) can only differ if
-// |v| is within ~2.5e-4 of a half-integer (>30 ulps of margin at |v| <= 127.5),
-// and only those elements are recomputed with the fp64-exact tanh.
+// Codes q(t) use an f32 fast path whose error against the reference's v = t*scale
+// is bounded; the code floor(|v| + 1/2) can only differ if v is within that bound
+// of a half-integer, and only those elements are recomputed with the fp64-exact
+// tanh.  Two fast paths:
+//   k_att_score6 (one MUFU per element): att_proj is fixed for the whole decode,
+//     so E_ap = fl32(e^(2 ap)) is computed once per batch (k_att_exp) and
+//     E_u = fl32(e^(2 u)) once per hypothesis and step (k_att_scale);
+//     e^(2(ap+u)) = E_ap * E_u and t = 1 - 2 / (1 + E_ap E_u): one FFMA, one
+//     MUFU.RCP, one FFMA per element (needs |ap|, |u| <= 20: no over/underflow);
+//   k_att_score5 (two MUFU): t = 1 - 2 / (1 + 2^(2x log2 e)) from x = fl(ap + u).
 #include <algorithm>
 
 #include "kernels.cuh"
@@ -63,6 +69,37 @@ __device__ __forceinline__ float att_threshold(float st) { return 0.5f - (st * 2
 constexpr float ATT_ST_FAST_MAX = 1.0e6f;   // above: window > 0.5, every element exact
 
 __device__ __noinline__ int att_code_exact(float x, float st) { return quant_code(tanh_b(x), st); }
+
+// One-MUFU fast path (k_att_score6): v_fast = fl(st - 2 st rcp.approx(fl(E_ap E_u + 1))).
+// With E_ap, E_u rounded once from fp64 exps (rel. err <= 2^-24 each), the FFMA's
+// rounding (2^-24) and rcp.approx.ftz.f32 (<= 2^-23, measured exhaustively:
+// profiles/r02_att_exp_err.json), r is within delta_r <= 3e-7 relative of
+// 1 / (1 + e^(2(ap+u))); hence |v_fast - st tanh(ap+u)| <= 2 st delta_r + half an
+// ulp of v, tanh(ap+u) is within 2.7e-8 of tanh(fl(ap+u)) (|x| sech^2 x <= 0.45),
+// and the reference's v carries one rounding of t (st 2^-25) and one of the
+// product: |v_fast - v| <= 6.6e-7 st + 1.52e-5.  The window adds ~50% margin
+// (a Monte-Carlo of 2^33 draws per distribution stays below 0.5 of it, same file).
+__device__ __forceinline__ float att_e_threshold(float st) { return 0.5f - (st * 1.02e-6f + 1.53e-5f); }
+constexpr float ATT_E_BOUND = 20.0f;   // |ap|, |u| <= 20: E_ap E_u in [1.8e-35, 5.5e34], no ftz / overflow
+int g_att_exp = 1;                      // 0: two-MUFU scorer everywhere (A/B testing)
+
+// E_ap = fl32(e^(2 ap)) for n values of att_proj (fp64 exp, rounded once).  Values
+// beyond the fast path's bound are clamped (their sentences take the two-MUFU path).
+__global__ void k_att_exp(const float* __restrict__ ap, int64_t n, float* __restrict__ out) {
+    pdl_entry();
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const double x = fmin(fmax((double)ap[i], -(double)ATT_E_BOUND), (double)ATT_E_BOUND);
+        out[i] = __double2float_rn(exp_f64(2.0 * x));
+    }
+}
+
+int att_exp_launch(const float* att_proj, int64_t n, float* out, cudaStream_t st) {
+    if (n <= 0) return QNMT_OK;
+    const unsigned grid = (unsigned)std::min<int64_t>(cdiv(n, 256), 148 * 16);
+    QNMT_LAUNCH(k_att_exp, grid, 256, 0, st, att_proj, n, out);
+    QNMT_CHECK_LAUNCH("k_att_exp");
+    return QNMT_OK;
+}
 
 // load this thread's strided slice of APC att_proj rows (a = tid + AT*k)
 __device__ __forceinline__ void load_ap(const float* __restrict__ ap, int64_t A, int i0, int i1,
@@ -108,14 +145,16 @@ int att_minmax_launch(const float* att_proj, const int64_t* sent_row, const int3
 }
 
 // Per-hypothesis scale of the whole [A, l] tanh block (layers.py:226) from the
-// column extrema, and the fast-path threshold: st_thr[c] = {st, att_threshold(st)}.
+// column extrema, and the fast-path thresholds:
+//   st_thr[c] = {st, att_threshold(st), att_e_threshold(st), eligible for k_att_score6}.
+// With eu != nullptr also E_u[c][a] = fl32(e^(2 u[c][a])) (fp64 exp, rounded once).
 // Grid (n_sent, AMAXP): CTA (s, j) handles hypothesis j of sentence s.
 __global__ void __launch_bounds__(AT)
 k_att_scale(const float* __restrict__ u, int64_t ldu, const int32_t* __restrict__ sent_col_off,
             const int32_t* __restrict__ sent_ncols, const float* __restrict__ mm, int64_t A,
-            float2* __restrict__ st_thr, int32_t* err_flag, uint32_t* zero_seg) {
+            float4* __restrict__ st_thr, int32_t* err_flag, uint32_t* zero_seg, float* __restrict__ eu) {
     pdl_entry();
-    __shared__ uint32_t mred[AT / 32];
+    __shared__ uint32_t mred[AT / 32], bred[AT / 32];
     const int s = blockIdx.x, j = blockIdx.y;
     // the context kernel of this step max-reduces |ctx| per sentence into zero_seg[s]
     // (replaces a memset node, which would break the programmatic-dependent-launch chain)
@@ -125,28 +164,51 @@ k_att_scale(const float* __restrict__ u, int64_t ldu, const int32_t* __restrict_
     const float* un = u + (int64_t)c * ldu;
     const float* mx = mm + ((int64_t)s * 2) * A;
     const float* mn = mx + A;
-    uint32_t m = 0;
+    uint32_t m = 0, b = 0;   // b: max of |ap| extrema and |u| (fast-path eligibility)
+    float uv[AKA];
 #pragma unroll
     for (int k = 0; k < AKA; ++k) {   // A <= AT * AKA: all loads in flight at once
         const int64_t a = threadIdx.x + (int64_t)AT * k;
+        uv[k] = 0.0f;
         if (a < A) {
-            const float uv = un[a];
-            m = max(m, __float_as_uint(__fadd_rn(mx[a], uv)) & 0x7fffffffu);
-            m = max(m, __float_as_uint(__fadd_rn(mn[a], uv)) & 0x7fffffffu);
+            uv[k] = un[a];
+            const float x0 = mx[a], x1 = mn[a];
+            m = max(m, __float_as_uint(__fadd_rn(x0, uv[k])) & 0x7fffffffu);
+            m = max(m, __float_as_uint(__fadd_rn(x1, uv[k])) & 0x7fffffffu);
+            b = max(b, max(__float_as_uint(x0) & 0x7fffffffu, __float_as_uint(x1) & 0x7fffffffu));
+            b = max(b, __float_as_uint(uv[k]) & 0x7fffffffu);
+        }
+    }
+    if (eu) {
+#pragma unroll
+        for (int k = 0; k < AKA; ++k) {
+            const int64_t a = threadIdx.x + (int64_t)AT * k;
+            if (a < A) {
+                const double x = fmin(fmax((double)uv[k], -(double)ATT_E_BOUND), (double)ATT_E_BOUND);
+                eu[(int64_t)c * A + a] = __double2float_rn(exp_f64(2.0 * x));
+            }
         }
     }
     m = warp_max(m);
-    if ((threadIdx.x & 31) == 0) mred[threadIdx.x >> 5] = m;
+    b = warp_max(b);
+    if ((threadIdx.x & 31) == 0) {
+        mred[threadIdx.x >> 5] = m;
+        bred[threadIdx.x >> 5] = b;
+    }
     __syncthreads();
     if (threadIdx.x == 0) {
-        for (int w = 0; w < AT / 32; ++w) m = max(m, mred[w]);
+        for (int w = 0; w < AT / 32; ++w) {
+            m = max(m, mred[w]);
+            b = max(b, bred[w]);
+        }
         if (m >= 0x7f800000u) {
             set_flag(err_flag, QNMT_FLAG_NUMERIC);
             m = 0;
         }
         const float tmax = tanh_b(__uint_as_float(m));   // max |fl32(tanh)| = fl32(tanh(max |x|))
         const float st = (tmax == 0.0f) ? 1.0f : __fdiv_rn(127.0f, tmax);
-        st_thr[c] = make_float2(st, att_threshold(st));
+        const bool elig = eu != nullptr && b <= __float_as_uint(ATT_E_BOUND) && st <= ATT_ST_FAST_MAX;
+        st_thr[c] = make_float4(st, att_threshold(st), att_e_threshold(st), elig ? 1.0f : 0.0f);
     }
 }
 
@@ -157,7 +219,7 @@ k_att_scale(const float* __restrict__ u, int64_t ldu, const int32_t* __restrict_
 __global__ void __launch_bounds__(AT, 2)
 k_att_score4(const float* __restrict__ u, int64_t ldu, const int32_t* __restrict__ sent_col_off,
              const int32_t* __restrict__ sent_ncols, const float* __restrict__ att_proj,
-             const float2* __restrict__ st_thr, const int64_t* __restrict__ sent_row,
+             const float4* __restrict__ st_thr, const int64_t* __restrict__ sent_row,
              const int32_t* __restrict__ sent_len, int64_t A, const int8_t* __restrict__ v_codes,
              const float* __restrict__ v_scale, float* __restrict__ scores, int32_t max_len) {
     pdl_entry();
@@ -180,9 +242,9 @@ k_att_score4(const float* __restrict__ u, int64_t ldu, const int32_t* __restrict
         vv[k] = a < A ? (int)v_codes[a] : 0;
         uvv[k] = a < A ? u[(int64_t)c0 * ldu + a] : 0.0f;
     }
-    float2 sp = st_thr[c0];
+    float4 sp = st_thr[c0];
     for (int j = 0; j < P; ++j) {
-        float2 spx = sp;
+        float4 spx = sp;
         if (j + 1 < P) {   // prefetch the next hypothesis' query row and scale
             const float* un = u + (int64_t)(c0 + j + 1) * ldu;
 #pragma unroll
@@ -252,39 +314,50 @@ k_att_score4(const float* __restrict__ u, int64_t ldu, const int32_t* __restrict
     }
 }
 
-// Same scores with each thread's slice of the att_proj tile parked in shared
-// memory (APC5 positions x its a-quads; a thread only ever reads its own slots,
-// so no barrier), registers holding just the query slice, codes and
-// accumulators: 3 CTAs / SM instead of 2 to hide the MUFU / FMA latency.  Thread
-// t owns a-quads 4t + 4*AT*k; quads past A are zero (no bounds checks in the
-// hot loop).  Warps store their per-position sums in shared memory and the last
-// warp to finish writes the scores (no end-of-CTA barrier wait).
+// Same scores with each thread's slice of the tile parked in shared memory
+// (APC5 positions x its a-quads; a thread only ever reads its own slots, so no
+// barrier), registers holding just the query slice, codes and accumulators:
+// 4 CTAs / SM to hide the MUFU / FMA latency.  Thread t owns a-quads
+// 4t + 4*AT*k; quads past A are zero (no bounds checks in the hot loop).  Warps
+// store their per-position sums in shared memory and the last warp to finish
+// writes the scores (no end-of-CTA barrier wait).
+//   EXPM = false (k_att_score5): tile = att_proj, query = u, two MUFU per element;
+//   EXPM = true  (k_att_score6, sentences whose hypotheses are all eligible):
+//     tile = E_ap, query = E_u, one MUFU per element; elements in the rounding
+//     window are recomputed exactly from att_proj / u in global memory.
 constexpr int APC5 = 6;        // positions per CTA (48 KB of tile slices: 4 CTAs / SM)
 constexpr int AQ5 = 2;         // a-quads per thread (A <= 4 * AT * AQ5 = 2048)
 
-__global__ void __launch_bounds__(AT, 4)
-k_att_score5(const float* __restrict__ u, int64_t ldu, const int32_t* __restrict__ sent_col_off,
-             const int32_t* __restrict__ sent_ncols, const float* __restrict__ att_proj,
-             const float2* __restrict__ st_thr, const int64_t* __restrict__ sent_row,
-             const int32_t* __restrict__ sent_len, int64_t A, const int8_t* __restrict__ v_codes,
-             const float* __restrict__ v_scale, float* __restrict__ scores, int32_t max_len) {
-    pdl_entry();
-    extern __shared__ float4 sap[];   // [APC5][AQ5][AT]
-    __shared__ int red5[AMAXP][APC5][AT / 32];
-    __shared__ int s_done;
-    const int s = blockIdx.y;
-    const int P = sent_ncols[s];
-    const int l = sent_len[s];
-    const int i0 = blockIdx.x * APC5;
-    if (P == 0 || i0 >= l) return;
+struct ScoreArgs {
+    const float* u;
+    int64_t ldu;
+    const int32_t* sent_col_off;
+    const int32_t* sent_ncols;
+    const float* att_proj;
+    const float* att_exp;      // E_ap [rows][A] (score6)
+    const float* eu;           // E_u [N][A] (score6)
+    const float4* st_thr;
+    const int64_t* sent_row;
+    const int32_t* sent_len;
+    int64_t A;
+    const int8_t* v_codes;
+    const float* v_scale;
+    float* scores;
+    int32_t max_len;
+};
+
+template <bool EXPM>
+__device__ __forceinline__ void att_score_body(const ScoreArgs& g, float4* sap, int (*red5)[APC5][AT / 32],
+                                               int* s_done, int s, int P, int l, int i0) {
     const int i1 = min(l, i0 + APC5);
     const int np = i1 - i0;
-    const int c0 = sent_col_off[s];
+    const int c0 = g.sent_col_off[s];
     const int lane = threadIdx.x & 31;
-    const int64_t A4 = A / 4;
-    if (threadIdx.x == 0) s_done = 0;
+    const int64_t A = g.A, A4 = A / 4;
+    const int64_t row0 = g.sent_row[s] + i0;
+    if (threadIdx.x == 0) *s_done = 0;
     {   // this thread's slots of the tile (positions past i1 and quads past A are zero)
-        const float4* src = reinterpret_cast<const float4*>(att_proj + (sent_row[s] + i0) * A);
+        const float4* src = reinterpret_cast<const float4*>((EXPM ? g.att_exp : g.att_proj) + row0 * A);
 #pragma unroll
         for (int p = 0; p < APC5; ++p)
 #pragma unroll
@@ -294,38 +367,53 @@ k_att_score5(const float* __restrict__ u, int64_t ldu, const int32_t* __restrict
                     (p < np && q < A4) ? src[p * A4 + q] : make_float4(0.f, 0.f, 0.f, 0.f);
             }
     }
+    const float* qsrc = EXPM ? g.eu : g.u;   // query side: E_u [N][A] or u [N][ldu]
+    const int64_t ldq = EXPM ? A : g.ldu;
     int vv[AQ5][4];
     float4 uq[AQ5], ux[AQ5];
 #pragma unroll
     for (int k = 0; k < AQ5; ++k) {
         const int64_t q = threadIdx.x + (int64_t)AT * k;
         const bool ok = q < A4;
-        const char4 c = ok ? reinterpret_cast<const char4*>(v_codes)[q] : make_char4(0, 0, 0, 0);
+        const char4 c = ok ? reinterpret_cast<const char4*>(g.v_codes)[q] : make_char4(0, 0, 0, 0);
         vv[k][0] = c.x; vv[k][1] = c.y; vv[k][2] = c.z; vv[k][3] = c.w;
-        uq[k] = ok ? reinterpret_cast<const float4*>(u + (int64_t)c0 * ldu)[q] : make_float4(0.f, 0.f, 0.f, 0.f);
+        uq[k] = ok ? reinterpret_cast<const float4*>(qsrc + (int64_t)c0 * ldq)[q] : make_float4(0.f, 0.f, 0.f, 0.f);
     }
-    float2 sp = st_thr[c0];
+    float4 sp = g.st_thr[c0];
     int vsum = 0;
 #pragma unroll
     for (int k = 0; k < AQ5; ++k) vsum += vv[k][0] + vv[k][1] + vv[k][2] + vv[k][3];
     const int vsum_off = (int)((unsigned)vsum * 0x4B400000u);
     __syncthreads();   // s_done initialised
     for (int j = 0; j < P; ++j) {
-        float2 spx = sp;
+        float4 spx = sp;
         if (j + 1 < P) {   // prefetch the next hypothesis' query slice and scale
 #pragma unroll
             for (int k = 0; k < AQ5; ++k) {
                 const int64_t q = threadIdx.x + (int64_t)AT * k;
-                ux[k] = q < A4 ? reinterpret_cast<const float4*>(u + (int64_t)(c0 + j + 1) * ldu)[q]
+                ux[k] = q < A4 ? reinterpret_cast<const float4*>(qsrc + (int64_t)(c0 + j + 1) * ldq)[q]
                                : make_float4(0.f, 0.f, 0.f, 0.f);
             }
-            spx = st_thr[c0 + j + 1];
+            spx = g.st_thr[c0 + j + 1];
         }
-        const float st = sp.x, thr = sp.y, m2st = -2.0f * st;
+        const float st = sp.x, thr = EXPM ? sp.z : sp.y, m2st = -2.0f * st;
         int acc[APC5];
 #pragma unroll
         for (int p = 0; p < APC5; ++p) acc[p] = 0;
-        if (st <= ATT_ST_FAST_MAX) {   // CTA-uniform
+        // v for element e of quad k at position p (the fast path)
+        auto fast_v = [&](const float4& apq, int k, int e) -> float {
+            const float a4[4] = {apq.x, apq.y, apq.z, apq.w};
+            const float u4[4] = {uq[k].x, uq[k].y, uq[k].z, uq[k].w};
+            float r;
+            if (EXPM) {
+                r = rcp_approx(fmaf(a4[e], u4[e], 1.0f));
+            } else {
+                const float x = __fadd_rn(a4[e], u4[e]);
+                r = rcp_approx(__fadd_rn(ex2_approx(__fmul_rn(x, 2.8853900817779268f)), 1.0f));
+            }
+            return fmaf(m2st, r, st);
+        };
+        if (EXPM || st <= ATT_ST_FAST_MAX) {   // CTA-uniform
             float dmx[APC5];   // per position: max distance of v to its rounding integer
 #pragma unroll
             for (int p = 0; p < APC5; ++p) {
@@ -334,13 +422,9 @@ k_att_score5(const float* __restrict__ u, int64_t ldu, const int32_t* __restrict
 #pragma unroll
                 for (int k = 0; k < AQ5; ++k) {
                     const float4 apq = sap[(p * AQ5 + k) * AT + threadIdx.x];
-                    const float ap4[4] = {apq.x, apq.y, apq.z, apq.w};
-                    const float u4[4] = {uq[k].x, uq[k].y, uq[k].z, uq[k].w};
 #pragma unroll
                     for (int e = 0; e < 4; ++e) {
-                        const float x = __fadd_rn(ap4[e], u4[e]);
-                        const float r = rcp_approx(__fadd_rn(ex2_approx(__fmul_rn(x, 2.8853900817779268f)), 1.0f));
-                        const float v = fmaf(m2st, r, st);
+                        const float v = fast_v(apq, k, e);
                         const float mg = __fadd_rn(v, 12582912.0f);   // 1.5 * 2^23
                         dmx[p] = fmaxf(dmx[p], fabsf(__fsub_rn(v, __fsub_rn(mg, 12582912.0f))));
                         // code = bits - 0x4B400000: the offset is removed once per position below
@@ -352,7 +436,7 @@ k_att_score5(const float* __restrict__ u, int64_t ldu, const int32_t* __restrict
             for (int p = 0; p < APC5; ++p)   // sum_a v_a * code_a = sum_a v_a * bits_a - 0x4B400000 * sum_a v_a (mod 2^32)
                 if (p < np) acc[p] = (int)((unsigned)acc[p] - (unsigned)vsum_off);
             // rare: a position with an element within the window of a rounding boundary is
-            // recomputed, flagged elements exactly (fp64 tanh)
+            // recomputed, flagged elements exactly (fp64 tanh of x = fl(ap + u))
 #pragma unroll
             for (int p = 0; p < APC5; ++p) {
                 if (p >= np) break;
@@ -361,21 +445,22 @@ k_att_score5(const float* __restrict__ u, int64_t ldu, const int32_t* __restrict
 #pragma unroll
                 for (int k = 0; k < AQ5; ++k) {
                     const float4 apq = sap[(p * AQ5 + k) * AT + threadIdx.x];
-                    const float ap4[4] = {apq.x, apq.y, apq.z, apq.w};
-                    const float u4[4] = {uq[k].x, uq[k].y, uq[k].z, uq[k].w};
 #pragma unroll
                     for (int e = 0; e < 4; ++e) {
-                        const float x = __fadd_rn(ap4[e], u4[e]);
-                        const float r = rcp_approx(__fadd_rn(ex2_approx(__fmul_rn(x, 2.8853900817779268f)), 1.0f));
-                        const float v = fmaf(m2st, r, st);
+                        const float v = fast_v(apq, k, e);
                         const float mg = __fadd_rn(v, 12582912.0f);
-                        if (fabsf(__fsub_rn(v, __fsub_rn(mg, 12582912.0f))) > thr && vv[k][e] != 0)
+                        if (fabsf(__fsub_rn(v, __fsub_rn(mg, 12582912.0f))) > thr && vv[k][e] != 0) {
+                            const int64_t a = 4 * (threadIdx.x + (int64_t)AT * k) + e;
+                            const float x = EXPM ? __fadd_rn(g.att_proj[(row0 + p) * A + a],
+                                                             g.u[(int64_t)(c0 + j) * g.ldu + a])
+                                                 : __fadd_rn((&apq.x)[e], (&uq[k].x)[e]);
                             d += vv[k][e] * (att_code_exact(x, st) - (__float_as_int(mg) - 0x4B400000));
+                        }
                     }
                 }
                 acc[p] += d;
             }
-        } else {   // degenerate scale (max |tanh| < 1.3e-4): exact codes throughout
+        } else {   // degenerate scale (max |tanh| < 1.3e-4): exact codes throughout (two-MUFU mode only)
             for (int p = 0; p < np; ++p) {
                 int a_sum = 0;
 #pragma unroll
@@ -405,7 +490,7 @@ k_att_score5(const float* __restrict__ u, int64_t ldu, const int32_t* __restrict
     int last = 0;
     if (lane == 0) {
         __threadfence_block();
-        last = atomicAdd(&s_done, 1) == AT / 32 - 1;
+        last = atomicAdd(s_done, 1) == AT / 32 - 1;
     }
     if (!__shfl_sync(0xffffffffu, last, 0)) return;
     __threadfence_block();
@@ -414,8 +499,40 @@ k_att_score5(const float* __restrict__ u, int64_t ldu, const int32_t* __restrict
         int t = 0;
 #pragma unroll
         for (int w = 0; w < AT / 32; ++w) t += red5[j][p][w];
-        scores[(int64_t)(c0 + j) * max_len + i0 + p] = dequant(t, v_scale[0], st_thr[c0 + j].x);
+        g.scores[(int64_t)(c0 + j) * g.max_len + i0 + p] = dequant(t, g.v_scale[0], g.st_thr[c0 + j].x);
     }
+}
+
+// two-MUFU scorer for every sentence
+__global__ void __launch_bounds__(AT, 4)
+k_att_score5(ScoreArgs g) {
+    pdl_entry();
+    extern __shared__ float4 sap[];   // [APC5][AQ5][AT]
+    __shared__ int red5[AMAXP][APC5][AT / 32];
+    __shared__ int s_done;
+    const int s = blockIdx.y;
+    const int P = g.sent_ncols[s], l = g.sent_len[s], i0 = blockIdx.x * APC5;
+    if (P == 0 || i0 >= l) return;
+    att_score_body<false>(g, sap, red5, &s_done, s, P, l, i0);
+}
+
+// one-MUFU scorer where every live hypothesis of the sentence is eligible, else two-MUFU
+__global__ void __launch_bounds__(AT, 4)
+k_att_score6(ScoreArgs g) {
+    pdl_entry();
+    extern __shared__ float4 sap[];   // [APC5][AQ5][AT]
+    __shared__ int red5[AMAXP][APC5][AT / 32];
+    __shared__ int s_done;
+    const int s = blockIdx.y;
+    const int P = g.sent_ncols[s], l = g.sent_len[s], i0 = blockIdx.x * APC5;
+    if (P == 0 || i0 >= l) return;
+    const int c0 = g.sent_col_off[s];
+    bool elig = true;
+    for (int j = 0; j < P; ++j) elig &= g.st_thr[c0 + j].w != 0.0f;
+    if (elig)
+        att_score_body<true>(g, sap, red5, &s_done, s, P, l, i0);
+    else
+        att_score_body<false>(g, sap, red5, &s_done, s, P, l, i0);
 }
 
 // softmax over the l scores of every hypothesis of sentence s (fp64, fixed
@@ -716,33 +833,44 @@ int attention_launch(const float* u, int64_t ldu, int64_t N, const int32_t* sent
                      const float* states, const int64_t* sent_row, const int32_t* sent_len, int32_t max_len,
                      int64_t A, int64_t H2, const int8_t* v_codes, const float* v_scale, float* ctx, int64_t ldc,
                      float* alpha, int64_t lda, void* scratch, int32_t* err_flag, cudaStream_t st,
-                     uint32_t* ctx_segmax, int max_p) {
+                     uint32_t* ctx_segmax, int max_p, const float* att_exp) {
     if (N <= 0 || n_sent <= 0) return QNMT_OK;
     if (A > (int64_t)AT * AKA) {
         set_error("qnmt_attention: attention dim %lld > %d", (long long)A, AT * AKA);
         return QNMT_ERR_SHAPE;
     }
-    // scratch: scores [N][max_len] | st_thr [N] float2 | (column extrema [n_sent][2][A])
+    // scratch: scores [N][max_len] | st_thr [N] float4 | (column extrema [n_sent][2][A]) | (E_u [N][A])
     float* scores = reinterpret_cast<float*>(scratch);
-    float2* st_thr = reinterpret_cast<float2*>(scores + ((N * max_len + 63) / 64) * 64);
+    float4* st_thr = reinterpret_cast<float4*>(scores + ((N * max_len + 63) / 64) * 64);
+    float* tail = reinterpret_cast<float*>(st_thr) + ((4 * N + 63) / 64) * 64;
     if (!att_minmax) {   // extrema not supplied by the caller: compute them into scratch
-        float* mm = reinterpret_cast<float*>(st_thr) + ((2 * N + 63) / 64) * 64;
+        float* mm = tail;
+        tail += ((2 * (int64_t)n_sent * A + 63) / 64) * 64;
         TRY_LAUNCH(att_minmax_launch(att_proj, sent_row, sent_len, n_sent, A, mm, st));
         att_minmax = mm;
     }
-    QNMT_LAUNCH(k_att_scale, dim3((unsigned)n_sent, AMAXP), AT, 0, st, u, ldu, sent_col_off, sent_ncols, att_minmax, A,
-                                                              st_thr, err_flag, ctx_segmax);
-    QNMT_CHECK_LAUNCH("k_att_scale");
     const bool quads = A % 4 == 0 && ldu % 4 == 0 && A <= 4 * AT * AQ5 && ((uintptr_t)u % 16) == 0 &&
                        ((uintptr_t)att_proj % 16) == 0 && ((uintptr_t)v_codes % 4) == 0;
-    if (quads) {   // smem-staged tile, 3 CTAs / SM
+    const bool expm = quads && att_exp != nullptr && g_att_exp && ((uintptr_t)att_exp % 16) == 0;
+    float* eu = expm ? tail : nullptr;
+    QNMT_LAUNCH(k_att_scale, dim3((unsigned)n_sent, AMAXP), AT, 0, st, u, ldu, sent_col_off, sent_ncols, att_minmax, A,
+                st_thr, err_flag, ctx_segmax, eu);
+    QNMT_CHECK_LAUNCH("k_att_scale");
+    if (quads) {   // smem-staged tile, 4 CTAs / SM
         const size_t smem5 = (size_t)APC5 * AQ5 * AT * sizeof(float4);
-        static size_t done = 0;   // (dynamic + static > 48 KB needs the opt-in)
-        QNMT_CUDA(raise_smem_limit((const void*)k_att_score5, smem5, done));
+        static size_t done5 = 0, done6 = 0;   // (dynamic + static > 48 KB needs the opt-in)
+        ScoreArgs ga{u, ldu, sent_col_off, sent_ncols, att_proj, att_exp, eu, st_thr, sent_row, sent_len, A,
+                     v_codes, v_scale, scores, max_len};
         dim3 g5((unsigned)cdiv(max_len, APC5), (unsigned)n_sent);
-        QNMT_LAUNCH(k_att_score5, g5, AT, smem5, st, u, ldu, sent_col_off, sent_ncols, att_proj, st_thr, sent_row, sent_len,
-                                            A, v_codes, v_scale, scores, max_len);
-        QNMT_CHECK_LAUNCH("k_att_score5");
+        if (expm) {
+            QNMT_CUDA(raise_smem_limit((const void*)k_att_score6, smem5, done6));
+            QNMT_LAUNCH(k_att_score6, g5, AT, smem5, st, ga);
+            QNMT_CHECK_LAUNCH("k_att_score6");
+        } else {
+            QNMT_CUDA(raise_smem_limit((const void*)k_att_score5, smem5, done5));
+            QNMT_LAUNCH(k_att_score5, g5, AT, smem5, st, ga);
+            QNMT_CHECK_LAUNCH("k_att_score5");
+        }
     } else {
         dim3 g1((unsigned)cdiv(max_len, APC), (unsigned)n_sent);
         QNMT_LAUNCH(k_att_score4, g1, AT, 0, st, u, ldu, sent_col_off, sent_ncols, att_proj, st_thr, sent_row, sent_len, A,
@@ -866,14 +994,25 @@ int col_ranges_launch(const int32_t* col_sent, int64_t N, int32_t n_sent, int32_
 
 extern "C" int qnmt_attention(const float* u, int64_t ldu, int64_t N, const int32_t* sent_col_off,
                               const int32_t* sent_ncols, int32_t n_sent, const float* att_proj,
-                              const float* att_minmax, const float* states, const int64_t* sent_row, const int32_t* sent_len,
+                              const float* att_minmax, const float* att_exp, const float* states,
+                              const int64_t* sent_row, const int32_t* sent_len,
                               int32_t max_len, int64_t A, int64_t H2, const int8_t* v_codes,
                               const float* v_scale, float* ctx, int64_t ldc, float* alpha, int64_t lda,
                               void* scratch, int32_t* err_flag, void* stream) {
     return qnmt::attention_launch(u, ldu, N, sent_col_off, sent_ncols, n_sent, att_proj, att_minmax, states,
                                   sent_row,
                                   sent_len, max_len, A, H2, v_codes, v_scale, ctx, ldc, alpha, lda, scratch,
-                                  err_flag, qnmt::as_stream(stream));
+                                  err_flag, qnmt::as_stream(stream), nullptr, 16, att_exp);
+}
+
+extern "C" int qnmt_attention_exp(const float* att_proj, int64_t n, float* att_exp, void* stream) {
+    return qnmt::att_exp_launch(att_proj, n, att_exp, qnmt::as_stream(stream));
+}
+
+extern "C" int qnmt_set_att_exp(int32_t enable) {
+    const int old = qnmt::g_att_exp;
+    qnmt::g_att_exp = enable ? 1 : 0;
+    return old;
 }
 
 extern "C" int qnmt_attention_stats(const float* att_proj, const int64_t* sent_row, const int32_t* sent_len,

@@ -108,6 +108,7 @@ struct qnmt_engine {
     int32_t* s0_dst;         // [S] original index of sorted slot
     float* enc_states;       // [PMAX][2H]  (engine-owned encoder output for translate)
     float* enc_att;          // [PMAX][A]
+    float* enc_attx;         // [PMAX][A] fl32(e^(2 att_proj)) for the one-MUFU attention scorer
     float* enc_s0;           // [S][H]
     int64_t* sent_row;       // [S]
     int32_t* sent_len;       // [S]
@@ -426,6 +427,7 @@ struct StepIO {
     const int32_t* sent_col_off;   // [nseg] first column of each sentence (columns grouped by sentence)
     const int32_t* sent_ncols;     // [nseg] live columns of each sentence
     const float* att_minmax;       // [nseg][2][A] column extrema of att_proj (nullable)
+    const float* att_exp;          // fl32(e^(2 att_proj)) rows (nullable: two-MUFU scorer)
     int max_cols;                  // bound on columns per sentence (fused quantize smem)
     bool codes_ready;              // q_s (and q_q for the previous-state query) hold this step's state codes
     bool fuse_vocab;               // skip the vocab GEMM: the caller runs cands_launch (vocab_topk.cu)
@@ -665,7 +667,8 @@ static int step_core(qnmt_engine* e, const StepIO& io, cudaStream_t st) {
     // (ctx_max is zeroed by the attention scale kernel)
     TRY(attention_launch(u, ldu, N, io.sent_col_off, io.sent_ncols, io.nseg, io.att_proj, io.att_minmax, io.states,
                          io.sent_row, io.sent_len, io.max_len, A, 2 * H, m->v, m->v_s, e->ctx, 2 * H,
-                         io.alpha, io.lda, e->att_scratch, e->err, st, fq ? e->ctx_max : nullptr, io.max_cols));
+                         io.alpha, io.lda, e->att_scratch, e->err, st, fq ? e->ctx_max : nullptr, io.max_cols,
+                         io.att_exp));
     TRY(stamp(e, ST_ATT1, io, st));
     prof_mark(e, PG_QUANT, st);
     if (fq) {
@@ -879,6 +882,7 @@ int qnmt_engine_create(const qnmt_model* m, int32_t max_sentences, int32_t max_s
         e->s0_dst = a.take<int32_t>(S);
         e->enc_states = a.take<float>(P * 2 * H);
         e->enc_att = a.take<float>(P * A);
+        e->enc_attx = a.take<float>(P * A);
         e->enc_s0 = a.take<float>(S * H);
         e->sent_row = a.take<int64_t>(S);
         e->sent_len = a.take<int32_t>(S);
@@ -909,7 +913,7 @@ int qnmt_engine_create(const qnmt_model* m, int32_t max_sentences, int32_t max_s
         e->sc_ro = a.take<float>(S);
         e->logits = a.take<float>(N * V);
         e->vocab_part = a.take<char>(vocab_topk_part_bytes((int64_t)N, (int64_t)V));
-        e->att_scratch = a.take<char>(N * (L + 2) * 4 + 2 * S * A * 4 + 1024);
+        e->att_scratch = a.take<char>(N * (L + 4) * 4 + 2 * S * A * 4 + N * A * 4 + 1024);
         e->att_mm = a.take<float>(2 * S * A);
         e->ctx_max = a.take<uint32_t>(S);
         e->w2x = a.take<int8_t>((3 * H + R) * E);
@@ -1098,7 +1102,7 @@ int qnmt_decoder_step(qnmt_engine* e, int64_t N, const int32_t* col_sent, int32_
     QNMT_CUDA(cudaMemsetAsync(e->err, 0, 4, st));
     TRY(col_ranges_launch(col_sent, N, n_sent, e->rng_off, e->rng_cnt, st));
     StepIO io{N, n_sent, col_sent, y, s, sp, states, att_proj, sent_row, sent_len, max_len,
-              s_int, s_new, logits, alpha, lda, e->rng_off, e->rng_cnt, nullptr, 16, false, false};
+              s_int, s_new, logits, alpha, lda, e->rng_off, e->rng_cnt, nullptr, nullptr, 16, false, false};
     TRY(step_core(e, io, st));
     return check_flag(e, st);
 }
@@ -1126,7 +1130,7 @@ static int capture_step(qnmt_engine* e, int cur, int n, int beam, int k_list, cu
         NdevScope nd(e->d_N + cur);
         StepIO io{NM, n, e->col_sent[cur], e->y[cur], e->st_s[cur], e->st_sp[cur], e->enc_states, e->enc_att,
                   e->sent_row, e->sent_len, e->L, e->s_int, e->s_new, e->logits, nullptr, 0,
-                  e->col_off, e->P, e->att_mm, beam, e->fq_ok, vocab_fusable(e, k_list)};
+                  e->col_off, e->P, e->att_mm, e->enc_attx, beam, e->fq_ok, vocab_fusable(e, k_list)};
         rc = stamp(e, ST_STEP0, io, cs);
         if (rc == QNMT_OK) rc = step_core(e, io, cs);
         if (rc == QNMT_OK) rc = cands_launch(e, io, e->live[cur], k_list, cs);
@@ -1239,6 +1243,7 @@ static int init_member(qnmt_engine* e, const int32_t* src_ids, bool ids_on_devic
     QNMT_CUDA(h2d(e, e->sent_row, b.row.data(), (size_t)n * 8, st));
     QNMT_CUDA(h2d(e, e->sent_len, src_len, (size_t)n * 4, st));
     TRY(att_minmax_launch(e->enc_att, e->sent_row, e->sent_len, n, m->A, e->att_mm, st));
+    if (!m->fp32) TRY(att_exp_launch(e->enc_att, b.P * m->A, e->enc_attx, st));
     QNMT_CUDA(cudaMemcpyAsync(e->st_s[0], e->enc_s0, (size_t)n * H * 4, cudaMemcpyDeviceToDevice, st));
     QNMT_CUDA(cudaMemcpyAsync(e->st_sp[0], e->enc_s0, (size_t)n * H * 4, cudaMemcpyDeviceToDevice, st));
     if (e->fq_ok) {   // first step's state codes (later steps get them from gather_q); column n = sentence n
@@ -1363,7 +1368,7 @@ static int decode_core(qnmt_engine* e, const int32_t* src_ids, bool ids_on_devic
     for (int t = 0; t < Tmax && N > 0; ++t) {
         StepIO io{N, n, e->col_sent[cur], e->y[cur], e->st_s[cur], e->st_sp[cur], e->enc_states,
                   e->enc_att, e->sent_row, e->sent_len, Lmax, e->s_int, e->s_new, e->logits, nullptr, 0,
-                  e->col_off, e->P, e->att_mm, beam, e->fq_ok, vocab_fusable(e, k_list)};
+                  e->col_off, e->P, e->att_mm, e->enc_attx, beam, e->fq_ok, vocab_fusable(e, k_list)};
         TRY(step_core(e, io, st));
         TRY(cands_launch(e, io, e->live[cur], k_list, st));
         prof_mark(e, PG_SEARCH, st);
@@ -1420,7 +1425,7 @@ static int decode_ensemble(qnmt_engine* const* es, int nm, const int32_t* src_id
             qnmt_engine* e = es[i];
             StepIO io{N, n, lead->col_sent[cur], lead->y[cur], e->st_s[cur], e->st_sp[cur], e->enc_states,
                       e->enc_att, e->sent_row, e->sent_len, b.Lmax, e->s_int, e->s_new, e->logits, nullptr, 0,
-                      lead->col_off, lead->P, e->att_mm, beam, e->fq_ok, false};
+                      lead->col_off, lead->P, e->att_mm, e->enc_attx, beam, e->fq_ok, false};
             TRY(step_core(e, io, st));
         }
         TRY(ens_topk_launch(rows, nm, N, V, V, lead->live[cur], k_list, lead->cand_score, lead->cand_tok, lead->err,

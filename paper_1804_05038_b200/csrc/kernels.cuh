@@ -26,7 +26,9 @@ int attention_launch(const float* u, int64_t ldu, int64_t N, const int32_t* sent
                      const float* states, const int64_t* sent_row, const int32_t* sent_len, int32_t max_len,
                      int64_t A, int64_t H2, const int8_t* v_codes, const float* v_scale, float* ctx, int64_t ldc,
                      float* alpha, int64_t lda, void* scratch, int32_t* err_flag, cudaStream_t st,
-                     uint32_t* ctx_segmax = nullptr, int max_p = 16);
+                     uint32_t* ctx_segmax = nullptr, int max_p = 16, const float* att_exp = nullptr);
+// E_ap = fl32(e^(2 att_proj)) for the one-MUFU attention scorer (n values)
+int att_exp_launch(const float* att_proj, int64_t n, float* out, cudaStream_t st);
 int att_minmax_launch(const float* att_proj, const int64_t* sent_row, const int32_t* sent_len, int32_t n_sent,
                       int64_t A, float* mm, cudaStream_t st);
 int col_ranges_launch(const int32_t* col_sent, int64_t N, int32_t n_sent, int32_t* off, int32_t* cnt,

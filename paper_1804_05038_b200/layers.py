@@ -287,6 +287,17 @@ class EncoderStates:
     def length(self) -> int:
         return int(self.states_k.shape[0])
 
+    def att_exp_k(self) -> torch.Tensor:
+        """fl32(e^(2 att_proj)) [l][A] for the one-MUFU attention scorer (computed once)."""
+        e = getattr(self, "_att_exp", None)
+        if e is None:
+            ap = self.att_proj_k.contiguous()
+            self.att_proj_k = ap
+            e = torch.empty_like(ap)
+            _lib.call("qnmt_attention_exp", ap.data_ptr(), ap.numel(), e.data_ptr(), _dev.stream_ptr())
+            self._att_exp = e
+        return e
+
 
 def _one_sentence_meta(length, P, dev):
     sent_row = torch.zeros(1, dtype=torch.int64, device=dev)
@@ -307,7 +318,7 @@ def attend_k(att: AttentionNet, q_k: torch.Tensor, enc: EncoderStates):
     ncols = torch.full((1,), P, dtype=torch.int32, device=dev)
     ctx = torch.empty((P, H2), dtype=torch.float32, device=dev)
     alpha = torch.empty((P, length), dtype=torch.float32, device=dev)
-    scratch = torch.empty(P * (length + 2) + 2 * A + 1024, dtype=torch.int32, device=dev)
+    scratch = torch.empty(P * (length + 4) + 2 * A + P * A + 1024, dtype=torch.int32, device=dev)
     v = att.scorer.weight
     if P > 16:
         raise ShapeError("attend supports at most 16 query columns per call")
@@ -318,7 +329,7 @@ def attend_k(att: AttentionNet, q_k: torch.Tensor, enc: EncoderStates):
                   scratch.data_ptr(), _dev.flag().data_ptr(), _dev.stream_ptr())
         return ctx, alpha
     _lib.call("qnmt_attention", u.data_ptr(), A, P, col_off.data_ptr(), ncols.data_ptr(), 1,
-              enc.att_proj_k.data_ptr(), None,
+              enc.att_proj_k.data_ptr(), None, enc.att_exp_k().data_ptr(),
               enc.states_k.data_ptr(), sent_row.data_ptr(), sent_len.data_ptr(), length, A, H2,
               v.device_data().data_ptr(), v.device_scale().data_ptr(), ctx.data_ptr(), H2,
               alpha.data_ptr(), length, scratch.data_ptr(), _dev.flag().data_ptr(), _dev.stream_ptr())
