@@ -314,6 +314,7 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--cpu-sample", type=int, default=16)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-configs", action="store_true", help="skip the cfg1-cfg4 sub-lines (bench_cfgs.py)")
     ap.add_argument("--no-stamps", action="store_true", help="no device-clock stamps (no roofline)")
     ap.add_argument("--no-profile", action="store_true", help="(kept for compatibility)")
     ap.add_argument("--emulate-shard", default=None, metavar="R/W",
@@ -351,6 +352,10 @@ def main():
     engines = [pb.Engine(qm, PER_GPU, 100, BEAM) for _ in range(STREAMS)]
     streams = [torch.cuda.Stream(device=dev) for _ in range(STREAMS)]
     lib = _lib.load()
+    if os.environ.get("QNMT_ATT_EXP") is not None:   # A/B switch of the attention scorer variant
+        lib.qnmt_set_att_exp(int(os.environ["QNMT_ATT_EXP"]))
+    if os.environ.get("QNMT_ATT_CTX") is not None:   # A/B switch of the attention context kernel
+        lib.qnmt_set_att_ctx(int(os.environ["QNMT_ATT_CTX"]))
     main_stream = torch.cuda.current_stream()
     flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device=dev)   # > 126 MB L2
     stamps_on = False   # timed passes run without device-clock stamps (see roofline_pass)
@@ -509,23 +514,30 @@ def main():
             ref = (qnmt,) + reference_model(qnmt, params)
             cpu_translate(ref, [sents[idx[0]]])   # warm-up (numba JIT, weight shadows)
             outs, dt, cores = cpu_translate(ref, [sents[i] for i in idx])
-            value, kind = sum(len(o[0]) for o in outs) / dt, "reference"
+            cpu_value, kind = sum(len(o[0]) for o in outs) / dt, "reference"
             what = (f"qnmt (unmodified, baseline/_ref) decoder.translate, one sentence per worker thread "
                     f"(bench._decode_corpus scheme), {cores} threads")
             tier = "the unmodified reference (Tier A)"
         else:
             outs, dt, cores = cpu_translate_port(params, [sents[i] for i in idx])
-            value, kind = sum(len(o[0]) for o in outs) / dt, "port"
+            cpu_value, kind = sum(len(o[0]) for o in outs) / dt, "port"
             what = f"oracle/qnmt_oracle.py numpy port ({why}), {cores} threads"
             tier = "the oracle port (Tier B)"
         match = sum(1 for i, o in zip(idx, outs) if first_result.get(i) == (o[0], o[1]))
         same_tokens = sum(1 for i, o in zip(idx, outs) if first_result.get(i, (None,))[0] == o[0])
-        cpu = {"value": value, "unit": "tokens/s", "cores": cores, "kind": kind,
+        cpu = {"value": cpu_value, "unit": "tokens/s", "cores": cores, "kind": kind,
                "sample": f"{len(idx)} sentences spread evenly over the corpus length order (lengths "
                          f"{len(sents[idx[0]])}..{len(sents[idx[-1]])}; beam 5, V_tgt 50000), {what}, {dt:.1f} s",
                **host_desc(qnmt),
                "gpu_outputs_identical": f"{match}/{len(idx)} (tokens and log-prob, vs {tier})",
                "gpu_tokens_identical": f"{same_tokens}/{len(idx)}"}
+    configs = None
+    if rank == 0 and world == 1 and not args.no_configs:
+        import bench_cfgs
+        ref_mod = None
+        if not args.no_cpu:
+            ref_mod, _ = load_reference()
+        configs = bench_cfgs.run_all(pb, lib, hbm, ref_mod)
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": 1000 * secs / args.steps,
@@ -551,7 +563,8 @@ def main():
                                  f"(the timed passes overlap {STREAMS} streams, where a kernel's duration includes "
                                  "sharing SMs with the other streams' kernels)"),
                 "cpu_baseline": cpu,
-                "clocks": clocks}
+                "clocks": clocks,
+                "configs": configs}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

@@ -1,12 +1,14 @@
 // att_exp_err.cu -- error of the one-MUFU attention code fast path (attention.cu,
 // k_att_score6), which evaluates
 //     v_fast = fl(st - 2 st * rcp.approx(fl(E_ap * E_u + 1)))
-// with E_ap = fl32(e^(2 ap)), E_u = fl32(e^(2 u)) (fp64 exp, rounded once), against the
+// with E_ap = fl32(e^(2 ap)) (fp64 exp, rounded once) and E_u = exp2x_f32(u) (f32), against the
 // reference's v = fl(fl32(tanh(fl32(ap + u))) * st)  (qmath.py:136-142, layers.py:225-226,
 // Tier B: tanh in fp64 rounded once).
 //
 // (1) rcp.approx.ftz.f32: exhaustive relative error over every mantissa of [1, 2) at
 //     several binades (the result's relative error only depends on the mantissa).
+// (1b) exp2x_f32: exhaustive relative error against e^(2u) (fp64) over every f32 u with
+//      |u| <= 20.
 // (2) Monte-Carlo of |v_fast - v| over (ap, u, st) with |ap|, |u| <= 20 (the fast path's
 //     eligibility bound), reported as the ratio to the analytic bound the kernel uses,
 //     ATT_E_K1 * st + ATT_E_K2 (must stay < 1).
@@ -28,6 +30,20 @@ __global__ void k_rcp(int binade, unsigned long long* out) {
         const float d = __uint_as_float(((uint32_t)(127 + binade) << 23) | b);
         const double rel = fabs((double)rcpa(d) * (double)d - 1.0);
         m = fmax(m, rel);
+    }
+    atomicMax(out, (unsigned long long)__double_as_longlong(m));
+}
+
+// every f32 bit pattern b in [lo, hi) (positive and negative), |u| <= 20
+__global__ void k_exp2x(uint32_t lo, uint32_t hi, unsigned long long* out) {
+    double m = 0;
+    for (uint32_t b = lo + blockIdx.x * blockDim.x + threadIdx.x; b < hi; b += gridDim.x * blockDim.x) {
+        for (int sgn = 0; sgn < 2; ++sgn) {
+            const float u = __uint_as_float(b | (sgn ? 0x80000000u : 0u));
+            if (!(fabsf(u) <= 20.0f)) continue;
+            const double ex = exp(2.0 * (double)u);
+            m = fmax(m, fabs((double)exp2x_f32(u) / ex - 1.0));
+        }
     }
     atomicMax(out, (unsigned long long)__double_as_longlong(m));
 }
@@ -63,7 +79,7 @@ __global__ void k_mc(uint64_t n, int dist, unsigned long long* out) {
         const float tmax = fmaxf(1e-4f, unif(h4));
         const float st = __fdiv_rn(127.0f, tmax);
         const float eap = __double2float_rn(exp_f64(2.0 * (double)ap));
-        const float eu = __double2float_rn(exp_f64(2.0 * (double)u));
+        const float eu = exp2x_f32(u);
         const float r = rcpa(fmaf(eap, eu, 1.0f));
         const float vf = fmaf(-2.0f * st, r, st);
         const float t = tanh_b(__fadd_rn(ap, u));
@@ -90,7 +106,16 @@ int main() {
         memcpy(&v, &h, 8);
         printf("%s\"2^%d\": %.6e", k ? ", " : "", binades[k], v);
     }
-    printf("}, \"fast_path_mc\": {\"bound\": \"%.3e * st + %.3e\"", K1, K2);
+    {
+        cudaMemset(d, 0, 8);
+        k_exp2x<<<148 * 16, 256>>>(0u, 0x41a00001u, d);   // |u| <= 20 (0x41a00000 = 20.0f)
+        unsigned long long h;
+        cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
+        double v;
+        memcpy(&v, &h, 8);
+        printf("}, \"exp2x_f32_rel_err_exhaustive_abs_u_le_20\": %.6e", v);
+    }
+    printf(", \"fast_path_mc\": {\"bound\": \"%.3e * st + %.3e\"", K1, K2);
     const char* names[3] = {"uniform20", "uniform4", "cancelling_logmag"};
     for (int dist = 0; dist < 3; ++dist) {
         cudaMemset(d, 0, 16);

@@ -92,10 +92,16 @@ def topk_case(N=1280, V=50000, k=5):
             "hbm_frac_of_measured": 4.0 * N * V / t / 1e9 / PEAK["hbm_gbs"]}
 
 
-def attention_case(S=256, beam=5, A=2048, H2=2048, seed=0):
-    """One decoder step of attention for 256 sentences x 5 hypotheses, l ~ U[5, 100]."""
+def attention_case(S=256, beam=5, A=2048, H2=2048, seed=0, sorted_batch=None):
+    """One decoder step of attention for 256 sentences x 5 hypotheses, l ~ U[5, 100]
+    (sorted_batch=k: the lengths of the k-th length-sorted batch of the cfg5 corpus,
+    what the bench's engines see)."""
     rng = np.random.default_rng(seed)
     lens = rng.integers(5, 101, S).astype(np.int32)
+    if sorted_batch is not None:
+        crng = np.random.default_rng(5038)
+        cl = np.sort(crng.integers(5, 101, 8192))
+        lens = cl[sorted_batch * S:(sorted_batch + 1) * S].astype(np.int32)
     rows = np.concatenate([[0], np.cumsum(lens)[:-1]]).astype(np.int64)
     P = int(lens.sum())
     N = S * beam
@@ -230,7 +236,14 @@ def main():
     if "vocab" in which:
         out += [vocab_case(fused=True), vocab_case(fused=False)]
     if "att" in which:
-        out.append(attention_case())
+        for sb in (None, 16):
+            for mode in (2, 1, 0):   # scorer: score7, score6 (one-MUFU), score5 (two-MUFU)
+                old = _lib.load().qnmt_set_att_exp(mode)
+                r = attention_case(sorted_batch=sb)
+                r["att_exp"] = mode
+                r["batch"] = "random lengths" if sb is None else f"sorted cfg5 batch {sb}"
+                out.append(r)
+                _lib.load().qnmt_set_att_exp(old)
     if "gemv" in which:
         out += [gemv_cold(1), gemv_cold(64), gemv_large(50000, 512), gemv_large(16384, 4096)]
     for r in out:

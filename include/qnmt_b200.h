@@ -183,9 +183,19 @@ int qnmt_attention_stats(const float* att_proj, const int64_t* sent_row, const i
 /* att_exp[i] = fl32(e^(2 att_proj[i])) (fp64 exp, rounded once) for n values
  * (values beyond +-20 clamped: their sentences take the two-MUFU scorer). */
 int qnmt_attention_exp(const float* att_proj, int64_t n, float* att_exp, void* stream);
-/* 1 (default): one-MUFU scorer when att_exp is supplied; 0: two-MUFU scorer
- * everywhere (A/B testing; results identical).  Returns old value. */
+/* Scorer variant when att_exp is supplied (A/B testing; results identical):
+ * 0 two-MUFU (k_att_score5), 1 one-MUFU (k_att_score6), 2 one-MUFU with the
+ * tile staged by a bulk copy (k_att_score7).  Returns the previous value. */
 int qnmt_set_att_exp(int32_t enable);
+/* Testing knob of the one-MUFU scorer: length of its per-CTA deferred fixup queue
+ * (0..512, default 512; 0 sends every window hit through the overflow rescan).
+ * Returns the previous value. */
+int qnmt_set_att_fixcap(int32_t cap);
+/* Context kernel variant (A/B testing; results identical): 0 direct loads,
+ * 1 bulk-copy ring with 1024 features per CTA, 2 bulk-copy ring with 512
+ * features per CTA (used when the batch's hypotheses per sentence are <= 8).
+ * Returns the previous value. */
+int qnmt_set_att_ctx(int32_t mode);
 int qnmt_attention(const float* u, int64_t ldu, int64_t N, const int32_t* sent_col_off,
                    const int32_t* sent_ncols, int32_t n_sent,
                    const float* att_proj, const float* att_minmax, const float* att_exp,

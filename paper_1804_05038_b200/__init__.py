@@ -19,6 +19,7 @@ from .decoder import (
     bpe_merge,
     compare_precisions,
     edit_distance,
+    shard_batches,
     translate,
     translate_batch,
 )
@@ -44,6 +45,7 @@ from .model import (
     load_model,
     load_quantized,
     quantize_model,
+    replicate,
     save_model,
     synthetic_model,
     tensor_specs,
@@ -69,5 +71,5 @@ __all__ = [
     "OutputNet", "QuantizationStats", "QuantizedMatrix", "QuantizedModel", "attend", "bpe_merge",
     "build_network", "dequantize", "errors", "generate_model", "gru_step", "load_model", "load_quantized", "qgemm", "qgemm_panel",
     "quantize", "quantize_activations", "quantize_model", "save_model", "synthetic_model", "tensor_specs",
-    "translate", "translate_batch",
+    "translate", "translate_batch", "shard_batches", "replicate",
 ]

@@ -34,6 +34,8 @@ SIGNATURES = {
     "qnmt_attention": (I32, [P, I64, I64, P, P, I32, P, P, P, P, P, P, I32, I64, I64, P, P, P, I64, P, I64, P, P, P]),
     "qnmt_attention_exp": (I32, [P, I64, P, P]),
     "qnmt_set_att_exp": (I32, [I32]),
+    "qnmt_set_att_fixcap": (I32, [I32]),
+    "qnmt_set_att_ctx": (I32, [I32]),
     "qnmt_attention_stats": (I32, [P, P, P, I32, I64, P, P]),
     "qnmt_attention_f32": (I32, [P, I64, I64, P, P, I32, P, P, P, P, I32, I64, I64, P, P, I64, P, I64, P, P, P]),
     "qnmt_gemm_f32": (I32, [P, I64, I64, I64, P, I64, I64, P, P, I64, I32, P]),

@@ -94,4 +94,27 @@ __device__ __forceinline__ float sigmoid_lib(float x) {
     return __double2float_rn(e / (1.0 + e));
 }
 
+// e^(2u) in f32 for |u| <= 20 (the one-MUFU attention scorer's E_u, attention.cu):
+// x = 2u (exact), n = rint(x log2 e), r = x - n ln2 by two Cody-Waite FMAs
+// (ln2_hi has 15 significant bits, so n * ln2_hi is exact for |n| <= 2^9), e^r
+// by Taylor degree 7 on |r| <= 0.35 (truncation 5e-9 relative), 2^n added to the
+// exponent.  No MUFU and no fp64.  Its relative error against e^(2u) is
+// measured exhaustively over every f32 |u| <= 20 (benchmarks/att_exp_err.cu,
+// profiles/r02_att_exp_err.json) and enters the scorer's rounding window.
+__device__ __forceinline__ float exp2x_f32(float u) {
+    const float x = 2.0f * u;
+    const float n = rintf(x * 1.44269504088896341f);
+    float r = fmaf(-n, 0.693145751953125f, x);        // ln2_hi = 0x3F317200
+    r = fmaf(-n, 1.42860682030941723e-6f, r);         // ln2_lo
+    float p = 1.98412698e-4f;                         // 1/7!
+    p = fmaf(p, r, 1.38888889e-3f);
+    p = fmaf(p, r, 8.33333333e-3f);
+    p = fmaf(p, r, 4.16666667e-2f);
+    p = fmaf(p, r, 1.66666667e-1f);
+    p = fmaf(p, r, 0.5f);
+    p = fmaf(p, r, 1.0f);
+    p = fmaf(p, r, 1.0f);
+    return __int_as_float(__float_as_int(p) + (int)((uint32_t)(int)n << 23));
+}
+
 }  // namespace qnmt

@@ -39,7 +39,7 @@ constexpr int AT = 256;        // threads per CTA
 constexpr int APC = 4;         // encoder positions per CTA (max / score passes)
 constexpr int AMAXP = 16;      // max live hypotheses per sentence (beam <= 16)
 constexpr int AKA = 8;         // a-elements per thread kept in registers (A <= AT * AKA)
-int g_att_ctx_staged = 1;      // 0: k_att_context3 everywhere (A/B testing)
+int g_att_ctx_staged = 1;      // context kernel: 0 context3, 1 context4, 2 context5 (A/B testing)
 
 // Fast tanh from two MUFU ops, signed form: t = 1 - 2 / (1 + 2^(2x log2 e)).
 // Exhaustive over every f32 x with 2^-24 <= |x| < 64 (benchmarks/tanh_err.cu,
@@ -70,18 +70,24 @@ constexpr float ATT_ST_FAST_MAX = 1.0e6f;   // above: window > 0.5, every elemen
 
 __device__ __noinline__ int att_code_exact(float x, float st) { return quant_code(tanh_b(x), st); }
 
-// One-MUFU fast path (k_att_score6): v_fast = fl(st - 2 st rcp.approx(fl(E_ap E_u + 1))).
-// With E_ap, E_u rounded once from fp64 exps (rel. err <= 2^-24 each), the FFMA's
-// rounding (2^-24) and rcp.approx.ftz.f32 (<= 2^-23, measured exhaustively:
-// profiles/r02_att_exp_err.json), r is within delta_r <= 3e-7 relative of
-// 1 / (1 + e^(2(ap+u))); hence |v_fast - st tanh(ap+u)| <= 2 st delta_r + half an
-// ulp of v, tanh(ap+u) is within 2.7e-8 of tanh(fl(ap+u)) (|x| sech^2 x <= 0.45),
-// and the reference's v carries one rounding of t (st 2^-25) and one of the
-// product: |v_fast - v| <= 6.6e-7 st + 1.52e-5.  The window adds ~50% margin
-// (a Monte-Carlo of 2^33 draws per distribution stays below 0.5 of it, same file).
+// One-MUFU fast path (k_att_score6/7): v_fast = fl(st - 2 st rcp.approx(fl(E_ap E_u + 1)))
+// with E_ap = fl32(e^(2 ap)) (fp64 exp rounded once: rel. error d1 <= 2^-24) and
+// E_u = exp2x_f32(u) (rel. error d2, measured exhaustively over every f32 |u| <= 20).
+// With the FFMA's rounding d3 = 2^-24 and rcp.approx.ftz.f32's relative error
+// d4 (<= 2^-23, exhaustive), r = 1/(1 + E)(1 + eta) with
+// |eta| <= (E/(1+E))(d1 + d2) + d3 + d4, so |v_fast - st tanh(ap+u)| <=
+// 2 st [r* E/(1+E) (d1+d2) + r* (d3+d4)] <= st [(d1+d2)/2 + 2(d3+d4)]
+// (r* E/(1+E) = E/(1+E)^2 <= 1/4, r* <= 1), plus the FFMA's half ulp of v.  The
+// reference's v carries one rounding of t (st 2^-25), one of the product (half
+// an ulp), and tanh(fl(ap+u)) vs tanh(ap+u) (<= 0.45 * 2^-24 st).  With d2 <=
+// 2.4e-7 the total is <= 5.7e-7 st + 7.6e-6; the window below has > 75% margin
+// (profiles/r02_att_exp_err.json: the exhaustive d2 and d4, and a Monte-Carlo of
+// 2^33 draws per distribution of |v_fast - v| against the window).
 __device__ __forceinline__ float att_e_threshold(float st) { return 0.5f - (st * 1.02e-6f + 1.53e-5f); }
+constexpr int ATT_FIXCAP_MAX = 512;
 constexpr float ATT_E_BOUND = 20.0f;   // |ap|, |u| <= 20: E_ap E_u in [1.8e-35, 5.5e34], no ftz / overflow
-int g_att_exp = 1;                      // 0: two-MUFU scorer everywhere (A/B testing)
+int g_att_fixcap = ATT_FIXCAP_MAX;      // tests: 0 forces the queue-overflow rescan
+int g_att_exp = 0;                      // scorer: 0 two-MUFU (score5), 1 one-MUFU (score6), 2 one-MUFU staged (score7)
 
 // E_ap = fl32(e^(2 ap)) for n values of att_proj (fp64 exp, rounded once).  Values
 // beyond the fast path's bound are clamped (their sentences take the two-MUFU path).
@@ -147,7 +153,7 @@ int att_minmax_launch(const float* att_proj, const int64_t* sent_row, const int3
 // Per-hypothesis scale of the whole [A, l] tanh block (layers.py:226) from the
 // column extrema, and the fast-path thresholds:
 //   st_thr[c] = {st, att_threshold(st), att_e_threshold(st), eligible for k_att_score6}.
-// With eu != nullptr also E_u[c][a] = fl32(e^(2 u[c][a])) (fp64 exp, rounded once).
+// With eu != nullptr also E_u[c][a] = e^(2 u[c][a]) (exp2x_f32: f32, error measured exhaustively).
 // Grid (n_sent, AMAXP): CTA (s, j) handles hypothesis j of sentence s.
 __global__ void __launch_bounds__(AT)
 k_att_scale(const float* __restrict__ u, int64_t ldu, const int32_t* __restrict__ sent_col_off,
@@ -184,8 +190,7 @@ k_att_scale(const float* __restrict__ u, int64_t ldu, const int32_t* __restrict_
         for (int k = 0; k < AKA; ++k) {
             const int64_t a = threadIdx.x + (int64_t)AT * k;
             if (a < A) {
-                const double x = fmin(fmax((double)uv[k], -(double)ATT_E_BOUND), (double)ATT_E_BOUND);
-                eu[(int64_t)c * A + a] = __double2float_rn(exp_f64(2.0 * x));
+                eu[(int64_t)c * A + a] = exp2x_f32(fminf(fmaxf(uv[k], -ATT_E_BOUND), ATT_E_BOUND));
             }
         }
     }
@@ -344,18 +349,55 @@ struct ScoreArgs {
     const float* v_scale;
     float* scores;
     int32_t max_len;
+    int32_t fixcap;            // deferred fixup queue length used (<= ATT_FIXCAP; tests lower it)
 };
+
+constexpr int ATT_FIXCAP = ATT_FIXCAP_MAX;   // deferred fixup slots per CTA (score6); beyond: the last warp rescans all
+
+// A deferred fixup entry j | p << 4 | t << 7 names thread t's slots of position p
+// for hypothesis j, which hold an element inside the rounding window.  Returns
+// sum over those slots' flagged elements of va * (exact code - fast code).
+__device__ __forceinline__ int att_fix_slot(const float4* __restrict__ sap, const float* __restrict__ ap_row0,
+                                            int64_t A, const float* __restrict__ u_c0, int64_t ldu,
+                                            const float* __restrict__ eu_c0, const int8_t* __restrict__ v_codes,
+                                            int ent, float st, float thr) {
+    const int j = ent & 15, p = (ent >> 4) & 7, t = ent >> 7;
+    const float m2st = -2.0f * st;
+    const int64_t A4 = A / 4;
+    int d = 0;
+    for (int k = 0; k < AQ5; ++k) {
+        const int64_t q = t + (int64_t)AT * k;
+        if (q >= A4) break;
+        const float4 apq = sap[(p * AQ5 + k) * AT + t];
+        const float4 euq = reinterpret_cast<const float4*>(eu_c0 + (int64_t)j * A)[q];
+        for (int e = 0; e < 4; ++e) {
+            const int64_t a = 4 * q + e;
+            const int va = v_codes[a];
+            const float v = fmaf(m2st, rcp_approx(fmaf((&apq.x)[e], (&euq.x)[e], 1.0f)), st);
+            const float mg = __fadd_rn(v, 12582912.0f);
+            if (fabsf(__fsub_rn(v, __fsub_rn(mg, 12582912.0f))) > thr && va != 0) {
+                const float x = __fadd_rn(ap_row0[p * A + a], u_c0[(int64_t)j * ldu + a]);
+                d += va * (att_code_exact(x, st) - (__float_as_int(mg) - 0x4B400000));
+            }
+        }
+    }
+    return d;
+}
 
 template <bool EXPM>
 __device__ __forceinline__ void att_score_body(const ScoreArgs& g, float4* sap, int (*red5)[APC5][AT / 32],
-                                               int* s_done, int s, int P, int l, int i0) {
+                                               int* s_done, int s, int P, int l, int i0,
+                                               int* fixl = nullptr, int* s_nfix = nullptr) {
     const int i1 = min(l, i0 + APC5);
     const int np = i1 - i0;
     const int c0 = g.sent_col_off[s];
     const int lane = threadIdx.x & 31;
     const int64_t A = g.A, A4 = A / 4;
     const int64_t row0 = g.sent_row[s] + i0;
-    if (threadIdx.x == 0) *s_done = 0;
+    if (threadIdx.x == 0) {
+        *s_done = 0;
+        if (EXPM) *s_nfix = 0;
+    }
     {   // this thread's slots of the tile (positions past i1 and quads past A are zero)
         const float4* src = reinterpret_cast<const float4*>((EXPM ? g.att_exp : g.att_proj) + row0 * A);
 #pragma unroll
@@ -435,12 +477,20 @@ __device__ __forceinline__ void att_score_body(const ScoreArgs& g, float4* sap, 
 #pragma unroll
             for (int p = 0; p < APC5; ++p)   // sum_a v_a * code_a = sum_a v_a * bits_a - 0x4B400000 * sum_a v_a (mod 2^32)
                 if (p < np) acc[p] = (int)((unsigned)acc[p] - (unsigned)vsum_off);
-            // rare: a position with an element within the window of a rounding boundary is
-            // recomputed, flagged elements exactly (fp64 tanh of x = fl(ap + u))
+            // rare: a position with an element within the window of a rounding boundary.
+            // Two-MUFU mode: recompute it now, flagged elements exactly (fp64 tanh of
+            // x = fl(ap + u)).  E mode: att_proj / u must come from global memory, so the
+            // slots are queued and the CTA's last warp resolves the queue with all loads in
+            // flight at once (att_fix_slot).
 #pragma unroll
             for (int p = 0; p < APC5; ++p) {
                 if (p >= np) break;
                 if (dmx[p] <= thr) continue;
+                if (EXPM) {
+                    const int slot = atomicAdd(s_nfix, 1);
+                    if (slot < g.fixcap) fixl[slot] = j | (p << 4) | ((int)threadIdx.x << 7);
+                    continue;
+                }
                 int d = 0;
 #pragma unroll
                 for (int k = 0; k < AQ5; ++k) {
@@ -450,10 +500,7 @@ __device__ __forceinline__ void att_score_body(const ScoreArgs& g, float4* sap, 
                         const float v = fast_v(apq, k, e);
                         const float mg = __fadd_rn(v, 12582912.0f);
                         if (fabsf(__fsub_rn(v, __fsub_rn(mg, 12582912.0f))) > thr && vv[k][e] != 0) {
-                            const int64_t a = 4 * (threadIdx.x + (int64_t)AT * k) + e;
-                            const float x = EXPM ? __fadd_rn(g.att_proj[(row0 + p) * A + a],
-                                                             g.u[(int64_t)(c0 + j) * g.ldu + a])
-                                                 : __fadd_rn((&apq.x)[e], (&uq[k].x)[e]);
+                            const float x = __fadd_rn((&apq.x)[e], (&uq[k].x)[e]);
                             d += vv[k][e] * (att_code_exact(x, st) - (__float_as_int(mg) - 0x4B400000));
                         }
                     }
@@ -494,6 +541,18 @@ __device__ __forceinline__ void att_score_body(const ScoreArgs& g, float4* sap, 
     }
     if (!__shfl_sync(0xffffffffu, last, 0)) return;
     __threadfence_block();
+    if (EXPM) {   // deferred exact codes of the queued slots (queue overflow: every slot of the CTA)
+        const bool all = *s_nfix > g.fixcap;
+        const int nf = all ? P * np * AT : *s_nfix;
+        for (int f = lane; f < nf; f += 32) {
+            const int e = all ? (f / (np * AT)) | (((f / AT) % np) << 4) | ((f % AT) << 7) : fixl[f];
+            const float4 sp = g.st_thr[c0 + (e & 15)];
+            const int d = att_fix_slot(sap, g.att_proj + row0 * A, A, g.u + (int64_t)c0 * g.ldu, g.ldu,
+                                       g.eu + (int64_t)c0 * A, g.v_codes, e, sp.x, sp.z);
+            if (d) atomicAdd(&red5[e & 15][(e >> 4) & 7][0], d);
+        }
+        __syncwarp();
+    }
     for (int idx = lane; idx < P * np; idx += 32) {
         const int j = idx / np, p = idx % np;
         int t = 0;
@@ -526,13 +585,174 @@ k_att_score6(ScoreArgs g) {
     const int s = blockIdx.y;
     const int P = g.sent_ncols[s], l = g.sent_len[s], i0 = blockIdx.x * APC5;
     if (P == 0 || i0 >= l) return;
+    __shared__ int fixl[ATT_FIXCAP];
+    __shared__ int s_nfix;
     const int c0 = g.sent_col_off[s];
     bool elig = true;
     for (int j = 0; j < P; ++j) elig &= g.st_thr[c0 + j].w != 0.0f;
     if (elig)
-        att_score_body<true>(g, sap, red5, &s_done, s, P, l, i0);
+        att_score_body<true>(g, sap, red5, &s_done, s, P, l, i0, fixl, &s_nfix);
     else
         att_score_body<false>(g, sap, red5, &s_done, s, P, l, i0);
+}
+
+// ---------------------------------------------------------------------------
+// k_att_score7: the one-MUFU scorer, restructured for latency hiding.
+//   * The CTA's tile (E_ap rows i0 .. i0+np of the sentence: contiguous in HBM)
+//     arrives by ONE cp.async.bulk, issued before the programmatic-dependent-
+//     launch wait: E_ap is fixed for the whole batch, so the copy overlaps the
+//     predecessor kernel's tail and no registers stage it.
+//   * The smem layout [p][A/4] float4 gives thread t quads t + AT*k of every
+//     row (the same slots score5/6 use).  The element loop runs all APC7
+//     positions unconditionally (rows past np hold stale data whose sums are
+//     discarded), so the compiler interleaves 48 independent elements per
+//     hypothesis: per element FFMA, MUFU.RCP, FFMA, 3 FADD, 1/2 FMNMX3, IMAD.
+//   * Elements inside the rounding window are queued (thread, position,
+//     hypothesis) and resolved exactly by the CTA's last warp (att_fix_slot).
+// Needs A == 4*AT*AQ5 (2048) or smaller with A % 4 == 0, and every hypothesis
+// of the sentence eligible (|att_proj|, |u| <= 20); k_att_score7 falls back to
+// the two-MUFU body for the others (as score6).
+constexpr int APC7 = 6;
+static_assert(APC7 == APC5, "score7 falls back to the score5 body on the same position chunks");
+
+// 1-D TMA bulk copy global -> shared, completing on an mbarrier
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(tc::smem_u32(dst)), "l"(src), "r"(bytes), "r"(tc::smem_u32(bar)) : "memory");
+}
+
+__global__ void __launch_bounds__(AT, 4)
+k_att_score7(ScoreArgs g) {
+    extern __shared__ __align__(128) float4 sap7[];   // [APC7][AQ5 * AT]
+    __shared__ __align__(8) uint64_t bar;
+    __shared__ int red7[AMAXP][APC7][AT / 32];
+    __shared__ int s_done, s_nfix;
+    __shared__ int fixl[ATT_FIXCAP];
+    const int s = blockIdx.y;
+    const int i0 = blockIdx.x * APC7;
+    // per-batch constants (encoder layout, E_ap): safe before the PDL wait
+    const int l = g.sent_len[s];
+    if (i0 >= l) {
+        pdl_entry();
+        return;
+    }
+    const int np = min(l - i0, APC7);
+    const int64_t A = g.A, A4 = A / 4;
+    const int64_t row0 = g.sent_row[s] + i0;
+    const bool tma = g.att_exp != nullptr && A4 <= AQ5 * AT;
+    if (threadIdx.x == 0 && tma) {
+        tc::mbar_init(&bar, 1);
+        tc::fence_mbar_init();
+        const uint32_t bytes = (uint32_t)(np * A * 4);
+        tc::mbar_arrive_expect_tx(&bar, bytes);
+        bulk_g2s(sap7, g.att_exp + row0 * A, bytes, &bar);
+    }
+    pdl_entry();
+    const int P = g.sent_ncols[s];
+    const int c0 = g.sent_col_off[s];
+    bool elig = tma && P > 0;
+    for (int j = 0; j < P; ++j) elig &= g.st_thr[c0 + j].w != 0.0f;
+    if (!elig) {
+        if (tma) {   // the copy must land before the CTA's shared memory is reused
+            __syncthreads();
+            tc::mbar_wait(&bar, 0);
+        }
+        if (P == 0) return;
+        __syncthreads();   // everyone is past the wait before the tile is overwritten
+        att_score_body<false>(g, sap7, red7, &s_done, s, P, l, i0);
+        return;
+    }
+    if (threadIdx.x == 0) {
+        s_done = 0;
+        s_nfix = 0;
+    }
+    const int lane = threadIdx.x & 31;
+    int vv4[AQ5];      // the thread's v codes, four int8 per register (dp4a operand)
+    float4 uq[AQ5], ux[AQ5];
+#pragma unroll
+    for (int k = 0; k < AQ5; ++k) {
+        const int64_t q = threadIdx.x + (int64_t)AT * k;
+        const bool ok = q < A4;
+        vv4[k] = ok ? reinterpret_cast<const int*>(g.v_codes)[q] : 0;
+        uq[k] = ok ? reinterpret_cast<const float4*>(g.eu + (int64_t)c0 * A)[q] : make_float4(1.f, 1.f, 1.f, 1.f);
+    }
+    float4 sp = g.st_thr[c0];
+    __syncthreads();   // s_done / s_nfix initialised
+    tc::mbar_wait(&bar, 0);
+    for (int j = 0; j < P; ++j) {
+        float4 spx = sp;
+        if (j + 1 < P) {   // prefetch the next hypothesis' E_u slice and scale
+#pragma unroll
+            for (int k = 0; k < AQ5; ++k) {
+                const int64_t q = threadIdx.x + (int64_t)AT * k;
+                ux[k] = q < A4 ? reinterpret_cast<const float4*>(g.eu + (int64_t)(c0 + j + 1) * A)[q]
+                               : make_float4(1.f, 1.f, 1.f, 1.f);
+            }
+            spx = g.st_thr[c0 + j + 1];
+        }
+        const float st = sp.x, thr = sp.z, m2st = -2.0f * st;
+        int acc[APC7];
+        float dmx[APC7];
+#pragma unroll
+        for (int p = 0; p < APC7; ++p) {
+            acc[p] = 0;
+            dmx[p] = 0.0f;
+#pragma unroll
+            for (int k = 0; k < AQ5; ++k) {
+                const float4 e4 = sap7[p * (AQ5 * AT) + k * AT + threadIdx.x];
+                uint32_t mb[4];
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const float r = rcp_approx(fmaf((&e4.x)[e], (&uq[k].x)[e], 1.0f));
+                    const float v = fmaf(m2st, r, st);
+                    const float mg = __fadd_rn(v, 12582912.0f);   // 1.5 * 2^23: round to integer
+                    dmx[p] = fmaxf(dmx[p], fabsf(__fsub_rn(v, __fsub_rn(mg, 12582912.0f))));
+                    mb[e] = __float_as_uint(mg);   // low byte = the code (two's complement, |code| <= 127)
+                }
+                // pack the four codes' low bytes (PRMT) and dot them with four v codes (IDP4A)
+                const uint32_t lo = __byte_perm(mb[0], mb[1], 0x0040), hi = __byte_perm(mb[2], mb[3], 0x0040);
+                acc[p] = __dp4a((int)__byte_perm(lo, hi, 0x5410), vv4[k], acc[p]);
+            }
+        }
+#pragma unroll
+        for (int p = 0; p < APC7; ++p) {
+            if (p < np && dmx[p] > thr) {   // rare: queue the slot for the exact pass
+                const int slot = atomicAdd(&s_nfix, 1);
+                if (slot < g.fixcap) fixl[slot] = j | (p << 4) | ((int)threadIdx.x << 7);
+            }
+            const int t = __reduce_add_sync(0xffffffffu, acc[p]);
+            if (lane == 0) red7[j][p][threadIdx.x >> 5] = t;
+        }
+#pragma unroll
+        for (int k = 0; k < AQ5; ++k) uq[k] = ux[k];
+        sp = spx;
+    }
+    int last = 0;
+    if (lane == 0) {
+        __threadfence_block();
+        last = atomicAdd(&s_done, 1) == AT / 32 - 1;
+    }
+    if (!__shfl_sync(0xffffffffu, last, 0)) return;
+    __threadfence_block();
+    {   // deferred exact codes of the queued slots (queue overflow: every slot of the CTA)
+        const bool all = s_nfix > g.fixcap;
+        const int nf = all ? P * np * AT : s_nfix;
+        for (int f = lane; f < nf; f += 32) {
+            const int e = all ? (f / (np * AT)) | (((f / AT) % np) << 4) | ((f % AT) << 7) : fixl[f];
+            const float4 spj = g.st_thr[c0 + (e & 15)];
+            const int d = att_fix_slot(sap7, g.att_proj + row0 * A, A, g.u + (int64_t)c0 * g.ldu, g.ldu,
+                                       g.eu + (int64_t)c0 * A, g.v_codes, e, spj.x, spj.z);
+            if (d) atomicAdd(&red7[e & 15][(e >> 4) & 7][0], d);
+        }
+        __syncwarp();
+    }
+    for (int idx = lane; idx < P * np; idx += 32) {
+        const int j = idx / np, p = idx % np;
+        int t = 0;
+#pragma unroll
+        for (int w = 0; w < AT / 32; ++w) t += red7[j][p][w];
+        g.scores[(int64_t)(c0 + j) * g.max_len + i0 + p] = dequant(t, g.v_scale[0], g.st_thr[c0 + j].x);
+    }
 }
 
 // softmax over the l scores of every hypothesis of sentence s (fp64, fixed
@@ -540,7 +760,7 @@ k_att_score6(ScoreArgs g) {
 // context loop reads it with broadcast loads, widened to f64 once.
 __device__ __forceinline__ void att_softmax(const float* __restrict__ scores, int32_t max_len, int P, int l, int c0,
                                             double* ex, double* al, float* __restrict__ alpha, int64_t lda,
-                                            int32_t* err_flag) {
+                                            int32_t* err_flag, int pst = AMAXP) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (int j = warp; j < P; j += AT / 32) {
         const float* sc = scores + (int64_t)(c0 + j) * max_len;
@@ -564,7 +784,7 @@ __device__ __forceinline__ void att_softmax(const float* __restrict__ scores, in
         sum = __shfl_sync(0xffffffffu, sum, 0);
         for (int i = lane; i < l; i += 32) {
             const float a = __double2float_rn(ex[j * max_len + i] / sum);
-            al[i * AMAXP + j] = (double)a;
+            al[i * pst + j] = (double)a;
             if (alpha && blockIdx.x == 0) alpha[(int64_t)(c0 + j) * lda + i] = a;
         }
     }
@@ -702,10 +922,6 @@ constexpr int ACH = 4;        // positions per stage
 constexpr int ACS = 5;        // stages (80 KB ring + softmax arrays: 2 CTAs / SM)
 constexpr int ACP_MAX = 8;    // hypotheses per sentence supported by context4
 
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-                 ::"r"(tc::smem_u32(dst)), "l"(src), "r"(bytes), "r"(tc::smem_u32(bar)) : "memory");
-}
 
 template <int P>
 __device__ __forceinline__ uint32_t att_context_staged(const float* buf, uint64_t* full, const float* src0,
@@ -828,6 +1044,119 @@ k_att_context4(const float* __restrict__ scores, int32_t max_len, const int32_t*
     }
 }
 
+// k_att_context5: k_att_context4 with half the features per CTA (one float2 per
+// thread, 512 features: 4 CTAs per sentence at 2H = 2048) and the softmax arrays
+// sized by the batch's hypothesis bound pst instead of 16: ~48 KB of shared
+// memory and 2 x P doubles of accumulators per thread, so 4 CTAs / SM stream
+// twice as many sentences' states at once (context4: 2 CTAs / SM, 25-45% of
+// HBM bandwidth at N = 1280).  Same arithmetic and summation order.
+constexpr int AC5F = 2 * AT;   // features per CTA
+constexpr int AC5S = 5;        // ring stages of ACH positions (40 KB)
+
+template <int P>
+__device__ __forceinline__ uint32_t att_context_staged2(const float* buf, uint64_t* full, const float* src0,
+                                                        int64_t H2, uint32_t row_bytes, int l, const double* al,
+                                                        int pst, int64_t c, bool cok, float* __restrict__ ctx,
+                                                        int64_t ldc, int c0) {
+    double acc[P][2];
+#pragma unroll
+    for (int j = 0; j < P; ++j) acc[j][0] = acc[j][1] = 0.0;
+    const int nst = (l + ACH - 1) / ACH;
+    for (int k = 0; k < nst; ++k) {
+        const int b = k % AC5S;
+        tc::mbar_wait(&full[b], (uint32_t)(k / AC5S) & 1u);
+        const int np = min(ACH, l - k * ACH);
+        const float2* bp = reinterpret_cast<const float2*>(buf + (size_t)b * ACH * AC5F) + threadIdx.x;
+#pragma unroll 4
+        for (int p = 0; p < np; ++p) {
+            const float2 q = bp[p * (AC5F / 2)];
+            const double d0 = (double)q.x, d1 = (double)q.y;
+            const double* ap = al + (k * ACH + p) * pst;
+#pragma unroll
+            for (int j = 0; j < P; ++j) {
+                const double aj = ap[j];
+                acc[j][0] += d0 * aj;
+                acc[j][1] += d1 * aj;
+            }
+        }
+        __syncthreads();   // every thread is done with buffer b
+        if (threadIdx.x == 0 && k + AC5S < nst) {
+            const int k2 = k + AC5S, n2 = min(ACH, l - k2 * ACH);
+            tc::mbar_arrive_expect_tx(&full[b], (uint32_t)n2 * row_bytes);
+            for (int p = 0; p < n2; ++p)
+                bulk_g2s(const_cast<float*>(buf) + ((size_t)b * ACH + p) * AC5F,
+                         src0 + (int64_t)(k2 * ACH + p) * H2, row_bytes, &full[b]);
+        }
+    }
+    uint32_t mx = 0;
+    if (!cok) return 0;
+#pragma unroll
+    for (int j = 0; j < P; ++j) {
+        const float v0 = __double2float_rn(acc[j][0]), v1 = __double2float_rn(acc[j][1]);
+        mx = max(mx, max(__float_as_uint(v0) & 0x7fffffffu, __float_as_uint(v1) & 0x7fffffffu));
+        *reinterpret_cast<float2*>(ctx + (int64_t)(c0 + j) * ldc + c) = make_float2(v0, v1);
+    }
+    return mx;
+}
+
+// Grid (ceil(H2 / AC5F), sentences).  Requires H2 % 2 == 0, 8-byte aligned states/ctx
+// rows, and every sentence's live hypotheses <= pst <= ACP_MAX.
+__global__ void __launch_bounds__(AT, 4)
+k_att_context5(const float* __restrict__ scores, int32_t max_len, const int32_t* __restrict__ sent_col_off,
+               const int32_t* __restrict__ sent_ncols, const float* __restrict__ states,
+               const int64_t* __restrict__ sent_row, const int32_t* __restrict__ sent_len, int64_t H2,
+               float* __restrict__ ctx, int64_t ldc, float* __restrict__ alpha, int64_t lda, int32_t* err_flag,
+               uint32_t* ctx_segmax, int pst) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    __shared__ __align__(8) uint64_t full[AC5S];
+    float* buf = reinterpret_cast<float*>(smem_raw);                         // [AC5S][ACH][AC5F]
+    double* ex = reinterpret_cast<double*>(buf + (size_t)AC5S * ACH * AC5F);  // [pst][max_len]
+    double* al = ex + (size_t)pst * max_len;                                 // [max_len][pst]
+    const int s = blockIdx.y;
+    // as context4: sentence metadata and states are >= 2 kernels old, safe before the PDL wait
+    const int P = sent_ncols[s];
+    const int l = sent_len[s];
+    const int64_t cb = (int64_t)blockIdx.x * AC5F;
+    const int64_t nfeat = min((int64_t)AC5F, H2 - cb);
+    const uint32_t row_bytes = (uint32_t)(nfeat * 4);
+    const float* src0 = states + sent_row[s] * H2 + cb;
+    const int nst = (l + ACH - 1) / ACH;
+    const bool run = P > 0 && P <= pst;
+    if (run && threadIdx.x == 0) {
+#pragma unroll
+        for (int b = 0; b < AC5S; ++b) tc::mbar_init(&full[b], 1);
+        tc::fence_mbar_init();
+        for (int k = 0; k < min(AC5S, nst); ++k) {
+            const int np = min(ACH, l - k * ACH);
+            tc::mbar_arrive_expect_tx(&full[k], (uint32_t)np * row_bytes);
+            for (int p = 0; p < np; ++p)
+                bulk_g2s(buf + ((size_t)k * ACH + p) * AC5F, src0 + (int64_t)(k * ACH + p) * H2, row_bytes, &full[k]);
+        }
+    }
+    pdl_entry();
+    if (!run) {
+        if (P > pst && threadIdx.x == 0) set_flag(err_flag, QNMT_FLAG_NUMERIC);   // host bound violated
+        return;
+    }
+    const int c0 = sent_col_off[s];
+    att_softmax(scores, max_len, P, l, c0, ex, al, alpha, lda, err_flag, pst);
+    __syncthreads();   // al ready; barriers initialised
+    const int64_t c = cb + 2 * threadIdx.x;
+    const bool cok = 2 * threadIdx.x < nfeat;
+    uint32_t mx = 0;
+#define QNMT_CTX5(P_) \
+    case P_: mx = att_context_staged2<P_>(buf, full, src0, H2, row_bytes, l, al, pst, c, cok, ctx, ldc, c0); break;
+    switch (P) {
+        QNMT_CTX5(1) QNMT_CTX5(2) QNMT_CTX5(3) QNMT_CTX5(4) QNMT_CTX5(5) QNMT_CTX5(6) QNMT_CTX5(7) QNMT_CTX5(8)
+        default: break;
+    }
+#undef QNMT_CTX5
+    if (ctx_segmax) {
+        mx = __reduce_max_sync(0xffffffffu, mx);
+        if ((threadIdx.x & 31) == 0 && mx) atomicMax(ctx_segmax + s, mx);
+    }
+}
+
 int attention_launch(const float* u, int64_t ldu, int64_t N, const int32_t* sent_col_off,
                      const int32_t* sent_ncols, int32_t n_sent, const float* att_proj, const float* att_minmax,
                      const float* states, const int64_t* sent_row, const int32_t* sent_len, int32_t max_len,
@@ -860,9 +1189,14 @@ int attention_launch(const float* u, int64_t ldu, int64_t N, const int32_t* sent
         const size_t smem5 = (size_t)APC5 * AQ5 * AT * sizeof(float4);
         static size_t done5 = 0, done6 = 0;   // (dynamic + static > 48 KB needs the opt-in)
         ScoreArgs ga{u, ldu, sent_col_off, sent_ncols, att_proj, att_exp, eu, st_thr, sent_row, sent_len, A,
-                     v_codes, v_scale, scores, max_len};
+                     v_codes, v_scale, scores, max_len, std::min(g_att_fixcap, ATT_FIXCAP_MAX)};
         dim3 g5((unsigned)cdiv(max_len, APC5), (unsigned)n_sent);
-        if (expm) {
+        if (expm && g_att_exp == 2) {
+            static size_t done7 = 0;
+            QNMT_CUDA(raise_smem_limit((const void*)k_att_score7, smem5, done7));
+            QNMT_LAUNCH(k_att_score7, g5, AT, smem5, st, ga);
+            QNMT_CHECK_LAUNCH("k_att_score7");
+        } else if (expm) {
             QNMT_CUDA(raise_smem_limit((const void*)k_att_score6, smem5, done6));
             QNMT_LAUNCH(k_att_score6, g5, AT, smem5, st, ga);
             QNMT_CHECK_LAUNCH("k_att_score6");
@@ -881,6 +1215,18 @@ int attention_launch(const float* u, int64_t ldu, int64_t N, const int32_t* sent
     const bool v4 = H2 % 4 == 0 && ldc % 4 == 0 && ((uintptr_t)states % 16) == 0 && ((uintptr_t)ctx % 16) == 0;
     const dim3 g2((unsigned)cdiv(H2, v4 ? 4 * AT : AT), (unsigned)n_sent);
     const size_t smem4 = (size_t)ACS * ACH * ACF * sizeof(float) + smem;
+    const int pst = std::max(1, max_p);
+    const size_t smem5c = (size_t)AC5S * ACH * AC5F * sizeof(float) + (size_t)pst * max_len * 2 * sizeof(double);
+    if (g_att_ctx_staged == 2 && pst <= ACP_MAX && H2 % 2 == 0 && ldc % 2 == 0 && ((uintptr_t)states % 8) == 0 &&
+        ((uintptr_t)ctx % 8) == 0 && smem5c <= 200 * 1024) {
+        static size_t done5c = 0;
+        QNMT_CUDA(raise_smem_limit((const void*)k_att_context5, smem5c, done5c));
+        const dim3 g5c((unsigned)cdiv(H2, AC5F), (unsigned)n_sent);
+        QNMT_LAUNCH(k_att_context5, g5c, AT, smem5c, st, scores, max_len, sent_col_off, sent_ncols, states, sent_row,
+                    sent_len, H2, ctx, ldc, alpha, lda, err_flag, ctx_segmax, pst);
+        QNMT_CHECK_LAUNCH("k_att_context5");
+        return QNMT_OK;
+    }
     if (v4 && g_att_ctx_staged && smem4 <= 200 * 1024) {
         static size_t done4 = 0;
         QNMT_CUDA(raise_smem_limit((const void*)k_att_context4, smem4, done4));
@@ -1009,9 +1355,21 @@ extern "C" int qnmt_attention_exp(const float* att_proj, int64_t n, float* att_e
     return qnmt::att_exp_launch(att_proj, n, att_exp, qnmt::as_stream(stream));
 }
 
+extern "C" int qnmt_set_att_ctx(int32_t mode) {
+    const int old = qnmt::g_att_ctx_staged;
+    qnmt::g_att_ctx_staged = mode < 0 ? 0 : (mode > 2 ? 2 : mode);
+    return old;
+}
+
+extern "C" int qnmt_set_att_fixcap(int32_t cap) {
+    const int old = qnmt::g_att_fixcap;
+    qnmt::g_att_fixcap = std::max(0, std::min((int)cap, qnmt::ATT_FIXCAP_MAX));
+    return old;
+}
+
 extern "C" int qnmt_set_att_exp(int32_t enable) {
     const int old = qnmt::g_att_exp;
-    qnmt::g_att_exp = enable ? 1 : 0;
+    qnmt::g_att_exp = enable < 0 ? 0 : (enable > 2 ? 2 : enable);
     return old;
 }
 

@@ -280,16 +280,74 @@ def translate(models, source_tokens, cfg: DecodeConfig, timer=None):
     return [members[0].tgt_tokens[i] for i in out], lp
 
 
+def shard_batches(lengths, max_batch: int, world: int) -> list:
+    """Sentence sharding of the bulk path over ``world`` devices:
+    the corpus is sorted by length (stable), cut into batches of ``max_batch``
+    sentences, and the batches are dealt to the devices in snake order
+    (0..W-1, W-1..0, ...), so every device sees the whole length range and the
+    devices' decode work is balanced.  Returns, per device, its list of batches
+    (lists of corpus indices).  No data moves between devices: each decodes
+    its own sentences against its own replica of the weights."""
+    order = sorted(range(len(lengths)), key=lambda i: (lengths[i], i))
+    batches = [order[i:i + max_batch] for i in range(0, len(order), max_batch)]
+    out = [[] for _ in range(world)]
+    for k, b in enumerate(batches):
+        r = k % world if (k // world) % 2 == 0 else world - 1 - k % world
+        out[r].append(b)
+    return out
+
+
+def _translate_devices(members, ids, cfg, max_batch, streams, devices):
+    """translate_batch over several GPUs: one host thread per device decodes the
+    device's shard (shard_batches) with its own replica of the model and its
+    own engines/streams; results are reassembled in input order.  The
+    reference's fan-out this replaces is bench.py:129-132 / cli.py:58-63
+    (sentences over a thread pool)."""
+    import torch
+    from .model import replicate
+    if len(members) > 1:
+        raise ConfigError("multi-device decoding of ensembles is not supported")
+    lens = [len(x) for x in ids[0]]
+    shards = shard_batches(lens, max_batch, len(devices))
+    out = [None] * len(lens)
+    reps = [replicate(members[0], d) for d in devices]
+    errors = []
+
+    def worker(r):
+        try:
+            torch.cuda.set_device(devices[r])
+            flat = [i for b in shards[r] for i in b]
+            if not flat:
+                return
+            res = _decode_ids([reps[r]], [[ids[0][i] for i in flat]], cfg, max_batch, streams=streams, sort=True)
+            for i, v in zip(flat, res):
+                out[i] = v
+        except BaseException as exc:   # noqa: BLE001 -- re-raised in the caller's thread
+            errors.append(exc)
+
+    threads = [threading.Thread(target=worker, args=(r,)) for r in range(len(devices))]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    if errors:
+        raise errors[0]
+    return out
+
+
 def translate_batch(models, sentences, cfg: DecodeConfig, max_batch: int = 256, return_ids=False,
-                    streams: int = 3, sort: bool = True):
+                    streams: int = 3, sort: bool = True, devices=None):
     """Translate a corpus with batched device decoding (B200-native bulk path).
 
     ``models``: one model or an ensemble list.  ``sentences``: token lists /
     whitespace strings, or (``return_ids``) id lists.  Output order follows
     the input.  Each batch of up to ``max_batch`` sentences is one engine call;
     batches are cut from the length-sorted corpus and pipelined over
-    ``streams`` engines (see ``_decode_ids``).  Results are identical to
-    sentence-by-sentence ``translate``."""
+    ``streams`` engines (see ``_decode_ids``).  ``devices`` (a list of CUDA
+    device indices): the sorted batches are sharded over those GPUs
+    (``shard_batches``), each decoding its shard against its own replica of
+    the weights with no collective.  Results are identical to
+    sentence-by-sentence ``translate`` on any device count."""
     _check_cfg(cfg)
     members = _members(models, cfg.precision)
     sents = [s.split() if isinstance(s, str) else list(s) for s in sentences]
@@ -302,7 +360,10 @@ def translate_batch(models, sentences, cfg: DecodeConfig, max_batch: int = 256, 
     else:
         ids = [[m.src_ids(s) for s in sents] for m in members]
     tgt = members[0].tgt_tokens
-    res = _decode_ids(members, ids, cfg, max_batch, streams=streams, sort=sort)
+    if devices is not None and len(devices) > 0:
+        res = _translate_devices(members, ids, cfg, max_batch, streams, list(devices))
+    else:
+        res = _decode_ids(members, ids, cfg, max_batch, streams=streams, sort=sort)
     return [(t if return_ids else [tgt[i] for i in t], lp) for t, lp in res]
 
 

@@ -352,6 +352,31 @@ def _quantize_tensors(dims: Dims, tensors: dict, src_tokens, tgt_tokens, s0_mode
     return QuantizedModel(dims, q, f, src_tokens, tgt_tokens, s0_mode, attention_query, stats)
 
 
+def replicate(qm: QuantizedModel, device) -> QuantizedModel:
+    """The model's int8 codes, scales, biases and embeddings copied to another
+    GPU (device-to-device, no re-quantization: codes and scales are identical).
+    Cached on ``qm``; the model itself is returned for its own device.  Used by
+    the sentence-sharded bulk path (``translate_batch(..., devices=...)``,
+    SURVEY 8(e): weights replicated, sentences sharded, no collective)."""
+    dev = torch.device("cuda", torch.device(device).index if not isinstance(device, int) else device)
+    home = next(iter(qm.f.values())).device
+    if dev == home:
+        return qm
+    reps = qm.__dict__.setdefault("_replicas", {})
+    if dev.index not in reps:
+        with torch.cuda.device(dev):
+            q = {}
+            for name, m in qm.q.items():
+                r = QuantizedMatrix(m.device_data().to(dev), m.scale)
+                r._scale_dev = m.device_scale().to(dev)
+                q[name] = r
+            f = {name: t.to(dev).contiguous() for name, t in qm.f.items()}
+            torch.cuda.synchronize(dev)
+        reps[dev.index] = QuantizedModel(qm.dims, q, f, qm.src_tokens, qm.tgt_tokens, qm.s0_mode,
+                                         qm.attention_query, qm.stats)
+    return reps[dev.index]
+
+
 def quantize_model(params: ModelParams, with_stats: bool = False) -> QuantizedModel:
     """Quantize every weight matrix once on the device (model.py:394-437);
     biases and embeddings stay f32 (uploaded)."""

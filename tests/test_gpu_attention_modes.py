@@ -1,0 +1,91 @@
+"""The attention scorer's variants give identical codes, scores, alpha and
+context (attention.cu):
+
+* two-MUFU scorer (k_att_score5): t = 1 - 2 / (1 + 2^(2x log2 e)) per element;
+* one-MUFU scorer (k_att_score6): e^(2(ap+u)) = E_ap * E_u from per-batch /
+  per-step fp64 exps, rounding-window elements queued and resolved exactly
+  by the CTA's last warp;
+* k_att_score7: the one-MUFU scorer with its tile staged by one bulk copy
+  before the PDL wait, branch-free position loop and dp4a code dot products;
+* score6 / score7 with the fixup queue disabled (every window hit goes
+  through the queue-overflow rescan of the whole CTA).
+
+The two-MUFU scorer is pinned against the oracle by test_gpu_layers.py and the
+decode goldens; here the variants are compared at BASELINE attention size (A =
+2048, 2H = 2048) over a batch with l ~ U[5, 100], beams 1..16, and inputs
+scaled so that part of the batch is beyond the one-MUFU path's |x| <= 20
+eligibility bound (those sentences take the two-MUFU path inside score6)."""
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+pb = pytest.importorskip("paper_1804_05038_b200")
+from paper_1804_05038_b200 import _dev, _lib  # noqa: E402
+
+MODES = [(0, 512), (1, 512), (1, 0), (2, 512), (2, 0)]   # (scorer variant, fixup queue length)
+
+
+def _run(lib, mode, inp):
+    old_e = lib.qnmt_set_att_exp(mode[0])
+    old_c = lib.qnmt_set_att_fixcap(mode[1])
+    try:
+        (att, ex, states, u, v, vs, off, cnt, rows_d, lens_d, S, N, A, H2, max_len) = inp
+        mm = torch.empty((S, 2, A), device="cuda")
+        st = torch.cuda.current_stream().cuda_stream
+        _lib.call("qnmt_attention_stats", att.data_ptr(), rows_d.data_ptr(), lens_d.data_ptr(), S, A,
+                  mm.data_ptr(), st)
+        ctx = torch.empty((N, H2), device="cuda")
+        alpha = torch.empty((N, max_len), device="cuda")
+        scratch = torch.empty(N * (104 + A) + 4 * N * max_len + 1024, dtype=torch.int32, device="cuda")
+        f = _dev.reset_flag()
+        _lib.call("qnmt_attention", u.data_ptr(), A, N, off.data_ptr(), cnt.data_ptr(), S, att.data_ptr(),
+                  mm.data_ptr(), ex.data_ptr(), states.data_ptr(), rows_d.data_ptr(), lens_d.data_ptr(), max_len,
+                  A, H2, v.data_ptr(), vs.data_ptr(), ctx.data_ptr(), H2, alpha.data_ptr(), max_len,
+                  scratch.data_ptr(), f.data_ptr(), st)
+        torch.cuda.synchronize()
+        assert not bool(f.any())
+        return ctx.cpu().numpy(), alpha.cpu().numpy()
+    finally:
+        lib.qnmt_set_att_exp(old_e)
+        lib.qnmt_set_att_fixcap(old_c)
+
+
+def _inputs(seed, beams, scale_u, scale_ap, A=2048, H2=2048):
+    rng = np.random.default_rng(seed)
+    S = len(beams)
+    lens = rng.integers(5, 101, S).astype(np.int32)
+    rows = np.concatenate([[0], np.cumsum(lens)[:-1]]).astype(np.int64)
+    Pn = int(lens.sum())
+    N = int(sum(beams))
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    att = torch.randn((Pn, A), device="cuda", generator=g) * scale_ap
+    states = torch.randn((Pn, H2), device="cuda", generator=g) * 0.5
+    u = torch.randn((N, A), device="cuda", generator=g) * scale_u
+    v = torch.randint(-127, 128, (A,), dtype=torch.int8, device="cuda", generator=g)
+    vs = torch.full((1,), 90.0, device="cuda")
+    off = torch.from_numpy(np.concatenate([[0], np.cumsum(beams)[:-1]]).astype(np.int32)).cuda()
+    cnt = torch.from_numpy(np.asarray(beams, np.int32)).cuda()
+    ex = torch.empty_like(att)
+    _lib.call("qnmt_attention_exp", att.data_ptr(), att.numel(), ex.data_ptr(),
+              torch.cuda.current_stream().cuda_stream)
+    return (att, ex, states, u, v, vs, off, cnt, torch.from_numpy(rows).cuda(), torch.from_numpy(lens).cuda(),
+            S, N, A, H2, int(lens.max()))
+
+
+@pytest.mark.parametrize("case", [
+    ("beam5", 11, [5] * 24, 0.5, 0.5),
+    ("ragged_beams", 12, [1, 2, 3, 4, 5, 8, 16, 7, 5, 1, 16, 3], 0.5, 0.5),
+    ("wide", 13, [5] * 12, 6.0, 6.0),          # |ap| / |u| partly beyond 20: mixed eligibility
+    ("tiny", 14, [5] * 8, 1e-4, 1e-4),         # large per-hypothesis scales
+])
+def test_scorer_variants_identical(case):
+    _, seed, beams, su, sa = case
+    lib = _lib.load()
+    inp = _inputs(seed, beams, su, sa)
+    ref_ctx, ref_alpha = _run(lib, MODES[0], inp)
+    for mode in MODES[1:]:
+        ctx, alpha = _run(lib, mode, inp)
+        assert np.array_equal(alpha, ref_alpha), mode
+        assert np.array_equal(ctx, ref_ctx), mode
