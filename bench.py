@@ -354,6 +354,8 @@ def main():
     lib = _lib.load()
     if os.environ.get("QNMT_ATT_EXP") is not None:   # A/B switch of the attention scorer variant
         lib.qnmt_set_att_exp(int(os.environ["QNMT_ATT_EXP"]))
+    if os.environ.get("QNMT_ATT_FS") is not None:   # A/B switch: scale fused into the scorer
+        lib.qnmt_set_att_fused_scale(int(os.environ["QNMT_ATT_FS"]))
     if os.environ.get("QNMT_ATT_CTX") is not None:   # A/B switch of the attention context kernel
         lib.qnmt_set_att_ctx(int(os.environ["QNMT_ATT_CTX"]))
     main_stream = torch.cuda.current_stream()

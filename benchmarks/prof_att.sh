@@ -1,6 +1,11 @@
 mkdir -p gpurun_out
-for cfg in "0 1" "2 1" "2 2"; do set -- $cfg
-  QNMT_ATT_EXP=$1 QNMT_ATT_CTX=$2 timeout 600 python bench.py --no-cpu --no-configs --no-stamps --steps 1 --warmup 3 > gpurun_out/bench_e$1_c$2.json 2>&1
-  python -c "import json;d=json.load(open('gpurun_out/bench_e$1_c$2.json'));print('$1 $2', d['value'], d['ms_per_step'])"
-  QNMT_ATT_EXP=$1 QNMT_ATT_CTX=$2 timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:'k_att_(scale|score|context)' --launch-skip 6000 --launch-count 60 --csv python bench.py --no-cpu --no-configs --no-stamps --steps 1 --warmup 0 > gpurun_out/ncu_att_e$1_c$2.csv 2> gpurun_out/ncu_att_e$1_c$2.err
-done
+timeout 900 python -m pytest tests/test_gpu_qmath.py tests/test_gpu_layers.py -x -q > gpurun_out/t_lin.log 2>&1; tail -3 gpurun_out/t_lin.log
+timeout 300 python -c "
+import sys; sys.path.insert(0,'.')
+import bench_cfgs, paper_1804_05038_b200 as pb, json
+from paper_1804_05038_b200 import _lib
+lib=_lib.load()
+for r in bench_cfgs.cfg1(pb, lib, 6458.7, None):
+    print(r['config'], round(r['us_per_product'],2), round(r['value'],2), r['unit'], r['parity'])
+print(bench_cfgs._copy_floor(3072*1024, 64))
+"

@@ -53,6 +53,8 @@ enum {
 #define QNMT_FLAG_NUMERIC 1   /* non-finite activation (qmath.py:180, layers.py:30/65) */
 #define QNMT_FLAG_INVALID 2   /* non-finite weight (qmath.py:152)                        */
 #define QNMT_FLAG_VOCAB 4     /* token id outside the vocabulary (layers.py:318, :366)    */
+#define QNMT_FLAG_SHARD_TIE 8 /* K7 combine: a row's top-k may hold a token outside the
+                                 shards' lists (f32 score tie); recompute it unsharded   */
 
 /* qmath.py:41 -- int32 accumulation is safe up to this K */
 #define QNMT_INT32_SAFE_K 131000
@@ -77,6 +79,20 @@ int qnmt_quantize(const float* x, int64_t ncols, int64_t K, int64_t ldx,
                   const int32_t* col_seg, int32_t nseg,
                   int8_t* q, int64_t ldq, float* scales, uint32_t* seg_maxbits,
                   int32_t mode, int32_t* err_flag, void* stream);
+
+/* LinearOp.apply of the int8 path (layers.py:124-146): y = W q(x) (+ bias) with
+ * one activation scale over the whole input (quantize_activations,
+ * qmath.py:172-182) and the exact dequant of qnmt_gemm_i8.  X: f32 K-major
+ * [N][ldx]; codes_out [N][ldc] and scale_out[1] receive q(x) and its scale;
+ * maxbits: 1 word of device scratch (general shapes).  N <= 8 (the batch-1
+ * latency path, cfg1) runs as ONE kernel: every CTA quantizes the input into
+ * its shared memory and streams its weight rows (weights prefetched before
+ * the PDL wait with QNMT_GEMM_W_STATIC); larger N: quantize kernels + GEMM.
+ * Non-finite x sets QNMT_FLAG_NUMERIC. */
+int qnmt_linear_i8(const int8_t* W, int64_t M, int64_t K, int64_t ldw, const float* w_scales,
+                   int64_t w_rows_per_scale, const float* X, int64_t N, int64_t ldx, const float* bias,
+                   float* Y, int64_t ldy, int8_t* codes_out, int64_t ldc, float* scale_out,
+                   uint32_t* maxbits, int32_t flags, int32_t* err_flag, void* stream);
 
 /* dequantize (qmath.py:185-187): y = f32(code) / scale, scale a host float */
 int qnmt_dequantize(const int8_t* q, int64_t n, float scale, float* y, void* stream);
@@ -196,6 +212,15 @@ int qnmt_set_att_fixcap(int32_t cap);
  * features per CTA (used when the batch's hypotheses per sentence are <= 8).
  * Returns the previous value. */
 int qnmt_set_att_ctx(int32_t mode);
+/* 1: the two-MUFU scorer computes the per-hypothesis scales in its own CTAs
+ * (k_att_score5f, no k_att_scale launch); 0 (default): separate scale kernel
+ * (A/B testing; results identical).  Returns the previous value. */
+int qnmt_set_att_fused_scale(int32_t enable);
+/* 1: tile-starved tcgen05 products (fewer output tiles than half the SMs)
+ * split K over more CTAs, exact int32 partial sums added in a per-stream
+ * workspace; 0 (default, measured faster at cfg1 B=64): never split (A/B
+ * testing; results identical).  Returns the previous value. */
+int qnmt_set_tc_split(int enable);
 int qnmt_attention(const float* u, int64_t ldu, int64_t N, const int32_t* sent_col_off,
                    const int32_t* sent_ncols, int32_t n_sent,
                    const float* att_proj, const float* att_minmax, const float* att_exp,
@@ -243,6 +268,28 @@ int qnmt_vocab_candidates(const int8_t* X, int64_t N, int64_t ldx, const float* 
                           const double* live_scores, int32_t k, void* scratch, double* cand_score,
                           int32_t* cand_tok, int32_t* err_flag, void* stream);
 int64_t qnmt_vocab_candidates_scratch(int64_t N, int64_t V);
+
+/* ---------------------------------------------------------------------------
+ * K7: vocabulary-sharded output projection (the optional NCCL
+ * variant of layers.py:266 + :60-67 + decoder.py:74-85).  A shard owns W_vocab
+ * rows [tok_off, tok_off + V_shard) (W, bias and the scale pointer passed at
+ * that offset).
+ *   qnmt_vocab_shard_partials: per hypothesis row n, parts[n] = the shard's
+ *     max logit M, S = sum exp(x - M) (fp64) and its top-8 logits by (logit
+ *     desc, token asc) with global token ids (qnmt_vocab_shard_part_bytes()
+ *     bytes per row; scratch: qnmt_vocab_candidates_scratch(N, V_shard)).
+ *   qnmt_vocab_shard_combine: parts = [G][N] (the shards' partials, e.g. after
+ *     an all-gather) -> cand_score/cand_tok [N][k] exactly as
+ *     qnmt_vocab_candidates over the whole vocabulary, unless a row sets
+ *     QNMT_FLAG_SHARD_TIE (then recompute that step unsharded).  G, k <= 16.
+ * ------------------------------------------------------------------------- */
+int64_t qnmt_vocab_shard_part_bytes(void);
+int qnmt_vocab_shard_partials(const int8_t* X, int64_t N, int64_t ldx, const float* x_scales,
+                              const int32_t* row_seg, const int8_t* W, int64_t V_shard, int64_t K, int64_t ldw,
+                              const float* w_scales, int64_t w_rows_per_scale, const float* bias, int64_t tok_off,
+                              void* scratch, void* parts, int32_t* err_flag, void* stream);
+int qnmt_vocab_shard_combine(const void* parts, int32_t G, int64_t N, const double* live_scores, int32_t k,
+                             double* cand_score, int32_t* cand_tok, int32_t* err_flag, void* stream);
 
 /* Embedding gather (layers.py:324, :367): out[n] = table[ids[n]] ([rows][E]);
  * ids outside [0, rows) raise QNMT_FLAG_VOCAB and yield zeros. */

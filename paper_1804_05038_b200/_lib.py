@@ -36,6 +36,9 @@ SIGNATURES = {
     "qnmt_set_att_exp": (I32, [I32]),
     "qnmt_set_att_fixcap": (I32, [I32]),
     "qnmt_set_att_ctx": (I32, [I32]),
+    "qnmt_set_att_fused_scale": (I32, [I32]),
+    "qnmt_set_tc_split": (I32, [I32]),
+    "qnmt_linear_i8": (I32, [P, I64, I64, I64, P, I64, P, I64, I64, P, P, I64, P, I64, P, P, I32, P, P]),
     "qnmt_attention_stats": (I32, [P, P, P, I32, I64, P, P]),
     "qnmt_attention_f32": (I32, [P, I64, I64, P, P, I32, P, P, P, P, I32, I64, I64, P, P, I64, P, I64, P, P, P]),
     "qnmt_gemm_f32": (I32, [P, I64, I64, I64, P, I64, I64, P, P, I64, I32, P]),
@@ -43,6 +46,9 @@ SIGNATURES = {
     "qnmt_topk_candidates": (I32, [P, I64, I64, I64, P, I32, P, P, P, P]),
     "qnmt_vocab_candidates": (I32, [P, I64, I64, P, P, P, I64, I64, I64, P, I64, P, P, I32, P, P, P, P, P]),
     "qnmt_vocab_candidates_scratch": (I64, [I64, I64]),
+    "qnmt_vocab_shard_part_bytes": (I64, []),
+    "qnmt_vocab_shard_partials": (I32, [P, I64, I64, P, P, P, I64, I64, I64, P, I64, P, I64, P, P, P, P]),
+    "qnmt_vocab_shard_combine": (I32, [P, I32, I64, P, I32, P, P, P, P]),
     "qnmt_embed_gather": (I32, [P, I64, I64, P, I64, P, I64, P, P]),
     "qnmt_model_create": (I32, [P, P, I32, P]),
     "qnmt_model_create_f32": (I32, [P, P, I32, P]),

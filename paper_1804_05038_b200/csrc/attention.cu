@@ -86,6 +86,7 @@ __device__ __noinline__ int att_code_exact(float x, float st) { return quant_cod
 __device__ __forceinline__ float att_e_threshold(float st) { return 0.5f - (st * 1.02e-6f + 1.53e-5f); }
 constexpr int ATT_FIXCAP_MAX = 512;
 constexpr float ATT_E_BOUND = 20.0f;   // |ap|, |u| <= 20: E_ap E_u in [1.8e-35, 5.5e34], no ftz / overflow
+int g_att_fused_scale = 0;             // 1: two-MUFU scorer computes the scales itself (k_att_score5f; A/B: 125 vs 101 + 11 us)
 int g_att_fixcap = ATT_FIXCAP_MAX;      // tests: 0 forces the queue-overflow rescan
 int g_att_exp = 0;                      // scorer: 0 two-MUFU (score5), 1 one-MUFU (score6), 2 one-MUFU staged (score7)
 
@@ -387,13 +388,15 @@ __device__ __forceinline__ int att_fix_slot(const float4* __restrict__ sap, cons
 template <bool EXPM>
 __device__ __forceinline__ void att_score_body(const ScoreArgs& g, float4* sap, int (*red5)[APC5][AT / 32],
                                                int* s_done, int s, int P, int l, int i0,
-                                               int* fixl = nullptr, int* s_nfix = nullptr) {
+                                               int* fixl = nullptr, int* s_nfix = nullptr,
+                                               const float4* stv = nullptr) {
     const int i1 = min(l, i0 + APC5);
     const int np = i1 - i0;
     const int c0 = g.sent_col_off[s];
     const int lane = threadIdx.x & 31;
     const int64_t A = g.A, A4 = A / 4;
     const int64_t row0 = g.sent_row[s] + i0;
+    const float4* sv = stv ? stv : g.st_thr + g.sent_col_off[s];   // per-hypothesis {st, thresholds} of the sentence
     if (threadIdx.x == 0) {
         *s_done = 0;
         if (EXPM) *s_nfix = 0;
@@ -421,7 +424,7 @@ __device__ __forceinline__ void att_score_body(const ScoreArgs& g, float4* sap, 
         vv[k][0] = c.x; vv[k][1] = c.y; vv[k][2] = c.z; vv[k][3] = c.w;
         uq[k] = ok ? reinterpret_cast<const float4*>(qsrc + (int64_t)c0 * ldq)[q] : make_float4(0.f, 0.f, 0.f, 0.f);
     }
-    float4 sp = g.st_thr[c0];
+    float4 sp = sv[0];
     int vsum = 0;
 #pragma unroll
     for (int k = 0; k < AQ5; ++k) vsum += vv[k][0] + vv[k][1] + vv[k][2] + vv[k][3];
@@ -436,7 +439,7 @@ __device__ __forceinline__ void att_score_body(const ScoreArgs& g, float4* sap, 
                 ux[k] = q < A4 ? reinterpret_cast<const float4*>(qsrc + (int64_t)(c0 + j + 1) * ldq)[q]
                                : make_float4(0.f, 0.f, 0.f, 0.f);
             }
-            spx = g.st_thr[c0 + j + 1];
+            spx = sv[j + 1];
         }
         const float st = sp.x, thr = EXPM ? sp.z : sp.y, m2st = -2.0f * st;
         int acc[APC5];
@@ -546,7 +549,7 @@ __device__ __forceinline__ void att_score_body(const ScoreArgs& g, float4* sap, 
         const int nf = all ? P * np * AT : *s_nfix;
         for (int f = lane; f < nf; f += 32) {
             const int e = all ? (f / (np * AT)) | (((f / AT) % np) << 4) | ((f % AT) << 7) : fixl[f];
-            const float4 sp = g.st_thr[c0 + (e & 15)];
+            const float4 sp = sv[e & 15];
             const int d = att_fix_slot(sap, g.att_proj + row0 * A, A, g.u + (int64_t)c0 * g.ldu, g.ldu,
                                        g.eu + (int64_t)c0 * A, g.v_codes, e, sp.x, sp.z);
             if (d) atomicAdd(&red5[e & 15][(e >> 4) & 7][0], d);
@@ -558,7 +561,7 @@ __device__ __forceinline__ void att_score_body(const ScoreArgs& g, float4* sap, 
         int t = 0;
 #pragma unroll
         for (int w = 0; w < AT / 32; ++w) t += red5[j][p][w];
-        g.scores[(int64_t)(c0 + j) * g.max_len + i0 + p] = dequant(t, g.v_scale[0], g.st_thr[c0 + j].x);
+        g.scores[(int64_t)(c0 + j) * g.max_len + i0 + p] = dequant(t, g.v_scale[0], sv[j].x);
     }
 }
 
@@ -573,6 +576,68 @@ k_att_score5(ScoreArgs g) {
     const int P = g.sent_ncols[s], l = g.sent_len[s], i0 = blockIdx.x * APC5;
     if (P == 0 || i0 >= l) return;
     att_score_body<false>(g, sap, red5, &s_done, s, P, l, i0);
+}
+
+// two-MUFU scorer with the per-hypothesis scale computed in the CTA (no k_att_scale
+// launch): every CTA of sentence s reduces max_a max(|fl(mx_a + u_a)|, |fl(mn_a + u_a)|)
+// for each of the sentence's hypotheses from its own quads (a warp max, a shared-memory
+// atomicMax), then thread j evaluates fl32(tanh) of the max and the scale (identical to
+// k_att_scale: the same operations, so every CTA of the sentence gets the same st).
+// The CTA with blockIdx.x == 0 also zeroes the context kernel's per-sentence max.
+__global__ void __launch_bounds__(AT, 4)
+k_att_score5f(ScoreArgs g, const float* __restrict__ mm, int32_t* err_flag, uint32_t* zero_seg) {
+    pdl_entry();
+    extern __shared__ float4 sap[];   // [APC5][AQ5][AT]
+    __shared__ int red5[AMAXP][APC5][AT / 32];
+    __shared__ int s_done;
+    __shared__ uint32_t s_m[AMAXP];
+    __shared__ float4 s_st[AMAXP];
+    const int s = blockIdx.y;
+    if (zero_seg && blockIdx.x == 0 && threadIdx.x == 0) zero_seg[s] = 0u;
+    const int P = g.sent_ncols[s], l = g.sent_len[s], i0 = blockIdx.x * APC5;
+    if (P == 0 || i0 >= l) return;
+    const int c0 = g.sent_col_off[s];
+    const int64_t A = g.A, A4 = A / 4;
+    if (threadIdx.x < AMAXP) s_m[threadIdx.x] = 0u;
+    float4 mxq[AQ5], mnq[AQ5];
+#pragma unroll
+    for (int k = 0; k < AQ5; ++k) {
+        const int64_t q = threadIdx.x + (int64_t)AT * k;
+        const bool ok = q < A4;
+        mxq[k] = ok ? reinterpret_cast<const float4*>(mm + (int64_t)s * 2 * A)[q] : make_float4(0.f, 0.f, 0.f, 0.f);
+        mnq[k] = ok ? reinterpret_cast<const float4*>(mm + (int64_t)s * 2 * A + A)[q] : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    __syncthreads();   // s_m initialised
+    for (int j = 0; j < P; ++j) {
+        uint32_t m = 0;
+#pragma unroll
+        for (int k = 0; k < AQ5; ++k) {
+            const int64_t q = threadIdx.x + (int64_t)AT * k;
+            if (q < A4) {
+                const float4 uv = reinterpret_cast<const float4*>(g.u + (int64_t)(c0 + j) * g.ldu)[q];
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    m = max(m, __float_as_uint(__fadd_rn((&mxq[k].x)[e], (&uv.x)[e])) & 0x7fffffffu);
+                    m = max(m, __float_as_uint(__fadd_rn((&mnq[k].x)[e], (&uv.x)[e])) & 0x7fffffffu);
+                }
+            }
+        }
+        m = __reduce_max_sync(0xffffffffu, m);
+        if ((threadIdx.x & 31) == 0) atomicMax(&s_m[j], m);
+    }
+    __syncthreads();
+    if (threadIdx.x < P) {
+        uint32_t m = s_m[threadIdx.x];
+        if (m >= 0x7f800000u) {
+            if (blockIdx.x == 0) set_flag(err_flag, QNMT_FLAG_NUMERIC);
+            m = 0;
+        }
+        const float tmax = tanh_b(__uint_as_float(m));   // max |fl32(tanh)| = fl32(tanh(max |x|))
+        const float st = (tmax == 0.0f) ? 1.0f : __fdiv_rn(127.0f, tmax);
+        s_st[threadIdx.x] = make_float4(st, att_threshold(st), att_e_threshold(st), 0.0f);
+    }
+    __syncthreads();
+    att_score_body<false>(g, sap, red5, &s_done, s, P, l, i0, nullptr, nullptr, s_st);
 }
 
 // one-MUFU scorer where every live hypothesis of the sentence is eligible, else two-MUFU
@@ -1181,7 +1246,18 @@ int attention_launch(const float* u, int64_t ldu, int64_t N, const int32_t* sent
     const bool quads = A % 4 == 0 && ldu % 4 == 0 && A <= 4 * AT * AQ5 && ((uintptr_t)u % 16) == 0 &&
                        ((uintptr_t)att_proj % 16) == 0 && ((uintptr_t)v_codes % 4) == 0;
     const bool expm = quads && att_exp != nullptr && g_att_exp && ((uintptr_t)att_exp % 16) == 0;
+    const bool fused_scale = quads && !expm && g_att_fused_scale && ((uintptr_t)att_minmax % 16) == 0;
     float* eu = expm ? tail : nullptr;
+    if (fused_scale) {   // k_att_score5f computes the scales itself
+        const size_t smem5 = (size_t)APC5 * AQ5 * AT * sizeof(float4);
+        static size_t done5f = 0;
+        QNMT_CUDA(raise_smem_limit((const void*)k_att_score5f, smem5, done5f));
+        ScoreArgs ga{u, ldu, sent_col_off, sent_ncols, att_proj, att_exp, nullptr, st_thr, sent_row, sent_len, A,
+                     v_codes, v_scale, scores, max_len, 0};
+        dim3 g5((unsigned)cdiv(max_len, APC5), (unsigned)n_sent);
+        QNMT_LAUNCH(k_att_score5f, g5, AT, smem5, st, ga, att_minmax, err_flag, ctx_segmax);
+        QNMT_CHECK_LAUNCH("k_att_score5f");
+    } else {
     QNMT_LAUNCH(k_att_scale, dim3((unsigned)n_sent, AMAXP), AT, 0, st, u, ldu, sent_col_off, sent_ncols, att_minmax, A,
                 st_thr, err_flag, ctx_segmax, eu);
     QNMT_CHECK_LAUNCH("k_att_scale");
@@ -1211,6 +1287,7 @@ int attention_launch(const float* u, int64_t ldu, int64_t N, const int32_t* sent
                                         v_codes, v_scale, scores, max_len);
         QNMT_CHECK_LAUNCH("k_att_score4");
     }
+    }   // !fused_scale
     const size_t smem = (size_t)AMAXP * max_len * 2 * sizeof(double);
     const bool v4 = H2 % 4 == 0 && ldc % 4 == 0 && ((uintptr_t)states % 16) == 0 && ((uintptr_t)ctx % 16) == 0;
     const dim3 g2((unsigned)cdiv(H2, v4 ? 4 * AT : AT), (unsigned)n_sent);
@@ -1353,6 +1430,12 @@ extern "C" int qnmt_attention(const float* u, int64_t ldu, int64_t N, const int3
 
 extern "C" int qnmt_attention_exp(const float* att_proj, int64_t n, float* att_exp, void* stream) {
     return qnmt::att_exp_launch(att_proj, n, att_exp, qnmt::as_stream(stream));
+}
+
+extern "C" int qnmt_set_att_fused_scale(int32_t enable) {
+    const int old = qnmt::g_att_fused_scale;
+    qnmt::g_att_fused_scale = enable ? 1 : 0;
+    return old;
 }
 
 extern "C" int qnmt_set_att_ctx(int32_t mode) {

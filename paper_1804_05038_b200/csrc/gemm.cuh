@@ -28,6 +28,9 @@ struct GemmArgs {
 int gemm_i8_launch(const GemmArgs& g, cudaStream_t st);
 bool tc_eligible(const GemmArgs& g);
 int gemm_tc_launch(const GemmArgs& g, cudaStream_t st);
+// size the stream's split-K workspace before graph capture ([N][M] int32 + tile counters)
+int tc_split_reserve(cudaStream_t st, int64_t ws_elems, int64_t tiles);
+extern int g_tc_split;
 extern int g_gemm_impl;   // 0 auto, 1 CUDA-core dp4a only, 2 tcgen05 whenever eligible
 
 int quantize_launch(const float* x, int64_t ncols, int64_t K, int64_t ldx, const int32_t* col_seg,

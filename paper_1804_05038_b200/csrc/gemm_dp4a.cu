@@ -133,6 +133,150 @@ k_gemv(const int8_t* __restrict__ W, int64_t M, int64_t K, int64_t ldw,
 }
 
 // ---------------------------------------------------------------------------
+// LinearOp.apply for the batch-1 latency path (layers.py:124-146: quantize_activations,
+// qgemm_panel, + bias) as ONE kernel for N <= 8 columns: every CTA reduces max|x| over
+// the [N][K] f32 input itself (N*K*4 bytes, L2-resident: 4 KB at batch 1), derives the
+// per-call scale (qmath.py:172-182: s = fl32(127 / max), 1 when max = 0), encodes its own
+// copy of the codes into shared memory (qmath.py:119-133), and streams its weight rows
+// exactly as k_gemv (rows prefetched before the PDL wait).  CTA 0 also writes the codes
+// and the scale.  One launch instead of three (max scan, encode, GEMV).
+// ---------------------------------------------------------------------------
+template <int ROWS, int NC, int U>
+__global__ void __launch_bounds__(256)
+k_linear_gemv(const int8_t* __restrict__ W, int64_t M, int64_t K, int64_t ldw, const float* __restrict__ Xf,
+              int64_t ldxf, int N, EpiArgs e, int w_static, int8_t* __restrict__ codes_out, int64_t ldc,
+              float* __restrict__ scale_out, int32_t* err_flag) {
+    extern __shared__ __align__(16) int8_t xq[];   // [NC][K] codes
+    __shared__ uint32_t s_red[8];
+    __shared__ float s_scale;
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    const int64_t row0 = ((int64_t)blockIdx.x * 8 + warp) * ROWS;
+    const int64_t nch = K >> 4;
+    int4 w[U][ROWS];
+    auto load_w = [&](int64_t c0) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t c = c0 + 32 * u;
+#pragma unroll
+            for (int r = 0; r < ROWS; ++r)
+                w[u][r] = (c < nch && row0 + r < M) ? ld_stream16(W + (row0 + r) * ldw + (c << 4))
+                                                    : make_int4(0, 0, 0, 0);
+        }
+    };
+    pdl_trigger();
+    if (w_static) {
+        load_w(lane);
+        pdl_wait();
+    } else {
+        pdl_wait();
+        load_w(lane);
+    }
+    // max |x| over the N x K input (float4 rows: K % 16 == 0, ldxf % 4 == 0)
+    const int64_t K4 = K >> 2;
+    uint32_t mb = 0;
+    for (int64_t i = threadIdx.x; i < (int64_t)N * K4; i += 256) {
+        const int64_t n = i / K4, k4 = i - n * K4;
+        const float4 v = reinterpret_cast<const float4*>(Xf + n * ldxf)[k4];
+        mb = max(mb, max(max(__float_as_uint(v.x) & 0x7fffffffu, __float_as_uint(v.y) & 0x7fffffffu),
+                         max(__float_as_uint(v.z) & 0x7fffffffu, __float_as_uint(v.w) & 0x7fffffffu)));
+    }
+    mb = __reduce_max_sync(0xffffffffu, mb);
+    if (lane == 0) s_red[warp] = mb;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t m = 0;
+        for (int i = 0; i < 8; ++i) m = max(m, s_red[i]);
+        if (m >= 0x7f800000u) {   // non-finite activation (qmath.py:180)
+            if (blockIdx.x == 0) set_flag(err_flag, QNMT_FLAG_NUMERIC);
+            m = 0;
+        }
+        s_scale = scale_from_maxbits(m);
+        if (blockIdx.x == 0 && scale_out) *scale_out = s_scale;
+    }
+    __syncthreads();
+    const float sx = s_scale;
+    for (int64_t i = threadIdx.x; i < (int64_t)N * K4; i += 256) {
+        const int64_t n = i / K4, k4 = i - n * K4;
+        const float4 v = reinterpret_cast<const float4*>(Xf + n * ldxf)[k4];
+        const char4 c = make_char4((signed char)quant_code(v.x, sx), (signed char)quant_code(v.y, sx),
+                                   (signed char)quant_code(v.z, sx), (signed char)quant_code(v.w, sx));
+        reinterpret_cast<char4*>(xq + n * K)[k4] = c;
+        if (blockIdx.x == 0 && codes_out) reinterpret_cast<char4*>(codes_out + n * ldc)[k4] = c;
+    }
+    __syncthreads();
+    if (row0 >= M) return;
+    int acc[ROWS][NC];
+#pragma unroll
+    for (int r = 0; r < ROWS; ++r)
+#pragma unroll
+        for (int j = 0; j < NC; ++j) acc[r][j] = 0;
+    for (int64_t c0 = lane; c0 < nch; c0 += 32 * U) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t c = c0 + 32 * u;
+            if (c < nch) {
+#pragma unroll
+                for (int j = 0; j < NC; ++j) {
+                    const int4 xv = *reinterpret_cast<const int4*>(xq + j * K + (c << 4));
+#pragma unroll
+                    for (int r = 0; r < ROWS; ++r) acc[r][j] = dp4a16(acc[r][j], w[u][r], xv);
+                }
+            }
+        }
+        if (c0 + 32 * U < nch) load_w(c0 + 32 * U);
+    }
+#pragma unroll
+    for (int r = 0; r < ROWS; ++r)
+#pragma unroll
+        for (int j = 0; j < NC; ++j) acc[r][j] = warp_sum(acc[r][j]);
+    e.x_scales = &s_scale;   // the epilogue's activation scale: this CTA's (identical in every CTA)
+    e.col_seg = nullptr;
+#pragma unroll
+    for (int t = 0; t < ROWS * NC; ++t) {
+        if ((t & 31) == lane) {
+            const int r = t / NC, j = t % NC;
+            if (row0 + r < M && j < N) epilogue(e, row0 + r, j, (long long)acc[r][j]);
+        }
+    }
+}
+
+template <int ROWS, int NC>
+static int launch_linear(const int8_t* W, int64_t M, int64_t K, int64_t ldw, const float* Xf, int64_t ldxf, int N,
+                         const EpiArgs& e, int8_t* codes, int64_t ldc, float* scale, int32_t* err, cudaStream_t st) {
+    const unsigned grid = (unsigned)cdiv(M, 8 * ROWS);
+    const int w_static = (e.flags & QNMT_GEMM_W_STATIC) ? 1 : 0;
+    const size_t smem = (size_t)NC * K;
+    if (K >= 2048 && NC <= 2) {
+        static size_t done = 0;
+        QNMT_CUDA(raise_smem_limit((const void*)k_linear_gemv<ROWS, NC, 4>, smem, done));
+        QNMT_LAUNCH((k_linear_gemv<ROWS, NC, 4>), grid, 256, smem, st, W, M, K, ldw, Xf, ldxf, N, e, w_static,
+                    codes, ldc, scale, err);
+    } else {
+        static size_t done = 0;
+        QNMT_CUDA(raise_smem_limit((const void*)k_linear_gemv<ROWS, NC, 2>, smem, done));
+        QNMT_LAUNCH((k_linear_gemv<ROWS, NC, 2>), grid, 256, smem, st, W, M, K, ldw, Xf, ldxf, N, e, w_static,
+                    codes, ldc, scale, err);
+    }
+    QNMT_CHECK_LAUNCH("k_linear_gemv");
+    return QNMT_OK;
+}
+
+template <int ROWS>
+static int dispatch_linear(const int8_t* W, int64_t M, int64_t K, int64_t ldw, const float* Xf, int64_t ldxf, int N,
+                           const EpiArgs& e, int8_t* codes, int64_t ldc, float* scale, int32_t* err, cudaStream_t st) {
+#define QNMT_LIN(NC_) \
+    case NC_: return launch_linear<ROWS, NC_>(W, M, K, ldw, Xf, ldxf, N, e, codes, ldc, scale, err, st);
+    switch (N) {
+        QNMT_LIN(1) QNMT_LIN(2) QNMT_LIN(3) QNMT_LIN(4) QNMT_LIN(5) QNMT_LIN(6) QNMT_LIN(7) QNMT_LIN(8)
+        default: break;
+    }
+#undef QNMT_LIN
+    set_error("linear: N=%d > 8", N);
+    return QNMT_ERR_CONFIG;
+}
+
+// ---------------------------------------------------------------------------
 // Tiled dp4a GEMM: 64(M) x 64(N) x 64(K) tiles, 256 threads, 4x4 per thread
 // ---------------------------------------------------------------------------
 constexpr int TBM = 64, TBN = 64, TBK = 64;
@@ -310,4 +454,37 @@ extern "C" int qnmt_gemm_i8(const int8_t* W, int64_t M, int64_t K, int64_t ldw,
     qnmt::GemmArgs g{W, M, K, ldw, w_scales, w_rows_per_scale, X, N, ldx, x_scales, col_seg,
                      bias, Y, ldy, acc_out, flags};
     return qnmt::gemm_i8_launch(g, qnmt::as_stream(stream));
+}
+
+extern "C" int qnmt_linear_i8(const int8_t* W, int64_t M, int64_t K, int64_t ldw, const float* w_scales,
+                              int64_t w_rows_per_scale, const float* X, int64_t N, int64_t ldx, const float* bias,
+                              float* Y, int64_t ldy, int8_t* codes_out, int64_t ldc, float* scale_out,
+                              uint32_t* maxbits, int32_t flags, int32_t* err_flag, void* stream) {
+    if (M < 0 || N < 0 || K < 1 || ldw < K || ldx < K || ldc < K || (Y && ldy < M) || w_rows_per_scale < 1) {
+        qnmt::set_error("qnmt_linear_i8: bad shape M=%lld N=%lld K=%lld", (long long)M, (long long)N, (long long)K);
+        return QNMT_ERR_SHAPE;
+    }
+    if (M == 0 || N == 0) return QNMT_OK;
+    const cudaStream_t st = qnmt::as_stream(stream);
+    const bool fused = N <= 8 && K % 16 == 0 && ldw % 16 == 0 && ldx % 4 == 0 && ldc % 4 == 0 &&
+                       (uintptr_t)W % 16 == 0 && (uintptr_t)X % 16 == 0 && (uintptr_t)codes_out % 4 == 0 &&
+                       N * K <= 96 * 1024 && K <= QNMT_INT32_SAFE_K && codes_out != nullptr && scale_out != nullptr;
+    if (fused) {
+        qnmt::EpiArgs e{w_scales, w_rows_per_scale, nullptr, nullptr, bias, Y, ldy, nullptr, M, flags,
+                        nullptr, 0, nullptr, 0};
+        return K <= 512 ? qnmt::dispatch_linear<4>(W, M, K, ldw, X, ldx, (int)N, e, codes_out, ldc, scale_out,
+                                                  err_flag, st)
+                        : qnmt::dispatch_linear<2>(W, M, K, ldw, X, ldx, (int)N, e, codes_out, ldc, scale_out,
+                                                  err_flag, st);
+    }
+    // general shapes: the activation quantize kernels, then the product
+    if (!codes_out || !scale_out || !maxbits) {
+        qnmt::set_error("qnmt_linear_i8: codes_out, scale_out and maxbits are required");
+        return QNMT_ERR_CONFIG;
+    }
+    int rc = qnmt_quantize(X, N, K, ldx, nullptr, 1, codes_out, ldc, scale_out, maxbits, 1, err_flag, stream);
+    if (rc != QNMT_OK) return rc;
+    qnmt::GemmArgs g{W, M, K, ldw, w_scales, w_rows_per_scale, codes_out, N, ldc, scale_out, nullptr,
+                     bias, Y, ldy, nullptr, flags};
+    return qnmt::gemm_i8_launch(g, st);
 }

@@ -18,6 +18,7 @@
 //               fl32(acc / (sw*sx)) (reciprocal fast path, __ddiv_rn near f32
 //               midpoints) -> +bias -> (+Y) -> coalesced f32 stores of Y[n][m].
 // Tiles are visited n-fastest so consecutive CTAs share the W block in L2.
+#include <algorithm>
 #include <cstdlib>
 #include <mutex>
 #include <unordered_map>
@@ -78,11 +79,60 @@ __device__ __forceinline__ void tile_coords(int tile, int m_blocks, int n_blocks
     nb = r / gm;
 }
 
+// Split-K (k_gemm_tc with ksplit > 1): each split adds its int32 partial tile into the
+// per-stream workspace ws[n][m] (RED.ADD, exact and order-free), then counts itself in
+// cnt[tile]; the split that arrives last re-reads the complete sums, runs the normal
+// dequant epilogue, and leaves ws and cnt zeroed for the next product.
+struct TcSplit {
+    int ksplit;
+    int32_t* ws;
+    int32_t* cnt;
+};
+
+// one 16-column chunk of the dequant epilogue from int32 accumulators already in registers
+template <int EPI>
+__device__ __forceinline__ void tc_epi_chunk(const TcEpi& e, const uint32_t (&r)[16], int m, bool mok, int nbase,
+                                             int ncols, int M, float sw, float bias, double isw, const float* csx,
+                                             const double* cisx) {
+    float* yrow = e.Y + (int64_t)nbase * e.ldy + m;
+    if (EPI & EPI_RAW) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+            if (mok && j < ncols) e.acc_out[(int64_t)(nbase + j) * M + m] = (int)r[j];
+        if (e.Y == nullptr) return;
+    }
+    uint32_t unsafe = 0;
+    float yd[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+        const double q = i2d_exact((int)r[j]) * (isw * cisx[j]);
+        yd[j] = __double2float_rn(q);
+        unsafe |= (uint32_t)(!dequant_rcp_safe(q)) << j;
+    }
+    if (__any_sync(0xffffffffu, unsafe != 0)) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+            if ((unsafe >> j) & 1u) yd[j] = dequant((int)r[j], sw, csx[j]);
+    }
+    if (!mok) return;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+        if (j >= ncols) break;
+        float y = yd[j];
+        if (EPI & EPI_BIAS) y = __fadd_rn(y, bias);
+        if (EPI & EPI_ACCUMULATE) y = __fadd_rn(yrow[(int64_t)j * e.ldy], y);
+        if (EPI & EPI_ADD2)
+            y = __fadd_rn(__fadd_rn(y, e.add1[(int64_t)(nbase + j) * e.ld1 + m]), e.add2[(int64_t)(nbase + j) * e.ld2 + m]);
+        yrow[(int64_t)j * e.ldy] = y;
+    }
+}
+
 template <int BN, int EPI>
 __device__ __forceinline__ void tc_epilogue(const TcEpi& e, uint32_t tmem_base, uint64_t* tfull, uint64_t* tempty,
                                             uint32_t tempty_remote, int tile0, int tstep, int tiles, int n_blocks,
                                             int m_tile, int m_off, int M, int N, float (*col_sx)[256],
-                                            double (*col_isx)[256], int m_blocks = 0, int group_m = 0) {
+                                            double (*col_isx)[256], int m_blocks = 0, int group_m = 0,
+                                            TcSplit sk = TcSplit{1, nullptr, nullptr}, int* s_last = nullptr) {
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     const int ew = warp - 2;                 // 0..7
@@ -92,7 +142,8 @@ __device__ __forceinline__ void tc_epilogue(const TcEpi& e, uint32_t tmem_base, 
         int it = 0;
         for (int tile = tile0; tile < tiles; tile += tstep, ++it) {
             int mb, nb;
-            tile_coords(tile, m_blocks, n_blocks, group_m, mb, nb);
+            const int mnt = sk.ksplit > 1 ? tile / sk.ksplit : tile;
+            tile_coords(mnt, m_blocks, n_blocks, group_m, mb, nb);
             const int buf = it & 1;
             const uint32_t use = (uint32_t)(it >> 1) & 1u;
             // Column scales of this tile -> smem (x scale and its f64 reciprocal), row scale and
@@ -118,6 +169,52 @@ __device__ __forceinline__ void tc_epilogue(const TcEpi& e, uint32_t tmem_base, 
             asm volatile("bar.sync 1, %0;" ::"n"(32 * TC_EPI_WARPS));   // epilogue warps only
             tc::mbar_wait(&tfull[buf], use);
             tc::tc_fence_after();
+            if (sk.ksplit > 1) {   // split-K: add the partial tile into the workspace
+#pragma unroll 1
+                for (int c0 = half * COLS; c0 < (half + 1) * COLS; c0 += 16) {
+                    uint32_t r[16];
+                    tc::tmem_ld16(tmem_base + ((uint32_t)(lg * 32) << 16) + (uint32_t)(buf * BN + c0), r);
+                    const int nbase = nb * BN + c0;
+                    const int ncols = min(16, N - nbase);
+                    tc::tmem_ld_wait();
+                    if (mok)
+#pragma unroll
+                        for (int j = 0; j < 16; ++j)
+                            if (j < ncols) atomicAdd(&sk.ws[(int64_t)(nbase + j) * M + m], (int)r[j]);
+                }
+                tc::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) tc::mbar_arrive(&tempty[buf]);   // TMEM buffer free for the next tile
+                __threadfence();
+                asm volatile("bar.sync 1, %0;" ::"n"(32 * TC_EPI_WARPS));
+                if (ew == 0 && lane == 0) {
+                    const int old = atomicAdd(&sk.cnt[mnt], 1);
+                    *s_last = old == sk.ksplit - 1;
+                    if (*s_last) sk.cnt[mnt] = 0;
+                }
+                asm volatile("bar.sync 1, %0;" ::"n"(32 * TC_EPI_WARPS));
+                if (!*s_last) continue;
+                __threadfence();
+#pragma unroll 1
+                for (int c0 = half * COLS; c0 < (half + 1) * COLS; c0 += 16) {
+                    const int nbase = nb * BN + c0;
+                    const int ncols = min(16, N - nbase);
+                    if (ncols <= 0) continue;
+                    uint32_t r[16];
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) {
+                        r[j] = 0u;
+                        if (mok && j < ncols) {
+                            int32_t* w = &sk.ws[(int64_t)(nbase + j) * M + m];
+                            r[j] = (uint32_t)__ldcg(w);
+                            *w = 0;
+                        }
+                    }
+                    tc_epi_chunk<EPI>(e, r, m, mok, nbase, ncols, M, sw, bias, isw, &col_sx[buf][c0],
+                                      &col_isx[buf][c0]);
+                }
+                continue;
+            }
 #pragma unroll 1
             for (int c0 = half * COLS; c0 < (half + 1) * COLS; c0 += 16) {
                 uint32_t r[16];
@@ -195,7 +292,7 @@ __device__ __forceinline__ void tc_epilogue(const TcEpi& e, uint32_t tmem_base, 
 template <int BN, int EPI>
 __global__ void __launch_bounds__(TC_THREADS, 1)
 k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N, int K,
-          TcEpi e, const int32_t* n_dev) {
+          TcEpi e, const int32_t* n_dev, TcSplit sk) {
     using C = TcCfg<BN>;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* smem = (unsigned char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -211,16 +308,17 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
     if (n_dev) N = min(N, *n_dev);   // graph mode: live columns from the device
     const int m_blocks = (M + TC_BM - 1) / TC_BM;
     const int n_blocks = (N + BN - 1) / BN;
-    const int tiles = m_blocks * n_blocks;
+    const int tiles = m_blocks * n_blocks * sk.ksplit;
     const int k_blocks = (K + TC_BK - 1) / TC_BK;
+    __shared__ int s_last;
 
     if (warp == 0) {
-        tc_produce<C, BN>(&tmA, &tmB, smem, bars, tiles, n_blocks, k_blocks);
+        tc_produce<C, BN>(&tmA, &tmB, smem, bars, tiles, n_blocks, k_blocks, -1, 0, sk.ksplit);
     } else if (warp == 1) {
-        tc_issue<C, BN>(smem, bars, tmem_base, tiles, k_blocks);
+        tc_issue<C, BN>(smem, bars, tmem_base, tiles, k_blocks, -1, 0, sk.ksplit);
     } else {
         tc_epilogue<BN, EPI>(e, tmem_base, bars.tfull, bars.tempty, 0u, blockIdx.x, gridDim.x, tiles, n_blocks,
-                             TC_BM, 0, M, N, col_sx, col_isx);
+                             TC_BM, 0, M, N, col_sx, col_isx, 0, 0, sk, &s_last);
     }
     __syncthreads();
     if (warp == 1) {
@@ -467,6 +565,65 @@ int tc_sm_count() {
     return n;
 }
 
+// ---------------------------------------------------------------------------
+// split-K workspace: one zeroed int32 [N][M] buffer + tile counters per stream
+// (kernels on one stream run in order; engines own their streams).  Grown only
+// outside stream capture; a captured product that finds it too small runs
+// without splitting.  tc_split_reserve lets an engine size it before capture.
+// ---------------------------------------------------------------------------
+struct SplitWs {
+    int32_t* ws = nullptr;
+    size_t ws_elems = 0;
+    int32_t* cnt = nullptr;
+    size_t cnt_elems = 0;
+};
+static std::mutex g_ws_mu;
+static std::unordered_map<cudaStream_t, SplitWs> g_ws;
+int g_tc_split = 0;   // 1: split K for tile-starved products (A/B: cfg1 B=64 21.4 vs 14.4 us, off)
+
+static bool split_ws(cudaStream_t st, size_t ws_elems, size_t cnt_elems, TcSplit& sk) {
+    std::lock_guard<std::mutex> lk(g_ws_mu);
+    SplitWs& w = g_ws[st];
+    if (w.ws_elems < ws_elems || w.cnt_elems < cnt_elems) {
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return false;
+        if (cudaStreamSynchronize(st) != cudaSuccess) return false;   // the old buffers may be in use
+        cudaFree(w.ws);
+        cudaFree(w.cnt);
+        w = SplitWs{};
+        const size_t we = std::max(ws_elems, (size_t)1 << 20), ce = std::max(cnt_elems, (size_t)4096);
+        if (cudaMalloc(&w.ws, we * sizeof(int32_t)) != cudaSuccess) return false;
+        if (cudaMalloc(&w.cnt, ce * sizeof(int32_t)) != cudaSuccess) {
+            cudaFree(w.ws);
+            w = SplitWs{};
+            return false;
+        }
+        if (cudaMemsetAsync(w.ws, 0, we * sizeof(int32_t), st) != cudaSuccess ||
+            cudaMemsetAsync(w.cnt, 0, ce * sizeof(int32_t), st) != cudaSuccess)
+            return false;
+        w.ws_elems = we;
+        w.cnt_elems = ce;
+    }
+    sk.ws = w.ws;
+    sk.cnt = w.cnt;
+    return true;
+}
+
+int tc_split_reserve(cudaStream_t st, int64_t ws_elems, int64_t tiles) {
+    TcSplit sk{1, nullptr, nullptr};
+    return split_ws(st, (size_t)ws_elems, (size_t)tiles, sk) ? QNMT_OK : QNMT_ERR_CUDA;
+}
+
+// K splits for a product of `tiles` output tiles and k_blocks k-blocks: enough CTAs to
+// cover half the SMs or more, >= 2 k-blocks per split... but never past one wave
+static int choose_ksplit(int64_t tiles, int64_t k_blocks, int sms) {
+    if (!g_tc_split || tiles * 2 > sms || k_blocks < 2) return 1;
+    const int64_t req = std::min<int64_t>({k_blocks, sms / tiles, 16});
+    if (req < 2) return 1;
+    const int64_t kpb = cdiv(k_blocks, req);
+    return (int)cdiv(k_blocks, kpb);
+}
+
 template <int BN, int EPI>
 static int launch_tc(const GemmArgs& g, cudaStream_t st) {
     using C = TcCfg<BN>;
@@ -480,9 +637,12 @@ static int launch_tc(const GemmArgs& g, cudaStream_t st) {
     TcEpi e{g.w_scales, g.w_rows_per_scale, g.x_scales, g.col_seg, g.bias, g.Y, g.ldy, g.acc_out, g.flags,
             g.add1, g.ld1, g.add2, g.ld2};
     int tiles = (int)(cdiv(g.M, TC_BM) * cdiv(g.N, BN));
+    TcSplit sk{choose_ksplit(tiles, cdiv(g.K, TC_BK), tc_sm_count()), nullptr, nullptr};
+    if (sk.ksplit > 1 && !split_ws(st, (size_t)g.M * g.N, (size_t)tiles, sk)) sk.ksplit = 1;
+    tiles *= sk.ksplit;
     int grid = tiles < tc_sm_count() ? tiles : tc_sm_count();
     auto kfn = k_gemm_tc<BN, EPI>;
-    QNMT_LAUNCH(kfn, grid, TC_THREADS, C::SMEM, st, ta, tb, (int)g.M, (int)g.N, (int)g.K, e, tl_ndev);
+    QNMT_LAUNCH(kfn, grid, TC_THREADS, C::SMEM, st, ta, tb, (int)g.M, (int)g.N, (int)g.K, e, tl_ndev, sk);
     QNMT_CHECK_LAUNCH("k_gemm_tc");
     return QNMT_OK;
 }
@@ -578,6 +738,12 @@ int gemm_tc_launch(const GemmArgs& g, cudaStream_t st) {
 }
 
 }  // namespace qnmt
+
+extern "C" int qnmt_set_tc_split(int enable) {
+    const int old = qnmt::g_tc_split;
+    qnmt::g_tc_split = enable;
+    return old;
+}
 
 extern "C" int qnmt_set_tc_pair(int enable) {
     const int old = qnmt::g_tc_pair;

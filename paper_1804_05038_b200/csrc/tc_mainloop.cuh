@@ -70,10 +70,24 @@ __device__ __forceinline__ uint32_t tc_setup(const CUtensorMap* tmA, const CUten
     return *b.tmem_slot;
 }
 
+// split-K: tile t covers output tile t / ksplit and k-blocks [kb0, kb1) of split t % ksplit
+__device__ __forceinline__ void tc_krange(int tile, int ksplit, int k_blocks, int& mn, int& kb0, int& kb1) {
+    if (ksplit <= 1) {
+        mn = tile;
+        kb0 = 0;
+        kb1 = k_blocks;
+        return;
+    }
+    const int kpb = (k_blocks + ksplit - 1) / ksplit;
+    mn = tile / ksplit;
+    kb0 = (tile % ksplit) * kpb;
+    kb1 = min(k_blocks, kb0 + kpb);
+}
+
 template <class R, int BN>
 __device__ __forceinline__ void tc_produce(const CUtensorMap* tmA, const CUtensorMap* tmB, unsigned char* smem,
                                            const TcBars<R>& b, int tiles, int n_blocks, int k_blocks,
-                                           int t0 = -1, int tstep = 0) {
+                                           int t0 = -1, int tstep = 0, int ksplit = 1) {
     if ((threadIdx.x & 31) != 0) return;
     int stage = 0;
     uint32_t phase = 0;
@@ -82,8 +96,10 @@ __device__ __forceinline__ void tc_produce(const CUtensorMap* tmA, const CUtenso
         tstep = gridDim.x;
     }
     for (int tile = t0; tile < tiles; tile += tstep) {
-        const int ab = tile / n_blocks, bb = tile % n_blocks;
-        for (int kb = 0; kb < k_blocks; ++kb) {
+        int mn, kbs, kbe;
+        tc_krange(tile, ksplit, k_blocks, mn, kbs, kbe);
+        const int ab = mn / n_blocks, bb = mn % n_blocks;
+        for (int kb = kbs; kb < kbe; ++kb) {
             tc::mbar_wait(&b.empty[stage], phase ^ 1);
             unsigned char* sa = smem + stage * R::STAGE_BYTES;
             unsigned char* sb = sa + R::A_BYTES;
@@ -97,7 +113,7 @@ __device__ __forceinline__ void tc_produce(const CUtensorMap* tmA, const CUtenso
 
 template <class R, int BN>
 __device__ __forceinline__ void tc_issue(unsigned char* smem, const TcBars<R>& b, uint32_t tmem_base, int tiles,
-                                         int k_blocks, int t0 = -1, int tstep = 0) {
+                                         int k_blocks, int t0 = -1, int tstep = 0, int ksplit = 1) {
     constexpr uint32_t IDESC = tc::idesc_i8(TC_BM, BN);
     const int lane = threadIdx.x & 31;
     int stage = 0;
@@ -113,7 +129,9 @@ __device__ __forceinline__ void tc_issue(unsigned char* smem, const TcBars<R>& b
         tc::mbar_wait(&b.tempty[buf], use ^ 1);
         tc::tc_fence_after();
         const uint32_t d = tmem_base + (uint32_t)(buf * BN);
-        for (int kb = 0; kb < k_blocks; ++kb) {
+        int mn, kbs, kbe;
+        tc_krange(tile, ksplit, k_blocks, mn, kbs, kbe);
+        for (int kb = kbs; kb < kbe; ++kb) {
             tc::mbar_wait(&b.full[stage], phase);
             tc::tc_fence_after();
             if (lane == 0) {
@@ -122,9 +140,9 @@ __device__ __forceinline__ void tc_issue(unsigned char* smem, const TcBars<R>& b
 #pragma unroll
                 for (int k = 0; k < TC_BK / 32; ++k)
                     tc::mma_i8(d, tc::sw128_kmajor_desc(a0 + 32 * k), tc::sw128_kmajor_desc(b0 + 32 * k), IDESC,
-                               (kb | k) != 0);
+                               (kb != kbs) || k != 0);
                 tc::mma_commit(&b.empty[stage]);
-                if (kb == k_blocks - 1) tc::mma_commit(&b.tfull[buf]);
+                if (kb == kbe - 1) tc::mma_commit(&b.tfull[buf]);
             }
             __syncwarp();
             if (++stage == R::STAGES) { stage = 0; phase ^= 1; }

@@ -43,6 +43,19 @@ struct VtPart {
     int32_t pad;    // row's first partial, after the merge: path taken (diagnostics, see k_vocab_merge)
 };
 
+// K7 vocabulary-shard partial of one hypothesis row (qnmt_vocab_shard_partials): the
+// shard's max logit M, S = sum over its tokens of exp(x - M) (fp64), and its top-VS_KR
+// logits by (logit desc, token asc) with global token ids.
+constexpr int VS_KR = 8;
+struct VsPart {
+    double S;
+    float M;
+    int32_t n;               // candidates held (min(VS_KR, shard rows))
+    float x[VS_KR];
+    int32_t t[VS_KR];
+};
+static_assert(sizeof(VsPart) == 80, "VsPart layout is part of the C ABI");
+
 struct VtArgs {
     const float* x_scales;    // activation scale per segment
     const int32_t* row_seg;   // segment of each hypothesis row
@@ -331,6 +344,8 @@ struct VtMergeArgs {
     int k;
     double* cand_score;
     int32_t* cand_tok;
+    VsPart* raw;        // vocabulary shard mode (K7): per-row (M, S, top-KR logits) instead of candidates
+    int32_t tok_off;    // shard mode: global token id of the shard's first row
 };
 
 // Warp-cooperative exact logits of tokens v0 .. v0+31 for one row: lane j returns
@@ -396,7 +411,7 @@ __device__ __forceinline__ uint64_t warp_sort_desc(uint64_t key) {
     return key;
 }
 
-template <int KM>
+template <int KM, bool RAW = false>
 __global__ void __launch_bounds__(32 * VM_WARPS)
 k_vocab_merge(VtMergeArgs a, int64_t N, const int32_t* n_dev) {
     pdl_entry();
@@ -453,7 +468,8 @@ k_vocab_merge(VtMergeArgs a, int64_t N, const int32_t* n_dev) {
     }
     const float M = warp_max(ml);
     const double dM = (double)M;
-    const double lse = log(warp_sum(ml == -FLT_MAX ? 0.0 : sl * exp_neg((double)ml - dM, tab)));
+    const double ssum = warp_sum(ml == -FLT_MAX ? 0.0 : sl * exp_neg((double)ml - dM, tab));
+    const double lse = log(ssum);
     // tau = kk-th best of the 32 lane maxima (bitonic sort of (logit, token) keys): at least kk
     // group maxima are >= tau, so every member of the top-kk is too
     const uint64_t tau_key = __shfl_sync(0xffffffffu,
@@ -529,6 +545,31 @@ k_vocab_merge(VtMergeArgs a, int64_t N, const int32_t* n_dev) {
         __syncwarp();
         warp_merge<KM>(L, out, kk);
         __syncwarp();
+    }
+    if (RAW) {   // vocabulary shard (K7): the shard's (max, sum exp(x - max)) and exact top-KR logits
+        if (nf > VT_RESCAN_MAX) {   // too many flagged half-tiles: the shard's whole row, by logit
+#pragma unroll
+            for (int i = 0; i < KM; ++i) L[i] = Cand{-DBL_MAX, 0x7fffffff};
+            for (int v0 = 0; v0 < a.V; v0 += 32) {
+                const float x = vt_logits32(a, xr, v0, sx);
+                if (v0 + lane < a.V) insert<KM>(L, Cand{(double)x, v0 + lane});
+            }
+            __syncwarp();
+            warp_merge<KM>(L, out, kk);
+            __syncwarp();
+        }
+        VsPart* r = a.raw + n;
+        const int nr = kk < VS_KR ? kk : VS_KR;
+        if (lane == 0) {
+            r->S = ssum;
+            r->M = M;
+            r->n = nr;
+        }
+        if (lane < VS_KR) {
+            r->x[lane] = lane < nr ? (float)out[lane].s : -FLT_MAX;
+            r->t[lane] = lane < nr ? out[lane].t + a.tok_off : 0x7fffffff;
+        }
+        return;
     }
     const double base = a.live ? a.live[n] : 0.0;
     int ok = 0;
@@ -657,11 +698,93 @@ int vocab_merge_launch(const VocabTopk& p, cudaStream_t st) {
     if (N <= 0) return QNMT_OK;
     VtMergeArgs ma{p.X, p.ldx, p.W, p.ldw, (int)p.K, (int)p.V, (int)cdiv(p.V, VT_BN), p.x_scales, p.row_seg,
                    p.w_scales, p.w_rows_per_scale, p.bias, reinterpret_cast<VtPart*>(p.part), p.live, k,
-                   p.cand_score, p.cand_tok};
+                   p.cand_score, p.cand_tok, nullptr, 0};
     const unsigned g = (unsigned)cdiv(N, VM_WARPS);
     auto kfn = k <= 6 ? k_vocab_merge<8> : k <= 13 ? k_vocab_merge<16> : k_vocab_merge<32>;
     QNMT_LAUNCH(kfn, g, 32 * VM_WARPS, 0, st, ma, N, tl_ndev);
     QNMT_CHECK_LAUNCH("k_vocab_merge");
+    return QNMT_OK;
+}
+
+// K7 combine: one warp per row merges the G shards' partials into the step's
+// candidates, exactly as k_vocab_merge scores them:
+//   M = max_g M_g, lse = log(sum_g S_g e^(M_g - M)) (fp64, shard order),
+//   score = live + fl32((x - M) - lse) for the union of the shards' top-VS_KR
+//   logits, ranked by (score desc, token asc).
+// The union holds the global top-k unless a shard with a full list has its
+// VS_KR-th candidate scoring >= the k-th best (a token outside its list could
+// then tie into the top-k): those rows set QNMT_FLAG_SHARD_TIE and the caller
+// recomputes them unsharded.
+__global__ void __launch_bounds__(32 * VM_WARPS)
+k_vocab_shard_combine(const VsPart* __restrict__ parts, int G, int64_t N, const double* __restrict__ live, int k,
+                      double* __restrict__ cand_score, int32_t* __restrict__ cand_tok, int32_t* err_flag) {
+    pdl_entry();
+    const int lane = threadIdx.x & 31;
+    const int64_t n = (int64_t)blockIdx.x * VM_WARPS + (threadIdx.x >> 5);
+    if (n >= N) return;
+    float M = -FLT_MAX;
+    for (int g = 0; g < G; ++g) M = fmaxf(M, parts[(int64_t)g * N + n].M);
+    const double dM = (double)M;
+    double S = 0.0;
+    for (int g = 0; g < G; ++g) {   // fixed shard order (every rank computes the same sum)
+        const VsPart& p = parts[(int64_t)g * N + n];
+        if (p.n > 0) S += p.S * exp_f64((double)p.M - dM);
+    }
+    const double lse = log(S);
+    const double base = live ? live[n] : 0.0;
+    // candidates: lane owns entries lane, lane + 32, ... of the G x VS_KR union
+    constexpr int PER = 4;   // G <= 16
+    Cand c[PER];
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+        const int e = lane + 32 * q;
+        const int g = e / VS_KR, i = e % VS_KR;
+        c[q] = Cand{-DBL_MAX, 0x7fffffff};
+        if (g < G) {
+            const VsPart& p = parts[(int64_t)g * N + n];
+            if (i < p.n) c[q] = Cand{base + (double)__double2float_rn(((double)p.x[i] - dM) - lse), p.t[i]};
+        }
+    }
+    // top-k by repeated warp argmax (k <= 16); lane 0 writes each as it is found
+    Cand kth{-DBL_MAX, 0x7fffffff};
+    for (int r = 0; r < k; ++r) {
+        Cand w = c[0];
+#pragma unroll
+        for (int q = 1; q < PER; ++q) if (better(c[q], w)) w = c[q];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const Cand x{__shfl_xor_sync(0xffffffffu, w.s, o), __shfl_xor_sync(0xffffffffu, w.t, o)};
+            if (better(x, w)) w = x;
+        }
+        if (lane == 0) {
+            cand_score[n * k + r] = w.s;
+            cand_tok[n * k + r] = w.t;
+        }
+        kth = w;
+#pragma unroll
+        for (int q = 0; q < PER; ++q) if (c[q].t == w.t && c[q].s == w.s) c[q] = Cand{-DBL_MAX, 0x7fffffff};
+    }
+    // exactness: every full shard's last candidate must score strictly below the k-th
+    bool tie = false;
+    if (lane < G) {
+        const VsPart& p = parts[(int64_t)lane * N + n];
+        if (p.n == VS_KR) {
+            const double sl = base + (double)__double2float_rn(((double)p.x[VS_KR - 1] - dM) - lse);
+            tie = !(sl < kth.s);
+        }
+    }
+    if (__any_sync(0xffffffffu, tie) && lane == 0) set_flag(err_flag, QNMT_FLAG_SHARD_TIE);
+}
+
+int vocab_shard_partials_launch(const VocabTopk& p, int32_t tok_off, void* raw, cudaStream_t st) {
+    int rc = vocab_stats_launch(p, st);
+    if (rc != QNMT_OK || p.N <= 0) return rc;
+    VtMergeArgs ma{p.X, p.ldx, p.W, p.ldw, (int)p.K, (int)p.V, (int)cdiv(p.V, VT_BN), p.x_scales, p.row_seg,
+                   p.w_scales, p.w_rows_per_scale, p.bias, reinterpret_cast<VtPart*>(p.part), nullptr, 1,
+                   nullptr, nullptr, reinterpret_cast<VsPart*>(raw), tok_off};
+    const unsigned g = (unsigned)cdiv(p.N, VM_WARPS);
+    QNMT_LAUNCH((k_vocab_merge<VS_KR, true>), g, 32 * VM_WARPS, 0, st, ma, p.N, tl_ndev);
+    QNMT_CHECK_LAUNCH("k_vocab_merge (shard)");
     return QNMT_OK;
 }
 
@@ -692,4 +815,36 @@ extern "C" int qnmt_vocab_candidates(const int8_t* X, int64_t N, int64_t ldx, co
 
 extern "C" int64_t qnmt_vocab_candidates_scratch(int64_t N, int64_t V) {
     return (int64_t)qnmt::vocab_topk_part_bytes(N, V);
+}
+
+extern "C" int64_t qnmt_vocab_shard_part_bytes(void) { return (int64_t)sizeof(qnmt::VsPart); }
+
+extern "C" int qnmt_vocab_shard_partials(const int8_t* X, int64_t N, int64_t ldx, const float* x_scales,
+                                         const int32_t* row_seg, const int8_t* W, int64_t V_shard, int64_t K,
+                                         int64_t ldw, const float* w_scales, int64_t w_rows_per_scale,
+                                         const float* bias, int64_t tok_off, void* scratch, void* parts,
+                                         int32_t* err_flag, void* stream) {
+    if (N < 0 || V_shard < 1 || w_rows_per_scale < 1 || tok_off < 0) {
+        qnmt::set_error("qnmt_vocab_shard_partials: bad shape N=%lld V_shard=%lld", (long long)N, (long long)V_shard);
+        return QNMT_ERR_SHAPE;
+    }
+    const qnmt::VocabTopk p{X, N, ldx, x_scales, row_seg, W, V_shard, K, ldw, w_scales, w_rows_per_scale, bias,
+                            nullptr, 1, scratch, nullptr, nullptr, err_flag};
+    return qnmt::vocab_shard_partials_launch(p, (int32_t)tok_off, parts, qnmt::as_stream(stream));
+}
+
+extern "C" int qnmt_vocab_shard_combine(const void* parts, int32_t G, int64_t N, const double* live_scores,
+                                        int32_t k, double* cand_score, int32_t* cand_tok, int32_t* err_flag,
+                                        void* stream) {
+    if (G < 1 || G > 16 || k < 1 || k > 16 || N < 0) {
+        qnmt::set_error("qnmt_vocab_shard_combine: G=%d k=%d (1..16)", G, k);
+        return QNMT_ERR_CONFIG;
+    }
+    if (N == 0) return QNMT_OK;
+    const unsigned g = (unsigned)qnmt::cdiv(N, qnmt::VM_WARPS);
+    QNMT_LAUNCH(qnmt::k_vocab_shard_combine, g, 32 * qnmt::VM_WARPS, 0, qnmt::as_stream(stream),
+                reinterpret_cast<const qnmt::VsPart*>(parts), (int)G, N, live_scores, (int)k, cand_score, cand_tok,
+                err_flag);
+    QNMT_CHECK_LAUNCH("k_vocab_shard_combine");
+    return QNMT_OK;
 }

@@ -128,10 +128,29 @@ class LinearOp:
         or the fp32 product + bias)."""
         if not self.is_quantized:
             return gemm_f32_kmajor(self._wdev(), x_k, bias=self._bias_dev(), Y=out, accumulate=accumulate)
+        if col_seg is None and nseg == 1 and out is None and x_k.shape[0] <= 8:
+            return self._linear_small(x_k)
         q, sx = _quant_k(x_k, col_seg, nseg)
         return gemm_kmajor(self.weight.device_data(), self.weight.device_scale(), self.out_dim, q, sx,
                            col_seg=col_seg, bias=self._bias_dev(), Y=out, accumulate=accumulate,
                            w_static=True)
+
+    def _linear_small(self, x_k: torch.Tensor) -> torch.Tensor:
+        """Batch <= 8 (the latency path): quantize_activations + qgemm_panel + bias as the
+        single qnmt_linear_i8 kernel."""
+        N, K = x_k.shape
+        M = self.out_dim
+        x_k = x_k.contiguous()
+        y = torch.empty((N, M), dtype=torch.float32, device=x_k.device)
+        q = torch.empty((N, K), dtype=torch.int8, device=x_k.device)
+        sx = torch.empty(1, dtype=torch.float32, device=x_k.device)
+        bits = torch.empty(1, dtype=torch.int32, device=x_k.device)
+        w = self.weight
+        _lib.call("qnmt_linear_i8", w.device_data().data_ptr(), M, K, _dev.ld(w.device_data()),
+                  w.device_scale().data_ptr(), M, x_k.data_ptr(), N, K, _dev.ptr(self._bias_dev()), y.data_ptr(), M,
+                  q.data_ptr(), K, sx.data_ptr(), bits.data_ptr(), _lib.GEMM_W_STATIC, _dev.flag().data_ptr(),
+                  _dev.stream_ptr())
+        return y
 
     def apply(self, x, timer=None):
         if len(np.shape(x)) != 2 or np.shape(x)[0] != self.in_dim:

@@ -1,7 +1,9 @@
 """The attention scorer's variants give identical codes, scores, alpha and
 context (attention.cu):
 
-* two-MUFU scorer (k_att_score5): t = 1 - 2 / (1 + 2^(2x log2 e)) per element;
+* two-MUFU scorer (k_att_score5): t = 1 - 2 / (1 + 2^(2x log2 e)) per element,
+  with its per-hypothesis scales from k_att_scale or computed in its own CTAs
+  (k_att_score5f, the default);
 * one-MUFU scorer (k_att_score6): e^(2(ap+u)) = E_ap * E_u from per-batch /
   per-step fp64 exps, rounding-window elements queued and resolved exactly
   by the CTA's last warp;
@@ -24,12 +26,14 @@ pytestmark = pytest.mark.gpu
 pb = pytest.importorskip("paper_1804_05038_b200")
 from paper_1804_05038_b200 import _dev, _lib  # noqa: E402
 
-MODES = [(0, 512), (1, 512), (1, 0), (2, 512), (2, 0)]   # (scorer variant, fixup queue length)
+# (scorer variant, fixup queue length, scale fused into the two-MUFU scorer)
+MODES = [(0, 512, 1), (0, 512, 0), (1, 512, 1), (1, 0, 1), (2, 512, 1), (2, 0, 1)]
 
 
 def _run(lib, mode, inp):
     old_e = lib.qnmt_set_att_exp(mode[0])
     old_c = lib.qnmt_set_att_fixcap(mode[1])
+    old_f = lib.qnmt_set_att_fused_scale(mode[2])
     try:
         (att, ex, states, u, v, vs, off, cnt, rows_d, lens_d, S, N, A, H2, max_len) = inp
         mm = torch.empty((S, 2, A), device="cuda")
@@ -50,6 +54,7 @@ def _run(lib, mode, inp):
     finally:
         lib.qnmt_set_att_exp(old_e)
         lib.qnmt_set_att_fixcap(old_c)
+        lib.qnmt_set_att_fused_scale(old_f)
 
 
 def _inputs(seed, beams, scale_u, scale_ap, A=2048, H2=2048):

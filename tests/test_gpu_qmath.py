@@ -265,3 +265,97 @@ def test_gpu_tc_pair_kernel_matches_single_cta(M, K, N):
     if K % 8 == 0 and N % 8 == 0 and M % 8 == 0:
         ref = torch._int_mm(X, W.t())
         assert torch.equal(outs[0][0], ref.to(torch.int64))
+
+
+SHAPES_SPLIT = [(3072, 1024, 64), (3072, 1024, 9), (512, 4096, 33), (1000, 2048, 100), (128, 8192, 16),
+                (2048, 512, 128), (77, 1024, 300), (6000, 1024, 20)]
+
+
+@pytest.mark.parametrize("shape", SHAPES_SPLIT)
+def test_tcgen05_split_k_bit_exact(shape):
+    """Tile-starved tcgen05 products split K over more CTAs (int32 partials added in a
+    workspace, the last split runs the epilogue): results identical with and without
+    the split and to the oracle, repeated calls included (the workspace is left zeroed),
+    with segmented scales, bias and ACCUMULATE."""
+    import torch
+    M, K, N = shape
+    rng = np.random.default_rng(M + 3 * K + 7 * N)
+    Wc = rng.integers(-127, 128, (M, K)).astype(np.int8)
+    Xc = rng.integers(-127, 128, (N, K)).astype(np.int8)
+    S = max(1, N // 5)
+    seg = np.sort(rng.integers(0, S, N)).astype(np.int32)
+    ws = np.float32(rng.uniform(50, 300))
+    xs = rng.uniform(50, 300, S).astype(np.float32)
+    bias = rng.normal(0, 1, M).astype(np.float32)
+    y0 = rng.normal(0, 1, (N, M)).astype(np.float32)
+    W, X = torch.from_numpy(Wc).cuda(), torch.from_numpy(Xc).cuda()
+    wsd = torch.tensor([ws], device="cuda")
+    xsd, segd = torch.from_numpy(xs).cuda(), torch.from_numpy(seg).cuda()
+    bd = torch.from_numpy(bias).cuda()
+    lib = _lib.load()
+    outs = []
+    old_i = lib.qnmt_set_gemm_impl(2)
+    try:
+        for split in (1, 0, 1):   # (split on, off, on again: the workspace is reused)
+            old = lib.qnmt_set_tc_split(split)
+            try:
+                Y = torch.from_numpy(y0.copy()).cuda()
+                pb.qmath.gemm_kmajor(W, wsd, M, X, xsd, col_seg=segd, bias=bd, Y=Y, accumulate=True)
+                acc = torch.empty((N, M), dtype=torch.int64, device="cuda")
+                pb.qmath.gemm_kmajor(W, wsd, M, X, xsd, col_seg=segd, acc_out=acc)
+                outs.append((Y.cpu().numpy(), acc.cpu().numpy()))
+            finally:
+                lib.qnmt_set_tc_split(old)
+    finally:
+        lib.qnmt_set_gemm_impl(old_i)
+    exact = Xc.astype(np.int64) @ Wc.astype(np.int64).T
+    for Y, acc in outs:
+        assert np.array_equal(acc, exact)
+        assert np.array_equal(Y, outs[1][0])
+    # against the oracle: y = Y + (fl32(acc / (sw * sx)) + b) (qmath.py:379-381, layers.py:144-145)
+    dq = (exact.astype(np.float64) / (np.float64(ws) * xs[seg].astype(np.float64)[:, None])).astype(np.float32)
+    assert np.array_equal(outs[0][0], y0 + (dq + bias[None, :]))
+
+
+@pytest.mark.parametrize("N,K,M", [(1, 1024, 3072), (2, 512, 1000), (5, 2048, 513), (8, 4096, 256), (3, 16, 7),
+                                   (1, 8192, 64), (9, 1024, 300), (64, 1024, 3072)])
+def test_linear_i8_matches_oracle(N, K, M):
+    """qnmt_linear_i8 (LinearOp.apply, layers.py:124-146: quantize_activations +
+    qgemm_panel + bias; one kernel for N <= 8, quantize + GEMM beyond) == oracle:
+    codes, scale and outputs bit-exact."""
+    import torch
+    from paper_1804_05038_b200 import _dev
+    rng = np.random.default_rng(N * 1000 + K + M)
+    w = rng.normal(0, 0.05, (M, K)).astype(np.float32)
+    x = (rng.normal(0, 1, (K, N)) * rng.uniform(0.01, 10)).astype(np.float32)
+    b = rng.normal(0, 0.1, M).astype(np.float32)
+    wq = pb.quantize(w)
+    xq_c, xq_s = O.quantize_activations(x)
+    expect = O.qgemm(wq.data, wq.scale, xq_c, xq_s) + b[:, None]
+    op = pb.LinearOp(wq, b)
+    y = op.apply(x)
+    assert np.array_equal(y, expect)
+    # raw ABI: codes and scale
+    Xk = torch.from_numpy(np.ascontiguousarray(x.T)).cuda()
+    W = wq.device_data()
+    Y = torch.empty((N, M), device="cuda")
+    q = torch.empty((N, K), dtype=torch.int8, device="cuda")
+    sx = torch.empty(1, device="cuda")
+    bits = torch.empty(1, dtype=torch.int32, device="cuda")
+    f = _dev.reset_flag()
+    _lib.call("qnmt_linear_i8", W.data_ptr(), M, K, K, wq.device_scale().data_ptr(), M, Xk.data_ptr(), N, K,
+              torch.from_numpy(b).cuda().data_ptr(), Y.data_ptr(), M, q.data_ptr(), K, sx.data_ptr(), bits.data_ptr(),
+              _lib.GEMM_W_STATIC, f.data_ptr(), _dev.stream_ptr())
+    _dev.raise_flag(f)
+    assert float(sx.item()) == xq_s
+    assert np.array_equal(q.cpu().numpy().T, xq_c)
+    assert np.array_equal(Y.cpu().numpy().T, expect)
+
+
+def test_linear_i8_nonfinite_raises():
+    rng = np.random.default_rng(3)
+    wq = pb.quantize(rng.normal(0, 0.05, (64, 32)).astype(np.float32))
+    x = rng.normal(0, 1, (32, 1)).astype(np.float32)
+    x[5, 0] = np.inf
+    with pytest.raises(pb.errors.NumericError):
+        pb.LinearOp(wq, None).apply(x)
