@@ -356,6 +356,8 @@ def main():
         lib.qnmt_set_att_exp(int(os.environ["QNMT_ATT_EXP"]))
     if os.environ.get("QNMT_ATT_FS") is not None:   # A/B switch: scale fused into the scorer
         lib.qnmt_set_att_fused_scale(int(os.environ["QNMT_ATT_FS"]))
+    if os.environ.get("QNMT_ATT_S8") is not None:   # A/B switch: bulk-staged two-MUFU scorer
+        lib.qnmt_set_att_score8(int(os.environ["QNMT_ATT_S8"]))
     if os.environ.get("QNMT_ATT_CTX") is not None:   # A/B switch of the attention context kernel
         lib.qnmt_set_att_ctx(int(os.environ["QNMT_ATT_CTX"]))
     main_stream = torch.cuda.current_stream()

@@ -1,11 +1,13 @@
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_gpu_qmath.py tests/test_gpu_layers.py -x -q > gpurun_out/t_lin.log 2>&1; tail -3 gpurun_out/t_lin.log
+date +%s > gpurun_out/t0
+timeout 1200 python -m pytest tests -m gpu -x -q > gpurun_out/gputest_all.log 2>&1; tail -3 gpurun_out/gputest_all.log
+date +%s
+for s8 in 1 0; do QNMT_ATT_S8=$s8 timeout 400 python bench.py --no-cpu --no-configs --steps 3 > gpurun_out/bench_s8_$s8.json 2> gpurun_out/bench_s8_$s8.err; echo "rc=$? $(date +%s)"; python -c "import json;d=json.load(open('gpurun_out/bench_s8_$s8.json'));print($s8, d['value'], d['e2e']['value'], d['kernels']['attention']['us_per_launch'])"; done
 timeout 300 python -c "
 import sys; sys.path.insert(0,'.')
-import bench_cfgs, paper_1804_05038_b200 as pb, json
+import bench_cfgs, paper_1804_05038_b200 as pb
 from paper_1804_05038_b200 import _lib
 lib=_lib.load()
-for r in bench_cfgs.cfg1(pb, lib, 6458.7, None):
-    print(r['config'], round(r['us_per_product'],2), round(r['value'],2), r['unit'], r['parity'])
-print(bench_cfgs._copy_floor(3072*1024, 64))
+r = bench_cfgs.cfg2_cfg3(pb, lib, 6458.7, None, (lambda p: (p, pb.quantize_model(p), None, None))(pb.synthetic_model(pb.Dims(**bench_cfgs.DIMS32), 1804)))
+for x in r: print(x['config'], x['value'], x.get('us_per_decoder_step'), x['parity'])
 "

@@ -216,6 +216,10 @@ int qnmt_set_att_ctx(int32_t mode);
  * (k_att_score5f, no k_att_scale launch); 0 (default): separate scale kernel
  * (A/B testing; results identical).  Returns the previous value. */
 int qnmt_set_att_fused_scale(int32_t enable);
+/* 1 (default): the two-MUFU scorer stages its tile with one bulk copy before
+ * the PDL wait (k_att_score8); 0: register-staged k_att_score5 (A/B testing;
+ * results identical).  Returns the previous value. */
+int qnmt_set_att_score8(int32_t enable);
 /* 1: tile-starved tcgen05 products (fewer output tiles than half the SMs)
  * split K over more CTAs, exact int32 partial sums added in a per-stream
  * workspace; 0 (default, measured faster at cfg1 B=64): never split (A/B

@@ -37,6 +37,7 @@ SIGNATURES = {
     "qnmt_set_att_fixcap": (I32, [I32]),
     "qnmt_set_att_ctx": (I32, [I32]),
     "qnmt_set_att_fused_scale": (I32, [I32]),
+    "qnmt_set_att_score8": (I32, [I32]),
     "qnmt_set_tc_split": (I32, [I32]),
     "qnmt_linear_i8": (I32, [P, I64, I64, I64, P, I64, P, I64, I64, P, P, I64, P, I64, P, P, I32, P, P]),
     "qnmt_attention_stats": (I32, [P, P, P, I32, I64, P, P]),

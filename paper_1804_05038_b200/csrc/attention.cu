@@ -86,6 +86,8 @@ __device__ __noinline__ int att_code_exact(float x, float st) { return quant_cod
 __device__ __forceinline__ float att_e_threshold(float st) { return 0.5f - (st * 1.02e-6f + 1.53e-5f); }
 constexpr int ATT_FIXCAP_MAX = 512;
 constexpr float ATT_E_BOUND = 20.0f;   // |ap|, |u| <= 20: E_ap E_u in [1.8e-35, 5.5e34], no ftz / overflow
+int g_att_score8 = 1;                  // two-MUFU scorer with the bulk-copied tile (k_att_score8)
+#define A4_FITS(A) ((A) / 4 <= AQ5 * AT)
 int g_att_fused_scale = 0;             // 1: two-MUFU scorer computes the scales itself (k_att_score5f; A/B: 125 vs 101 + 11 us)
 int g_att_fixcap = ATT_FIXCAP_MAX;      // tests: 0 forces the queue-overflow rescan
 int g_att_exp = 0;                      // scorer: 0 two-MUFU (score5), 1 one-MUFU (score6), 2 one-MUFU staged (score7)
@@ -705,12 +707,12 @@ k_att_score7(ScoreArgs g) {
     const int64_t A = g.A, A4 = A / 4;
     const int64_t row0 = g.sent_row[s] + i0;
     const bool tma = g.att_exp != nullptr && A4 <= AQ5 * AT;
-    if (threadIdx.x == 0 && tma) {
+    if (threadIdx.x == 0 && tma) {   // one row per copy: smem rows have the fixed stride AQ5 * AT quads
         tc::mbar_init(&bar, 1);
         tc::fence_mbar_init();
-        const uint32_t bytes = (uint32_t)(np * A * 4);
-        tc::mbar_arrive_expect_tx(&bar, bytes);
-        bulk_g2s(sap7, g.att_exp + row0 * A, bytes, &bar);
+        tc::mbar_arrive_expect_tx(&bar, (uint32_t)(np * A * 4));
+        for (int p = 0; p < np; ++p)
+            bulk_g2s(sap7 + p * (AQ5 * AT), g.att_exp + (row0 + p) * A, (uint32_t)(A * 4), &bar);
     }
     pdl_entry();
     const int P = g.sent_ncols[s];
@@ -816,6 +818,145 @@ k_att_score7(ScoreArgs g) {
         int t = 0;
 #pragma unroll
         for (int w = 0; w < AT / 32; ++w) t += red7[j][p][w];
+        g.scores[(int64_t)(c0 + j) * g.max_len + i0 + p] = dequant(t, g.v_scale[0], g.st_thr[c0 + j].x);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// k_att_score8: the two-MUFU scorer (codes identical to score5) restructured like
+// score7: the CTA's att_proj tile (rows i0 .. i0+np, contiguous) arrives by one
+// cp.async.bulk issued before the PDL wait (att_proj is fixed for the batch), so
+// no registers or instructions stage it; the 6-position element loop runs
+// unconditionally (stale rows are discarded) and the codes are summed by dp4a.
+// A position with an element inside the rounding window is rescanned inline from
+// the tile in shared memory (x = fl(ap + u) needs no global access), flagged
+// elements with the fp64 tanh.  Sentences with a degenerate scale (some
+// hypothesis' max |tanh| < 1.3e-4) take the score5 body.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(AT, 4)
+k_att_score8(ScoreArgs g) {
+    extern __shared__ __align__(128) float4 sap8[];   // [APC7][AQ5 * AT] = [p][A/4]
+    __shared__ __align__(8) uint64_t bar;
+    __shared__ int red8[AMAXP][APC7][AT / 32];
+    __shared__ int s_done;
+    const int s = blockIdx.y;
+    const int i0 = blockIdx.x * APC7;
+    const int l = g.sent_len[s];   // per-batch constants: safe before the PDL wait
+    if (i0 >= l) {
+        pdl_entry();
+        return;
+    }
+    const int np = min(l - i0, APC7);
+    const int64_t A = g.A, A4 = A / 4;
+    const int64_t row0 = g.sent_row[s] + i0;
+    if (threadIdx.x == 0) {   // one row per copy: smem rows have the fixed stride AQ5 * AT quads
+        tc::mbar_init(&bar, 1);
+        tc::fence_mbar_init();
+        tc::mbar_arrive_expect_tx(&bar, (uint32_t)(np * A * 4));
+        for (int p = 0; p < np; ++p)
+            bulk_g2s(sap8 + p * (AQ5 * AT), g.att_proj + (row0 + p) * A, (uint32_t)(A * 4), &bar);
+    }
+    pdl_entry();
+    const int P = g.sent_ncols[s];
+    const int c0 = g.sent_col_off[s];
+    bool fast = P > 0;
+    for (int j = 0; j < P; ++j) fast &= g.st_thr[c0 + j].x <= ATT_ST_FAST_MAX;
+    if (!fast) {
+        __syncthreads();
+        tc::mbar_wait(&bar, 0);   // the copy lands before the tile is restaged / the CTA exits
+        if (P == 0) return;
+        __syncthreads();
+        att_score_body<false>(g, sap8, red8, &s_done, s, P, l, i0);
+        return;
+    }
+    if (threadIdx.x == 0) s_done = 0;
+    const int lane = threadIdx.x & 31;
+    int vv4[AQ5];   // four int8 v codes per register (dp4a operand)
+    float4 uq[AQ5], ux[AQ5];
+#pragma unroll
+    for (int k = 0; k < AQ5; ++k) {
+        const int64_t q = threadIdx.x + (int64_t)AT * k;
+        const bool ok = q < A4;
+        vv4[k] = ok ? reinterpret_cast<const int*>(g.v_codes)[q] : 0;
+        uq[k] = ok ? reinterpret_cast<const float4*>(g.u + (int64_t)c0 * g.ldu)[q] : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    float4 sp = g.st_thr[c0];
+    __syncthreads();   // s_done initialised
+    tc::mbar_wait(&bar, 0);
+    for (int j = 0; j < P; ++j) {
+        float4 spx = sp;
+        if (j + 1 < P) {   // prefetch the next hypothesis' query slice and scale
+#pragma unroll
+            for (int k = 0; k < AQ5; ++k) {
+                const int64_t q = threadIdx.x + (int64_t)AT * k;
+                ux[k] = q < A4 ? reinterpret_cast<const float4*>(g.u + (int64_t)(c0 + j + 1) * g.ldu)[q]
+                               : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+            spx = g.st_thr[c0 + j + 1];
+        }
+        const float st = sp.x, thr = sp.y, m2st = -2.0f * st;
+        int acc[APC7];
+        float dmx[APC7];
+#pragma unroll
+        for (int p = 0; p < APC7; ++p) {
+            acc[p] = 0;
+            dmx[p] = 0.0f;
+#pragma unroll
+            for (int k = 0; k < AQ5; ++k) {
+                const float4 a4 = sap8[p * (AQ5 * AT) + k * AT + threadIdx.x];
+                uint32_t mb[4];
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const float x = __fadd_rn((&a4.x)[e], (&uq[k].x)[e]);
+                    const float r = rcp_approx(__fadd_rn(ex2_approx(__fmul_rn(x, 2.8853900817779268f)), 1.0f));
+                    const float v = fmaf(m2st, r, st);
+                    const float mg = __fadd_rn(v, 12582912.0f);   // 1.5 * 2^23: round to integer
+                    dmx[p] = fmaxf(dmx[p], fabsf(__fsub_rn(v, __fsub_rn(mg, 12582912.0f))));
+                    mb[e] = __float_as_uint(mg);   // low byte = the code
+                }
+                const uint32_t lo = __byte_perm(mb[0], mb[1], 0x0040), hi = __byte_perm(mb[2], mb[3], 0x0040);
+                acc[p] = __dp4a((int)__byte_perm(lo, hi, 0x5410), vv4[k], acc[p]);
+            }
+        }
+#pragma unroll
+        for (int p = 0; p < APC7; ++p) {
+            if (p < np && dmx[p] > thr) {   // rare: exact codes of this position's window elements
+                int d = 0;
+#pragma unroll
+                for (int k = 0; k < AQ5; ++k) {
+                    const float4 a4 = sap8[p * (AQ5 * AT) + k * AT + threadIdx.x];
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const float x = __fadd_rn((&a4.x)[e], (&uq[k].x)[e]);
+                        const float r = rcp_approx(__fadd_rn(ex2_approx(__fmul_rn(x, 2.8853900817779268f)), 1.0f));
+                        const float v = fmaf(m2st, r, st);
+                        const float mg = __fadd_rn(v, 12582912.0f);
+                        const int va = (int)(int8_t)(vv4[k] >> (8 * e));
+                        if (fabsf(__fsub_rn(v, __fsub_rn(mg, 12582912.0f))) > thr && va != 0)
+                            d += va * (att_code_exact(x, st) - (int)(int8_t)(__float_as_uint(mg) & 0xffu));
+                    }
+                }
+                acc[p] += d;
+            }
+            const int t = __reduce_add_sync(0xffffffffu, acc[p]);
+            if (lane == 0) red8[j][p][threadIdx.x >> 5] = t;
+        }
+#pragma unroll
+        for (int k = 0; k < AQ5; ++k) uq[k] = ux[k];
+        sp = spx;
+    }
+    int last = 0;
+    if (lane == 0) {
+        __threadfence_block();
+        last = atomicAdd(&s_done, 1) == AT / 32 - 1;
+    }
+    if (!__shfl_sync(0xffffffffu, last, 0)) return;
+    __threadfence_block();
+    for (int idx = lane; idx < P * np; idx += 32) {
+        const int j = idx / np, p = idx % np;
+        int t = 0;
+#pragma unroll
+        for (int w = 0; w < AT / 32; ++w) t += red8[j][p][w];
         g.scores[(int64_t)(c0 + j) * g.max_len + i0 + p] = dequant(t, g.v_scale[0], g.st_thr[c0 + j].x);
     }
 }
@@ -1276,6 +1417,11 @@ int attention_launch(const float* u, int64_t ldu, int64_t N, const int32_t* sent
             QNMT_CUDA(raise_smem_limit((const void*)k_att_score6, smem5, done6));
             QNMT_LAUNCH(k_att_score6, g5, AT, smem5, st, ga);
             QNMT_CHECK_LAUNCH("k_att_score6");
+        } else if (g_att_score8 && A4_FITS(A)) {
+            static size_t done8 = 0;
+            QNMT_CUDA(raise_smem_limit((const void*)k_att_score8, smem5, done8));
+            QNMT_LAUNCH(k_att_score8, g5, AT, smem5, st, ga);
+            QNMT_CHECK_LAUNCH("k_att_score8");
         } else {
             QNMT_CUDA(raise_smem_limit((const void*)k_att_score5, smem5, done5));
             QNMT_LAUNCH(k_att_score5, g5, AT, smem5, st, ga);
@@ -1430,6 +1576,12 @@ extern "C" int qnmt_attention(const float* u, int64_t ldu, int64_t N, const int3
 
 extern "C" int qnmt_attention_exp(const float* att_proj, int64_t n, float* att_exp, void* stream) {
     return qnmt::att_exp_launch(att_proj, n, att_exp, qnmt::as_stream(stream));
+}
+
+extern "C" int qnmt_set_att_score8(int32_t enable) {
+    const int old = qnmt::g_att_score8;
+    qnmt::g_att_score8 = enable ? 1 : 0;
+    return old;
 }
 
 extern "C" int qnmt_set_att_fused_scale(int32_t enable) {

@@ -350,7 +350,7 @@ static int encode_core(qnmt_engine* e, const int32_t* ids_dev, const int32_t* le
         pa.h2 = e->h2;
         pa.ctl = e->pk_ctl;
         pa.err = e->err;
-        QNMT_CUDA(cudaMemsetAsync(e->pk_ctl, 0, 8 * sizeof(int32_t), st));
+        QNMT_CUDA(cudaMemsetAsync(e->pk_ctl, 0, PK_CTL_INTS * sizeof(int32_t), st));
         TRY(enc1_launch(pa, st));
     } else {
     QNMT_CUDA(cudaMemsetAsync(e->h2, 0, sizeof(float) * (size_t)n * 2 * H, st));
@@ -950,7 +950,7 @@ int qnmt_engine_create(const qnmt_model* m, int32_t max_sentences, int32_t max_s
         e->max_steps = a.take<int32_t>(S);
         e->steps_run = a.take<int32_t>(S);
         e->np_tmp = a.take<int32_t>(S);
-        e->pk_ctl = a.take<int32_t>(8);
+        e->pk_ctl = a.take<int32_t>(PK_CTL_INTS);
         e->fin_cnt = a.take<int32_t>(S);
         e->fin_best = a.take<double>(S);
         if (pass == 0) {
@@ -1326,6 +1326,7 @@ static int decode_greedy1(qnmt_engine* e, const BatchPlan& b, cudaStream_t st) {
     a.step_dev = e->d_step;
     int32_t* ctl0 = e->h_pinned + 4;   // host staging of the control words
     ctl0[0] = 2; ctl0[1] = 0x7fffffff; ctl0[2] = 0; ctl0[3] = 0; ctl0[4] = 0;
+    QNMT_CUDA(cudaMemsetAsync(e->pk_ctl, 0, PK_CTL_INTS * sizeof(int32_t), st));   // barrier counters
     QNMT_CUDA(h2d(e, e->pk_ctl, ctl0, 5 * sizeof(int32_t), st));
     TRY(greedy1_launch(a, st));
     return check_flag(e, st);

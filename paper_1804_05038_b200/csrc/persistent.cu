@@ -43,7 +43,10 @@ constexpr int PK_MAXD = 2048;          // longest vector quantized per CTA (2H, 
 
 __device__ __forceinline__ float ldcg(const float* p) { return __ldcg(p); }
 
-// grid-wide barrier (generation counter); every CTA is resident (cooperative launch)
+// grid-wide barrier (generation counter); every CTA is resident (cooperative launch).
+// (A two-level variant -- groups of 16 CTAs on their own counters -- measured slower:
+// cfg3 74.3 vs 67.6 us per decoder step; the second atomic hop costs more latency than
+// the 148-way contention on one counter.)
 __device__ __forceinline__ void gsync(int32_t* ctl) {
     __syncthreads();
     if (threadIdx.x == 0) {

@@ -4,6 +4,10 @@
 
 namespace qnmt {
 
+// control words of the persistent kernels: [0..4] y, best token, done, barrier top
+// counter, barrier generation; [32 + 32 g] barrier group counters (persistent.cu gsync)
+constexpr int PK_CTL_INTS = 32 + 32 * 16;
+
 struct PkArgs {
     int E, H, A, R, V;
     const float* tgt_embed;

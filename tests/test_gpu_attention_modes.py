@@ -7,6 +7,8 @@ context (attention.cu):
 * one-MUFU scorer (k_att_score6): e^(2(ap+u)) = E_ap * E_u from per-batch /
   per-step fp64 exps, rounding-window elements queued and resolved exactly
   by the CTA's last warp;
+* k_att_score8: the two-MUFU scorer with its att_proj tile staged by one bulk
+  copy before the PDL wait, branch-free position loop and dp4a code sums;
 * k_att_score7: the one-MUFU scorer with its tile staged by one bulk copy
   before the PDL wait, branch-free position loop and dp4a code dot products;
 * score6 / score7 with the fixup queue disabled (every window hit goes
@@ -26,14 +28,16 @@ pytestmark = pytest.mark.gpu
 pb = pytest.importorskip("paper_1804_05038_b200")
 from paper_1804_05038_b200 import _dev, _lib  # noqa: E402
 
-# (scorer variant, fixup queue length, scale fused into the two-MUFU scorer)
-MODES = [(0, 512, 1), (0, 512, 0), (1, 512, 1), (1, 0, 1), (2, 512, 1), (2, 0, 1)]
+# (scorer variant, fixup queue length, scale fused into the two-MUFU scorer, bulk-staged two-MUFU scorer)
+MODES = [(0, 512, 0, 0), (0, 512, 0, 1), (0, 512, 1, 0), (1, 512, 0, 0), (1, 0, 0, 0), (2, 512, 0, 0),
+         (2, 0, 0, 0)]
 
 
 def _run(lib, mode, inp):
     old_e = lib.qnmt_set_att_exp(mode[0])
     old_c = lib.qnmt_set_att_fixcap(mode[1])
     old_f = lib.qnmt_set_att_fused_scale(mode[2])
+    old_8 = lib.qnmt_set_att_score8(mode[3])
     try:
         (att, ex, states, u, v, vs, off, cnt, rows_d, lens_d, S, N, A, H2, max_len) = inp
         mm = torch.empty((S, 2, A), device="cuda")
@@ -55,6 +59,7 @@ def _run(lib, mode, inp):
         lib.qnmt_set_att_exp(old_e)
         lib.qnmt_set_att_fixcap(old_c)
         lib.qnmt_set_att_fused_scale(old_f)
+        lib.qnmt_set_att_score8(old_8)
 
 
 def _inputs(seed, beams, scale_u, scale_ap, A=2048, H2=2048):
@@ -84,11 +89,13 @@ def _inputs(seed, beams, scale_u, scale_ap, A=2048, H2=2048):
     ("ragged_beams", 12, [1, 2, 3, 4, 5, 8, 16, 7, 5, 1, 16, 3], 0.5, 0.5),
     ("wide", 13, [5] * 12, 6.0, 6.0),          # |ap| / |u| partly beyond 20: mixed eligibility
     ("tiny", 14, [5] * 8, 1e-4, 1e-4),         # large per-hypothesis scales
+    ("small_A", 15, [5, 3, 1, 5], 0.5, 0.5, 40, 96),    # A, 2H below one CTA's quads
+    ("mid_A", 16, [5] * 6, 0.5, 0.5, 1000, 512),
 ])
 def test_scorer_variants_identical(case):
-    _, seed, beams, su, sa = case
+    _, seed, beams, su, sa = case[:5]
     lib = _lib.load()
-    inp = _inputs(seed, beams, su, sa)
+    inp = _inputs(seed, beams, su, sa, *case[5:])
     ref_ctx, ref_alpha = _run(lib, MODES[0], inp)
     for mode in MODES[1:]:
         ctx, alpha = _run(lib, mode, inp)
