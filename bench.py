@@ -55,8 +55,13 @@ METRIC = "tokens/sec (int8 beam-5 decode, target tokens excl. EOS)"
 WORKLOAD = ("cfg5 bulk translation: one step = the whole seeded 8192-sentence corpus (l~U[5,100]) sharded over "
             "the GPUs, 256 sentences per engine call, beam 5, max_ratio 1.5, V_tgt 50000, H 1024, E 512, A 2048, "
             "R 512")
-# DRAM bytes per algorithmic byte measured by `ncu --set full` at N = 1280 (profiles/r01_ncu_summary.md)
-NCU_TRAFFIC_RATIO = {"attention": 264.4 / 249.8, "vocab_stats": 27.72 / 50.30, "vocab_merge": 24.14 / 24.13}
+# DRAM bytes (dram__bytes_read.sum + dram__bytes_write.sum) per algorithmic byte, per launch, measured by
+# ncu on the current kernels in one cfg5 batch decode (batch 16, N = 1280, sum l = 13941;
+# benchmarks/one_batch.py): attention = k_att_scale + k_att_score8 + k_att_context4
+# (profiles/r02_ob_e0_c1_att_launches.csv, profiles/r02_ob_score8_att_launches.csv): 249.8 MB of 249.4 MB;
+# k_vocab_stats 27.13 + 0.60 MB of 50.30 MB (partials stay in L2) and k_vocab_merge 25.41 MB of
+# 24.13 MB (profiles/r02_ncu_full_summary.md)
+NCU_TRAFFIC_RATIO = {"attention": 249.76 / 249.38, "vocab_stats": 27.73 / 50.30, "vocab_merge": 25.41 / 24.13}
 
 
 def peaks():
@@ -292,6 +297,19 @@ def kernel_rooflines(rows, hbm, peak_kind, sm_mhz=None):
             continue
         ach = work[k] / t[k] / 1e9
         ratio = NCU_TRAFFIC_RATIO.get(k)
+        if k == "vocab_stats":   # a fused int8 GEMM: its roofline is the tensor pipe (HBM figures kept beside)
+            tops = ops_vocab / t[k] / 1e12
+            out[k] = {"bound": "tensor", "achieved": tops, "peak": 4500.0, "unit": "int8 TOPS",
+                      "frac": tops / 4500.0, "peak_source": "spec (4.5 POPS dense int8)",
+                      "hbm_GBps": ach, "hbm_frac": ach / hbm,
+                      "us_per_launch": 1e6 * t[k] / max(launches, 1),
+                      "traffic": (work[k] / max(launches, 1) * ratio) if ratio else None,
+                      "algorithmic_bytes_per_launch": work[k] / max(launches, 1),
+                      "share_of_step": t[k] / t["step"] if t["step"] > 0 else None}
+            unit, pk = peaks_c[k]
+            ca = comp[k] / t[k]
+            out[k]["compute"] = {"unit": unit, "achieved": ca, "peak": pk, "frac": ca / pk}
+            continue
         out[k] = {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
                   "us_per_launch": 1e6 * t[k] / max(launches, 1),
                   "traffic": (work[k] / max(launches, 1) * ratio) if ratio else None,
@@ -301,8 +319,6 @@ def kernel_rooflines(rows, hbm, peak_kind, sm_mhz=None):
             unit, pk = peaks_c[k]
             ca = comp[k] / t[k]
             out[k]["compute"] = {"unit": unit, "achieved": ca, "peak": pk, "frac": ca / pk}
-    if "vocab_stats" in out:
-        out["vocab_stats"]["int8_tensor_ops_per_s"] = ops_vocab / t["vocab_stats"]
     return out
 
 

@@ -1,13 +1,4 @@
 mkdir -p gpurun_out
-date +%s > gpurun_out/t0
 timeout 1200 python -m pytest tests -m gpu -x -q > gpurun_out/gputest_all.log 2>&1; tail -3 gpurun_out/gputest_all.log
-date +%s
-for s8 in 1 0; do QNMT_ATT_S8=$s8 timeout 400 python bench.py --no-cpu --no-configs --steps 3 > gpurun_out/bench_s8_$s8.json 2> gpurun_out/bench_s8_$s8.err; echo "rc=$? $(date +%s)"; python -c "import json;d=json.load(open('gpurun_out/bench_s8_$s8.json'));print($s8, d['value'], d['e2e']['value'], d['kernels']['attention']['us_per_launch'])"; done
-timeout 300 python -c "
-import sys; sys.path.insert(0,'.')
-import bench_cfgs, paper_1804_05038_b200 as pb
-from paper_1804_05038_b200 import _lib
-lib=_lib.load()
-r = bench_cfgs.cfg2_cfg3(pb, lib, 6458.7, None, (lambda p: (p, pb.quantize_model(p), None, None))(pb.synthetic_model(pb.Dims(**bench_cfgs.DIMS32), 1804)))
-for x in r: print(x['config'], x['value'], x.get('us_per_decoder_step'), x['parity'])
-"
+for m2 in 1 0; do QNMT_MERGE2=$m2 timeout 400 python bench.py --no-cpu --no-configs --steps 3 > gpurun_out/bench_m2_$m2.json 2> gpurun_out/bench_m2_$m2.err; python -c "import json;d=json.load(open('gpurun_out/bench_m2_$m2.json'));k=d['kernels'];print($m2, d['value'], d['e2e']['value'], k['vocab_merge']['us_per_launch'], k['vocab_stats']['us_per_launch'])"; done
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:k_vocab_merge --launch-skip 20 --launch-count 20 --csv python benchmarks/one_batch.py 16 1 > gpurun_out/ncu_m2.csv 2>/dev/null; grep -c merge gpurun_out/ncu_m2.csv
