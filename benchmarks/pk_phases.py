@@ -10,6 +10,7 @@ import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_1804_05038_b200 as pb  # noqa: E402
+from paper_1804_05038_b200.engine import engine_pool  # noqa: E402
 from paper_1804_05038_b200 import _lib  # noqa: E402
 
 NAMES = ["P0 emb/s + GEMV Wx2,Uzr2", "P1 gates + GEMV Uc2", "P2 combine + GEMV Uatt,Uzr3", "P3 scale + scores",

@@ -1,13 +1,11 @@
 mkdir -p gpurun_out
-timeout 600 python -m pytest tests/test_gpu_qmath.py -x -q > gpurun_out/t_gs.log 2>&1; tail -2 gpurun_out/t_gs.log
+timeout 900 python -m pytest tests/test_gpu_translate.py tests/test_baseline_parity.py -x -q > gpurun_out/t_pk.log 2>&1; tail -2 gpurun_out/t_pk.log
+timeout 300 python benchmarks/pk_phases.py > gpurun_out/pk_phases.json 2>&1; cat gpurun_out/pk_phases.json
 timeout 300 python -c "
 import sys; sys.path.insert(0,'.')
 import bench_cfgs, paper_1804_05038_b200 as pb
 from paper_1804_05038_b200 import _lib
 lib=_lib.load()
-for gs in (1,0):
-    lib.qnmt_set_gemv_gs(gs)
-    for M,K in ((32768,1024),(65536,1024),(65536,512),(16384,4096)):
-        r=bench_cfgs.gemv_stream(pb, 6458.7, M=M, K=K)
-        print(gs, M, K, round(r['us'],2), round(r['GBps'],1), round(r['hbm_frac'],3))
+r = bench_cfgs.cfg2_cfg3(pb, lib, 6458.7, None, (lambda p: (p, pb.quantize_model(p), None, None))(pb.synthetic_model(pb.Dims(**bench_cfgs.DIMS32), 1804)))
+for x in r: print(x['config'], x['value'], x.get('ms'), x.get('us_per_decoder_step'), x['parity'])
 "

@@ -127,6 +127,7 @@ __device__ __forceinline__ void gemv(const int8_t* __restrict__ W, int M, int K,
         int acc[PK_RB];
 #pragma unroll
         for (int r = 0; r < PK_RB; ++r) acc[r] = 0;
+#pragma unroll 2   // K <= 1024: every chunk's loads issued together (one L2 round trip)
         for (int k = lane * 16; k < K; k += 512) {
             const int4 b = *reinterpret_cast<const int4*>(q + k);
             int4 wv[PK_RB];
@@ -150,11 +151,26 @@ __device__ __forceinline__ void gemv(const int8_t* __restrict__ W, int M, int K,
         }
         const int m = mb + lane;
         if (lane < PK_RB && m < m1) {
-            float y = dequant(mine, ws[m / rps], sx);
+            const float sw = ws[m / rps];
+            float y = dequant_rcp(mine, (1.0 / (double)sw) * (1.0 / (double)sx), sw, sx);   // == dequant()
             if (bias) y = __fadd_rn(y, bias[m]);
             out[row0 + m] = y;
         }
     }
+}
+
+// L1 prefetch of the weight rows this warp's gemv() will read in the next phase
+// (same row distribution), issued before the grid barrier so the L2 latency of the
+// first loads overlaps the barrier wait.
+__device__ __forceinline__ void prefetch_rows(const int8_t* __restrict__ W, int M, int K, int gw, int nw) {
+    const int lane = threadIdx.x & 31;
+    const int rpw = (M + nw - 1) / nw;
+    const int m0 = gw * rpw, m1 = min(M, m0 + rpw);
+    if (m0 >= m1) return;
+    const int64_t bytes = (int64_t)(m1 - m0) * K;
+    const int8_t* base = W + (int64_t)m0 * K;
+    for (int64_t o = (int64_t)lane * 128; o < bytes; o += 32 * 128)
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(base + o));
 }
 
 #define PK_STAMP(k)                                                                 \
@@ -179,19 +195,23 @@ __global__ void __launch_bounds__(PK_T, 1) k_greedy1(PkArgs a) {
     int y = 2;            // BOS = EOS (decoder.py:109); afterwards the token every CTA selected
     for (int t = 0; t < a.max_steps; ++t) {
         // ---- P0: q(emb[y]), q(s); GEMV [W_x2; W_e] and U_zr2 ----
+        #pragma unroll 4   // independent iterations: their L2 loads in flight together
         for (int j = threadIdx.x; j < E; j += PK_T) vals[j] = a.tgt_embed[(int64_t)y * E + j];
         __syncthreads();
         const float se = quantize_vec(vals, E, q, red, a.err);
         gemv(a.w2x, LX, E, a.w2x_s, 1, q, se, a.b2x, a.gxr, 0, gw, nw);
         __syncthreads();
+        #pragma unroll 4   // independent iterations: their L2 loads in flight together
         for (int j = threadIdx.x; j < H; j += PK_T) vals[j] = ldcg(a.s + j);
         __syncthreads();
         const float ss = quantize_vec(vals, H, q, red, a.err);
         gemv(a.uzr2, 2 * H, H, a.uzr2_s, H, q, ss, nullptr, a.gh, 0, gw, nw);
+        prefetch_rows(a.uc2, H, H, gw, nw);
         gsync(a.ctl);
         PK_STAMP(0);
         // ---- P1: gates of dec_r -> q(r * s); GEMV U_c2 ----
         bool bad = false;
+        #pragma unroll 4   // independent iterations: their L2 loads in flight together
         for (int j = threadIdx.x; j < H; j += PK_T) {
             const float pz = __fadd_rn(ldcg(a.gxr + j), ldcg(a.gh + j));
             const float pr = __fadd_rn(ldcg(a.gxr + H + j), ldcg(a.gh + H + j));
@@ -202,9 +222,11 @@ __global__ void __launch_bounds__(PK_T, 1) k_greedy1(PkArgs a) {
         __syncthreads();
         const float srh = quantize_vec(vals, H, q, red, a.err);
         gemv(a.uc2, H, H, a.uc2_s, H, q, srh, nullptr, a.ghc, 0, gw, nw);
+        prefetch_rows(a.wuq, A + 2 * H, H, gw, nw);
         gsync(a.ctl);
         PK_STAMP(1);
         // ---- P2: combine of dec_r -> s', q(s'); GEMV [U_att; U_zr3] ----
+        #pragma unroll 4   // independent iterations: their L2 loads in flight together
         for (int j = threadIdx.x; j < H; j += PK_T) {
             const float z = sigmoid_b(__fadd_rn(ldcg(a.gxr + j), ldcg(a.gh + j)));
             const float pc = __fadd_rn(ldcg(a.gxr + 2 * H + j), ldcg(a.ghc + j));
@@ -223,6 +245,7 @@ __global__ void __launch_bounds__(PK_T, 1) k_greedy1(PkArgs a) {
         float st;
         {
             uint32_t m = 0;
+            #pragma unroll 4   // independent iterations: their L2 loads in flight together
             for (int k = threadIdx.x; k < A; k += PK_T) {
                 const float u = ldcg(a.uq + k);
                 m = max(m, __float_as_uint(__fadd_rn(a.att_mm[k], u)) & 0x7fffffffu);
@@ -236,11 +259,13 @@ __global__ void __launch_bounds__(PK_T, 1) k_greedy1(PkArgs a) {
             const float tmax = tanh_b(__uint_as_float(m));
             st = (tmax == 0.0f) ? 1.0f : __fdiv_rn(127.0f, tmax);
         }
+        #pragma unroll 4   // independent iterations: their L2 loads in flight together
         for (int k = threadIdx.x; k < A; k += PK_T) vals[k] = ldcg(a.uq + k);
         __syncthreads();
         for (int i = blockIdx.x; i < a.l; i += gridDim.x) {
             int acc = 0;
             const float* ap = a.att + (int64_t)i * A;
+            #pragma unroll 4   // independent iterations: their L2 loads in flight together
             for (int k = threadIdx.x; k < A; k += PK_T)
                 acc += (int)a.v[k] * quant_code(tanh_b(__fadd_rn(ap[k], vals[k])), st);
             acc = warp_sum(acc);
@@ -301,17 +326,21 @@ __global__ void __launch_bounds__(PK_T, 1) k_greedy1(PkArgs a) {
                 a.ctx[c] = __double2float_rn(acc);
             }
         }
+        prefetch_rows(a.w3x, LX, 2 * H, gw, nw);
         gsync(a.ctl);
         PK_STAMP(4);
         // ---- P5: q(ctx); GEMV [W_x3; W_c] ----
+        #pragma unroll 4   // independent iterations: their L2 loads in flight together
         for (int j = threadIdx.x; j < 2 * H; j += PK_T) vals[j] = ldcg(a.ctx + j);
         __syncthreads();
         const float sctx = quantize_vec(vals, 2 * H, q, red, a.err);
         gemv(a.w3x, LX, 2 * H, a.w3x_s, 1, q, sctx, a.b3x, a.gxq, 0, gw, nw);
+        prefetch_rows(a.uc3, H, H, gw, nw);
         gsync(a.ctl);
         PK_STAMP(5);
         // ---- P6: gates of dec_q (h = s') -> q(r * s'); GEMV U_c3 ----
         bad = false;
+        #pragma unroll 4   // independent iterations: their L2 loads in flight together
         for (int j = threadIdx.x; j < H; j += PK_T) {
             const float pz = __fadd_rn(ldcg(a.gxq + j), ldcg(a.uq + A + j));
             const float pr = __fadd_rn(ldcg(a.gxq + H + j), ldcg(a.uq + A + H + j));
@@ -322,9 +351,11 @@ __global__ void __launch_bounds__(PK_T, 1) k_greedy1(PkArgs a) {
         __syncthreads();
         const float srh3 = quantize_vec(vals, H, q, red, a.err);
         gemv(a.uc3, H, H, a.uc3_s, H, q, srh3, nullptr, a.ghc, 0, gw, nw);
+        prefetch_rows(a.w_state, R, H, gw, nw);
         gsync(a.ctl);
         PK_STAMP(6);
         // ---- P7: combine of dec_q -> s_new (next state), q(s_new); GEMV W_s + b_r ----
+        #pragma unroll 4   // independent iterations: their L2 loads in flight together
         for (int j = threadIdx.x; j < H; j += PK_T) {
             const float z = sigmoid_b(__fadd_rn(ldcg(a.gxq + j), ldcg(a.uq + A + j)));
             const float pc = __fadd_rn(ldcg(a.gxq + 2 * H + j), ldcg(a.ghc + j));
@@ -337,9 +368,11 @@ __global__ void __launch_bounds__(PK_T, 1) k_greedy1(PkArgs a) {
         __syncthreads();
         const float ssn = quantize_vec(vals, H, q, red, a.err);
         gemv(a.w_state, R, H, a.w_state_s, R, q, ssn, a.b_r, a.ro, 0, gw, nw);
+        prefetch_rows(a.w_vocab, V, R, gw, nw);
         gsync(a.ctl);
         PK_STAMP(7);
         // ---- P8: readout tanh -> q; vocabulary GEMV (logits) ----
+        #pragma unroll 4   // independent iterations: their L2 loads in flight together
         for (int j = threadIdx.x; j < R; j += PK_T) {
             const float x = __fadd_rn(__fadd_rn(ldcg(a.ro + j), ldcg(a.gxr + 3 * H + j)), ldcg(a.gxq + 3 * H + j));
             if (!is_finite_f(x) && blockIdx.x == 0) set_flag(a.err, QNMT_FLAG_NUMERIC);
@@ -348,13 +381,15 @@ __global__ void __launch_bounds__(PK_T, 1) k_greedy1(PkArgs a) {
         __syncthreads();
         const float sro = quantize_vec(vals, R, q, red, a.err);
         gemv(a.w_vocab, V, R, a.w_vocab_s, V, q, sro, a.b_vocab, a.logits, 0, gw, nw);
-        gsync(a.ctl);
+        __threadfence_block();
+        __syncthreads();   // P9 reads only the logits this CTA's warps just wrote: no grid barrier
         PK_STAMP(8);
-        // ---- P9: per-CTA (max, sum exp(x - max)) over a contiguous token range ----
-        const int per = (V + gridDim.x - 1) / gridDim.x;
+        // ---- P9: per-CTA (max, sum exp(x - max)) over the CTA's own vocabulary GEMV rows ----
+        const int per = PK_W * ((V + nw - 1) / nw);
         const int v0 = blockIdx.x * per, v1 = min(V, v0 + per);
         {
             float m = -3.402823466e38f;
+            #pragma unroll 4   // independent iterations: their L2 loads in flight together
             for (int v = v0 + threadIdx.x; v < v1; v += PK_T) m = fmaxf(m, ldcg(a.logits + v));
             m = warp_max(m);
             if (lane == 0) vals[warp] = m;
@@ -362,6 +397,7 @@ __global__ void __launch_bounds__(PK_T, 1) k_greedy1(PkArgs a) {
             float mm = vals[0];
             for (int w = 1; w < PK_W; ++w) mm = fmaxf(mm, vals[w]);
             double sacc = 0.0;
+            #pragma unroll 4   // independent iterations: their L2 loads in flight together
             for (int v = v0 + threadIdx.x; v < v1; v += PK_T) {
                 const float x = ldcg(a.logits + v);
                 if (!is_finite_f(x)) set_flag(a.err, QNMT_FLAG_NUMERIC);
@@ -378,6 +414,8 @@ __global__ void __launch_bounds__(PK_T, 1) k_greedy1(PkArgs a) {
                 a.part[2 * blockIdx.x + 1] = v0 < v1 ? tot : 0.0;
             }
         }
+        prefetch_rows(a.w2x, LX, E, gw, nw);   // the next step's P0 (after P10 / P11, no barrier between)
+        prefetch_rows(a.uzr2, 2 * H, H, gw, nw);
         gsync(a.ctl);
         PK_STAMP(9);
         // ---- P10: lse (every CTA, same order); smallest token with the best log-prob ----
@@ -535,6 +573,7 @@ __global__ void __launch_bounds__(PK_T, 1) k_enc1(PeArgs a) {
         for (int d = 0; d < 2; ++d) {
             const float* gx = a.gx + ((int64_t)pos[d] * 2 + d) * 3 * H;
             bool bad = false;
+            #pragma unroll 4   // independent iterations: their L2 loads in flight together
             for (int j = threadIdx.x; j < H; j += PK_T) {
                 const float pz = __fadd_rn(gx[j], ldcg(a.gh + d * 2 * H + j));
                 const float pr = __fadd_rn(gx[H + j], ldcg(a.gh + d * 2 * H + H + j));
@@ -554,6 +593,7 @@ __global__ void __launch_bounds__(PK_T, 1) k_enc1(PeArgs a) {
 #pragma unroll
         for (int d = 0; d < 2; ++d) {
             const float* gx = a.gx + ((int64_t)pos[d] * 2 + d) * 3 * H + 2 * H;
+            #pragma unroll 4   // independent iterations: their L2 loads in flight together
             for (int j = threadIdx.x; j < H; j += PK_T) {
                 const float pc = __fadd_rn(gx[j], ldcg(a.ghc + d * H + j));
                 if (!is_finite_f(pc) && blockIdx.x == 0) set_flag(a.err, QNMT_FLAG_NUMERIC);
