@@ -436,6 +436,12 @@ int qnmt_engine_profile_read(const qnmt_engine* e, double* ms, double* calls, do
 
 /* device bytes held by the engine (scratch + history) */
 size_t qnmt_engine_bytes(const qnmt_engine* e);
+/* Checked mode (QNMT_CANARY=1 in the environment when the engine is created):
+ * every device buffer of the engine is followed by a 256-byte guard band of
+ * 0xA5.  Returns the number of guard bytes that changed (0: no out-of-bounds
+ * write into a neighbouring buffer so far), -1 if the engine is not in checked
+ * mode.  Synchronises the stream. */
+int64_t qnmt_engine_check_canaries(qnmt_engine* e, void* stream);
 
 #if defined(__GNUC__)
 #pragma GCC visibility pop

@@ -57,6 +57,7 @@ SIGNATURES = {
     "qnmt_engine_create": (I32, [P, I32, I32, I32, P]),
     "qnmt_engine_destroy": (I32, [P]),
     "qnmt_engine_bytes": (C.c_size_t, [P]),
+    "qnmt_engine_check_canaries": (I64, [P, P]),
     "qnmt_translate_batch": (I32, [P, P, P, I32, I32, F64, P, I32, P, P, P]),
     "qnmt_translate_ensemble": (I32, [P, I32, P, P, I32, I32, F64, P, I32, P, P, P]),
     "qnmt_encode_batch": (I32, [P, P, P, I32, P, P, P, P]),

@@ -56,17 +56,39 @@ struct qnmt_model {
 namespace qnmt {
 
 // simple bump allocator over one cudaMalloc block
+// Bump allocator of an engine's device block.  Checked mode (QNMT_CANARY=1 in the
+// environment when the engine is created): every buffer is followed by a 256-byte
+// guard band filled with 0xA5; qnmt_engine_check_canaries counts guard bytes that
+// changed -- an out-of-bounds write into a neighbouring buffer (the memcheck class
+// of bug) shows up there.  (compute-sanitizer is not available on the GPU pool.)
+constexpr size_t ARENA_GUARD = 256;
 struct Arena {
     char* base = nullptr;
     size_t cap = 0, used = 0;
+    bool guard = false;
+    std::vector<size_t>* guards = nullptr;   // guard band offsets (checked mode)
     template <typename T>
     T* take(size_t n) {
         size_t bytes = (n * sizeof(T) + 255) & ~(size_t)255;
         T* p = reinterpret_cast<T*>(base + used);
         used += bytes;
+        if (guard) {
+            if (guards) guards->push_back(used);
+            used += ARENA_GUARD;
+        }
         return p;
     }
 };
+
+__global__ void k_check_guards(const unsigned char* base, const size_t* offs, int n, unsigned long long* bad) {
+    for (int g = blockIdx.x; g < n; g += gridDim.x) {
+        const unsigned char* p = base + offs[g];
+        int c = 0;
+        for (int i = threadIdx.x; i < (int)ARENA_GUARD; i += blockDim.x) c += p[i] != 0xA5;
+        c = __reduce_add_sync(0xffffffffu, c);
+        if ((threadIdx.x & 31) == 0 && c) atomicAdd(bad, (unsigned long long)c);
+    }
+}
 
 }  // namespace qnmt
 
@@ -77,6 +99,9 @@ struct qnmt_engine {
     int64_t PMAX;      // S * L
     char* block = nullptr;
     size_t block_bytes = 0;
+    bool guard = false;              // checked mode: guard bands after every device buffer
+    std::vector<size_t> guards;      // their offsets in block
+    size_t* guards_dev = nullptr;
     // shared
     int32_t* err;            // device sticky flag
     uint32_t* seg_bits;      // [max(PMAX, 2S, S)]
@@ -850,9 +875,13 @@ int qnmt_engine_create(const qnmt_model* m, int32_t max_sentences, int32_t max_s
     e->NMAX = N; e->PMAX = P;
     const size_t idx = std::max(P, std::max(2 * S, N));
     size_t bytes = 0;
+    {
+        const char* cv = getenv("QNMT_CANARY");
+        e->guard = cv && cv[0] == '1';
+    }
     // size pass then carve pass
     for (int pass = 0; pass < 2; ++pass) {
-        Arena a{e->block, pass ? e->block_bytes : 0, 0};
+        Arena a{e->block, pass ? e->block_bytes : 0, 0, e->guard, pass ? &e->guards : nullptr};
         e->err = a.take<int32_t>(4);
         e->seg_bits = a.take<uint32_t>(idx);
         e->iota = a.take<int32_t>(idx);
@@ -960,6 +989,11 @@ int qnmt_engine_create(const qnmt_model* m, int32_t max_sentences, int32_t max_s
             if (ce != cudaSuccess) { delete e; return cuda_status(ce, "engine cudaMalloc"); }
         }
     }
+    if (e->guard) {   // fill the guard bands; their offsets to the device for the checker
+        for (size_t o : e->guards) cudaMemset(e->block + o, 0xA5, ARENA_GUARD);
+        cudaMalloc(&e->guards_dev, std::max<size_t>(1, e->guards.size()) * sizeof(size_t));
+        cudaMemcpy(e->guards_dev, e->guards.data(), e->guards.size() * sizeof(size_t), cudaMemcpyHostToDevice);
+    }
     std::vector<int32_t> io(idx), ev(S), od(S);
     for (size_t i = 0; i < idx; ++i) io[i] = (int32_t)i;
     for (size_t i = 0; i < S; ++i) { ev[i] = (int32_t)(2 * i); od[i] = (int32_t)(2 * i + 1); }
@@ -1022,6 +1056,7 @@ int qnmt_engine_destroy(qnmt_engine* e) {
     if (!e) return QNMT_OK;
     cudaDeviceSynchronize();
     if (e->block) cudaFree(e->block);
+    if (e->guards_dev) cudaFree(e->guards_dev);
     if (e->hblock) cudaFree(e->hblock);
     if (e->h_pinned) cudaFreeHost(e->h_pinned);
     if (e->res_host) cudaFreeHost(e->res_host);
@@ -1079,6 +1114,22 @@ int qnmt_engine_profile_read(const qnmt_engine* e, double* ms, double* calls, do
 }
 
 size_t qnmt_engine_bytes(const qnmt_engine* e) { return e ? e->block_bytes + e->hblock_bytes : 0; }
+
+int64_t qnmt_engine_check_canaries(qnmt_engine* e, void* stream) {
+    if (!e || !e->guard) return -1;
+    cudaStream_t st = qnmt::as_stream(stream);
+    unsigned long long* bad = nullptr;
+    if (cudaMalloc(&bad, sizeof(unsigned long long)) != cudaSuccess) return -2;
+    cudaMemsetAsync(bad, 0, sizeof(unsigned long long), st);
+    if (!e->guards.empty())
+        qnmt::k_check_guards<<<std::min<size_t>(e->guards.size(), 1024), 256, 0, st>>>(
+            reinterpret_cast<const unsigned char*>(e->block), e->guards_dev, (int)e->guards.size(), bad);
+    unsigned long long h = 0;
+    cudaMemcpyAsync(&h, bad, sizeof(h), cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    cudaFree(bad);
+    return (int64_t)h;
+}
 
 int qnmt_encode_batch(qnmt_engine* e, const int32_t* src_ids_dev, const int32_t* src_len, int32_t n,
                       float* states, float* att_proj, float* s0, void* stream) {
