@@ -45,7 +45,7 @@ def _run(lib, mode, inp):
         _lib.call("qnmt_attention_stats", att.data_ptr(), rows_d.data_ptr(), lens_d.data_ptr(), S, A,
                   mm.data_ptr(), st)
         ctx = torch.empty((N, H2), device="cuda")
-        alpha = torch.empty((N, max_len), device="cuda")
+        alpha = torch.zeros((N, max_len), device="cuda")   # (entries past a sentence's length stay 0)
         scratch = torch.empty(N * (104 + A) + 4 * N * max_len + 1024, dtype=torch.int32, device="cuda")
         f = _dev.reset_flag()
         _lib.call("qnmt_attention", u.data_ptr(), A, N, off.data_ptr(), cnt.data_ptr(), S, att.data_ptr(),
@@ -91,6 +91,8 @@ def _inputs(seed, beams, scale_u, scale_ap, A=2048, H2=2048):
     ("tiny", 14, [5] * 8, 1e-4, 1e-4),         # large per-hypothesis scales
     ("small_A", 15, [5, 3, 1, 5], 0.5, 0.5, 40, 96),    # A, 2H below one CTA's quads
     ("mid_A", 16, [5] * 6, 0.5, 0.5, 1000, 512),
+    ("small_x", 17, [5] * 12, 0.09, 0.09),     # |x| <= 0.75 throughout (the decode's own range)
+    ("small_x_mixed", 18, [5, 3, 5, 1] * 4, 0.12, 0.12),
 ])
 def test_scorer_variants_identical(case):
     _, seed, beams, su, sa = case[:5]
@@ -99,5 +101,7 @@ def test_scorer_variants_identical(case):
     ref_ctx, ref_alpha = _run(lib, MODES[0], inp)
     for mode in MODES[1:]:
         ctx, alpha = _run(lib, mode, inp)
-        assert np.array_equal(alpha, ref_alpha), mode
+        bad = np.argwhere(alpha != ref_alpha)
+        assert np.array_equal(alpha, ref_alpha), (mode, len(bad), bad[:6].tolist(),
+                                                  [(float(alpha[tuple(b)]), float(ref_alpha[tuple(b)])) for b in bad[:3]])
         assert np.array_equal(ctx, ref_ctx), mode
