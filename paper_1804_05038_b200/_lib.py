@@ -12,7 +12,8 @@ import threading
 
 from . import errors
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libqnmt_b200.so")
+LIB_PATH = os.environ.get("QNMT_LIB_PATH") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib",
+                                                            "libqnmt_b200.so")   # (override: A/B builds)
 
 P = C.c_void_p
 I64 = C.c_int64

@@ -31,6 +31,9 @@
 #include "kernels.cuh"
 #include "tc_common.cuh"
 
+#ifndef QNMT_APC
+#define QNMT_APC 6
+#endif
 #define TRY_LAUNCH(x) do { int _r = (x); if (_r != QNMT_OK) return _r; } while (0)
 
 namespace qnmt {
@@ -333,7 +336,7 @@ k_att_score4(const float* __restrict__ u, int64_t ldu, const int32_t* __restrict
 //   EXPM = true  (k_att_score6, sentences whose hypotheses are all eligible):
 //     tile = E_ap, query = E_u, one MUFU per element; elements in the rounding
 //     window are recomputed exactly from att_proj / u in global memory.
-constexpr int APC5 = 6;        // positions per CTA (48 KB of tile slices: 4 CTAs / SM)
+constexpr int APC5 = QNMT_APC;   // positions per CTA (6: 48 KB of tile slices, 4 CTAs / SM)
 constexpr int AQ5 = 2;         // a-quads per thread (A <= 4 * AT * AQ5 = 2048)
 
 struct ScoreArgs {
@@ -679,7 +682,7 @@ k_att_score6(ScoreArgs g) {
 // Needs A == 4*AT*AQ5 (2048) or smaller with A % 4 == 0, and every hypothesis
 // of the sentence eligible (|att_proj|, |u| <= 20); k_att_score7 falls back to
 // the two-MUFU body for the others (as score6).
-constexpr int APC7 = 6;
+constexpr int APC7 = APC5;
 static_assert(APC7 == APC5, "score7 falls back to the score5 body on the same position chunks");
 
 // 1-D TMA bulk copy global -> shared, completing on an mbarrier
