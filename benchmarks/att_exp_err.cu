@@ -55,7 +55,7 @@ __device__ __forceinline__ uint32_t hash32(uint32_t x) {
 __device__ __forceinline__ float unif(uint32_t h) { return (h >> 8) * (1.0f / 16777216.0f); }
 
 // analytic bound used by the kernel (attention.cu, att_e_threshold): K1 * st + K2
-constexpr double K1 = 1.02e-6, K2 = 1.53e-5;
+constexpr double K1 = 5.5e-7, K2 = 9.5e-6;
 
 __global__ void k_mc(uint64_t n, int dist, unsigned long long* out) {
     double worst = 0, worst_abs = 0;
