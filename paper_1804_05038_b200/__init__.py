@@ -58,6 +58,7 @@ from .qmath import (
     QuantizedMatrix,
     dequantize,
     gemm_f32,
+    gemm_f32_blocked,
     qgemm,
     qgemm_panel,
     quantize,
@@ -67,7 +68,7 @@ from .qmath import (
 __all__ = [
     "AttentionNet", "BeamHypothesis", "DecodeConfig", "DecoderState", "Dims", "EncoderStates",
     "Engine", "Float32Model", "GruCell", "ParityReport", "bleu", "compare_precisions", "edit_distance",
-    "gemm_f32", "to_device_f32", "INT8_MAX", "INT32_SAFE_K", "LinearOp", "ModelParams", "Network",
+    "gemm_f32", "gemm_f32_blocked", "to_device_f32", "INT8_MAX", "INT32_SAFE_K", "LinearOp", "ModelParams", "Network",
     "OutputNet", "QuantizationStats", "QuantizedMatrix", "QuantizedModel", "attend", "bpe_merge",
     "build_network", "dequantize", "errors", "generate_model", "gru_step", "load_model", "load_quantized", "qgemm", "qgemm_panel",
     "quantize", "quantize_activations", "quantize_model", "save_model", "synthetic_model", "tensor_specs",

@@ -43,29 +43,26 @@ constexpr int PK_MAXD = 2048;          // longest vector quantized per CTA (2H, 
 
 __device__ __forceinline__ float ldcg(const float* p) { return __ldcg(p); }
 
-// grid-wide barrier (generation counter); every CTA is resident (cooperative launch).
+// grid-wide barrier; every CTA is resident (cooperative launch).  One monotonically
+// increasing arrival counter (zeroed by the host before the launch): barrier number b is
+// passed when the counter reaches b * gridDim.x, so an arrival is ONE fire-and-forget
+// red.release (no returned value, no reset, no separate generation word) and the wait is
+// an acquire load of the same word -- the last arriver's critical path is one L2 hop
+// instead of four dependent round trips (load generation, add, exchange, add generation).
+// `epoch` is the caller's running target (uniform across the grid).
 // (A two-level variant -- groups of 16 CTAs on their own counters -- measured slower:
-// cfg3 74.3 vs 67.6 us per decoder step; the second atomic hop costs more latency than
-// the 148-way contention on one counter.)
-__device__ __forceinline__ void gsync(int32_t* ctl) {
+// cfg3 74.3 vs 67.6 us per decoder step; the second hop costs more latency than the
+// 148-way contention on one counter.)
+__device__ __forceinline__ void gsync(int32_t* ctl, unsigned& epoch) {
     __syncthreads();
+    epoch += gridDim.x;
     if (threadIdx.x == 0) {
         unsigned* count = reinterpret_cast<unsigned*>(ctl + 3);
-        unsigned* gen = reinterpret_cast<unsigned*>(ctl + 4);
-        unsigned g;
-        asm volatile("ld.acquire.gpu.u32 %0, [%1];" : "=r"(g) : "l"(gen) : "memory");
-        __threadfence();
-        if (atomicAdd(count, 1u) == gridDim.x - 1) {
-            atomicExch(count, 0u);
-            __threadfence();
-            atomicAdd(gen, 1u);
-        } else {
-            unsigned cur;
-            do {
-                asm volatile("ld.acquire.gpu.u32 %0, [%1];" : "=r"(cur) : "l"(gen) : "memory");
-            } while (cur == g);
-        }
-        __threadfence();
+        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(count) : "memory");
+        unsigned cur;
+        do {
+            asm volatile("ld.acquire.gpu.u32 %0, [%1];" : "=r"(cur) : "l"(count) : "memory");
+        } while ((int)(cur - epoch) < 0);
     }
     __syncthreads();
 }
@@ -181,6 +178,7 @@ __device__ __forceinline__ void prefetch_rows(const int8_t* __restrict__ W, int 
     }
 
 __global__ void __launch_bounds__(PK_T, 1) k_greedy1(PkArgs a) {
+    unsigned gs_epoch = 0;   // grid-barrier target (gsync)
     extern __shared__ __align__(16) unsigned char pk_smem[];
     __shared__ __align__(16) int8_t q[PK_MAXD];
     __shared__ __align__(16) float vals[PK_MAXD];
@@ -207,7 +205,7 @@ __global__ void __launch_bounds__(PK_T, 1) k_greedy1(PkArgs a) {
         const float ss = quantize_vec(vals, H, q, red, a.err);
         gemv(a.uzr2, 2 * H, H, a.uzr2_s, H, q, ss, nullptr, a.gh, 0, gw, nw);
         prefetch_rows(a.uc2, H, H, gw, nw);
-        gsync(a.ctl);
+        gsync(a.ctl, gs_epoch);
         PK_STAMP(0);
         // ---- P1: gates of dec_r -> q(r * s); GEMV U_c2 ----
         bool bad = false;
@@ -223,7 +221,7 @@ __global__ void __launch_bounds__(PK_T, 1) k_greedy1(PkArgs a) {
         const float srh = quantize_vec(vals, H, q, red, a.err);
         gemv(a.uc2, H, H, a.uc2_s, H, q, srh, nullptr, a.ghc, 0, gw, nw);
         prefetch_rows(a.wuq, A + 2 * H, H, gw, nw);
-        gsync(a.ctl);
+        gsync(a.ctl, gs_epoch);
         PK_STAMP(1);
         // ---- P2: combine of dec_r -> s', q(s'); GEMV [U_att; U_zr3] ----
         #pragma unroll 4   // independent iterations: their L2 loads in flight together
@@ -239,7 +237,7 @@ __global__ void __launch_bounds__(PK_T, 1) k_greedy1(PkArgs a) {
         __syncthreads();
         const float ssp = quantize_vec(vals, H, q, red, a.err);
         gemv(a.wuq, A + 2 * H, H, a.wuq_s, 1, q, ssp, nullptr, a.uq, 0, gw, nw);
-        gsync(a.ctl);
+        gsync(a.ctl, gs_epoch);
         PK_STAMP(2);
         // ---- P3: attention scale (every CTA) and scores (one CTA per position) ----
         float st;
@@ -279,7 +277,7 @@ __global__ void __launch_bounds__(PK_T, 1) k_greedy1(PkArgs a) {
             }
             __syncthreads();
         }
-        gsync(a.ctl);
+        gsync(a.ctl, gs_epoch);
         PK_STAMP(3);
         // ---- P4: softmax (every CTA, fp64, sequential sum) and context features ----
         {
@@ -327,7 +325,7 @@ __global__ void __launch_bounds__(PK_T, 1) k_greedy1(PkArgs a) {
             }
         }
         prefetch_rows(a.w3x, LX, 2 * H, gw, nw);
-        gsync(a.ctl);
+        gsync(a.ctl, gs_epoch);
         PK_STAMP(4);
         // ---- P5: q(ctx); GEMV [W_x3; W_c] ----
         #pragma unroll 4   // independent iterations: their L2 loads in flight together
@@ -336,7 +334,7 @@ __global__ void __launch_bounds__(PK_T, 1) k_greedy1(PkArgs a) {
         const float sctx = quantize_vec(vals, 2 * H, q, red, a.err);
         gemv(a.w3x, LX, 2 * H, a.w3x_s, 1, q, sctx, a.b3x, a.gxq, 0, gw, nw);
         prefetch_rows(a.uc3, H, H, gw, nw);
-        gsync(a.ctl);
+        gsync(a.ctl, gs_epoch);
         PK_STAMP(5);
         // ---- P6: gates of dec_q (h = s') -> q(r * s'); GEMV U_c3 ----
         bad = false;
@@ -352,7 +350,7 @@ __global__ void __launch_bounds__(PK_T, 1) k_greedy1(PkArgs a) {
         const float srh3 = quantize_vec(vals, H, q, red, a.err);
         gemv(a.uc3, H, H, a.uc3_s, H, q, srh3, nullptr, a.ghc, 0, gw, nw);
         prefetch_rows(a.w_state, R, H, gw, nw);
-        gsync(a.ctl);
+        gsync(a.ctl, gs_epoch);
         PK_STAMP(6);
         // ---- P7: combine of dec_q -> s_new (next state), q(s_new); GEMV W_s + b_r ----
         #pragma unroll 4   // independent iterations: their L2 loads in flight together
@@ -369,7 +367,7 @@ __global__ void __launch_bounds__(PK_T, 1) k_greedy1(PkArgs a) {
         const float ssn = quantize_vec(vals, H, q, red, a.err);
         gemv(a.w_state, R, H, a.w_state_s, R, q, ssn, a.b_r, a.ro, 0, gw, nw);
         prefetch_rows(a.w_vocab, V, R, gw, nw);
-        gsync(a.ctl);
+        gsync(a.ctl, gs_epoch);
         PK_STAMP(7);
         // ---- P8: readout tanh -> q; vocabulary GEMV (logits) ----
         #pragma unroll 4   // independent iterations: their L2 loads in flight together
@@ -416,7 +414,7 @@ __global__ void __launch_bounds__(PK_T, 1) k_greedy1(PkArgs a) {
         }
         prefetch_rows(a.w2x, LX, E, gw, nw);   // the next step's P0 (after P10 / P11, no barrier between)
         prefetch_rows(a.uzr2, 2 * H, H, gw, nw);
-        gsync(a.ctl);
+        gsync(a.ctl, gs_epoch);
         PK_STAMP(9);
         // ---- P10: lse (every CTA, same order); smallest token with the best log-prob ----
         // (thread c reads partial c; block tree reductions in a fixed order: every CTA gets the
@@ -546,6 +544,7 @@ int greedy1_launch(const PkArgs& a, cudaStream_t st) {
 // kernels (k_gru_gates / k_gru_combine, per-(sentence, direction) scales).
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(PK_T, 1) k_enc1(PeArgs a) {
+    unsigned gs_epoch = 0;   // grid-barrier target (gsync)
     extern __shared__ __align__(16) unsigned char pe_smem[];
     const int H = a.H;
     float* h = reinterpret_cast<float*>(pe_smem);   // [2][H]
@@ -566,7 +565,7 @@ __global__ void __launch_bounds__(PK_T, 1) k_enc1(PeArgs a) {
 #pragma unroll
         for (int d = 0; d < 2; ++d)
             gemv(a.uzr[d], 2 * H, H, a.uzr_s[d], H, q + d * H, sh[d], nullptr, a.gh + d * 2 * H, 0, gw, nw);
-        gsync(a.ctl);
+        gsync(a.ctl, gs_epoch);
         // S2: gates -> q(r * h_d) -> U_c_d
         float srh[2];
 #pragma unroll
@@ -588,7 +587,7 @@ __global__ void __launch_bounds__(PK_T, 1) k_enc1(PeArgs a) {
 #pragma unroll
         for (int d = 0; d < 2; ++d)
             gemv(a.uc[d], H, H, a.uc_s[d], H, q + d * H, srh[d], nullptr, a.ghc + d * H, 0, gw, nw);
-        gsync(a.ctl);
+        gsync(a.ctl, gs_epoch);
         // S3: combine; the new states stay in this CTA's shared memory
 #pragma unroll
         for (int d = 0; d < 2; ++d) {

@@ -350,13 +350,17 @@ def translate_batch(models, sentences, cfg: DecodeConfig, max_batch: int = 256, 
     sentence-by-sentence ``translate`` on any device count."""
     _check_cfg(cfg)
     members = _members(models, cfg.precision)
-    sents = [s.split() if isinstance(s, str) else list(s) for s in sentences]
+    if return_ids:   # id arrays pass through untouched (no per-token Python objects on the bulk path)
+        sents = [s if isinstance(s, np.ndarray) and s.ndim == 1 else np.asarray(list(s), dtype=np.int64)
+                 for s in sentences]
+    else:
+        sents = [s.split() if isinstance(s, str) else list(s) for s in sentences]
     if not sents:
         return []
     if any(len(s) == 0 for s in sents):
         raise EmptyInputError("cannot translate an empty sentence")
     if return_ids:
-        ids = [[np.asarray(s, dtype=np.int64) for s in sents]] * len(members)
+        ids = [sents] * len(members)
     else:
         ids = [[m.src_ids(s) for s in sents] for m in members]
     tgt = members[0].tgt_tokens

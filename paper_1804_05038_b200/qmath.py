@@ -223,6 +223,13 @@ def gemm_f32(a, b):
     return Y.contiguous().cpu().numpy() if _dev.is_numpy(a) or _dev.is_numpy(b) else Y
 
 
+def gemm_f32_blocked(a, b):
+    """The reference's cache-blocked schedule (qmath.py:462-474) exists to show that
+    blocking buys nothing on narrow panels; it equals :func:`gemm_f32` up to
+    reassociation.  The device has one fp64-evaluated schedule, so this is that call."""
+    return gemm_f32(a, b)
+
+
 def qgemm(a: QuantizedMatrix, b: QuantizedMatrix):
     """Quantized product with exact integer accumulation, emitted as float32.
 
