@@ -326,6 +326,107 @@ k_att_score4(const float* __restrict__ u, int64_t ldu, const int32_t* __restrict
     }
 }
 
+// Attention dims beyond the register-resident kernels (A > AT * AKA = 2048): the same
+// arithmetic with the a-loop strided over the CTA instead of unrolled into registers.
+// k_att_scale_wide: per-hypothesis scale and thresholds, exactly as k_att_scale.
+__global__ void __launch_bounds__(AT)
+k_att_scale_wide(const float* __restrict__ u, int64_t ldu, const int32_t* __restrict__ sent_col_off,
+                 const int32_t* __restrict__ sent_ncols, const float* __restrict__ mm, int64_t A,
+                 float4* __restrict__ st_thr, int32_t* err_flag, uint32_t* zero_seg) {
+    pdl_entry();
+    __shared__ uint32_t mred[AT / 32];
+    const int s = blockIdx.x, j = blockIdx.y;
+    if (zero_seg && j == 0 && threadIdx.x == 0) zero_seg[s] = 0u;
+    if (j >= sent_ncols[s]) return;
+    const int c = sent_col_off[s] + j;
+    const float* un = u + (int64_t)c * ldu;
+    const float* mx = mm + ((int64_t)s * 2) * A;
+    const float* mn = mx + A;
+    uint32_t m = 0;
+    for (int64_t a = threadIdx.x; a < A; a += AT) {
+        const float uv = un[a];
+        m = max(m, __float_as_uint(__fadd_rn(mx[a], uv)) & 0x7fffffffu);
+        m = max(m, __float_as_uint(__fadd_rn(mn[a], uv)) & 0x7fffffffu);
+    }
+    m = warp_max(m);
+    if ((threadIdx.x & 31) == 0) mred[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 0; w < AT / 32; ++w) m = max(m, mred[w]);
+        if (m >= 0x7f800000u) {
+            set_flag(err_flag, QNMT_FLAG_NUMERIC);
+            m = 0;
+        }
+        const float tmax = tanh_b(__uint_as_float(m));
+        const float st = (tmax == 0.0f) ? 1.0f : __fdiv_rn(127.0f, tmax);
+        st_thr[c] = make_float4(st, att_threshold(st), att_e_threshold(st), 0.0f);
+    }
+}
+
+// k_att_score_wide: scores for APC positions x all P hypotheses of one sentence, any A.
+// Per element the two-MUFU fast path of k_att_score4 with the exact code taken at once
+// for an element inside the rounding window (the same codes as every other scorer).
+__global__ void __launch_bounds__(AT)
+k_att_score_wide(const float* __restrict__ u, int64_t ldu, const int32_t* __restrict__ sent_col_off,
+                 const int32_t* __restrict__ sent_ncols, const float* __restrict__ att_proj,
+                 const float4* __restrict__ st_thr, const int64_t* __restrict__ sent_row,
+                 const int32_t* __restrict__ sent_len, int64_t A, const int8_t* __restrict__ v_codes,
+                 const float* __restrict__ v_scale, float* __restrict__ scores, int32_t max_len) {
+    pdl_entry();
+    __shared__ long long red[APC][AT / 32];
+    const int s = blockIdx.y;
+    const int P = sent_ncols[s];
+    const int l = sent_len[s];
+    const int i0 = blockIdx.x * APC;
+    if (P == 0 || i0 >= l) return;
+    const int np = min(l - i0, APC);
+    const int c0 = sent_col_off[s];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const float* ap = att_proj + (sent_row[s] + i0) * A;
+    for (int j = 0; j < P; ++j) {
+        const float* un = u + (int64_t)(c0 + j) * ldu;
+        const float4 sp = st_thr[c0 + j];
+        const float st = sp.x, thr = sp.y, m2st = -2.0f * st;
+        const bool fast = st <= ATT_ST_FAST_MAX;
+        long long acc[APC] = {};
+        for (int64_t a = threadIdx.x; a < A; a += AT) {
+            const int vk = (int)v_codes[a];
+            const float uv = un[a];
+            if (vk == 0) continue;
+#pragma unroll
+            for (int p = 0; p < APC; ++p) {
+                if (p >= np) break;
+                const float x = __fadd_rn(ap[(int64_t)p * A + a], uv);
+                int code;
+                if (fast) {
+                    const float r = rcp_approx(__fadd_rn(ex2_approx(__fmul_rn(x, 2.8853900817779268f)), 1.0f));
+                    const float v = fmaf(m2st, r, st);
+                    const float mg = __fadd_rn(v, 12582912.0f);   // 1.5 * 2^23
+                    code = __float_as_int(mg) - 0x4B400000;
+                    if (fabsf(__fsub_rn(v, __fsub_rn(mg, 12582912.0f))) > thr) code = att_code_exact(x, st);
+                } else {
+                    code = att_code_exact(x, st);
+                }
+                acc[p] += (long long)(vk * code);
+            }
+        }
+        __syncthreads();   // red of the previous hypothesis consumed
+#pragma unroll
+        for (int p = 0; p < APC; ++p) {
+            long long t = acc[p];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+            if (lane == 0) red[p][warp] = t;
+        }
+        __syncthreads();
+        if (threadIdx.x < np) {
+            long long t = 0;
+            for (int w = 0; w < AT / 32; ++w) t += red[threadIdx.x][w];
+            scores[(int64_t)(c0 + j) * max_len + i0 + threadIdx.x] = dequant(t, v_scale[0], st);
+        }
+    }
+}
+
 // Same scores with each thread's slice of the tile parked in shared memory
 // (APC5 positions x its a-quads; a thread only ever reads its own slots, so no
 // barrier), registers holding just the query slice, codes and accumulators:
@@ -1374,10 +1475,7 @@ int attention_launch(const float* u, int64_t ldu, int64_t N, const int32_t* sent
                      float* alpha, int64_t lda, void* scratch, int32_t* err_flag, cudaStream_t st,
                      uint32_t* ctx_segmax, int max_p, const float* att_exp) {
     if (N <= 0 || n_sent <= 0) return QNMT_OK;
-    if (A > (int64_t)AT * AKA) {
-        set_error("qnmt_attention: attention dim %lld > %d", (long long)A, AT * AKA);
-        return QNMT_ERR_SHAPE;
-    }
+    const bool wide = A > (int64_t)AT * AKA;   // beyond the register-resident kernels: strided a-loops
     // scratch: scores [N][max_len] | st_thr [N] float4 | (column extrema [n_sent][2][A]) | (E_u [N][A])
     float* scores = reinterpret_cast<float*>(scratch);
     float4* st_thr = reinterpret_cast<float4*>(scores + ((N * max_len + 63) / 64) * 64);
@@ -1388,7 +1486,7 @@ int attention_launch(const float* u, int64_t ldu, int64_t N, const int32_t* sent
         TRY_LAUNCH(att_minmax_launch(att_proj, sent_row, sent_len, n_sent, A, mm, st));
         att_minmax = mm;
     }
-    const bool quads = A % 4 == 0 && ldu % 4 == 0 && A <= 4 * AT * AQ5 && ((uintptr_t)u % 16) == 0 &&
+    const bool quads = !wide && A % 4 == 0 && ldu % 4 == 0 && A <= 4 * AT * AQ5 && ((uintptr_t)u % 16) == 0 &&
                        ((uintptr_t)att_proj % 16) == 0 && ((uintptr_t)v_codes % 4) == 0;
     const bool expm = quads && att_exp != nullptr && g_att_exp && ((uintptr_t)att_exp % 16) == 0;
     const bool fused_scale = quads && !expm && g_att_fused_scale && ((uintptr_t)att_minmax % 16) == 0;
@@ -1402,6 +1500,14 @@ int attention_launch(const float* u, int64_t ldu, int64_t N, const int32_t* sent
         dim3 g5((unsigned)cdiv(max_len, APC5), (unsigned)n_sent);
         QNMT_LAUNCH(k_att_score5f, g5, AT, smem5, st, ga, att_minmax, err_flag, ctx_segmax);
         QNMT_CHECK_LAUNCH("k_att_score5f");
+    } else if (wide) {
+        QNMT_LAUNCH(k_att_scale_wide, dim3((unsigned)n_sent, AMAXP), AT, 0, st, u, ldu, sent_col_off, sent_ncols,
+                    att_minmax, A, st_thr, err_flag, ctx_segmax);
+        QNMT_CHECK_LAUNCH("k_att_scale_wide");
+        dim3 gw((unsigned)cdiv(max_len, APC), (unsigned)n_sent);
+        QNMT_LAUNCH(k_att_score_wide, gw, AT, 0, st, u, ldu, sent_col_off, sent_ncols, att_proj, st_thr, sent_row,
+                    sent_len, A, v_codes, v_scale, scores, max_len);
+        QNMT_CHECK_LAUNCH("k_att_score_wide");
     } else {
     QNMT_LAUNCH(k_att_scale, dim3((unsigned)n_sent, AMAXP), AT, 0, st, u, ldu, sent_col_off, sent_ncols, att_minmax, A,
                 st_thr, err_flag, ctx_segmax, eu);

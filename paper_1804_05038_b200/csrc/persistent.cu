@@ -35,7 +35,10 @@
 
 namespace qnmt {
 
-constexpr int PK_T = 256;              // threads per CTA (8 warps)
+#ifndef QNMT_PK_T
+#define QNMT_PK_T 256
+#endif
+constexpr int PK_T = QNMT_PK_T;        // threads per CTA (8 warps)
 constexpr int PK_W = PK_T / 32;
 constexpr int PK_MAXD = 2048;          // longest vector quantized per CTA (2H, A <= 2048)
 

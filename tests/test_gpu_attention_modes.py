@@ -105,3 +105,34 @@ def test_scorer_variants_identical(case):
         assert np.array_equal(alpha, ref_alpha), (mode, len(bad), bad[:6].tolist(),
                                                   [(float(alpha[tuple(b)]), float(ref_alpha[tuple(b)])) for b in bad[:3]])
         assert np.array_equal(ctx, ref_ctx), mode
+
+
+@pytest.mark.parametrize("A", [2052, 2304, 4096])
+def test_attention_dims_beyond_2048_match_the_oracle(A):
+    """Attention dims past the register-resident scorers (A > 2048) take the strided
+    kernels (k_att_scale_wide / k_att_score_wide): attend, a teacher-free beam decode and a
+    batch decode are bit-identical to the oracle."""
+    from oracle import qnmt_oracle as O
+    d = pb.Dims(64, 61, 16, 32, A, 16)
+    params = pb.synthetic_model(d, 21, weight_std=0.3, bias_std=0.1, eos_bias=0.5)
+    qm = pb.quantize_model(params)
+    om = O.QModel(O.Dims(**d.as_dict()), params.tensors)
+    net = pb.build_network(qm)
+    src = [5, 9, 17, 33, 40, 8, 2, 11]
+    enc = net.encode(src)
+    rng = np.random.default_rng(A)
+    for P, scale in ((1, 1.0), (5, 1.0), (16, 1.0), (3, 1e-5), (4, 30.0)):
+        h = (rng.normal(0, 0.5, (d.hidden, P)) * scale).astype(np.float32)
+        att_proj = (enc.att_proj * np.float32(scale)).astype(np.float32)
+        ctx, alpha = pb.attend(net.attention, h, pb.EncoderStates(enc.states, att_proj, enc.s0))
+        ctx_o, alpha_o = om.attend(h, enc.states, att_proj)
+        assert np.array_equal(alpha, alpha_o), (P, scale)
+        assert np.array_equal(ctx, ctx_o), (P, scale)
+    srcs = [src, [3, 4], list(range(10, 31))]
+    got = pb.translate_batch(qm, srcs, pb.DecodeConfig(beam=3, max_ratio=2.0, precision="int8"), return_ids=True)
+    for sr, g in zip(srcs, got):
+        want = om.translate(sr, beam=3, max_ratio=2.0)
+        assert g[0] == want[0] and g[1] == want[1], (sr, g, want)
+    one = pb.translate_batch(qm, [src], pb.DecodeConfig(beam=1, max_ratio=1.5, precision="int8"), return_ids=True)[0]
+    want = om.translate(src, beam=1, max_ratio=1.5)
+    assert one[0] == want[0] and one[1] == want[1]
