@@ -225,6 +225,17 @@ int qnmt_set_att_score8(int32_t enable);
  * workspace; 0 (default, measured faster at cfg1 B=64): never split (A/B
  * testing; results identical).  Returns the previous value. */
 int qnmt_set_tc_split(int enable);
+/* 1: in batched decode steps (more than 8 columns) the GRU gate
+ * nonlinearities run in the tcgen05 GEMM epilogues -- z = sigmoid(W_z x + U_z h)
+ * and r*h on the accumulators of the cell's input GEMM, h' = (1-z) h + z tanh(..)
+ * on those of the candidate GEMM (layers.py:170-181) -- with the per-sentence
+ * max |.| for the next quantization reduced there too; 0 (default, measured
+ * faster on the cfg5 decode): the separate fused elementwise + quantize kernels.
+ * Results are identical.  Returns the old value. */
+int qnmt_set_gate_epi(int enable);
+/* Tile widths (64..256, multiple of 32; 0 = the general rule) of the two GRU-epilogue
+ * GEMMs (tuning knob; results identical).  Returns the old gates width. */
+int qnmt_set_gru_epi_bn(int gates_bn, int combine_bn);
 int qnmt_attention(const float* u, int64_t ldu, int64_t N, const int32_t* sent_col_off,
                    const int32_t* sent_ncols, int32_t n_sent,
                    const float* att_proj, const float* att_minmax, const float* att_exp,

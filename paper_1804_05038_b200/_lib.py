@@ -70,6 +70,8 @@ SIGNATURES = {
     "qnmt_kernel_launches": (I64, []),
     "qnmt_set_gemm_impl": (I32, [I32]),
     "qnmt_set_tc_pair": (I32, [I32]),
+    "qnmt_set_gate_epi": (I32, [I32]),
+    "qnmt_set_gru_epi_bn": (I32, [I32, I32]),
     "qnmt_set_greedy1": (I32, [I32]),
     "qnmt_set_topk_exact": (I32, [I32]),
     "qnmt_set_vocab_fused": (I32, [I32]),

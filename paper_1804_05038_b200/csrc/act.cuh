@@ -53,7 +53,7 @@ __device__ __forceinline__ double expm1_f64(double t) {
     int k;
     const double r = exp_reduce(t, k);
     const double q = expm1_core(r);
-    if (k == 0) return q;
+    // branch-free: for k == 0, s = 1 and fma(1, q, 0) = q exactly (q is never -0: r = -0 gives +0)
     const double s = scale2k(1.0, k);
     return fma(s, q, s - 1.0);
 }
@@ -80,7 +80,8 @@ __device__ __forceinline__ float tanh_b(float x) {
 __device__ __forceinline__ float sigmoid_b(float x) {
     const double v = (double)x;
     const double t = -fabs(v);
-    const double e = t < -700.0 ? 0.0 : exp_f64(t);   // below: f32 result 0 either way
+    const double ex = exp_f64(t < -700.0 ? -700.0 : t);   // (branch-free: clamp, then select; NaN stays NaN)
+    const double e = t < -700.0 ? 0.0 : ex;           // below: f32 result 0 either way
     const double d = 1.0 + e;
     return __double2float_rn(div12(v >= 0.0 ? 1.0 : e, d));
 }

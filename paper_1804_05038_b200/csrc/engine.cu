@@ -168,6 +168,8 @@ struct qnmt_engine {
     void* att_scratch;
     float* att_mm;           // [S][2][A] per-sentence column max / min of att_proj
     uint32_t* ctx_max;       // [S] max |ctx| bits per sentence (attention context -> its quantization)
+    uint32_t* gmax = nullptr; // [4][S] max |r*h| / |h'| bits per sentence of the two decoder cells (GRU epilogues)
+    bool gate_epi = false;   // GRU gates / combine run in the tcgen05 GEMM epilogues (gemm.cuh GruEpi)
     bool fq_ok = false;      // per-sentence fused op + quantize kernels fit in shared memory (fused_q.cu)
     // Stacked weights (copied at engine creation) for GEMMs that share an input:
     //   w2x = [cell2 W_x; W_e] x q(emb), w3x = [cell3 W_x; W_c] x q(ctx): the readout terms
@@ -295,8 +297,9 @@ static cudaError_t h2d(qnmt_engine* e, void* dst, const void* src, size_t bytes,
 static int gemm(const int8_t* W, int64_t M, int64_t K, const float* ws, int64_t rps, const int8_t* X,
                 int64_t N, int64_t ldx, const float* xs, const int32_t* seg, const float* bias, float* Y,
                 int64_t ldy, int32_t flags, cudaStream_t st, const float* add1 = nullptr, int64_t ld1 = 0,
-                const float* add2 = nullptr, int64_t ld2 = 0) {
+                const float* add2 = nullptr, int64_t ld2 = 0, const GruEpi* gru = nullptr) {
     GemmArgs g{W, M, K, K, ws, rps, X, N, ldx, xs, seg, bias, Y, ldy, nullptr, flags | QNMT_GEMM_W_STATIC};
+    if (gru) g.gru = *gru;
     g.add1 = add1;
     g.ld1 = ld1;
     g.add2 = add2;
@@ -518,6 +521,14 @@ static int stamp(qnmt_engine* e, int slot, const StepIO& io, cudaStream_t st, in
 // otherwise elementwise kernels followed by the two-pass quantization.
 // Optional stacking (see qnmt_engine::w2x): xs = {W, per-row scales, bias, rows, out, ld} replaces the
 // cell's own W_x GEMM; gh_pre (ld ldgh_pre) is a U_zr product already computed by a stacked GEMM.
+// GRU gates / combine in the tcgen05 epilogues (qnmt_set_gate_epi; QNMT_GATE_EPI=0/1 for A/B runs).
+// Off by default: measured slower than the separate fused kernels on the cfg5 decode (the fp64
+// sigmoid / tanh chains run on the 8 epilogue warps of a CTA that owns its SM; K3g).
+int g_gate_epi = [] {
+    const char* v = getenv("QNMT_GATE_EPI");
+    return v ? atoi(v) != 0 : 0;
+}();
+
 struct XSide {
     const int8_t* w;
     const float* ws;
@@ -530,8 +541,12 @@ struct XSide {
 static int gru_cell(qnmt_engine* e, const Cell& c, const StepIO& io, const int8_t* qx, const float* sx,
                     const int8_t* qh, const float* sh, const float* h, float* h_out, int8_t* q_out, float* sc_out,
                     cudaStream_t st, const XSide* xs = nullptr, const float* gh_pre = nullptr,
-                    int64_t ldgh_pre = 0) {
+                    int64_t ldgh_pre = 0, int cell_slot = 0) {
     const int64_t H = e->m->H, N = io.N;
+    // GRU elementwise phases inside the tcgen05 epilogues (N > 8: those GEMMs take the tcgen05 path)
+    const bool ge = e->gate_epi && g_gate_epi && g_gemm_impl != 1 && N > 8;
+    uint32_t* mx_rh = e->gmax + (size_t)(2 * cell_slot) * e->S;
+    uint32_t* mx_h = e->gmax + (size_t)(2 * cell_slot + 1) * e->S;
     const int32_t* seg = io.col_sent;
     const int ns = io.nseg;
     float* gx = xs ? xs->out : e->gx;
@@ -539,6 +554,30 @@ static int gru_cell(qnmt_engine* e, const Cell& c, const StepIO& io, const int8_
     const float* gh = gh_pre ? gh_pre : e->gh;
     const int64_t ldgh = gh_pre ? ldgh_pre : 2 * H;
     prof_mark(e, PG_GEMM, st, 2.0 * N * (3 * H * c.in + 2 * H * H), 3.0 * H * c.in + 2.0 * H * H);
+    if (ge) {
+        // U_zr h first; the W_x GEMM's epilogue then computes z and r*h from both products
+        if (!gh_pre) TRY(gemm(c.uzr, 2 * H, H, c.uzr_s, H, qh, N, H, sh, seg, nullptr, e->gh, 2 * H, 0, st));
+        GruEpi ga;
+        ga.mode = 1; ga.H = H; ga.g = gh; ga.ldg = ldgh; ga.h = h; ga.ldh = H; ga.z = e->z; ga.out = e->rh;
+        ga.ldo = H; ga.segmax = mx_rh; ga.err_flag = e->err;
+        if (xs)
+            TRY(gemm(xs->w, xs->rows, c.in, xs->ws, 1, qx, N, c.in, sx, seg, xs->b, gx, ldgx, 0, st, nullptr, 0,
+                     nullptr, 0, &ga));
+        else
+            TRY(gemm(c.wx, 3 * H, c.in, c.wx_s, H, qx, N, c.in, sx, seg, c.bx, gx, ldgx, 0, st, nullptr, 0, nullptr,
+                     0, &ga));
+        prof_mark(e, PG_QUANT, st);
+        TRY(quantize_encode_launch(e->rh, N, H, H, seg, e->q_rh, H, e->sc_rh, mx_rh, 1, e->err, st));
+        prof_mark(e, PG_GEMM, st, 2.0 * N * H * H, (double)H * H);
+        GruEpi gc;
+        gc.mode = 2; gc.H = H; gc.g = gx + 2 * H; gc.ldg = ldgx; gc.h = h; gc.ldh = H; gc.z = e->z; gc.out = h_out;
+        gc.ldo = H; gc.segmax = mx_h; gc.err_flag = e->err;
+        TRY(gemm(c.uc, H, H, c.uc_s, H, e->q_rh, N, H, e->sc_rh, seg, nullptr, nullptr, H, 0, st, nullptr, 0, nullptr,
+                 0, &gc));
+        prof_mark(e, PG_QUANT, st);
+        TRY(quantize_encode_launch(h_out, N, H, H, seg, q_out, H, sc_out, mx_h, 1, e->err, st));
+        return QNMT_OK;
+    }
     if (xs)
         TRY(gemm(xs->w, xs->rows, c.in, xs->ws, 1, qx, N, c.in, sx, seg, xs->b, gx, ldgx, 0, st));
     else
@@ -661,7 +700,7 @@ static int step_core(qnmt_engine* e, const StepIO& io, cudaStream_t st) {
     prof_mark(e, PG_EMBED, st);
     if (fq) {
         TRY(embed_q_launch(m->tgt_embed, V, E, io.y, io.sent_col_off, io.sent_ncols, ns, io.max_cols, e->q_emb,
-                           e->sc_emb, e->err, st));
+                           e->sc_emb, e->err, st, e->gate_epi ? e->gmax : nullptr, e->S));
     } else {
         TRY(embed_gather_launch(m->tgt_embed, V, E, io.y, N, e->emb, E, e->err, st));
         TRY(quantize_launch(e->emb, N, E, E, seg, ns, e->q_emb, E, e->sc_emb, e->seg_bits, 1, e->err, st));
@@ -676,7 +715,7 @@ static int step_core(qnmt_engine* e, const StepIO& io, cudaStream_t st) {
     int8_t* q_si = m->aq == 1 ? e->q_si : e->q_q;
     float* sc_si = m->aq == 1 ? e->sc_si : e->sc_q;
     TRY(gru_cell(e, m->cell[2], io, e->q_emb, e->sc_emb, e->q_s, e->sc_s, io.s, io.s_int, q_si, sc_si, st,
-                 stk ? &xs2 : nullptr));
+                 stk ? &xs2 : nullptr, nullptr, 0, 0));
     prof_mark(e, PG_GEMM, st, 2.0 * N * A * H, (double)A * H);
     const float* u = e->u;
     int64_t ldu = A;
@@ -705,7 +744,7 @@ static int step_core(qnmt_engine* e, const StepIO& io, cudaStream_t st) {
     }
     // s = GRU_q(ctx, s')                                        (layers.py:375)
     TRY(gru_cell(e, m->cell[3], io, e->q_ctx, e->sc_ctx, q_si, sc_si, io.s_int, io.s_new, e->q_sn, e->sc_sn, st,
-                 stk ? &xs3 : nullptr, stk_u ? e->uq + A : nullptr, LU));
+                 stk ? &xs3 : nullptr, stk_u ? e->uq + A : nullptr, LU, 1));
     // readout = tanh(((W_s s + b_r) + W_e emb) + W_c ctx)       (layers.py:255-265)
     prof_mark(e, PG_GEMM, st, 2.0 * N * R * (H + E + 2 * H), (double)R * (H + E + 2 * H));
     if (stk) {   // W_e emb and W_c ctx were computed with the cells' input GEMMs; added in tanh_q below
@@ -945,6 +984,7 @@ int qnmt_engine_create(const qnmt_model* m, int32_t max_sentences, int32_t max_s
         e->att_scratch = a.take<char>(N * (L + 4) * 4 + 2 * S * A * 4 + N * A * 4 + 1024);
         e->att_mm = a.take<float>(2 * S * A);
         e->ctx_max = a.take<uint32_t>(S);
+        e->gmax = a.take<uint32_t>(4 * S);
         e->w2x = a.take<int8_t>((3 * H + R) * E);
         e->w2x_s = a.take<float>(3 * H + R);
         e->b2x = a.take<float>(3 * H + R);
@@ -1045,6 +1085,8 @@ int qnmt_engine_create(const qnmt_model* m, int32_t max_sentences, int32_t max_s
         e->stack_ok = true;
         e->stack_u = m->aq == 0;
     }
+    cudaMemset(e->gmax, 0, 4 * S * sizeof(uint32_t));
+    e->gate_epi = e->fq_ok && H % 32 == 0 && E % 16 == 0 && H % 16 == 0;
     cudaStreamCreateWithFlags(&e->cap_stream, cudaStreamNonBlocking);
     cudaError_t ce = cudaMallocHost(&e->h_pinned, 64);
     if (ce != cudaSuccess) { cudaFree(e->block); delete e; return cuda_status(ce, "cudaMallocHost"); }
@@ -1553,3 +1595,9 @@ int64_t qnmt_last_d2h_bytes(const qnmt_engine* e) { return e ? e->d2h_bytes : 0;
 int64_t qnmt_last_h2d_bytes(const qnmt_engine* e) { return e ? e->h2d_bytes : 0; }
 
 }  // extern "C"
+
+extern "C" int qnmt_set_gate_epi(int enable) {
+    const int old = qnmt::g_gate_epi;
+    qnmt::g_gate_epi = enable ? 1 : 0;
+    return old;
+}

@@ -144,8 +144,10 @@ k_combine_q(const float* __restrict__ gxc, int64_t ldgx, const float* __restrict
 __global__ void __launch_bounds__(FQ_T, 2)
 k_embed_q(const float* __restrict__ table, int64_t rows, int64_t E, const int32_t* __restrict__ ids,
           const int32_t* __restrict__ off, const int32_t* __restrict__ cnt, int8_t* __restrict__ q_out,
-          float* sc_out, int32_t* err_flag, int max_cols) {
+          float* sc_out, int32_t* err_flag, int max_cols, uint32_t* zero4, int zstride) {
     pdl_entry();
+    // first kernel of a decoder step: clear this sentence's four GRU-epilogue maxima (engine.cu gmax)
+    if (zero4 && threadIdx.x < 4) zero4[(size_t)threadIdx.x * zstride + blockIdx.x] = 0u;
     FQ_SEG_PROLOGUE
     uint32_t m = 0;
     const int64_t G = (int64_t)P * E / 4;
@@ -267,12 +269,13 @@ int combine_q_launch(const float* gxc, int64_t ldgx, const float* ghc, int64_t l
 
 int embed_q_launch(const float* table, int64_t rows, int64_t E, const int32_t* ids, const int32_t* off,
                    const int32_t* cnt, int n_seg, int max_cols, int8_t* q_out, float* sc_out, int32_t* err_flag,
-                   cudaStream_t st) {
+                   cudaStream_t st, uint32_t* zero4, int zstride) {
     if (n_seg <= 0) return QNMT_OK;
     const size_t smem = (size_t)max_cols * E * sizeof(float);
     static size_t done = 0;
     FQ_TRY(set_smem((const void*)k_embed_q, smem, done));
-    QNMT_LAUNCH(k_embed_q, (unsigned)n_seg, FQ_T, smem, st, table, rows, E, ids, off, cnt, q_out, sc_out, err_flag, max_cols);
+    QNMT_LAUNCH(k_embed_q, (unsigned)n_seg, FQ_T, smem, st, table, rows, E, ids, off, cnt, q_out, sc_out, err_flag, max_cols,
+                zero4, zstride);
     QNMT_CHECK_LAUNCH("k_embed_q");
     return QNMT_OK;
 }

@@ -4,6 +4,29 @@
 
 namespace qnmt {
 
+// GRU elementwise phases computed in the tcgen05 GEMM epilogue (layers.py:170-181)
+// instead of a separate pass over the products (fused_q.cu k_gates_q / k_combine_q).
+//   mode 1 (gates, on the cell's W_x GEMM with bias): rows m < H: z[n][m] =
+//     sigmoid((dq + b) + g[n][m]); rows H <= m < 2H: out[n][m-H] = sigmoid((dq + b) +
+//     g[n][m]) * h[n][m-H]; rows >= 2H are stored to Y as usual.  g = the U_zr h product.
+//   mode 2 (combine, on the U_c GEMM, M = H): out[n][m] = (1 - z) h + z tanh(g[n][m] + dq),
+//     g = the candidate rows of the W_x product.
+// Both raise segmax[col_seg[n]] to max |out| bits (atomicMax) for the quantization
+// of out that follows (quantize_encode_launch); non-finite pre-activations set err_flag.
+struct GruEpi {
+    int32_t mode = 0;
+    int64_t H = 0;
+    const float* g = nullptr;
+    int64_t ldg = 0;
+    const float* h = nullptr;
+    int64_t ldh = 0;
+    float* z = nullptr;
+    float* out = nullptr;
+    int64_t ldo = 0;
+    uint32_t* segmax = nullptr;
+    int32_t* err_flag = nullptr;
+};
+
 struct GemmArgs {
     const int8_t* W;
     int64_t M, K, ldw;
@@ -23,6 +46,8 @@ struct GemmArgs {
     int64_t ld1 = 0;
     const float* add2 = nullptr;
     int64_t ld2 = 0;
+    // optional GRU epilogue (tcgen05 path only), see GruEpi
+    struct GruEpi gru = {};
 };
 
 int gemm_i8_launch(const GemmArgs& g, cudaStream_t st);

@@ -392,6 +392,10 @@ int gemm_i8_launch(const GemmArgs& g, cudaStream_t st) {
     // (in graph mode only for N <= 2: at beam-size N the tcgen05 tile is faster, measured cfg3 beam 5)
     const bool gemv_ok = g_gemm_impl != 2 && g.N <= (tl_ndev ? 2 : 8) && aligned && g.K <= QNMT_INT32_SAFE_K &&
                          g.K > 0;
+    if (g.gru.mode) {   // GRU elementwise phase in the epilogue: tcgen05 kernels only
+        if (!tc_eligible(g)) { set_error("gemm: the GRU epilogue needs the tcgen05 path"); return QNMT_ERR_CONFIG; }
+        return gemm_tc_launch(g, st);
+    }
     if (g.add1 && !gemv_ok) {
         if (!tc_eligible(g)) { set_error("gemm: epilogue addends need the tcgen05 path"); return QNMT_ERR_CONFIG; }
         return gemm_tc_launch(g, st);

@@ -19,10 +19,12 @@
 //               midpoints) -> +bias -> (+Y) -> coalesced f32 stores of Y[n][m].
 // Tiles are visited n-fastest so consecutive CTAs share the W block in L2.
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <mutex>
 #include <unordered_map>
 
+#include "act.cuh"
 #include "gemm.cuh"
 #include "tc_mainloop.cuh"
 
@@ -49,11 +51,24 @@ struct TcEpi {
     int64_t ld1;
     const float* add2;
     int64_t ld2;
+    GruEpi gru;
 };
 
 // EPI_ADD2: two precomputed f32 terms added in order after the bias (the readout's
 // ((W_s s + b_r) + W_e e) + W_c c with W_e e and W_c c from stacked GEMMs)
-enum { EPI_BIAS = 1, EPI_ACCUMULATE = 2, EPI_RAW = 4, EPI_ADD2 = 8 };
+// EPI_GATES / EPI_COMBINE: the GRU elementwise phases on the accumulators (GruEpi, gemm.cuh)
+enum { EPI_BIAS = 1, EPI_ACCUMULATE = 2, EPI_RAW = 4, EPI_ADD2 = 8, EPI_GATES = 16, EPI_COMBINE = 32 };
+
+// per-column max over the warp's 32 rows of |out| bits -> segmax[col_seg[n]]
+__device__ __forceinline__ void gru_segmax(const TcEpi& e, const uint32_t (&mb)[16], int nbase, int ncols, int lane) {
+    uint32_t mine = 0;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+        const uint32_t r = __reduce_max_sync(0xffffffffu, mb[j]);
+        if (lane == j) mine = r;
+    }
+    if (lane < ncols && mine) atomicMax(e.gru.segmax + (e.col_seg ? e.col_seg[nbase + lane] : 0), mine);
+}
 
 // Epilogue warps (2..9) of one CTA: every tile of the persistent schedule
 // (tile0, tile0 + tstep, ...) -> TMEM accumulator rows m_tile * mb + m_off + [0, 128)
@@ -228,6 +243,21 @@ __device__ __forceinline__ void tc_epilogue(const TcEpi& e, uint32_t tmem_base, 
                 }
                 float* yrow = e.Y + (int64_t)nbase * e.ldy + m;
                 float yv[16], a1v[16], a2v[16];
+                // GRU epilogues: addend g, previous state h and (combine) z of this thread's row
+                float gv[16], hv[16], zv[16];
+                const int64_t gH = e.gru.H;
+                const bool g_row = (EPI & EPI_COMBINE) || ((EPI & EPI_GATES) && m < 2 * gH);   // row gets the GRU op
+                const bool g_rrow = (EPI & EPI_GATES) && m >= gH && m < 2 * gH;               // reset-gate row
+                if (EPI & (EPI_GATES | EPI_COMBINE)) {
+                    const int64_t hm = (EPI & EPI_COMBINE) ? m : m - gH;
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) {
+                        const bool ok = mok && j < ncols;
+                        gv[j] = (ok && g_row) ? e.gru.g[(int64_t)(nbase + j) * e.gru.ldg + m] : 0.0f;
+                        hv[j] = (ok && ((EPI & EPI_COMBINE) || g_rrow)) ? e.gru.h[(int64_t)(nbase + j) * e.gru.ldh + hm] : 0.0f;
+                        if (EPI & EPI_COMBINE) zv[j] = ok ? e.gru.z[(int64_t)(nbase + j) * gH + m] : 0.0f;
+                    }
+                }
                 if (EPI & EPI_ACCUMULATE) {
 #pragma unroll
                     for (int j = 0; j < 16; ++j) yv[j] = (mok && j < ncols) ? yrow[(int64_t)j * e.ldy] : 0.0f;
@@ -267,6 +297,41 @@ __device__ __forceinline__ void tc_epilogue(const TcEpi& e, uint32_t tmem_base, 
                     if (EPI & EPI_ACCUMULATE) y = __fadd_rn(yv[j], y);
                     if (EPI & EPI_ADD2) y = __fadd_rn(__fadd_rn(y, a1v[j]), a2v[j]);
                     yd[j] = y;
+                }
+                if (EPI & (EPI_GATES | EPI_COMBINE)) {
+                    // a warp's 32 rows lie on one side of the H / 2H boundaries (H % 32 == 0, checked by the host)
+                    const bool wg = __any_sync(0xffffffffu, g_row);
+                    if (wg) {
+                        uint32_t mb_[16];
+                        bool bad = false;
+                        float vo[16], sg[16];
+                        // arithmetic first (branch-free, 16 independent fp64 chains), stores after
+#pragma unroll
+                        for (int j = 0; j < 16; ++j) {
+                            const float p = __fadd_rn(gv[j], yd[j]);   // fadd is commutative: (x + h) as fused_q.cu
+                            bad |= mok && j < ncols && g_row && !is_finite_f(p);
+                            if (EPI & EPI_COMBINE) {
+                                vo[j] = __fadd_rn(__fmul_rn(__fsub_rn(1.0f, zv[j]), hv[j]), __fmul_rn(zv[j], tanh_b(p)));
+                            } else {
+                                sg[j] = sigmoid_b(p);
+                                vo[j] = __fmul_rn(sg[j], hv[j]);
+                            }
+                        }
+#pragma unroll
+                        for (int j = 0; j < 16; ++j) {
+                            const bool ok = mok && j < ncols && g_row;
+                            if (EPI & EPI_COMBINE) {
+                                if (ok) e.gru.out[(int64_t)(nbase + j) * e.gru.ldo + m] = vo[j];
+                            } else {
+                                if (ok && !g_rrow) e.gru.z[(int64_t)(nbase + j) * gH + m] = sg[j];
+                                if (ok && g_rrow) e.gru.out[(int64_t)(nbase + j) * e.gru.ldo + (m - gH)] = vo[j];
+                            }
+                            mb_[j] = (ok && ((EPI & EPI_COMBINE) || g_rrow)) ? (__float_as_uint(vo[j]) & 0x7fffffffu) : 0u;
+                        }
+                        if (bad) set_flag(e.gru.err_flag, QNMT_FLAG_NUMERIC);
+                        gru_segmax(e, mb_, nbase, ncols, lane);
+                    }
+                    if ((EPI & EPI_COMBINE) || wg) continue;   // no plain store for GRU rows
                 }
                 if (mok && ncols == 16) {
 #pragma unroll
@@ -635,9 +700,10 @@ static int launch_tc(const GemmArgs& g, cudaStream_t st) {
     rc = tc_get_map(g.X, g.N, g.K, g.ldx, BN, &tb);
     if (rc) return rc;
     TcEpi e{g.w_scales, g.w_rows_per_scale, g.x_scales, g.col_seg, g.bias, g.Y, g.ldy, g.acc_out, g.flags,
-            g.add1, g.ld1, g.add2, g.ld2};
+            g.add1, g.ld1, g.add2, g.ld2, g.gru};
     int tiles = (int)(cdiv(g.M, TC_BM) * cdiv(g.N, BN));
-    TcSplit sk{choose_ksplit(tiles, cdiv(g.K, TC_BK), tc_sm_count()), nullptr, nullptr};
+    TcSplit sk{(EPI & (EPI_GATES | EPI_COMBINE)) ? 1 : choose_ksplit(tiles, cdiv(g.K, TC_BK), tc_sm_count()), nullptr,
+               nullptr};
     if (sk.ksplit > 1 && !split_ws(st, (size_t)g.M * g.N, (size_t)tiles, sk)) sk.ksplit = 1;
     tiles *= sk.ksplit;
     int grid = tiles < tc_sm_count() ? tiles : tc_sm_count();
@@ -648,6 +714,13 @@ static int launch_tc(const GemmArgs& g, cudaStream_t st) {
 }
 
 int g_tc_pair = 1;   // 0: never use the CTA-pair kernel (A/B testing)
+// tile width of the GRU-epilogue GEMMs ([0] gates, [1] combine); 0 = the general rule
+int g_gru_bn[2] = {0, 0};
+static const int g_gru_bn_env = [] {   // QNMT_GRU_BN="gates,combine" (A/B runs)
+    const char* v = getenv("QNMT_GRU_BN");
+    if (v) sscanf(v, "%d,%d", &g_gru_bn[0], &g_gru_bn[1]);
+    return 0;
+}();
 
 template <int EPI>
 static int launch_tc2(const GemmArgs& g, cudaStream_t st) {
@@ -661,7 +734,7 @@ static int launch_tc2(const GemmArgs& g, cudaStream_t st) {
     rc = tc_get_map(g.X, g.N, g.K, g.ldx, BN / 2, &tb);
     if (rc) return rc;
     TcEpi e{g.w_scales, g.w_rows_per_scale, g.x_scales, g.col_seg, g.bias, g.Y, g.ldy, g.acc_out, g.flags,
-            g.add1, g.ld1, g.add2, g.ld2};
+            g.add1, g.ld1, g.add2, g.ld2, GruEpi{}};
     const int tiles = (int)(cdiv(g.M, 2 * TC_BM) * cdiv(g.N, BN));
     const int pairs = tc_sm_count() / 2;
     const int grid = 2 * (tiles < pairs ? tiles : pairs);
@@ -684,9 +757,19 @@ int gemm_tc_launch(const GemmArgs& g, cudaStream_t st) {
     const int64_t mb = cdiv(g.M, TC_BM);
     const int sms = tc_sm_count();
     const int epi = (g.bias ? EPI_BIAS : 0) | ((g.flags & QNMT_GEMM_ACCUMULATE) ? EPI_ACCUMULATE : 0) |
-                    (g.acc_out ? EPI_RAW : 0) | (g.add1 ? EPI_ADD2 : 0);
+                    (g.acc_out ? EPI_RAW : 0) | (g.add1 ? EPI_ADD2 : 0) | (g.gru.mode == 1 ? EPI_GATES : 0) |
+                    (g.gru.mode == 2 ? EPI_COMBINE : 0);
+    if (g.gru.mode) {
+        if (g.gru.H % 32 != 0 || !g.gru.g || !g.gru.h || !g.gru.z || !g.gru.out || !g.gru.segmax ||
+            (g.gru.mode == 1 && (epi != (EPI_BIAS | EPI_GATES) || g.M < 2 * g.gru.H)) ||
+            (g.gru.mode == 2 && (epi != EPI_COMBINE || g.M != g.gru.H))) {
+            set_error("gemm_tc: bad GRU epilogue arguments (mode %d epi %d M %lld H %lld)", g.gru.mode, epi,
+                      (long long)g.M, (long long)g.gru.H);
+            return QNMT_ERR_CONFIG;
+        }
+    }
     // large products (at least two waves of 256 x 256 pair tiles, not graph-captured): CTA pairs
-    if (g_tc_pair && !tl_ndev && !(epi & EPI_ADD2) && g.M >= 2 * TC_BM && g.N >= 256 &&
+    if (g_tc_pair && !tl_ndev && !(epi & (EPI_ADD2 | EPI_GATES | EPI_COMBINE)) && g.M >= 2 * TC_BM && g.N >= 256 &&
         cdiv(g.M, 2 * TC_BM) * cdiv(g.N, 256) >= sms) {
         switch (epi) {
             case 0: return launch_tc2<0>(g, st);
@@ -721,6 +804,7 @@ int gemm_tc_launch(const GemmArgs& g, cudaStream_t st) {
             }
         }
         if (forced) bn = forced;
+        if (g.gru.mode && g_gru_bn[g.gru.mode - 1]) bn = g_gru_bn[g.gru.mode - 1];
     }
 #define QNMT_TC_CASE(BN_, E_) \
     if (bn == BN_ && epi == E_) return launch_tc<BN_, E_>(g, st);
@@ -730,6 +814,9 @@ int gemm_tc_launch(const GemmArgs& g, cudaStream_t st) {
     QNMT_TC_BN4(96) QNMT_TC_BN4(160) QNMT_TC_BN4(192) QNMT_TC_BN4(224)
     QNMT_TC_CASE(64, 9) QNMT_TC_CASE(96, 9) QNMT_TC_CASE(128, 9) QNMT_TC_CASE(160, 9) QNMT_TC_CASE(192, 9)
     QNMT_TC_CASE(224, 9) QNMT_TC_CASE(256, 9)
+#define QNMT_TC_GRU(BN_) QNMT_TC_CASE(BN_, 17) QNMT_TC_CASE(BN_, 32)
+    QNMT_TC_GRU(64) QNMT_TC_GRU(96) QNMT_TC_GRU(128) QNMT_TC_GRU(160) QNMT_TC_GRU(192) QNMT_TC_GRU(224) QNMT_TC_GRU(256)
+#undef QNMT_TC_GRU
 #undef QNMT_TC_BN4
 #undef QNMT_TC_BN8
 #undef QNMT_TC_CASE
@@ -742,6 +829,15 @@ int gemm_tc_launch(const GemmArgs& g, cudaStream_t st) {
 extern "C" int qnmt_set_tc_split(int enable) {
     const int old = qnmt::g_tc_split;
     qnmt::g_tc_split = enable;
+    return old;
+}
+
+// tile widths of the GRU-epilogue GEMMs (0 = general rule); returns the old gates width
+extern "C" int qnmt_set_gru_epi_bn(int gates_bn, int combine_bn) {
+    const int old = qnmt::g_gru_bn[0];
+    auto okbn = [](int b) { return b == 0 || (b >= 64 && b <= 256 && b % 32 == 0); };
+    if (okbn(gates_bn)) qnmt::g_gru_bn[0] = gates_bn;
+    if (okbn(combine_bn)) qnmt::g_gru_bn[1] = combine_bn;
     return old;
 }
 

@@ -91,7 +91,7 @@ int combine_q_launch(const float* gxc, int64_t ldgx, const float* ghc, int64_t l
                      cudaStream_t st);
 int embed_q_launch(const float* table, int64_t rows, int64_t E, const int32_t* ids, const int32_t* off,
                    const int32_t* cnt, int n_seg, int max_cols, int8_t* q_out, float* sc_out, int32_t* err_flag,
-                   cudaStream_t st);
+                   cudaStream_t st, uint32_t* zero4 = nullptr, int zstride = 0);
 int tanh_q_launch(const float* x, int64_t ldx, int64_t D, const int32_t* off, const int32_t* cnt, int n_seg,
                   int max_cols, int8_t* q_out, float* sc_out, int32_t* err_flag, cudaStream_t st,
                   const float* a1 = nullptr, int64_t ld1 = 0, const float* a2 = nullptr, int64_t ld2 = 0);
