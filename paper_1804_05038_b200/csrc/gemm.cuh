@@ -62,4 +62,8 @@ int quantize_launch(const float* x, int64_t ncols, int64_t K, int64_t ldx, const
                     int32_t nseg, int8_t* q, int64_t ldq, float* scales, uint32_t* seg_maxbits,
                     int32_t mode, int32_t* err_flag, cudaStream_t st);
 
+bool quantize_small_eligible(const float* x, int64_t ncols, int64_t K, int64_t ldx, const int8_t* q, int64_t ldq);
+int quantize_small_launch(const float* x, int64_t ncols, int64_t K, int8_t* q, float* scale_out, uint32_t* maxbits_out,
+                          int32_t mode, int32_t* err_flag, cudaStream_t st);
+
 }  // namespace qnmt

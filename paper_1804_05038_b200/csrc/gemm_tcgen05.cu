@@ -357,7 +357,7 @@ __device__ __forceinline__ void tc_epilogue(const TcEpi& e, uint32_t tmem_base, 
 template <int BN, int EPI>
 __global__ void __launch_bounds__(TC_THREADS, 1)
 k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N, int K,
-          TcEpi e, const int32_t* n_dev, TcSplit sk) {
+          TcEpi e, const int32_t* n_dev, TcSplit sk, int pre) {
     using C = TcCfg<BN>;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* smem = (unsigned char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -369,6 +369,8 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
     const int lane = threadIdx.x & 31;
     pdl_trigger();
     const uint32_t tmem_base = tc_setup<C>(&tmA, &tmB, bars, TC_EPI_WARPS);
+    // static weights, host-known N: the first tile's weight blocks stream while the predecessor runs
+    if (pre > 0 && warp == 0 && lane == 0) tc_prefetch_a<C>(&tmA, smem, bars, (N + BN - 1) / BN, pre);
     pdl_wait();   // everything above overlaps the predecessor kernel (PDL)
     if (n_dev) N = min(N, *n_dev);   // graph mode: live columns from the device
     const int m_blocks = (M + TC_BM - 1) / TC_BM;
@@ -378,7 +380,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
     __shared__ int s_last;
 
     if (warp == 0) {
-        tc_produce<C, BN>(&tmA, &tmB, smem, bars, tiles, n_blocks, k_blocks, -1, 0, sk.ksplit);
+        tc_produce<C, BN>(&tmA, &tmB, smem, bars, tiles, n_blocks, k_blocks, -1, 0, sk.ksplit, pre);
     } else if (warp == 1) {
         tc_issue<C, BN>(smem, bars, tmem_base, tiles, k_blocks, -1, 0, sk.ksplit);
     } else {
@@ -689,6 +691,12 @@ static int choose_ksplit(int64_t tiles, int64_t k_blocks, int sms) {
     return (int)cdiv(k_blocks, kpb);
 }
 
+// static weight blocks requested before the PDL wait (QNMT_TC_PREFETCH_W=0 for A/B runs)
+static const int g_tc_prefetch_w = [] {
+    const char* v = getenv("QNMT_TC_PREFETCH_W");
+    return v ? atoi(v) : 1;
+}();
+
 template <int BN, int EPI>
 static int launch_tc(const GemmArgs& g, cudaStream_t st) {
     using C = TcCfg<BN>;
@@ -708,7 +716,12 @@ static int launch_tc(const GemmArgs& g, cudaStream_t st) {
     tiles *= sk.ksplit;
     int grid = tiles < tc_sm_count() ? tiles : tc_sm_count();
     auto kfn = k_gemm_tc<BN, EPI>;
-    QNMT_LAUNCH(kfn, grid, TC_THREADS, C::SMEM, st, ta, tb, (int)g.M, (int)g.N, (int)g.K, e, tl_ndev, sk);
+    // weights flagged static (not written by the predecessor kernel): request the first tile's
+    // A blocks before the PDL wait (not in graph-captured steps: N is device-side there)
+    const int kb_all = (int)cdiv(g.K, TC_BK);
+    const int pre = ((g.flags & QNMT_GEMM_W_STATIC) && !tl_ndev && sk.ksplit == 1 && g_tc_prefetch_w)
+                        ? (kb_all < C::STAGES ? kb_all : C::STAGES) : 0;
+    QNMT_LAUNCH(kfn, grid, TC_THREADS, C::SMEM, st, ta, tb, (int)g.M, (int)g.N, (int)g.K, e, tl_ndev, sk, pre);
     QNMT_CHECK_LAUNCH("k_gemm_tc");
     return QNMT_OK;
 }

@@ -83,10 +83,94 @@ __global__ void k_encode(const float* __restrict__ x, int64_t ncols, int64_t K, 
     }
 }
 
+// ---------------------------------------------------------------------------
+// k_quant_cluster: quantize_activations (qmath.py:157-182) of one small
+// contiguous matrix in ONE launch -- the two-pass scheme above costs a memset
+// and two dependent launches, more than the 0.25 MB of data.  A cluster of 8
+// CTAs: every thread keeps its <= 4 float4 of x in registers, the CTA maxima
+// meet through distributed shared memory, then every thread encodes its own
+// values.  n = ncols * K <= QC_CAP elements, one segment.
+// ---------------------------------------------------------------------------
+constexpr int QC_T = 512, QC_CTAS = 8, QC_R = 4;
+constexpr int64_t QC_CAP = (int64_t)QC_CTAS * QC_T * QC_R * 4;
+
+__global__ void __cluster_dims__(QC_CTAS, 1, 1) __launch_bounds__(QC_T)
+k_quant_cluster(const float* __restrict__ x, int64_t n4, int8_t* __restrict__ q, float* __restrict__ scale_out,
+                uint32_t* maxbits_out, int32_t mode, int32_t* err_flag) {
+    pdl_entry();
+    __shared__ uint32_t red[QC_T / 32];
+    __shared__ uint32_t cta_max;
+    float4 v[QC_R];
+    uint32_t m = 0;
+    const int64_t i0 = (int64_t)blockIdx.x * QC_T + threadIdx.x;
+#pragma unroll
+    for (int r = 0; r < QC_R; ++r) {
+        const int64_t i = i0 + (int64_t)r * QC_CTAS * QC_T;
+        v[r] = i < n4 ? reinterpret_cast<const float4*>(x)[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+        m = max(max(m, max(__float_as_uint(v[r].x) & 0x7fffffffu, __float_as_uint(v[r].y) & 0x7fffffffu)),
+                max(__float_as_uint(v[r].z) & 0x7fffffffu, __float_as_uint(v[r].w) & 0x7fffffffu));
+    }
+    m = warp_max(m);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t mm = 0;
+#pragma unroll
+        for (int w = 0; w < QC_T / 32; ++w) mm = max(mm, red[w]);
+        cta_max = mm;
+    }
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    uint32_t bits = 0;
+    {
+        const uint32_t local = (uint32_t)__cvta_generic_to_shared(&cta_max);
+#pragma unroll
+        for (uint32_t c = 0; c < QC_CTAS; ++c) {
+            uint32_t ra, val;
+            asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(local), "r"(c));
+            asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(val) : "r"(ra) : "memory");
+            bits = max(bits, val);
+        }
+    }
+    // no CTA may exit while a peer still reads its shared memory
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    if (blockIdx.x == 0 && threadIdx.x == 0 && maxbits_out) *maxbits_out = bits;
+    if (bits >= 0x7f800000u) {   // non-finite input: flag, codes of a failed call are zeros (as k_encode)
+        if (threadIdx.x == 0) set_flag(err_flag, mode == 0 ? QNMT_FLAG_INVALID : QNMT_FLAG_NUMERIC);
+        bits = 0;
+    }
+    const float s = scale_from_maxbits(bits);
+    if (blockIdx.x == 0 && threadIdx.x == 0 && scale_out) *scale_out = s;
+#pragma unroll
+    for (int r = 0; r < QC_R; ++r) {
+        const int64_t i = i0 + (int64_t)r * QC_CTAS * QC_T;
+        if (i < n4)
+            reinterpret_cast<uint32_t*>(q)[i] = (uint32_t)(quant_code(v[r].x, s) & 0xff) |
+                                                ((uint32_t)(quant_code(v[r].y, s) & 0xff) << 8) |
+                                                ((uint32_t)(quant_code(v[r].z, s) & 0xff) << 16) |
+                                                ((uint32_t)(quant_code(v[r].w, s) & 0xff) << 24);
+    }
+}
+
+// one-launch quantization of a small contiguous single-segment matrix; false = not eligible
+bool quantize_small_eligible(const float* x, int64_t ncols, int64_t K, int64_t ldx, const int8_t* q, int64_t ldq) {
+    return ldx == K && ldq == K && ncols * K > 0 && (ncols * K) % 4 == 0 && ncols * K <= QC_CAP &&
+           (uintptr_t)x % 16 == 0 && (uintptr_t)q % 4 == 0 && tl_ndev == nullptr;
+}
+
+int quantize_small_launch(const float* x, int64_t ncols, int64_t K, int8_t* q, float* scale_out, uint32_t* maxbits_out,
+                          int32_t mode, int32_t* err_flag, cudaStream_t st) {
+    QNMT_LAUNCH(k_quant_cluster, QC_CTAS, QC_T, 0, st, x, ncols * K / 4, q, scale_out, maxbits_out, mode, err_flag);
+    QNMT_CHECK_LAUNCH("k_quant_cluster");
+    return QNMT_OK;
+}
+
 int quantize_launch(const float* x, int64_t ncols, int64_t K, int64_t ldx, const int32_t* col_seg,
                     int32_t nseg, int8_t* q, int64_t ldq, float* scales, uint32_t* seg_maxbits,
                     int32_t mode, int32_t* err_flag, cudaStream_t st) {
     if (ncols <= 0 || K <= 0) return QNMT_OK;
+    // small single-segment matrices (LinearOp.apply on a batch of columns): one cluster launch
+    if (!col_seg && nseg == 1 && scales && seg_maxbits && quantize_small_eligible(x, ncols, K, ldx, q, ldq))
+        return quantize_small_launch(x, ncols, K, q, scales, seg_maxbits, mode, err_flag, st);
     QNMT_CUDA(cudaMemsetAsync(seg_maxbits, 0, sizeof(uint32_t) * (size_t)nseg, st));
     bool vec4 = (K % 4 == 0) && (ldx % 4 == 0) && (ldq % 4 == 0) &&
                 ((uintptr_t)x % 16 == 0) && ((uintptr_t)q % 4 == 0);

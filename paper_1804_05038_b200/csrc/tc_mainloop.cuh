@@ -84,10 +84,26 @@ __device__ __forceinline__ void tc_krange(int tile, int ksplit, int k_blocks, in
     kb1 = min(k_blocks, kb0 + kpb);
 }
 
+// Static A operand (weights): the A blocks of the CTA's first tile can be requested before the
+// programmatic-dependent-launch wait -- they do not depend on the predecessor kernel, so they
+// stream from HBM while it (e.g. the activation quantization) still runs.  Warp 0 lane 0, after
+// tc_setup; `pre` = min(STAGES, k_blocks) stages, each armed for the full stage (the B block is
+// added by tc_produce(..., pre) after the wait).  Requires ksplit == 1, blockIdx.x < tiles and a
+// host-known n_blocks.
+template <class R>
+__device__ __forceinline__ void tc_prefetch_a(const CUtensorMap* tmA, unsigned char* smem, const TcBars<R>& b,
+                                              int n_blocks, int pre) {
+    const int ab = (int)blockIdx.x / n_blocks;
+    for (int s = 0; s < pre; ++s) {
+        tc::mbar_arrive_expect_tx(&b.full[s], R::STAGE_BYTES);
+        tc::tma_load_2d(smem + s * R::STAGE_BYTES, tmA, &b.full[s], s * TC_BK, ab * TC_BM);
+    }
+}
+
 template <class R, int BN>
 __device__ __forceinline__ void tc_produce(const CUtensorMap* tmA, const CUtensorMap* tmB, unsigned char* smem,
                                            const TcBars<R>& b, int tiles, int n_blocks, int k_blocks,
-                                           int t0 = -1, int tstep = 0, int ksplit = 1) {
+                                           int t0 = -1, int tstep = 0, int ksplit = 1, int pre = 0) {
     if ((threadIdx.x & 31) != 0) return;
     int stage = 0;
     uint32_t phase = 0;
@@ -103,8 +119,10 @@ __device__ __forceinline__ void tc_produce(const CUtensorMap* tmA, const CUtenso
             tc::mbar_wait(&b.empty[stage], phase ^ 1);
             unsigned char* sa = smem + stage * R::STAGE_BYTES;
             unsigned char* sb = sa + R::A_BYTES;
-            tc::mbar_arrive_expect_tx(&b.full[stage], R::STAGE_BYTES);
-            tc::tma_load_2d(sa, tmA, &b.full[stage], kb * TC_BK, ab * TC_BM);
+            if (!(pre > 0 && tile == t0 && kb < pre)) {   // (else armed and A requested by tc_prefetch_a)
+                tc::mbar_arrive_expect_tx(&b.full[stage], R::STAGE_BYTES);
+                tc::tma_load_2d(sa, tmA, &b.full[stage], kb * TC_BK, ab * TC_BM);
+            }
             tc::tma_load_2d(sb, tmB, &b.full[stage], kb * TC_BK, bb * BN);
             if (++stage == R::STAGES) { stage = 0; phase ^= 1; }
         }
