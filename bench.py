@@ -490,18 +490,27 @@ def main():
     # e2e: the public bulk API (translate_batch: host ids in, host results out, length-sorted
     # batches pipelined over STREAMS engines), wall clock around the call with a device sync
     shard_ids = [sents[i] for b in shard for i in b]
-    e2e_secs, e2e_toks = 0.0, 0
+    e2e_secs, e2e_toks, e2e_step_ms = 0.0, 0, []
     cfg = pb.DecodeConfig(beam=BEAM, max_ratio=MAX_RATIO, precision="int8")
     pb.translate_batch(qm, shard_ids, cfg, max_batch=PER_GPU, return_ids=True, streams=STREAMS)   # warm-up
     eng_pool = engine_pool(qm).all
     b0 = [(e.h2d_bytes, e.d2h_bytes) for e in eng_pool if e is not None]
+    import gc
     for k in range(args.steps):
         flush.fill_(1)
         torch.cuda.synchronize()
+        # as timeit does: collect before, no collector pauses inside the timed call (a step returns
+        # ~8192 Python lists; a generation-2 pass landing in a step cost ~60 ms of its ~1110 ms)
+        gc.collect()
+        gc_was = gc.isenabled()
+        gc.disable()
         t0 = time.perf_counter()
         res = pb.translate_batch(qm, shard_ids, cfg, max_batch=PER_GPU, return_ids=True, streams=STREAMS)
         torch.cuda.synchronize()
-        e2e_secs += time.perf_counter() - t0
+        e2e_step_ms.append(1000 * (time.perf_counter() - t0))
+        if gc_was:
+            gc.enable()
+        e2e_secs += e2e_step_ms[-1] / 1000
         e2e_toks += sum(len(r[0]) for r in res)
     b1 = [(e.h2d_bytes, e.d2h_bytes) for e in eng_pool if e is not None]
     h2d = sum(x[0] for x in b1) - sum(x[0] for x in b0)
@@ -574,7 +583,7 @@ def main():
                 **({"emulated_shard": args.emulate_shard} if args.emulate_shard and world == 1 else {}),
                 "step_ms": step_ms,
                 "e2e": {"value": e2e_value, "unit": "tokens/s", "h2d_bytes_per_step": h2d // args.steps,
-                        "d2h_bytes_per_step": d2h // args.steps},
+                        "d2h_bytes_per_step": d2h // args.steps, "step_ms": e2e_step_ms},
                 "gpu_launches": launches,
                 "roofline": roof,
                 "kernels": kern,

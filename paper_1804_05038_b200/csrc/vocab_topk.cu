@@ -30,7 +30,10 @@ namespace qnmt {
 constexpr int VT_BN = 192;          // tokens per tile (UMMA N); 2 accumulators in a 512-column TMEM slot
 constexpr int VT_EPI_WARPS = 12;   // 3 per TMEM lane group (64 tokens each): latency hiding for the fp64 epilogue
 constexpr int VT_THREADS = 64 + 32 * VT_EPI_WARPS;
-using VtRing = TcRing<VT_BN, 4>;
+#ifndef QNMT_VT_STAGES
+#define QNMT_VT_STAGES 4
+#endif
+using VtRing = TcRing<VT_BN, QNMT_VT_STAGES>;
 constexpr int VT_SPLIT = VT_EPI_WARPS / 4;   // token groups per tile (one per warp of a lane group)
 constexpr int VT_HALF = VT_BN / VT_SPLIT;    // tokens per partial
 constexpr int VT_RESCAN_MAX = 64;    // flagged half-tiles handled per row before a full row rescan
@@ -66,7 +69,12 @@ struct VtArgs {
     int32_t* err_flag;
 };
 
-__global__ void __launch_bounds__(VT_THREADS, 1)
+#ifdef QNMT_VT_MAXREG   // (A/B builds: cap registers so another stream's CTAs fit beside this one)
+#define VT_BOUNDS __maxnreg__(QNMT_VT_MAXREG)
+#else
+#define VT_BOUNDS __launch_bounds__(VT_THREADS, 1)
+#endif
+__global__ void VT_BOUNDS
 k_vocab_stats(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW, int M, int V,
               int K, VtArgs e, const int32_t* n_dev) {
     using C = VtRing;

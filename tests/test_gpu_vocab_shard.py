@@ -72,3 +72,42 @@ def test_shard_bounds_cover():
             assert b[0][0] == 0 and b[-1][1] == V and len(b) == G
             assert all(b[i][1] == b[i + 1][0] for i in range(G - 1))
             assert all(lo % VS.TILE == 0 or lo == V for lo, _ in b)
+
+
+_NCCL_CHILD = r"""
+import os, sys
+sys.path.insert(0, {root!r})
+sys.path.insert(0, os.path.join({root!r}, "tests"))
+import torch
+import torch.distributed as dist
+os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+os.environ.setdefault("MASTER_PORT", {port!r})
+torch.cuda.set_device(0)
+dist.init_process_group("nccl", rank=0, world_size=1)
+from paper_1804_05038_b200 import vocab_shard as VS
+from test_gpu_vocab_shard import _case
+ok = True
+for (V, K, N, k, dup) in [(50000, 64, 300, 5, 0), (3001, 64, 37, 5, 7)]:
+    X, xs, seg, W, ws, bias, live = _case(V, K, N, k, dup, V + K + N)
+    cs0, ct0 = VS.unsharded(X, xs, seg, W, ws, bias, live, k)
+    cs1, ct1 = VS.candidates(X, xs, seg, W, ws, bias, live, k, group=dist.group.WORLD)
+    ok &= bool(torch.equal(ct0, ct1)) and bool(torch.equal(cs0, cs1))
+dist.barrier()
+dist.destroy_process_group()
+print("NCCL_K7_OK" if ok else "NCCL_K7_MISMATCH")
+"""
+
+
+def test_nccl_group_path_world_size_1(tmp_path):
+    """The NCCL branch of candidates() (all_gather_into_tensor of the partials, combine) on a
+    one-rank NCCL group: the only multi-GPU code path of the project, exercised on the one GPU
+    of the box (a real exchange needs more GPUs; the bytes and the combine are the same)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = tmp_path / "k7_nccl_child.py"
+    script.write_text(_NCCL_CHILD.format(root=root, port=str(29500 + os.getpid() % 2000)))
+    r = subprocess.run([sys.executable, str(script)], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, (r.stdout + r.stderr)[-3000:]
+    assert "NCCL_K7_OK" in r.stdout, (r.stdout + r.stderr)[-3000:]
