@@ -611,9 +611,248 @@ __global__ void __launch_bounds__(PK_T, 1) k_enc1(PeArgs a) {
         for (int j = threadIdx.x; j < 2 * H; j += PK_T) a.h2[j] = h[j];
 }
 
+// ---------------------------------------------------------------------------
+// k_enc1c: the batch-1 bidirectional recurrence with the recurrent weights
+// RESIDENT IN SHARED MEMORY of one 16-CTA cluster per direction.  U_zr and U_c of
+// one direction are 3 H^2 bytes (3 MB at H = 1024): 16 CTAs x 192 KB hold them,
+// so a position costs two cluster barriers and two all-gathers of H floats
+// through distributed shared memory, instead of two grid-wide barriers over all
+// SMs plus 6 MB of L2 reads per position (k_enc1: ~19 us per position).
+//
+//   CTA r of direction d owns the hidden indices J = [r H/16, (r+1) H/16): the
+//   z rows J and the r rows H + J of U_zr, the rows J of U_c (loaded once),
+//   and a full copy of the state h.
+//   S1  q(h) (every CTA); its 2|J| rows of U_zr q(h); z_J; v_J = r_J * h_J;
+//       v_J stored into every CTA's `vals` (st.shared::cluster); cluster barrier
+//   S2  q(v) (every CTA); its |J| rows of U_c q(v); h'_J = (1-z) h + z tanh(.);
+//       h'_J stored into every CTA's h and the output; cluster barrier
+//
+// Same arithmetic as k_enc1 (quantize_vec, exact integer dots, dequant_rcp ==
+// dequant, fp64 sigmoid / tanh rounded once), so the states are bit-identical.
+// ---------------------------------------------------------------------------
+constexpr int EC_CL = 16;    // CTAs per cluster
+constexpr int EC_T = 512;    // threads per CTA
+constexpr int EC_W = EC_T / 32;
+
+__device__ __forceinline__ void ec_cluster_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t ec_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+// store v at the same shared-memory offset as `local` in every CTA of the cluster
+__device__ __forceinline__ void ec_bcast(float* local, float v) {
+    const uint32_t la = (uint32_t)__cvta_generic_to_shared(local);
+#pragma unroll
+    for (uint32_t c = 0; c < EC_CL; ++c) {
+        uint32_t ra;
+        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(la), "r"(c));
+        asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(ra), "f"(v) : "memory");
+    }
+}
+
+// block max / quantization with EC_T threads (quantize_vec's arithmetic)
+__device__ float ec_quantize(const float* vals, int D, int8_t* q, uint32_t* red, int32_t* err, bool lead) {
+    uint32_t m = 0;
+    for (int j = threadIdx.x; j < D; j += EC_T) m = max(m, __float_as_uint(vals[j]) & 0x7fffffffu);
+    m = warp_max(m);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+    __syncthreads();
+    uint32_t mm = red[0];
+#pragma unroll
+    for (int w = 1; w < EC_W; ++w) mm = max(mm, red[w]);
+    if (mm >= 0x7f800000u) {
+        if (threadIdx.x == 0 && lead) set_flag(err, QNMT_FLAG_NUMERIC);
+        mm = 0;
+    }
+    const float sc = scale_from_maxbits(mm);
+    for (int j = threadIdx.x; j < D; j += EC_T) q[j] = (int8_t)quant_code(vals[j], sc);
+    __syncthreads();
+    return sc;
+}
+
+// rows [0, M) of a shared-memory weight block (row stride K) against q: out[m] =
+// dequant(acc, ws[m / rows_per_scale], sx).  Warp w takes rows w, w + EC_W, ... in groups of 8.
+__device__ __forceinline__ void ec_gemv(const int8_t* W, int M, int K, const float* ws, int rows_per_scale,
+                                        const int8_t* q, float sx, float* out) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int mb = warp * 8; mb < M; mb += EC_W * 8) {
+        int acc[8];
+#pragma unroll
+        for (int r = 0; r < 8; ++r) acc[r] = 0;
+        for (int k = lane * 16; k < K; k += 512) {
+            const int4 b = *reinterpret_cast<const int4*>(q + k);
+#pragma unroll
+            for (int r = 0; r < 8; ++r) {
+                const int4 wv = (mb + r < M) ? *reinterpret_cast<const int4*>(W + (size_t)(mb + r) * K + k)
+                                             : make_int4(0, 0, 0, 0);
+                acc[r] = __dp4a(wv.x, b.x, acc[r]);
+                acc[r] = __dp4a(wv.y, b.y, acc[r]);
+                acc[r] = __dp4a(wv.z, b.z, acc[r]);
+                acc[r] = __dp4a(wv.w, b.w, acc[r]);
+            }
+        }
+        int mine = 0;
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+            const int tot = __reduce_add_sync(0xffffffffu, acc[r]);
+            if (lane == r) mine = tot;
+        }
+        const int m = mb + lane;
+        if (lane < 8 && m < M) {
+            const float sw = ws[m / rows_per_scale];
+            out[m] = dequant_rcp(mine, (1.0 / (double)sw) * (1.0 / (double)sx), sw, sx);   // == dequant()
+        }
+    }
+}
+
+__global__ void __launch_bounds__(EC_T, 1) k_enc1c(PeArgs a) {
+    extern __shared__ __align__(16) unsigned char ec_smem[];
+    const int H = a.H, J = H / EC_CL;
+    const int d = blockIdx.x / EC_CL;           // cluster = direction
+    const int r = (int)ec_rank();
+    const int j0 = r * J;
+    int8_t* wzr = reinterpret_cast<int8_t*>(ec_smem);       // [2J][H]: z rows J, then r rows J
+    int8_t* wc = wzr + (size_t)2 * J * H;                   // [J][H]
+    float* h = reinterpret_cast<float*>(wc + (size_t)J * H);   // [H] state (full copy)
+    float* vals = h + H;                                    // [H] r * h (all-gathered)
+    float* gloc = vals + H;                                 // [2J] this CTA's U_zr / U_c products
+    float* zloc = gloc + 2 * J;                             // [J]
+    int8_t* q = reinterpret_cast<int8_t*>(zloc + J);        // [H]
+    __shared__ uint32_t red[EC_W];
+    __shared__ float wsc[3];                                // z, r, c block scales of this direction
+    // resident weights: this CTA's rows (16-byte chunks; H % 16 == 0)
+    {
+        const int cpr = H / 16;   // chunks per row
+        const int4* gz = reinterpret_cast<const int4*>(a.uzr[d] + (size_t)j0 * H);
+        const int4* gr = reinterpret_cast<const int4*>(a.uzr[d] + (size_t)(H + j0) * H);
+        const int4* gc = reinterpret_cast<const int4*>(a.uc[d] + (size_t)j0 * H);
+        int4* sz = reinterpret_cast<int4*>(wzr);
+        int4* sr = reinterpret_cast<int4*>(wzr + (size_t)J * H);
+        int4* sc = reinterpret_cast<int4*>(wc);
+        for (int i = threadIdx.x; i < J * cpr; i += EC_T) {
+            sz[i] = __ldg(gz + i);
+            sr[i] = __ldg(gr + i);
+            sc[i] = __ldg(gc + i);
+        }
+        if (threadIdx.x == 0) {
+            wsc[0] = a.uzr_s[d][0];
+            wsc[1] = a.uzr_s[d][1];
+            wsc[2] = a.uc_s[d][0];
+        }
+    }
+    for (int j = threadIdx.x; j < H; j += EC_T) h[j] = 0.0f;   // layers.py:330
+    __syncthreads();
+    ec_cluster_sync();   // every CTA's buffers exist before any remote store
+    for (int t = 0; t < a.l; ++t) {
+        const int pos = d == 0 ? t : a.l - 1 - t;
+        const float* gx = a.gx + ((int64_t)pos * 2 + d) * 3 * H;
+        // this position's input-side terms: requested first, consumed after the products (the L2
+        // round trip overlaps the quantization and the dot products)
+        float gx_z = 0.0f, gx_r = 0.0f, gx_c = 0.0f;
+        if (threadIdx.x < J) {
+            gx_z = gx[j0 + threadIdx.x];
+            gx_r = gx[H + j0 + threadIdx.x];
+            gx_c = gx[2 * H + j0 + threadIdx.x];
+        }
+        // S1: q(h), this CTA's rows of U_zr, gates of its indices
+        const float sh = ec_quantize(h, H, q, red, a.err, r == 0);
+        ec_gemv(wzr, 2 * J, H, wsc, J, q, sh, gloc);   // rows [0, J): z scale, [J, 2J): r scale
+        __syncthreads();
+        if (threadIdx.x < J) {
+            const int j = j0 + threadIdx.x;
+            const float pz = __fadd_rn(gx_z, gloc[threadIdx.x]);
+            const float pr = __fadd_rn(gx_r, gloc[J + threadIdx.x]);
+            if (!(is_finite_f(pz) && is_finite_f(pr))) set_flag(a.err, QNMT_FLAG_NUMERIC);
+            zloc[threadIdx.x] = sigmoid_b(pz);
+            ec_bcast(vals + j, __fmul_rn(sigmoid_b(pr), h[j]));
+        }
+        ec_cluster_sync();   // vals complete in every CTA
+        // S2: q(r * h), this CTA's rows of U_c, new state of its indices
+        const float srh = ec_quantize(vals, H, q, red, a.err, r == 0);
+        ec_gemv(wc, J, H, wsc + 2, J, q, srh, gloc);
+        __syncthreads();
+        if (threadIdx.x < J) {
+            const int j = j0 + threadIdx.x;
+            const float pc = __fadd_rn(gx_c, gloc[threadIdx.x]);
+            if (!is_finite_f(pc)) set_flag(a.err, QNMT_FLAG_NUMERIC);
+            const float z = zloc[threadIdx.x];
+            const float v = __fadd_rn(__fmul_rn(__fsub_rn(1.0f, z), h[j]), __fmul_rn(z, tanh_b(pc)));
+            a.states[(int64_t)pos * 2 * H + (d == 0 ? H : 0) + j] = v;
+            ec_bcast(h + j, v);   // peers read only their own slice of h after the S1 barrier
+        }
+        ec_cluster_sync();   // h complete in every CTA
+    }
+    if (threadIdx.x < J) a.h2[d * H + j0 + threadIdx.x] = h[j0 + threadIdx.x];
+}
+
+static size_t enc1c_smem(int H) {
+    const size_t J = (size_t)H / EC_CL;
+    return 3 * J * H + sizeof(float) * (2 * (size_t)H + 3 * J) + (size_t)H + 64;
+}
+
+// launches k_enc1c when the shape fits and two 16-CTA clusters can be resident; false = not used
+static bool enc1c_try(const PeArgs& a, cudaStream_t st, int& rc) {
+    rc = QNMT_OK;
+    static const int enabled = [] {
+        const char* v = getenv("QNMT_ENC1C");
+        return v ? atoi(v) : 1;
+    }();
+    const int H = a.H;
+    if (!enabled || H % 64 != 0 || H / EC_CL > EC_T) return false;   // J = H/16 rows per CTA, 16-byte aligned buffers
+    const size_t smem = enc1c_smem(H);
+    if (smem > 227 * 1024) return false;
+    static int ready = 0;   // 0 unknown, 1 usable, -1 not usable
+    static size_t smem_set = 0;
+    if (ready < 0) return false;
+    if (cudaFuncSetAttribute((const void*)k_enc1c, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess ||
+        (smem > smem_set &&
+         cudaFuncSetAttribute((const void*)k_enc1c, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+             cudaSuccess)) {
+        cudaGetLastError();
+        ready = -1;
+        return false;
+    }
+    smem_set = smem > smem_set ? smem : smem_set;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(2 * EC_CL);
+    cfg.blockDim = dim3(EC_T);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = EC_CL;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (ready == 0) {
+        int ncl = 0;
+        if (cudaOccupancyMaxActiveClusters(&ncl, (const void*)k_enc1c, &cfg) != cudaSuccess || ncl < 2) {
+            cudaGetLastError();
+            ready = -1;
+            return false;
+        }
+        ready = 1;
+    }
+    const cudaError_t le = cudaLaunchKernelEx(&cfg, k_enc1c, a);
+    if (le != cudaSuccess) {
+        rc = cuda_status(le, "k_enc1c");
+        return true;
+    }
+    count_launch();
+    return true;
+}
+
 int g_enc1 = 1;
 
 int enc1_launch(const PeArgs& a, cudaStream_t st) {
+    {   // preferred: weights resident in the shared memory of one cluster per direction
+        int rc;
+        if (enc1c_try(a, st, rc)) return rc;
+    }
     const size_t smem = (size_t)a.H * (2 + 2 + 1) * sizeof(float) + 2 * (size_t)a.H;
     if (smem > 48 * 1024) {
         static size_t done = 0;

@@ -351,3 +351,30 @@ def test_gpu_persistent_encoder_matches_batched_encoder():
         ost, oatt, os0 = om.encode(src)
         assert np.array_equal(st1.t().cpu().numpy(), ost) and np.array_equal(att1.t().cpu().numpy(), oatt)
         assert np.array_equal(s01.t().cpu().numpy(), os0)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("hidden", [64, 128, 192, 320])
+def test_gpu_cluster_resident_encoder_matches_batched_encoder_and_oracle(hidden):
+    """Hidden sizes that are a multiple of 64 take k_enc1c (persistent.cu): the recurrent weights
+    resident in the shared memory of one 16-CTA cluster per direction, two cluster barriers and
+    two distributed-shared-memory all-gathers per position.  States, att_proj and s0 of
+    one-sentence encodes == the batched encoder's (per-step kernels) == the oracle, for lengths
+    1 .. 64; the BASELINE-dims cfg2 golden (H = 1024) goes through the same kernel."""
+    import paper_1804_05038_b200 as pb
+    d = pb.Dims(300, 251, 32, hidden, 64, 32)
+    params = pb.synthetic_model(d, 90 + hidden, 0.2, 0.1, 0.6)
+    qm = pb.quantize_model(params)
+    om = O.QModel(O.Dims(**d.as_dict()), params.tensors)
+    eng = pb.Engine(qm, 8, 64, 4)
+    rng = np.random.default_rng(hidden)
+    sents = [rng.integers(3, 300, n).tolist() for n in (1, 2, 5, 31, 64)]
+    st_b, att_b, s0_b, rows, lens = eng.encode_batch(sents)
+    for k, src in enumerate(sents):
+        st1, att1, s01, _, _ = eng.encode_batch([src])
+        r0, l = int(rows[k]), len(src)
+        assert torch.equal(st1, st_b[r0:r0 + l]) and torch.equal(att1, att_b[r0:r0 + l])
+        assert torch.equal(s01[0], s0_b[k])
+        ost, oatt, os0 = om.encode(src)
+        assert np.array_equal(st1.t().cpu().numpy(), ost) and np.array_equal(att1.t().cpu().numpy(), oatt)
+        assert np.array_equal(s01.t().cpu().numpy(), os0)
