@@ -631,7 +631,10 @@ __global__ void __launch_bounds__(PK_T, 1) k_enc1(PeArgs a) {
 // dequant, fp64 sigmoid / tanh rounded once), so the states are bit-identical.
 // ---------------------------------------------------------------------------
 constexpr int EC_CL = 16;    // CTAs per cluster
-constexpr int EC_T = 512;    // threads per CTA
+#ifndef QNMT_EC_T
+#define QNMT_EC_T 512
+#endif
+constexpr int EC_T = QNMT_EC_T;    // threads per CTA
 constexpr int EC_W = EC_T / 32;
 
 __device__ __forceinline__ void ec_cluster_sync() {
@@ -751,23 +754,23 @@ __global__ void __launch_bounds__(EC_T, 1) k_enc1c(PeArgs a) {
         const float* gx = a.gx + ((int64_t)pos * 2 + d) * 3 * H;
         // this position's input-side terms: requested first, consumed after the products (the L2
         // round trip overlaps the quantization and the dot products)
-        float gx_z = 0.0f, gx_r = 0.0f, gx_c = 0.0f;
-        if (threadIdx.x < J) {
-            gx_z = gx[j0 + threadIdx.x];
-            gx_r = gx[H + j0 + threadIdx.x];
-            gx_c = gx[2 * H + j0 + threadIdx.x];
-        }
+        float gx_zr = 0.0f, gx_c = 0.0f;
+        if (threadIdx.x < 2 * J) gx_zr = threadIdx.x < J ? gx[j0 + threadIdx.x] : gx[H + j0 + threadIdx.x - J];
+        if (threadIdx.x < J) gx_c = gx[2 * H + j0 + threadIdx.x];
         // S1: q(h), this CTA's rows of U_zr, gates of its indices
         const float sh = ec_quantize(h, H, q, red, a.err, r == 0);
         ec_gemv(wzr, 2 * J, H, wsc, J, q, sh, gloc);   // rows [0, J): z scale, [J, 2J): r scale
         __syncthreads();
-        if (threadIdx.x < J) {
-            const int j = j0 + threadIdx.x;
-            const float pz = __fadd_rn(gx_z, gloc[threadIdx.x]);
-            const float pr = __fadd_rn(gx_r, gloc[J + threadIdx.x]);
-            if (!(is_finite_f(pz) && is_finite_f(pr))) set_flag(a.err, QNMT_FLAG_NUMERIC);
-            zloc[threadIdx.x] = sigmoid_b(pz);
-            ec_bcast(vals + j, __fmul_rn(sigmoid_b(pr), h[j]));
+        if (threadIdx.x < 2 * J) {   // one fp64 sigmoid chain per thread: z by threads [0, J), r by [J, 2J)
+            const bool is_r = threadIdx.x >= J;
+            const int jj = is_r ? threadIdx.x - J : threadIdx.x;
+            const float p = __fadd_rn(gx_zr, gloc[threadIdx.x]);
+            if (!is_finite_f(p)) set_flag(a.err, QNMT_FLAG_NUMERIC);
+            const float sg = sigmoid_b(p);
+            if (is_r)
+                ec_bcast(vals + j0 + jj, __fmul_rn(sg, h[j0 + jj]));
+            else
+                zloc[jj] = sg;
         }
         ec_cluster_sync();   // vals complete in every CTA
         // S2: q(r * h), this CTA's rows of U_c, new state of its indices
@@ -801,7 +804,7 @@ static bool enc1c_try(const PeArgs& a, cudaStream_t st, int& rc) {
         return v ? atoi(v) : 1;
     }();
     const int H = a.H;
-    if (!enabled || H % 64 != 0 || H / EC_CL > EC_T) return false;   // J = H/16 rows per CTA, 16-byte aligned buffers
+    if (!enabled || H % 64 != 0 || 2 * (H / EC_CL) > EC_T) return false;   // J = H/16 rows per CTA, 16-byte aligned buffers
     const size_t smem = enc1c_smem(H);
     if (smem > 227 * 1024) return false;
     static int ready = 0;   // 0 unknown, 1 usable, -1 not usable
