@@ -307,6 +307,18 @@ static int gemm(const int8_t* W, int64_t M, int64_t K, const float* ws, int64_t 
     return gemm_i8_launch(g, st);
 }
 
+// the two directions' products of an encoder step (same shape): one launch when the tcgen05
+// path takes them, else one after the other
+static int gemm_pair(const int8_t* W0, const float* ws0, const int8_t* W1, const float* ws1, int64_t M, int64_t K,
+                     int64_t rps, const int8_t* X0, const int8_t* X1, int64_t N, int64_t ldx, const float* xs,
+                     const int32_t* seg0, const int32_t* seg1, float* Y0, float* Y1, int64_t ldy, cudaStream_t st) {
+    GemmArgs g0{W0, M, K, K, ws0, rps, X0, N, ldx, xs, seg0, nullptr, Y0, ldy, nullptr, QNMT_GEMM_W_STATIC};
+    GemmArgs g1{W1, M, K, K, ws1, rps, X1, N, ldx, xs, seg1, nullptr, Y1, ldy, nullptr, QNMT_GEMM_W_STATIC};
+    if (g_gemm_impl != 1 && (N > 8 || tl_ndev) && gemm_tc_dual_eligible(g0, g1)) return gemm_tc_dual_launch(g0, g1, st);
+    const int rc = gemm_i8_launch(g0, st);
+    return rc != QNMT_OK ? rc : gemm_i8_launch(g1, st);
+}
+
 static int encode_core_f32(qnmt_engine* e, const int32_t* ids_dev, const int32_t* len, int n, int Lmax, int64_t P,
                            const std::vector<int>& perm, float* states, float* att_proj, float* s0,
                            cudaStream_t st);
@@ -395,19 +407,13 @@ static int encode_core(qnmt_engine* e, const int32_t* ids_dev, const int32_t* le
         uint32_t* qm_rh = qm_h + 2 * n;
         uint32_t* qm_hn = qm_h + 4 * n;
         TRY(quantize_encode_launch(e->h2, N2, H, H, e->iota, e->q_h2, H, e->sc_h2, qm_h, 1, e->err, st));
-        for (int d = 0; d < 2; ++d) {
-            const Cell& c = m->cell[d];
-            TRY(gemm(c.uzr, 2 * H, H, c.uzr_s, H, e->q_h2 + d * H, na, 2 * H, e->sc_h2,
-                     d ? e->odd : e->even, nullptr, e->gh2 + d * 2 * H, 4 * H, 0, st));
-        }
+        TRY(gemm_pair(m->cell[0].uzr, m->cell[0].uzr_s, m->cell[1].uzr, m->cell[1].uzr_s, 2 * H, H, H, e->q_h2,
+                      e->q_h2 + H, na, 2 * H, e->sc_h2, e->even, e->odd, e->gh2, e->gh2 + 2 * H, 4 * H, st));
         TRY(gru_gates_launch(e->gx_enc, 3 * H, gxr, e->gh2, 2 * H, e->h2, H, N2, H, e->z2, e->rh2, e->err, st,
                              qm_rh, nullptr));
         TRY(quantize_encode_launch(e->rh2, N2, H, H, e->iota, e->q_rh2, H, e->sc_rh2, qm_rh, 1, e->err, st));
-        for (int d = 0; d < 2; ++d) {
-            const Cell& c = m->cell[d];
-            TRY(gemm(c.uc, H, H, c.uc_s, H, e->q_rh2 + d * H, na, 2 * H, e->sc_rh2, d ? e->odd : e->even,
-                     nullptr, e->ghc2 + d * H, 2 * H, 0, st));
-        }
+        TRY(gemm_pair(m->cell[0].uc, m->cell[0].uc_s, m->cell[1].uc, m->cell[1].uc_s, H, H, H, e->q_rh2,
+                      e->q_rh2 + H, na, 2 * H, e->sc_rh2, e->even, e->odd, e->ghc2, e->ghc2 + H, 2 * H, st));
         TRY(gru_combine_launch(e->gx_enc, 3 * H, gxr, e->ghc2, H, e->z2, e->h2, H, N2, H, e->h2, H,
                                states, H, outr, e->err, st, qm_hn, nullptr));
     }

@@ -53,6 +53,9 @@ struct GemmArgs {
 int gemm_i8_launch(const GemmArgs& g, cudaStream_t st);
 bool tc_eligible(const GemmArgs& g);
 int gemm_tc_launch(const GemmArgs& g, cudaStream_t st);
+// two plain products of one shape in one launch (k_gemm_tc_dual)
+bool gemm_tc_dual_eligible(const GemmArgs& g0, const GemmArgs& g1);
+int gemm_tc_dual_launch(const GemmArgs& g0, const GemmArgs& g1, cudaStream_t st);
 // size the stream's split-K workspace before graph capture ([N][M] int32 + tile counters)
 int tc_split_reserve(cudaStream_t st, int64_t ws_elems, int64_t tiles);
 extern int g_tc_split;

@@ -394,6 +394,55 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
     }
 }
 
+
+// ---------------------------------------------------------------------------
+// Two products of one shape in ONE launch (the encoder's per-direction U_zr h and
+// U_c (r*h): same M, N, K, different weights / activations / outputs).  At decode
+// sizes a tcgen05 product is ~8 us of prologue, pipeline fill and epilogue for
+// well under 1 us of MMA; the two directions' CTAs run side by side instead
+// of back to back.  CTAs [0, per) take product 0, [per, 2 per) product 1, each
+// with k_gemm_tc's persistent tile loop over its own product.
+// ---------------------------------------------------------------------------
+template <int BN, int EPI>
+__global__ void __launch_bounds__(TC_THREADS, 1)
+k_gemm_tc_dual(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__ CUtensorMap tmB0,
+               const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ CUtensorMap tmB1, int M, int N, int K,
+               const __grid_constant__ TcEpi e0, const __grid_constant__ TcEpi e1, const int32_t* n_dev, int per) {
+    using C = TcCfg<BN>;
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char* smem = (unsigned char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    const TcBars<C> bars(smem);
+    __shared__ float col_sx[2][256];
+    __shared__ double col_isx[2][256];
+    const int warp = threadIdx.x >> 5;
+    const bool second = (int)blockIdx.x >= per;
+    const int local = (int)blockIdx.x - (second ? per : 0);
+    const CUtensorMap* tmA = second ? &tmA1 : &tmA0;
+    const CUtensorMap* tmB = second ? &tmB1 : &tmB0;
+    const TcEpi& e = second ? e1 : e0;
+    pdl_trigger();
+    const uint32_t tmem_base = tc_setup<C>(tmA, tmB, bars, TC_EPI_WARPS);
+    pdl_wait();
+    if (n_dev) N = min(N, *n_dev);
+    const int m_blocks = (M + TC_BM - 1) / TC_BM;
+    const int n_blocks = (N + BN - 1) / BN;
+    const int tiles = m_blocks * n_blocks;
+    const int k_blocks = (K + TC_BK - 1) / TC_BK;
+    if (warp == 0) {
+        tc_produce<C, BN>(tmA, tmB, smem, bars, tiles, n_blocks, k_blocks, local, per);
+    } else if (warp == 1) {
+        tc_issue<C, BN>(smem, bars, tmem_base, tiles, k_blocks, local, per);
+    } else {
+        tc_epilogue<BN, EPI>(e, tmem_base, bars.tfull, bars.tempty, 0u, local, per, tiles, n_blocks, TC_BM, 0, M, N,
+                             col_sx, col_isx);
+    }
+    __syncthreads();
+    if (warp == 1) {
+        tc::tc_fence_after();
+        tc::tmem_dealloc<C::TMEM_COLS>(tmem_base);
+    }
+}
+
 // ---------------------------------------------------------------------------
 // CTA-pair variant for large products (tcgen05.mma.cta_group::2, M = 256).
 // A cluster of two CTAs on one TPC computes a 256 x BN tile: CTA r loads A rows
@@ -758,6 +807,68 @@ static int launch_tc2(const GemmArgs& g, cudaStream_t st) {
     QNMT_LAUNCH(k_gemm_tc2<BN, EPI>, grid, TC_THREADS, C::SMEM, st, ta, tb, (int)g.M, (int)g.N, (int)g.K, e, group_m);
     QNMT_CHECK_LAUNCH("k_gemm_tc2");
     return QNMT_OK;
+}
+
+
+template <int BN>
+static int launch_tc_dual(const GemmArgs& g0, const GemmArgs& g1, cudaStream_t st) {
+    using C = TcCfg<BN>;
+    static size_t attr_done = 0;
+    QNMT_CUDA(raise_smem_limit((const void*)k_gemm_tc_dual<BN, 0>, C::SMEM, attr_done));
+    CUtensorMap ta0, tb0, ta1, tb1;
+    int rc = tc_get_map(g0.W, g0.M, g0.K, g0.ldw, TC_BM, &ta0);
+    if (!rc) rc = tc_get_map(g0.X, g0.N, g0.K, g0.ldx, BN, &tb0);
+    if (!rc) rc = tc_get_map(g1.W, g1.M, g1.K, g1.ldw, TC_BM, &ta1);
+    if (!rc) rc = tc_get_map(g1.X, g1.N, g1.K, g1.ldx, BN, &tb1);
+    if (rc) return rc;
+    const TcEpi e0{g0.w_scales, g0.w_rows_per_scale, g0.x_scales, g0.col_seg, g0.bias, g0.Y, g0.ldy, nullptr, g0.flags,
+                   nullptr, 0, nullptr, 0, GruEpi{}};
+    const TcEpi e1{g1.w_scales, g1.w_rows_per_scale, g1.x_scales, g1.col_seg, g1.bias, g1.Y, g1.ldy, nullptr, g1.flags,
+                   nullptr, 0, nullptr, 0, GruEpi{}};
+    const int tiles = (int)(cdiv(g0.M, TC_BM) * cdiv(g0.N, BN));
+    const int half = tc_sm_count() / 2;
+    const int per = tiles < half ? tiles : half;
+    auto kfn = k_gemm_tc_dual<BN, 0>;
+    QNMT_LAUNCH(kfn, 2 * per, TC_THREADS, C::SMEM, st, ta0, tb0, ta1, tb1, (int)g0.M, (int)g0.N, (int)g0.K, e0, e1,
+                tl_ndev, per);
+    QNMT_CHECK_LAUNCH("k_gemm_tc_dual");
+    return QNMT_OK;
+}
+
+// two plain products (no bias / accumulate / addends) of one shape in one launch; false = not eligible
+bool gemm_tc_dual_eligible(const GemmArgs& g0, const GemmArgs& g1) {
+    static const int enabled = [] {
+        const char* v = getenv("QNMT_TC_DUAL");   // (A/B runs)
+        return v ? atoi(v) : 1;
+    }();
+    return enabled && g0.M == g1.M && g0.N == g1.N && g0.K == g1.K && g0.N > 8 && !g0.bias && !g1.bias &&
+           !g0.acc_out && !g1.acc_out && !g0.add1 && !g1.add1 && !g0.gru.mode && !g1.gru.mode &&
+           !(g0.flags & QNMT_GEMM_ACCUMULATE) && !(g1.flags & QNMT_GEMM_ACCUMULATE) && tc_eligible(g0) &&
+           tc_eligible(g1) && g_gemm_impl != 1;
+}
+
+int gemm_tc_dual_launch(const GemmArgs& g0, const GemmArgs& g1, cudaStream_t st) {
+    const int64_t mb = cdiv(g0.M, TC_BM);
+    const int half = tc_sm_count() / 2;
+    static const int cand[] = {64, 96, 128, 160, 192, 224, 256};
+    int bn = 256;
+    int64_t best = INT64_MAX;
+    for (int b : cand) {   // fewest waves over half the SMs, then the narrowest tile
+        const int64_t waves = cdiv(mb * cdiv(g0.N, b), half);
+        if (waves < best) {
+            best = waves;
+            bn = b;
+        }
+    }
+    switch (bn) {
+        case 64: return launch_tc_dual<64>(g0, g1, st);
+        case 96: return launch_tc_dual<96>(g0, g1, st);
+        case 128: return launch_tc_dual<128>(g0, g1, st);
+        case 160: return launch_tc_dual<160>(g0, g1, st);
+        case 192: return launch_tc_dual<192>(g0, g1, st);
+        case 224: return launch_tc_dual<224>(g0, g1, st);
+        default: return launch_tc_dual<256>(g0, g1, st);
+    }
 }
 
 bool tc_eligible(const GemmArgs& g) {
