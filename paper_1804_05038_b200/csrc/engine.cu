@@ -307,6 +307,12 @@ static int gemm(const int8_t* W, int64_t M, int64_t K, const float* ws, int64_t 
     return gemm_i8_launch(g, st);
 }
 
+// encoder steps with the per-column fused phase + quantize kernels (QNMT_ENC_FQ=0 for A/B runs)
+static const int g_enc_fq = [] {
+    const char* v = getenv("QNMT_ENC_FQ");
+    return v ? atoi(v) : 1;
+}();
+
 // the two directions' products of an encoder step (same shape): one launch when the tcgen05
 // path takes them, else one after the other
 static int gemm_pair(const int8_t* W0, const float* ws0, const int8_t* W1, const float* ws1, int64_t M, int64_t K,
@@ -406,6 +412,20 @@ static int encode_core(qnmt_engine* e, const int32_t* ids_dev, const int32_t* le
         uint32_t* qm_h = e->enc_qm + (size_t)t * 4 * n;
         uint32_t* qm_rh = qm_h + 2 * n;
         uint32_t* qm_hn = qm_h + 4 * n;
+        if (e->fq_ok && g_enc_fq) {
+            // one CTA per (sentence, direction) column: GRU phase + the codes the next product reads
+            if (t == 0)   // h = 0: codes 0, scale of a zero segment
+                TRY(quantize_encode_launch(e->h2, N2, H, H, e->iota, e->q_h2, H, e->sc_h2, qm_h, 1, e->err, st));
+            TRY(gemm_pair(m->cell[0].uzr, m->cell[0].uzr_s, m->cell[1].uzr, m->cell[1].uzr_s, 2 * H, H, H, e->q_h2,
+                          e->q_h2 + H, na, 2 * H, e->sc_h2, e->even, e->odd, e->gh2, e->gh2 + 2 * H, 4 * H, st));
+            TRY(enc_gates_q_launch(e->gx_enc, 3 * H, gxr, e->gh2, 2 * H, e->h2, H, N2, H, e->z2, e->q_rh2, e->sc_rh2,
+                                   e->err, st));
+            TRY(gemm_pair(m->cell[0].uc, m->cell[0].uc_s, m->cell[1].uc, m->cell[1].uc_s, H, H, H, e->q_rh2,
+                          e->q_rh2 + H, na, 2 * H, e->sc_rh2, e->even, e->odd, e->ghc2, e->ghc2 + H, 2 * H, st));
+            TRY(enc_combine_q_launch(e->gx_enc, 3 * H, gxr, e->ghc2, H, e->z2, e->h2, H, N2, H, states, H, outr,
+                                     e->q_h2, e->sc_h2, e->err, st));
+            continue;
+        }
         TRY(quantize_encode_launch(e->h2, N2, H, H, e->iota, e->q_h2, H, e->sc_h2, qm_h, 1, e->err, st));
         TRY(gemm_pair(m->cell[0].uzr, m->cell[0].uzr_s, m->cell[1].uzr, m->cell[1].uzr_s, 2 * H, H, H, e->q_h2,
                       e->q_h2 + H, na, 2 * H, e->sc_h2, e->even, e->odd, e->gh2, e->gh2 + 2 * H, 4 * H, st));

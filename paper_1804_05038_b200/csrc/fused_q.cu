@@ -229,6 +229,82 @@ k_gather_q(const float* __restrict__ a, const float* __restrict__ b, const int32
     }
 }
 
+
+// ---------------------------------------------------------------------------
+// Encoder steps (layers.py:331-340, batched over sentences and directions): a
+// quantization segment is ONE column (sentence, direction), so one CTA per
+// column computes the GRU phase, reduces max |v| and writes the codes the next
+// product reads -- instead of the phase kernel, an atomicMax pass and an encode
+// launch.  gx rows go through the per-step row map (position of the column's
+// sentence at this step); combine also scatters the new state to `states`.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(FQ_T, 2)
+k_enc_gates_q(const float* __restrict__ gx, int64_t ldgx, const int32_t* __restrict__ gx_row,
+              const float* __restrict__ gh, int64_t ldgh, const float* __restrict__ h, int64_t ldh, int64_t H,
+              float* __restrict__ z, int8_t* __restrict__ q_rh, float* sc_rh, int32_t* err_flag) {
+    pdl_entry();
+    extern __shared__ float vals[];
+    __shared__ uint32_t red[FQ_T / 32];
+    const int64_t n = blockIdx.x;
+    const float* gxr = gx + (int64_t)gx_row[n] * ldgx;
+    uint32_t m = 0;
+    bool bad = false;
+    for (int64_t g = threadIdx.x; g < H / 4; g += FQ_T) {
+        const int64_t j = 4 * g;
+        const float4 xz = ld4(gxr + j), xr = ld4(gxr + H + j);
+        const float4 hz = ld4(gh + n * ldgh + j), hr = ld4(gh + n * ldgh + H + j);
+        const float4 hh = ld4(h + n * ldh + j);
+        const float4 pz = make_float4(__fadd_rn(xz.x, hz.x), __fadd_rn(xz.y, hz.y), __fadd_rn(xz.z, hz.z),
+                                      __fadd_rn(xz.w, hz.w));
+        const float4 pr = make_float4(__fadd_rn(xr.x, hr.x), __fadd_rn(xr.y, hr.y), __fadd_rn(xr.z, hr.z),
+                                      __fadd_rn(xr.w, hr.w));
+        bad |= !fin4(pz) || !fin4(pr);
+        st4(z + n * H + j, make_float4(sigmoid_b(pz.x), sigmoid_b(pz.y), sigmoid_b(pz.z), sigmoid_b(pz.w)));
+        const float4 v = make_float4(__fmul_rn(sigmoid_b(pr.x), hh.x), __fmul_rn(sigmoid_b(pr.y), hh.y),
+                                     __fmul_rn(sigmoid_b(pr.z), hh.z), __fmul_rn(sigmoid_b(pr.w), hh.w));
+        st4(vals + j, v);
+        m = max4(m, v);
+    }
+    if (bad) set_flag(err_flag, QNMT_FLAG_NUMERIC);
+    const float sc = seg_scale(m, red, err_flag, sc_rh + n);
+    seg_encode(vals, 1, H, (int)n, sc, q_rh, H);
+}
+
+__global__ void __launch_bounds__(FQ_T, 2)
+k_enc_combine_q(const float* __restrict__ gx, int64_t ldgx, const int32_t* __restrict__ gx_row,
+                const float* __restrict__ ghc, int64_t ldghc, const float* __restrict__ z, float* __restrict__ h,
+                int64_t ldh, int64_t H, float* __restrict__ states, int64_t lds, const int32_t* __restrict__ out_row,
+                int8_t* __restrict__ q_h, float* sc_h, int32_t* err_flag) {
+    pdl_entry();
+    extern __shared__ float vals[];
+    __shared__ uint32_t red[FQ_T / 32];
+    const int64_t n = blockIdx.x;
+    const float* gxc = gx + (int64_t)gx_row[n] * ldgx + 2 * H;
+    float* so = states + (int64_t)out_row[n] * lds;
+    uint32_t m = 0;
+    bool bad = false;
+    for (int64_t g = threadIdx.x; g < H / 4; g += FQ_T) {
+        const int64_t j = 4 * g;
+        const float4 xc = ld4(gxc + j), hc = ld4(ghc + n * ldghc + j);
+        const float4 zz = ld4(z + n * H + j), hh = ld4(h + n * ldh + j);
+        const float4 pc = make_float4(__fadd_rn(xc.x, hc.x), __fadd_rn(xc.y, hc.y), __fadd_rn(xc.z, hc.z),
+                                      __fadd_rn(xc.w, hc.w));
+        bad |= !fin4(pc);
+        float4 v;
+        v.x = __fadd_rn(__fmul_rn(__fsub_rn(1.0f, zz.x), hh.x), __fmul_rn(zz.x, tanh_b(pc.x)));
+        v.y = __fadd_rn(__fmul_rn(__fsub_rn(1.0f, zz.y), hh.y), __fmul_rn(zz.y, tanh_b(pc.y)));
+        v.z = __fadd_rn(__fmul_rn(__fsub_rn(1.0f, zz.z), hh.z), __fmul_rn(zz.z, tanh_b(pc.z)));
+        v.w = __fadd_rn(__fmul_rn(__fsub_rn(1.0f, zz.w), hh.w), __fmul_rn(zz.w, tanh_b(pc.w)));
+        st4(h + n * ldh + j, v);   // (this thread read these four before)
+        st4(so + j, v);
+        st4(vals + j, v);
+        m = max4(m, v);
+    }
+    if (bad) set_flag(err_flag, QNMT_FLAG_NUMERIC);
+    const float sc = seg_scale(m, red, err_flag, sc_h + n);
+    seg_encode(vals, 1, H, (int)n, sc, q_h, H);
+}
+
 static int set_smem(const void* fn, size_t bytes, size_t& done) {
     if (bytes > FQ_SMEM_MAX) {
         set_error("fused quantize: %zu bytes of segment values exceed shared memory", bytes);
@@ -264,6 +340,32 @@ int combine_q_launch(const float* gxc, int64_t ldgx, const float* ghc, int64_t l
     QNMT_LAUNCH(k_combine_q, (unsigned)n_seg, FQ_T, smem, st, gxc, ldgx, ghc, ldghc, z, h, ldh, H, off, cnt, h_out, ldo,
                                                       q_out, sc_out, err_flag, max_cols);
     QNMT_CHECK_LAUNCH("k_combine_q");
+    return QNMT_OK;
+}
+
+int enc_gates_q_launch(const float* gx, int64_t ldgx, const int32_t* gx_row, const float* gh, int64_t ldgh,
+                       const float* h, int64_t ldh, int64_t ncols, int64_t H, float* z, int8_t* q_rh, float* sc_rh,
+                       int32_t* err_flag, cudaStream_t st) {
+    if (ncols <= 0) return QNMT_OK;
+    const size_t smem = (size_t)H * sizeof(float);
+    static size_t done = 0;
+    FQ_TRY(set_smem((const void*)k_enc_gates_q, smem, done));
+    QNMT_LAUNCH(k_enc_gates_q, (unsigned)ncols, FQ_T, smem, st, gx, ldgx, gx_row, gh, ldgh, h, ldh, H, z, q_rh, sc_rh,
+                err_flag);
+    QNMT_CHECK_LAUNCH("k_enc_gates_q");
+    return QNMT_OK;
+}
+
+int enc_combine_q_launch(const float* gx, int64_t ldgx, const int32_t* gx_row, const float* ghc, int64_t ldghc,
+                         const float* z, float* h, int64_t ldh, int64_t ncols, int64_t H, float* states, int64_t lds,
+                         const int32_t* out_row, int8_t* q_h, float* sc_h, int32_t* err_flag, cudaStream_t st) {
+    if (ncols <= 0) return QNMT_OK;
+    const size_t smem = (size_t)H * sizeof(float);
+    static size_t done = 0;
+    FQ_TRY(set_smem((const void*)k_enc_combine_q, smem, done));
+    QNMT_LAUNCH(k_enc_combine_q, (unsigned)ncols, FQ_T, smem, st, gx, ldgx, gx_row, ghc, ldghc, z, h, ldh, H, states,
+                lds, out_row, q_h, sc_h, err_flag);
+    QNMT_CHECK_LAUNCH("k_enc_combine_q");
     return QNMT_OK;
 }
 

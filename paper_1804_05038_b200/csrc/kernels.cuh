@@ -89,6 +89,13 @@ int combine_q_launch(const float* gxc, int64_t ldgx, const float* ghc, int64_t l
                      const float* h, int64_t ldh, int64_t H, const int32_t* off, const int32_t* cnt, int n_seg,
                      int max_cols, float* h_out, int64_t ldo, int8_t* q_out, float* sc_out, int32_t* err_flag,
                      cudaStream_t st);
+// encoder steps: one CTA per (sentence, direction) column -- GRU phase + quantization of its output
+int enc_gates_q_launch(const float* gx, int64_t ldgx, const int32_t* gx_row, const float* gh, int64_t ldgh,
+                       const float* h, int64_t ldh, int64_t ncols, int64_t H, float* z, int8_t* q_rh, float* sc_rh,
+                       int32_t* err_flag, cudaStream_t st);
+int enc_combine_q_launch(const float* gx, int64_t ldgx, const int32_t* gx_row, const float* ghc, int64_t ldghc,
+                         const float* z, float* h, int64_t ldh, int64_t ncols, int64_t H, float* states, int64_t lds,
+                         const int32_t* out_row, int8_t* q_h, float* sc_h, int32_t* err_flag, cudaStream_t st);
 int embed_q_launch(const float* table, int64_t rows, int64_t E, const int32_t* ids, const int32_t* off,
                    const int32_t* cnt, int n_seg, int max_cols, int8_t* q_out, float* sc_out, int32_t* err_flag,
                    cudaStream_t st, uint32_t* zero4 = nullptr, int zstride = 0);
