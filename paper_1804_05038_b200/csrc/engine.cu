@@ -307,6 +307,12 @@ static int gemm(const int8_t* W, int64_t M, int64_t K, const float* ws, int64_t 
     return gemm_i8_launch(g, st);
 }
 
+// graph-captured steps: k_search_layout + k_gather_q as one launch (QNMT_LAYOUT_GATHER=0 for A/B runs)
+static const int g_layout_gather = [] {
+    const char* v = getenv("QNMT_LAYOUT_GATHER");
+    return v ? atoi(v) : 1;
+}();
+
 // encoder steps with the per-column fused phase + quantize kernels (QNMT_ENC_FQ=0 for A/B runs)
 static const int g_enc_fq = [] {
     const char* v = getenv("QNMT_ENC_FQ");
@@ -1245,6 +1251,7 @@ static int capture_step(qnmt_engine* e, int cur, int n, int beam, int k_list, cu
     cudaStream_t cs = e->cap_stream;
     QNMT_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeRelaxed));
     int rc = QNMT_OK;
+    bool fused_gather = false;
     {
         NdevScope nd(e->d_N + cur);
         StepIO io{NM, n, e->col_sent[cur], e->y[cur], e->st_s[cur], e->st_sp[cur], e->enc_states, e->enc_att,
@@ -1260,10 +1267,20 @@ static int capture_step(qnmt_engine* e, int cur, int n, int beam, int k_list, cu
                            e->col_sent[cur ^ 1], e->parent_col, e->y[cur ^ 1], e->live[cur ^ 1],
                            e->d_N + (cur ^ 1), e->d_step};
             ss.np_tmp = e->np_tmp;
-            rc = search_step_launch(ss, 0, n, beam, k_list, cs);
+            if (e->fq_ok && g_layout_gather) {   // selection, then layout + state gather in one launch
+                rc = search_select_launch(ss, 0, n, beam, k_list, cs);
+                if (rc == QNMT_OK)
+                    rc = layout_gather_q_launch(ss, n, beam, k_list, e->s_new, m->aq == 1 ? e->s_int : nullptr, H,
+                                                e->st_s[cur ^ 1], e->st_sp[cur ^ 1], e->q_s, e->sc_s,
+                                                m->aq == 1 ? e->q_q : nullptr, m->aq == 1 ? e->sc_q : nullptr, e->err,
+                                                cs);
+                fused_gather = true;
+            } else {
+                rc = search_step_launch(ss, 0, n, beam, k_list, cs);
+            }
         }
     }
-    if (rc == QNMT_OK) {
+    if (rc == QNMT_OK && !fused_gather) {
         NdevScope nd(e->d_N + (cur ^ 1));
         rc = gather_next(e, cur, NM, n, beam, cs);
     }

@@ -15,6 +15,7 @@
 //   k_tanh_q     q(tanh(x))       readout activation   (layers.py:265)
 //   k_gather_q   s, s', q(s), q(s') next-step states by parent column (decoder.py:131-140)
 #include "kernels.cuh"
+#include "search.cuh"
 
 namespace qnmt {
 
@@ -305,6 +306,101 @@ k_enc_combine_q(const float* __restrict__ gx, int64_t ldgx, const int32_t* __res
     seg_encode(vals, 1, H, (int)n, sc, q_h, H);
 }
 
+// ---------------------------------------------------------------------------
+// k_layout_gather_q: k_search_layout (search.cu) + k_gather_q in one launch, one
+// CTA per sentence.  The next step's column offset of sentence s is the sum of
+// the live selections of the sentences before it -- every CTA sums the
+// per-sentence counts itself (<= 1024 ints) instead of waiting for a one-CTA
+// prefix-sum kernel; it then writes the layout of its own columns (sentence,
+// parent column, token, live score) and gathers / quantizes their states by
+// parent.  CTA 0 publishes the live column count and advances the step counter.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(FQ_T, 2)
+k_layout_gather_q(SearchState ss, int step, int n_sent, int k_list, const float* __restrict__ a,
+                  const float* __restrict__ b, int64_t H, float* __restrict__ a_out, float* __restrict__ b_out,
+                  int8_t* __restrict__ qa, float* sca, int8_t* __restrict__ qb, float* scb, int32_t* err_flag,
+                  int max_cols) {
+    pdl_entry();
+    extern __shared__ float vals[];
+    __shared__ uint32_t red[FQ_T / 32];
+    __shared__ int psum[2][FQ_T / 32];
+    __shared__ int s_parent[16];
+    const int s = blockIdx.x;
+    int before = 0, total = 0;
+    for (int i = threadIdx.x; i < n_sent; i += FQ_T) {
+        const int v = ss.np_tmp[i];
+        total += v;
+        before += i < s ? v : 0;
+    }
+    before = __reduce_add_sync(0xffffffffu, before);
+    total = __reduce_add_sync(0xffffffffu, total);
+    if ((threadIdx.x & 31) == 0) {
+        psum[0][threadIdx.x >> 5] = before;
+        psum[1][threadIdx.x >> 5] = total;
+    }
+    __syncthreads();
+    before = total = 0;
+#pragma unroll
+    for (int w = 0; w < FQ_T / 32; ++w) {
+        before += psum[0][w];
+        total += psum[1][w];
+    }
+    const int P = ss.np_tmp[s];
+    const int c0 = before;
+    const int old_off = ss.col_off[s];
+    if (threadIdx.x < P && threadIdx.x < 16) {   // layout of this sentence's next-step columns
+        const int64_t idx = (int64_t)old_off * k_list + threadIdx.x;
+        const int v = ss.cand_tok[idx];
+        const int n = c0 + threadIdx.x;
+        const int pc = old_off + (v >> 26);
+        ss.col_sent_next[n] = s;
+        ss.parent_col[n] = pc;
+        s_parent[threadIdx.x] = pc;
+        ss.y_next[n] = v & ((1 << 26) - 1);
+        ss.live_next[n] = ss.cand_score[idx];
+    }
+    __syncthreads();   // old_off read by every thread; s_parent visible
+    if (threadIdx.x == 0) {
+        ss.P[s] = P;
+        ss.col_off[s] = c0;
+        if (s == 0) {
+            *ss.n_live = total;
+            if (ss.step_dev) *ss.step_dev = *ss.step_dev + 1;
+        }
+    }
+    if (P == 0) return;
+    if (P > max_cols) {
+        if (threadIdx.x == 0) set_flag(err_flag, QNMT_FLAG_INVALID);
+        return;
+    }
+    float* va = vals;                    // [P][H]
+    float* vb = vals + (int64_t)P * H;   // [P][H]
+    uint32_t ma = 0, mb = 0;
+    const int64_t G = (int64_t)P * H / 4;
+#pragma unroll 2
+    for (int64_t g = threadIdx.x; g < G; g += FQ_T) {
+        const int64_t c = (4 * g) / H, j = 4 * g - c * H, n = c0 + c;
+        const int64_t p = s_parent[c];
+        const float4 xa = ld4(a + p * H + j);
+        st4(a_out + n * H + j, xa);
+        st4(va + 4 * g, xa);
+        ma = max4(ma, xa);
+        if (b) {
+            const float4 xb = ld4(b + p * H + j);
+            st4(b_out + n * H + j, xb);
+            st4(vb + 4 * g, xb);
+            mb = max4(mb, xb);
+        }
+    }
+    const float sa = seg_scale(ma, red, err_flag, sca + s);
+    seg_encode(va, P, H, c0, sa, qa, H);
+    if (qb) {
+        __syncthreads();   // red reused
+        const float sb = seg_scale(mb, red, err_flag, scb + s);
+        seg_encode(vb, P, H, c0, sb, qb, H);
+    }
+}
+
 static int set_smem(const void* fn, size_t bytes, size_t& done) {
     if (bytes > FQ_SMEM_MAX) {
         set_error("fused quantize: %zu bytes of segment values exceed shared memory", bytes);
@@ -366,6 +462,23 @@ int enc_combine_q_launch(const float* gx, int64_t ldgx, const int32_t* gx_row, c
     QNMT_LAUNCH(k_enc_combine_q, (unsigned)ncols, FQ_T, smem, st, gx, ldgx, gx_row, ghc, ldghc, z, h, ldh, H, states,
                 lds, out_row, q_h, sc_h, err_flag);
     QNMT_CHECK_LAUNCH("k_enc_combine_q");
+    return QNMT_OK;
+}
+
+int layout_gather_q_launch(const SearchState& ss, int n_sent, int beam, int k_list, const float* a, const float* b,
+                           int64_t H, float* a_out, float* b_out, int8_t* qa, float* sca, int8_t* qb, float* scb,
+                           int32_t* err_flag, cudaStream_t st) {
+    if (n_sent <= 0) return QNMT_OK;
+    if (!ss.np_tmp || !ss.step_dev || beam > 16 || k_list > 16) {
+        set_error("layout_gather_q: needs the graph-mode search state (np_tmp, step_dev), beam <= 16");
+        return QNMT_ERR_CONFIG;
+    }
+    const size_t smem = (size_t)2 * beam * H * sizeof(float);
+    static size_t done = 0;
+    FQ_TRY(set_smem((const void*)k_layout_gather_q, smem, done));
+    QNMT_LAUNCH(k_layout_gather_q, (unsigned)n_sent, FQ_T, smem, st, ss, 0, n_sent, k_list, a, b, H, a_out, b_out, qa,
+                sca, qb, scb, err_flag, beam);
+    QNMT_CHECK_LAUNCH("k_layout_gather_q");
     return QNMT_OK;
 }
 

@@ -357,6 +357,18 @@ int search_step_launch(const SearchState& ss, int step, int n_sent, int beam, in
     return QNMT_OK;
 }
 
+int search_select_launch(const SearchState& ss, int step, int n_sent, int beam, int k_list, cudaStream_t st) {
+    if (n_sent > SEARCH_T || beam > 16 || k_list > 16) {
+        set_error("search: n_sent=%d beam=%d exceed limits (%d, 16)", n_sent, beam, SEARCH_T);
+        return QNMT_ERR_CONFIG;
+    }
+    if (!ss.np_tmp) { set_error("search: no per-sentence scratch"); return QNMT_ERR_CONFIG; }
+    QNMT_LAUNCH(k_search_select, (unsigned)cdiv(n_sent, SEL_WARPS), 32 * SEL_WARPS, 0, st, ss, step, n_sent, beam,
+                k_list);
+    QNMT_CHECK_LAUNCH("k_search_select");
+    return QNMT_OK;
+}
+
 int gather_rows_launch(const float* a, const float* b, const int32_t* parent, int64_t N, int64_t H,
                        float* a_out, float* b_out, cudaStream_t st, uint32_t* a_max, uint32_t* b_max,
                        const int32_t* col_seg) {

@@ -52,6 +52,12 @@ int finalize_launch(const FinalizeArgs& a, int n, cudaStream_t st);
 
 int search_step_launch(const SearchState& ss, int step, int n_sent, int beam, int k_list,
                        cudaStream_t st);
+// the selection alone (k_search_select); the layout then comes from layout_gather_q_launch
+int search_select_launch(const SearchState& ss, int step, int n_sent, int beam, int k_list, cudaStream_t st);
+// k_search_layout + k_gather_q in one launch (graph-captured steps: step counter on the device)
+int layout_gather_q_launch(const SearchState& ss, int n_sent, int beam, int k_list, const float* a, const float* b,
+                           int64_t H, float* a_out, float* b_out, int8_t* qa, float* sca, int8_t* qb, float* scb,
+                           int32_t* err_flag, cudaStream_t st);
 // optional a_max/b_max: per-segment max |a_out| / |b_out| (segment = col_seg[n]) for the next step
 int gather_rows_launch(const float* a, const float* b, const int32_t* parent, int64_t N, int64_t H,
                        float* a_out, float* b_out, cudaStream_t st, uint32_t* a_max = nullptr,
