@@ -393,6 +393,13 @@ __device__ __forceinline__ float vt_logits32(const VtMergeArgs& a, const int8_t*
 
 constexpr int VM_WARPS = 4;   // rows per merge CTA (one warp per row)
 
+#ifdef QNMT_VM_PROF   // (benchmarks/build_variant.sh + benchmarks/vm_prof.py: per-row phase clocks of k_vocab_merge)
+__device__ long long g_vm_prof[8 * 2048];
+#define VM_STAMP(k) do { if (lane == 0 && n < 2048) g_vm_prof[n * 8 + (k)] = clock64(); } while (0)
+#else
+#define VM_STAMP(k) do { } while (0)
+#endif
+
 // (logit desc, token asc) as one descending u64 key: order-preserving f32 bits, then ~token
 __device__ __forceinline__ uint64_t cand_key(float x, int tok) {
     const uint32_t b = __float_as_uint(x);
@@ -435,6 +442,7 @@ k_vocab_merge(VtMergeArgs a, int64_t N, const int32_t* n_dev) {
     if (n >= N || beyond(n_dev, n)) return;   // warp-uniform
     const int np = VT_SPLIT * a.n_blocks;
     VtPart* pr = a.part + n * np;
+    VM_STAMP(0);
     // pass 1: online (max, sum exp), each lane's best (max, token) and largest runner-up
     const int kk = a.V < KM ? a.V : KM;
     Cand* out = lst[wib];
@@ -478,6 +486,7 @@ k_vocab_merge(VtMergeArgs a, int64_t N, const int32_t* n_dev) {
     const double dM = (double)M;
     const double ssum = warp_sum(ml == -FLT_MAX ? 0.0 : sl * exp_neg((double)ml - dM, tab));
     const double lse = log(ssum);
+    VM_STAMP(1);
     // tau = kk-th best of the 32 lane maxima (bitonic sort of (logit, token) keys): at least kk
     // group maxima are >= tau, so every member of the top-kk is too
     const uint64_t tau_key = __shfl_sync(0xffffffffu,
@@ -511,6 +520,7 @@ k_vocab_merge(VtMergeArgs a, int64_t N, const int32_t* n_dev) {
         warp_merge<KM>(L0, out, kk);
     }
     __syncwarp();
+    VM_STAMP(2);
     const Cand tau = key_cand(tau_key);
     Cand L[KM];
     // half-tiles whose runner-up reaches the KM-th value may hold more of the top-KM
@@ -579,6 +589,7 @@ k_vocab_merge(VtMergeArgs a, int64_t N, const int32_t* n_dev) {
         }
         return;
     }
+    VM_STAMP(3);
     const double base = a.live ? a.live[n] : 0.0;
     int ok = 0;
     if (nf <= VT_RESCAN_MAX) {
@@ -606,6 +617,7 @@ k_vocab_merge(VtMergeArgs a, int64_t N, const int32_t* n_dev) {
     // (0 merged, 1 boundary-tie rescan, 2 whole row)
     if (ok) {
         if (lane == 0) pr[0].pad = nf;
+        VM_STAMP(4);
         return;
     }
 #pragma unroll
@@ -661,6 +673,14 @@ k_vocab_merge(VtMergeArgs a, int64_t N, const int32_t* n_dev) {
             a.cand_tok[n * a.k + i] = out[i].t;
         }
 }
+
+#ifdef QNMT_VM_PROF
+}  // namespace qnmt
+extern "C" __attribute__((visibility("default"))) int qnmt_debug_vm_prof(long long* out, int rows) {
+    return (int)cudaMemcpyFromSymbol(out, qnmt::g_vm_prof, sizeof(long long) * 8 * (size_t)rows);
+}
+namespace qnmt {
+#endif
 
 bool vocab_topk_eligible(int64_t K, int64_t ldx, int64_t ldw, const void* X, const void* W, int k) {
     return K % 16 == 0 && K > 0 && K <= QNMT_INT32_SAFE_K && ldx % 16 == 0 && ldw % 16 == 0 &&
