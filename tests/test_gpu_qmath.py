@@ -359,3 +359,38 @@ def test_linear_i8_nonfinite_raises():
     x[5, 0] = np.inf
     with pytest.raises(pb.errors.NumericError):
         pb.LinearOp(wq, None).apply(x)
+
+
+@pytest.mark.parametrize("shape", [(1, 4), (1, 16), (3, 1364), (8, 1024), (63, 1040), (64, 1024), (16, 4096),
+                                   (64, 1028), (65, 1024), (9, 7)])
+def test_cluster_quantize_small_matrices(shape):
+    """One-launch quantization of small single-segment matrices (k_quant_cluster: 8 CTAs, values in
+    registers, maxima through distributed shared memory) and its neighbours just beyond the
+    65536-value capacity / with a length that is not a multiple of 4 (two-pass kernels): codes
+    and scale == the oracle's quantize_activations, incl. all-zero input and a huge dynamic range."""
+    from paper_1804_05038_b200.layers import _quant_k
+    n, K = shape
+    rng = np.random.default_rng(n * 10007 + K)
+    for kind in ("normal", "zero", "range", "tiny"):
+        if kind == "normal":
+            x = rng.normal(0, 1, (n, K)).astype(F32)
+        elif kind == "zero":
+            x = np.zeros((n, K), F32)
+        elif kind == "range":
+            x = (rng.normal(0, 1, (n, K)) * 10.0 ** rng.uniform(-6, 6, (n, K))).astype(F32)
+        else:
+            x = (rng.normal(0, 1, (n, K)) * 1e-30).astype(F32)
+        q, sc = _quant_k(torch.from_numpy(x).cuda())
+        oc, os_ = O.quantize_activations(x.T)
+        assert sc.cpu().numpy()[0] == np.float32(os_), (shape, kind)
+        assert np.array_equal(q.cpu().numpy().T, oc), (shape, kind)
+
+
+def test_cluster_quantize_non_finite_raises():
+    x = np.ones((64, 1024), F32)
+    x[17, 333] = np.inf
+    with pytest.raises(pb.errors.NumericError):
+        pb.quantize_activations(torch.from_numpy(np.ascontiguousarray(x.T)).cuda())
+    x[17, 333] = np.nan
+    with pytest.raises(pb.errors.NumericError):
+        pb.quantize_activations(torch.from_numpy(np.ascontiguousarray(x.T)).cuda())
