@@ -333,6 +333,8 @@ def main():
     ap.add_argument("--no-configs", action="store_true", help="skip the cfg1-cfg4 sub-lines (bench_cfgs.py)")
     ap.add_argument("--no-stamps", action="store_true", help="no device-clock stamps (no roofline)")
     ap.add_argument("--no-profile", action="store_true", help="(kept for compatibility)")
+    ap.add_argument("--batch", type=int, default=0,
+                    help="sentences per engine call (default 256, BASELINE's per-GPU batch; experiments only)")
     ap.add_argument("--emulate-shard", default=None, metavar="R/W",
                     help="development: run rank R's shard of a W-way split on this one GPU (no process "
                          "group; the line reports that rank alone)")
@@ -360,6 +362,9 @@ def main():
     params = pb.synthetic_model(pb.Dims(**DIMS), MODEL_SEED)
     qm = pb.quantize_model(params)
     sents = corpus()
+    if args.batch > 0:
+        global PER_GPU
+        PER_GPU = args.batch
     if args.emulate_shard and world == 1:
         er, ew = (int(x) for x in args.emulate_shard.split("/"))
         shard = shard_batches(sents, er, ew)
