@@ -27,8 +27,14 @@
 
 namespace qnmt {
 
-constexpr int VT_BN = 192;          // tokens per tile (UMMA N); 2 accumulators in a 512-column TMEM slot
-constexpr int VT_EPI_WARPS = 12;   // 3 per TMEM lane group (64 tokens each): latency hiding for the fp64 epilogue
+#ifndef QNMT_VT_BN      // (A/B builds: 256 tokens per tile with 16 epilogue warps)
+#define QNMT_VT_BN 192
+#endif
+#ifndef QNMT_VT_EPI_WARPS
+#define QNMT_VT_EPI_WARPS 12
+#endif
+constexpr int VT_BN = QNMT_VT_BN;          // tokens per tile (UMMA N); 2 accumulators in a 512-column TMEM slot
+constexpr int VT_EPI_WARPS = QNMT_VT_EPI_WARPS;   // 3 per TMEM lane group (64 tokens each): latency hiding for the fp64 epilogue
 constexpr int VT_THREADS = 64 + 32 * VT_EPI_WARPS;
 #ifndef QNMT_VT_STAGES
 #define QNMT_VT_STAGES 4
