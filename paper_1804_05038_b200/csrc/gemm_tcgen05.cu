@@ -34,8 +34,14 @@ constexpr int TC_EPI_WARPS = 8;
 constexpr int TC_THREADS = 64 + 32 * TC_EPI_WARPS;
 
 // ring depth: as many stages as fit ~200 KB of smem, at most 8
+// (QNMT_TC_SMEM_KB: A/B builds with a shallower ring that leaves shared memory to other streams' CTAs)
+#ifndef QNMT_TC_SMEM_KB
+#define QNMT_TC_SMEM_KB 200
+#endif
 template <int BN>
-using TcCfg = TcRing<BN, (200 * 1024 / (TC_BM * TC_BK + BN * TC_BK)) < 8 ? (200 * 1024 / (TC_BM * TC_BK + BN * TC_BK)) : 8>;
+using TcCfg = TcRing<BN, (QNMT_TC_SMEM_KB * 1024 / (TC_BM * TC_BK + BN * TC_BK)) < 8
+                             ? (QNMT_TC_SMEM_KB * 1024 / (TC_BM * TC_BK + BN * TC_BK))
+                             : 8>;
 
 struct TcEpi {
     const float* w_scales;
