@@ -14,5 +14,5 @@ from paper_1804_05038_b200 import _lib  # noqa: E402
 params = pb.synthetic_model(pb.Dims(**bench_cfgs.DIMS32), 1804)
 model = (params, pb.quantize_model(params), None, None)
 for r in bench_cfgs.cfg2_cfg3(pb, _lib.load(), 6458.7, None, model):
-    keep = {k: r[k] for k in r if k in ("config", "value", "unit", "ms", "us_per_step", "parity", "e2e")}
+    keep = {k: r[k] for k in r if k in ("config", "value", "unit", "ms", "us_per_step", "parity", "e2e", "fp32_path")}
     print(json.dumps(keep))
