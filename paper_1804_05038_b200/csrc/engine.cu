@@ -1012,7 +1012,9 @@ int qnmt_engine_create(const qnmt_model* m, int32_t max_sentences, int32_t max_s
         e->q_ro = a.take<int8_t>(N * R);
         e->sc_ro = a.take<float>(S);
         e->logits = a.take<float>(N * V);
-        e->vocab_part = a.take<char>(vocab_topk_part_bytes((int64_t)N, (int64_t)V));
+        // (also the persistent greedy kernel's per-CTA (max, sum) partials: 2 doubles per CTA, up to
+        // 256 CTAs -- more than the fused kernel's partials of one row of a small vocabulary)
+        e->vocab_part = a.take<char>(std::max<size_t>(vocab_topk_part_bytes((int64_t)N, (int64_t)V), 256 * 2 * sizeof(double)));
         e->att_scratch = a.take<char>(N * (L + 4) * 4 + 2 * S * A * 4 + N * A * 4 + 1024);
         e->att_mm = a.take<float>(2 * S * A);
         e->ctx_max = a.take<uint32_t>(S);

@@ -378,3 +378,23 @@ def test_gpu_cluster_resident_encoder_matches_batched_encoder_and_oracle(hidden)
         ost, oatt, os0 = om.encode(src)
         assert np.array_equal(st1.t().cpu().numpy(), ost) and np.array_equal(att1.t().cpu().numpy(), oatt)
         assert np.array_equal(s01.t().cpu().numpy(), os0)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("vocab,attn", [(297, 16), (40, 32), (700, 16), (1297, 64)])
+def test_gpu_persistent_greedy_small_vocabulary(vocab, attn):
+    """Regression: the persistent batch-1 greedy kernel writes one (max, sum) pair per CTA into the
+    engine's vocabulary-partials buffer; sized for the fused kernel's partials of one row it was too
+    small for vocabularies under ~6000 tokens, and the overflow corrupted the attention scores of
+    the same step (NumericError on finite models; found by benchmarks/stress_parity.py)."""
+    import paper_1804_05038_b200 as pb
+    d = pb.Dims(188, vocab, 16, 128, attn, 48)
+    params = pb.synthetic_model(d, 169549767, 0.2, 0.1, 1.5, "transform", "current")
+    qm = pb.quantize_model(params)
+    om = O.QModel(O.Dims(**d.as_dict()), params.tensors)
+    rng = np.random.default_rng(vocab)
+    for _ in range(4):
+        s = rng.integers(3, 188, int(rng.integers(1, 20))).tolist()
+        got = pb.translate_batch(qm, [s], pb.DecodeConfig(1, 1.0, "int8"), return_ids=True)[0]
+        want = om.translate(s, 1, 1.0)
+        assert got[0] == want[0] and got[1] == want[1], (vocab, attn, s)
