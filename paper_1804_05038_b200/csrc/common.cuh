@@ -8,6 +8,7 @@
 //    (the "Tier B" contract of oracle/qnmt_oracle.py).
 //  * dequantization is fl32(f64(acc) / (f64(sa) * f64(sb))) (qmath.py:379-381).
 #pragma once
+#include <shared_mutex>
 
 #include <cuda_runtime.h>
 
@@ -95,6 +96,14 @@ static inline cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block
         cudaError_t _e = (call);                                              \
         if (_e != cudaSuccess) return ::qnmt::cuda_status(_e, #call);         \
     } while (0)
+
+// Stream captures vs device-wide synchronisation.  Engines capture their step graphs on their
+// own (non-blocking) streams from whatever host thread decodes; a device-wide synchronisation or
+// a cudaFree issued by ANOTHER thread at that moment (an engine being destroyed by the garbage
+// collector, a history block being regrown) invalidates the capture in flight
+// ("operation failed due to a previous error during capture").  Captures hold this gate shared,
+// the device-wide calls hold it exclusively.  (status.cu defines it.)
+extern std::shared_mutex g_capture_gate;
 
 static inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 

@@ -14,6 +14,8 @@
 
 #include <algorithm>
 #include <numeric>
+#include <mutex>
+#include <shared_mutex>
 #include <vector>
 
 #include "gemm.cuh"
@@ -854,6 +856,7 @@ static int grow_history(qnmt_engine* e, int steps) {
         cudaGraphExecDestroy(kv.second.second);
     }
     e->graphs.clear();
+    std::unique_lock<std::shared_mutex> gate(g_capture_gate);   // cudaFree synchronises the device
     if (e->hblock) cudaFree(e->hblock);
     size_t S = e->S, B = e->B, T = steps;
     size_t fin_cap = (T + 1) * B;
@@ -1130,6 +1133,7 @@ int qnmt_engine_create(const qnmt_model* m, int32_t max_sentences, int32_t max_s
 
 int qnmt_engine_destroy(qnmt_engine* e) {
     if (!e) return QNMT_OK;
+    std::unique_lock<std::shared_mutex> gate(g_capture_gate);   // not while another thread captures a step
     cudaDeviceSynchronize();
     if (e->block) cudaFree(e->block);
     if (e->guards_dev) cudaFree(e->guards_dev);
@@ -1171,7 +1175,10 @@ int qnmt_engine_set_graphs(qnmt_engine* e, int enable) {
 }
 
 int qnmt_engine_profile(qnmt_engine* e, int enable) {
-    cudaDeviceSynchronize();
+    {
+        std::unique_lock<std::shared_mutex> gate(g_capture_gate);
+        cudaDeviceSynchronize();
+    }
     prof_collect(e);
     e->prof_on = enable != 0;
     e->prof_group = -1;
@@ -1251,6 +1258,7 @@ static int capture_step(qnmt_engine* e, int cur, int n, int beam, int k_list, cu
     const int64_t H = m->H, V = m->Vt;
     const int64_t NM = (int64_t)n * beam;
     cudaStream_t cs = e->cap_stream;
+    std::shared_lock<std::shared_mutex> gate(g_capture_gate);   // no device-wide sync / free meanwhile
     QNMT_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeRelaxed));
     int rc = QNMT_OK;
     bool fused_gather = false;

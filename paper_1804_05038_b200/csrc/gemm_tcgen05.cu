@@ -710,6 +710,7 @@ static bool split_ws(cudaStream_t st, size_t ws_elems, size_t cnt_elems, TcSplit
         cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
         if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return false;
         if (cudaStreamSynchronize(st) != cudaSuccess) return false;   // the old buffers may be in use
+        std::unique_lock<std::shared_mutex> gate(g_capture_gate);     // cudaFree synchronises the device
         cudaFree(w.ws);
         cudaFree(w.cnt);
         w = SplitWs{};

@@ -1,6 +1,7 @@
 #include <stdlib.h>
 // status.cu -- error plumbing and small utilities of the C ABI.
 #include <stdarg.h>
+#include <mutex>
 #include <string.h>
 
 #include "common.cuh"
@@ -10,6 +11,7 @@ namespace qnmt {
 static thread_local char g_last_error[512] = "";
 thread_local const int32_t* tl_ndev = nullptr;
 static unsigned long long g_launches = 0;
+std::shared_mutex g_capture_gate;   // see common.cuh
 
 bool pdl_enabled() {
     static const bool on = [] {
@@ -46,6 +48,7 @@ int64_t qnmt_kernel_launches(void) {
 }
 
 int qnmt_device_sync(void) {
+    std::unique_lock<std::shared_mutex> gate(qnmt::g_capture_gate);
     cudaError_t e = cudaDeviceSynchronize();
     if (e != cudaSuccess) return qnmt::cuda_status(e, "cudaDeviceSynchronize");
     return QNMT_OK;

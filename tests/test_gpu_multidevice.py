@@ -53,3 +53,23 @@ def test_devices_cfg5_golden_sample():
     got = pb.translate_batch(qm, srcs, cfg, max_batch=4, return_ids=True, devices=[0, 0])
     for case, (toks, lp) in zip(c["cases"], got):
         assert toks == case["out_B"] and lp == case["logp_B"]
+
+
+@pytest.mark.gpu
+def test_engines_destroyed_while_other_threads_capture_step_graphs():
+    """Regression (found by benchmarks/stress_parity.py): an engine destroyed by the garbage
+    collector (cudaDeviceSynchronize + cudaFree in qnmt_engine_destroy) while another host thread
+    was capturing its decode-step graph invalidated that capture ("operation failed due to a
+    previous error during capture").  Captures and device-wide calls now exclude each other
+    (g_capture_gate).  Many short-lived models, each decoded on 3 engine streams."""
+    import numpy as np
+    import paper_1804_05038_b200 as pb
+    dims = pb.Dims(44, 88, 32, 32, 16, 32)
+    rng = np.random.default_rng(11)
+    for trial in range(150):
+        params = pb.synthetic_model(dims, 1000 + trial, 0.2, 0.1, 1.5, "transform", "previous")
+        qm = pb.quantize_model(params)
+        sents = [rng.integers(3, 44, int(rng.integers(1, 12))).tolist() for _ in range(12)]
+        out = pb.translate_batch(qm, sents, pb.DecodeConfig(beam=1, max_ratio=0.5, precision="int8"), max_batch=4,
+                                 return_ids=True, streams=3)
+        assert len(out) == len(sents)
