@@ -332,26 +332,31 @@ def attend_k(att: AttentionNet, q_k: torch.Tensor, enc: EncoderStates):
     length = enc.length
     H2 = enc.states_k.shape[1]
     dev = u.device
-    sent_row, sent_len, _ = _one_sentence_meta(length, P, dev)
-    col_off = torch.zeros(1, dtype=torch.int32, device=dev)
-    ncols = torch.full((1,), P, dtype=torch.int32, device=dev)
     ctx = torch.empty((P, H2), dtype=torch.float32, device=dev)
     alpha = torch.empty((P, length), dtype=torch.float32, device=dev)
-    scratch = torch.empty(P * (length + 4) + 2 * A + P * A + 1024, dtype=torch.int32, device=dev)
     v = att.scorer.weight
-    if P > 16:
-        raise ShapeError("attend supports at most 16 query columns per call")
-    if not att.scorer.is_quantized:   # fp32 scorer (layers.py:226 with a float LinearOp)
-        _lib.call("qnmt_attention_f32", u.data_ptr(), A, P, col_off.data_ptr(), ncols.data_ptr(), 1,
-                  enc.att_proj_k.data_ptr(), enc.states_k.data_ptr(), sent_row.data_ptr(), sent_len.data_ptr(),
-                  length, A, H2, att.scorer._wdev().data_ptr(), ctx.data_ptr(), H2, alpha.data_ptr(), length,
-                  scratch.data_ptr(), _dev.flag().data_ptr(), _dev.stream_ptr())
-        return ctx, alpha
-    _lib.call("qnmt_attention", u.data_ptr(), A, P, col_off.data_ptr(), ncols.data_ptr(), 1,
-              enc.att_proj_k.data_ptr(), None, enc.att_exp_k().data_ptr(),
-              enc.states_k.data_ptr(), sent_row.data_ptr(), sent_len.data_ptr(), length, A, H2,
-              v.device_data().data_ptr(), v.device_scale().data_ptr(), ctx.data_ptr(), H2,
-              alpha.data_ptr(), length, scratch.data_ptr(), _dev.flag().data_ptr(), _dev.stream_ptr())
+    # The kernels take up to 16 query columns of one sentence per call (a beam).  u above was
+    # quantized over the whole [hidden, P] block as the reference does (layers.py:221); the scorer
+    # quantizes every column's tanh block on its own (layers.py:225-226), so wider queries are
+    # simply processed 16 columns at a time.
+    for c0 in range(0, P, 16):
+        pc = min(16, P - c0)
+        sent_row, sent_len, _ = _one_sentence_meta(length, pc, dev)
+        col_off = torch.zeros(1, dtype=torch.int32, device=dev)
+        ncols = torch.full((1,), pc, dtype=torch.int32, device=dev)
+        scratch = torch.empty(pc * (length + 4) + 2 * A + pc * A + 1024, dtype=torch.int32, device=dev)
+        uc, cc, ac = u[c0:c0 + pc], ctx[c0:c0 + pc], alpha[c0:c0 + pc]
+        if not att.scorer.is_quantized:   # fp32 scorer (layers.py:226 with a float LinearOp)
+            _lib.call("qnmt_attention_f32", uc.data_ptr(), A, pc, col_off.data_ptr(), ncols.data_ptr(), 1,
+                      enc.att_proj_k.data_ptr(), enc.states_k.data_ptr(), sent_row.data_ptr(), sent_len.data_ptr(),
+                      length, A, H2, att.scorer._wdev().data_ptr(), cc.data_ptr(), H2, ac.data_ptr(), length,
+                      scratch.data_ptr(), _dev.flag().data_ptr(), _dev.stream_ptr())
+        else:
+            _lib.call("qnmt_attention", uc.data_ptr(), A, pc, col_off.data_ptr(), ncols.data_ptr(), 1,
+                      enc.att_proj_k.data_ptr(), None, enc.att_exp_k().data_ptr(),
+                      enc.states_k.data_ptr(), sent_row.data_ptr(), sent_len.data_ptr(), length, A, H2,
+                      v.device_data().data_ptr(), v.device_scale().data_ptr(), cc.data_ptr(), H2,
+                      ac.data_ptr(), length, scratch.data_ptr(), _dev.flag().data_ptr(), _dev.stream_ptr())
     return ctx, alpha
 
 

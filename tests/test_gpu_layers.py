@@ -140,3 +140,18 @@ def test_errors(specs):
     bad[0, 0] = np.nan
     with pytest.raises(pb.errors.NumericError):
         net.dec_r.update_in.apply(bad)
+
+
+@pytest.mark.parametrize("P", [17, 33, 40])
+def test_attend_more_than_16_query_columns(specs, P):
+    """attend on wider query blocks than one beam (the kernels take 16 columns per call; the
+    state projection is quantized over the whole block as layers.py:221 does)."""
+    net, om, qm, params = net_and_oracle(specs, "med")
+    rng = np.random.default_rng(P)
+    src = rng.integers(3, params.dims.src_vocab, 11).tolist()
+    enc = net.encode(np.asarray(src))
+    ost, oatt, os0 = om.encode(src)
+    q = (rng.normal(0, 1, (params.dims.hidden, P)) * 0.7).astype(F32)
+    ctx, alpha = pb.attend(net.attention, q, enc)
+    octx, oalpha = om.attend(q, ost, oatt)
+    assert np.array_equal(alpha, oalpha) and np.array_equal(ctx, octx)
