@@ -1402,7 +1402,19 @@ static int init_member(qnmt_engine* e, const int32_t* src_ids, bool ids_on_devic
 
 // search state: one column per sentence, y = EOS (BOS), live score 0 (decoder.py:105-110)
 static int init_search(qnmt_engine* e, const BatchPlan& b, int32_t n, cudaStream_t st) {
-    TRY(grow_history(e, b.Tmax));
+    {
+        // Size the history for the longest sentence this engine can hold at this batch's length
+        // ratio, not for this batch: regrowing drops the captured step graphs (they point into
+        // the old block), and an engine of a pool that meets a slightly longer batch than before
+        // paid a re-capture (~0.1-0.25 s) in the middle of a corpus (seen as e2e outlier steps).
+        int want = b.Tmax;
+        if (b.Tmax > e->hist_steps && b.Lmax > 0) {
+            const long long cap = ((long long)b.Tmax * e->L + b.Lmax - 1) / b.Lmax + 1;
+            want = (int)std::min<long long>(std::max<long long>(cap, b.Tmax), std::max(4096, b.Tmax));
+            if ((size_t)e->S * e->B * (size_t)want * 28 > ((size_t)256 << 20)) want = b.Tmax;   // (huge engines: exact fit)
+        }
+        TRY(grow_history(e, want));
+    }
     e->last_n = n;
     e->last_tmax = b.Tmax;
     std::vector<int32_t> iota_n(n), y0(n, 2), ones(n, 1);
